@@ -1,0 +1,158 @@
+// dualpath/engine.hpp — the GPU executor of the DualPath KV loading path.
+//
+// The reference's seam is start_flow(req, Stage, bytes) -> complete_stage(req,
+// Stage) (/root/reference/proj/src/desim.cpp:468-499, :696-776): a simulated
+// fluid flow per byte-moving Stage.  Here the planner (pdsim::desim, plan
+// mode) fixes every scheduler decision bit-identically to the reference, and
+// this executor turns the decisions into real transfers on B200s:
+//
+//   StorageRead  (desim.cpp:603-606) -> per-engine storage-NIC gate (token
+//                                       bucket at storage_cap_Bps, FIFO), the
+//                                       Full Blocks already in pinned host DRAM
+//   LoopbackH2D  (desim.cpp:614-616) -> K1 dp_h2d_layer_gather on the PE
+//   DeToPe       (desim.cpp:617-619) -> K2 dp_h2d_push_p2p_layer on the DE,
+//                                       NVLink stores into the PE pool
+//   layer gate   (desim.cpp:623-628) -> per-(ticket, layer) landed counters
+//
+// One EngineRuntime per GPU (engine e = one process per GPU under torchrun,
+// or one thread per GPU in a single process).  Every runtime builds the same
+// ExecPlan from the same plan, so block tables and slot ids agree without
+// any host exchange; the only exchange is the PE pools' IPC handles.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "dualpath/kv_abi.h"
+#include "pdsim/desim.hpp"
+#include "pdsim/types.hpp"
+
+namespace dualpath {
+
+struct ExecOptions {
+  double storage_cap_Bps = 0;          // per-engine storage NIC; 0 = uncapped (PCIe binds)
+  std::int64_t store_fb = 0;           // Full Blocks per engine store; 0 = auto
+  std::int64_t store_bytes_max = 8LL << 30;
+  std::uint64_t seed = 9;              // content seed (oracle/kvref.c)
+  std::int32_t pool_slots = 0;         // slots per PE pool; 0 = auto (plan peak)
+  std::int64_t pool_bytes_max = 120LL << 30;
+  std::int32_t wait_timeout_ms = 30000;
+};
+
+// One request's hit-KV transfer (all layers), in global execution order.
+struct LoadJob {
+  int req = 0;              // plan request id
+  int traj = 0;
+  int round = 0;
+  int reader = 0;           // engine reading storage: pe (PE path) or de (DE path)
+  int pe = 0;               // destination engine (owner of the pool)
+  bool de_path = false;
+  std::int64_t cached = 0;  // C
+  std::int32_t n_blk = 0;
+  std::int64_t blk_off = 0; // offset of this job's blocks in the reader's tables
+  std::int32_t ticket = 0;  // counter row in the PE pool
+  std::vector<std::int32_t> preds;         // tickets in the same PE pool whose slots this
+  std::vector<std::uint32_t> pred_targets; // reuses (written by another engine), and their
+                                           // all-layer landed-item targets
+};
+
+struct ExecPlan {
+  pdsim::ClusterConfig cfg;
+  ExecOptions opt;
+  int n_engines = 0;
+  int n_pe = 0;
+  dp_kv_geom geom{};
+  std::int64_t store_fb = 0;
+  std::int32_t pool_slots = 0;
+  std::int32_t items_per_block = 1;        // landed-counter items per Layer Block
+  std::vector<LoadJob> jobs;               // global execution (slot allocation) order
+  std::vector<std::vector<int>> by_reader; // job indices per reading engine
+  std::vector<std::vector<int>> by_pe;     // job indices per destination PE
+  std::vector<std::vector<std::int64_t>> src_fb;  // per reader: flat Full Block ids
+  std::vector<std::vector<std::int32_t>> slots;   // per reader: flat destination slots
+  std::vector<std::int32_t> n_tickets;            // per PE
+  std::vector<std::int64_t> reader_bytes;         // hit bytes read per engine
+  std::int64_t hit_bytes = 0;                     // sum C * L * b
+  std::int64_t prompt_tokens = 0;                 // sum (C + A) over all requests
+  std::int64_t requests = 0;
+  std::int32_t peak_slots = 0;                    // max live slots on any PE
+
+  std::int64_t fb_of(int traj, std::int64_t block) const;  // storage mapping
+  std::int64_t fb_stride = 1;                               // blocks per session
+};
+
+// Builds the executor plan from planner output.  Requests with C = 0 move no
+// hit KV and get no job.  Slots are allocated per PE at t_read_done and freed
+// at t_pe_release (virtual time, frees first at equal time), FIFO reuse.
+ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
+                         std::span<const pdsim::Trajectory> trajectories,
+                         const pdsim::desim::SimReport& plan, const ExecOptions& opt);
+
+struct StepResult {
+  double device_ms = 0;         // CUDA-event time of this engine's step
+  double host_ms = 0;           // wall time of run_step()
+  std::int64_t bytes_read = 0;  // hit bytes this engine read from storage
+  std::int64_t launches = 0;    // kernels launched by this engine
+  std::int64_t jobs = 0;
+};
+
+class EngineRuntime {
+ public:
+  EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, int device);
+  ~EngineRuntime();
+  EngineRuntime(const EngineRuntime&) = delete;
+  EngineRuntime& operator=(const EngineRuntime&) = delete;
+
+  int engine() const { return engine_; }
+  int device() const { return device_; }
+  bool is_pe() const { return engine_ < plan_->n_pe; }
+
+  // PE pool export / import (cross-process) or same-process peer attach.
+  dp_pool_handle export_pool() const;
+  void attach_peer(int pe_engine, const dp_pool_handle& handle);
+  void attach_peer_local(int pe_engine, const EngineRuntime& pe);
+
+  // Zero this PE's landed counters (call on every PE, then barrier, before a step).
+  void reset_counters();
+  // Issue this engine's transfers for one pass over the plan and wait for
+  // them (and, on a PE, for every push landing in its pool).
+  StepResult run_step();
+
+  // Parity helpers: content hash of a pool Layer Block (PE only), and the
+  // raw pool / counters for tests.
+  std::vector<std::uint64_t> checksum(int layer, std::span<const std::int32_t> slots,
+                                      std::span<const std::int32_t> ntok);
+  std::vector<std::uint32_t> counters() const;
+  const dp_pool* pool() const { return pool_; }
+  const dp_store* store() const { return store_; }
+
+ private:
+  void upload_tables();
+
+  std::shared_ptr<const ExecPlan> plan_;
+  int engine_;
+  int device_;
+  void* stream_ = nullptr;
+  void* ev_start_ = nullptr;
+  void* ev_end_ = nullptr;
+  dp_store* store_ = nullptr;
+  dp_pool* pool_ = nullptr;                 // owned (PE only)
+  std::vector<dp_pool*> peers_;             // per engine id: view of that PE's pool
+  std::int64_t* d_src_ = nullptr;           // device block tables of this reader
+  std::int32_t* d_slots_ = nullptr;
+  std::int32_t* d_wait_tickets_ = nullptr;  // PE: DE-path tickets landing here
+  std::uint32_t* d_wait_targets_ = nullptr;
+  std::int32_t n_wait_ = 0;
+  std::int32_t* d_pred_tickets_ = nullptr;  // hazard waits, flattened per job
+  std::uint32_t* d_pred_targets_ = nullptr;
+  std::vector<std::int64_t> pred_off_;      // per job index in by_reader: offset into preds
+};
+
+// Runs run_step() of several same-process engines concurrently (one host
+// thread each) and returns their results in order.
+std::vector<StepResult> run_step_all(std::span<EngineRuntime* const> engines);
+
+}  // namespace dualpath

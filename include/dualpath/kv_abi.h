@@ -1,0 +1,148 @@
+/*
+ * dualpath/kv_abi.h — C ABI of the B200 DualPath KV-Cache loading path.
+ *
+ * The reference (pdsim, /root/reference/proj) has no FFI for this path: KV
+ * loading is a byte count inside a simulated flow.  The drop-in seam is the
+ * Stage pair start_flow(req, Stage, bytes, path) ... complete_stage(req, Stage)
+ * (proj/src/desim.cpp:468-499, :696-776).  Every entry point below replaces one
+ * byte-moving Stage or one of the KV interfaces the reference defines:
+ *
+ *   dp_kv_geom            <- ClusterConfig KV fields (proj/include/pdsim/types.hpp:18-20,30-39)
+ *   dp_store_*            <- StorageRead source: Full Blocks [L][T][b] in host DRAM
+ *                            (desim.cpp:603-606)
+ *   dp_h2d_layer_gather   <- Stage::LoopbackH2D, PE read path (desim.cpp:612-616)
+ *   dp_h2d_push_p2p_layer <- Stage::DeToPe, DE read path (desim.cpp:617-619)
+ *   dp_wait_layer         <- maybe_start_compute gate layer_h2d_done > layer_compute_done
+ *                            (desim.cpp:623-628)
+ *   dp_pool_*             <- the PE HBM KV pool (paged; not modelled by the reference,
+ *                            SPEC.md:106) and BlockRef layer_block (types.cpp:62-71)
+ *
+ * Conventions (no exceptions cross this ABI):
+ *   - every call returns int: 0 = ok, < 0 = dp_status error code;
+ *   - dp_last_error() returns a thread-local message for the last failing call;
+ *   - a dp_stream argument is a cudaStream_t (NULL = legacy default stream);
+ *     calls taking one are asynchronous on that stream;
+ *   - pointer fields inside dp_job must be device-accessible (device memory or
+ *     mapped pinned host memory) on the device that runs the kernel.
+ */
+#ifndef DUALPATH_KV_ABI_H
+#define DUALPATH_KV_ABI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DP_ABI_VERSION 1
+#define DP_MAX_JOBS_PER_LAUNCH 64
+
+typedef void* dp_stream; /* cudaStream_t */
+
+typedef enum dp_status {
+  DP_OK = 0,
+  DP_EINVAL = -1,  /* bad argument (reference: std::invalid_argument) */
+  DP_ECUDA = -2,   /* CUDA runtime error */
+  DP_ENOMEM = -3,  /* allocation failed */
+  DP_ETIMEOUT = -4 /* a dp_wait_layer watchdog fired */
+} dp_status;
+
+/* KV geometry.  Layer Block = block_tokens * bytes_per_token_layer bytes;
+ * Full Block = n_layer Layer Blocks concatenated (types.hpp:33-39). */
+typedef struct dp_kv_geom {
+  int32_t n_layer;
+  int32_t block_tokens;
+  int64_t bytes_per_token_layer; /* must be a multiple of 16 */
+} dp_kv_geom;
+
+/* One request's hit-KV transfer for a layer range (one or more Stage flows).
+ * Blocks k = 0..n_blk-1 hold tokens [k*T, min((k+1)*T, n_tokens)); only the
+ * valid bytes of the last (partial) block are moved, so a layer moves exactly
+ * n_tokens * b bytes, the reference ledger kvb_layer (desim.cpp:569-571). */
+typedef struct dp_job {
+  const int64_t* src_fb;   /* [n_blk] Full Block index in the source store */
+  const int32_t* dst_slot; /* [n_blk] slot in the destination pool (block table) */
+  int64_t n_tokens;        /* hit tokens C of the request */
+  int32_t n_blk;           /* ceil(C / T) (types.cpp:55-60) */
+  int32_t layer_begin;     /* first layer to move */
+  int32_t layer_end;       /* one past the last layer */
+  int32_t ticket;          /* landed-counter row in the destination pool, or -1 */
+} dp_job;
+
+typedef struct dp_store dp_store; /* pinned, mapped host DRAM holding Full Blocks */
+typedef struct dp_pool dp_pool;   /* paged HBM pool [n_layer][n_slots][T][b] + counters */
+
+/* Cross-process export of a pool (CUDA IPC), 128 bytes. */
+typedef struct dp_pool_handle {
+  unsigned char ipc[64];
+  dp_kv_geom geom;
+  int32_t n_slots;
+  int32_t n_tickets;
+  int32_t device;
+  int32_t reserved[5];
+} dp_pool_handle;
+
+int dp_abi_version(void);
+const char* dp_last_error(void);
+int dp_geom_check(const dp_kv_geom* geom);
+
+/* Storage tier emulation.  Creates n_fb Full Blocks of pinned+mapped host
+ * memory and fills them on `device` with the deterministic content
+ *   word(p, w) = splitmix64((p << 32 | w) ^ (seed * 0xD1B54A32D192ED03))
+ * for Full Block p, 8-byte word w (the oracle restates this, oracle/kvref.c). */
+int dp_store_create(int device, const dp_kv_geom* geom, int64_t n_fb, uint64_t seed,
+                    dp_store** out);
+int dp_store_destroy(dp_store* store);
+int dp_store_info(const dp_store* store, void** host_ptr, int64_t* bytes, int64_t* n_fb);
+
+/* Paged HBM pool with n_tickets rows of landed counters: row t holds one
+ * counter per layer (items landed for that layer) and, in column n_layer,
+ * the items landed over all layers of the ticket. */
+int dp_pool_create(int device, const dp_kv_geom* geom, int32_t n_slots, int32_t n_tickets,
+                   dp_pool** out);
+int dp_pool_destroy(dp_pool* pool);
+int dp_pool_info(const dp_pool* pool, void** base, uint32_t** counters, int64_t* data_bytes);
+int dp_pool_reset_counters(dp_pool* pool, dp_stream stream);
+int dp_pool_export(const dp_pool* pool, dp_pool_handle* out);
+/* Open an exported pool in another process (peer view used by DE engines). */
+int dp_pool_import(int device, const dp_pool_handle* handle, dp_pool** out);
+/* Same-process peer view of `pool` for `device` (enables P2P access). */
+int dp_pool_peer_view(int device, const dp_pool* pool, dp_pool** out);
+
+/* K1 (PE read path, LoopbackH2D): Layer Blocks from `src` (host, over the
+ * PE's PCIe) into `pe` on the same device.  Bumps landed[ticket][layer] by
+ * the number of items per layer (see dp_layer_items). */
+int dp_h2d_layer_gather(dp_pool* pe, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
+                        dp_stream stream);
+/* K2 (DE read path, DeToPe): run on the DE device: Layer Blocks from the DE's
+ * store over the DE's PCIe, stored over NVLink into the PE pool `pe_view`
+ * (from dp_pool_import / dp_pool_peer_view), then a system-scope release of
+ * the PE's landed counters. */
+int dp_h2d_push_p2p_layer(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs,
+                          int32_t n_jobs, dp_stream de_stream);
+
+/* Items (landed-counter increments) per layer for a job of n_blk blocks. */
+int dp_layer_items(const dp_kv_geom* geom, int32_t n_blk, int32_t* out);
+
+/* Block `stream` until landed[ticket][layer] >= target (acquire, system
+ * scope; layer == n_layer waits on the all-layer column), with a watchdog of
+ * timeout_ms (then DP_ETIMEOUT via dp_wait_status). */
+int dp_wait_layer(const dp_pool* pool, int32_t ticket, int32_t layer, uint32_t target,
+                  int32_t timeout_ms, dp_stream stream);
+/* Same for n tickets at once (tickets/targets device-accessible). */
+int dp_wait_tickets(const dp_pool* pool, const int32_t* tickets, const uint32_t* targets,
+                    int32_t n, int32_t layer, int32_t timeout_ms, dp_stream stream);
+/* Returns DP_ETIMEOUT if any wait on this device's pool has timed out. */
+int dp_wait_status(const dp_pool* pool);
+
+/* 64-bit content hash of each listed Layer Block (valid tokens only):
+ *   H = sum_i splitmix64(word_i + (i + 1) * 0x9E3779B97F4A7C15)  (mod 2^64)
+ * slots/ntok/out are device-accessible arrays of length n. */
+int dp_pool_checksum(const dp_pool* pool, int32_t layer, const int32_t* slots,
+                     const int32_t* ntok, int32_t n, uint64_t* out, dp_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DUALPATH_KV_ABI_H */

@@ -1,0 +1,424 @@
+// _core: the Python shim of the DualPath B200 engine.
+//
+// Mirrors the reference module /root/reference/proj/python/bindings.cpp:83-190
+// (ClusterConfig, Round, Trajectory, synthesize, load_trace, save_trace,
+// simulate -> dict, ConfigError, SimulationError) and adds what the GPU path
+// needs: the decision log in simulate()'s result (the parity artefact the
+// reference does not export), the per-request plan, and the
+// executor (ExecPlan / EngineRuntime).  The GIL is released around planning
+// and GPU steps.
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cstring>
+
+#include "dualpath/engine.hpp"
+#include "dualpath/kv_abi.h"
+#include "pdsim/desim.hpp"
+#include "pdsim/metrics.hpp"
+#include "pdsim/scheduler.hpp"
+#include "pdsim/types.hpp"
+#include "pdsim/workload.hpp"
+
+namespace py = pybind11;
+using namespace pdsim;
+
+namespace {
+
+py::dict report_dict(const desim::SimReport& rep, bool with_flows) {
+  py::dict d;
+  d["makespan"] = rep.makespan;
+  d["duration"] = rep.duration;
+  d["completed_requests"] = rep.completed_requests;
+  d["total_requests"] = rep.total_requests;
+  d["mean_jct"] = rep.mean_jct();
+  d["slo_violated"] = rep.slo_violated;
+  d["steady_state"] = rep.steady_state;
+  py::list lat;
+  for (const auto& r : rep.latencies) {
+    py::dict e;
+    e["request_id"] = r.request_id;
+    e["ttft"] = r.ttft;
+    e["ttst"] = r.ttst;
+    e["tpot"] = r.tpot;
+    e["sched_component"] = r.sched_component;
+    e["alloc_component"] = r.alloc_component;
+    e["read_component"] = r.read_component;
+    e["prefill_component"] = r.prefill_component;
+    lat.append(e);
+  }
+  d["latencies"] = lat;
+  py::list jct;
+  for (const auto& [id, v] : rep.trajectory_jct) jct.append(py::make_tuple(id, v));
+  d["trajectory_jct"] = jct;
+  py::list usage;
+  for (const auto& u : rep.usage) {
+    py::dict e;
+    e["kind"] = std::string(desim::to_string(u.kind));
+    e["node_id"] = u.node_id;
+    e["engine_id"] = u.engine_id;
+    e["capacity"] = u.capacity;
+    e["total_bytes"] = u.total_bytes;
+    e["buckets"] = u.buckets;
+    usage.append(e);
+  }
+  d["usage"] = usage;
+  // [B200] decision log: (t, request, pe, de, path 0=pe/1=de, pe_cat, de_cat)
+  py::list dec;
+  for (const auto& x : rep.decisions)
+    dec.append(py::make_tuple(x.t, x.request_id, x.pe, x.de, x.path == ReadPath::PEPath ? 0 : 1,
+                              x.pe_category, x.de_category));
+  d["decisions"] = dec;
+  if (with_flows) {
+    py::list fl;
+    for (const auto& f : rep.flows)
+      fl.append(py::make_tuple(f.request_id, static_cast<int>(f.stage), f.bytes, f.t_start, f.t_end));
+    d["flows"] = fl;
+    d["event_log"] = rep.event_log;
+  }
+  d["burst_latencies"] = rep.burst_latencies;
+  d["events_processed"] = rep.events_processed;
+  return d;
+}
+
+desim::SimOptions make_options(const std::string& policy, const std::string& sched_mode,
+                               double alpha, double beta, std::uint64_t seed) {
+  desim::SimOptions opt;
+  if (policy == "dual_path") opt.policy = desim::Policy::DualPath;
+  else if (policy == "pe_only") opt.policy = desim::Policy::PEOnly;
+  else if (policy == "oracle") opt.policy = desim::Policy::Oracle;
+  else throw std::invalid_argument("unknown policy '" + policy + "'");
+  if (sched_mode == "adaptive") opt.sched_mode = desim::SchedMode::Adaptive;
+  else if (sched_mode == "round_robin") opt.sched_mode = desim::SchedMode::RoundRobin;
+  else throw std::invalid_argument("unknown sched_mode '" + sched_mode + "'");
+  opt.sched.alpha = static_cast<std::int64_t>(alpha);
+  opt.sched.beta = static_cast<std::int64_t>(beta);
+  opt.seed = seed;
+  return opt;
+}
+
+py::bytes handle_bytes(const dp_pool_handle& h) {
+  return py::bytes(reinterpret_cast<const char*>(&h), sizeof(h));
+}
+
+dp_pool_handle handle_from(const py::bytes& b) {
+  std::string s = b;
+  if (s.size() != sizeof(dp_pool_handle)) throw std::invalid_argument("bad pool handle size");
+  dp_pool_handle h;
+  std::memcpy(&h, s.data(), sizeof(h));
+  return h;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_core, m) {
+  m.doc() = "DualPath KV-Cache loading on B200: planner (pdsim-compatible) and GPU executor";
+
+  py::class_<ClusterConfig>(m, "ClusterConfig")
+      .def(py::init<>())
+      .def_readwrite("prefill_nodes", &ClusterConfig::prefill_nodes)
+      .def_readwrite("decode_nodes", &ClusterConfig::decode_nodes)
+      .def_readwrite("engines_per_node", &ClusterConfig::engines_per_node)
+      .def_readwrite("cnic_bandwidth", &ClusterConfig::cnic_bandwidth)
+      .def_readwrite("storage_multiple", &ClusterConfig::storage_multiple)
+      .def_readwrite("dram_bandwidth", &ClusterConfig::dram_bandwidth)
+      .def_readwrite("n_layer", &ClusterConfig::n_layer)
+      .def_readwrite("kv_bytes_per_token_per_layer", &ClusterConfig::kv_bytes_per_token_per_layer)
+      .def_readwrite("block_size_tokens", &ClusterConfig::block_size_tokens)
+      .def_readwrite("hbm_capacity_tokens", &ClusterConfig::hbm_capacity_tokens)
+      .def_readwrite("pe_buffer_bytes", &ClusterConfig::pe_buffer_bytes)
+      .def_readwrite("de_buffer_bytes", &ClusterConfig::de_buffer_bytes)
+      .def("validate", &ClusterConfig::validate)
+      .def("kv_bytes_per_token", &ClusterConfig::kv_bytes_per_token)
+      .def("layer_block_bytes", &ClusterConfig::layer_block_bytes)
+      .def("full_block_bytes", &ClusterConfig::full_block_bytes)
+      .def("total_engines", &ClusterConfig::total_engines);
+
+  py::class_<Round>(m, "Round")
+      .def(py::init<>())
+      .def(py::init([](std::int64_t a, std::int64_t g) { return Round{a, g}; }))
+      .def_readwrite("append_tokens", &Round::append_tokens)
+      .def_readwrite("gen_tokens", &Round::gen_tokens);
+
+  py::class_<Trajectory>(m, "Trajectory")
+      .def(py::init<>())
+      .def_readwrite("id", &Trajectory::id)
+      .def_readwrite("rounds", &Trajectory::rounds)
+      .def("total_tokens", &Trajectory::total_tokens)
+      .def("validate", &Trajectory::validate);
+
+  m.def("context_before", &context_before);
+  m.def("blocks_for", &blocks_for);
+
+  m.def(
+      "synthesize",
+      [](std::int64_t max_len, int count, std::uint64_t seed, double mean_turns,
+         double mean_append, double mean_gen, double sigma_turns, double sigma_append,
+         double sigma_gen) {
+        SyntheticSpec spec;
+        spec.max_len = max_len;
+        spec.count = count;
+        spec.seed = seed;
+        spec.mean_turns = mean_turns;
+        spec.mean_append = mean_append;
+        spec.mean_gen = mean_gen;
+        spec.sigma_turns = sigma_turns;
+        spec.sigma_append = sigma_append;
+        spec.sigma_gen = sigma_gen;
+        return synthesize(spec);
+      },
+      py::arg("max_len") = 65536, py::arg("count") = 16, py::arg("seed") = 1,
+      py::arg("mean_turns") = 157.0, py::arg("mean_append") = 429.0, py::arg("mean_gen") = 176.0,
+      py::arg("sigma_turns") = 0.5, py::arg("sigma_append") = 0.6, py::arg("sigma_gen") = 0.6);
+
+  m.def("load_trace", &load_trace);
+  m.def("save_trace", [](const std::string& path, const std::vector<Trajectory>& t) {
+    save_trace(path, t);
+  });
+
+  // scheduler pure functions (snapshots as dicts-free tuples for tests)
+  m.def("select_read_path", [](std::int64_t pe_q, std::int64_t de_q) {
+    return select_read_path(pe_q, de_q) == ReadPath::PEPath ? 0 : 1;
+  });
+  auto to_snaps = [](const std::vector<std::vector<std::int64_t>>& rows, EngineKind kind) {
+    std::vector<EngineSnapshot> s;
+    for (const auto& r : rows) {
+      if (r.size() != 6) throw std::invalid_argument("snapshot rows are 6-tuples");
+      EngineSnapshot e;
+      e.engine_id = static_cast<int>(r[0]);
+      e.node_id = static_cast<int>(r[1]);
+      e.kind = kind;
+      e.seq_e = r[2];
+      e.tok_e = r[3];
+      e.read_q = r[4];
+      e.hbm_free_tokens = r[5];
+      s.push_back(e);
+    }
+    return s;
+  };
+  auto to_reqs = [](const std::vector<std::pair<int, std::int64_t>>& q) {
+    std::vector<PendingRequest> out;
+    for (const auto& [id, t] : q) out.push_back({id, t});
+    return out;
+  };
+  auto params = [](std::int64_t alpha, std::int64_t beta, double z) {
+    SchedulerParams p;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.z_factor = z;
+    return p;
+  };
+  m.def("schedule_pe_fetch",
+        [=](const std::vector<std::pair<int, std::int64_t>>& q,
+            const std::vector<std::vector<std::int64_t>>& snaps, std::int64_t alpha,
+            std::int64_t beta, double z) {
+          std::vector<std::tuple<int, int, int>> out;
+          for (const auto& a :
+               schedule_pe_fetch(to_reqs(q), to_snaps(snaps, EngineKind::PE), params(alpha, beta, z)))
+            out.emplace_back(a.request_id, a.engine_id, a.category);
+          return out;
+        });
+  m.def("schedule_de_within_group",
+        [=](const std::vector<std::pair<int, std::int64_t>>& q,
+            const std::vector<std::vector<std::int64_t>>& snaps, std::int64_t alpha,
+            std::int64_t beta, double z) {
+          std::vector<std::tuple<int, int, int>> out;
+          for (const auto& a : schedule_de_within_group(to_reqs(q), to_snaps(snaps, EngineKind::DE),
+                                                        params(alpha, beta, z)))
+            out.emplace_back(a.request_id, a.engine_id, a.category);
+          return out;
+        });
+  m.def("schedule_de_groups", [=](const std::vector<std::pair<int, std::int64_t>>& q,
+                                  const std::vector<std::pair<int, std::int64_t>>& groups) {
+    std::vector<GroupLoad> g;
+    for (const auto& [id, t] : groups) g.push_back({id, t});
+    return schedule_de_groups(to_reqs(q), g);
+  });
+
+  // Full-control planner entry: every SimOptions field by keyword.
+  m.def(
+      "plan",
+      [](const ClusterConfig& cfg, const std::vector<Trajectory>& trajs, const std::string& policy,
+         const std::string& sched_mode, std::int64_t alpha, std::int64_t beta, double z,
+         double quota, double cb, double cq, double cl, double c0, double dctx, double dstep,
+         double sub, double amort, double bucket, bool flows, bool events, double aps,
+         std::uint64_t seed, double slo_ttft, double slo_tpot, double steady_window,
+         double steady_lookback, double steady_threshold) {
+        desim::SimOptions opt = make_options(policy, sched_mode, static_cast<double>(alpha),
+                                             static_cast<double>(beta), seed);
+        opt.sched.z_factor = z;
+        opt.sched.compute_quota = quota;
+        opt.cost.prefill = {cb, cq, cl, c0};
+        opt.cost.decode_per_ctx_token = dctx;
+        opt.cost.decode_step_overhead = dstep;
+        opt.submission_overhead = sub;
+        opt.batch_amortization = amort;
+        opt.bucket_width = bucket;
+        opt.record_flows = flows;
+        opt.record_events = events;
+        desim::SimReport rep;
+        {
+          py::gil_scoped_release nogil;
+          if (aps > 0) {
+            desim::SloSpec slo{slo_ttft, slo_tpot};
+            desim::SteadySpec st{steady_window, steady_lookback, steady_threshold};
+            rep = desim::run_online(cfg, trajs, aps, slo, st, opt);
+          } else {
+            rep = desim::run_offline(cfg, trajs, opt);
+          }
+        }
+        py::dict d = report_dict(rep, flows || events);
+        py::list reqs;
+        for (const auto& r : rep.requests)
+          reqs.append(py::make_tuple(r.request_id, r.traj_index, r.round, r.cached, r.append, r.gen,
+                                     r.pe, r.de, r.path == ReadPath::PEPath ? 0 : 1, r.t_arrival,
+                                     r.t_sched, r.t_admit, r.t_read_done, r.t_pe_release, r.t_done));
+        d["requests"] = reqs;
+        return d;
+      },
+      py::arg("cluster"), py::arg("trajectories"), py::arg("policy") = "dual_path",
+      py::arg("sched_mode") = "adaptive", py::arg("alpha") = 100000, py::arg("beta") = 500000,
+      py::arg("z") = 1.05, py::arg("quota") = 0.3, py::arg("cb") = 0.0, py::arg("cq") = 0.0,
+      py::arg("cl") = 0.0, py::arg("c0") = 0.0, py::arg("dctx") = 0.0, py::arg("dstep") = 2e-3,
+      py::arg("sub") = 1e-6, py::arg("amort") = 1.0, py::arg("bucket") = 0.5,
+      py::arg("flows") = false, py::arg("events") = false, py::arg("aps") = 0.0,
+      py::arg("seed") = 1, py::arg("slo_ttft") = 4.0, py::arg("slo_tpot") = 0.05,
+      py::arg("steady_window") = 15.0, py::arg("steady_lookback") = 180.0,
+      py::arg("steady_threshold") = 0.05);
+
+  // Reference-shaped entry (bindings.cpp:169-186) plus the decision log.
+  m.def(
+      "simulate",
+      [](const ClusterConfig& cfg, const std::vector<Trajectory>& trajs, const std::string& policy,
+         const std::string& sched_mode, double alpha, double beta, double aps, std::uint64_t seed) {
+        desim::SimOptions opt = make_options(policy, sched_mode, alpha, beta, seed);
+        desim::SimReport rep;
+        {
+          py::gil_scoped_release nogil;
+          if (aps > 0) {
+            desim::SloSpec slo;
+            desim::SteadySpec st;
+            rep = desim::run_online(cfg, trajs, aps, slo, st, opt);
+          } else {
+            rep = desim::run_offline(cfg, trajs, opt);
+          }
+        }
+        return report_dict(rep, false);
+      },
+      py::arg("cluster"), py::arg("trajectories"), py::arg("policy") = "dual_path",
+      py::arg("sched_mode") = "adaptive", py::arg("alpha") = 100000, py::arg("beta") = 500000,
+      py::arg("aps") = 0.0, py::arg("seed") = 0);
+
+  py::register_exception<desim::ConfigError>(m, "ConfigError");
+  py::register_exception<desim::SimulationError>(m, "SimulationError");
+
+  // ---------------------------------------------------------------- executor
+  py::class_<dualpath::ExecOptions>(m, "ExecOptions")
+      .def(py::init<>())
+      .def_readwrite("storage_cap_Bps", &dualpath::ExecOptions::storage_cap_Bps)
+      .def_readwrite("store_fb", &dualpath::ExecOptions::store_fb)
+      .def_readwrite("store_bytes_max", &dualpath::ExecOptions::store_bytes_max)
+      .def_readwrite("seed", &dualpath::ExecOptions::seed)
+      .def_readwrite("pool_slots", &dualpath::ExecOptions::pool_slots)
+      .def_readwrite("pool_bytes_max", &dualpath::ExecOptions::pool_bytes_max)
+      .def_readwrite("wait_timeout_ms", &dualpath::ExecOptions::wait_timeout_ms);
+
+  py::class_<dualpath::ExecPlan, std::shared_ptr<dualpath::ExecPlan>>(m, "ExecPlan")
+      .def_readonly("n_engines", &dualpath::ExecPlan::n_engines)
+      .def_readonly("n_pe", &dualpath::ExecPlan::n_pe)
+      .def_readonly("store_fb", &dualpath::ExecPlan::store_fb)
+      .def_readonly("fb_stride", &dualpath::ExecPlan::fb_stride)
+      .def_readonly("pool_slots", &dualpath::ExecPlan::pool_slots)
+      .def_readonly("peak_slots", &dualpath::ExecPlan::peak_slots)
+      .def_readonly("items_per_block", &dualpath::ExecPlan::items_per_block)
+      .def_readonly("n_tickets", &dualpath::ExecPlan::n_tickets)
+      .def_readonly("reader_bytes", &dualpath::ExecPlan::reader_bytes)
+      .def_readonly("hit_bytes", &dualpath::ExecPlan::hit_bytes)
+      .def_readonly("prompt_tokens", &dualpath::ExecPlan::prompt_tokens)
+      .def_readonly("requests", &dualpath::ExecPlan::requests)
+      .def("fb_of", &dualpath::ExecPlan::fb_of)
+      .def("jobs", [](const dualpath::ExecPlan& x) {
+        // (req, traj, round, reader, pe, de_path, cached, n_blk, ticket, slots, src_fb, preds)
+        py::list out;
+        for (const auto& j : x.jobs) {
+          std::vector<std::int32_t> sl(x.slots[j.reader].begin() + j.blk_off,
+                                       x.slots[j.reader].begin() + j.blk_off + j.n_blk);
+          std::vector<std::int64_t> fb(x.src_fb[j.reader].begin() + j.blk_off,
+                                       x.src_fb[j.reader].begin() + j.blk_off + j.n_blk);
+          out.append(py::make_tuple(j.req, j.traj, j.round, j.reader, j.pe, j.de_path, j.cached,
+                                    j.n_blk, j.ticket, sl, fb, j.preds));
+        }
+        return out;
+      })
+      .def("by_reader", [](const dualpath::ExecPlan& x, int e) { return x.by_reader.at(e); })
+      .def("by_pe", [](const dualpath::ExecPlan& x, int e) { return x.by_pe.at(e); });
+
+  m.def(
+      "build_exec_plan",
+      [](const ClusterConfig& cfg, const std::vector<Trajectory>& trajs, const py::dict& planned,
+         const dualpath::ExecOptions& opt) {
+        // rebuild the RequestPlan list from plan()'s "requests" tuples
+        desim::SimReport rep;
+        for (const auto& item : planned["requests"].cast<py::list>()) {
+          auto t = item.cast<py::tuple>();
+          desim::RequestPlan r;
+          r.request_id = t[0].cast<int>();
+          r.traj_index = t[1].cast<int>();
+          r.round = t[2].cast<int>();
+          r.cached = t[3].cast<std::int64_t>();
+          r.append = t[4].cast<std::int64_t>();
+          r.gen = t[5].cast<std::int64_t>();
+          r.pe = t[6].cast<int>();
+          r.de = t[7].cast<int>();
+          r.path = t[8].cast<int>() == 0 ? ReadPath::PEPath : ReadPath::DEPath;
+          r.t_arrival = t[9].cast<double>();
+          r.t_sched = t[10].cast<double>();
+          r.t_admit = t[11].cast<double>();
+          r.t_read_done = t[12].cast<double>();
+          r.t_pe_release = t[13].cast<double>();
+          r.t_done = t[14].cast<double>();
+          rep.requests.push_back(r);
+        }
+        py::gil_scoped_release nogil;
+        return std::make_shared<dualpath::ExecPlan>(dualpath::build_exec_plan(cfg, trajs, rep, opt));
+      },
+      py::arg("cluster"), py::arg("trajectories"), py::arg("planned"), py::arg("options"));
+
+  py::class_<dualpath::StepResult>(m, "StepResult")
+      .def_readonly("device_ms", &dualpath::StepResult::device_ms)
+      .def_readonly("host_ms", &dualpath::StepResult::host_ms)
+      .def_readonly("bytes_read", &dualpath::StepResult::bytes_read)
+      .def_readonly("launches", &dualpath::StepResult::launches)
+      .def_readonly("jobs", &dualpath::StepResult::jobs);
+
+  py::class_<dualpath::EngineRuntime>(m, "EngineRuntime")
+      .def(py::init([](std::shared_ptr<dualpath::ExecPlan> plan, int engine, int device) {
+             py::gil_scoped_release nogil;
+             return std::make_unique<dualpath::EngineRuntime>(plan, engine, device);
+           }),
+           py::arg("plan"), py::arg("engine"), py::arg("device"))
+      .def_property_readonly("engine", &dualpath::EngineRuntime::engine)
+      .def_property_readonly("device", &dualpath::EngineRuntime::device)
+      .def_property_readonly("is_pe", &dualpath::EngineRuntime::is_pe)
+      .def("export_pool", [](const dualpath::EngineRuntime& e) { return handle_bytes(e.export_pool()); })
+      .def("attach_peer", [](dualpath::EngineRuntime& e, int pe, const py::bytes& h) {
+        e.attach_peer(pe, handle_from(h));
+      })
+      .def("attach_peer_local", &dualpath::EngineRuntime::attach_peer_local)
+      .def("reset_counters", &dualpath::EngineRuntime::reset_counters)
+      .def("run_step", &dualpath::EngineRuntime::run_step, py::call_guard<py::gil_scoped_release>())
+      .def("checksum",
+           [](dualpath::EngineRuntime& e, int layer, const std::vector<std::int32_t>& slots,
+              const std::vector<std::int32_t>& ntok) { return e.checksum(layer, slots, ntok); })
+      .def("counters", &dualpath::EngineRuntime::counters);
+
+  m.def(
+      "run_step_all",
+      [](std::vector<dualpath::EngineRuntime*> engines) {
+        py::gil_scoped_release nogil;
+        return dualpath::run_step_all(engines);
+      },
+      py::arg("engines"));
+
+  m.attr("ABI_VERSION") = dp_abi_version();
+}

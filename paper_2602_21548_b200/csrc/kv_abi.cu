@@ -1,0 +1,649 @@
+// B200 (sm_100a) implementation of the DualPath KV loading C ABI
+// (include/dualpath/kv_abi.h).
+//
+// Kernels:
+//   K1 kv_gather<false>  — LoopbackH2D (proj/src/desim.cpp:614-616): Layer Blocks
+//       of Full Blocks in pinned host DRAM -> paged PE HBM pool, zero-copy
+//       16-byte loads over the PE's PCIe link.
+//   K2 kv_gather<true>   — DeToPe (proj/src/desim.cpp:617-619): the same gather
+//       run on the DE GPU, reading the DE's host DRAM over the DE's PCIe link
+//       and storing straight into the PE pool over NVLink (peer pointer),
+//       then a system-scope release of the PE's per-layer landed counter.
+//   kv_wait_ge           — the layer gate of maybe_start_compute (desim.cpp:623-628).
+//   kv_block_checksum    — per-Layer-Block content hash for parity checks.
+//   kv_store_fill        — deterministic storage content (restated in oracle/kvref.c).
+//
+// Work decomposition: one CTA-sized item = one chunk (<= 64 KiB) of one
+// Layer Block.  Items are ordered (job, layer, block, chunk) so a request's
+// layer l lands before l+1 (layerwise prefill).  A launch
+// carries up to DP_MAX_JOBS_PER_LAUNCH job headers in its parameter block;
+// each warp decodes its item's job with a ballot over the job prefix sums.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "dualpath/kv_abi.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 8;
+constexpr int64_t kChunkBytes = 64 * 1024;  // max bytes per item
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kSeedMul = 0xD1B54A32D192ED03ull;
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define DP_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(DP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + kGolden;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct GatherParams {
+  const char* store;     // source Full Blocks (device-visible host pointer)
+  char* pool;            // destination pool data base (local or peer)
+  uint32_t* counters;    // destination landed counters [n_tickets][n_layer + 1]
+  int64_t lb_bytes;      // Layer Block bytes T*b
+  int64_t fb_bytes;      // Full Block bytes L*T*b
+  int64_t bpt;           // b, bytes per token per layer
+  int64_t layer_stride;  // n_slots * lb_bytes
+  int32_t n_layer;
+  int32_t block_tokens;
+  int32_t n_chunk;       // items per Layer Block
+  int32_t n_jobs;
+  int64_t item_begin[DP_MAX_JOBS_PER_LAUNCH + 1];
+  dp_job jobs[DP_MAX_JOBS_PER_LAUNCH];
+};
+static_assert(sizeof(GatherParams) <= 4000, "kernel parameter block too large");
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Warp-cooperative decode of the job owning `item`: lane j tests job
+// j (and j+32), the ballot's population count is the job index.
+__device__ __forceinline__ int decode_job(const GatherParams& p, int64_t item) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lo = __ballot_sync(
+      0xffffffffu, lane + 1 < p.n_jobs && p.item_begin[lane + 1] <= item);
+  const unsigned hi = __ballot_sync(
+      0xffffffffu, lane + 33 < p.n_jobs && p.item_begin[lane + 33] <= item);
+  return __popc(lo) + __popc(hi);
+}
+
+template <bool kPeer>
+__global__ void __launch_bounds__(kThreads) kv_gather(const __grid_constant__ GatherParams p) {
+  const int64_t total = p.item_begin[p.n_jobs];
+  const int tid = threadIdx.x;
+  for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+    const int j = decode_job(p, item);
+    const dp_job& job = p.jobs[j];
+    const int64_t local = item - p.item_begin[j];
+    const int64_t per_layer = static_cast<int64_t>(job.n_blk) * p.n_chunk;
+    const int layer = job.layer_begin + static_cast<int>(local / per_layer);
+    const int64_t rem = local % per_layer;
+    const int blk = static_cast<int>(rem / p.n_chunk);
+    const int chunk = static_cast<int>(rem % p.n_chunk);
+
+    const int64_t fb = job.src_fb[blk];
+    const int64_t slot = job.dst_slot[blk];
+    const int64_t tok0 = static_cast<int64_t>(blk) * p.block_tokens;
+    const int64_t ntok = min(static_cast<int64_t>(p.block_tokens), job.n_tokens - tok0);
+    const int64_t valid = ntok * p.bpt;
+    const int64_t beg = static_cast<int64_t>(chunk) * kChunkBytes;
+    const int64_t end = min(beg + kChunkBytes, valid);
+
+    if (end > beg) {
+      const uint4* src = reinterpret_cast<const uint4*>(p.store + fb * p.fb_bytes +
+                                                        layer * p.lb_bytes + beg);
+      uint4* dst = reinterpret_cast<uint4*>(p.pool + layer * p.layer_stride +
+                                            slot * p.lb_bytes + beg);
+      const int n16 = static_cast<int>((end - beg) >> 4);
+      for (int base = 0; base < n16; base += kThreads * kUnroll) {
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int i = base + u * kThreads + tid;
+          if (i < n16) v[u] = ld_stream(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int i = base + u * kThreads + tid;
+          if (i < n16) st_v4(dst + i, v[u]);
+        }
+      }
+    }
+    if (job.ticket >= 0) {
+      // all of this CTA's stores are ordered before the counter release
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t* row = p.counters + static_cast<int64_t>(job.ticket) * (p.n_layer + 1);
+        if (kPeer) {
+          asm volatile("fence.acq_rel.sys;" ::: "memory");
+          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(row + layer) : "memory");
+          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(row + p.n_layer) : "memory");
+        } else {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(row + layer) : "memory");
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(row + p.n_layer) : "memory");
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t global_timer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void kv_wait_ge(const uint32_t* ctr, uint32_t target, uint64_t timeout_ns,
+                           int* err_flag) {
+  const uint64_t t0 = global_timer_ns();
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    if (global_timer_ns() - t0 > timeout_ns) {
+      atomicExch_system(err_flag, 1);
+      break;
+    }
+    __nanosleep(256);
+  }
+}
+
+// One thread per (counter, target) pair; used to make an engine's step end
+// cover every push that lands in its pool, and for slot-reuse hazards.
+__global__ void kv_wait_many(const uint32_t* counters, int32_t row_len, const int32_t* tickets,
+                             const uint32_t* targets, int32_t n, int32_t col,
+                             uint64_t timeout_ns, int* err_flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t* ctr = counters + static_cast<int64_t>(tickets[i]) * row_len + col;
+  const uint32_t target = targets[i];
+  const uint64_t t0 = global_timer_ns();
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    if (global_timer_ns() - t0 > timeout_ns) {
+      atomicExch_system(err_flag, 1);
+      break;
+    }
+    __nanosleep(512);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    kv_block_checksum(const char* pool, int64_t layer_off, int64_t lb_bytes, int64_t bpt,
+                      const int32_t* slots, const int32_t* ntok, int32_t n, uint64_t* out) {
+  __shared__ uint64_t partial[kThreads / 32];
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const uint64_t* words =
+        reinterpret_cast<const uint64_t*>(pool + layer_off + static_cast<int64_t>(slots[b]) * lb_bytes);
+    const int64_t nw = static_cast<int64_t>(ntok[b]) * bpt / 8;
+    uint64_t acc = 0;
+    for (int64_t i = threadIdx.x; i < nw; i += kThreads)
+      acc += splitmix64(words[i] + static_cast<uint64_t>(i + 1) * kGolden);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) partial[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t s = 0;
+      for (int w = 0; w < kThreads / 32; ++w) s += partial[w];
+      out[b] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// word(p, w) = splitmix64((p << 32 | w) ^ seed*kSeedMul), two words per thread.
+__global__ void kv_store_fill(uint64_t* dst, int64_t n_pairs, int64_t words_per_fb,
+                              uint64_t seed_mix) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_pairs;
+       i += stride) {
+    const int64_t w0 = 2 * i;
+    const uint64_t fb = static_cast<uint64_t>(w0 / words_per_fb);
+    const uint64_t w = static_cast<uint64_t>(w0 % words_per_fb);
+    const uint64_t a = splitmix64(((fb << 32) | w) ^ seed_mix);
+    const uint64_t b = splitmix64(((fb << 32) | (w + 1)) ^ seed_mix);
+    asm volatile("st.global.v2.u64 [%0], {%1,%2};" ::"l"(dst + w0), "l"(a), "l"(b) : "memory");
+  }
+}
+
+int sm_count(int device) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n > 0 ? n : 148;
+}
+
+int64_t chunks_per_block(const dp_kv_geom& g) {
+  const int64_t lb = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
+  return (lb + kChunkBytes - 1) / kChunkBytes;
+}
+
+bool geom_equal(const dp_kv_geom& a, const dp_kv_geom& b) {
+  return a.n_layer == b.n_layer && a.block_tokens == b.block_tokens &&
+         a.bytes_per_token_layer == b.bytes_per_token_layer;
+}
+
+}  // namespace
+
+struct dp_store {
+  int device = -1;
+  dp_kv_geom geom{};
+  int64_t n_fb = 0;
+  uint64_t seed = 0;
+  char* host = nullptr;
+  int64_t bytes = 0;
+};
+
+struct dp_pool {
+  int device = -1;  // device whose address space `base` lives in
+  int home_device = -1;
+  dp_kv_geom geom{};
+  int32_t n_slots = 0;
+  int32_t n_tickets = 0;
+  char* base = nullptr;
+  uint32_t* counters = nullptr;
+  int64_t data_bytes = 0;
+  bool owner = false;
+  bool ipc_opened = false;
+  int* err_host = nullptr;  // mapped pinned watchdog flag
+};
+
+namespace {
+
+int64_t counters_offset(int64_t data_bytes) { return (data_bytes + 255) / 256 * 256; }
+
+int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
+                  dp_stream stream, bool peer) {
+  if (!pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0)
+    return fail(DP_EINVAL, "gather: null argument");
+  if (!geom_equal(pool->geom, src->geom))
+    return fail(DP_EINVAL, "gather: pool and store geometry differ");
+  if (peer == pool->owner)
+    return fail(DP_EINVAL, peer ? "push_p2p: destination must be a peer view of the PE pool"
+                                : "h2d_gather: destination must be the local PE pool");
+  const dp_kv_geom& g = pool->geom;
+  DeviceGuard guard(pool->device);
+  GatherParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.store = src->host;
+  p.pool = pool->base;
+  p.counters = pool->counters;
+  p.lb_bytes = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
+  p.fb_bytes = p.lb_bytes * g.n_layer;
+  p.bpt = g.bytes_per_token_layer;
+  p.layer_stride = p.lb_bytes * pool->n_slots;
+  p.n_layer = g.n_layer;
+  p.block_tokens = g.block_tokens;
+  p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
+  const int grid_cap = sm_count(pool->device) * 4;
+  auto s = static_cast<cudaStream_t>(stream);
+  for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_JOBS_PER_LAUNCH) {
+    const int32_t nj = std::min<int32_t>(DP_MAX_JOBS_PER_LAUNCH, n_jobs - j0);
+    p.n_jobs = 0;
+    int64_t items = 0;
+    for (int32_t j = 0; j < nj; ++j) {
+      const dp_job& job = jobs[j0 + j];
+      if (job.n_tokens < 0 || job.n_blk < 0 || job.layer_begin < 0 ||
+          job.layer_end > g.n_layer || job.layer_begin > job.layer_end)
+        return fail(DP_EINVAL, "gather: job " + std::to_string(j0 + j) + " out of range");
+      const int64_t need_blk = (job.n_tokens + g.block_tokens - 1) / g.block_tokens;
+      if (need_blk != job.n_blk)
+        return fail(DP_EINVAL, "gather: job " + std::to_string(j0 + j) +
+                                   " n_blk != ceil(n_tokens / block_tokens)");
+      if (job.ticket >= pool->n_tickets)
+        return fail(DP_EINVAL, "gather: ticket out of range");
+      if (job.n_blk > 0 && (!job.src_fb || !job.dst_slot))
+        return fail(DP_EINVAL, "gather: null block arrays");
+      const int64_t n = static_cast<int64_t>(job.n_blk) * p.n_chunk *
+                        (job.layer_end - job.layer_begin);
+      if (n == 0) continue;
+      p.jobs[p.n_jobs] = job;
+      p.item_begin[p.n_jobs] = items;
+      ++p.n_jobs;
+      items += n;
+    }
+    p.item_begin[p.n_jobs] = items;
+    if (items == 0) continue;
+    const int grid = static_cast<int>(std::min<int64_t>(items, grid_cap));
+    if (peer)
+      kv_gather<true><<<grid, kThreads, 0, s>>>(p);
+    else
+      kv_gather<false><<<grid, kThreads, 0, s>>>(p);
+    DP_CUDA(cudaGetLastError());
+  }
+  return DP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dp_abi_version(void) { return DP_ABI_VERSION; }
+
+const char* dp_last_error(void) { return g_last_error.c_str(); }
+
+int dp_geom_check(const dp_kv_geom* g) {
+  if (!g) return fail(DP_EINVAL, "geom: null");
+  if (g->n_layer < 1) return fail(DP_EINVAL, "geom: n_layer must be >= 1");
+  if (g->block_tokens < 1) return fail(DP_EINVAL, "geom: block_tokens must be >= 1");
+  if (g->bytes_per_token_layer <= 0 || g->bytes_per_token_layer % 16 != 0)
+    return fail(DP_EINVAL, "geom: bytes_per_token_layer must be a positive multiple of 16");
+  const int64_t fb = static_cast<int64_t>(g->n_layer) * g->block_tokens * g->bytes_per_token_layer;
+  if (fb / 8 >= (int64_t{1} << 32)) return fail(DP_EINVAL, "geom: Full Block too large");
+  return DP_OK;
+}
+
+int dp_store_create(int device, const dp_kv_geom* geom, int64_t n_fb, uint64_t seed,
+                    dp_store** out) {
+  if (!out) return fail(DP_EINVAL, "store_create: null out");
+  *out = nullptr;
+  if (int rc = dp_geom_check(geom)) return rc;
+  if (n_fb < 1) return fail(DP_EINVAL, "store_create: n_fb must be >= 1");
+  DeviceGuard guard(device);
+  auto* st = new dp_store;
+  st->device = device;
+  st->geom = *geom;
+  st->n_fb = n_fb;
+  st->seed = seed;
+  const int64_t fb = static_cast<int64_t>(geom->n_layer) * geom->block_tokens *
+                     geom->bytes_per_token_layer;
+  st->bytes = fb * n_fb;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&st->host), st->bytes,
+                                cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    delete st;
+    return fail(DP_ENOMEM, std::string("store_create: cudaHostAlloc: ") + cudaGetErrorString(e));
+  }
+  const int64_t n_pairs = st->bytes / 16;
+  const int grid = sm_count(device) * 8;
+  kv_store_fill<<<grid, kThreads>>>(reinterpret_cast<uint64_t*>(st->host), n_pairs, fb / 8,
+                                    seed * kSeedMul);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFreeHost(st->host);
+    delete st;
+    return fail(DP_ECUDA, std::string("store_create: fill: ") + cudaGetErrorString(e));
+  }
+  *out = st;
+  return DP_OK;
+}
+
+int dp_store_destroy(dp_store* st) {
+  if (!st) return DP_OK;
+  if (st->host) DP_CUDA(cudaFreeHost(st->host));
+  delete st;
+  return DP_OK;
+}
+
+int dp_store_info(const dp_store* st, void** host_ptr, int64_t* bytes, int64_t* n_fb) {
+  if (!st) return fail(DP_EINVAL, "store_info: null store");
+  if (host_ptr) *host_ptr = st->host;
+  if (bytes) *bytes = st->bytes;
+  if (n_fb) *n_fb = st->n_fb;
+  return DP_OK;
+}
+
+int dp_pool_create(int device, const dp_kv_geom* geom, int32_t n_slots, int32_t n_tickets,
+                   dp_pool** out) {
+  if (!out) return fail(DP_EINVAL, "pool_create: null out");
+  *out = nullptr;
+  if (int rc = dp_geom_check(geom)) return rc;
+  if (n_slots < 1 || n_tickets < 0) return fail(DP_EINVAL, "pool_create: bad sizes");
+  DeviceGuard guard(device);
+  auto* pool = new dp_pool;
+  pool->device = pool->home_device = device;
+  pool->geom = *geom;
+  pool->n_slots = n_slots;
+  pool->n_tickets = n_tickets;
+  pool->data_bytes = static_cast<int64_t>(geom->n_layer) * n_slots * geom->block_tokens *
+                     geom->bytes_per_token_layer;
+  const int64_t ctr_bytes = static_cast<int64_t>(n_tickets) * (geom->n_layer + 1) * 4;
+  const int64_t total = counters_offset(pool->data_bytes) + std::max<int64_t>(ctr_bytes, 256);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&pool->base), total);
+  if (e != cudaSuccess) {
+    delete pool;
+    return fail(DP_ENOMEM, std::string("pool_create: cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  pool->counters = reinterpret_cast<uint32_t*>(pool->base + counters_offset(pool->data_bytes));
+  pool->owner = true;
+  e = cudaMemset(pool->counters, 0, std::max<int64_t>(ctr_bytes, 256));
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(reinterpret_cast<void**>(&pool->err_host), sizeof(int), cudaHostAllocMapped |
+                                                                            cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaFree(pool->base);
+    delete pool;
+    return fail(DP_ECUDA, std::string("pool_create: ") + cudaGetErrorString(e));
+  }
+  *pool->err_host = 0;
+  *out = pool;
+  return DP_OK;
+}
+
+int dp_pool_destroy(dp_pool* pool) {
+  if (!pool) return DP_OK;
+  {
+    DeviceGuard guard(pool->device);
+    if (pool->owner && pool->base) cudaFree(pool->base);
+    if (pool->ipc_opened && pool->base) cudaIpcCloseMemHandle(pool->base);
+    if (pool->err_host) cudaFreeHost(pool->err_host);
+  }
+  delete pool;
+  return DP_OK;
+}
+
+int dp_pool_info(const dp_pool* pool, void** base, uint32_t** counters, int64_t* data_bytes) {
+  if (!pool) return fail(DP_EINVAL, "pool_info: null pool");
+  if (base) *base = pool->base;
+  if (counters) *counters = pool->counters;
+  if (data_bytes) *data_bytes = pool->data_bytes;
+  return DP_OK;
+}
+
+int dp_pool_reset_counters(dp_pool* pool, dp_stream stream) {
+  if (!pool) return fail(DP_EINVAL, "pool_reset_counters: null pool");
+  DeviceGuard guard(pool->device);
+  const int64_t ctr_bytes = static_cast<int64_t>(pool->n_tickets) * (pool->geom.n_layer + 1) * 4;
+  if (ctr_bytes > 0)
+    DP_CUDA(cudaMemsetAsync(pool->counters, 0, ctr_bytes, static_cast<cudaStream_t>(stream)));
+  if (pool->err_host) *pool->err_host = 0;
+  return DP_OK;
+}
+
+int dp_pool_export(const dp_pool* pool, dp_pool_handle* out) {
+  if (!pool || !out) return fail(DP_EINVAL, "pool_export: null argument");
+  if (!pool->owner) return fail(DP_EINVAL, "pool_export: only the owning pool can be exported");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "unexpected IPC handle size");
+  DeviceGuard guard(pool->device);
+  cudaIpcMemHandle_t h;
+  DP_CUDA(cudaIpcGetMemHandle(&h, pool->base));
+  std::memset(out, 0, sizeof(*out));
+  std::memcpy(out->ipc, &h, 64);
+  out->geom = pool->geom;
+  out->n_slots = pool->n_slots;
+  out->n_tickets = pool->n_tickets;
+  out->device = pool->device;
+  return DP_OK;
+}
+
+int dp_pool_import(int device, const dp_pool_handle* h, dp_pool** out) {
+  if (!h || !out) return fail(DP_EINVAL, "pool_import: null argument");
+  *out = nullptr;
+  if (int rc = dp_geom_check(&h->geom)) return rc;
+  DeviceGuard guard(device);
+  cudaIpcMemHandle_t ih;
+  std::memcpy(&ih, h->ipc, 64);
+  void* ptr = nullptr;
+  DP_CUDA(cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess));
+  auto* v = new dp_pool;
+  v->device = device;
+  v->home_device = h->device;
+  v->geom = h->geom;
+  v->n_slots = h->n_slots;
+  v->n_tickets = h->n_tickets;
+  v->base = static_cast<char*>(ptr);
+  v->data_bytes = static_cast<int64_t>(h->geom.n_layer) * h->n_slots * h->geom.block_tokens *
+                  h->geom.bytes_per_token_layer;
+  v->counters = reinterpret_cast<uint32_t*>(v->base + counters_offset(v->data_bytes));
+  v->ipc_opened = true;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&v->err_host), sizeof(int),
+                                cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaIpcCloseMemHandle(ptr);
+    delete v;
+    return fail(DP_ECUDA, std::string("pool_import: ") + cudaGetErrorString(e));
+  }
+  *v->err_host = 0;
+  *out = v;
+  return DP_OK;
+}
+
+int dp_pool_peer_view(int device, const dp_pool* pool, dp_pool** out) {
+  if (!pool || !out) return fail(DP_EINVAL, "pool_peer_view: null argument");
+  *out = nullptr;
+  if (device == pool->device) return fail(DP_EINVAL, "pool_peer_view: same device");
+  int can = 0;
+  DP_CUDA(cudaDeviceCanAccessPeer(&can, device, pool->device));
+  if (!can) return fail(DP_EINVAL, "pool_peer_view: no P2P path between devices");
+  DeviceGuard guard(device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(pool->device, 0);
+  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+    return fail(DP_ECUDA, std::string("pool_peer_view: ") + cudaGetErrorString(e));
+  cudaGetLastError();
+  auto* v = new dp_pool(*pool);
+  v->device = device;
+  v->owner = false;
+  v->ipc_opened = false;
+  v->err_host = nullptr;
+  e = cudaHostAlloc(reinterpret_cast<void**>(&v->err_host), sizeof(int),
+                    cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    delete v;
+    return fail(DP_ECUDA, std::string("pool_peer_view: ") + cudaGetErrorString(e));
+  }
+  *v->err_host = 0;
+  *out = v;
+  return DP_OK;
+}
+
+int dp_h2d_layer_gather(dp_pool* pe, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
+                        dp_stream stream) {
+  return launch_gather(pe, src, jobs, n_jobs, stream, /*peer=*/false);
+}
+
+int dp_h2d_push_p2p_layer(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs,
+                          int32_t n_jobs, dp_stream de_stream) {
+  return launch_gather(pe_view, de_src, jobs, n_jobs, de_stream, /*peer=*/true);
+}
+
+int dp_layer_items(const dp_kv_geom* geom, int32_t n_blk, int32_t* out) {
+  if (int rc = dp_geom_check(geom)) return rc;
+  if (!out || n_blk < 0) return fail(DP_EINVAL, "layer_items: bad argument");
+  *out = static_cast<int32_t>(n_blk * chunks_per_block(*geom));
+  return DP_OK;
+}
+
+int dp_wait_layer(const dp_pool* pool, int32_t ticket, int32_t layer, uint32_t target,
+                  int32_t timeout_ms, dp_stream stream) {
+  if (!pool) return fail(DP_EINVAL, "wait_layer: null pool");
+  if (ticket < 0 || ticket >= pool->n_tickets || layer < 0 || layer > pool->geom.n_layer)
+    return fail(DP_EINVAL, "wait_layer: ticket/layer out of range");
+  if (timeout_ms <= 0) return fail(DP_EINVAL, "wait_layer: timeout must be > 0");
+  DeviceGuard guard(pool->device);
+  const uint32_t* ctr =
+      pool->counters + static_cast<int64_t>(ticket) * (pool->geom.n_layer + 1) + layer;
+  kv_wait_ge<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+      ctr, target, static_cast<uint64_t>(timeout_ms) * 1000000ull, pool->err_host);
+  DP_CUDA(cudaGetLastError());
+  return DP_OK;
+}
+
+int dp_wait_tickets(const dp_pool* pool, const int32_t* tickets, const uint32_t* targets,
+                    int32_t n, int32_t layer, int32_t timeout_ms, dp_stream stream) {
+  if (!pool || n < 0 || (n > 0 && (!tickets || !targets)))
+    return fail(DP_EINVAL, "wait_tickets: bad argument");
+  if (layer < 0 || layer > pool->geom.n_layer)
+    return fail(DP_EINVAL, "wait_tickets: layer out of range");
+  if (timeout_ms <= 0) return fail(DP_EINVAL, "wait_tickets: timeout must be > 0");
+  if (n == 0) return DP_OK;
+  DeviceGuard guard(pool->device);
+  kv_wait_many<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      pool->counters, pool->geom.n_layer + 1, tickets, targets, n, layer,
+      static_cast<uint64_t>(timeout_ms) * 1000000ull, pool->err_host);
+  DP_CUDA(cudaGetLastError());
+  return DP_OK;
+}
+
+int dp_wait_status(const dp_pool* pool) {
+  if (!pool) return fail(DP_EINVAL, "wait_status: null pool");
+  if (pool->err_host && *reinterpret_cast<volatile int*>(pool->err_host))
+    return fail(DP_ETIMEOUT, "wait_layer: watchdog fired (producer never released the layer)");
+  return DP_OK;
+}
+
+int dp_pool_checksum(const dp_pool* pool, int32_t layer, const int32_t* slots,
+                     const int32_t* ntok, int32_t n, uint64_t* out, dp_stream stream) {
+  if (!pool || n < 0 || (n > 0 && (!slots || !ntok || !out)))
+    return fail(DP_EINVAL, "pool_checksum: bad argument");
+  if (layer < 0 || layer >= pool->geom.n_layer)
+    return fail(DP_EINVAL, "pool_checksum: layer out of range");
+  if (n == 0) return DP_OK;
+  DeviceGuard guard(pool->device);
+  const int64_t lb = static_cast<int64_t>(pool->geom.block_tokens) * pool->geom.bytes_per_token_layer;
+  const int grid = std::min(n, sm_count(pool->device) * 8);
+  kv_block_checksum<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      pool->base, layer * lb * pool->n_slots, lb, pool->geom.bytes_per_token_layer, slots, ntok,
+      n, out);
+  DP_CUDA(cudaGetLastError());
+  return DP_OK;
+}
+
+}  // extern "C"
