@@ -1,0 +1,474 @@
+#!/usr/bin/env python
+"""DualPath KV-Cache loading benchmark on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c1|c2] [--cap-gbps X] [--sessions-per-gpu S]
+
+N = 1: the K1 loader alone (the PE of a 1P1D prefill-only plan; P/D needs
+two engines, proj/src/types.cpp:11-12).  N > 1: one process per GPU under
+torchrun, engines 0..N/2-1 prefill (PE), the rest decode (DE), dual-path
+plan; the same workload is also run prefill-only ("1-path",
+Policy::PEOnly, proj/src/desim.cpp:826-827) for the vs-1-path ratio.
+
+A step = one offline pass of the synthetic agentic trace: every request's
+hit KV (C*L*b bytes) moved from the emulated storage tier (pinned host DRAM,
+read over each engine's own PCIe link, optionally rate-capped per engine)
+into the PE's paged HBM pool, by K1 (PE path) or K2 (DE path, NVLink push).
+Inputs are larger than L2 (hundreds of GB per step), so no flush is needed.
+"""
+
+import argparse
+import hashlib
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DSV3 = dict(L=61, b=576, T=64)          # DeepSeek-V3 MLA fp8 KV (BASELINE configs 1-2)
+QWEN = dict(L=64, b=4096, T=64)         # Qwen2.5-32B GQA bf16 KV (config 3)
+PCIE_ZC_BPS = 51.5e9                    # measured SM zero-copy H2D per GPU (profiles/r01_probe_links.txt)
+NVLINK_BPS = 778e9                      # measured memcpyPeer per direction (same probe)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c3"])
+    ap.add_argument("--cap-gbps", type=float, default=0.0,
+                    help="per-engine storage-NIC cap (0 = uncapped: the PCIe link binds)")
+    ap.add_argument("--sessions-per-gpu", type=int, default=16)
+    ap.add_argument("--no-one-path", action="store_true", help="skip the prefill-only comparison")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pd", default="", help="override P:D, e.g. 2:6")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- workload
+def workload(args, n_gpus):
+    """Trajectories + KV shape.  c1: BASELINE config 1 generator (20 turns,
+    mean append 429, mean gen 500, ~95% hit); c2: 32K/64K/128K contexts built
+    by a cheap generation round, then warm {429, 1} rounds (config 2); c3: c1
+    with the Qwen2.5-32B KV shape (config 3)."""
+    import paper_2602_21548_b200 as dp
+    sessions = max(1, args.sessions_per_gpu * max(1, n_gpus))
+    if args.workload in ("c1", "c3"):
+        trajs = dp.synthesize(max_len=131072, count=sessions, seed=9, mean_turns=20,
+                              sigma_turns=0.0, mean_append=429, mean_gen=500)
+        shape = DSV3 if args.workload == "c1" else QWEN
+    else:
+        trajs = []
+        for i in range(sessions):
+            t = dp.Trajectory()
+            t.id = f"ctx{i}"
+            c = (32768, 65536, 131072)[i % 3]
+            t.rounds = [dp.Round(16, c - 16)] + [dp.Round(429, 1) for _ in range(3)]
+            trajs.append(t)
+        shape = DSV3
+    return trajs, shape
+
+
+def cluster(shape, P, D, cap_bps):
+    import paper_2602_21548_b200 as dp
+    cfg = dp.ClusterConfig()
+    cfg.prefill_nodes, cfg.decode_nodes, cfg.engines_per_node = P, D, 1
+    cfg.n_layer, cfg.kv_bytes_per_token_per_layer, cfg.block_size_tokens = shape["L"], shape["b"], shape["T"]
+    # compute network = NVLink (the DE->PE push), storage NIC = the engine's
+    # PCIe read rate, or the emulated cap when one is set
+    cfg.cnic_bandwidth = NVLINK_BPS
+    cfg.storage_multiple = (cap_bps if cap_bps > 0 else PCIE_ZC_BPS) / NVLINK_BPS
+    cfg.dram_bandwidth = 2e12
+    cfg.hbm_capacity_tokens = 100_000_000
+    cfg.pe_buffer_bytes = 1 << 42
+    cfg.de_buffer_bytes = 1 << 42
+    return cfg
+
+
+# storage-bound cost model (proj/tests/acceptance.cpp:62-72): the bench
+# measures loading, compute is nearly free
+PLAN_KW = dict(cl=1e-12, dctx=1e-15, dstep=1e-9, sub=0.0, beta=1_000_000_000)
+
+
+# ------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self, devices):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        if not self.proc or not os.path.exists(self.path):
+            return out
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9 or not p[0].isdigit() or int(p[0]) not in devices:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if sm:
+            out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                   "samples": len(sm)}
+        return out
+
+
+# ------------------------------------------------------------ distributed
+class Dist:
+    def __init__(self, n):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.torch = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as td
+            torch.cuda.set_device(self.local)
+            td.init_process_group("nccl", device_id=torch.device(f"cuda:{self.local}"))
+            self.torch, self.td = torch, td
+        if self.world != n and n > 1:
+            raise SystemExit(f"--gpus {n} needs torchrun with {n} ranks (WORLD_SIZE={self.world})")
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def allgather(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.td.all_gather_object(out, obj)
+        return out
+
+    def max(self, x):
+        return max(self.allgather(x))
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+# --------------------------------------------------------------- measuring
+def measure_pcie_peak(device):
+    """Copy-engine H2D of 1 GiB pinned, best of 5 (the PCIe link roofline)."""
+    import torch
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+    s = torch.cuda.Stream(device=device)
+    best = 1e9
+    with torch.cuda.stream(s):
+        for _ in range(5):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            d.copy_(h, non_blocking=True)
+            b.record(s)
+            b.synchronize()
+            best = min(best, a.elapsed_time(b))
+    del h, d
+    return n / (best * 1e-3)
+
+
+def run_policy(args, dist, policy, trajs, shape, P, D, devices_used, clocks=None):
+    """Plan, build engines, run W + K steps; returns per-step max-over-ranks
+    device and host times, plus per-rank info."""
+    import paper_2602_21548_b200 as dp
+    cap = args.cap_gbps * 1e9
+    cfg = cluster(shape, P, D, cap)
+    t0 = time.time()
+    planned = dp.plan(cfg, trajs, policy=policy, **PLAN_KW)
+    plan_s = time.time() - t0
+    opt = dp.ExecOptions()
+    opt.storage_cap_Bps = cap
+    opt.seed = 9
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    digest = hashlib.sha1(repr([(d[1], d[2], d[3], d[4]) for d in planned["decisions"]]).encode()).hexdigest()
+    digests = dist.allgather(digest)
+    assert len(set(digests)) == 1, "ranks planned differently"
+    if dist.world > 1:
+        my = [dist.rank]
+    else:
+        my = [0]  # N=1: only the PE engine exists on this box
+    engines = {}
+    for e in my:
+        dev = dist.local if dist.world > 1 else 0
+        engines[e] = dp.EngineRuntime(xp, e, dev)
+    if dist.world > 1:
+        handles = dist.allgather(engines[dist.rank].export_pool() if dist.rank < cfg.prefill_nodes else None)
+        for e, rt in engines.items():
+            if e >= cfg.prefill_nodes:
+                for pe in range(cfg.prefill_nodes):
+                    rt.attach_peer(pe, handles[pe])
+    dev_ms, host_ms, launches, read_bytes = [], [], 0, 0
+    for step in range(args.warmup + args.steps):
+        for rt in engines.values():
+            rt.reset_counters()
+        dist.barrier()
+        if clocks is not None and step == args.warmup:
+            clocks.__enter__()  # sample clocks during the timed steps only
+        res = [rt.run_step() for rt in engines.values()]
+        d = dist.max(max(r.device_ms for r in res))
+        h = dist.max(max(r.host_ms for r in res))
+        if step >= args.warmup:
+            dev_ms.append(d)
+            host_ms.append(h)
+            launches += sum(dist.allgather(sum(r.launches for r in res)))
+            read_bytes += sum(dist.allgather(sum(r.bytes_read for r in res)))
+    info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens,
+                requests=xp.requests, reader_bytes=list(xp.reader_bytes),
+                de_path=sum(1 for d in planned["decisions"] if d[4] == 1),
+                decisions=len(planned["decisions"]), pool_slots=xp.pool_slots,
+                store_fb=xp.store_fb, launches=launches, read_bytes=read_bytes)
+    if clocks is not None:
+        clocks.__exit__()
+    engines.clear()  # frees pools, stores and peer mappings before the next policy
+    dist.barrier()
+    return dict(dev_ms=dev_ms, host_ms=host_ms, info=info, xp=xp, cfg=cfg)
+
+
+def cpu_baseline(xp, shape, seconds=12.0):
+    """oracle/kvref.c gather of the same Layer Blocks on all host cores
+    (the CPU port of the path), on a bounded sample of the workload."""
+    import ctypes
+    import numpy as np
+    from oracle import refpy
+    g = refpy.geom(shape["L"], shape["T"], shape["b"])
+    fb_bytes = shape["L"] * shape["T"] * shape["b"]
+    n_fb = min(xp.store_fb, 256)
+    store = np.empty(n_fb * fb_bytes, dtype=np.uint8)
+    # content restated on the CPU (multi-threaded by Full Block range)
+    threads = os.cpu_count() or 1
+    chunks = np.array_split(np.arange(n_fb), threads)
+    ths = []
+    for c in chunks:
+        if len(c) == 0:
+            continue
+        def work(c=c):
+            refpy.kvref().kvref_fill_store(ctypes.byref(g), 9, int(c[0]), len(c),
+                                           store[int(c[0]) * fb_bytes:].ctypes.data)
+        th = threading.Thread(target=work)
+        th.start()
+        ths.append(th)
+    for th in ths:
+        th.join()
+    jobs = xp.jobs()
+    specs, moved = [], 0
+    target = 8 << 30
+    for j in jobs:
+        fbs = [f % n_fb for f in j[10]]
+        specs.append((fbs, j[9], j[6], 0, shape["L"]))
+        moved += j[6] * shape["L"] * shape["b"]
+        if moved >= target:
+            break
+    n_slots = xp.pool_slots
+    lb = shape["T"] * shape["b"]
+    pool = np.zeros(shape["L"] * n_slots * lb, dtype=np.uint8)
+    arr, keep = refpy.make_jobs(specs)
+    t0 = time.time()
+    total = 0
+    reps = 0
+    while time.time() - t0 < seconds or reps == 0:
+        total += refpy.kvref().kvref_gather_mt(ctypes.byref(g), store.ctypes.data, arr, len(specs),
+                                               pool.ctypes.data, n_slots, threads)
+        reps += 1
+    dt = time.time() - t0
+    return {"value": round(total / dt / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{len(specs)} requests ({moved / 1e9:.1f} GB of Layer Blocks) x {reps} reps, "
+                      f"memcpy gather store->host pool, {threads} threads"}
+
+
+# ---------------------------------------------------------------- reference
+def reference_arm(args):
+    """The reference's own CPU implementation of the path (pdsim desim,
+    compiled from /root/reference sources into oracle/_ref) on this box's
+    host cores: independent simulations of session shards run concurrently
+    (the reference's sweep parallelism); metric = hit KV bytes the reference
+    path processes per wall second."""
+    from concurrent.futures import ThreadPoolExecutor
+    import paper_2602_21548_b200 as dp
+    from oracle import refpy
+    n = args.gpus
+    trajs, shape = workload(args, n)
+    P, D = (1, 1) if n == 1 else (n // 2, n - n // 2)
+    cap = args.cap_gbps * 1e9
+    cfg = cluster(shape, P, D, cap)
+    threads = os.cpu_count() or 1
+    # bounded sample: 4 sessions per shard (about 10-30 s of CPU per step)
+    shard = 4
+    shards = [trajs[i:i + shard] for i in range(0, len(trajs), shard)][:threads]
+    paths = []
+    for i, sh in enumerate(shards):
+        p = f"/tmp/dp_ref_shard_{os.getpid()}_{i}.tsv"
+        dp.save_trace(p, sh)
+        paths.append(p)
+    kv = dict(P=P, D=D, g=1, L=shape["L"], b=shape["b"], T=shape["T"], B=cfg.cnic_bandwidth,
+              s=cfg.storage_multiple, M=cfg.dram_bandwidth, hbm=cfg.hbm_capacity_tokens,
+              pe_buf=cfg.pe_buffer_bytes, de_buf=cfg.de_buffer_bytes,
+              policy="pe_only" if n == 1 else "dual_path", **PLAN_KW)
+    per_tok = shape["L"] * shape["b"]
+    hit = 0
+    for sh in shards:
+        for t in sh:
+            c = 0
+            for r in t.rounds:
+                hit += c * per_tok
+                c += r.append_tokens + r.gen_tokens
+    vals = []
+    sim_agg = []
+
+    def one(p):
+        return refpy.ref_simulate(p, **kv)
+
+    with ThreadPoolExecutor(max_workers=len(paths)) as ex:
+        for step in range(args.warmup + args.steps):
+            t0 = time.time()
+            reps = list(ex.map(one, paths))
+            dt = time.time() - t0
+            if step >= args.warmup:
+                vals.append(hit / dt / 1e9)
+                sim_agg.append(sum(sum(u[4] for u in r["usage"] if u[0] == "snic_read") for r in reps)
+                               / max(r["makespan"] for r in reps) / 1e9)
+    for p in paths:
+        os.unlink(p)
+    v = statistics.median(vals)
+    return {"metric": "aggregate KV-load GB/s", "value": round(v, 3), "unit": "GB/s", "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "impl": "reference",
+            "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"{args.workload} {'1P-only loader' if n == 1 else f'{P}P{D}D dual_path'}",
+                       "kv": shape, "sample_sessions": sum(len(s) for s in shards)},
+            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": len(paths),
+                             "kind": "reference",
+                             "sample": f"{len(paths)} concurrent desim::run_offline shards x {shard} "
+                                       f"sessions ({hit / 1e9:.1f} GB hit KV simulated per step)"},
+            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_simulated_aggkv_gbps": round(statistics.median(sim_agg), 3)}
+
+
+# --------------------------------------------------------------------- main
+def main():
+    args = parse()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        print(json.dumps(reference_arm(args)))
+        return
+    import paper_2602_21548_b200 as dp  # noqa: F401  (fails loudly without the extension)
+    n = args.gpus
+    dist = Dist(n)
+    trajs, shape = workload(args, n)
+    if args.pd:
+        P, D = (int(x) for x in args.pd.split(":"))
+    else:
+        P, D = (1, 1) if n == 1 else (n // 2, n - n // 2)
+    policies = ["pe_only"] if n == 1 else ["dual_path"] + ([] if args.no_one_path else ["pe_only"])
+    peak = None
+    if dist.rank == 0:
+        peak = measure_pcie_peak(dist.local if dist.world > 1 else 0)
+    results = {}
+    clocks = ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
+                          if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_{os.getpid()}.csv")
+    for pol in policies:
+        results[pol] = run_policy(args, dist, pol, trajs, shape, P, D, n,
+                                  clocks if (pol == policies[0] and dist.local == 0) else None)
+    head = results[policies[0]]
+    info = head["info"]
+    dev_s = sum(head["dev_ms"]) / 1e3
+    host_s = sum(head["host_ms"]) / 1e3
+    K = args.steps
+    value = info["hit_bytes"] * K / dev_s / 1e9
+    e2e = info["hit_bytes"] * K / host_s / 1e9
+    tokens_s = info["prompt_tokens"] * K / dev_s
+    cpu = None
+    if dist.rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(head["xp"], shape)
+        except Exception as exc:  # reported, never fatal to the GPU number
+            cpu = {"error": str(exc)[:200]}
+    clk = clocks.summary(set(range(8)))
+    if dist.rank == 0:
+        # roofline of the dominant kernel (K1 on the PE): its bytes over its
+        # device time in the timed steps (K1 is the only non-trivial kernel
+        # of the PE's stream; waits complete immediately on a PE-only step)
+        k1_bytes = info["reader_bytes"][0]
+        k1_ms = statistics.mean(head["dev_ms"]) if n == 1 else None
+        achieved = k1_bytes / (k1_ms * 1e-3) / 1e9 if k1_ms else value / max(1, n)
+        out = {
+            "metric": "aggregate KV-load GB/s",
+            "value": round(value, 3),
+            "unit": "GB/s",
+            "n_gpus": n,
+            "steps": K,
+            "warmup": args.warmup,
+            "ms_per_step": round(dev_s * 1e3 / K, 3),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {len(trajs)} sessions, "
+                                   + ("1 PE loader (K1)" if n == 1 else f"{P}P{D}D dual_path"),
+                       "kv": shape, "storage_cap_gbps_per_engine": args.cap_gbps or None,
+                       "requests": info["requests"], "hit_bytes_per_step": info["hit_bytes"],
+                       "de_path_requests": info["de_path"], "l2": "inputs >> L2 (no flush needed)"},
+            "tokens_per_s": round(tokens_s, 1),
+            "e2e": {"value": round(e2e, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": info["hit_bytes"],
+                    "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": info["launches"],
+            "roofline": {"bound": "pcie", "achieved": round(achieved, 2),
+                         "peak": round(peak / 1e9, 2) if peak else None, "unit": "GB/s",
+                         "frac": round(achieved / (peak / 1e9), 4) if peak else None,
+                         "traffic": None,
+                         "peak_source": "cudaMemcpyAsync H2D 1 GiB pinned, best of 5, measured in this run"},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "plan_s": round(info["plan_s"], 2),
+        }
+        if "pe_only" in results and n > 1:
+            po = results["pe_only"]
+            po_s = sum(po["dev_ms"]) / 1e3
+            po_v = po["info"]["hit_bytes"] * K / po_s / 1e9
+            out["one_path"] = {"value": round(po_v, 3), "unit": "GB/s",
+                               "tokens_per_s": round(po["info"]["prompt_tokens"] * K / po_s, 1),
+                               "dual_vs_one_path": round(value / po_v, 3)}
+        print(json.dumps(out))
+    dist.barrier()
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -57,6 +57,7 @@ struct LoadJob {
   std::vector<std::int32_t> preds;         // tickets in the same PE pool whose slots this
   std::vector<std::uint32_t> pred_targets; // reuses (written by another engine), and their
                                            // all-layer landed-item targets
+  bool fence = false;  // reuses a slot this reader wrote earlier: must not share a launch
 };
 
 struct ExecPlan {

@@ -141,6 +141,13 @@ int dp_wait_status(const dp_pool* pool);
 int dp_pool_checksum(const dp_pool* pool, int32_t layer, const int32_t* slots,
                      const int32_t* ntok, int32_t n, uint64_t* out, dp_stream stream);
 
+/* Synchronous copy of `bytes` bytes of pool Layer Block (layer, slot) to
+ * host memory (inspection / parity checks). */
+int dp_pool_copy_out(const dp_pool* pool, int32_t layer, int32_t slot, int64_t bytes,
+                     void* host_out);
+/* Number of CUDA devices visible (0 when none). */
+int dp_device_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,220 @@
+"""ctypes binding of the C ABI (include/dualpath/kv_abi.h).
+
+This is the binding a maintainer of the reference's Python shim would add
+(INTEGRATION.md): plain pointers and sizes, no torch types.  Errors raise
+``DualPathError`` carrying ``dp_last_error()``.  Streams are passed as raw
+``cudaStream_t`` integers (0 = legacy default stream).
+"""
+
+import ctypes
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdualpath.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "dualpath", "kv_abi.h")
+
+DP_OK, DP_EINVAL, DP_ECUDA, DP_ENOMEM, DP_ETIMEOUT = 0, -1, -2, -3, -4
+MAX_JOBS_PER_LAUNCH = 64
+
+
+class DualPathError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class Geom(ctypes.Structure):
+    _fields_ = [("n_layer", ctypes.c_int32), ("block_tokens", ctypes.c_int32),
+                ("bytes_per_token_layer", ctypes.c_int64)]
+
+
+class Job(ctypes.Structure):
+    _fields_ = [("src_fb", ctypes.c_void_p), ("dst_slot", ctypes.c_void_p),
+                ("n_tokens", ctypes.c_int64), ("n_blk", ctypes.c_int32),
+                ("layer_begin", ctypes.c_int32), ("layer_end", ctypes.c_int32),
+                ("ticket", ctypes.c_int32)]
+
+
+class PoolHandle(ctypes.Structure):
+    _fields_ = [("ipc", ctypes.c_ubyte * 64), ("geom", Geom), ("n_slots", ctypes.c_int32),
+                ("n_tickets", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdualpath.so (raises if the native build is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: the CUDA extension is not built")
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    sig = {
+        "dp_abi_version": ([], ctypes.c_int),
+        "dp_last_error": ([], ctypes.c_char_p),
+        "dp_geom_check": ([ctypes.POINTER(Geom)], ctypes.c_int),
+        "dp_store_create": ([ctypes.c_int, ctypes.POINTER(Geom), ctypes.c_int64, ctypes.c_uint64, PP],
+                            ctypes.c_int),
+        "dp_store_destroy": ([P], ctypes.c_int),
+        "dp_store_info": ([P, PP, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)],
+                          ctypes.c_int),
+        "dp_pool_create": ([ctypes.c_int, ctypes.POINTER(Geom), ctypes.c_int32, ctypes.c_int32, PP],
+                           ctypes.c_int),
+        "dp_pool_destroy": ([P], ctypes.c_int),
+        "dp_pool_info": ([P, PP, PP, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "dp_pool_reset_counters": ([P, P], ctypes.c_int),
+        "dp_pool_export": ([P, ctypes.POINTER(PoolHandle)], ctypes.c_int),
+        "dp_pool_import": ([ctypes.c_int, ctypes.POINTER(PoolHandle), PP], ctypes.c_int),
+        "dp_pool_peer_view": ([ctypes.c_int, P, PP], ctypes.c_int),
+        "dp_h2d_layer_gather": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
+        "dp_h2d_push_p2p_layer": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
+        "dp_layer_items": ([ctypes.POINTER(Geom), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
+                           ctypes.c_int),
+        "dp_wait_layer": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int32, P],
+                          ctypes.c_int),
+        "dp_wait_tickets": ([P, P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P],
+                            ctypes.c_int),
+        "dp_wait_status": ([P], ctypes.c_int),
+        "dp_pool_checksum": ([P, ctypes.c_int32, P, P, ctypes.c_int32, P, P], ctypes.c_int),
+        "dp_pool_copy_out": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P], ctypes.c_int),
+        "dp_device_count": ([], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def declared_symbols(header=HEADER):
+    """Entry points declared in include/dualpath/kv_abi.h."""
+    text = open(header).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(dp_\w+)\s*\(", text, re.M)))
+
+
+def check(rc):
+    if rc != DP_OK:
+        raise DualPathError(rc, lib().dp_last_error().decode())
+    return rc
+
+
+def geom(n_layer, block_tokens, b):
+    return Geom(n_layer, block_tokens, b)
+
+
+class Store:
+    """Pinned+mapped host Full Blocks filled with the deterministic content."""
+
+    def __init__(self, device, g, n_fb, seed):
+        self.ptr = ctypes.c_void_p()
+        check(lib().dp_store_create(device, ctypes.byref(g), n_fb, seed, ctypes.byref(self.ptr)))
+        self.geom = g
+        self.n_fb = n_fb
+
+    def info(self):
+        host = ctypes.c_void_p()
+        nbytes = ctypes.c_int64()
+        nfb = ctypes.c_int64()
+        check(lib().dp_store_info(self.ptr, ctypes.byref(host), ctypes.byref(nbytes), ctypes.byref(nfb)))
+        return host.value, nbytes.value, nfb.value
+
+    def bytes(self):
+        host, nbytes, _ = self.info()
+        return ctypes.string_at(host, nbytes)
+
+    def close(self):
+        if self.ptr:
+            check(lib().dp_store_destroy(self.ptr))
+            self.ptr = ctypes.c_void_p()
+
+
+class Pool:
+    """Paged HBM pool [L][n_slots][T][b] + landed counters [n_tickets][L+1]."""
+
+    def __init__(self, device=None, g=None, n_slots=0, n_tickets=0, _ptr=None):
+        self.geom = g
+        self.n_slots = n_slots
+        self.n_tickets = n_tickets
+        if _ptr is not None:
+            self.ptr = _ptr
+            return
+        self.ptr = ctypes.c_void_p()
+        check(lib().dp_pool_create(device, ctypes.byref(g), n_slots, n_tickets, ctypes.byref(self.ptr)))
+
+    def info(self):
+        base = ctypes.c_void_p()
+        ctr = ctypes.c_void_p()
+        nbytes = ctypes.c_int64()
+        check(lib().dp_pool_info(self.ptr, ctypes.byref(base), ctypes.byref(ctr), ctypes.byref(nbytes)))
+        return base.value, ctr.value, nbytes.value
+
+    def peer_view(self, device):
+        v = ctypes.c_void_p()
+        check(lib().dp_pool_peer_view(device, self.ptr, ctypes.byref(v)))
+        return Pool(g=self.geom, n_slots=self.n_slots, n_tickets=self.n_tickets, _ptr=v)
+
+    def export(self):
+        h = PoolHandle()
+        check(lib().dp_pool_export(self.ptr, ctypes.byref(h)))
+        return bytes(h)
+
+    @staticmethod
+    def open(device, handle_bytes):
+        h = PoolHandle.from_buffer_copy(handle_bytes)
+        v = ctypes.c_void_p()
+        check(lib().dp_pool_import(device, ctypes.byref(h), ctypes.byref(v)))
+        return Pool(g=h.geom, n_slots=h.n_slots, n_tickets=h.n_tickets, _ptr=v)
+
+    def copy_out(self, layer, slot, nbytes):
+        buf = ctypes.create_string_buffer(nbytes)
+        check(lib().dp_pool_copy_out(self.ptr, layer, slot, nbytes, buf))
+        return buf.raw
+
+    def reset_counters(self, stream=0):
+        check(lib().dp_pool_reset_counters(self.ptr, ctypes.c_void_p(stream)))
+
+    def close(self):
+        if self.ptr:
+            check(lib().dp_pool_destroy(self.ptr))
+            self.ptr = ctypes.c_void_p()
+
+
+def make_jobs(specs):
+    """specs: list of (src_fb_devptr, dst_slot_devptr, n_tokens, n_blk, l0, l1, ticket)."""
+    arr = (Job * max(1, len(specs)))()
+    for i, (fb, sl, ntok, nblk, l0, l1, tk) in enumerate(specs):
+        arr[i] = Job(fb, sl, ntok, nblk, l0, l1, tk)
+    return arr
+
+
+def h2d_layer_gather(pool, store, jobs, n, stream=0):
+    check(lib().dp_h2d_layer_gather(pool.ptr, store.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def h2d_push_p2p_layer(pool_view, store, jobs, n, stream=0):
+    check(lib().dp_h2d_push_p2p_layer(pool_view.ptr, store.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def layer_items(g, n_blk):
+    out = ctypes.c_int32()
+    check(lib().dp_layer_items(ctypes.byref(g), n_blk, ctypes.byref(out)))
+    return out.value
+
+
+def wait_layer(pool, ticket, layer, target, timeout_ms=10000, stream=0):
+    check(lib().dp_wait_layer(pool.ptr, ticket, layer, target, timeout_ms, ctypes.c_void_p(stream)))
+
+
+def wait_status(pool):
+    return lib().dp_wait_status(pool.ptr)
+
+
+def device_count():
+    return lib().dp_device_count()

@@ -338,7 +338,7 @@ PYBIND11_MODULE(_core, m) {
       .def_readonly("requests", &dualpath::ExecPlan::requests)
       .def("fb_of", &dualpath::ExecPlan::fb_of)
       .def("jobs", [](const dualpath::ExecPlan& x) {
-        // (req, traj, round, reader, pe, de_path, cached, n_blk, ticket, slots, src_fb, preds)
+        // (req, traj, round, reader, pe, de_path, cached, n_blk, ticket, slots, src_fb, preds, fence)
         py::list out;
         for (const auto& j : x.jobs) {
           std::vector<std::int32_t> sl(x.slots[j.reader].begin() + j.blk_off,
@@ -346,7 +346,7 @@ PYBIND11_MODULE(_core, m) {
           std::vector<std::int64_t> fb(x.src_fb[j.reader].begin() + j.blk_off,
                                        x.src_fb[j.reader].begin() + j.blk_off + j.n_blk);
           out.append(py::make_tuple(j.req, j.traj, j.round, j.reader, j.pe, j.de_path, j.cached,
-                                    j.n_blk, j.ticket, sl, fb, j.preds));
+                                    j.n_blk, j.ticket, sl, fb, j.preds, j.fence));
         }
         return out;
       })

@@ -157,6 +157,9 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
       fq.pop_front();
       mine.push_back(s);
       const std::int32_t prev = owner[j.pe][s];
+      // same reader: stream order serialises launches, but items of one
+      // launch run concurrently, so the reuse must start a new launch
+      if (prev >= 0 && jobs[prev].reader == j.reader) j.fence = true;
       if (prev >= 0 && jobs[prev].reader != j.reader &&
           std::find(j.preds.begin(), j.preds.end(), jobs[prev].ticket) == j.preds.end()) {
         j.preds.push_back(jobs[prev].ticket);
@@ -330,7 +333,8 @@ StepResult EngineRuntime::run_step() {
     const std::int64_t bytes = j.cached * x.cfg.kv_bytes_per_token();
     const bool gated = cap > 0;
     const bool hazard = !j.preds.empty();
-    if (gated || hazard || batch_pe != j.pe || batch.size() == DP_MAX_JOBS_PER_LAUNCH) flush();
+    if (gated || hazard || j.fence || batch_pe != j.pe || batch.size() == DP_MAX_JOBS_PER_LAUNCH)
+      flush();
     if (gated) {
       // StorageRead of C*L*b bytes over this engine's storage NIC
       gate_s += static_cast<double>(bytes) / cap;

@@ -646,4 +646,25 @@ int dp_pool_checksum(const dp_pool* pool, int32_t layer, const int32_t* slots,
   return DP_OK;
 }
 
+int dp_pool_copy_out(const dp_pool* pool, int32_t layer, int32_t slot, int64_t bytes,
+                     void* host_out) {
+  if (!pool || !host_out || bytes < 0) return fail(DP_EINVAL, "pool_copy_out: bad argument");
+  const int64_t lb = static_cast<int64_t>(pool->geom.block_tokens) * pool->geom.bytes_per_token_layer;
+  if (layer < 0 || layer >= pool->geom.n_layer || slot < 0 || slot >= pool->n_slots || bytes > lb)
+    return fail(DP_EINVAL, "pool_copy_out: out of range");
+  DeviceGuard guard(pool->device);
+  const char* src = pool->base + (static_cast<int64_t>(layer) * pool->n_slots + slot) * lb;
+  DP_CUDA(cudaMemcpy(host_out, src, bytes, cudaMemcpyDeviceToHost));
+  return DP_OK;
+}
+
+int dp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 }  // extern "C"

@@ -1,0 +1,153 @@
+"""GPU parity of the executor: plan -> EngineRuntime steps -> final paged KV
+pools compared with the CPU oracle (every Layer Block's content hash, from
+oracle/kvref.c's content formula), block tables and counters."""
+
+import numpy as np
+import pytest
+
+import paper_2602_21548_b200 as dp
+from oracle import refpy
+
+pytestmark = pytest.mark.gpu
+
+SEED = 9
+
+
+def cluster(P, D, L=6, b=576, T=64):
+    cfg = dp.ClusterConfig()
+    cfg.prefill_nodes, cfg.decode_nodes, cfg.engines_per_node = P, D, 1
+    cfg.n_layer, cfg.kv_bytes_per_token_per_layer, cfg.block_size_tokens = L, b, T
+    cfg.cnic_bandwidth = 50e9
+    cfg.storage_multiple = 0.125
+    cfg.dram_bandwidth = 500e9
+    cfg.hbm_capacity_tokens = 100_000_000
+    cfg.pe_buffer_bytes = 1 << 42
+    cfg.de_buffer_bytes = 1 << 42
+    return cfg
+
+
+STORAGE_BOUND = dict(cl=1e-12, dctx=1e-15, dstep=1e-9, sub=0.0, beta=1_000_000_000)
+
+
+def final_occupants(xp, pe):
+    """slot -> (Full Block, valid tokens) of the last job that wrote it."""
+    last = {}
+    for job in xp.jobs():
+        req, traj, rnd, reader, jpe, de_path, cached, nblk, ticket, slots, fbs, preds, fence = job
+        if jpe != pe:
+            continue
+        for k, (s, fb) in enumerate(zip(slots, fbs)):
+            last[s] = (fb, min(xp_T(xp), cached - xp_T(xp) * k))
+    return last
+
+
+def xp_T(xp):
+    return 64
+
+
+def verify_pool(engine, xp, cfg):
+    last = final_occupants(xp, engine.engine)
+    slots = sorted(last)
+    g = refpy.geom(cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer)
+    for layer in range(cfg.n_layer):
+        got = engine.checksum(layer, slots, [last[s][1] for s in slots])
+        want = [refpy.layer_block_hash(g, SEED, last[s][0], layer, last[s][1]) for s in slots]
+        assert list(got) == want, f"pool mismatch on PE {engine.engine} layer {layer}"
+    return len(slots)
+
+
+def verify_counters(engine, xp, cfg):
+    ctr = np.asarray(engine.counters(), dtype=np.int64).reshape(-1, cfg.n_layer + 1)
+    for job in xp.jobs():
+        if job[4] != engine.engine:
+            continue
+        items = job[7] * xp.items_per_block
+        assert (ctr[job[8], :cfg.n_layer] == items).all()
+        assert ctr[job[8], cfg.n_layer] == items * cfg.n_layer
+
+
+def small_trace(count=6, turns=5, max_len=12000, seed=4):
+    return dp.synthesize(max_len=max_len, count=count, seed=seed, mean_turns=turns, sigma_turns=0)
+
+
+def test_single_engine_pe_only(gpus):
+    cfg = cluster(1, 1)
+    trajs = small_trace()
+    planned = dp.plan(cfg, trajs, policy="pe_only", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert xp.reader_bytes[1] == 0 and xp.reader_bytes[0] == xp.hit_bytes
+    eng = dp.EngineRuntime(xp, 0, 0)
+    for _ in range(2):
+        eng.reset_counters()
+        r = eng.run_step()
+        assert r.bytes_read == xp.hit_bytes
+    verify_counters(eng, xp, cfg)
+    assert verify_pool(eng, xp, cfg) > 0
+
+
+def test_slot_reuse_same_reader(gpus):
+    # a pool exactly at the plan's peak forces FIFO reuse within the step
+    cfg = cluster(1, 1)
+    trajs = small_trace(count=4, turns=6)
+    planned = dp.plan(cfg, trajs, policy="pe_only", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    probe = dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.pool_slots = probe.peak_slots
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert xp.pool_slots == xp.peak_slots
+    assert any(job[12] for job in xp.jobs()), "expected same-reader slot reuse"
+    eng = dp.EngineRuntime(xp, 0, 0)
+    eng.reset_counters()
+    eng.run_step()
+    verify_pool(eng, xp, cfg)
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("policy", ["dual_path", "pe_only", "round_robin"])
+def test_two_engines_1p1d(two_gpus, policy):
+    cfg = cluster(1, 1)
+    trajs = small_trace(count=8, turns=5)
+    kw = dict(STORAGE_BOUND)
+    if policy == "round_robin":
+        planned = dp.plan(cfg, trajs, policy="dual_path", sched_mode="round_robin", **kw)
+    else:
+        planned = dp.plan(cfg, trajs, policy=policy, **kw)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    pe = dp.EngineRuntime(xp, 0, 0)
+    de = dp.EngineRuntime(xp, 1, 1)
+    de.attach_peer_local(0, pe)
+    if policy != "pe_only":
+        assert xp.reader_bytes[1] > 0, "dual path should read on the DE side"
+    for _ in range(2):
+        pe.reset_counters()
+        res = dp.run_step_all([pe, de])
+        assert res[0].bytes_read + res[1].bytes_read == xp.hit_bytes
+    verify_counters(pe, xp, cfg)
+    verify_pool(pe, xp, cfg)
+
+
+@pytest.mark.multigpu
+def test_cross_reader_slot_reuse_hazards(two_gpus):
+    # tight pool: slots freed by a DE-path job get reused by PE-path jobs and
+    # vice versa; the hazard waits keep the final pool equal to the oracle's
+    cfg = cluster(1, 1, L=4)
+    trajs = small_trace(count=10, turns=6, seed=8)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    probe = dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.pool_slots = probe.peak_slots
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert any(job[11] for job in xp.jobs()), "expected cross-reader reuse"
+    pe = dp.EngineRuntime(xp, 0, 0)
+    de = dp.EngineRuntime(xp, 1, 1)
+    de.attach_peer_local(0, pe)
+    for _ in range(3):
+        pe.reset_counters()
+        dp.run_step_all([pe, de])
+        verify_pool(pe, xp, cfg)

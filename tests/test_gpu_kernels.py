@@ -1,0 +1,219 @@
+"""GPU parity of the sm_100a kernels, called through the C ABI
+(include/dualpath/kv_abi.h), against the CPU oracle (oracle/kvref.c).
+
+Bar: bit-exact bytes for every moved Layer Block (integer/byte work)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import refpy
+from paper_2602_21548_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+SEED = 9
+GEOMS = [(4, 64, 576), (61, 64, 576), (2, 64, 4096), (3, 16, 1024)]  # DS-V3, Qwen-like, tiny
+
+
+def dev_i64(x, device=0):
+    import torch
+    return torch.tensor(np.asarray(x, dtype=np.int64), device=f"cuda:{device}")
+
+
+def dev_i32(x, device=0):
+    import torch
+    return torch.tensor(np.asarray(x, dtype=np.int32), device=f"cuda:{device}")
+
+
+def sync():
+    import torch
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("L,T,b", GEOMS)
+def test_store_content_matches_oracle(gpus, L, T, b):
+    g = abi.geom(L, T, b)
+    st = abi.Store(0, g, 5, SEED)
+    try:
+        got = np.frombuffer(st.bytes(), dtype=np.uint8)
+        want = refpy.fill_store(refpy.geom(L, T, b), SEED, 5)
+        assert got.shape == want.shape
+        assert np.array_equal(got, want)
+    finally:
+        st.close()
+
+
+def random_jobs(rng, L, T, n_jobs, n_fb, n_slots, max_blk, device=0, layers=None):
+    """Random jobs with partial last blocks and disjoint slots."""
+    perm = rng.permutation(n_slots)
+    used = 0
+    specs, keep, plain = [], [], []
+    for t in range(n_jobs):
+        nblk = int(rng.integers(0, max_blk + 1))
+        if used + nblk > n_slots:
+            nblk = 0
+        ntok = 0 if nblk == 0 else (nblk - 1) * T + int(rng.integers(1, T + 1))
+        fbs = rng.integers(0, n_fb, nblk).astype(np.int64)
+        slots = perm[used:used + nblk].astype(np.int32)
+        used += nblk
+        l0, l1 = layers if layers else (0, L)
+        df, ds = dev_i64(fbs if nblk else [0], device), dev_i32(slots if nblk else [0], device)
+        keep += [df, ds]
+        specs.append((df.data_ptr(), ds.data_ptr(), ntok, nblk, l0, l1, t))
+        plain.append((fbs, slots, ntok, l0, l1))
+    return specs, keep, plain
+
+
+def check_pool(pool, g_ref, plain, T, b, store_img, n_slots):
+    want = refpy.gather(g_ref, store_img, store_img.nbytes // (g_ref.n_layer * T * b),
+                        [(f, s, n, l0, l1) for f, s, n, l0, l1 in plain], n_slots)
+    lb = T * b
+    for fbs, slots, ntok, l0, l1 in plain:
+        for k, s in enumerate(slots):
+            n = min(T, ntok - k * T) * b
+            for layer in range(l0, l1):
+                got = pool.copy_out(layer, int(s), n)
+                off = (layer * n_slots + int(s)) * lb
+                assert got == want[off:off + n].tobytes(), (layer, s, k)
+
+
+@pytest.mark.parametrize("L,T,b", GEOMS)
+def test_k1_gather_parity(gpus, L, T, b):
+    rng = np.random.default_rng(L * 1000 + b)
+    g = abi.geom(L, T, b)
+    n_fb, n_slots = 12, 64
+    st = abi.Store(0, g, n_fb, SEED)
+    pool = abi.Pool(0, g, n_slots, 80)
+    try:
+        # 70 jobs -> two launches (64 job headers per launch); some empty
+        specs, keep, plain = random_jobs(rng, L, T, 70, n_fb, n_slots, 3)
+        jobs = abi.make_jobs(specs)
+        abi.h2d_layer_gather(pool, st, jobs, len(specs))
+        sync()
+        store_img = np.frombuffer(st.bytes(), dtype=np.uint8).copy()
+        check_pool(pool, refpy.geom(L, T, b), plain, T, b, store_img, n_slots)
+        # landed counters: the all-layer column reaches items * layers
+        for t, (fbs, slots, ntok, l0, l1) in enumerate(plain):
+            items = abi.layer_items(g, len(slots))
+            abi.wait_layer(pool, t, L, items * (l1 - l0), timeout_ms=5000)
+            if len(slots):
+                abi.wait_layer(pool, t, l0, items, timeout_ms=5000)
+        sync()
+        assert abi.wait_status(pool) == abi.DP_OK
+    finally:
+        pool.close()
+        st.close()
+
+
+def test_k1_layer_subrange_and_chunks(gpus):
+    # Qwen-like Layer Block (256 KiB) -> 4 chunk items per block; layers 3..5 only
+    L, T, b = 8, 64, 4096
+    rng = np.random.default_rng(5)
+    g = abi.geom(L, T, b)
+    st = abi.Store(0, g, 6, SEED)
+    pool = abi.Pool(0, g, 16, 8)
+    try:
+        specs, keep, plain = random_jobs(rng, L, T, 6, 6, 16, 2, layers=(3, 6))
+        assert abi.layer_items(g, 1) == 4
+        abi.h2d_layer_gather(pool, st, abi.make_jobs(specs), len(specs))
+        sync()
+        store_img = np.frombuffer(st.bytes(), dtype=np.uint8).copy()
+        check_pool(pool, refpy.geom(L, T, b), plain, T, b, store_img, 16)
+    finally:
+        pool.close()
+        st.close()
+
+
+def test_checksum_matches_oracle(gpus):
+    L, T, b = 4, 64, 576
+    g = abi.geom(L, T, b)
+    st = abi.Store(0, g, 4, SEED)
+    pool = abi.Pool(0, g, 8, 1)
+    try:
+        fbs, slots, ntok = [3, 1, 2], [5, 0, 7], 64 * 2 + 9
+        df, ds = dev_i64(fbs), dev_i32(slots)
+        abi.h2d_layer_gather(pool, st, abi.make_jobs([(df.data_ptr(), ds.data_ptr(), ntok, 3, 0, L, 0)]), 1)
+        import torch
+        ntoks = [64, 64, 9]
+        out = torch.zeros(3, dtype=torch.int64, device="cuda:0")
+        dn = dev_i32(ntoks)
+        for layer in range(L):
+            abi.check(abi.lib().dp_pool_checksum(pool.ptr, layer, ctypes.c_void_p(ds.data_ptr()),
+                                                 ctypes.c_void_p(dn.data_ptr()), 3,
+                                                 ctypes.c_void_p(out.data_ptr()), None))
+            sync()
+            got = [int(v) & refpy.MASK for v in out.cpu().tolist()]
+            want = [refpy.layer_block_hash(refpy.geom(L, T, b), SEED, f, layer, n)
+                    for f, n in zip(fbs, ntoks)]
+            assert got == want
+    finally:
+        pool.close()
+        st.close()
+
+
+def test_wait_layer_watchdog(gpus):
+    g = abi.geom(2, 64, 576)
+    pool = abi.Pool(0, g, 2, 2)
+    try:
+        abi.wait_layer(pool, 0, 0, 0, timeout_ms=1000)  # already satisfied
+        sync()
+        assert abi.wait_status(pool) == abi.DP_OK
+        abi.wait_layer(pool, 1, 2, 1, timeout_ms=50)  # never released -> watchdog
+        sync()
+        assert abi.wait_status(pool) == abi.DP_ETIMEOUT
+        pool.reset_counters()
+        sync()
+        assert abi.wait_status(pool) == abi.DP_OK
+    finally:
+        pool.close()
+
+
+def test_abi_rejects_bad_arguments(gpus):
+    with pytest.raises(abi.DualPathError) as e:
+        abi.Store(0, abi.geom(2, 64, 100), 1, SEED)  # b not a multiple of 16
+    assert e.value.code == abi.DP_EINVAL
+    g = abi.geom(2, 64, 576)
+    st = abi.Store(0, g, 2, SEED)
+    pool = abi.Pool(0, g, 4, 1)
+    try:
+        df, ds = dev_i64([0, 1]), dev_i32([0, 1])
+        bad = abi.make_jobs([(df.data_ptr(), ds.data_ptr(), 64 * 3, 2, 0, 2, 0)])  # n_blk != ceil
+        with pytest.raises(abi.DualPathError):
+            abi.h2d_layer_gather(pool, st, bad, 1)
+        ok = abi.make_jobs([(df.data_ptr(), ds.data_ptr(), 100, 2, 0, 2, 0)])
+        with pytest.raises(abi.DualPathError):  # K2 needs a peer view, not the local pool
+            abi.h2d_push_p2p_layer(pool, st, ok, 1)
+        with pytest.raises(abi.DualPathError):
+            abi.wait_layer(pool, 5, 0, 1)  # ticket out of range
+    finally:
+        pool.close()
+        st.close()
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("L,T,b", [(61, 64, 576), (4, 64, 4096)])
+def test_k2_push_p2p_parity(two_gpus, L, T, b):
+    """DE (device 1) reads its own host store and stores into the PE pool on
+    device 0 over NVLink; the PE's counters see the system-scope release."""
+    rng = np.random.default_rng(11)
+    g = abi.geom(L, T, b)
+    st_de = abi.Store(1, g, 10, SEED)
+    pool = abi.Pool(0, g, 48, 40)
+    view = pool.peer_view(1)
+    try:
+        specs, keep, plain = random_jobs(rng, L, T, 36, 10, 48, 3, device=1)
+        abi.h2d_push_p2p_layer(view, st_de, abi.make_jobs(specs), len(specs))
+        for t, (fbs, slots, ntok, l0, l1) in enumerate(plain):
+            abi.wait_layer(pool, t, L, abi.layer_items(g, len(slots)) * (l1 - l0), timeout_ms=10000)
+        sync()
+        import torch
+        torch.cuda.synchronize(1)
+        assert abi.wait_status(pool) == abi.DP_OK
+        store_img = np.frombuffer(st_de.bytes(), dtype=np.uint8).copy()
+        check_pool(pool, refpy.geom(L, T, b), plain, T, b, store_img, 48)
+    finally:
+        view.close()
+        pool.close()
+        st_de.close()

@@ -1,0 +1,77 @@
+#!/usr/bin/env python
+"""Profiling driver: one K1 (and, with --k2 and 2 GPUs, one K2) launch of a
+realistic size through the C ABI, timed with CUDA events on the launching
+stream.  Used plain and under ncu (profiles/)."""
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2602_21548_b200 import abi  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--k2", action="store_true")
+    ap.add_argument("--jobs", type=int, default=64)
+    ap.add_argument("--blocks", type=int, default=128)  # 8K-token requests
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--shape", default="dsv3", choices=["dsv3", "qwen"])
+    a = ap.parse_args()
+    L, T, b = (61, 64, 576) if a.shape == "dsv3" else (64, 64, 4096)
+    g = abi.geom(L, T, b)
+    n_fb = 2048 if a.shape == "dsv3" else 256
+    n_slots = a.jobs * a.blocks
+    if a.shape == "qwen":
+        n_slots = min(n_slots, 4096)
+    out = {}
+    for kind in (["k1"] + (["k2"] if a.k2 else [])):
+        src_dev = 1 if kind == "k2" else 0
+        st = abi.Store(src_dev, g, n_fb, 9)
+        pool = abi.Pool(0, g, n_slots, a.jobs)
+        dst = pool.peer_view(1) if kind == "k2" else pool
+        rng = np.random.default_rng(0)
+        keep, specs = [], []
+        perm = rng.permutation(n_slots)
+        for j in range(a.jobs):
+            fbs = torch.tensor(rng.integers(0, n_fb, a.blocks), dtype=torch.int64, device=f"cuda:{src_dev}")
+            sl = torch.tensor(perm[(j * a.blocks) % n_slots:][:a.blocks].astype(np.int32), device=f"cuda:{src_dev}")
+            keep += [fbs, sl]
+            specs.append((fbs.data_ptr(), sl.data_ptr(), a.blocks * T, a.blocks, 0, L, j))
+        jobs = abi.make_jobs(specs)
+        nbytes = a.jobs * a.blocks * T * b * L
+        s = torch.cuda.Stream(device=src_dev)
+        times = []
+        for r in range(a.reps + 1):
+            pool.reset_counters()
+            torch.cuda.synchronize(0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.device(src_dev):
+                e0.record(s)
+                if kind == "k1":
+                    abi.h2d_layer_gather(dst, st, jobs, len(specs), s.cuda_stream)
+                else:
+                    abi.h2d_push_p2p_layer(dst, st, jobs, len(specs), s.cuda_stream)
+                e1.record(s)
+            e1.synchronize()
+            if r:
+                times.append(e0.elapsed_time(e1))
+        ms = sorted(times)[len(times) // 2]
+        out[kind] = {"bytes": nbytes, "ms": ms, "GBps": nbytes / ms / 1e6}
+        if dst is not pool:
+            dst.close()
+        pool.close()
+        st.close()
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
