@@ -418,7 +418,7 @@ def main():
             cpu = cpu_baseline(head["xp"], shape)
         except Exception as exc:  # reported, never fatal to the GPU number
             cpu = {"error": str(exc)[:200]}
-    clk = clocks.summary(set(range(8)))
+    clk = clocks.summary(set(range(n)))
     if dist.rank == 0:
         # roofline of the dominant kernel (K1 on the PE): its bytes over its
         # device time in the timed steps (K1 is the only non-trivial kernel
