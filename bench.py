@@ -18,7 +18,6 @@ Inputs are larger than L2 (hundreds of GB per step), so no flush is needed.
 """
 
 import argparse
-import hashlib
 import json
 import os
 import statistics
@@ -146,38 +145,12 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ distributed
-class Dist:
-    def __init__(self, n):
-        self.world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.torch = None
-        if self.world > 1:
-            import torch
-            import torch.distributed as td
-            torch.cuda.set_device(self.local)
-            td.init_process_group("nccl", device_id=torch.device(f"cuda:{self.local}"))
-            self.torch, self.td = torch, td
-        if self.world != n and n > 1:
-            raise SystemExit(f"--gpus {n} needs torchrun with {n} ranks (WORLD_SIZE={self.world})")
-
-    def barrier(self):
-        if self.world > 1:
-            self.td.barrier()
-
-    def allgather(self, obj):
-        if self.world == 1:
-            return [obj]
-        out = [None] * self.world
-        self.td.all_gather_object(out, obj)
-        return out
-
-    def max(self, x):
-        return max(self.allgather(x))
-
-    def close(self):
-        if self.world > 1:
-            self.td.destroy_process_group()
+def make_group(n):
+    from paper_2602_21548_b200 import dist as dpdist
+    g = dpdist.Group("nccl")
+    if g.world != n and n > 1:
+        raise SystemExit(f"--gpus {n} needs torchrun with {n} ranks (WORLD_SIZE={g.world})")
+    return g
 
 
 # --------------------------------------------------------------- measuring
@@ -215,8 +188,8 @@ def run_policy(args, dist, policy, trajs, shape, P, D, devices_used, clocks=None
     opt.storage_cap_Bps = cap
     opt.seed = 9
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
-    digest = hashlib.sha1(repr([(d[1], d[2], d[3], d[4]) for d in planned["decisions"]]).encode()).hexdigest()
-    digests = dist.allgather(digest)
+    from paper_2602_21548_b200 import dist as dpdist
+    digests = dist.allgather(dpdist.plan_digest(planned))
     assert len(set(digests)) == 1, "ranks planned differently"
     if dist.world > 1:
         my = [dist.rank]
@@ -227,11 +200,7 @@ def run_policy(args, dist, policy, trajs, shape, P, D, devices_used, clocks=None
         dev = dist.local if dist.world > 1 else 0
         engines[e] = dp.EngineRuntime(xp, e, dev)
     if dist.world > 1:
-        handles = dist.allgather(engines[dist.rank].export_pool() if dist.rank < cfg.prefill_nodes else None)
-        for e, rt in engines.items():
-            if e >= cfg.prefill_nodes:
-                for pe in range(cfg.prefill_nodes):
-                    rt.attach_peer(pe, handles[pe])
+        dpdist.connect_pools(dist, engines, cfg.prefill_nodes)
     dev_ms, host_ms, launches, read_bytes = [], [], 0, 0
     for step in range(args.warmup + args.steps):
         for rt in engines.values():
@@ -388,7 +357,7 @@ def main():
         return
     import paper_2602_21548_b200 as dp  # noqa: F401  (fails loudly without the extension)
     n = args.gpus
-    dist = Dist(n)
+    dist = make_group(n)
     trajs, shape = workload(args, n)
     if args.pd:
         P, D = (int(x) for x in args.pd.split(":"))

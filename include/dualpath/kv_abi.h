@@ -79,7 +79,7 @@ typedef struct dp_pool_handle {
   int32_t n_slots;
   int32_t n_tickets;
   int32_t device;
-  int32_t reserved[5];
+  int32_t reserved[9];
 } dp_pool_handle;
 
 int dp_abi_version(void);

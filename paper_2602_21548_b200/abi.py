@@ -39,7 +39,7 @@ class Job(ctypes.Structure):
 class PoolHandle(ctypes.Structure):
     _fields_ = [("ipc", ctypes.c_ubyte * 64), ("geom", Geom), ("n_slots", ctypes.c_int32),
                 ("n_tickets", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("reserved", ctypes.c_int32 * 9)]
 
 
 _lib = None

@@ -243,7 +243,8 @@ PYBIND11_MODULE(_core, m) {
          double quota, double cb, double cq, double cl, double c0, double dctx, double dstep,
          double sub, double amort, double bucket, bool flows, bool events, double aps,
          std::uint64_t seed, double slo_ttft, double slo_tpot, double steady_window,
-         double steady_lookback, double steady_threshold) {
+         double steady_lookback, double steady_threshold, double burst_period,
+         double burst_bytes, double burst_start, double burst_stop) {
         desim::SimOptions opt = make_options(policy, sched_mode, static_cast<double>(alpha),
                                              static_cast<double>(beta), seed);
         opt.sched.z_factor = z;
@@ -256,6 +257,7 @@ PYBIND11_MODULE(_core, m) {
         opt.bucket_width = bucket;
         opt.record_flows = flows;
         opt.record_events = events;
+        if (burst_period > 0) opt.bursts = desim::BurstSpec{burst_period, burst_bytes, burst_start, burst_stop};
         desim::SimReport rep;
         {
           py::gil_scoped_release nogil;
@@ -284,7 +286,8 @@ PYBIND11_MODULE(_core, m) {
       py::arg("flows") = false, py::arg("events") = false, py::arg("aps") = 0.0,
       py::arg("seed") = 1, py::arg("slo_ttft") = 4.0, py::arg("slo_tpot") = 0.05,
       py::arg("steady_window") = 15.0, py::arg("steady_lookback") = 180.0,
-      py::arg("steady_threshold") = 0.05);
+      py::arg("steady_threshold") = 0.05, py::arg("burst_period") = 0.0,
+      py::arg("burst_bytes") = 1e6, py::arg("burst_start") = 0.0, py::arg("burst_stop") = 1.0);
 
   // Reference-shaped entry (bindings.cpp:169-186) plus the decision log.
   m.def(

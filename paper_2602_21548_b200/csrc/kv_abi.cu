@@ -85,6 +85,8 @@ struct GatherParams {
   dp_job jobs[DP_MAX_JOBS_PER_LAUNCH];
 };
 static_assert(sizeof(GatherParams) <= 4000, "kernel parameter block too large");
+static_assert(sizeof(dp_pool_handle) == 128, "dp_pool_handle is a fixed 128-byte wire format");
+static_assert(sizeof(dp_job) == 40, "dp_job layout");
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 v;

@@ -1,0 +1,61 @@
+"""The C ABI library loads and exports every entry point include/dualpath/kv_abi.h
+declares; argument validation that needs no GPU (CPU only)."""
+
+import ctypes
+
+import pytest
+
+from paper_2602_21548_b200 import abi
+
+
+def test_header_declares_the_path_entry_points():
+    syms = abi.declared_symbols()
+    for need in ("dp_h2d_layer_gather", "dp_h2d_push_p2p_layer", "dp_wait_layer", "dp_store_create",
+                 "dp_pool_create", "dp_pool_export", "dp_pool_import", "dp_pool_checksum",
+                 "dp_last_error"):
+        assert need in syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(abi.LIB_PATH)
+    missing = [s for s in abi.declared_symbols() if not hasattr(lib, s)]
+    assert missing == []
+
+
+def test_abi_version_and_geometry_checks():
+    L = abi.lib()
+    assert L.dp_abi_version() == 1
+    assert L.dp_geom_check(ctypes.byref(abi.geom(61, 64, 576))) == abi.DP_OK
+    assert L.dp_geom_check(ctypes.byref(abi.geom(64, 64, 4096))) == abi.DP_OK
+    for bad in (abi.geom(0, 64, 576), abi.geom(4, 0, 576), abi.geom(4, 64, 100), abi.geom(4, 64, 0)):
+        assert L.dp_geom_check(ctypes.byref(bad)) == abi.DP_EINVAL
+        assert L.dp_last_error()  # thread-local message set
+    assert L.dp_geom_check(None) == abi.DP_EINVAL
+
+
+def test_layer_items():
+    # 64 KiB chunks: one item per DS-V3 Layer Block, four per Qwen Layer Block
+    assert abi.layer_items(abi.geom(61, 64, 576), 10) == 10
+    assert abi.layer_items(abi.geom(64, 64, 4096), 10) == 40
+    with pytest.raises(abi.DualPathError):
+        abi.layer_items(abi.geom(61, 64, 576), -1)
+
+
+def test_null_arguments_fail_cleanly():
+    L = abi.lib()
+    assert L.dp_h2d_layer_gather(None, None, None, 0, None) == abi.DP_EINVAL
+    assert L.dp_h2d_push_p2p_layer(None, None, None, 0, None) == abi.DP_EINVAL
+    assert L.dp_wait_layer(None, 0, 0, 0, 1, None) == abi.DP_EINVAL
+    assert L.dp_pool_checksum(None, 0, None, None, 0, None, None) == abi.DP_EINVAL
+    assert L.dp_store_info(None, None, None, None) == abi.DP_EINVAL
+    assert L.dp_store_destroy(None) == abi.DP_OK
+    assert L.dp_pool_destroy(None) == abi.DP_OK
+    out = ctypes.c_void_p()
+    assert L.dp_pool_create(0, ctypes.byref(abi.geom(4, 64, 100)), 4, 1, ctypes.byref(out)) == abi.DP_EINVAL
+    assert out.value is None
+
+
+def test_pool_handle_layout_is_128_bytes():
+    assert ctypes.sizeof(abi.PoolHandle) == 128
+    assert ctypes.sizeof(abi.Job) == 40
+    assert ctypes.sizeof(abi.Geom) == 16

@@ -1,0 +1,122 @@
+"""Executor plan invariants (CPU): the decisions -> block tables / slots /
+hazards translation that every engine derives identically."""
+
+import pytest
+
+import paper_2602_21548_b200 as dp
+
+SB = dict(cl=1e-12, dctx=1e-15, dstep=1e-9, sub=0.0, beta=1_000_000_000)
+
+
+def cluster(P, D, L=8, b=576, T=64, cap=6.25e9):
+    c = dp.ClusterConfig()
+    c.prefill_nodes, c.decode_nodes, c.engines_per_node = P, D, 1
+    c.n_layer, c.kv_bytes_per_token_per_layer, c.block_size_tokens = L, b, T
+    c.cnic_bandwidth, c.storage_multiple, c.dram_bandwidth = 50e9, cap / 50e9, 500e9
+    c.hbm_capacity_tokens, c.pe_buffer_bytes, c.de_buffer_bytes = 100_000_000, 1 << 42, 1 << 42
+    return c
+
+
+def build(P, D, policy="dual_path", pool_slots=0, count=10, turns=6, seed=8):
+    cfg = cluster(P, D)
+    trajs = dp.synthesize(max_len=20000, count=count, seed=seed, mean_turns=turns, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy=policy, **SB)
+    opt = dp.ExecOptions()
+    opt.pool_slots = pool_slots
+    return cfg, trajs, planned, dp.build_exec_plan(cfg, trajs, planned, opt)
+
+
+def replay(xp, planned):
+    """Re-derive live slots in virtual time and check no two live jobs share one."""
+    reqs = {r[0]: r for r in planned["requests"]}
+    jobs = xp.jobs()
+    evs = []
+    for j in jobs:
+        r = reqs[j[0]]
+        evs.append((r[12], 1, j[0], j))
+        if r[13] >= 0:
+            evs.append((r[13], 0, j[0], j))
+    evs.sort(key=lambda e: (e[0], e[1], e[2]))
+    live = {}
+    for t, kind, req, j in evs:
+        for s in j[9]:
+            key = (j[4], s)
+            if kind == 1:
+                assert key not in live, f"slot {key} double-booked"
+                live[key] = req
+            else:
+                assert live.pop(key) == req
+
+
+@pytest.mark.parametrize("P,D", [(1, 1), (2, 2), (1, 3), (3, 1)])
+def test_decisions_become_jobs(P, D):
+    cfg, trajs, planned, xp = build(P, D)
+    dec = {d[1]: d for d in planned["decisions"]}
+    jobs = xp.jobs()
+    hit = 0
+    for req, traj, rnd, reader, pe, de_path, cached, nblk, ticket, slots, fbs, preds, fence in jobs:
+        d = dec[req]
+        assert pe == d[2] and de_path == (d[4] == 1)
+        assert reader == (d[3] if de_path else d[2])
+        assert cached == dp.context_before(trajs[traj], rnd) > 0
+        assert nblk == dp.blocks_for(cached, cfg) == len(slots) == len(fbs)
+        assert all(0 <= f < xp.store_fb for f in fbs)
+        assert fbs == [xp.fb_of(traj, k) for k in range(nblk)]
+        hit += cached * cfg.kv_bytes_per_token()
+    assert hit == xp.hit_bytes == sum(xp.reader_bytes)
+    # every request with cached KV has exactly one job
+    want = sorted(r[0] for r in planned["requests"] if r[3] > 0)
+    assert sorted(j[0] for j in jobs) == want
+    # tickets are dense per PE
+    for pe in range(xp.n_pe):
+        t = sorted(j[8] for j in jobs if j[4] == pe)
+        assert t == list(range(len(t))) and len(t) == xp.n_tickets[pe]
+    replay(xp, planned)
+
+
+def test_pe_only_reads_only_on_prefill_engines():
+    cfg, trajs, planned, xp = build(2, 2, policy="pe_only")
+    assert xp.reader_bytes[2] == xp.reader_bytes[3] == 0
+    assert all(not j[5] for j in xp.jobs())
+
+
+def test_tight_pool_records_hazards():
+    _, _, planned, probe = build(1, 1, count=12)
+    _, _, planned, xp = build(1, 1, count=12, pool_slots=probe.peak_slots)
+    jobs = xp.jobs()
+    by_ticket = {j[8]: j for j in jobs}
+    last_writer = {}
+    for j in jobs:  # global (allocation) order
+        preds, fence = set(), False
+        for s in j[9]:
+            if s in last_writer:
+                w = last_writer[s]
+                if w[3] == j[3]:
+                    fence = True
+                else:
+                    preds.add(w[8])
+            last_writer[s] = j
+        assert set(j[11]) == preds and j[12] == fence
+        for t in j[11]:
+            assert by_ticket[t][3] != j[3]
+    assert any(j[11] for j in jobs) and any(j[12] for j in jobs)
+    replay(xp, planned)
+
+
+def test_pool_below_peak_is_rejected():
+    _, _, planned, probe = build(1, 1)
+    with pytest.raises(ValueError, match="peak"):
+        build(1, 1, pool_slots=max(1, probe.peak_slots - 1))
+
+
+def test_store_mapping_and_size_cap():
+    cfg = cluster(1, 1)
+    trajs = dp.synthesize(max_len=20000, count=6, seed=1, mean_turns=4, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, **SB)
+    opt = dp.ExecOptions()
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert xp.store_fb == xp.fb_stride * len(trajs)  # no aliasing when it fits
+    opt.store_bytes_max = 3 * cfg.full_block_bytes()
+    xp2 = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert xp2.store_fb == 3
+    assert all(0 <= f < 3 for j in xp2.jobs() for f in j[10])

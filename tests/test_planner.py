@@ -1,0 +1,217 @@
+"""Planner parity (CPU): the product's plan-mode engine vs the reference
+simulator, bit for bit.
+
+Live comparisons run the compiled reference (oracle/_ref); the committed
+fixtures tests/golden/decisions_*.json (tests/golden/make_golden.py) pin the
+same answers without it.  Acceptance criteria C3, C4, C9 of
+/root/reference/proj/tests/acceptance.cpp are restated against the product."""
+
+import json
+import os
+import random
+
+import pytest
+
+import paper_2602_21548_b200 as dp
+from oracle import refpy
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+needs_ref = pytest.mark.skipif(not refpy.ref_available(), reason="oracle/_ref not built")
+
+STAGES = ["storage_read", "loopback_h2d", "pe_to_de", "de_to_pe", "miss_merge", "decode_h2d",
+          "layer_compute", "decode", "persist_d2h", "persist_write", "burst"]
+
+# ref_shim key -> dp.plan keyword (cluster keys handled separately)
+PLAN_KEYS = {"policy", "sched_mode", "alpha", "beta", "z", "quota", "cb", "cq", "cl", "c0", "dctx",
+             "dstep", "sub", "amort", "bucket", "aps", "seed", "slo_ttft", "slo_tpot",
+             "steady_window", "steady_lookback", "steady_threshold", "burst_period", "burst_bytes",
+             "burst_start", "burst_stop"}
+
+
+def make_cluster(P=1, D=1, g=2, L=4, b=1024, T=64, B=50e9, s=1.0, M=500e9, hbm=4_000_000,
+                 pe_buf=1 << 34, de_buf=1 << 34, **_):
+    c = dp.ClusterConfig()
+    c.prefill_nodes, c.decode_nodes, c.engines_per_node = P, D, g
+    c.n_layer, c.kv_bytes_per_token_per_layer, c.block_size_tokens = L, b, T
+    c.cnic_bandwidth, c.storage_multiple, c.dram_bandwidth = B, s, M
+    c.hbm_capacity_tokens, c.pe_buffer_bytes, c.de_buffer_bytes = hbm, pe_buf, de_buf
+    return c
+
+
+def run_mine(trajs, **kv):
+    cfg = make_cluster(**kv)
+    kw = {k: v for k, v in kv.items() if k in PLAN_KEYS}
+    return dp.plan(cfg, trajs, flows=True, events=True, **kw)
+
+
+def compare(trace_path, **kv):
+    trajs = dp.load_trace(trace_path)
+    mine = run_mine(trajs, **kv)
+    ref = refpy.ref_simulate(trace_path, flows=1, events=1, **kv)
+    assert [list(d) for d in mine["decisions"]] == ref["decisions"]
+    assert [list(f) for f in mine["flows"]] == ref["flows"]
+    assert mine["makespan"] == ref["makespan"]
+    assert mine["duration"] == ref["duration"]
+    assert mine["completed_requests"] == ref["completed_requests"]
+    assert [u["total_bytes"] for u in mine["usage"]] == [u[4] for u in ref["usage"]]
+    assert [u["buckets"] for u in mine["usage"]] == [u[5] for u in ref["usage"]]
+    assert [json.loads(e) for e in mine["event_log"]] == ref["event_log"]
+    lat = [[r["request_id"], r["ttft"], r["ttst"], r["tpot"], r["sched_component"],
+            r["alloc_component"], r["read_component"], r["prefill_component"]]
+           for r in mine["latencies"]]
+    assert lat == ref["latencies"]
+    assert [list(x) for x in mine["trajectory_jct"]] == ref["trajectory_jct"]
+    assert mine["burst_latencies"] == ref["burst_latencies"]
+    assert mine["slo_violated"] == ref["slo_violated"]
+    assert mine["steady_state"] == ref["steady_state"]
+    return mine, ref
+
+
+QUICK = dict(cl=1e-6, dctx=1e-10, dstep=1e-4)  # test_desim.cpp:29-36
+STORAGE_BOUND = dict(cl=1e-12, dctx=1e-15, dstep=1e-9, alpha=100_000, beta=1_000_000_000, sub=0)
+
+
+@pytest.fixture(scope="module")
+def small_trace(tmp_path_factory):
+    p = str(tmp_path_factory.mktemp("tr") / "small.tsv")
+    dp.save_trace(p, dp.synthesize(max_len=4096, count=24, seed=7))
+    return p
+
+
+@needs_ref
+@pytest.mark.parametrize("kv", [
+    dict(P=2, D=2, g=2, **QUICK),
+    dict(P=1, D=1, g=2, policy="pe_only", **QUICK),
+    dict(P=1, D=1, g=2, policy="oracle", **QUICK),
+    dict(P=1, D=1, g=3, sched_mode="round_robin", **QUICK),
+    dict(P=1, D=2, g=4, B=25e9, s=0.2, **STORAGE_BOUND),
+    dict(P=2, D=1, g=1, L=61, b=576, s=0.125, M=500e9, **STORAGE_BOUND),
+    dict(P=1, D=1, g=2, amort=4.0, sub=2e-6, cl=1e-6, dstep=1e-4, z=1.3, alpha=5000, beta=20000),
+    dict(P=1, D=1, g=2, pe_buf=17 << 20, de_buf=18 << 20, **QUICK),  # admission stalls
+])
+def test_offline_bit_exact(small_trace, kv):
+    compare(small_trace, **kv)
+
+
+@needs_ref
+@pytest.mark.parametrize("policy", ["dual_path", "pe_only"])
+def test_bursts_bit_exact(small_trace, policy):
+    # synthetic high-priority collective bursts on every CNIC read (two-class
+    # WRR with the 1% low floor, desim.cpp:95-135, :936-940)
+    _, ref = compare(small_trace, P=1, D=1, g=2, policy=policy, burst_period=1e-3,
+                     burst_bytes=2e6, burst_start=0.0, burst_stop=0.2, **QUICK)
+    assert ref["burst_latencies"]
+
+
+@needs_ref
+@pytest.mark.parametrize("aps", [0.5, 20.0])
+def test_online_bit_exact(tmp_path, aps):
+    # Poisson arrivals + SLO / steady-state control (desim.cpp:1036-1051, :942-953)
+    p = str(tmp_path / "on.tsv")
+    dp.save_trace(p, dp.synthesize(max_len=8192, count=40, seed=11))
+    compare(p, P=1, D=1, g=2, aps=aps, seed=3, slo_ttft=0.5, steady_window=0.2,
+            steady_lookback=0.5, **QUICK)
+
+
+@needs_ref
+def test_config_errors_match_reference(tmp_path):
+    # test_desim.cpp:273-282 and validate_workload (desim.cpp:327-352)
+    p = str(tmp_path / "e.tsv")
+    t = dp.Trajectory()
+    t.id = "t"
+    t.rounds = [dp.Round(500, 10)]
+    dp.save_trace(p, [t])
+    for kv in (dict(hbm=100), dict(de_buf=1024)):
+        with pytest.raises(dp.ConfigError):
+            run_mine([t], P=1, D=1, g=2, **QUICK, **kv)
+        with pytest.raises(refpy.RefError, match="ConfigError"):
+            refpy.ref_simulate(p, P=1, D=1, g=2, **QUICK, **kv)
+
+
+@pytest.mark.parametrize("name", ["tiny_2p2d", "dsv3_1p1d", "qwen_4p4d_rr"])
+def test_golden_decisions_fixture(tmp_path, name):
+    fx = json.load(open(os.path.join(GOLDEN, f"decisions_{name}.json")))
+    trajs = dp.synthesize(**fx["synthesize"])
+    mine = run_mine(trajs, **fx["simulate"])
+    assert [list(d) for d in mine["decisions"]] == fx["decisions"]
+    assert mine["makespan"] == fx["makespan"]
+    ledger = {}
+    for req, stage, nbytes, t0, t1 in mine["flows"]:
+        ledger[STAGES[stage]] = ledger.get(STAGES[stage], 0.0) + nbytes
+    assert ledger == fx["ledger"]
+
+
+def test_byte_conservation_1000_requests():
+    # acceptance.cpp:211-256 (C3), exact equality of the per-stage ledger
+    rng = random.Random(2024)
+    trajs, n = [], 0
+    mt = dp  # noqa
+    while n < 1000:
+        t = dp.Trajectory()
+        t.id = f"r{len(trajs)}"
+        rounds = 1 + rng.randrange(5)
+        t.rounds = [dp.Round(rng.randrange(2000), 1 + rng.randrange(400)) for _ in range(rounds)]
+        n += rounds
+        trajs.append(t)
+    kv = dict(P=1, D=1, g=2, L=4, b=4096, T=256, B=50e9, s=1.0, M=500e9, hbm=100_000_000,
+              pe_buf=1 << 42, de_buf=1 << 42, **STORAGE_BOUND)
+    rep = run_mine(trajs, **kv)
+    f = 4 * 4096.0
+    want_read = want_prompt = want_persist = 0.0
+    for t in trajs:
+        c = 0
+        for r in t.rounds:
+            want_read += c * f
+            want_prompt += (c + r.append_tokens) * f
+            want_persist += r.gen_tokens * f
+            c += r.append_tokens + r.gen_tokens
+    got = {}
+    for req, stage, nbytes, t0, t1 in rep["flows"]:
+        got[STAGES[stage]] = got.get(STAGES[stage], 0.0) + nbytes
+    assert rep["completed_requests"] == rep["total_requests"]
+    assert got["storage_read"] == want_read
+    assert got["loopback_h2d"] + got["de_to_pe"] == want_read
+    assert got["pe_to_de"] + got["miss_merge"] + got["de_to_pe"] == want_prompt
+    assert got["decode_h2d"] == want_prompt
+    assert got["persist_write"] == want_persist == got["persist_d2h"]
+
+
+def saturating(P, D, g):
+    trajs = []
+    for i in range(2 * (P + D) * g):
+        t = dp.Trajectory()
+        t.id = f"s{i}"
+        t.rounds = [dp.Round(30_000, 1)] + [dp.Round(0, 1) for _ in range(4)]
+        trajs.append(t)
+    return trajs
+
+
+def test_dual_path_pooling_ratio():
+    # acceptance.cpp:258-272 (C4): JCT(dual)/JCT(PE-only) in [0.45, 0.55]
+    # at 1P1D and [0.30, 0.40] at 1P2D (storage-bound)
+    def makespan(P, D, policy):
+        kv = dict(P=P, D=D, g=4, L=4, b=4096, T=256, B=50e9, s=1.0, M=500e9,
+                  hbm=100_000_000, pe_buf=1 << 42, de_buf=1 << 42, policy=policy, **STORAGE_BOUND)
+        return run_mine(saturating(P, D, 4), **kv)["makespan"]
+    r11 = makespan(1, 1, "dual_path") / makespan(1, 1, "pe_only")
+    r12 = makespan(1, 2, "dual_path") / makespan(1, 2, "pe_only")
+    assert 0.45 <= r11 <= 0.55
+    assert 0.30 <= r12 <= 0.40
+
+
+def test_replay_is_bit_identical():
+    # acceptance.cpp:517-549 (C9)
+    trajs = dp.synthesize(max_len=16384, count=24, seed=123)
+    for policy in ("dual_path", "pe_only"):
+        kv = dict(P=2, D=2, g=2, L=4, b=4096, T=256, policy=policy, cl=1e-7, dctx=1e-11, dstep=1e-4)
+        a, b = run_mine(trajs, **kv), run_mine(trajs, **kv)
+        assert a["event_log"] == b["event_log"]
+        assert a["flows"] == b["flows"] and a["decisions"] == b["decisions"]
+        assert a["makespan"] == b["makespan"]
+
+
+def test_offline_decisions_do_not_depend_on_seed():
+    trajs = dp.synthesize(max_len=8192, count=8, seed=2)
+    a = run_mine(trajs, P=1, D=1, g=2, seed=1, **QUICK)
+    b = run_mine(trajs, P=1, D=1, g=2, seed=77, **QUICK)
+    assert a["decisions"] == b["decisions"]
