@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-one-path", action="store_true", help="skip the prefill-only comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pd", default="", help="override P:D, e.g. 2:6")
+    ap.add_argument("--online", type=float, default=0.0,
+                    help="config 5: Poisson arrivals at this many sessions/s, replayed in real time")
+    ap.add_argument("--caps", default="", help="config 5: per-engine storage caps, GB/s, comma list")
     return ap.parse_args()
 
 
@@ -55,8 +58,10 @@ def parse():
 def workload(args, n_gpus):
     """Trajectories + KV shape.  c1: BASELINE config 1 generator (20 turns,
     mean append 429, mean gen 500, ~95% hit); c2: 32K/64K/128K contexts built
-    by a cheap generation round, then warm {429, 1} rounds (config 2); c3: c1
-    with the Qwen2.5-32B KV shape (config 3)."""
+    by one cold prefill round {C, 1}, then warm {429, 1} rounds (config 2; a
+    cold append instead of the reference tests' long generation round, whose
+    64-token persistence flows would dominate planning); c3: c1 with the
+    Qwen2.5-32B KV shape (config 3)."""
     import paper_2602_21548_b200 as dp
     sessions = max(1, args.sessions_per_gpu * max(1, n_gpus))
     if args.workload in ("c1", "c3"):
@@ -69,15 +74,17 @@ def workload(args, n_gpus):
             t = dp.Trajectory()
             t.id = f"ctx{i}"
             c = (32768, 65536, 131072)[i % 3]
-            t.rounds = [dp.Round(16, c - 16)] + [dp.Round(429, 1) for _ in range(3)]
+            t.rounds = [dp.Round(c - 1, 1)] + [dp.Round(429, 1) for _ in range(3)]
             trajs.append(t)
         shape = DSV3
     return trajs, shape
 
 
-def cluster(shape, P, D, cap_bps):
+def cluster(shape, P, D, cap_bps, caps=None):
     import paper_2602_21548_b200 as dp
     cfg = dp.ClusterConfig()
+    if caps:
+        cfg.storage_bandwidth_per_node = list(caps)  # g = 1: one node per engine
     cfg.prefill_nodes, cfg.decode_nodes, cfg.engines_per_node = P, D, 1
     cfg.n_layer, cfg.kv_bytes_per_token_per_layer, cfg.block_size_tokens = shape["L"], shape["b"], shape["T"]
     # compute network = NVLink (the DE->PE push), storage NIC = the engine's
@@ -175,17 +182,29 @@ def measure_pcie_peak(device):
     return n / (best * 1e-3)
 
 
-def run_policy(args, dist, policy, trajs, shape, P, D, devices_used, clocks=None):
+def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
     """Plan, build engines, run W + K steps; returns per-step max-over-ranks
-    device and host times, plus per-rank info."""
+    device and host times, plus per-rank info.  variant = (policy, sched_mode)."""
     import paper_2602_21548_b200 as dp
+    policy, sched_mode = variant
     cap = args.cap_gbps * 1e9
-    cfg = cluster(shape, P, D, cap)
+    caps = [float(x) * 1e9 for x in args.caps.split(",")] if args.caps else None
+    if caps and len(caps) != P + D:
+        raise SystemExit(f"--caps needs {P + D} entries")
+    cfg = cluster(shape, P, D, cap, caps)
+    kw = dict(PLAN_KW)
+    if args.online > 0:
+        # Poisson arrivals (desim.cpp:1036-1051); SLO / steady-state stops off
+        kw.update(aps=args.online, seed=1, slo_ttft=1e9, steady_lookback=1e9)
     t0 = time.time()
-    planned = dp.plan(cfg, trajs, policy=policy, **PLAN_KW)
+    planned = dp.plan(cfg, trajs, policy=policy, sched_mode=sched_mode, **kw)
     plan_s = time.time() - t0
     opt = dp.ExecOptions()
     opt.storage_cap_Bps = cap
+    if caps:
+        opt.storage_cap_per_engine = caps
+    if args.online > 0:
+        opt.pace_scale = 1.0
     opt.seed = 9
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     from paper_2602_21548_b200 import dist as dpdist
@@ -201,7 +220,7 @@ def run_policy(args, dist, policy, trajs, shape, P, D, devices_used, clocks=None
         engines[e] = dp.EngineRuntime(xp, e, dev)
     if dist.world > 1:
         dpdist.connect_pools(dist, engines, cfg.prefill_nodes)
-    dev_ms, host_ms, launches, read_bytes = [], [], 0, 0
+    dev_ms, host_ms, launches, read_bytes, spans = [], [], 0, 0, None
     for step in range(args.warmup + args.steps):
         for rt in engines.values():
             rt.reset_counters()
@@ -216,10 +235,16 @@ def run_policy(args, dist, policy, trajs, shape, P, D, devices_used, clocks=None
             host_ms.append(h)
             launches += sum(dist.allgather(sum(r.launches for r in res)))
             read_bytes += sum(dist.allgather(sum(r.bytes_read for r in res)))
+            spans = {}
+            for part in dist.allgather({e: r.spans for e, r in zip(engines, res)}):
+                spans.update(part)
+    snic = sum(u["total_bytes"] for u in planned["usage"] if u["kind"] == "snic_read")
     info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens,
+                model_gbps=snic / planned["makespan"] / 1e9 if planned["makespan"] > 0 else None,
                 requests=xp.requests, reader_bytes=list(xp.reader_bytes),
                 de_path=sum(1 for d in planned["decisions"] if d[4] == 1),
-                decisions=len(planned["decisions"]), pool_slots=xp.pool_slots,
+                decisions=len(planned["decisions"]), pool_slots=xp.pool_slots, spans=spans,
+                caps=caps,
                 store_fb=xp.store_fb, launches=launches, read_bytes=read_bytes)
     if clocks is not None:
         clocks.__exit__()
@@ -281,69 +306,88 @@ def cpu_baseline(xp, shape, seconds=12.0):
 
 # ---------------------------------------------------------------- reference
 def reference_arm(args):
-    """The reference's own CPU implementation of the path (pdsim desim,
-    compiled from /root/reference sources into oracle/_ref) on this box's
-    host cores: independent simulations of session shards run concurrently
-    (the reference's sweep parallelism); metric = hit KV bytes the reference
-    path processes per wall second."""
-    from concurrent.futures import ThreadPoolExecutor
+    """The reference's own CPU implementation of the path: pdsim's
+    desim::run_offline, compiled from /root/reference sources into
+    oracle/_ref, run on this box's host (single-threaded by design,
+    SPEC.md:403) on a session sample of the same workload and P:D config.
+    The reference moves no bytes; its value of the metric is its own
+    aggregate KV-load GB/s for the workload: storage-read bytes / makespan
+    (the SnicRead ledger, desim.cpp:405-425, 956-987).  Wall time per run is
+    reported beside it."""
     import paper_2602_21548_b200 as dp
     from oracle import refpy
     n = args.gpus
     trajs, shape = workload(args, n)
     P, D = (1, 1) if n == 1 else (n // 2, n - n // 2)
+    if args.pd:
+        P, D = (int(x) for x in args.pd.split(":"))
     cap = args.cap_gbps * 1e9
     cfg = cluster(shape, P, D, cap)
-    threads = os.cpu_count() or 1
-    # bounded sample: 4 sessions per shard (about 10-30 s of CPU per step)
-    shard = 4
-    shards = [trajs[i:i + shard] for i in range(0, len(trajs), shard)][:threads]
-    paths = []
-    for i, sh in enumerate(shards):
-        p = f"/tmp/dp_ref_shard_{os.getpid()}_{i}.tsv"
-        dp.save_trace(p, sh)
-        paths.append(p)
+    sample = trajs[: max(2, min(len(trajs), 4 * n))]
+    path = f"/tmp/dp_ref_sample_{os.getpid()}.tsv"
+    dp.save_trace(path, sample)
     kv = dict(P=P, D=D, g=1, L=shape["L"], b=shape["b"], T=shape["T"], B=cfg.cnic_bandwidth,
               s=cfg.storage_multiple, M=cfg.dram_bandwidth, hbm=cfg.hbm_capacity_tokens,
               pe_buf=cfg.pe_buffer_bytes, de_buf=cfg.de_buffer_bytes,
               policy="pe_only" if n == 1 else "dual_path", **PLAN_KW)
-    per_tok = shape["L"] * shape["b"]
-    hit = 0
-    for sh in shards:
-        for t in sh:
-            c = 0
-            for r in t.rounds:
-                hit += c * per_tok
-                c += r.append_tokens + r.gen_tokens
-    vals = []
-    sim_agg = []
-
-    def one(p):
-        return refpy.ref_simulate(p, **kv)
-
-    with ThreadPoolExecutor(max_workers=len(paths)) as ex:
+    vals, walls = [], []
+    try:
         for step in range(args.warmup + args.steps):
             t0 = time.time()
-            reps = list(ex.map(one, paths))
-            dt = time.time() - t0
+            rep = refpy.ref_simulate(path, **kv)
+            wall = time.time() - t0
+            snic = sum(u[4] for u in rep["usage"] if u[0] == "snic_read")
             if step >= args.warmup:
-                vals.append(hit / dt / 1e9)
-                sim_agg.append(sum(sum(u[4] for u in r["usage"] if u[0] == "snic_read") for r in reps)
-                               / max(r["makespan"] for r in reps) / 1e9)
-    for p in paths:
-        os.unlink(p)
+                vals.append(snic / rep["makespan"] / 1e9)
+                walls.append(wall)
+    finally:
+        os.unlink(path)
     v = statistics.median(vals)
     return {"metric": "aggregate KV-load GB/s", "value": round(v, 3), "unit": "GB/s", "n_gpus": n,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "impl": "reference",
             "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{args.workload} {'1P-only loader' if n == 1 else f'{P}P{D}D dual_path'}",
-                       "kv": shape, "sample_sessions": sum(len(s) for s in shards)},
-            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": len(paths),
-                             "kind": "reference",
-                             "sample": f"{len(paths)} concurrent desim::run_offline shards x {shard} "
-                                       f"sessions ({hit / 1e9:.1f} GB hit KV simulated per step)"},
+            "config": {"workload": f"{args.workload}: {len(sample)} sessions, "
+                                   + ("1P loader (pe_only)" if n == 1 else f"{P}P{D}D dual_path"),
+                       "kv": shape},
+            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "reference",
+                             "sample": f"desim::run_offline on {len(sample)} sessions of the workload "
+                                       f"(the reference simulator, 1 thread); value = its storage-read "
+                                       f"bytes / makespan; {statistics.median(walls):.2f} s wall per run"},
             "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "reference_simulated_aggkv_gbps": round(statistics.median(sim_agg), 3)}
+            "reference_wall_s_per_run": round(statistics.median(walls), 3)}
+
+
+def storage_balance(spans, caps, n_engines, width=0.05, window=4):
+    """Windowed max/avg of per-engine storage-read traffic (the paper's SNIC
+    balance metric, load_balance_ratio proj/src/metrics.cpp:9-42) from the
+    executor's measured storage spans; with caps, also per-NIC utilisation."""
+    import paper_2602_21548_b200 as dp
+    if not spans or not any(spans.values()):
+        return None
+    end = max(t1 for ss in spans.values() for _, t1, _ in ss)
+    nb = int(end / width) + 1
+
+    def series(norm):
+        out = []
+        for e in range(n_engines):
+            b = [0.0] * nb
+            for t0, t1, nbytes in spans.get(e, []):
+                rate = nbytes / max(t1 - t0, 1e-12) / (norm[e] if norm else 1.0)
+                k0, k1 = int(t0 / width), int(t1 / width)
+                for k in range(k0, min(k1, nb - 1) + 1):
+                    lo, hi = max(t0, k * width), min(t1, (k + 1) * width)
+                    if hi > lo:
+                        b[k] += rate * (hi - lo)
+            out.append(b)
+        return out
+
+    def mean_ratio(ser):
+        pts = [m for _, m, ok in dp.load_balance_ratio(ser, width, window) if ok]
+        return round(sum(pts) / len(pts), 4) if pts else None
+    res = {"bytes_max_avg": mean_ratio(series(None)), "bucket_s": width, "window": window}
+    if caps:
+        res["utilisation_max_avg"] = mean_ratio(series(caps))
+    return res
 
 
 # --------------------------------------------------------------------- main
@@ -363,16 +407,22 @@ def main():
         P, D = (int(x) for x in args.pd.split(":"))
     else:
         P, D = (1, 1) if n == 1 else (n // 2, n - n // 2)
-    policies = ["pe_only"] if n == 1 else ["dual_path"] + ([] if args.no_one_path else ["pe_only"])
+    if args.online > 0:
+        variants = [("dual_path", "adaptive"), ("dual_path", "round_robin")]
+    elif n == 1:
+        variants = [("pe_only", "adaptive")]
+    else:
+        variants = [("dual_path", "adaptive")] + ([] if args.no_one_path else [("pe_only", "adaptive")])
+    policies = [v[0] if v[1] == "adaptive" else v[1] for v in variants]
     peak = None
     if dist.rank == 0:
         peak = measure_pcie_peak(dist.local if dist.world > 1 else 0)
     results = {}
     clocks = ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
                           if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_{os.getpid()}.csv")
-    for pol in policies:
-        results[pol] = run_policy(args, dist, pol, trajs, shape, P, D, n,
-                                  clocks if (pol == policies[0] and dist.local == 0) else None)
+    for name, var in zip(policies, variants):
+        results[name] = run_policy(args, dist, var, trajs, shape, P, D,
+                                   clocks if (name == policies[0] and dist.local == 0) else None)
     head = results[policies[0]]
     info = head["info"]
     dev_s = sum(head["dev_ms"]) / 1e3
@@ -412,7 +462,10 @@ def main():
                                    + ("1 PE loader (K1)" if n == 1 else f"{P}P{D}D dual_path"),
                        "kv": shape, "storage_cap_gbps_per_engine": args.cap_gbps or None,
                        "requests": info["requests"], "hit_bytes_per_step": info["hit_bytes"],
-                       "de_path_requests": info["de_path"], "l2": "inputs >> L2 (no flush needed)"},
+                       "de_path_requests": info["de_path"],
+                       "read_gb_per_engine": [round(x / 1e9, 2) for x in info["reader_bytes"]],
+                       "l2": "inputs >> L2 (no flush needed)"},
+            "model_prediction_gbps": round(info["model_gbps"], 3) if info["model_gbps"] else None,
             "tokens_per_s": round(tokens_s, 1),
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": info["hit_bytes"],
@@ -427,6 +480,17 @@ def main():
             "clocks": clk,
             "plan_s": round(info["plan_s"], 2),
         }
+        if args.online > 0:
+            out["config"]["online_sessions_per_s"] = args.online
+            out["config"]["caps_gbps"] = [float(x) for x in args.caps.split(",")] if args.caps else None
+            out["balance"] = {"adaptive": storage_balance(info["spans"], info["caps"], P + D)}
+            if "round_robin" in results:
+                rr = results["round_robin"]
+                rr_s = sum(rr["dev_ms"]) / 1e3
+                rr_v = rr["info"]["hit_bytes"] * K / rr_s / 1e9
+                out["round_robin"] = {"value": round(rr_v, 3), "unit": "GB/s",
+                                      "adaptive_vs_rr": round(value / rr_v, 3)}
+                out["balance"]["round_robin"] = storage_balance(rr["info"]["spans"], rr["info"]["caps"], P + D)
         if "pe_only" in results and n > 1:
             po = results["pe_only"]
             po_s = sum(po["dev_ms"]) / 1e3

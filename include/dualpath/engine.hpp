@@ -34,6 +34,9 @@ namespace dualpath {
 
 struct ExecOptions {
   double storage_cap_Bps = 0;          // per-engine storage NIC; 0 = uncapped (PCIe binds)
+  std::vector<double> storage_cap_per_engine;  // overrides storage_cap_Bps per engine
+  double pace_scale = 0;               // > 0: online replay, a job's storage read starts no
+                                       // earlier than its planned t_admit * pace_scale
   std::int64_t store_fb = 0;           // Full Blocks per engine store; 0 = auto
   std::int64_t store_bytes_max = 8LL << 30;
   std::uint64_t seed = 9;              // content seed (oracle/kvref.c)
@@ -54,6 +57,8 @@ struct LoadJob {
   std::int32_t n_blk = 0;
   std::int64_t blk_off = 0; // offset of this job's blocks in the reader's tables
   std::int32_t ticket = 0;  // counter row in the PE pool
+  double t_admit = 0;       // plan: StorageRead starts (virtual s)
+  double t_read_done = 0;   // plan: hit transfer starts
   std::vector<std::int32_t> preds;         // tickets in the same PE pool whose slots this
   std::vector<std::uint32_t> pred_targets; // reuses (written by another engine), and their
                                            // all-layer landed-item targets
@@ -92,7 +97,14 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
                          std::span<const pdsim::Trajectory> trajectories,
                          const pdsim::desim::SimReport& plan, const ExecOptions& opt);
 
+struct StorageSpan {
+  double t_begin = 0;  // s since the step started
+  double t_end = 0;
+  std::int64_t bytes = 0;
+};
+
 struct StepResult {
+  std::vector<StorageSpan> spans;  // per job: its emulated storage read (gated runs)
   double device_ms = 0;         // CUDA-event time of this engine's step
   double host_ms = 0;           // wall time of run_step()
   std::int64_t bytes_read = 0;  // hit bytes this engine read from storage

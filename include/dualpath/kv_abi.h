@@ -121,6 +121,11 @@ int dp_h2d_layer_gather(dp_pool* pe, const dp_store* src, const dp_job* jobs, in
 int dp_h2d_push_p2p_layer(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs,
                           int32_t n_jobs, dp_stream de_stream);
 
+/* Cap on the CTAs a K1/K2 launch on `device` may use (0 = default, 4 per SM).
+ * The transfer is PCIe-bound, so a few CTAs keep the link full while leaving
+ * the SMs to the prefill compute (the isolation knob of config 4). */
+int dp_set_gather_ctas(int device, int32_t ctas);
+
 /* Items (landed-counter increments) per layer for a job of n_blk blocks. */
 int dp_layer_items(const dp_kv_geom* geom, int32_t n_blk, int32_t* out);
 

@@ -40,6 +40,7 @@ from ._core import (  # noqa: E402
     blocks_for,
     build_exec_plan,
     context_before,
+    load_balance_ratio,
     load_trace,
     plan,
     run_step_all,
@@ -69,6 +70,7 @@ __all__ = [
     "blocks_for",
     "build_exec_plan",
     "context_before",
+    "load_balance_ratio",
     "load_trace",
     "plan",
     "run_step_all",

@@ -84,6 +84,7 @@ def lib():
         "dp_pool_checksum": ([P, ctypes.c_int32, P, P, ctypes.c_int32, P, P], ctypes.c_int),
         "dp_pool_copy_out": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P], ctypes.c_int),
         "dp_device_count": ([], ctypes.c_int),
+        "dp_set_gather_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -214,6 +215,10 @@ def wait_layer(pool, ticket, layer, target, timeout_ms=10000, stream=0):
 
 def wait_status(pool):
     return lib().dp_wait_status(pool.ptr)
+
+
+def set_gather_ctas(device, ctas):
+    check(lib().dp_set_gather_ctas(device, ctas))
 
 
 def device_count():

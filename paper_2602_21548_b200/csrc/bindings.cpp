@@ -128,6 +128,7 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("hbm_capacity_tokens", &ClusterConfig::hbm_capacity_tokens)
       .def_readwrite("pe_buffer_bytes", &ClusterConfig::pe_buffer_bytes)
       .def_readwrite("de_buffer_bytes", &ClusterConfig::de_buffer_bytes)
+      .def_readwrite("storage_bandwidth_per_node", &ClusterConfig::storage_bandwidth_per_node)
       .def("validate", &ClusterConfig::validate)
       .def("kv_bytes_per_token", &ClusterConfig::kv_bytes_per_token)
       .def("layer_block_bytes", &ClusterConfig::layer_block_bytes)
@@ -312,6 +313,14 @@ PYBIND11_MODULE(_core, m) {
       py::arg("sched_mode") = "adaptive", py::arg("alpha") = 100000, py::arg("beta") = 500000,
       py::arg("aps") = 0.0, py::arg("seed") = 0);
 
+  m.def("load_balance_ratio",
+        [](const std::vector<std::vector<double>>& series, double bucket_width, int window) {
+          std::vector<std::tuple<double, double, bool>> out;
+          for (const auto& p : load_balance_ratio(series, bucket_width, window))
+            out.emplace_back(p.t, p.max_avg, p.defined);
+          return out;
+        });
+
   py::register_exception<desim::ConfigError>(m, "ConfigError");
   py::register_exception<desim::SimulationError>(m, "SimulationError");
 
@@ -319,6 +328,8 @@ PYBIND11_MODULE(_core, m) {
   py::class_<dualpath::ExecOptions>(m, "ExecOptions")
       .def(py::init<>())
       .def_readwrite("storage_cap_Bps", &dualpath::ExecOptions::storage_cap_Bps)
+      .def_readwrite("storage_cap_per_engine", &dualpath::ExecOptions::storage_cap_per_engine)
+      .def_readwrite("pace_scale", &dualpath::ExecOptions::pace_scale)
       .def_readwrite("store_fb", &dualpath::ExecOptions::store_fb)
       .def_readwrite("store_bytes_max", &dualpath::ExecOptions::store_bytes_max)
       .def_readwrite("seed", &dualpath::ExecOptions::seed)
@@ -388,6 +399,12 @@ PYBIND11_MODULE(_core, m) {
       py::arg("cluster"), py::arg("trajectories"), py::arg("planned"), py::arg("options"));
 
   py::class_<dualpath::StepResult>(m, "StepResult")
+      .def_property_readonly("spans",
+                             [](const dualpath::StepResult& r) {
+                               std::vector<std::tuple<double, double, std::int64_t>> v;
+                               for (const auto& s : r.spans) v.emplace_back(s.t_begin, s.t_end, s.bytes);
+                               return v;
+                             })
       .def_readonly("device_ms", &dualpath::StepResult::device_ms)
       .def_readonly("host_ms", &dualpath::StepResult::host_ms)
       .def_readonly("bytes_read", &dualpath::StepResult::bytes_read)

@@ -97,6 +97,8 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     j.reader = j.de_path ? r.de : r.pe;
     j.cached = r.cached;
     j.n_blk = static_cast<std::int32_t>((r.cached + T - 1) / T);
+    j.t_admit = r.t_admit;
+    j.t_read_done = r.t_read_done;
     const int idx = static_cast<int>(jobs.size());
     jobs.push_back(std::move(j));
     evs.push_back({r.t_read_done, 1, r.request_id, idx});
@@ -126,6 +128,9 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     x.pool_slots = static_cast<std::int32_t>(
         std::min<std::int64_t>(slot_cap, std::max<std::int64_t>(1, 4 * static_cast<std::int64_t>(x.peak_slots))));
   }
+  if (!opt.storage_cap_per_engine.empty() &&
+      static_cast<int>(opt.storage_cap_per_engine.size()) != x.n_engines)
+    throw std::invalid_argument("build_exec_plan: storage_cap_per_engine needs one entry per engine");
   if (x.pool_slots < x.peak_slots)
     throw std::invalid_argument("build_exec_plan: PE pool of " + std::to_string(x.pool_slots) +
                                 " slots is below the plan's peak of " +
@@ -325,20 +330,26 @@ StepResult EngineRuntime::run_step() {
                     DP_MAX_JOBS_PER_LAUNCH;
     batch.clear();
   };
-  const double cap = x.opt.storage_cap_Bps;
-  double gate_s = 0;  // emulated storage-NIC busy time (FIFO token bucket)
+  const double cap = x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
+                                                          : x.opt.storage_cap_per_engine[engine_];
+  const double pace = x.opt.pace_scale;
+  double gate_s = 0;  // emulated storage-NIC busy-until (FIFO token bucket), s since t0
   for (std::size_t i = 0; i < mine.size(); ++i) {
     const LoadJob& j = x.jobs[mine[i]];
     if (!peers_[j.pe]) throw std::runtime_error("run_step: PE " + std::to_string(j.pe) + " not attached");
     const std::int64_t bytes = j.cached * x.cfg.kv_bytes_per_token();
-    const bool gated = cap > 0;
+    const bool gated = cap > 0 || pace > 0;
     const bool hazard = !j.preds.empty();
     if (gated || hazard || j.fence || batch_pe != j.pe || batch.size() == DP_MAX_JOBS_PER_LAUNCH)
       flush();
     if (gated) {
-      // StorageRead of C*L*b bytes over this engine's storage NIC
-      gate_s += static_cast<double>(bytes) / cap;
+      // StorageRead of C*L*b bytes over this engine's storage NIC: starts
+      // when the NIC is free (and, replaying online, not before the planned
+      // admission), takes bytes / cap
+      const double begin = std::max(gate_s, pace > 0 ? j.t_admit * pace : 0.0);
+      gate_s = begin + (cap > 0 ? static_cast<double>(bytes) / cap : 0.0);
       std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
+      res.spans.push_back({begin, gate_s, bytes});
     }
     if (hazard) {
       const std::int64_t off = pred_off_[i];

@@ -256,6 +256,9 @@ __global__ void kv_store_fill(uint64_t* dst, int64_t n_pairs, int64_t words_per_
   }
 }
 
+constexpr int kMaxDevices = 64;
+int g_gather_ctas[kMaxDevices] = {};  // 0 = default
+
 int sm_count(int device) {
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
@@ -324,7 +327,8 @@ int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_
   p.n_layer = g.n_layer;
   p.block_tokens = g.block_tokens;
   p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
-  const int grid_cap = sm_count(pool->device) * 4;
+  const int dev_cap = (pool->device >= 0 && pool->device < kMaxDevices) ? g_gather_ctas[pool->device] : 0;
+  const int grid_cap = dev_cap > 0 ? dev_cap : sm_count(pool->device) * 4;
   auto s = static_cast<cudaStream_t>(stream);
   for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_JOBS_PER_LAUNCH) {
     const int32_t nj = std::min<int32_t>(DP_MAX_JOBS_PER_LAUNCH, n_jobs - j0);
@@ -584,6 +588,13 @@ int dp_h2d_layer_gather(dp_pool* pe, const dp_store* src, const dp_job* jobs, in
 int dp_h2d_push_p2p_layer(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs,
                           int32_t n_jobs, dp_stream de_stream) {
   return launch_gather(pe_view, de_src, jobs, n_jobs, de_stream, /*peer=*/true);
+}
+
+int dp_set_gather_ctas(int device, int32_t ctas) {
+  if (device < 0 || device >= kMaxDevices || ctas < 0)
+    return fail(DP_EINVAL, "set_gather_ctas: bad argument");
+  g_gather_ctas[device] = ctas;
+  return DP_OK;
 }
 
 int dp_layer_items(const dp_kv_geom* geom, int32_t n_blk, int32_t* out) {

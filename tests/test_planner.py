@@ -215,3 +215,31 @@ def test_offline_decisions_do_not_depend_on_seed():
     a = run_mine(trajs, P=1, D=1, g=2, seed=1, **QUICK)
     b = run_mine(trajs, P=1, D=1, g=2, seed=77, **QUICK)
     assert a["decisions"] == b["decisions"]
+
+
+def test_per_node_storage_bandwidth_extension():
+    # [B200 extension, config 5] uniform per-node values == the reference's s*B
+    trajs = dp.synthesize(max_len=8192, count=12, seed=4)
+    base = run_mine(trajs, P=2, D=2, g=1, B=50e9, s=0.125, **STORAGE_BOUND)
+    cfg = make_cluster(P=2, D=2, g=1, B=50e9, s=0.125)
+    cfg.storage_bandwidth_per_node = [0.125 * 50e9] * 4
+    same = dp.plan(cfg, trajs, flows=True, **STORAGE_BOUND)
+    assert same["decisions"] == base["decisions"] and same["makespan"] == base["makespan"]
+    # asymmetric caps: the slow nodes' storage queues grow, so the read-path
+    # split sends more reads to the fast side than under uniform caps
+    cfg.storage_bandwidth_per_node = [6.25e9, 1.5e9, 6.25e9, 1.5e9]
+    skew = dp.plan(cfg, trajs, **STORAGE_BOUND)
+    snic = {u["node_id"]: u["total_bytes"] for u in skew["usage"] if u["kind"] == "snic_read"}
+    assert snic[0] > snic[1] and snic[2] > snic[3]
+    cfg.storage_bandwidth_per_node = [1.0, 2.0]
+    with pytest.raises(ValueError):
+        cfg.validate()
+
+
+def test_online_plan_with_asymmetric_caps_completes():
+    trajs = dp.synthesize(max_len=8192, count=12, seed=4)
+    cfg = make_cluster(P=1, D=1, g=1, B=50e9, s=0.125)
+    cfg.storage_bandwidth_per_node = [6.25e9, 3.125e9]
+    rep = dp.plan(cfg, trajs, aps=5.0, seed=1, slo_ttft=1e9, steady_lookback=1e9, **STORAGE_BOUND)
+    assert rep["completed_requests"] == rep["total_requests"]
+    assert all(r[9] >= 0 for r in rep["requests"])

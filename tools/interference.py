@@ -1,0 +1,170 @@
+#!/usr/bin/env python
+"""BASELINE config 4: a per-layer bf16 GEMM stand-in on the prefill GPU and
+the interference of the KV loading path on it.
+
+Single process, two GPUs (PE = cuda:0, DE = cuda:1):
+
+1. isolation: mean GEMM time alone, then while (a) the DE pushes KV into the
+   PE pool over NVLink (K2), (b) the PE loads its own KV over PCIe (K1) at
+   several copy-CTA caps (dp_set_gather_ctas), (c) both.  The reference's
+   isolation bar is <= 2 % slowdown (proj/tests/acceptance.cpp:383-420).
+2. layerwise overlap: a 32K-token request's KV is pushed by the DE while the
+   PE computes layer l as soon as layer l has landed (dp_wait_layer on the
+   compute stream, the maybe_start_compute gate, proj/src/desim.cpp:623-628);
+   compare with load-then-compute.
+
+Prints one JSON object.  GEMMs use torch.matmul (cuBLAS) — a stand-in for
+the model's prefill compute, not part of the product path.
+"""
+
+import argparse
+import json
+import os
+import sys
+import threading
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2602_21548_b200 import abi  # noqa: E402
+
+L, T, B = 61, 64, 576
+
+
+def make_jobs(device, n_jobs, blocks, n_fb, n_slots, rng, layers=(0, L), ticket0=0):
+    keep, specs = [], []
+    perm = rng.permutation(n_slots)
+    for j in range(n_jobs):
+        fbs = torch.tensor(rng.integers(0, n_fb, blocks), dtype=torch.int64, device=f"cuda:{device}")
+        sl = torch.tensor(perm[(j * blocks) % n_slots:][:blocks].astype(np.int32), device=f"cuda:{device}")
+        keep += [fbs, sl]
+        specs.append((fbs.data_ptr(), sl.data_ptr(), blocks * T, blocks, layers[0], layers[1], ticket0 + j))
+    return abi.make_jobs(specs), keep
+
+
+def gemm_times(a, b, n, stream):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    with torch.cuda.stream(stream):
+        for e0, e1 in ev:
+            e0.record(stream)
+            torch.matmul(a, b)
+            e1.record(stream)
+    torch.cuda.synchronize(0)
+    return [e0.elapsed_time(e1) for e0, e1 in ev]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, default=8192)
+    ap.add_argument("--k", type=int, default=4096)
+    ap.add_argument("--gemms", type=int, default=300)
+    a = ap.parse_args()
+    assert torch.cuda.device_count() >= 2, "needs 2 GPUs"
+    g = abi.geom(L, T, B)
+    n_fb, blocks, n_jobs = 2048, 128, 64
+    n_slots = n_jobs * blocks
+    st_pe = abi.Store(0, g, n_fb, 9)
+    st_de = abi.Store(1, g, n_fb, 9)
+    pool = abi.Pool(0, g, n_slots, 2 * n_jobs + 1)
+    view = pool.peer_view(1)
+    rng = np.random.default_rng(0)
+    jobs_k2, keep2 = make_jobs(1, n_jobs, blocks, n_fb, n_slots, rng)
+    jobs_k1, keep1 = make_jobs(0, n_jobs, blocks, n_fb, n_slots, rng)
+    s_gemm = torch.cuda.Stream(device=0, priority=-1)  # high priority compute
+    s_k1 = torch.cuda.Stream(device=0, priority=0)
+    s_k2 = torch.cuda.Stream(device=1)
+    x = torch.randn(a.m, a.k, device="cuda:0", dtype=torch.bfloat16)
+    w = torch.randn(a.k, a.m, device="cuda:0", dtype=torch.bfloat16)
+    for _ in range(20):
+        torch.matmul(x, w)
+    torch.cuda.synchronize(0)
+    flops = 2.0 * a.m * a.m * a.k
+
+    def run_with(k1=False, k2=False, ctas=0):
+        for dev in (0, 1):
+            abi.set_gather_ctas(dev, ctas)
+        stop = threading.Event()
+        moved = {"k1": 0, "k2": 0}
+
+        def loader(kind):
+            dev, stream = (0, s_k1) if kind == "k1" else (1, s_k2)
+            with torch.cuda.device(dev):
+                while not stop.is_set():
+                    if kind == "k1":
+                        abi.h2d_layer_gather(pool, st_pe, jobs_k1, n_jobs, stream.cuda_stream)
+                    else:
+                        abi.h2d_push_p2p_layer(view, st_de, jobs_k2, n_jobs, stream.cuda_stream)
+                    stream.synchronize()
+                    moved[kind] += n_jobs * blocks * T * B * L
+        ths = [threading.Thread(target=loader, args=(kk,)) for kk, on in (("k1", k1), ("k2", k2)) if on]
+        for t in ths:
+            t.start()
+        import time
+        time.sleep(0.05)
+        t0 = time.time()
+        ts = gemm_times(x, w, a.gemms, s_gemm)
+        el = time.time() - t0
+        stop.set()
+        for t in ths:
+            t.join()
+        ts = sorted(ts)[len(ts) // 10: -len(ts) // 10]  # trimmed mean
+        mean = sum(ts) / len(ts)
+        return {"gemm_ms": round(mean, 4), "tflops": round(flops / mean / 1e9, 1),
+                "loader_gbps_during": {k: round(v / max(el, 1e-9) / 1e9, 1) for k, v in moved.items() if v}}
+
+    out = {"gemm": {"m": a.m, "n": a.m, "k": a.k, "dtype": "bf16"}}
+    out["alone"] = run_with()
+    base = out["alone"]["gemm_ms"]
+    cases = [("k2_push", dict(k2=True)), ("k1_default", dict(k1=True)),
+             ("k1_148ctas", dict(k1=True, ctas=148)), ("k1_32ctas", dict(k1=True, ctas=32)),
+             ("k1_8ctas", dict(k1=True, ctas=8)), ("k1_32ctas+k2", dict(k1=True, k2=True, ctas=32)),
+             ("k1_default+k2", dict(k1=True, k2=True))]
+    for name, kw in cases:
+        r = run_with(**kw)
+        r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base - 1.0), 2)
+        out[name] = r
+    for dev in (0, 1):
+        abi.set_gather_ctas(dev, 0)
+
+    # layerwise overlap: push one 32K-token request (512 blocks) and compute
+    # layer l once layer l has landed
+    req_blocks = 512
+    rng2 = np.random.default_rng(1)
+    jobs_req, keep3 = make_jobs(1, 1, req_blocks, n_fb, n_slots, rng2, ticket0=2 * n_jobs)
+    items = abi.layer_items(g, req_blocks)
+    import time
+
+    def pipeline(overlap):
+        pool.reset_counters()
+        torch.cuda.synchronize(0)
+        torch.cuda.synchronize(1)
+        t0 = time.time()
+        with torch.cuda.device(1):
+            abi.h2d_push_p2p_layer(view, st_de, jobs_req, 1, s_k2.cuda_stream)
+        if not overlap:
+            s_k2.synchronize()
+        with torch.cuda.stream(s_gemm):
+            for layer in range(L):
+                abi.wait_layer(pool, 2 * n_jobs, layer, items, 20000, s_gemm.cuda_stream)
+                torch.matmul(x, w)
+        torch.cuda.synchronize(0)
+        assert abi.wait_status(pool) == abi.DP_OK
+        return (time.time() - t0) * 1e3
+    pipeline(True)
+    ser = min(pipeline(False) for _ in range(3))
+    ovl = min(pipeline(True) for _ in range(3))
+    out["layerwise_32k_request"] = {"serial_ms": round(ser, 2), "overlapped_ms": round(ovl, 2),
+                                    "per_layer_load_ms": round(req_blocks * T * B / 51.5e9 * 1e3, 3),
+                                    "per_layer_gemm_ms": base, "speedup": round(ser / ovl, 3)}
+    view.close()
+    pool.close()
+    st_pe.close()
+    st_de.close()
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

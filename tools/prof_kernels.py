@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Profiling driver: one K1 (and, with --k2 and 2 GPUs, one K2) launch of a
 realistic size through the C ABI, timed with CUDA events on the launching
-stream.  Used plain and under ncu (profiles/)."""
+stream.  --ctas sweeps the gather CTA cap (dp_set_gather_ctas).  Used plain
+and under ncu (profiles/)."""
 
 import argparse
 import json
@@ -17,32 +18,19 @@ import torch  # noqa: E402
 from paper_2602_21548_b200 import abi  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--k2", action="store_true")
-    ap.add_argument("--jobs", type=int, default=64)
-    ap.add_argument("--blocks", type=int, default=128)  # 8K-token requests
-    ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--shape", default="dsv3", choices=["dsv3", "qwen"])
-    a = ap.parse_args()
-    L, T, b = (61, 64, 576) if a.shape == "dsv3" else (64, 64, 4096)
-    g = abi.geom(L, T, b)
-    n_fb = 2048 if a.shape == "dsv3" else 256
-    n_slots = a.jobs * a.blocks
-    if a.shape == "qwen":
-        n_slots = min(n_slots, 4096)
-    out = {}
-    for kind in (["k1"] + (["k2"] if a.k2 else [])):
-        src_dev = 1 if kind == "k2" else 0
-        st = abi.Store(src_dev, g, n_fb, 9)
-        pool = abi.Pool(0, g, n_slots, a.jobs)
-        dst = pool.peer_view(1) if kind == "k2" else pool
+def one(kind, a, g, L, T, b, n_fb, n_slots):
+    src_dev = 1 if kind == "k2" else 0
+    st = abi.Store(src_dev, g, n_fb, 9)
+    pool = abi.Pool(0, g, n_slots, a.jobs)
+    dst = pool.peer_view(1) if kind == "k2" else pool
+    try:
         rng = np.random.default_rng(0)
         keep, specs = [], []
         perm = rng.permutation(n_slots)
         for j in range(a.jobs):
             fbs = torch.tensor(rng.integers(0, n_fb, a.blocks), dtype=torch.int64, device=f"cuda:{src_dev}")
-            sl = torch.tensor(perm[(j * a.blocks) % n_slots:][:a.blocks].astype(np.int32), device=f"cuda:{src_dev}")
+            sl = torch.tensor(perm[(j * a.blocks) % n_slots:][:a.blocks].astype(np.int32),
+                              device=f"cuda:{src_dev}")
             keep += [fbs, sl]
             specs.append((fbs.data_ptr(), sl.data_ptr(), a.blocks * T, a.blocks, 0, L, j))
         jobs = abi.make_jobs(specs)
@@ -65,11 +53,35 @@ def main():
             if r:
                 times.append(e0.elapsed_time(e1))
         ms = sorted(times)[len(times) // 2]
-        out[kind] = {"bytes": nbytes, "ms": ms, "GBps": nbytes / ms / 1e6}
+        return {"bytes": nbytes, "ms": ms, "GBps": nbytes / ms / 1e6}
+    finally:
         if dst is not pool:
             dst.close()
         pool.close()
         st.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--k2", action="store_true")
+    ap.add_argument("--jobs", type=int, default=64)
+    ap.add_argument("--blocks", type=int, default=128)  # 8K-token requests
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--shape", default="dsv3", choices=["dsv3", "qwen"])
+    ap.add_argument("--ctas", default="0", help="comma list of gather CTA caps (0 = default)")
+    a = ap.parse_args()
+    L, T, b = (61, 64, 576) if a.shape == "dsv3" else (64, 64, 4096)
+    g = abi.geom(L, T, b)
+    n_fb = 2048 if a.shape == "dsv3" else 256
+    n_slots = a.jobs * a.blocks if a.shape == "dsv3" else min(a.jobs * a.blocks, 4096)
+    out = {}
+    for ctas in [int(x) for x in a.ctas.split(",")]:
+        for dev in range(torch.cuda.device_count()):
+            abi.set_gather_ctas(dev, ctas)
+        for kind in ["k1"] + (["k2"] if a.k2 else []):
+            out[kind if ctas == 0 else f"{kind}@{ctas}"] = one(kind, a, g, L, T, b, n_fb, n_slots)
+    for dev in range(torch.cuda.device_count()):
+        abi.set_gather_ctas(dev, 0)
     print(json.dumps(out))
 
 
