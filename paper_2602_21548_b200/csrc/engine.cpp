@@ -136,32 +136,55 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
                                 " slots is below the plan's peak of " +
                                 std::to_string(x.peak_slots) + " live blocks");
 
-  // pass 2: FIFO slot allocation in virtual time; hazards on reuse
-  std::vector<std::deque<std::int32_t>> free_q(x.n_pe);
-  std::vector<std::vector<std::int32_t>> owner(x.n_pe);  // slot -> job index of last writer
+  // pass 2: slot allocation in virtual time.  Freed slots go back to a queue
+  // of the engine that last wrote them; an allocation takes, in order, slots
+  // its own reader last wrote (ordered by its stream: only a launch boundary
+  // is needed), never-used slots, then other readers' slots (a cross-GPU
+  // hazard wait).  FIFO within each queue.
+  struct PeSlots {
+    std::deque<std::int32_t> fresh;
+    std::vector<std::deque<std::int32_t>> by_reader;
+    std::vector<std::int32_t> owner;  // slot -> job index of its last writer
+  };
+  std::vector<PeSlots> ps(x.n_pe);
   for (int p = 0; p < x.n_pe; ++p) {
-    owner[p].assign(x.pool_slots, -1);
-    for (std::int32_t s = 0; s < x.pool_slots; ++s) free_q[p].push_back(s);
+    ps[p].owner.assign(x.pool_slots, -1);
+    ps[p].by_reader.assign(x.n_engines, {});
+    for (std::int32_t s = 0; s < x.pool_slots; ++s) ps[p].fresh.push_back(s);
   }
+  auto take = [&](PeSlots& q, int reader) -> std::int32_t {
+    std::deque<std::int32_t>* src = nullptr;
+    if (!q.by_reader[reader].empty()) {
+      src = &q.by_reader[reader];
+    } else if (!q.fresh.empty()) {
+      src = &q.fresh;
+    } else {
+      for (int r = 0; r < x.n_engines && !src; ++r)
+        if (!q.by_reader[r].empty()) src = &q.by_reader[r];
+    }
+    if (!src) throw std::logic_error("build_exec_plan: slot allocator ran dry below the peak");
+    const std::int32_t s = src->front();
+    src->pop_front();
+    return s;
+  };
   std::vector<std::vector<std::int32_t>> job_slots(jobs.size());
   x.n_tickets.assign(x.n_pe, 0);
   std::vector<int> order;
   order.reserve(jobs.size());
   for (const Ev& e : evs) {
     LoadJob& j = jobs[e.job];
-    auto& fq = free_q[j.pe];
+    PeSlots& q = ps[j.pe];
     if (e.kind == 0) {
-      for (std::int32_t s : job_slots[e.job]) fq.push_back(s);
+      for (std::int32_t s : job_slots[e.job]) q.by_reader[j.reader].push_back(s);
       continue;
     }
     j.ticket = x.n_tickets[j.pe]++;
     auto& mine = job_slots[e.job];
     mine.reserve(j.n_blk);
     for (std::int32_t k = 0; k < j.n_blk; ++k) {
-      const std::int32_t s = fq.front();
-      fq.pop_front();
+      const std::int32_t s = take(q, j.reader);
       mine.push_back(s);
-      const std::int32_t prev = owner[j.pe][s];
+      const std::int32_t prev = q.owner[s];
       // same reader: stream order serialises launches, but items of one
       // launch run concurrently, so the reuse must start a new launch
       if (prev >= 0 && jobs[prev].reader == j.reader) j.fence = true;
@@ -171,7 +194,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
         j.pred_targets.push_back(static_cast<std::uint32_t>(
             static_cast<std::int64_t>(jobs[prev].n_blk) * x.items_per_block * cfg.n_layer));
       }
-      owner[j.pe][s] = e.job;
+      q.owner[s] = e.job;
     }
     order.push_back(e.job);
   }

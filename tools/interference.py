@@ -19,6 +19,7 @@ the model's prefill compute, not part of the product path.
 
 import argparse
 import json
+import time
 import os
 import sys
 import threading
@@ -60,7 +61,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, default=8192)
     ap.add_argument("--k", type=int, default=4096)
-    ap.add_argument("--gemms", type=int, default=300)
+    ap.add_argument("--gemms", type=int, default=6000)
     a = ap.parse_args()
     assert torch.cuda.device_count() >= 2, "needs 2 GPUs"
     g = abi.geom(L, T, B)
@@ -87,7 +88,8 @@ def main():
         for dev in (0, 1):
             abi.set_gather_ctas(dev, ctas)
         stop = threading.Event()
-        moved = {"k1": 0, "k2": 0}
+        done = {"k1": [], "k2": []}  # completion wall times of each loader launch
+        per_launch = n_jobs * blocks * T * B * L
 
         def loader(kind):
             dev, stream = (0, s_k1) if kind == "k1" else (1, s_k2)
@@ -98,22 +100,26 @@ def main():
                     else:
                         abi.h2d_push_p2p_layer(view, st_de, jobs_k2, n_jobs, stream.cuda_stream)
                     stream.synchronize()
-                    moved[kind] += n_jobs * blocks * T * B * L
+                    done[kind].append(time.time())
         ths = [threading.Thread(target=loader, args=(kk,)) for kk, on in (("k1", k1), ("k2", k2)) if on]
         for t in ths:
             t.start()
-        import time
-        time.sleep(0.05)
+        time.sleep(0.5)
         t0 = time.time()
         ts = gemm_times(x, w, a.gemms, s_gemm)
-        el = time.time() - t0
+        t1 = time.time()
         stop.set()
         for t in ths:
             t.join()
         ts = sorted(ts)[len(ts) // 10: -len(ts) // 10]  # trimmed mean
         mean = sum(ts) / len(ts)
+        rates = {}
+        for k, ts_done in done.items():
+            inside = [t for t in ts_done if t0 <= t <= t1]
+            if len(inside) >= 2:  # whole launches completed inside the GEMM window
+                rates[k] = round((len(inside) - 1) * per_launch / (inside[-1] - inside[0]) / 1e9, 1)
         return {"gemm_ms": round(mean, 4), "tflops": round(flops / mean / 1e9, 1),
-                "loader_gbps_during": {k: round(v / max(el, 1e-9) / 1e9, 1) for k, v in moved.items() if v}}
+                "window_s": round(t1 - t0, 2), "loader_gbps_during": rates}
 
     out = {"gemm": {"m": a.m, "n": a.m, "k": a.k, "dtype": "bf16"}}
     out["alone"] = run_with()
@@ -135,7 +141,6 @@ def main():
     rng2 = np.random.default_rng(1)
     jobs_req, keep3 = make_jobs(1, 1, req_blocks, n_fb, n_slots, rng2, ticket0=2 * n_jobs)
     items = abi.layer_items(g, req_blocks)
-    import time
 
     def pipeline(overlap):
         pool.reset_counters()
