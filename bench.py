@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--online", type=float, default=0.0,
                     help="config 5: Poisson arrivals at this many sessions/s, replayed in real time")
     ap.add_argument("--caps", default="", help="config 5: per-engine storage caps, GB/s, comma list")
+    ap.add_argument("--k1", default="sm", choices=["sm", "ce"],
+                    help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs)")
     return ap.parse_args()
 
 
@@ -205,6 +207,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
         opt.storage_cap_per_engine = caps
     if args.online > 0:
         opt.pace_scale = 1.0
+    opt.k1_mode = 1 if args.k1 == "ce" else 0
     opt.seed = 9
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     from paper_2602_21548_b200 import dist as dpdist
@@ -220,7 +223,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
         engines[e] = dp.EngineRuntime(xp, e, dev)
     if dist.world > 1:
         dpdist.connect_pools(dist, engines, cfg.prefill_nodes)
-    dev_ms, host_ms, launches, read_bytes, spans = [], [], 0, 0, None
+    dev_ms, host_ms, launches, read_bytes, spans, per_engine = [], [], 0, 0, None, None
     for step in range(args.warmup + args.steps):
         for rt in engines.values():
             rt.reset_counters()
@@ -235,15 +238,18 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
             host_ms.append(h)
             launches += sum(dist.allgather(sum(r.launches for r in res)))
             read_bytes += sum(dist.allgather(sum(r.bytes_read for r in res)))
-            spans = {}
-            for part in dist.allgather({e: r.spans for e, r in zip(engines, res)}):
-                spans.update(part)
+            spans, per_engine = {}, {}
+            for part in dist.allgather({e: (r.spans, r.device_ms) for e, r in zip(engines, res)}):
+                for e, (sp, ms) in part.items():
+                    spans[e] = sp
+                    per_engine[e] = round(ms, 1)
     snic = sum(u["total_bytes"] for u in planned["usage"] if u["kind"] == "snic_read")
     info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens,
                 model_gbps=snic / planned["makespan"] / 1e9 if planned["makespan"] > 0 else None,
                 requests=xp.requests, reader_bytes=list(xp.reader_bytes),
                 de_path=sum(1 for d in planned["decisions"] if d[4] == 1),
                 decisions=len(planned["decisions"]), pool_slots=xp.pool_slots, spans=spans,
+                per_engine_ms=[per_engine[e] for e in sorted(per_engine)] if per_engine else None,
                 caps=caps,
                 store_fb=xp.store_fb, launches=launches, read_bytes=read_bytes)
     if clocks is not None:
@@ -461,9 +467,11 @@ def main():
             "config": {"workload": f"{args.workload}: {len(trajs)} sessions, "
                                    + ("1 PE loader (K1)" if n == 1 else f"{P}P{D}D dual_path"),
                        "kv": shape, "storage_cap_gbps_per_engine": args.cap_gbps or None,
+                       "k1": args.k1,
                        "requests": info["requests"], "hit_bytes_per_step": info["hit_bytes"],
                        "de_path_requests": info["de_path"],
                        "read_gb_per_engine": [round(x / 1e9, 2) for x in info["reader_bytes"]],
+                       "last_step_ms_per_engine": info["per_engine_ms"],
                        "l2": "inputs >> L2 (no flush needed)"},
             "model_prediction_gbps": round(info["model_gbps"], 3) if info["model_gbps"] else None,
             "tokens_per_s": round(tokens_s, 1),

@@ -43,6 +43,9 @@ struct ExecOptions {
   std::int32_t pool_slots = 0;         // slots per PE pool; 0 = auto (plan peak)
   std::int64_t pool_bytes_max = 120LL << 30;
   std::int32_t wait_timeout_ms = 30000;
+  // PE-path loads (K1): 0 = SM gather kernel, 1 = copy engine (no SMs: the
+  // isolation mode while the PE computes, and the faster PCIe read path)
+  std::int32_t k1_mode = 0;
 };
 
 // One request's hit-KV transfer (all layers), in global execution order.

@@ -121,6 +121,16 @@ int dp_h2d_layer_gather(dp_pool* pe, const dp_store* src, const dp_job* jobs, in
 int dp_h2d_push_p2p_layer(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs,
                           int32_t n_jobs, dp_stream de_stream);
 
+/* K1 on the copy engine (no SMs): the same transfer as dp_h2d_layer_gather,
+ * issued as one strided cudaMemcpy2DAsync per contiguous run of blocks per
+ * layer (Full-Block pitch -> Layer-Block pitch) plus the partial last block,
+ * and after each layer a stream-ordered, fenced 32-bit write of the landed
+ * counters (cuStreamWriteValue32): ctr[ticket][l] = items, ctr[ticket][L] =
+ * items * layers done.  The isolation mode for a PE that is computing.
+ * HERE the dp_job block arrays (src_fb, dst_slot) must be HOST-readable. */
+int dp_h2d_layer_copy(dp_pool* pe, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
+                      dp_stream stream);
+
 /* Cap on the CTAs a K1/K2 launch on `device` may use (0 = default, 4 per SM).
  * The transfer is PCIe-bound, so a few CTAs keep the link full while leaving
  * the SMs to the prefill compute (the isolation knob of config 4). */

@@ -74,6 +74,7 @@ def lib():
         "dp_pool_peer_view": ([ctypes.c_int, P, PP], ctypes.c_int),
         "dp_h2d_layer_gather": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_h2d_push_p2p_layer": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
+        "dp_h2d_layer_copy": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_layer_items": ([ctypes.POINTER(Geom), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
                            ctypes.c_int),
         "dp_wait_layer": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int32, P],
@@ -201,6 +202,11 @@ def h2d_layer_gather(pool, store, jobs, n, stream=0):
 
 def h2d_push_p2p_layer(pool_view, store, jobs, n, stream=0):
     check(lib().dp_h2d_push_p2p_layer(pool_view.ptr, store.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def h2d_layer_copy(pool, store, jobs, n, stream=0):
+    """K1 on the copy engine; jobs' block arrays must be host memory."""
+    check(lib().dp_h2d_layer_copy(pool.ptr, store.ptr, jobs, n, ctypes.c_void_p(stream)))
 
 
 def layer_items(g, n_blk):

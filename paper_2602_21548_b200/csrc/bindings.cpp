@@ -330,6 +330,7 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("storage_cap_Bps", &dualpath::ExecOptions::storage_cap_Bps)
       .def_readwrite("storage_cap_per_engine", &dualpath::ExecOptions::storage_cap_per_engine)
       .def_readwrite("pace_scale", &dualpath::ExecOptions::pace_scale)
+      .def_readwrite("k1_mode", &dualpath::ExecOptions::k1_mode)
       .def_readwrite("store_fb", &dualpath::ExecOptions::store_fb)
       .def_readwrite("store_bytes_max", &dualpath::ExecOptions::store_bytes_max)
       .def_readwrite("seed", &dualpath::ExecOptions::seed)

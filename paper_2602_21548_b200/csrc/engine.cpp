@@ -342,15 +342,27 @@ StepResult EngineRuntime::run_step() {
   std::vector<dp_job> batch;
   batch.reserve(DP_MAX_JOBS_PER_LAUNCH);
   int batch_pe = -1;
+  const bool k1_ce = x.opt.k1_mode == 1;
   auto flush = [&]() {
     if (batch.empty()) return;
     dp_pool* dst = peers_[batch_pe];
-    const int rc = batch_pe == engine_
-                       ? dp_h2d_layer_gather(dst, store_, batch.data(), static_cast<int32_t>(batch.size()), s)
-                       : dp_h2d_push_p2p_layer(dst, store_, batch.data(), static_cast<int32_t>(batch.size()), s);
-    check(rc, batch_pe == engine_ ? "dp_h2d_layer_gather" : "dp_h2d_push_p2p_layer");
-    res.launches += (static_cast<std::int64_t>(batch.size()) + DP_MAX_JOBS_PER_LAUNCH - 1) /
-                    DP_MAX_JOBS_PER_LAUNCH;
+    const auto n = static_cast<int32_t>(batch.size());
+    int rc;
+    const char* what;
+    if (batch_pe != engine_) {
+      rc = dp_h2d_push_p2p_layer(dst, store_, batch.data(), n, s);
+      what = "dp_h2d_push_p2p_layer";
+    } else if (k1_ce) {
+      rc = dp_h2d_layer_copy(dst, store_, batch.data(), n, s);
+      what = "dp_h2d_layer_copy";
+    } else {
+      rc = dp_h2d_layer_gather(dst, store_, batch.data(), n, s);
+      what = "dp_h2d_layer_gather";
+    }
+    check(rc, what);
+    if (!(k1_ce && batch_pe == engine_))  // kernel launches (the copy engine path has none)
+      res.launches += (static_cast<std::int64_t>(batch.size()) + DP_MAX_JOBS_PER_LAUNCH - 1) /
+                      DP_MAX_JOBS_PER_LAUNCH;
     batch.clear();
   };
   const double cap = x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
@@ -383,8 +395,12 @@ StepResult EngineRuntime::run_step() {
       ++res.launches;
     }
     batch_pe = j.pe;
-    batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0,
-                           x.cfg.n_layer, j.ticket});
+    if (k1_ce && j.pe == engine_)  // copy engine: host-readable block tables
+      batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,
+                             j.cached, j.n_blk, 0, x.cfg.n_layer, j.ticket});
+    else
+      batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0,
+                             x.cfg.n_layer, j.ticket});
     res.bytes_read += bytes;
     ++res.jobs;
   }

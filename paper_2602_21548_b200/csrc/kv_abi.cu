@@ -18,9 +18,11 @@
 // layer l lands before l+1 (layerwise prefill).  A launch
 // carries up to DP_MAX_JOBS_PER_LAUNCH job headers in its parameter block;
 // each warp decodes its item's job with a ballot over the job prefix sums.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -588,6 +590,89 @@ int dp_h2d_layer_gather(dp_pool* pe, const dp_store* src, const dp_job* jobs, in
 int dp_h2d_push_p2p_layer(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs,
                           int32_t n_jobs, dp_stream de_stream) {
   return launch_gather(pe_view, de_src, jobs, n_jobs, de_stream, /*peer=*/true);
+}
+
+namespace {
+
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+// cuStreamWriteValue32 through the runtime's driver entry point (no link
+// dependency on libcuda, so the library still loads on a machine without a
+// driver; the copy-engine path then fails with DP_ECUDA).
+WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue32Fn>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+}  // namespace
+
+int dp_h2d_layer_copy(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
+                      dp_stream stream) {
+  if (!pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0)
+    return fail(DP_EINVAL, "h2d_layer_copy: null argument");
+  if (!pool->owner) return fail(DP_EINVAL, "h2d_layer_copy: destination must be the local PE pool");
+  if (!geom_equal(pool->geom, src->geom))
+    return fail(DP_EINVAL, "h2d_layer_copy: pool and store geometry differ");
+  const WriteValue32Fn wv = write_value32();
+  if (!wv) return fail(DP_ECUDA, "h2d_layer_copy: cuStreamWriteValue32 unavailable");
+  const dp_kv_geom& g = pool->geom;
+  const int64_t lb = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
+  const int64_t fbb = lb * g.n_layer;
+  const int64_t plane = lb * pool->n_slots;
+  const int32_t items = static_cast<int32_t>(chunks_per_block(g));
+  DeviceGuard guard(pool->device);
+  auto s = static_cast<cudaStream_t>(stream);
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    const dp_job& job = jobs[j];
+    const int64_t need_blk = (job.n_tokens + g.block_tokens - 1) / g.block_tokens;
+    if (job.n_tokens < 0 || job.n_blk != need_blk || job.layer_begin < 0 ||
+        job.layer_end > g.n_layer || job.layer_begin > job.layer_end || job.ticket >= pool->n_tickets)
+      return fail(DP_EINVAL, "h2d_layer_copy: job " + std::to_string(j) + " out of range");
+    if (job.n_blk == 0) continue;
+    for (int32_t k = 0; k < job.n_blk; ++k)
+      if (job.src_fb[k] < 0 || job.src_fb[k] >= src->n_fb || job.dst_slot[k] < 0 ||
+          job.dst_slot[k] >= pool->n_slots)
+        return fail(DP_EINVAL, "h2d_layer_copy: block " + std::to_string(k) + " out of range");
+    const int32_t full = job.n_tokens % g.block_tokens == 0 ? job.n_blk : job.n_blk - 1;
+    uint32_t* row = pool->counters + static_cast<int64_t>(job.ticket) * (g.n_layer + 1);
+    for (int32_t layer = job.layer_begin; layer < job.layer_end; ++layer) {
+      for (int32_t k = 0; k < full;) {
+        int32_t run = 1;
+        while (k + run < full && job.src_fb[k + run] == job.src_fb[k] + run &&
+               job.dst_slot[k + run] == job.dst_slot[k] + run)
+          ++run;
+        DP_CUDA(cudaMemcpy2DAsync(pool->base + layer * plane + job.dst_slot[k] * lb, lb,
+                                  src->host + job.src_fb[k] * fbb + layer * lb, fbb, lb, run,
+                                  cudaMemcpyHostToDevice, s));
+        k += run;
+      }
+      if (full < job.n_blk) {
+        const int32_t k = full;
+        const int64_t bytes = (job.n_tokens - static_cast<int64_t>(k) * g.block_tokens) * g.bytes_per_token_layer;
+        DP_CUDA(cudaMemcpyAsync(pool->base + layer * plane + job.dst_slot[k] * lb,
+                                src->host + job.src_fb[k] * fbb + layer * lb, bytes,
+                                cudaMemcpyHostToDevice, s));
+      }
+      if (job.ticket >= 0) {
+        const uint32_t per_layer = static_cast<uint32_t>(job.n_blk) * items;
+        if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + layer), per_layer, 0) !=
+                CUDA_SUCCESS ||
+            wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + g.n_layer),
+               per_layer * static_cast<uint32_t>(layer - job.layer_begin + 1), 0) != CUDA_SUCCESS)
+          return fail(DP_ECUDA, "h2d_layer_copy: cuStreamWriteValue32 failed");
+      }
+    }
+  }
+  return DP_OK;
 }
 
 int dp_set_gather_ctas(int device, int32_t ctas) {

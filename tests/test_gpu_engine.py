@@ -151,3 +151,23 @@ def test_cross_reader_slot_reuse_hazards(two_gpus):
         pe.reset_counters()
         dp.run_step_all([pe, de])
         verify_pool(pe, xp, cfg)
+
+
+@pytest.mark.multigpu
+def test_two_engines_k1_on_copy_engine(two_gpus):
+    cfg = cluster(1, 1)
+    trajs = small_trace(count=8, turns=5)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.k1_mode = 1
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    pe = dp.EngineRuntime(xp, 0, 0)
+    de = dp.EngineRuntime(xp, 1, 1)
+    de.attach_peer_local(0, pe)
+    for _ in range(2):
+        pe.reset_counters()
+        res = dp.run_step_all([pe, de])
+        assert res[0].launches <= 1  # the PE issues copies, not kernels (at most its final wait)
+    verify_counters(pe, xp, cfg)
+    verify_pool(pe, xp, cfg)

@@ -217,3 +217,44 @@ def test_k2_push_p2p_parity(two_gpus, L, T, b):
         view.close()
         pool.close()
         st_de.close()
+
+
+@pytest.mark.parametrize("L,T,b", [(61, 64, 576), (4, 64, 4096), (3, 16, 1024)])
+def test_k1_copy_engine_parity(gpus, L, T, b):
+    """K1 on the copy engine (dp_h2d_layer_copy): strided 2D copies of block
+    runs + fenced counter writes; same bytes and counters as the kernel."""
+    rng = np.random.default_rng(21)
+    g = abi.geom(L, T, b)
+    n_fb, n_slots = 16, 64
+    st = abi.Store(0, g, n_fb, SEED)
+    pool = abi.Pool(0, g, n_slots, 12)
+    try:
+        plain, keep, specs, used = [], [], [], 0
+        for t in range(12):
+            nblk = int(rng.integers(0, 6))
+            if used + nblk + 1 > n_slots:
+                nblk = 0
+            ntok = 0 if nblk == 0 else (nblk - 1) * T + int(rng.integers(1, T + 1))
+            # contiguous runs with breaks: consecutive Full Blocks and slots, split once
+            fb0 = int(rng.integers(0, n_fb - nblk)) if nblk else 0
+            fbs = np.arange(fb0, fb0 + nblk, dtype=np.int64)
+            slots = np.arange(used, used + nblk, dtype=np.int32)
+            if nblk >= 3:
+                slots[nblk // 2:] += 1  # a slot gap: two runs
+            used += nblk + 1
+            keep += [fbs, slots]
+            specs.append((fbs.ctypes.data, slots.ctypes.data, ntok, nblk, 0, L, t))
+            plain.append((fbs, slots, ntok, 0, L))
+        abi.h2d_layer_copy(pool, st, abi.make_jobs(specs), len(specs))
+        for t, (fbs, slots, ntok, l0, l1) in enumerate(plain):
+            items = abi.layer_items(g, len(slots))
+            abi.wait_layer(pool, t, L, items * L, timeout_ms=5000)
+            if len(slots):
+                abi.wait_layer(pool, t, L - 1, items, timeout_ms=5000)
+        sync()
+        assert abi.wait_status(pool) == abi.DP_OK
+        store_img = np.frombuffer(st.bytes(), dtype=np.uint8).copy()
+        check_pool(pool, refpy.geom(L, T, b), plain, T, b, store_img, n_slots)
+    finally:
+        pool.close()
+        st.close()

@@ -74,6 +74,14 @@ def main():
     rng = np.random.default_rng(0)
     jobs_k2, keep2 = make_jobs(1, n_jobs, blocks, n_fb, n_slots, rng)
     jobs_k1, keep1 = make_jobs(0, n_jobs, blocks, n_fb, n_slots, rng)
+    # the same PE-path load for the copy engine: host block tables, contiguous runs
+    ce_keep, ce_specs = [], []
+    for j in range(n_jobs):
+        fbs = np.arange(j * blocks, (j + 1) * blocks, dtype=np.int64) % n_fb
+        sl = np.arange(j * blocks, (j + 1) * blocks, dtype=np.int32) % n_slots
+        ce_keep += [fbs, sl]
+        ce_specs.append((fbs.ctypes.data, sl.ctypes.data, blocks * T, blocks, 0, L, j))
+    jobs_ce = abi.make_jobs(ce_specs)
     s_gemm = torch.cuda.Stream(device=0, priority=-1)  # high priority compute
     s_k1 = torch.cuda.Stream(device=0, priority=0)
     s_k2 = torch.cuda.Stream(device=1)
@@ -84,7 +92,7 @@ def main():
     torch.cuda.synchronize(0)
     flops = 2.0 * a.m * a.m * a.k
 
-    def run_with(k1=False, k2=False, ctas=0):
+    def run_with(k1=False, k2=False, ctas=0, ce=False):
         for dev in (0, 1):
             abi.set_gather_ctas(dev, ctas)
         stop = threading.Event()
@@ -95,7 +103,9 @@ def main():
             dev, stream = (0, s_k1) if kind == "k1" else (1, s_k2)
             with torch.cuda.device(dev):
                 while not stop.is_set():
-                    if kind == "k1":
+                    if kind == "k1" and ce:
+                        abi.h2d_layer_copy(pool, st_pe, jobs_ce, n_jobs, stream.cuda_stream)
+                    elif kind == "k1":
                         abi.h2d_layer_gather(pool, st_pe, jobs_k1, n_jobs, stream.cuda_stream)
                     else:
                         abi.h2d_push_p2p_layer(view, st_de, jobs_k2, n_jobs, stream.cuda_stream)
@@ -127,7 +137,9 @@ def main():
     cases = [("k2_push", dict(k2=True)), ("k1_default", dict(k1=True)),
              ("k1_148ctas", dict(k1=True, ctas=148)), ("k1_32ctas", dict(k1=True, ctas=32)),
              ("k1_8ctas", dict(k1=True, ctas=8)), ("k1_32ctas+k2", dict(k1=True, k2=True, ctas=32)),
-             ("k1_default+k2", dict(k1=True, k2=True))]
+             ("k1_default+k2", dict(k1=True, k2=True)),
+             ("k1_copy_engine", dict(k1=True, ce=True)),
+             ("k1_copy_engine+k2", dict(k1=True, k2=True, ce=True))]
     for name, kw in cases:
         r = run_with(**kw)
         r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base - 1.0), 2)
