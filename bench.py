@@ -100,6 +100,10 @@ def cluster(shape, P, D, cap_bps, caps=None):
     return cfg
 
 
+# ncu --set full of the K1 launch (profiles/r01_k1_full.ncu-rep): dram read +
+# write bytes per launch over the launch's algorithmic bytes (18.42 GB)
+TRAFFIC = {"c1": 18454911288, "c2": 18454911288}  # 85.6 MB read + 18.37 GB write
+
 # storage-bound cost model (proj/tests/acceptance.cpp:62-72): the bench
 # measures loading, compute is nearly free
 PLAN_KW = dict(cl=1e-12, dctx=1e-15, dstep=1e-9, sub=0.0, beta=1_000_000_000)
@@ -182,6 +186,52 @@ def measure_pcie_peak(device):
             best = min(best, a.elapsed_time(b))
     del h, d
     return n / (best * 1e-3)
+
+
+def measure_k1(device, shape, target_bytes=18421383168):
+    """The dominant kernel alone, live: one K1 launch (DS-V3 or Qwen Layer
+    Blocks, 8K-token requests, random Full Blocks and slots) through the C
+    ABI, CUDA events on its stream, median of 3 after a warm-up."""
+    import numpy as np
+    import torch
+    from paper_2602_21548_b200 import abi
+    L, T, b = shape["L"], shape["T"], shape["b"]
+    blocks = 128
+    per_job = blocks * T * b * L
+    jobs_n = max(1, min(64, target_bytes // per_job))  # DS-V3: the 64-job launch ncu profiled
+    g = abi.geom(L, T, b)
+    n_fb = max(blocks, (2 << 30) // (L * T * b))
+    st = abi.Store(device, g, n_fb, 9)
+    pool = abi.Pool(device, g, jobs_n * blocks, jobs_n)
+    try:
+        rng = np.random.default_rng(0)
+        keep, specs = [], []
+        perm = rng.permutation(jobs_n * blocks).astype(np.int32)
+        for j in range(jobs_n):
+            f = torch.tensor(rng.integers(0, n_fb, blocks), dtype=torch.int64, device=f"cuda:{device}")
+            sl = torch.tensor(perm[j * blocks:(j + 1) * blocks], device=f"cuda:{device}")
+            keep += [f, sl]
+            specs.append((f.data_ptr(), sl.data_ptr(), blocks * T, blocks, 0, L, j))
+        jobs = abi.make_jobs(specs)
+        s = torch.cuda.Stream(device=device)
+        times = []
+        for r in range(4):
+            pool.reset_counters(s.cuda_stream)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.device(device):
+                e0.record(s)
+                abi.h2d_layer_gather(pool, st, jobs, len(specs), s.cuda_stream)
+                e1.record(s)
+            e1.synchronize()
+            if r:
+                times.append(e0.elapsed_time(e1))
+        ms = sorted(times)[1]
+        nbytes = jobs_n * per_job
+        return nbytes / (ms * 1e-3) / 1e9, ms, nbytes
+    finally:
+        pool.close()
+        st.close()
 
 
 def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
@@ -444,13 +494,15 @@ def main():
         except Exception as exc:  # reported, never fatal to the GPU number
             cpu = {"error": str(exc)[:200]}
     clk = clocks.summary(set(range(n)))
+    k1 = None
     if dist.rank == 0:
-        # roofline of the dominant kernel (K1 on the PE): its bytes over its
-        # device time in the timed steps (K1 is the only non-trivial kernel
-        # of the PE's stream; waits complete immediately on a PE-only step)
-        k1_bytes = info["reader_bytes"][0]
-        k1_ms = statistics.mean(head["dev_ms"]) if n == 1 else None
-        achieved = k1_bytes / (k1_ms * 1e-3) / 1e9 if k1_ms else value / max(1, n)
+        k1 = measure_k1(dist.local if dist.world > 1 else 0, shape)
+    if dist.rank == 0:
+        # roofline of the dominant kernel, K1 (K2 is the same kernel body with
+        # peer stores, 0.999x its rate, profiles/r01_k1_k2_events.json),
+        # measured live on rank 0 after the timed steps: algorithmic bytes
+        # (C*L*b of the launch) / CUDA-event time of the launch
+        achieved, k1_ms, k1_bytes = k1
         out = {
             "metric": "aggregate KV-load GB/s",
             "value": round(value, 3),
@@ -482,8 +534,11 @@ def main():
             "roofline": {"bound": "pcie", "achieved": round(achieved, 2),
                          "peak": round(peak / 1e9, 2) if peak else None, "unit": "GB/s",
                          "frac": round(achieved / (peak / 1e9), 4) if peak else None,
-                         "traffic": None,
-                         "peak_source": "cudaMemcpyAsync H2D 1 GiB pinned, best of 5, measured in this run"},
+                         "traffic": TRAFFIC.get(args.workload),
+                         "kernel": "kv_gather<false> (K1)", "launch_bytes": k1_bytes,
+                         "launch_ms": round(k1_ms, 3),
+                         "peak_source": "cudaMemcpyAsync H2D 1 GiB pinned, best of 5, measured in this run",
+                         "step_rate_per_engine": round(value / max(1, n), 2)},
             "cpu_baseline": cpu,
             "clocks": clk,
             "plan_s": round(info["plan_s"], 2),
