@@ -121,6 +121,67 @@ int dp_h2d_layer_gather(dp_pool* pe, const dp_store* src, const dp_job* jobs, in
 int dp_h2d_push_p2p_layer(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs,
                           int32_t n_jobs, dp_stream de_stream);
 
+/* ------------------------------------------------------------------------
+ * PD handoff: PeToDe / MissMerge per layer
+ * (desim.cpp:630-640) and DecodeH2D (desim.cpp:650-651, :740-747).
+ *
+ * B200 mapping: the DE's decode pool (a dp_pool on the DE) must end up
+ * holding the whole prompt KV [0, C+A) of each request (de_need =
+ * full(prompt), desim.cpp:592).  On one NVLink domain the DE's DRAM hop is
+ * not needed:
+ *   - DE read path: the DE reads each hit Layer Block from its host store
+ *     ONCE and stores it both into the PE pool (NVLink, DeToPe) and into its
+ *     own decode pool (local HBM: the hit half of DecodeH2D) —
+ *     dp_h2d_push_p2p_dual;
+ *   - per layer on the PE, after that layer's hit KV has landed, the
+ *     prefill stand-in writes the miss tokens' KV [C, C+A) into the PE pool
+ *     and the layer is pushed to the DE pool over NVLink: all prompt tokens
+ *     on the PE read path (PeToDe), the miss tokens only on the DE read path
+ *     (MissMerge) — dp_prefill_handoff (K3).
+ * DE pool row of a request, per layer: (hit blocks if DE path, else 0) *
+ * items_per_block from the dual gather + prompt blocks * items_per_block
+ * from K3; column n_layer sums them over layers. */
+
+typedef struct dp_dual_job {
+  dp_job pe;               /* -> PE pool (peer view), as dp_h2d_push_p2p_layer */
+  const int32_t* de_slot;  /* [pe.n_blk] slots in the DE's own decode pool */
+  int32_t de_ticket;       /* DE pool landed-counter row, or -1 */
+  int32_t reserved;
+} dp_dual_job;
+
+typedef struct dp_handoff_job {
+  const int64_t* src_fb;   /* [n_blk] storage Full Block of each prompt block: the content
+                              the prefill stand-in writes for the miss tokens */
+  const int32_t* pe_slot;  /* [n_blk] the request's prompt blocks in the PE pool */
+  const int32_t* de_slot;  /* [n_blk] its blocks in the DE decode pool */
+  int64_t n_cached;        /* C: tokens [0, C) are hit KV (already in / landing in the PE pool) */
+  int64_t n_prompt;        /* C + A */
+  int32_t n_blk;           /* ceil((C + A) / T) */
+  int32_t push_hit;        /* 1: PE read path (PeToDe moves C + A); 0: DE path (MissMerge moves A) */
+  int32_t pe_ticket;       /* PE pool row whose layer l must reach pe_wait_items before layer l
+                              is processed (the maybe_start_compute gate), or -1 (stream-ordered) */
+  uint32_t pe_wait_items;  /* per-layer items of the hit KV */
+  int32_t de_ticket;       /* DE pool row released per layer, or -1 */
+  int32_t reserved;
+} dp_handoff_job;
+
+#define DP_MAX_DUAL_JOBS_PER_LAUNCH 48
+#define DP_MAX_HANDOFF_JOBS_PER_LAUNCH 48
+
+/* DE read path fused with DecodeH2D: run on the DE; one PCIe read per hit
+ * Layer Block, stored to the PE pool (peer, system-scope release of its
+ * counters) and to the DE's own decode pool `de_pool` (its counters too). */
+int dp_h2d_push_p2p_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* de_src,
+                         const dp_dual_job* jobs, int32_t n_jobs, dp_stream de_stream);
+
+/* K3, run on the PE: per layer (in order), per prompt block: wait for the
+ * layer's hit KV (pe_ticket), write the miss tokens' KV (content formula of
+ * the store, `seed`) into the PE pool, push the job's bytes of the layer to
+ * the DE pool `de_view` (peer) and release the DE pool row.  A gate wait
+ * longer than timeout_ms sets the PE pool's watchdog flag (dp_wait_status). */
+int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job* jobs,
+                       int32_t n_jobs, uint64_t seed, int32_t timeout_ms, dp_stream stream);
+
 /* K1 on the copy engine (no SMs): the same transfer as dp_h2d_layer_gather,
  * issued as one strided cudaMemcpy2DAsync per contiguous run of blocks per
  * layer (Full-Block pitch -> Layer-Block pitch) plus the partial last block,

@@ -36,6 +36,19 @@ class Job(ctypes.Structure):
                 ("ticket", ctypes.c_int32)]
 
 
+class DualJob(ctypes.Structure):
+    _fields_ = [("pe", Job), ("de_slot", ctypes.c_void_p), ("de_ticket", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class HandoffJob(ctypes.Structure):
+    _fields_ = [("src_fb", ctypes.c_void_p), ("pe_slot", ctypes.c_void_p), ("de_slot", ctypes.c_void_p),
+                ("n_cached", ctypes.c_int64), ("n_prompt", ctypes.c_int64), ("n_blk", ctypes.c_int32),
+                ("push_hit", ctypes.c_int32), ("pe_ticket", ctypes.c_int32),
+                ("pe_wait_items", ctypes.c_uint32), ("de_ticket", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
 class PoolHandle(ctypes.Structure):
     _fields_ = [("ipc", ctypes.c_ubyte * 64), ("geom", Geom), ("n_slots", ctypes.c_int32),
                 ("n_tickets", ctypes.c_int32), ("device", ctypes.c_int32),
@@ -75,6 +88,9 @@ def lib():
         "dp_h2d_layer_gather": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_h2d_push_p2p_layer": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_h2d_layer_copy": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
+        "dp_h2d_push_p2p_dual": ([P, P, P, ctypes.POINTER(DualJob), ctypes.c_int32, P], ctypes.c_int),
+        "dp_prefill_handoff": ([P, P, ctypes.POINTER(HandoffJob), ctypes.c_int32, ctypes.c_uint64,
+                                ctypes.c_int32, P], ctypes.c_int),
         "dp_layer_items": ([ctypes.POINTER(Geom), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
                            ctypes.c_int),
         "dp_wait_layer": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int32, P],
@@ -207,6 +223,15 @@ def h2d_push_p2p_layer(pool_view, store, jobs, n, stream=0):
 def h2d_layer_copy(pool, store, jobs, n, stream=0):
     """K1 on the copy engine; jobs' block arrays must be host memory."""
     check(lib().dp_h2d_layer_copy(pool.ptr, store.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def push_p2p_dual(pe_view, de_pool, store, jobs, n, stream=0):
+    check(lib().dp_h2d_push_p2p_dual(pe_view.ptr, de_pool.ptr, store.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def prefill_handoff(pe_pool, de_view, jobs, n, seed, timeout_ms=20000, stream=0):
+    check(lib().dp_prefill_handoff(pe_pool.ptr, de_view.ptr, jobs, n, seed, timeout_ms,
+                                   ctypes.c_void_p(stream)))
 
 
 def layer_items(g, n_blk):

@@ -106,7 +106,8 @@ __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
 
 // Warp-cooperative decode of the job owning `item`: lane j tests job
 // j (and j+32), the ballot's population count is the job index.
-__device__ __forceinline__ int decode_job(const GatherParams& p, int64_t item) {
+template <class Params>
+__device__ __forceinline__ int decode_job(const Params& p, int64_t item) {
   const int lane = threadIdx.x & 31;
   const unsigned lo = __ballot_sync(
       0xffffffffu, lane + 1 < p.n_jobs && p.item_begin[lane + 1] <= item);
@@ -763,6 +764,311 @@ int dp_device_count(void) {
     return 0;
   }
   return n;
+}
+
+}  // extern "C"
+
+// ============================================================= PD handoff
+// dp_h2d_push_p2p_dual (the DE read path fused with DecodeH2D) and
+// dp_prefill_handoff (K3: prefill stand-in + PeToDe / MissMerge per layer).
+namespace {
+
+struct DualParams {
+  const char* store;
+  char* pe_pool;        // peer
+  uint32_t* pe_ctr;
+  int64_t pe_stride;    // PE pool layer plane
+  char* de_pool;        // local decode pool
+  uint32_t* de_ctr;
+  int64_t de_stride;
+  int64_t lb_bytes, fb_bytes, bpt;
+  int32_t n_layer, block_tokens, n_chunk, n_jobs;
+  int64_t item_begin[DP_MAX_DUAL_JOBS_PER_LAUNCH + 1];
+  dp_dual_job jobs[DP_MAX_DUAL_JOBS_PER_LAUNCH];
+};
+static_assert(sizeof(DualParams) <= 4000, "kernel parameter block too large");
+
+struct HandoffParams {
+  char* pe_pool;        // local
+  char* de_pool;        // peer
+  uint32_t* pe_ctr;
+  uint32_t* de_ctr;
+  int64_t pe_stride, de_stride;
+  int* err_flag;
+  uint64_t timeout_ns;
+  uint64_t seed_mix;
+  int64_t lb_bytes, bpt;
+  int32_t n_layer, block_tokens, n_chunk, n_jobs;
+  int64_t item_begin[DP_MAX_HANDOFF_JOBS_PER_LAUNCH + 1];
+  dp_handoff_job jobs[DP_MAX_HANDOFF_JOBS_PER_LAUNCH];
+};
+static_assert(sizeof(HandoffParams) <= 4000, "kernel parameter block too large");
+static_assert(sizeof(dp_dual_job) == 56, "dp_dual_job layout");
+static_assert(sizeof(dp_handoff_job) == 64, "dp_handoff_job layout");
+
+__device__ __forceinline__ void release_sys(uint32_t* row, int layer, int n_layer) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(row + layer) : "memory");
+  asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(row + n_layer) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads) kv_gather_dual(const __grid_constant__ DualParams p) {
+  const int64_t total = p.item_begin[p.n_jobs];
+  const int tid = threadIdx.x;
+  for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+    const int j = decode_job(p, item);
+    const dp_dual_job& dj = p.jobs[j];
+    const dp_job& job = dj.pe;
+    const int64_t local = item - p.item_begin[j];
+    const int64_t per_layer = static_cast<int64_t>(job.n_blk) * p.n_chunk;
+    const int layer = job.layer_begin + static_cast<int>(local / per_layer);
+    const int64_t rem = local % per_layer;
+    const int blk = static_cast<int>(rem / p.n_chunk);
+    const int chunk = static_cast<int>(rem % p.n_chunk);
+    const int64_t tok0 = static_cast<int64_t>(blk) * p.block_tokens;
+    const int64_t valid = min(static_cast<int64_t>(p.block_tokens), job.n_tokens - tok0) * p.bpt;
+    const int64_t beg = static_cast<int64_t>(chunk) * kChunkBytes;
+    const int64_t end = min(beg + kChunkBytes, valid);
+    if (end > beg) {
+      const uint4* src = reinterpret_cast<const uint4*>(p.store + job.src_fb[blk] * p.fb_bytes +
+                                                        layer * p.lb_bytes + beg);
+      uint4* d_pe = reinterpret_cast<uint4*>(p.pe_pool + layer * p.pe_stride +
+                                             static_cast<int64_t>(job.dst_slot[blk]) * p.lb_bytes + beg);
+      uint4* d_de = reinterpret_cast<uint4*>(p.de_pool + layer * p.de_stride +
+                                             static_cast<int64_t>(dj.de_slot[blk]) * p.lb_bytes + beg);
+      const int n16 = static_cast<int>((end - beg) >> 4);
+      for (int base = 0; base < n16; base += kThreads * kUnroll) {
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int i = base + u * kThreads + tid;
+          if (i < n16) v[u] = ld_stream(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int i = base + u * kThreads + tid;
+          if (i < n16) {
+            st_v4(d_pe + i, v[u]);
+            st_v4(d_de + i, v[u]);
+          }
+        }
+      }
+    }
+    if (job.ticket >= 0 || dj.de_ticket >= 0) {
+      __syncthreads();
+      if (tid == 0) {
+        if (job.ticket >= 0)
+          release_sys(p.pe_ctr + static_cast<int64_t>(job.ticket) * (p.n_layer + 1), layer, p.n_layer);
+        if (dj.de_ticket >= 0)
+          release_sys(p.de_ctr + static_cast<int64_t>(dj.de_ticket) * (p.n_layer + 1), layer, p.n_layer);
+      }
+    }
+  }
+}
+
+// Two consecutive content words of Full Block fb, word index w (even).
+__device__ __forceinline__ uint4 content_pair(uint64_t fb, uint64_t w, uint64_t seed_mix) {
+  const uint64_t a = splitmix64(((fb << 32) | w) ^ seed_mix);
+  const uint64_t b = splitmix64(((fb << 32) | (w + 1)) ^ seed_mix);
+  return make_uint4(static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32),
+                    static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32));
+}
+
+__global__ void __launch_bounds__(kThreads) kv_prefill_handoff(const __grid_constant__ HandoffParams p) {
+  const int64_t total = p.item_begin[p.n_jobs];
+  const int tid = threadIdx.x;
+  for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+    const int j = decode_job(p, item);
+    const dp_handoff_job& job = p.jobs[j];
+    const int64_t local = item - p.item_begin[j];
+    const int64_t per_layer = static_cast<int64_t>(job.n_blk) * p.n_chunk;
+    const int layer = static_cast<int>(local / per_layer);
+    const int64_t rem = local % per_layer;
+    const int blk = static_cast<int>(rem / p.n_chunk);
+    const int chunk = static_cast<int>(rem % p.n_chunk);
+    const int64_t tok0 = static_cast<int64_t>(blk) * p.block_tokens;
+    const int64_t lb = p.lb_bytes;
+    const int64_t hit_end = max(int64_t{0}, min(lb, (job.n_cached - tok0) * p.bpt));
+    const int64_t prompt_end = max(int64_t{0}, min(lb, (job.n_prompt - tok0) * p.bpt));
+    const int64_t beg = static_cast<int64_t>(chunk) * kChunkBytes;
+    const int64_t end = min(beg + kChunkBytes, prompt_end);
+    // the layer gate: layer l's hit KV must have landed before "computing" l
+    if (job.pe_ticket >= 0) {
+      if (tid == 0) {
+        const uint32_t* ctr = p.pe_ctr + static_cast<int64_t>(job.pe_ticket) * (p.n_layer + 1) + layer;
+        const uint64_t t0 = global_timer_ns();
+        while (true) {
+          uint32_t v;
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+          if (v >= job.pe_wait_items) break;
+          if (global_timer_ns() - t0 > p.timeout_ns) {  // watchdog: report, do not hang
+            atomicExch_system(p.err_flag, 1);
+            break;
+          }
+          __nanosleep(256);
+        }
+      }
+      __syncthreads();
+    }
+    const int64_t pe_off = layer * p.pe_stride + static_cast<int64_t>(job.pe_slot[blk]) * lb;
+    const int64_t de_off = layer * p.de_stride + static_cast<int64_t>(job.de_slot[blk]) * lb;
+    // hit part: PeToDe pushes it, MissMerge leaves it to the DE
+    const int64_t h1 = min(end, hit_end);
+    if (job.push_hit && h1 > beg) {
+      const uint4* src = reinterpret_cast<const uint4*>(p.pe_pool + pe_off + beg);
+      uint4* dst = reinterpret_cast<uint4*>(p.de_pool + de_off + beg);
+      const int n16 = static_cast<int>((h1 - beg) >> 4);
+      for (int base = 0; base < n16; base += kThreads * kUnroll) {
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int i = base + u * kThreads + tid;
+          if (i < n16) v[u] = __ldcg(src + i);  // landed by another GPU: bypass L1
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int i = base + u * kThreads + tid;
+          if (i < n16) st_v4(dst + i, v[u]);
+        }
+      }
+    }
+    // miss part: the prefill stand-in's KV for tokens [C, C+A), written into
+    // the PE pool (its KV cache) and pushed to the DE pool
+    const int64_t m0 = max(beg, hit_end);
+    if (end > m0) {
+      const uint64_t fb = static_cast<uint64_t>(job.src_fb[blk]);
+      const uint64_t w_base = static_cast<uint64_t>((layer * lb) >> 3);
+      uint4* pe_dst = reinterpret_cast<uint4*>(p.pe_pool + pe_off);
+      uint4* de_dst = reinterpret_cast<uint4*>(p.de_pool + de_off);
+      for (int64_t i = (m0 >> 4) + tid; i < (end >> 4); i += kThreads) {
+        const uint4 v = content_pair(fb, w_base + 2 * static_cast<uint64_t>(i), p.seed_mix);
+        st_v4(pe_dst + i, v);
+        st_v4(de_dst + i, v);
+      }
+    }
+    if (job.de_ticket >= 0) {
+      __syncthreads();
+      if (tid == 0)
+        release_sys(p.de_ctr + static_cast<int64_t>(job.de_ticket) * (p.n_layer + 1), layer, p.n_layer);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int dp_h2d_push_p2p_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* src,
+                         const dp_dual_job* jobs, int32_t n_jobs, dp_stream stream) {
+  if (!pe_view || !de_pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0)
+    return fail(DP_EINVAL, "push_p2p_dual: null argument");
+  if (pe_view->owner) return fail(DP_EINVAL, "push_p2p_dual: PE destination must be a peer view");
+  if (!de_pool->owner) return fail(DP_EINVAL, "push_p2p_dual: decode pool must be the local pool");
+  if (pe_view->device != de_pool->device)
+    return fail(DP_EINVAL, "push_p2p_dual: the PE view must be mapped on the decode pool's device");
+  if (!geom_equal(pe_view->geom, src->geom) || !geom_equal(de_pool->geom, src->geom))
+    return fail(DP_EINVAL, "push_p2p_dual: geometry differs");
+  const dp_kv_geom& g = src->geom;
+  DeviceGuard guard(de_pool->device);
+  DualParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.store = src->host;
+  p.pe_pool = pe_view->base;
+  p.pe_ctr = pe_view->counters;
+  p.de_pool = de_pool->base;
+  p.de_ctr = de_pool->counters;
+  p.lb_bytes = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
+  p.fb_bytes = p.lb_bytes * g.n_layer;
+  p.bpt = g.bytes_per_token_layer;
+  p.pe_stride = p.lb_bytes * pe_view->n_slots;
+  p.de_stride = p.lb_bytes * de_pool->n_slots;
+  p.n_layer = g.n_layer;
+  p.block_tokens = g.block_tokens;
+  p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
+  const int dev_cap = de_pool->device < kMaxDevices ? g_gather_ctas[de_pool->device] : 0;
+  const int grid_cap = dev_cap > 0 ? dev_cap : sm_count(de_pool->device) * 4;
+  auto s = static_cast<cudaStream_t>(stream);
+  for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_DUAL_JOBS_PER_LAUNCH) {
+    const int32_t nj = std::min<int32_t>(DP_MAX_DUAL_JOBS_PER_LAUNCH, n_jobs - j0);
+    p.n_jobs = 0;
+    int64_t items = 0;
+    for (int32_t j = 0; j < nj; ++j) {
+      const dp_dual_job& dj = jobs[j0 + j];
+      const dp_job& job = dj.pe;
+      const int64_t need = (job.n_tokens + g.block_tokens - 1) / g.block_tokens;
+      if (job.n_tokens < 0 || job.n_blk != need || job.layer_begin < 0 || job.layer_end > g.n_layer ||
+          job.layer_begin > job.layer_end || job.ticket >= pe_view->n_tickets ||
+          dj.de_ticket >= de_pool->n_tickets || (job.n_blk > 0 && (!job.src_fb || !job.dst_slot || !dj.de_slot)))
+        return fail(DP_EINVAL, "push_p2p_dual: job " + std::to_string(j0 + j) + " out of range");
+      const int64_t n = static_cast<int64_t>(job.n_blk) * p.n_chunk * (job.layer_end - job.layer_begin);
+      if (n == 0) continue;
+      p.jobs[p.n_jobs] = dj;
+      p.item_begin[p.n_jobs] = items;
+      ++p.n_jobs;
+      items += n;
+    }
+    p.item_begin[p.n_jobs] = items;
+    if (items == 0) continue;
+    kv_gather_dual<<<static_cast<int>(std::min<int64_t>(items, grid_cap)), kThreads, 0, s>>>(p);
+    DP_CUDA(cudaGetLastError());
+  }
+  return DP_OK;
+}
+
+int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job* jobs,
+                       int32_t n_jobs, uint64_t seed, int32_t timeout_ms, dp_stream stream) {
+  if (!pe_pool || !de_view || (n_jobs > 0 && !jobs) || n_jobs < 0)
+    return fail(DP_EINVAL, "prefill_handoff: null argument");
+  if (!pe_pool->owner) return fail(DP_EINVAL, "prefill_handoff: the PE pool must be local");
+  if (de_view->owner) return fail(DP_EINVAL, "prefill_handoff: the DE pool must be a peer view");
+  if (de_view->device != pe_pool->device)
+    return fail(DP_EINVAL, "prefill_handoff: the DE view must be mapped on the PE's device");
+  if (!geom_equal(pe_pool->geom, de_view->geom)) return fail(DP_EINVAL, "prefill_handoff: geometry differs");
+  if (timeout_ms <= 0) return fail(DP_EINVAL, "prefill_handoff: timeout must be > 0");
+  const dp_kv_geom& g = pe_pool->geom;
+  DeviceGuard guard(pe_pool->device);
+  HandoffParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.pe_pool = pe_pool->base;
+  p.de_pool = de_view->base;
+  p.pe_ctr = pe_pool->counters;
+  p.de_ctr = de_view->counters;
+  p.lb_bytes = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
+  p.bpt = g.bytes_per_token_layer;
+  p.pe_stride = p.lb_bytes * pe_pool->n_slots;
+  p.de_stride = p.lb_bytes * de_view->n_slots;
+  p.err_flag = pe_pool->err_host;
+  p.timeout_ns = static_cast<uint64_t>(timeout_ms) * 1000000ull;
+  p.seed_mix = seed * kSeedMul;
+  p.n_layer = g.n_layer;
+  p.block_tokens = g.block_tokens;
+  p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
+  const int grid_cap = sm_count(pe_pool->device);
+  auto s = static_cast<cudaStream_t>(stream);
+  for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_HANDOFF_JOBS_PER_LAUNCH) {
+    const int32_t nj = std::min<int32_t>(DP_MAX_HANDOFF_JOBS_PER_LAUNCH, n_jobs - j0);
+    p.n_jobs = 0;
+    int64_t items = 0;
+    for (int32_t j = 0; j < nj; ++j) {
+      const dp_handoff_job& job = jobs[j0 + j];
+      const int64_t need = (job.n_prompt + g.block_tokens - 1) / g.block_tokens;
+      if (job.n_cached < 0 || job.n_prompt < job.n_cached || job.n_blk != need ||
+          job.pe_ticket >= pe_pool->n_tickets || job.de_ticket >= de_view->n_tickets ||
+          (job.n_blk > 0 && (!job.src_fb || !job.pe_slot || !job.de_slot)))
+        return fail(DP_EINVAL, "prefill_handoff: job " + std::to_string(j0 + j) + " out of range");
+      const int64_t n = static_cast<int64_t>(job.n_blk) * p.n_chunk * g.n_layer;
+      if (n == 0) continue;
+      p.jobs[p.n_jobs] = job;
+      p.item_begin[p.n_jobs] = items;
+      ++p.n_jobs;
+      items += n;
+    }
+    p.item_begin[p.n_jobs] = items;
+    if (items == 0) continue;
+    kv_prefill_handoff<<<static_cast<int>(std::min<int64_t>(items, grid_cap)), kThreads, 0, s>>>(p);
+    DP_CUDA(cudaGetLastError());
+  }
+  return DP_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,143 @@
+"""GPU parity of the PD handoff kernels through the C ABI:
+the DE read path fused with DecodeH2D (dp_h2d_push_p2p_dual) and K3
+(dp_prefill_handoff: prefill stand-in + PeToDe / MissMerge per layer).
+
+After a request's handoff, both the PE pool and the DE decode pool must hold
+the whole prompt KV [0, C+A) of every prompt block, byte for byte the content
+formula of oracle/kvref.c (the hit part comes from storage, the miss part is
+what the prefill stand-in writes: the same formula, i.e. what storage will
+hold once the turn is persisted)."""
+
+import numpy as np
+import pytest
+
+from oracle import refpy
+from paper_2602_21548_b200 import abi
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+SEED = 9
+
+
+def dev(x, device, dtype):
+    import torch
+    return torch.tensor(np.asarray(x, dtype=dtype), device=f"cuda:{device}")
+
+
+def sync_all():
+    import torch
+    for d in range(torch.cuda.device_count()):
+        torch.cuda.synchronize(d)
+
+
+def check_prompt(pool, g_ref, fbs, slots, n_prompt, T, b, L):
+    for k, (f, s) in enumerate(zip(fbs, slots)):
+        n = min(T, n_prompt - k * T)
+        for layer in range(L):
+            got = pool.copy_out(layer, int(s), n * b)
+            want = refpy.layer_block(g_ref, SEED, int(f), layer, n).tobytes()
+            assert got == want, (k, layer)
+
+
+@pytest.mark.parametrize("L,T,b", [(8, 64, 576), (4, 64, 4096)])
+@pytest.mark.parametrize("C,A", [(64 * 5 + 10, 300), (64 * 3, 64), (0, 200), (130, 0)])
+def test_de_path_dual_then_missmerge(two_gpus, L, T, b, C, A):
+    """DE read path: the DE reads the hit blocks once (dual: PE pool + its own
+    decode pool), the PE gates each layer on them, writes the miss KV and
+    pushes only the miss part (MissMerge)."""
+    g = abi.geom(L, T, b)
+    P = C + A
+    n_hit, n_prompt = -(-C // T), -(-P // T)
+    rng = np.random.default_rng(C * 7 + A)
+    st_de = abi.Store(1, g, 40, SEED)
+    pe_pool = abi.Pool(0, g, 32, 2)
+    de_pool = abi.Pool(1, g, 32, 2)
+    pe_view_on_de = pe_pool.peer_view(1)
+    de_view_on_pe = de_pool.peer_view(0)
+    try:
+        fbs = (rng.integers(0, 40 - n_prompt) + np.arange(n_prompt)).astype(np.int64)
+        pe_slots = rng.permutation(32)[:n_prompt].astype(np.int32)
+        de_slots = rng.permutation(32)[:n_prompt].astype(np.int32)
+        keep = [dev(fbs if n_prompt else [0], 1, np.int64), dev(pe_slots if n_prompt else [0], 1, np.int32),
+                dev(de_slots if n_prompt else [0], 1, np.int32)]
+        dj = (abi.DualJob * 1)()
+        dj[0].pe = abi.Job(keep[0].data_ptr(), keep[1].data_ptr(), C, n_hit, 0, L, 0)
+        dj[0].de_slot = keep[2].data_ptr()
+        dj[0].de_ticket = 0
+        on_pe = [dev(fbs if n_prompt else [0], 0, np.int64), dev(pe_slots if n_prompt else [0], 0, np.int32),
+                 dev(de_slots if n_prompt else [0], 0, np.int32)]
+        items = abi.layer_items(g, n_hit)
+        hj = (abi.HandoffJob * 1)()
+        hj[0] = abi.HandoffJob(on_pe[0].data_ptr(), on_pe[1].data_ptr(), on_pe[2].data_ptr(), C, P,
+                               n_prompt, 0, 0 if C else -1, items, 0, 0)
+        # K3 first: it must block on the dual gather's per-layer releases
+        abi.prefill_handoff(pe_pool, de_view_on_pe, hj, 1, SEED, timeout_ms=20000)
+        abi.push_p2p_dual(pe_view_on_de, de_pool, st_de, dj, 1)
+        sync_all()
+        assert abi.wait_status(pe_pool) == abi.DP_OK
+        gr = refpy.geom(L, T, b)
+        check_prompt(pe_pool, gr, fbs, pe_slots, P, T, b, L)
+        check_prompt(de_pool, gr, fbs, de_slots, P, T, b, L)
+        per_block = abi.layer_items(g, 1)
+        want_layer = (n_hit + n_prompt) * per_block
+        abi.wait_layer(de_pool, 0, L, want_layer * L, timeout_ms=2000)
+        abi.wait_layer(de_pool, 0, L - 1, want_layer, timeout_ms=2000)
+        sync_all()
+        assert abi.wait_status(de_pool) == abi.DP_OK
+    finally:
+        for x in (de_view_on_pe, pe_view_on_de, de_pool, pe_pool, st_de):
+            x.close()
+
+
+@pytest.mark.parametrize("C,A", [(64 * 7 + 33, 429), (64 * 2, 1), (0, 64 * 3 + 5)])
+def test_pe_path_load_then_petode(two_gpus, C, A):
+    """PE read path: K1 loads the hit KV into the PE pool; K3 (stream-ordered
+    after it) writes the miss KV and pushes the whole prompt (PeToDe)."""
+    L, T, b = 8, 64, 576
+    g = abi.geom(L, T, b)
+    P = C + A
+    n_hit, n_prompt = -(-C // T), -(-P // T)
+    rng = np.random.default_rng(P)
+    st_pe = abi.Store(0, g, 40, SEED)
+    pe_pool = abi.Pool(0, g, 32, 1)
+    de_pool = abi.Pool(1, g, 32, 1)
+    de_view = de_pool.peer_view(0)
+    try:
+        fbs = (rng.integers(0, 40 - n_prompt) + np.arange(n_prompt)).astype(np.int64)
+        pe_slots = rng.permutation(32)[:n_prompt].astype(np.int32)
+        de_slots = rng.permutation(32)[:n_prompt].astype(np.int32)
+        t = [dev(fbs, 0, np.int64), dev(pe_slots, 0, np.int32), dev(de_slots, 0, np.int32)]
+        if n_hit:
+            abi.h2d_layer_gather(pe_pool, st_pe, abi.make_jobs(
+                [(t[0].data_ptr(), t[1].data_ptr(), C, n_hit, 0, L, -1)]), 1)
+        hj = (abi.HandoffJob * 1)()
+        hj[0] = abi.HandoffJob(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), C, P, n_prompt, 1, -1, 0, 0, 0)
+        abi.prefill_handoff(pe_pool, de_view, hj, 1, SEED)  # same (legacy) stream: ordered after K1
+        sync_all()
+        gr = refpy.geom(L, T, b)
+        check_prompt(pe_pool, gr, fbs, pe_slots, P, T, b, L)
+        check_prompt(de_pool, gr, fbs, de_slots, P, T, b, L)
+        abi.wait_layer(de_pool, 0, L, n_prompt * L, timeout_ms=2000)
+        sync_all()
+        assert abi.wait_status(de_pool) == abi.DP_OK
+    finally:
+        for x in (de_view, de_pool, pe_pool, st_pe):
+            x.close()
+
+
+def test_handoff_gate_watchdog(two_gpus):
+    """A layer whose hit KV never lands trips the watchdog instead of hanging."""
+    L, T, b = 2, 64, 576
+    g = abi.geom(L, T, b)
+    pe_pool = abi.Pool(0, g, 4, 1)
+    de_pool = abi.Pool(1, g, 4, 1)
+    de_view = de_pool.peer_view(0)
+    try:
+        t = [dev([0, 1], 0, np.int64), dev([0, 1], 0, np.int32), dev([0, 1], 0, np.int32)]
+        hj = (abi.HandoffJob * 1)()
+        hj[0] = abi.HandoffJob(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), 64, 100, 2, 0, 0, 1, 0, 0)
+        abi.prefill_handoff(pe_pool, de_view, hj, 1, SEED, timeout_ms=50)
+        sync_all()
+        assert abi.wait_status(pe_pool) == abi.DP_ETIMEOUT
+    finally:
+        for x in (de_view, de_pool, pe_pool):
+            x.close()
