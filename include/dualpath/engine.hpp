@@ -46,6 +46,11 @@ struct ExecOptions {
   // PE-path loads (K1): 0 = SM gather kernel, 1 = copy engine (no SMs: the
   // isolation mode while the PE computes, and the faster PCIe read path)
   std::int32_t k1_mode = 0;
+  // PD handoff: every request's prompt KV also ends in its
+  // DE's decode pool — prefill stand-in + PeToDe / MissMerge per layer (K3)
+  // and the DE read path fused with DecodeH2D (dual store)
+  bool handoff = false;
+  std::int32_t de_pool_slots = 0;      // per DE decode pool; 0 = auto (4x plan peak)
 };
 
 // One request's hit-KV transfer (all layers), in global execution order.
@@ -66,6 +71,18 @@ struct LoadJob {
   std::vector<std::uint32_t> pred_targets; // reuses (written by another engine), and their
                                            // all-layer landed-item targets
   bool fence = false;  // reuses a slot this reader wrote earlier: must not share a launch
+  // ---- PD handoff (ExecOptions::handoff) ----
+  int de = -1;                   // the request's decode engine
+  std::int64_t prompt = 0;       // C + A
+  std::int32_t n_pblk = 0;       // prompt blocks (PE slots cover these in handoff mode)
+  std::int64_t ho_off = 0;       // offset of the prompt tables in the PE's handoff tables
+  std::int32_t de_ticket = -1;   // decode-pool row
+  std::vector<std::int32_t> k3_waits;      // jobs (same PE) whose K3 must finish before this
+                                           // job's K1 reuses their PE slots (event waits)
+  std::vector<std::int32_t> pe_done_preds; // PE done-rows (ticket + n_tickets) a DE-path
+  std::vector<std::uint32_t> pe_done_targets;  // job's dual gather waits for (PE slot reuse)
+  std::vector<std::int32_t> de_preds;      // decode-pool rows of the previous occupants of
+  std::vector<std::uint32_t> de_pred_targets;  // this job's DE slots
 };
 
 struct ExecPlan {
@@ -91,6 +108,19 @@ struct ExecPlan {
 
   std::int64_t fb_of(int traj, std::int64_t block) const;  // storage mapping
   std::int64_t fb_stride = 1;                               // blocks per session
+
+  // ---- PD handoff ----
+  bool handoff = false;
+  std::int32_t de_pool_slots = 0;
+  std::int32_t de_peak_slots = 0;
+  std::vector<std::int32_t> n_de_tickets;                  // per engine (0 for PEs)
+  std::vector<std::vector<int>> by_de;                     // job indices per decode engine
+  std::vector<std::vector<std::int64_t>> ho_src_fb;        // per PE: prompt blocks' Full Blocks
+  std::vector<std::vector<std::int32_t>> ho_pe_slot;       // per PE: prompt blocks' PE slots
+  std::vector<std::vector<std::int32_t>> ho_de_slot;       // per PE: prompt blocks' DE slots
+  std::vector<std::vector<std::int32_t>> dual_de_slot;     // per reader: hit blocks' DE slots
+  std::int64_t handoff_bytes = 0;  // pushed by K3: (C+A)*L*b PE path, A*L*b DE path
+  std::uint32_t de_total_items(const LoadJob& j) const;    // decode-pool row target (all layers)
 };
 
 // Builds the executor plan from planner output.  Requests with C = 0 move no
@@ -126,10 +156,13 @@ class EngineRuntime {
   int device() const { return device_; }
   bool is_pe() const { return engine_ < plan_->n_pe; }
 
-  // PE pool export / import (cross-process) or same-process peer attach.
+  // Pool export / import (cross-process) or same-process peer attach.  Every
+  // PE exports its prefill pool; with PD handoff every DE exports its decode
+  // pool too, and attach_* of a DE engine id gives a PE its view of it.
   dp_pool_handle export_pool() const;
-  void attach_peer(int pe_engine, const dp_pool_handle& handle);
-  void attach_peer_local(int pe_engine, const EngineRuntime& pe);
+  void attach_peer(int engine, const dp_pool_handle& handle);
+  void attach_peer_local(int engine, const EngineRuntime& other);
+  bool has_pool() const { return pool_ != nullptr; }
 
   // Zero this PE's landed counters (call on every PE, then barrier, before a step).
   void reset_counters();
@@ -165,6 +198,24 @@ class EngineRuntime {
   std::int32_t* d_pred_tickets_ = nullptr;  // hazard waits, flattened per job
   std::uint32_t* d_pred_targets_ = nullptr;
   std::vector<std::int64_t> pred_off_;      // per job index in by_reader: offset into preds
+
+  // ---- PD handoff ----
+  StepResult run_step_handoff();
+  void upload_handoff_tables();
+  void* stream_h_ = nullptr;                // PE: K3 (prefill stand-in + handoff) stream
+  std::vector<void*> ev_load_, ev_k3_;      // PE: per job in by_pe order
+  std::vector<int> pe_local_;               // job index -> position in by_pe (or -1)
+  std::vector<dp_pool*> de_views_;          // PE: per engine id: view of that DE's pool
+  std::int64_t* d_ho_src_ = nullptr;
+  std::int32_t* d_ho_pe_ = nullptr;
+  std::int32_t* d_ho_de_ = nullptr;
+  std::int32_t* d_dual_de_ = nullptr;
+  std::int32_t* d_wt_ = nullptr;            // flattened wait lists (tickets / targets)
+  std::uint32_t* d_wg_ = nullptr;
+  std::vector<std::int64_t> de_wait_off_;   // per job: offset of its de_preds in d_wt_
+  std::vector<std::int64_t> pe_done_off_;   // per job: offset of its pe_done_preds
+  std::int64_t final_wait_off_ = 0;         // DE: all own tickets (decode-ready gate)
+  std::int32_t final_wait_n_ = 0;
 };
 
 // Runs run_step() of several same-process engines concurrently (one host

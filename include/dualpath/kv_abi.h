@@ -162,7 +162,8 @@ typedef struct dp_handoff_job {
                               is processed (the maybe_start_compute gate), or -1 (stream-ordered) */
   uint32_t pe_wait_items;  /* per-layer items of the hit KV */
   int32_t de_ticket;       /* DE pool row released per layer, or -1 */
-  int32_t reserved;
+  int32_t pe_done_ticket;  /* PE pool row released per item once its work (reads of the PE
+                              pool included) is done, or -1: slot-reuse hazards */
 } dp_handoff_job;
 
 #define DP_MAX_DUAL_JOBS_PER_LAUNCH 48

@@ -46,7 +46,7 @@ class HandoffJob(ctypes.Structure):
                 ("n_cached", ctypes.c_int64), ("n_prompt", ctypes.c_int64), ("n_blk", ctypes.c_int32),
                 ("push_hit", ctypes.c_int32), ("pe_ticket", ctypes.c_int32),
                 ("pe_wait_items", ctypes.c_uint32), ("de_ticket", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("pe_done_ticket", ctypes.c_int32)]
 
 
 class PoolHandle(ctypes.Structure):

@@ -331,6 +331,8 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("storage_cap_per_engine", &dualpath::ExecOptions::storage_cap_per_engine)
       .def_readwrite("pace_scale", &dualpath::ExecOptions::pace_scale)
       .def_readwrite("k1_mode", &dualpath::ExecOptions::k1_mode)
+      .def_readwrite("handoff", &dualpath::ExecOptions::handoff)
+      .def_readwrite("de_pool_slots", &dualpath::ExecOptions::de_pool_slots)
       .def_readwrite("store_fb", &dualpath::ExecOptions::store_fb)
       .def_readwrite("store_bytes_max", &dualpath::ExecOptions::store_bytes_max)
       .def_readwrite("seed", &dualpath::ExecOptions::seed)
@@ -351,22 +353,40 @@ PYBIND11_MODULE(_core, m) {
       .def_readonly("hit_bytes", &dualpath::ExecPlan::hit_bytes)
       .def_readonly("prompt_tokens", &dualpath::ExecPlan::prompt_tokens)
       .def_readonly("requests", &dualpath::ExecPlan::requests)
+      .def_readonly("handoff", &dualpath::ExecPlan::handoff)
+      .def_readonly("handoff_bytes", &dualpath::ExecPlan::handoff_bytes)
+      .def_readonly("de_pool_slots", &dualpath::ExecPlan::de_pool_slots)
+      .def_readonly("de_peak_slots", &dualpath::ExecPlan::de_peak_slots)
+      .def_readonly("n_de_tickets", &dualpath::ExecPlan::n_de_tickets)
       .def("fb_of", &dualpath::ExecPlan::fb_of)
       .def("jobs", [](const dualpath::ExecPlan& x) {
-        // (req, traj, round, reader, pe, de_path, cached, n_blk, ticket, slots, src_fb, preds, fence)
+        // (req, traj, round, reader, pe, de_path, cached, n_blk, ticket, slots, src_fb, preds,
+        //  fence, de, prompt, n_pblk, de_ticket, pe_prompt_slots, de_slots, de_preds, k3_waits,
+        //  pe_done_preds)
         py::list out;
         for (const auto& j : x.jobs) {
           std::vector<std::int32_t> sl(x.slots[j.reader].begin() + j.blk_off,
                                        x.slots[j.reader].begin() + j.blk_off + j.n_blk);
           std::vector<std::int64_t> fb(x.src_fb[j.reader].begin() + j.blk_off,
                                        x.src_fb[j.reader].begin() + j.blk_off + j.n_blk);
-          out.append(py::make_tuple(j.req, j.traj, j.round, j.reader, j.pe, j.de_path, j.cached,
-                                    j.n_blk, j.ticket, sl, fb, j.preds, j.fence));
+          std::vector<std::int32_t> ps, dsl;
+          if (x.handoff) {
+            ps.assign(x.ho_pe_slot[j.pe].begin() + j.ho_off, x.ho_pe_slot[j.pe].begin() + j.ho_off + j.n_pblk);
+            dsl.assign(x.ho_de_slot[j.pe].begin() + j.ho_off, x.ho_de_slot[j.pe].begin() + j.ho_off + j.n_pblk);
+          } else {
+            ps = sl;
+          }
+          py::tuple t = py::make_tuple(j.req, j.traj, j.round, j.reader, j.pe, j.de_path, j.cached,
+                                       j.n_blk, j.ticket, sl, fb, j.preds);
+          py::tuple u = py::make_tuple(j.fence, j.de, j.prompt, j.n_pblk, j.de_ticket, ps, dsl,
+                                       j.de_preds, j.k3_waits, j.pe_done_preds);
+          out.append(py::reinterpret_steal<py::tuple>(PySequence_Concat(t.ptr(), u.ptr())));
         }
         return out;
       })
       .def("by_reader", [](const dualpath::ExecPlan& x, int e) { return x.by_reader.at(e); })
-      .def("by_pe", [](const dualpath::ExecPlan& x, int e) { return x.by_pe.at(e); });
+      .def("by_pe", [](const dualpath::ExecPlan& x, int e) { return x.by_pe.at(e); })
+      .def("by_de", [](const dualpath::ExecPlan& x, int e) { return x.by_de.at(e); });
 
   m.def(
       "build_exec_plan",
@@ -421,6 +441,7 @@ PYBIND11_MODULE(_core, m) {
       .def_property_readonly("engine", &dualpath::EngineRuntime::engine)
       .def_property_readonly("device", &dualpath::EngineRuntime::device)
       .def_property_readonly("is_pe", &dualpath::EngineRuntime::is_pe)
+      .def_property_readonly("has_pool", &dualpath::EngineRuntime::has_pool)
       .def("export_pool", [](const dualpath::EngineRuntime& e) { return handle_bytes(e.export_pool()); })
       .def("attach_peer", [](dualpath::EngineRuntime& e, int pe, const py::bytes& h) {
         e.attach_peer(pe, handle_from(h));

@@ -41,10 +41,88 @@ T* upload(const std::vector<T>& v) {
   return d;
 }
 
+// Free-slot queues of one pool.  Freed slots go back to a queue of the
+// engine that last wrote them; an allocation takes, in order, slots its own
+// writer last wrote (ordered by its stream), never-used slots, then other
+// writers' slots (a cross-GPU hazard).  FIFO within each queue.
+struct SlotQueues {
+  std::deque<std::int32_t> fresh;
+  std::vector<std::deque<std::int32_t>> by_writer;
+  std::vector<std::int32_t> owner;  // slot -> job index of its last occupant
+
+  SlotQueues(std::int32_t n_slots, int n_writers) : by_writer(n_writers), owner(n_slots, -1) {
+    for (std::int32_t s = 0; s < n_slots; ++s) fresh.push_back(s);
+  }
+  std::int32_t take(int writer) {
+    std::deque<std::int32_t>* src = nullptr;
+    if (!by_writer[writer].empty()) {
+      src = &by_writer[writer];
+    } else if (!fresh.empty()) {
+      src = &fresh;
+    } else {
+      for (auto& q : by_writer)
+        if (!q.empty()) {
+          src = &q;
+          break;
+        }
+    }
+    if (!src) throw std::logic_error("build_exec_plan: slot allocator ran dry below the peak");
+    const std::int32_t s = src->front();
+    src->pop_front();
+    return s;
+  }
+};
+
+struct TimedEv {
+  double t;
+  int kind;  // 0 = free, 1 = alloc
+  int req;
+  int job;
+};
+
+void sort_events(std::vector<TimedEv>& evs) {
+  std::sort(evs.begin(), evs.end(), [](const TimedEv& a, const TimedEv& b) {
+    if (a.t != b.t) return a.t < b.t;
+    if (a.kind != b.kind) return a.kind < b.kind;
+    return a.req < b.req;
+  });
+}
+
+// Peak live blocks over a key (PE or DE) for alloc/free events.
+std::int64_t peak_blocks(const std::vector<TimedEv>& evs, int n_keys,
+                         const std::vector<int>& key_of_job,
+                         const std::vector<std::int32_t>& blocks_of_job) {
+  std::vector<std::int64_t> live(n_keys, 0);
+  std::int64_t peak = 0;
+  for (const TimedEv& e : evs) {
+    const int k = key_of_job[e.job];
+    live[k] += e.kind == 1 ? blocks_of_job[e.job] : -blocks_of_job[e.job];
+    peak = std::max(peak, live[k]);
+  }
+  return peak;
+}
+
+std::int32_t size_pool(std::int32_t requested, std::int64_t peak, std::int64_t slot_cap,
+                       const char* what) {
+  const std::int64_t n = requested > 0
+                             ? requested
+                             : std::min<std::int64_t>(slot_cap, std::max<std::int64_t>(1, 4 * peak));
+  if (n < peak)
+    throw std::invalid_argument(std::string("build_exec_plan: ") + what + " of " + std::to_string(n) +
+                                " slots is below the plan's peak of " + std::to_string(peak) +
+                                " live blocks");
+  return static_cast<std::int32_t>(n);
+}
+
 }  // namespace
 
 std::int64_t ExecPlan::fb_of(int traj, std::int64_t block) const {
   return (static_cast<std::int64_t>(traj) * fb_stride + block) % store_fb;
+}
+
+std::uint32_t ExecPlan::de_total_items(const LoadJob& j) const {
+  const std::int64_t blocks = (j.de_path ? j.n_blk : 0) + j.n_pblk;
+  return static_cast<std::uint32_t>(blocks * items_per_block * cfg.n_layer);
 }
 
 ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
@@ -54,6 +132,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
   ExecPlan x;
   x.cfg = cfg;
   x.opt = opt;
+  x.handoff = opt.handoff;
   x.n_engines = cfg.total_engines();
   x.n_pe = cfg.prefill_nodes * cfg.engines_per_node;
   x.geom = {cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer};
@@ -61,6 +140,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
   check(dp_layer_items(&x.geom, 1, &x.items_per_block), "build_exec_plan");
   const std::int64_t fb_bytes = cfg.full_block_bytes();
   const std::int64_t T = cfg.block_size_tokens;
+  const std::int64_t L = cfg.n_layer;
 
   x.fb_stride = 1;
   for (const auto& t : trajectories)
@@ -72,20 +152,22 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     const std::int64_t cap = std::max<std::int64_t>(1, opt.store_bytes_max / fb_bytes);
     x.store_fb = std::max<std::int64_t>(1, std::min(want, cap));
   }
+  if (!opt.storage_cap_per_engine.empty() &&
+      static_cast<int>(opt.storage_cap_per_engine.size()) != x.n_engines)
+    throw std::invalid_argument("build_exec_plan: storage_cap_per_engine needs one entry per engine");
 
-  // jobs: every request with cached KV that reached the hit transfer
-  struct Ev {
-    double t;
-    int kind;  // 0 = free, 1 = alloc
-    int req;
-    int job;
-  };
-  std::vector<Ev> evs;
+  // jobs: every request with cached KV that reached the hit transfer (and,
+  // with the handoff, every request that reached prefill)
+  std::vector<TimedEv> pe_evs, de_evs;
   std::vector<LoadJob> jobs;
+  std::vector<int> pe_of, de_of;
+  std::vector<std::int32_t> pblocks, dblocks;
   for (const auto& r : plan.requests) {
     x.prompt_tokens += r.cached + r.append;
     ++x.requests;
-    if (r.cached <= 0 || r.pe < 0 || r.t_read_done < 0) continue;
+    if (r.pe < 0 || r.t_read_done < 0) continue;
+    if (r.cached <= 0 && !x.handoff) continue;
+    if (x.handoff && r.de < 0) continue;
     if (r.traj_index < 0 || static_cast<std::size_t>(r.traj_index) >= trajectories.size())
       throw std::invalid_argument("build_exec_plan: plan does not match the trajectories");
     LoadJob j;
@@ -93,132 +175,156 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     j.traj = r.traj_index;
     j.round = r.round;
     j.pe = r.pe;
+    j.de = r.de;
     j.de_path = r.path == pdsim::ReadPath::DEPath;
     j.reader = j.de_path ? r.de : r.pe;
     j.cached = r.cached;
+    j.prompt = r.cached + r.append;
     j.n_blk = static_cast<std::int32_t>((r.cached + T - 1) / T);
+    j.n_pblk = x.handoff ? static_cast<std::int32_t>((j.prompt + T - 1) / T) : j.n_blk;
     j.t_admit = r.t_admit;
     j.t_read_done = r.t_read_done;
     const int idx = static_cast<int>(jobs.size());
     jobs.push_back(std::move(j));
-    evs.push_back({r.t_read_done, 1, r.request_id, idx});
-    if (r.t_pe_release >= 0) evs.push_back({r.t_pe_release, 0, r.request_id, idx});
-  }
-  std::sort(evs.begin(), evs.end(), [](const Ev& a, const Ev& b) {
-    if (a.t != b.t) return a.t < b.t;
-    if (a.kind != b.kind) return a.kind < b.kind;
-    return a.req < b.req;
-  });
-
-  // pass 1: peak live blocks per PE
-  {
-    std::vector<std::int64_t> live(x.n_pe, 0);
-    std::int64_t peak = 0;
-    for (const Ev& e : evs) {
-      const LoadJob& j = jobs[e.job];
-      live[j.pe] += e.kind == 1 ? j.n_blk : -j.n_blk;
-      peak = std::max(peak, live[j.pe]);
+    pe_of.push_back(r.pe);
+    de_of.push_back(std::max(0, r.de));
+    pblocks.push_back(jobs.back().n_pblk);
+    dblocks.push_back(jobs.back().n_pblk);
+    pe_evs.push_back({r.t_read_done, 1, r.request_id, idx});
+    if (r.t_pe_release >= 0) pe_evs.push_back({r.t_pe_release, 0, r.request_id, idx});
+    if (x.handoff) {
+      de_evs.push_back({r.t_read_done, 1, r.request_id, idx});
+      if (r.t_done >= 0) de_evs.push_back({r.t_done, 0, r.request_id, idx});
     }
-    x.peak_slots = static_cast<std::int32_t>(peak);
   }
+  sort_events(pe_evs);
+  sort_events(de_evs);
   const std::int64_t slot_cap = std::max<std::int64_t>(1, opt.pool_bytes_max / fb_bytes);
-  if (opt.pool_slots > 0) {
-    x.pool_slots = opt.pool_slots;
-  } else {
-    x.pool_slots = static_cast<std::int32_t>(
-        std::min<std::int64_t>(slot_cap, std::max<std::int64_t>(1, 4 * static_cast<std::int64_t>(x.peak_slots))));
+  x.peak_slots = static_cast<std::int32_t>(peak_blocks(pe_evs, x.n_engines, pe_of, pblocks));
+  x.pool_slots = size_pool(opt.pool_slots, x.peak_slots, slot_cap, "PE pool");
+  if (x.handoff) {
+    x.de_peak_slots = static_cast<std::int32_t>(peak_blocks(de_evs, x.n_engines, de_of, dblocks));
+    x.de_pool_slots = size_pool(opt.de_pool_slots, x.de_peak_slots, slot_cap, "DE decode pool");
   }
-  if (!opt.storage_cap_per_engine.empty() &&
-      static_cast<int>(opt.storage_cap_per_engine.size()) != x.n_engines)
-    throw std::invalid_argument("build_exec_plan: storage_cap_per_engine needs one entry per engine");
-  if (x.pool_slots < x.peak_slots)
-    throw std::invalid_argument("build_exec_plan: PE pool of " + std::to_string(x.pool_slots) +
-                                " slots is below the plan's peak of " +
-                                std::to_string(x.peak_slots) + " live blocks");
 
-  // pass 2: slot allocation in virtual time.  Freed slots go back to a queue
-  // of the engine that last wrote them; an allocation takes, in order, slots
-  // its own reader last wrote (ordered by its stream: only a launch boundary
-  // is needed), never-used slots, then other readers' slots (a cross-GPU
-  // hazard wait).  FIFO within each queue.
-  struct PeSlots {
-    std::deque<std::int32_t> fresh;
-    std::vector<std::deque<std::int32_t>> by_reader;
-    std::vector<std::int32_t> owner;  // slot -> job index of its last writer
-  };
-  std::vector<PeSlots> ps(x.n_pe);
-  for (int p = 0; p < x.n_pe; ++p) {
-    ps[p].owner.assign(x.pool_slots, -1);
-    ps[p].by_reader.assign(x.n_engines, {});
-    for (std::int32_t s = 0; s < x.pool_slots; ++s) ps[p].fresh.push_back(s);
-  }
-  auto take = [&](PeSlots& q, int reader) -> std::int32_t {
-    std::deque<std::int32_t>* src = nullptr;
-    if (!q.by_reader[reader].empty()) {
-      src = &q.by_reader[reader];
-    } else if (!q.fresh.empty()) {
-      src = &q.fresh;
-    } else {
-      for (int r = 0; r < x.n_engines && !src; ++r)
-        if (!q.by_reader[r].empty()) src = &q.by_reader[r];
-    }
-    if (!src) throw std::logic_error("build_exec_plan: slot allocator ran dry below the peak");
-    const std::int32_t s = src->front();
-    src->pop_front();
-    return s;
-  };
-  std::vector<std::vector<std::int32_t>> job_slots(jobs.size());
+  // pass 2: PE slot allocation in virtual time -> the global job order
+  std::vector<SlotQueues> pe_q;
+  for (int p = 0; p < x.n_pe; ++p) pe_q.emplace_back(x.pool_slots, x.n_engines);
+  std::vector<std::vector<std::int32_t>> pe_slots(jobs.size()), de_slots(jobs.size());
   x.n_tickets.assign(x.n_pe, 0);
   std::vector<int> order;
   order.reserve(jobs.size());
-  for (const Ev& e : evs) {
+  for (const TimedEv& e : pe_evs) {
     LoadJob& j = jobs[e.job];
-    PeSlots& q = ps[j.pe];
+    SlotQueues& q = pe_q[j.pe];
     if (e.kind == 0) {
-      for (std::int32_t s : job_slots[e.job]) q.by_reader[j.reader].push_back(s);
+      for (std::int32_t s : pe_slots[e.job]) q.by_writer[j.reader].push_back(s);
       continue;
     }
     j.ticket = x.n_tickets[j.pe]++;
-    auto& mine = job_slots[e.job];
-    mine.reserve(j.n_blk);
-    for (std::int32_t k = 0; k < j.n_blk; ++k) {
-      const std::int32_t s = take(q, j.reader);
+    auto& mine = pe_slots[e.job];
+    mine.reserve(j.n_pblk);
+    for (std::int32_t k = 0; k < j.n_pblk; ++k) {
+      const std::int32_t s = q.take(j.reader);
       mine.push_back(s);
       const std::int32_t prev = q.owner[s];
-      // same reader: stream order serialises launches, but items of one
-      // launch run concurrently, so the reuse must start a new launch
-      if (prev >= 0 && jobs[prev].reader == j.reader) j.fence = true;
-      if (prev >= 0 && jobs[prev].reader != j.reader &&
-          std::find(j.preds.begin(), j.preds.end(), jobs[prev].ticket) == j.preds.end()) {
-        j.preds.push_back(jobs[prev].ticket);
-        j.pred_targets.push_back(static_cast<std::uint32_t>(
-            static_cast<std::int64_t>(jobs[prev].n_blk) * x.items_per_block * cfg.n_layer));
-      }
       q.owner[s] = e.job;
+      if (prev < 0) continue;
+      const LoadJob& pj = jobs[prev];
+      if (!x.handoff) {
+        // same reader: stream order serialises launches, but items of one
+        // launch run concurrently, so the reuse must start a new launch
+        if (pj.reader == j.reader) {
+          j.fence = true;
+        } else if (std::find(j.preds.begin(), j.preds.end(), pj.ticket) == j.preds.end()) {
+          j.preds.push_back(pj.ticket);
+          j.pred_targets.push_back(static_cast<std::uint32_t>(
+              static_cast<std::int64_t>(pj.n_blk) * x.items_per_block * L));
+        }
+      } else if (!j.de_path) {
+        // the previous occupant's K3 (same PE, handoff stream) must be done
+        if (std::find(j.k3_waits.begin(), j.k3_waits.end(), prev) == j.k3_waits.end())
+          j.k3_waits.push_back(prev);
+      } else if (std::find(j.pe_done_preds.begin(), j.pe_done_preds.end(), pj.ticket) ==
+                 j.pe_done_preds.end()) {
+        j.pe_done_preds.push_back(pj.ticket);  // + n_tickets[pe] once known
+        j.pe_done_targets.push_back(
+            static_cast<std::uint32_t>(static_cast<std::int64_t>(pj.n_pblk) * x.items_per_block * L));
+      }
     }
     order.push_back(e.job);
+  }
+  std::vector<int> pos(jobs.size(), -1);  // old job index -> global position
+  for (std::size_t i = 0; i < order.size(); ++i) pos[order[i]] = static_cast<int>(i);
+
+  // pass 3 (handoff): decode-pool slots, allocated at t_read_done and freed
+  // when the request completes
+  if (x.handoff) {
+    std::vector<SlotQueues> de_q;
+    for (int d = 0; d < x.n_engines; ++d) de_q.emplace_back(d >= x.n_pe ? x.de_pool_slots : 0, 1);
+    x.n_de_tickets.assign(x.n_engines, 0);
+    for (const TimedEv& e : de_evs) {
+      LoadJob& j = jobs[e.job];
+      SlotQueues& q = de_q[j.de];
+      if (e.kind == 0) {
+        for (std::int32_t s : de_slots[e.job]) q.by_writer[0].push_back(s);
+        continue;
+      }
+      j.de_ticket = x.n_de_tickets[j.de]++;
+      for (std::int32_t k = 0; k < j.n_pblk; ++k) {
+        const std::int32_t s = q.take(0);
+        de_slots[e.job].push_back(s);
+        const std::int32_t prev = q.owner[s];
+        q.owner[s] = e.job;
+        if (prev < 0) continue;
+        const LoadJob& pj = jobs[prev];
+        if (pos[prev] >= pos[e.job])
+          throw std::logic_error("build_exec_plan: decode-slot predecessor is not earlier");
+        if (std::find(j.de_preds.begin(), j.de_preds.end(), pj.de_ticket) == j.de_preds.end()) {
+          j.de_preds.push_back(pj.de_ticket);
+          j.de_pred_targets.push_back(x.de_total_items(pj));
+        }
+      }
+    }
   }
 
   x.by_reader.assign(x.n_engines, {});
   x.by_pe.assign(x.n_pe, {});
+  x.by_de.assign(x.n_engines, {});
   x.src_fb.assign(x.n_engines, {});
   x.slots.assign(x.n_engines, {});
+  x.dual_de_slot.assign(x.n_engines, {});
+  x.ho_src_fb.assign(x.n_pe, {});
+  x.ho_pe_slot.assign(x.n_pe, {});
+  x.ho_de_slot.assign(x.n_pe, {});
   x.reader_bytes.assign(x.n_engines, 0);
   x.jobs.reserve(order.size());
   for (int old : order) {
     LoadJob j = std::move(jobs[old]);
+    for (int& w : j.k3_waits) w = pos[w];
     const int idx = static_cast<int>(x.jobs.size());
     auto& src = x.src_fb[j.reader];
     auto& dst = x.slots[j.reader];
     j.blk_off = static_cast<std::int64_t>(src.size());
     for (std::int32_t k = 0; k < j.n_blk; ++k) {
       src.push_back(x.fb_of(j.traj, k));
-      dst.push_back(job_slots[old][k]);
+      dst.push_back(pe_slots[old][k]);
+      if (x.handoff) x.dual_de_slot[j.reader].push_back(de_slots[old][k]);
+    }
+    if (x.handoff) {
+      j.ho_off = static_cast<std::int64_t>(x.ho_src_fb[j.pe].size());
+      for (std::int32_t k = 0; k < j.n_pblk; ++k) {
+        x.ho_src_fb[j.pe].push_back(x.fb_of(j.traj, k));
+        x.ho_pe_slot[j.pe].push_back(pe_slots[old][k]);
+        x.ho_de_slot[j.pe].push_back(de_slots[old][k]);
+      }
+      x.handoff_bytes += (j.de_path ? j.prompt - j.cached : j.prompt) * cfg.kv_bytes_per_token();
+      x.by_de[j.de].push_back(idx);
     }
     const std::int64_t bytes = j.cached * cfg.kv_bytes_per_token();
     x.reader_bytes[j.reader] += bytes;
     x.hit_bytes += bytes;
-    x.by_reader[j.reader].push_back(idx);
+    if (j.n_blk > 0) x.by_reader[j.reader].push_back(idx);
     x.by_pe[j.pe].push_back(idx);
     x.jobs.push_back(std::move(j));
   }
@@ -230,6 +336,7 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   if (!plan_) throw std::invalid_argument("EngineRuntime: null plan");
   if (engine < 0 || engine >= plan_->n_engines)
     throw std::invalid_argument("EngineRuntime: engine out of range");
+  const ExecPlan& x = *plan_;
   DeviceScope ds(device_);
   cudaStream_t s;
   check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -239,32 +346,49 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   check_cuda(cudaEventCreate(&b), "cudaEventCreate");
   ev_start_ = a;
   ev_end_ = b;
-  peers_.assign(plan_->n_engines, nullptr);
-  if (!plan_->by_reader[engine_].empty())
-    check(dp_store_create(device_, &plan_->geom, plan_->store_fb, plan_->opt.seed, &store_),
-          "dp_store_create");
+  peers_.assign(x.n_engines, nullptr);
+  de_views_.assign(x.n_engines, nullptr);
+  if (!x.by_reader[engine_].empty())
+    check(dp_store_create(device_, &x.geom, x.store_fb, x.opt.seed, &store_), "dp_store_create");
   if (is_pe()) {
-    check(dp_pool_create(device_, &plan_->geom, plan_->pool_slots,
-                         std::max<std::int32_t>(1, plan_->n_tickets[engine_]), &pool_),
-          "dp_pool_create");
+    // handoff: rows [0, n) hit-KV landed, rows [n, 2n) handoff (K3) done
+    const std::int32_t rows = std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff ? 2 : 1);
+    check(dp_pool_create(device_, &x.geom, x.pool_slots, rows, &pool_), "dp_pool_create");
     peers_[engine_] = pool_;
+  } else if (x.handoff) {
+    check(dp_pool_create(device_, &x.geom, x.de_pool_slots,
+                         std::max<std::int32_t>(1, x.n_de_tickets[engine_]), &pool_),
+          "dp_pool_create (decode pool)");
   }
-  upload_tables();
+  if (x.handoff) {
+    upload_handoff_tables();
+  } else {
+    upload_tables();
+  }
 }
 
 EngineRuntime::~EngineRuntime() {
   DeviceScope ds(device_);
   if (stream_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
+  if (stream_h_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_h_));
   for (int e = 0; e < static_cast<int>(peers_.size()); ++e)
     if (peers_[e] && peers_[e] != pool_) dp_pool_destroy(peers_[e]);
+  for (dp_pool* v : de_views_)
+    if (v) dp_pool_destroy(v);
   if (pool_) dp_pool_destroy(pool_);
   if (store_) dp_store_destroy(store_);
   for (void* p : {static_cast<void*>(d_src_), static_cast<void*>(d_slots_),
                   static_cast<void*>(d_wait_tickets_), static_cast<void*>(d_wait_targets_),
-                  static_cast<void*>(d_pred_tickets_), static_cast<void*>(d_pred_targets_)})
+                  static_cast<void*>(d_pred_tickets_), static_cast<void*>(d_pred_targets_),
+                  static_cast<void*>(d_ho_src_), static_cast<void*>(d_ho_pe_),
+                  static_cast<void*>(d_ho_de_), static_cast<void*>(d_dual_de_),
+                  static_cast<void*>(d_wt_), static_cast<void*>(d_wg_)})
     if (p) cudaFree(p);
+  for (void* e : ev_load_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  for (void* e : ev_k3_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   if (ev_start_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_start_));
   if (ev_end_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_end_));
+  if (stream_h_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_h_));
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
 }
 
@@ -299,28 +423,86 @@ void EngineRuntime::upload_tables() {
   }
 }
 
+void EngineRuntime::upload_handoff_tables() {
+  const ExecPlan& x = *plan_;
+  d_src_ = upload(x.src_fb[engine_]);
+  d_slots_ = upload(x.slots[engine_]);
+  d_dual_de_ = upload(x.dual_de_slot[engine_]);
+  std::vector<std::int32_t> wt;
+  std::vector<std::uint32_t> wg;
+  de_wait_off_.assign(x.jobs.size(), -1);
+  pe_done_off_.assign(x.jobs.size(), -1);
+  pe_local_.assign(x.jobs.size(), -1);
+  if (is_pe()) {
+    d_ho_src_ = upload(x.ho_src_fb[engine_]);
+    d_ho_pe_ = upload(x.ho_pe_slot[engine_]);
+    d_ho_de_ = upload(x.ho_de_slot[engine_]);
+    cudaStream_t h;
+    check_cuda(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking), "cudaStreamCreate");
+    stream_h_ = h;
+    const auto& mine = x.by_pe[engine_];
+    for (std::size_t i = 0; i < mine.size(); ++i) {
+      pe_local_[mine[i]] = static_cast<int>(i);
+      cudaEvent_t a, b;
+      check_cuda(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "cudaEventCreate");
+      ev_load_.push_back(a);
+      ev_k3_.push_back(b);
+      const LoadJob& j = x.jobs[mine[i]];
+      de_wait_off_[mine[i]] = static_cast<std::int64_t>(wt.size());
+      wt.insert(wt.end(), j.de_preds.begin(), j.de_preds.end());
+      wg.insert(wg.end(), j.de_pred_targets.begin(), j.de_pred_targets.end());
+    }
+  }
+  // DE read path (dual): waits on the PE done-rows and on its own decode pool
+  for (int ji : x.by_reader[engine_]) {
+    const LoadJob& j = x.jobs[ji];
+    if (!j.de_path) continue;
+    pe_done_off_[ji] = static_cast<std::int64_t>(wt.size());
+    for (std::int32_t t : j.pe_done_preds) wt.push_back(t + x.n_tickets[j.pe]);
+    wg.insert(wg.end(), j.pe_done_targets.begin(), j.pe_done_targets.end());
+    if (de_wait_off_[ji] < 0) {  // a DE reading for its own decode pool (always: reader == de)
+      de_wait_off_[ji] = static_cast<std::int64_t>(wt.size());
+      wt.insert(wt.end(), j.de_preds.begin(), j.de_preds.end());
+      wg.insert(wg.end(), j.de_pred_targets.begin(), j.de_pred_targets.end());
+    }
+  }
+  if (!is_pe()) {  // decode-ready gate: every row of this decode pool complete
+    final_wait_off_ = static_cast<std::int64_t>(wt.size());
+    for (int ji : x.by_de[engine_]) {
+      wt.push_back(x.jobs[ji].de_ticket);
+      wg.push_back(x.de_total_items(x.jobs[ji]));
+    }
+    final_wait_n_ = static_cast<std::int32_t>(x.by_de[engine_].size());
+  }
+  d_wt_ = upload(wt);
+  d_wg_ = upload(wg);
+}
+
 dp_pool_handle EngineRuntime::export_pool() const {
-  if (!pool_) throw std::logic_error("export_pool: engine is not a PE");
+  if (!pool_) throw std::logic_error("export_pool: this engine owns no pool");
   dp_pool_handle h;
   check(dp_pool_export(pool_, &h), "dp_pool_export");
   return h;
 }
 
-void EngineRuntime::attach_peer(int pe_engine, const dp_pool_handle& handle) {
-  if (pe_engine < 0 || pe_engine >= plan_->n_pe || pe_engine == engine_)
-    throw std::invalid_argument("attach_peer: bad PE engine");
-  if (peers_[pe_engine]) return;
+void EngineRuntime::attach_peer(int engine, const dp_pool_handle& handle) {
+  if (engine < 0 || engine >= plan_->n_engines || engine == engine_)
+    throw std::invalid_argument("attach_peer: bad engine");
+  auto& slot = engine < plan_->n_pe ? peers_[engine] : de_views_[engine];
+  if (slot) return;
   dp_pool* v = nullptr;
   check(dp_pool_import(device_, &handle, &v), "dp_pool_import");
-  peers_[pe_engine] = v;
+  slot = v;
 }
 
-void EngineRuntime::attach_peer_local(int pe_engine, const EngineRuntime& pe) {
-  if (pe_engine == engine_ || !pe.pool_) throw std::invalid_argument("attach_peer_local: bad PE");
-  if (peers_[pe_engine]) return;
+void EngineRuntime::attach_peer_local(int engine, const EngineRuntime& other) {
+  if (engine == engine_ || !other.pool_) throw std::invalid_argument("attach_peer_local: bad engine");
+  auto& slot = engine < plan_->n_pe ? peers_[engine] : de_views_[engine];
+  if (slot) return;
   dp_pool* v = nullptr;
-  check(dp_pool_peer_view(device_, pe.pool_, &v), "dp_pool_peer_view");
-  peers_[pe_engine] = v;
+  check(dp_pool_peer_view(device_, other.pool_, &v), "dp_pool_peer_view");
+  slot = v;
 }
 
 void EngineRuntime::reset_counters() {
@@ -332,6 +514,7 @@ void EngineRuntime::reset_counters() {
 
 StepResult EngineRuntime::run_step() {
   const ExecPlan& x = *plan_;
+  if (x.handoff) return run_step_handoff();
   DeviceScope ds(device_);
   auto s = static_cast<cudaStream_t>(stream_);
   StepResult res;
@@ -424,9 +607,148 @@ StepResult EngineRuntime::run_step() {
   return res;
 }
 
+// PD handoff step.  A PE runs two streams: the load stream (its own reads,
+// K1, gated by the storage NIC) and the handoff stream (per request: K3 =
+// prefill stand-in + PeToDe / MissMerge, gated per layer on the request's hit
+// KV).  A DE runs its reads as the fused dual gather (PE pool + its decode
+// pool) and ends once every request of its decode pool is complete.
+StepResult EngineRuntime::run_step_handoff() {
+  const ExecPlan& x = *plan_;
+  DeviceScope ds(device_);
+  auto s = static_cast<cudaStream_t>(stream_);
+  auto h = static_cast<cudaStream_t>(stream_h_);
+  StepResult res;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto start = static_cast<cudaEvent_t>(ev_start_);
+  check_cuda(cudaEventRecord(start, s), "cudaEventRecord");
+  if (h) check_cuda(cudaStreamWaitEvent(h, start, 0), "cudaStreamWaitEvent");
+  const std::int32_t L = x.cfg.n_layer;
+  const double cap = x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
+                                                          : x.opt.storage_cap_per_engine[engine_];
+  const double pace = x.opt.pace_scale;
+  const bool gated = cap > 0 || pace > 0;
+  double gate_s = 0;
+  auto storage_gate = [&](const LoadJob& j) {
+    const std::int64_t bytes = j.cached * x.cfg.kv_bytes_per_token();
+    if (gated) {
+      const double begin = std::max(gate_s, pace > 0 ? j.t_admit * pace : 0.0);
+      gate_s = begin + (cap > 0 ? static_cast<double>(bytes) / cap : 0.0);
+      std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
+      res.spans.push_back({begin, gate_s, bytes});
+    }
+    res.bytes_read += bytes;
+    ++res.jobs;
+  };
+  const auto nt = [&](int pe) { return x.n_tickets[pe]; };
+
+  if (is_pe()) {
+    for (int ji : x.by_pe[engine_]) {
+      const LoadJob& j = x.jobs[ji];
+      const int li = pe_local_[ji];
+      auto ev_load = static_cast<cudaEvent_t>(ev_load_[li]);
+      auto ev_k3 = static_cast<cudaEvent_t>(ev_k3_[li]);
+      if (!de_views_[j.de]) throw std::runtime_error("run_step: DE " + std::to_string(j.de) + " not attached");
+      // --- load stream: this PE's own reads (PE path)
+      if (!j.de_path && j.n_blk > 0) {
+        for (int w : j.k3_waits)
+          check_cuda(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_k3_[pe_local_[w]]), 0),
+                     "cudaStreamWaitEvent");
+        storage_gate(j);
+        dp_job job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket};
+        if (x.opt.k1_mode == 1) {
+          job.src_fb = x.src_fb[engine_].data() + j.blk_off;
+          job.dst_slot = x.slots[engine_].data() + j.blk_off;
+          check(dp_h2d_layer_copy(pool_, store_, &job, 1, s), "dp_h2d_layer_copy");
+        } else {
+          check(dp_h2d_layer_gather(pool_, store_, &job, 1, s), "dp_h2d_layer_gather");
+          ++res.launches;
+        }
+        check_cuda(cudaEventRecord(ev_load, s), "cudaEventRecord");
+        check_cuda(cudaStreamWaitEvent(h, ev_load, 0), "cudaStreamWaitEvent");
+      } else if (!j.de_path) {
+        // cold request on the PE path: only its K3 reuses slots
+        for (int w : j.k3_waits)
+          check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_k3_[pe_local_[w]]), 0),
+                     "cudaStreamWaitEvent");
+      }
+      // --- handoff stream: decode-slot hazards, then K3
+      if (!j.de_preds.empty()) {
+        const std::int64_t off = de_wait_off_[ji];
+        check(dp_wait_tickets(de_views_[j.de], d_wt_ + off, d_wg_ + off,
+                              static_cast<int32_t>(j.de_preds.size()), L, x.opt.wait_timeout_ms, h),
+              "dp_wait_tickets (decode slots)");
+        ++res.launches;
+      }
+      dp_handoff_job hj{d_ho_src_ + j.ho_off,
+                        d_ho_pe_ + j.ho_off,
+                        d_ho_de_ + j.ho_off,
+                        j.cached,
+                        j.prompt,
+                        j.n_pblk,
+                        j.de_path ? 0 : 1,
+                        (j.de_path && j.n_blk > 0) ? j.ticket : -1,
+                        static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block),
+                        j.de_ticket,
+                        j.ticket + nt(engine_)};
+      check(dp_prefill_handoff(pool_, de_views_[j.de], &hj, 1, x.opt.seed, x.opt.wait_timeout_ms, h),
+            "dp_prefill_handoff");
+      ++res.launches;
+      check_cuda(cudaEventRecord(ev_k3, h), "cudaEventRecord");
+    }
+    // the step ends when both streams are drained
+    check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), s), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_end_), 0), "cudaStreamWaitEvent");
+    check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), h), "cudaEventRecord");
+  } else {
+    for (int ji : x.by_reader[engine_]) {  // DE read path: dual gather
+      const LoadJob& j = x.jobs[ji];
+      if (!peers_[j.pe]) throw std::runtime_error("run_step: PE " + std::to_string(j.pe) + " not attached");
+      if (!j.pe_done_preds.empty()) {
+        const std::int64_t off = pe_done_off_[ji];
+        check(dp_wait_tickets(peers_[j.pe], d_wt_ + off, d_wg_ + off,
+                              static_cast<int32_t>(j.pe_done_preds.size()), L, x.opt.wait_timeout_ms, s),
+              "dp_wait_tickets (prefill slots)");
+        ++res.launches;
+      }
+      if (!j.de_preds.empty()) {
+        const std::int64_t off = de_wait_off_[ji];
+        check(dp_wait_tickets(pool_, d_wt_ + off, d_wg_ + off, static_cast<int32_t>(j.de_preds.size()),
+                              L, x.opt.wait_timeout_ms, s),
+              "dp_wait_tickets (decode slots)");
+        ++res.launches;
+      }
+      storage_gate(j);
+      dp_dual_job dj{{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket},
+                     d_dual_de_ + j.blk_off,
+                     j.de_ticket,
+                     0};
+      check(dp_h2d_push_p2p_dual(peers_[j.pe], pool_, store_, &dj, 1, s), "dp_h2d_push_p2p_dual");
+      ++res.launches;
+    }
+    if (final_wait_n_ > 0) {  // decode-ready: every prompt landed in this decode pool
+      check(dp_wait_tickets(pool_, d_wt_ + final_wait_off_, d_wg_ + final_wait_off_, final_wait_n_, L,
+                            x.opt.wait_timeout_ms, s),
+            "dp_wait_tickets (decode ready)");
+      ++res.launches;
+    }
+    check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), s), "cudaEventRecord");
+  }
+  check_cuda(cudaEventSynchronize(static_cast<cudaEvent_t>(ev_end_)), "step sync");
+  if (pool_) check(dp_wait_status(pool_), "transfer watchdog");
+  for (dp_pool* p : peers_)
+    if (p && p != pool_) check(dp_wait_status(p), "transfer watchdog");
+  for (dp_pool* p : de_views_)
+    if (p) check(dp_wait_status(p), "transfer watchdog");
+  float ms = 0;
+  check_cuda(cudaEventElapsedTime(&ms, start, static_cast<cudaEvent_t>(ev_end_)), "cudaEventElapsedTime");
+  res.device_ms = ms;
+  res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return res;
+}
+
 std::vector<std::uint64_t> EngineRuntime::checksum(int layer, std::span<const std::int32_t> slots,
                                                     std::span<const std::int32_t> ntok) {
-  if (!pool_) throw std::logic_error("checksum: engine is not a PE");
+  if (!pool_) throw std::logic_error("checksum: this engine owns no pool");
   if (slots.size() != ntok.size()) throw std::invalid_argument("checksum: size mismatch");
   DeviceScope ds(device_);
   const std::size_t n = slots.size();
@@ -456,8 +778,10 @@ std::vector<std::uint32_t> EngineRuntime::counters() const {
   std::uint32_t* ctr = nullptr;
   std::int64_t bytes = 0;
   check(dp_pool_info(pool_, &base, &ctr, &bytes), "dp_pool_info");
-  const std::size_t n = static_cast<std::size_t>(std::max<std::int32_t>(1, plan_->n_tickets[engine_])) *
-                        (plan_->cfg.n_layer + 1);
+  const ExecPlan& x = *plan_;
+  const std::int32_t rows = is_pe() ? std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff ? 2 : 1)
+                                    : std::max<std::int32_t>(1, x.n_de_tickets[engine_]);
+  const std::size_t n = static_cast<std::size_t>(rows) * (x.cfg.n_layer + 1);
   std::vector<std::uint32_t> out(n);
   check_cuda(cudaMemcpy(out.data(), ctr, n * 4, cudaMemcpyDeviceToHost), "counters D2H");
   return out;

@@ -946,10 +946,15 @@ __global__ void __launch_bounds__(kThreads) kv_prefill_handoff(const __grid_cons
         st_v4(de_dst + i, v);
       }
     }
-    if (job.de_ticket >= 0) {
+    if (job.de_ticket >= 0 || job.pe_done_ticket >= 0) {
       __syncthreads();
-      if (tid == 0)
-        release_sys(p.de_ctr + static_cast<int64_t>(job.de_ticket) * (p.n_layer + 1), layer, p.n_layer);
+      if (tid == 0) {
+        if (job.de_ticket >= 0)
+          release_sys(p.de_ctr + static_cast<int64_t>(job.de_ticket) * (p.n_layer + 1), layer, p.n_layer);
+        if (job.pe_done_ticket >= 0)
+          release_sys(p.pe_ctr + static_cast<int64_t>(job.pe_done_ticket) * (p.n_layer + 1), layer,
+                      p.n_layer);
+      }
     }
   }
 }
@@ -1054,6 +1059,7 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
       const int64_t need = (job.n_prompt + g.block_tokens - 1) / g.block_tokens;
       if (job.n_cached < 0 || job.n_prompt < job.n_cached || job.n_blk != need ||
           job.pe_ticket >= pe_pool->n_tickets || job.de_ticket >= de_view->n_tickets ||
+          job.pe_done_ticket >= pe_pool->n_tickets ||
           (job.n_blk > 0 && (!job.src_fb || !job.pe_slot || !job.de_slot)))
         return fail(DP_EINVAL, "prefill_handoff: job " + std::to_string(j0 + j) + " out of range");
       const int64_t n = static_cast<int64_t>(job.n_blk) * p.n_chunk * g.n_layer;

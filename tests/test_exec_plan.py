@@ -54,7 +54,7 @@ def test_decisions_become_jobs(P, D):
     dec = {d[1]: d for d in planned["decisions"]}
     jobs = xp.jobs()
     hit = 0
-    for req, traj, rnd, reader, pe, de_path, cached, nblk, ticket, slots, fbs, preds, fence in jobs:
+    for req, traj, rnd, reader, pe, de_path, cached, nblk, ticket, slots, fbs, preds, fence, *_ in jobs:
         d = dec[req]
         assert pe == d[2] and de_path == (d[4] == 1)
         assert reader == (d[3] if de_path else d[2])
@@ -120,3 +120,64 @@ def test_store_mapping_and_size_cap():
     xp2 = dp.build_exec_plan(cfg, trajs, planned, opt)
     assert xp2.store_fb == 3
     assert all(0 <= f < 3 for j in xp2.jobs() for f in j[10])
+
+
+def build_handoff(P, D, policy="dual_path", tight=False, count=10, turns=6, seed=8):
+    cfg = cluster(P, D)
+    trajs = dp.synthesize(max_len=20000, count=count, seed=seed, mean_turns=turns, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy=policy, **SB)
+    opt = dp.ExecOptions()
+    opt.handoff = True
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    if tight:
+        opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots
+        xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    return cfg, trajs, planned, xp
+
+
+@pytest.mark.parametrize("P,D,tight", [(1, 1, False), (2, 2, False), (1, 1, True), (1, 3, True)])
+def test_handoff_plan_invariants(P, D, tight):
+    cfg, trajs, planned, xp = build_handoff(P, D, tight=tight)
+    T = cfg.block_size_tokens
+    reqs = {r[0]: r for r in planned["requests"]}
+    jobs = xp.jobs()
+    # every request that reached prefill has a job, cold ones included
+    assert sorted(j[0] for j in jobs) == sorted(r[0] for r in planned["requests"] if r[6] >= 0)
+    ho = 0
+    for j in jobs:
+        r = reqs[j[0]]
+        cached, prompt = r[3], r[3] + r[4]
+        assert j[6] == cached and j[14] == prompt and j[13] == r[7]
+        assert j[15] == -(-prompt // T) == len(j[17]) == len(j[18])
+        assert j[17][:j[7]] == j[9]  # the hit blocks are the first prompt blocks
+        ho += (prompt - cached if j[5] else prompt) * cfg.kv_bytes_per_token()
+    assert ho == xp.handoff_bytes
+    pos = {j[0]: i for i, j in enumerate(jobs)}
+    # live-slot exclusivity: PE slots [t_read_done, t_pe_release), DE slots [t_read_done, t_done)
+    for which, free_col, slot_col, key_col in (("pe", 13, 17, 4), ("de", 14, 18, 13)):
+        evs = []
+        for j in jobs:
+            r = reqs[j[0]]
+            evs.append((r[12], 1, j[0], j))
+            if r[free_col] >= 0:
+                evs.append((r[free_col], 0, j[0], j))
+        evs.sort(key=lambda e: (e[0], e[1], e[2]))
+        live, last = {}, {}
+        for t, kind, req, j in evs:
+            for s in j[slot_col]:
+                key = (j[key_col], s)
+                if kind == 1:
+                    assert key not in live, f"{which} slot {key} double-booked"
+                    live[key] = req
+                    if which == "de" and key in last:  # predecessor recorded, and earlier
+                        prev = last[key]
+                        assert prev[16] in j[19] and pos[prev[0]] < pos[j[0]]
+                    last[key] = j
+                else:
+                    assert live.pop(key) == req
+    # decode tickets dense per DE
+    for d in range(xp.n_pe, xp.n_engines):
+        t = sorted(j[16] for j in jobs if j[13] == d)
+        assert t == list(range(len(t))) and len(t) == xp.n_de_tickets[d]
+    if tight:
+        assert any(j[19] for j in jobs)  # decode-slot reuse hazards exercised

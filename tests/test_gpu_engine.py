@@ -33,7 +33,7 @@ def final_occupants(xp, pe):
     """slot -> (Full Block, valid tokens) of the last job that wrote it."""
     last = {}
     for job in xp.jobs():
-        req, traj, rnd, reader, jpe, de_path, cached, nblk, ticket, slots, fbs, preds, fence = job
+        req, traj, rnd, reader, jpe, de_path, cached, nblk, ticket, slots, fbs, preds, fence = job[:13]
         if jpe != pe:
             continue
         for k, (s, fb) in enumerate(zip(slots, fbs)):
@@ -171,3 +171,93 @@ def test_two_engines_k1_on_copy_engine(two_gpus):
         assert res[0].launches <= 1  # the PE issues copies, not kernels (at most its final wait)
     verify_counters(pe, xp, cfg)
     verify_pool(pe, xp, cfg)
+
+
+# ------------------------------------------------------------ PD handoff
+def prompt_occupants(xp, engine, T=64):
+    """slot -> (Full Block, valid prompt tokens) of the last job that used it,
+    in the PE pool (engine < n_pe) or in the DE decode pool."""
+    last = {}
+    for job in xp.jobs():
+        traj, pe, prompt, de = job[1], job[4], job[14], job[13]
+        if engine < xp.n_pe and pe == engine:
+            slots = job[17]
+        elif engine >= xp.n_pe and de == engine:
+            slots = job[18]
+        else:
+            continue
+        for k, s in enumerate(slots):
+            last[s] = (xp.fb_of(traj, k), min(T, prompt - T * k))
+    return last
+
+
+def verify_prompt_pool(engine, xp, cfg):
+    last = prompt_occupants(xp, engine.engine, cfg.block_size_tokens)
+    slots = sorted(last)
+    g = refpy.geom(cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer)
+    for layer in range(cfg.n_layer):
+        got = engine.checksum(layer, slots, [last[s][1] for s in slots])
+        want = [refpy.layer_block_hash(g, SEED, last[s][0], layer, last[s][1]) for s in slots]
+        assert list(got) == want, f"engine {engine.engine} layer {layer}"
+    return len(slots)
+
+
+def handoff_engines(xp, n):
+    import torch
+    assert torch.cuda.device_count() >= n
+    rts = [dp.EngineRuntime(xp, e, e) for e in range(n)]
+    for a in rts:
+        for b in rts:
+            if a is not b and b.has_pool and ((a.is_pe and not b.is_pe) or (b.is_pe and not a.is_pe)):
+                a.attach_peer_local(b.engine, b)
+    return rts
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("policy,tight", [("dual_path", False), ("dual_path", True), ("pe_only", True)])
+def test_handoff_1p1d(two_gpus, policy, tight):
+    cfg = cluster(1, 1, L=6)
+    trajs = small_trace(count=8, turns=5, seed=6)
+    planned = dp.plan(cfg, trajs, policy=policy, **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.handoff = True
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    if tight:
+        opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots
+        xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    rts = handoff_engines(xp, 2)
+    for _ in range(2):
+        for rt in rts:
+            rt.reset_counters()
+        res = dp.run_step_all(rts)
+        assert sum(r.bytes_read for r in res) == xp.hit_bytes
+    assert verify_prompt_pool(rts[0], xp, cfg) > 0
+    assert verify_prompt_pool(rts[1], xp, cfg) > 0
+    # decode-ready rows: every request's prompt fully landed in the decode pool
+    ctr = np.asarray(rts[1].counters(), dtype=np.int64).reshape(-1, cfg.n_layer + 1)
+    for job in xp.jobs():
+        blocks = (job[7] if job[5] else 0) + job[15]
+        assert ctr[job[16], cfg.n_layer] == blocks * xp.items_per_block * cfg.n_layer
+
+
+@pytest.mark.multigpu
+def test_handoff_2p2d_tight(gpus):
+    if gpus < 4:
+        pytest.skip("needs 4 GPUs")
+    cfg = cluster(2, 2, L=4)
+    trajs = small_trace(count=12, turns=5, seed=9)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.handoff = True
+    probe = dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.pool_slots, opt.de_pool_slots = probe.peak_slots, probe.de_peak_slots
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    rts = handoff_engines(xp, 4)
+    for _ in range(2):
+        for rt in rts:
+            rt.reset_counters()
+        dp.run_step_all(rts)
+    for rt in rts:
+        verify_prompt_pool(rt, xp, cfg)

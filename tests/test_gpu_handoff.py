@@ -49,7 +49,7 @@ def test_de_path_dual_then_missmerge(two_gpus, L, T, b, C, A):
     n_hit, n_prompt = -(-C // T), -(-P // T)
     rng = np.random.default_rng(C * 7 + A)
     st_de = abi.Store(1, g, 40, SEED)
-    pe_pool = abi.Pool(0, g, 32, 2)
+    pe_pool = abi.Pool(0, g, 32, 2)   # row 0: hit KV landed, row 1: handoff done
     de_pool = abi.Pool(1, g, 32, 2)
     pe_view_on_de = pe_pool.peer_view(1)
     de_view_on_pe = de_pool.peer_view(0)
@@ -68,7 +68,7 @@ def test_de_path_dual_then_missmerge(two_gpus, L, T, b, C, A):
         items = abi.layer_items(g, n_hit)
         hj = (abi.HandoffJob * 1)()
         hj[0] = abi.HandoffJob(on_pe[0].data_ptr(), on_pe[1].data_ptr(), on_pe[2].data_ptr(), C, P,
-                               n_prompt, 0, 0 if C else -1, items, 0, 0)
+                               n_prompt, 0, 0 if C else -1, items, 0, 1)
         # K3 first: it must block on the dual gather's per-layer releases
         abi.prefill_handoff(pe_pool, de_view_on_pe, hj, 1, SEED, timeout_ms=20000)
         abi.push_p2p_dual(pe_view_on_de, de_pool, st_de, dj, 1)
@@ -81,8 +81,10 @@ def test_de_path_dual_then_missmerge(two_gpus, L, T, b, C, A):
         want_layer = (n_hit + n_prompt) * per_block
         abi.wait_layer(de_pool, 0, L, want_layer * L, timeout_ms=2000)
         abi.wait_layer(de_pool, 0, L - 1, want_layer, timeout_ms=2000)
+        abi.wait_layer(pe_pool, 1, L, n_prompt * per_block * L, timeout_ms=2000)  # K3 done row
         sync_all()
         assert abi.wait_status(de_pool) == abi.DP_OK
+        assert abi.wait_status(pe_pool) == abi.DP_OK
     finally:
         for x in (de_view_on_pe, pe_view_on_de, de_pool, pe_pool, st_de):
             x.close()
@@ -110,7 +112,7 @@ def test_pe_path_load_then_petode(two_gpus, C, A):
             abi.h2d_layer_gather(pe_pool, st_pe, abi.make_jobs(
                 [(t[0].data_ptr(), t[1].data_ptr(), C, n_hit, 0, L, -1)]), 1)
         hj = (abi.HandoffJob * 1)()
-        hj[0] = abi.HandoffJob(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), C, P, n_prompt, 1, -1, 0, 0, 0)
+        hj[0] = abi.HandoffJob(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), C, P, n_prompt, 1, -1, 0, 0, -1)
         abi.prefill_handoff(pe_pool, de_view, hj, 1, SEED)  # same (legacy) stream: ordered after K1
         sync_all()
         gr = refpy.geom(L, T, b)
@@ -134,7 +136,7 @@ def test_handoff_gate_watchdog(two_gpus):
     try:
         t = [dev([0, 1], 0, np.int64), dev([0, 1], 0, np.int32), dev([0, 1], 0, np.int32)]
         hj = (abi.HandoffJob * 1)()
-        hj[0] = abi.HandoffJob(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), 64, 100, 2, 0, 0, 1, 0, 0)
+        hj[0] = abi.HandoffJob(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), 64, 100, 2, 0, 0, 1, 0, -1)
         abi.prefill_handoff(pe_pool, de_view, hj, 1, SEED, timeout_ms=50)
         sync_all()
         assert abi.wait_status(pe_pool) == abi.DP_ETIMEOUT
