@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--online", type=float, default=0.0,
                     help="config 5: Poisson arrivals at this many sessions/s, replayed in real time")
     ap.add_argument("--caps", default="", help="config 5: per-engine storage caps, GB/s, comma list")
+    ap.add_argument("--handoff", action="store_true",
+                    help="also run the PD handoff: prefill stand-in + PeToDe/MissMerge per layer "
+                         "into the DE decode pools, DE read path fused with DecodeH2D")
     ap.add_argument("--k1", default="sm", choices=["sm", "ce"],
                     help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs)")
     return ap.parse_args()
@@ -258,6 +261,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
     if args.online > 0:
         opt.pace_scale = 1.0
     opt.k1_mode = 1 if args.k1 == "ce" else 0
+    opt.handoff = bool(args.handoff)
     opt.seed = 9
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     from paper_2602_21548_b200 import dist as dpdist
@@ -295,6 +299,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
                     per_engine[e] = round(ms, 1)
     snic = sum(u["total_bytes"] for u in planned["usage"] if u["kind"] == "snic_read")
     info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens,
+                handoff_bytes=xp.handoff_bytes if args.handoff else 0,
                 model_gbps=snic / planned["makespan"] / 1e9 if planned["makespan"] > 0 else None,
                 requests=xp.requests, reader_bytes=list(xp.reader_bytes),
                 de_path=sum(1 for d in planned["decisions"] if d[4] == 1),
@@ -554,6 +559,11 @@ def main():
                 out["round_robin"] = {"value": round(rr_v, 3), "unit": "GB/s",
                                       "adaptive_vs_rr": round(value / rr_v, 3)}
                 out["balance"]["round_robin"] = storage_balance(rr["info"]["spans"], rr["info"]["caps"], P + D)
+        if args.handoff:
+            out["handoff"] = {"bytes_per_step": info["handoff_bytes"],
+                              "gbps": round(info["handoff_bytes"] * K / dev_s / 1e9, 3),
+                              "what": "PeToDe/MissMerge per layer into DE decode pools (K3, NVLink) "
+                                      "+ prefill stand-in; DE read path fused with DecodeH2D"}
         if "pe_only" in results and n > 1:
             po = results["pe_only"]
             po_s = sum(po["dev_ms"]) / 1e3

@@ -63,9 +63,11 @@ class Group:
 
 
 def connect_pools(group, engines, n_pe):
-    """Exchange PE pool handles and attach every DE engine to every PE pool.
+    """Exchange pool handles: every DE attaches every PE pool (K2 pushes), and
+    with the PD handoff every PE attaches every DE decode pool (K3 pushes).
     `engines` maps engine id -> EngineRuntime for the engines of this process."""
-    mine = {e: rt.export_pool() for e, rt in engines.items() if e < n_pe}
+    mine = {e: rt.export_pool() for e, rt in engines.items()
+            if e < n_pe or getattr(rt, "has_pool", False)}
     table = {}
     for part in group.allgather(mine):
         table.update(part)
@@ -76,4 +78,8 @@ def connect_pools(group, engines, n_pe):
         if e >= n_pe:
             for pe in range(n_pe):
                 rt.attach_peer(pe, table[pe])
+        else:
+            for de, h in sorted(table.items()):
+                if de >= n_pe:
+                    rt.attach_peer(de, h)
     return table
