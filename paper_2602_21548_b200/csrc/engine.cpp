@@ -42,9 +42,11 @@ T* upload(const std::vector<T>& v) {
 }
 
 // Free-slot queues of one pool.  Freed slots go back to a queue of the
-// engine that last wrote them; an allocation takes, in order, slots its own
-// writer last wrote (ordered by its stream), never-used slots, then other
-// writers' slots (a cross-GPU hazard).  FIFO within each queue.
+// engine that last wrote them; an allocation takes, in order, never-used
+// slots, the slots its own writer freed longest ago (ordered by its stream,
+// and long done in real time), then other writers' slots (a cross-GPU
+// hazard).  FIFO within each queue: reuse distance is maximal, so the
+// hazard waits an allocation records are almost always already satisfied.
 struct SlotQueues {
   std::deque<std::int32_t> fresh;
   std::vector<std::deque<std::int32_t>> by_writer;
@@ -55,10 +57,10 @@ struct SlotQueues {
   }
   std::int32_t take(int writer) {
     std::deque<std::int32_t>* src = nullptr;
-    if (!by_writer[writer].empty()) {
-      src = &by_writer[writer];
-    } else if (!fresh.empty()) {
+    if (!fresh.empty()) {
       src = &fresh;
+    } else if (!by_writer[writer].empty()) {
+      src = &by_writer[writer];
     } else {
       for (auto& q : by_writer)
         if (!q.empty()) {

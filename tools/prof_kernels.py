@@ -61,9 +61,52 @@ def one(kind, a, g, L, T, b, n_fb, n_slots):
         st.close()
 
 
+def k3(a, g, L, T, b, n_fb, n_slots):
+    """K3 alone (PE path: push the whole prompt of each job, C = 7/8 of it)."""
+    st = abi.Store(0, g, n_fb, 9)
+    pool = abi.Pool(0, g, n_slots, 2 * a.jobs)
+    de_pool = abi.Pool(1, g, n_slots, a.jobs)
+    de_view = de_pool.peer_view(0)
+    try:
+        rng = np.random.default_rng(0)
+        keep, specs, ho = [], [], (abi.HandoffJob * a.jobs)()
+        perm = rng.permutation(n_slots)
+        for j in range(a.jobs):
+            fbs = torch.tensor(rng.integers(0, n_fb, a.blocks), dtype=torch.int64, device="cuda:0")
+            sl = torch.tensor(perm[(j * a.blocks) % n_slots:][:a.blocks].astype(np.int32), device="cuda:0")
+            keep += [fbs, sl]
+            prompt = a.blocks * T
+            cached = prompt * 7 // 8
+            specs.append((fbs.data_ptr(), sl.data_ptr(), cached, -(-cached // T), 0, L, j))
+            ho[j] = abi.HandoffJob(fbs.data_ptr(), sl.data_ptr(), sl.data_ptr(), cached, prompt, a.blocks,
+                                   1, -1, 0, j, a.jobs + j)
+        abi.h2d_layer_gather(pool, st, abi.make_jobs(specs), len(specs))
+        torch.cuda.synchronize(0)
+        nbytes = a.jobs * a.blocks * T * b * L
+        times = []
+        s = torch.cuda.Stream(device=0)
+        for r in range(a.reps + 1):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            abi.prefill_handoff(pool, de_view, ho, a.jobs, 9, 20000, s.cuda_stream)
+            e1.record(s)
+            e1.synchronize()
+            if r:
+                times.append(e0.elapsed_time(e1))
+        ms = sorted(times)[len(times) // 2]
+        return {"bytes": nbytes, "ms": ms, "GBps": nbytes / ms / 1e6}
+    finally:
+        de_view.close()
+        de_pool.close()
+        pool.close()
+        st.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--k2", action="store_true")
+    ap.add_argument("--k3", action="store_true")
     ap.add_argument("--jobs", type=int, default=64)
     ap.add_argument("--blocks", type=int, default=128)  # 8K-token requests
     ap.add_argument("--reps", type=int, default=3)
@@ -82,6 +125,8 @@ def main():
             out[kind if ctas == 0 else f"{kind}@{ctas}"] = one(kind, a, g, L, T, b, n_fb, n_slots)
     for dev in range(torch.cuda.device_count()):
         abi.set_gather_ctas(dev, 0)
+    if a.k3:
+        out["k3"] = k3(a, g, L, T, b, n_fb, n_slots)
     print(json.dumps(out))
 
 
