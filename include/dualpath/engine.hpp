@@ -51,6 +51,9 @@ struct ExecOptions {
   // and the DE read path fused with DecodeH2D (dual store)
   bool handoff = false;
   std::int32_t de_pool_slots = 0;      // per DE decode pool; 0 = auto (4x plan peak)
+  // CTA cap of the SM gathers (dp_set_gather_ctas) on this run's devices;
+  // 0 = default (4 per SM), -1 = auto: 64 on a PE when the handoff shares it
+  std::int32_t gather_ctas = -1;
 };
 
 // One request's hit-KV transfer (all layers), in global execution order.

@@ -367,6 +367,10 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   } else {
     upload_tables();
   }
+  // K1 is PCIe-bound and keeps its rate down to ~32 CTAs; on a PE that also
+  // runs K3 the remaining SMs go to the handoff
+  const std::int32_t ctas = x.opt.gather_ctas >= 0 ? x.opt.gather_ctas : (x.handoff && is_pe() ? 64 : 0);
+  check(dp_set_gather_ctas(device_, ctas), "dp_set_gather_ctas");
 }
 
 EngineRuntime::~EngineRuntime() {
