@@ -54,6 +54,9 @@ struct ExecOptions {
   // CTA cap of the SM gathers (dp_set_gather_ctas) on this run's devices;
   // 0 = default (4 per SM), -1 = auto: 64 on a PE when the handoff shares it
   std::int32_t gather_ctas = -1;
+  // DE-path gate of K3: 0 = the handoff stream waits (cuStreamWaitValue32, no
+  // SMs) for the whole request's hit KV; 1 = K3 gates layer by layer in-kernel
+  std::int32_t k3_layer_gate = 0;
 };
 
 // One request's hit-KV transfer (all layers), in global execution order.

@@ -209,6 +209,11 @@ int dp_wait_layer(const dp_pool* pool, int32_t ticket, int32_t layer, uint32_t t
 /* Same for n tickets at once (tickets/targets device-accessible). */
 int dp_wait_tickets(const dp_pool* pool, const int32_t* tickets, const uint32_t* targets,
                     int32_t n, int32_t layer, int32_t timeout_ms, dp_stream stream);
+/* Make `stream` wait, without occupying SMs (cuStreamWaitValue32, GEQ), until
+ * the LOCAL pool's landed[ticket][layer] >= target.  No watchdog: use it for
+ * producers that are known to run (the executor's whole-request gate). */
+int dp_stream_wait_counter(const dp_pool* pool, int32_t ticket, int32_t layer, uint32_t target,
+                           dp_stream stream);
 /* Returns DP_ETIMEOUT if any wait on this device's pool has timed out. */
 int dp_wait_status(const dp_pool* pool);
 

@@ -98,6 +98,7 @@ def lib():
         "dp_wait_tickets": ([P, P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P],
                             ctypes.c_int),
         "dp_wait_status": ([P], ctypes.c_int),
+        "dp_stream_wait_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
         "dp_pool_checksum": ([P, ctypes.c_int32, P, P, ctypes.c_int32, P, P], ctypes.c_int),
         "dp_pool_copy_out": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P], ctypes.c_int),
         "dp_device_count": ([], ctypes.c_int),
@@ -242,6 +243,10 @@ def layer_items(g, n_blk):
 
 def wait_layer(pool, ticket, layer, target, timeout_ms=10000, stream=0):
     check(lib().dp_wait_layer(pool.ptr, ticket, layer, target, timeout_ms, ctypes.c_void_p(stream)))
+
+
+def stream_wait_counter(pool, ticket, layer, target, stream=0):
+    check(lib().dp_stream_wait_counter(pool.ptr, ticket, layer, target, ctypes.c_void_p(stream)))
 
 
 def wait_status(pool):

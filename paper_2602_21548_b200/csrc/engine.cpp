@@ -685,6 +685,14 @@ StepResult EngineRuntime::run_step_handoff() {
               "dp_wait_tickets (decode slots)");
         ++res.launches;
       }
+      const bool layer_gate = x.opt.k3_layer_gate == 1;
+      if (j.de_path && j.n_blk > 0 && !layer_gate) {
+        check(dp_stream_wait_counter(pool_, j.ticket, L,
+                                     static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) *
+                                                                x.items_per_block * L),
+                                     h),
+              "dp_stream_wait_counter");
+      }
       dp_handoff_job hj{d_ho_src_ + j.ho_off,
                         d_ho_pe_ + j.ho_off,
                         d_ho_de_ + j.ho_off,
@@ -692,7 +700,7 @@ StepResult EngineRuntime::run_step_handoff() {
                         j.prompt,
                         j.n_pblk,
                         j.de_path ? 0 : 1,
-                        (j.de_path && j.n_blk > 0) ? j.ticket : -1,
+                        (j.de_path && j.n_blk > 0 && layer_gate) ? j.ticket : -1,
                         static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block),
                         j.de_ticket,
                         j.ticket + nt(engine_)};

@@ -596,6 +596,21 @@ int dp_h2d_push_p2p_layer(dp_pool* pe_view, const dp_store* de_src, const dp_job
 namespace {
 
 using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+WaitValue32Fn wait_value32() {
+  static WaitValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitValue32Fn>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
 
 // cuStreamWriteValue32 through the runtime's driver entry point (no link
 // dependency on libcuda, so the library still loads on a machine without a
@@ -673,6 +688,23 @@ int dp_h2d_layer_copy(dp_pool* pool, const dp_store* src, const dp_job* jobs, in
       }
     }
   }
+  return DP_OK;
+}
+
+int dp_stream_wait_counter(const dp_pool* pool, int32_t ticket, int32_t layer, uint32_t target,
+                           dp_stream stream) {
+  if (!pool) return fail(DP_EINVAL, "stream_wait_counter: null pool");
+  if (!pool->owner) return fail(DP_EINVAL, "stream_wait_counter: the pool must be local");
+  if (ticket < 0 || ticket >= pool->n_tickets || layer < 0 || layer > pool->geom.n_layer)
+    return fail(DP_EINVAL, "stream_wait_counter: ticket/layer out of range");
+  const WaitValue32Fn wv = wait_value32();
+  if (!wv) return fail(DP_ECUDA, "stream_wait_counter: cuStreamWaitValue32 unavailable");
+  DeviceGuard guard(pool->device);
+  const uint32_t* ctr =
+      pool->counters + static_cast<int64_t>(ticket) * (pool->geom.n_layer + 1) + layer;
+  if (wv(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(ctr), target,
+         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    return fail(DP_ECUDA, "stream_wait_counter: cuStreamWaitValue32 failed");
   return DP_OK;
 }
 

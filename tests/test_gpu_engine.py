@@ -214,14 +214,16 @@ def handoff_engines(xp, n):
 
 
 @pytest.mark.multigpu
-@pytest.mark.parametrize("policy,tight", [("dual_path", False), ("dual_path", True), ("pe_only", True)])
-def test_handoff_1p1d(two_gpus, policy, tight):
+@pytest.mark.parametrize("policy,tight,layer_gate", [("dual_path", False, 0), ("dual_path", True, 0),
+                                                     ("pe_only", True, 0), ("dual_path", True, 1)])
+def test_handoff_1p1d(two_gpus, policy, tight, layer_gate):
     cfg = cluster(1, 1, L=6)
     trajs = small_trace(count=8, turns=5, seed=6)
     planned = dp.plan(cfg, trajs, policy=policy, **STORAGE_BOUND)
     opt = dp.ExecOptions()
     opt.seed = SEED
     opt.handoff = True
+    opt.k3_layer_gate = layer_gate
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     if tight:
         opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots

@@ -143,3 +143,42 @@ def test_handoff_gate_watchdog(two_gpus):
     finally:
         for x in (de_view, de_pool, pe_pool):
             x.close()
+
+
+def test_stream_wait_counter_orders_a_stream(two_gpus):
+    """dp_stream_wait_counter: the PE stream waits (no SMs) for a counter the
+    DE's dual gather releases, then K3 runs without its in-kernel gate."""
+    L, T, b = 4, 64, 576
+    g = abi.geom(L, T, b)
+    C, A = 64 * 3 + 5, 70
+    P = C + A
+    n_hit, n_prompt = -(-C // T), -(-P // T)
+    st_de = abi.Store(1, g, 16, SEED)
+    pe_pool = abi.Pool(0, g, 16, 2)
+    de_pool = abi.Pool(1, g, 16, 1)
+    pe_view = pe_pool.peer_view(1)
+    de_view = de_pool.peer_view(0)
+    try:
+        fbs = np.arange(3, 3 + n_prompt, dtype=np.int64)
+        ps = np.arange(n_prompt, dtype=np.int32)
+        dsl = np.arange(8, 8 + n_prompt, dtype=np.int32)
+        on_de = [dev(fbs, 1, np.int64), dev(ps, 1, np.int32), dev(dsl, 1, np.int32)]
+        on_pe = [dev(fbs, 0, np.int64), dev(ps, 0, np.int32), dev(dsl, 0, np.int32)]
+        items = abi.layer_items(g, n_hit)
+        abi.stream_wait_counter(pe_pool, 0, L, items * L)  # legacy stream of device 0
+        hj = (abi.HandoffJob * 1)()
+        hj[0] = abi.HandoffJob(on_pe[0].data_ptr(), on_pe[1].data_ptr(), on_pe[2].data_ptr(), C, P,
+                               n_prompt, 0, -1, 0, 0, 1)
+        abi.prefill_handoff(pe_pool, de_view, hj, 1, SEED)
+        dj = (abi.DualJob * 1)()
+        dj[0].pe = abi.Job(on_de[0].data_ptr(), on_de[1].data_ptr(), C, n_hit, 0, L, 0)
+        dj[0].de_slot = on_de[2].data_ptr()
+        dj[0].de_ticket = 0
+        abi.push_p2p_dual(pe_view, de_pool, st_de, dj, 1)
+        sync_all()
+        gr = refpy.geom(L, T, b)
+        check_prompt(pe_pool, gr, fbs, ps, P, T, b, L)
+        check_prompt(de_pool, gr, fbs, dsl, P, T, b, L)
+    finally:
+        for x in (de_view, pe_view, de_pool, pe_pool, st_de):
+            x.close()
