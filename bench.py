@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--handoff", action="store_true",
                     help="also run the PD handoff: prefill stand-in + PeToDe/MissMerge per layer "
                          "into the DE decode pools, DE read path fused with DecodeH2D")
+    ap.add_argument("--handoff-ctas", type=int, default=0, help="K3 CTA cap on PEs (0 = default)")
+    ap.add_argument("--gather-ctas", type=int, default=-1, help="K1/K2 CTA cap (-1 = auto)")
     ap.add_argument("--k1", default="sm", choices=["sm", "ce"],
                     help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs)")
     return ap.parse_args()
@@ -262,6 +264,8 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
         opt.pace_scale = 1.0
     opt.k1_mode = 1 if args.k1 == "ce" else 0
     opt.handoff = bool(args.handoff)
+    opt.handoff_ctas = args.handoff_ctas
+    opt.gather_ctas = args.gather_ctas
     opt.seed = 9
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     from paper_2602_21548_b200 import dist as dpdist
@@ -524,7 +528,7 @@ def main():
             "config": {"workload": f"{args.workload}: {len(trajs)} sessions, "
                                    + ("1 PE loader (K1)" if n == 1 else f"{P}P{D}D dual_path"),
                        "kv": shape, "storage_cap_gbps_per_engine": args.cap_gbps or None,
-                       "k1": args.k1,
+                       "k1": args.k1, "handoff_ctas": args.handoff_ctas or None,
                        "requests": info["requests"], "hit_bytes_per_step": info["hit_bytes"],
                        "de_path_requests": info["de_path"],
                        "read_gb_per_engine": [round(x / 1e9, 2) for x in info["reader_bytes"]],

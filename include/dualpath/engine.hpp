@@ -57,6 +57,7 @@ struct ExecOptions {
   // DE-path gate of K3: 0 = the handoff stream waits (cuStreamWaitValue32, no
   // SMs) for the whole request's hit KV; 1 = K3 gates layer by layer in-kernel
   std::int32_t k3_layer_gate = 0;
+  std::int32_t handoff_ctas = 0;       // K3 CTA cap on PEs (0 = default)
 };
 
 // One request's hit-KV transfer (all layers), in global execution order.

@@ -198,6 +198,11 @@ int dp_h2d_layer_copy(dp_pool* pe, const dp_store* src, const dp_job* jobs, int3
  * the SMs to the prefill compute (the isolation knob of config 4). */
 int dp_set_gather_ctas(int device, int32_t ctas);
 
+/* Cap on the CTAs of a K3 (dp_prefill_handoff) launch on `device` (0 =
+ * default, 4 per SM).  K3 shares the PE with K1: fewer K3 CTAs leave the
+ * register file to the loads. */
+int dp_set_handoff_ctas(int device, int32_t ctas);
+
 /* Items (landed-counter increments) per layer for a job of n_blk blocks. */
 int dp_layer_items(const dp_kv_geom* geom, int32_t n_blk, int32_t* out);
 

@@ -103,6 +103,7 @@ def lib():
         "dp_pool_copy_out": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P], ctypes.c_int),
         "dp_device_count": ([], ctypes.c_int),
         "dp_set_gather_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
+        "dp_set_handoff_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -255,6 +256,10 @@ def wait_status(pool):
 
 def set_gather_ctas(device, ctas):
     check(lib().dp_set_gather_ctas(device, ctas))
+
+
+def set_handoff_ctas(device, ctas):
+    check(lib().dp_set_handoff_ctas(device, ctas))
 
 
 def device_count():

@@ -335,6 +335,7 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("de_pool_slots", &dualpath::ExecOptions::de_pool_slots)
       .def_readwrite("gather_ctas", &dualpath::ExecOptions::gather_ctas)
       .def_readwrite("k3_layer_gate", &dualpath::ExecOptions::k3_layer_gate)
+      .def_readwrite("handoff_ctas", &dualpath::ExecOptions::handoff_ctas)
       .def_readwrite("store_fb", &dualpath::ExecOptions::store_fb)
       .def_readwrite("store_bytes_max", &dualpath::ExecOptions::store_bytes_max)
       .def_readwrite("seed", &dualpath::ExecOptions::seed)

@@ -371,6 +371,7 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   // runs K3 the remaining SMs go to the handoff
   const std::int32_t ctas = x.opt.gather_ctas >= 0 ? x.opt.gather_ctas : (x.handoff && is_pe() ? 64 : 0);
   check(dp_set_gather_ctas(device_, ctas), "dp_set_gather_ctas");
+  if (is_pe()) check(dp_set_handoff_ctas(device_, x.opt.handoff_ctas), "dp_set_handoff_ctas");
 }
 
 EngineRuntime::~EngineRuntime() {

@@ -261,6 +261,7 @@ __global__ void kv_store_fill(uint64_t* dst, int64_t n_pairs, int64_t words_per_
 
 constexpr int kMaxDevices = 64;
 int g_gather_ctas[kMaxDevices] = {};  // 0 = default
+int g_handoff_ctas[kMaxDevices] = {};  // 0 = default
 
 int sm_count(int device) {
   int n = 0;
@@ -708,6 +709,13 @@ int dp_stream_wait_counter(const dp_pool* pool, int32_t ticket, int32_t layer, u
   return DP_OK;
 }
 
+int dp_set_handoff_ctas(int device, int32_t ctas) {
+  if (device < 0 || device >= kMaxDevices || ctas < 0)
+    return fail(DP_EINVAL, "set_handoff_ctas: bad argument");
+  g_handoff_ctas[device] = ctas;
+  return DP_OK;
+}
+
 int dp_set_gather_ctas(int device, int32_t ctas) {
   if (device < 0 || device >= kMaxDevices || ctas < 0)
     return fail(DP_EINVAL, "set_gather_ctas: bad argument");
@@ -1080,7 +1088,8 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
   p.n_layer = g.n_layer;
   p.block_tokens = g.block_tokens;
   p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
-  const int grid_cap = sm_count(pe_pool->device) * 4;  // NVLink-bound: many stores in flight
+  const int ho_cap = pe_pool->device < kMaxDevices ? g_handoff_ctas[pe_pool->device] : 0;
+  const int grid_cap = ho_cap > 0 ? ho_cap : sm_count(pe_pool->device) * 4;  // NVLink-bound
   auto s = static_cast<cudaStream_t>(stream);
   for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_HANDOFF_JOBS_PER_LAUNCH) {
     const int32_t nj = std::min<int32_t>(DP_MAX_HANDOFF_JOBS_PER_LAUNCH, n_jobs - j0);

@@ -107,6 +107,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--k2", action="store_true")
     ap.add_argument("--k3", action="store_true")
+    ap.add_argument("--k3-ctas", default="0")
     ap.add_argument("--jobs", type=int, default=64)
     ap.add_argument("--blocks", type=int, default=128)  # 8K-token requests
     ap.add_argument("--reps", type=int, default=3)
@@ -126,7 +127,10 @@ def main():
     for dev in range(torch.cuda.device_count()):
         abi.set_gather_ctas(dev, 0)
     if a.k3:
-        out["k3"] = k3(a, g, L, T, b, n_fb, n_slots)
+        for ctas in [int(x) for x in a.k3_ctas.split(",")]:
+            abi.set_handoff_ctas(0, ctas)
+            out["k3" if ctas == 0 else f"k3@{ctas}"] = k3(a, g, L, T, b, n_fb, n_slots)
+        abi.set_handoff_ctas(0, 0)
     print(json.dumps(out))
 
 
