@@ -163,14 +163,16 @@ __global__ void __launch_bounds__(kThreads) kv_gather(const __grid_constant__ Ga
       __syncthreads();
       if (tid == 0) {
         uint32_t* row = p.counters + static_cast<int64_t>(job.ticket) * (p.n_layer + 1);
+        // one fence after the CTA barrier, then relaxed reductions (a
+        // release pattern; consumers acquire)
         if (kPeer) {
           asm volatile("fence.acq_rel.sys;" ::: "memory");
-          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(row + layer) : "memory");
-          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(row + p.n_layer) : "memory");
+          asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(row + layer) : "memory");
+          asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(row + p.n_layer) : "memory");
         } else {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(row + layer) : "memory");
-          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(row + p.n_layer) : "memory");
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(row + layer) : "memory");
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(row + p.n_layer) : "memory");
         }
       }
     }
@@ -846,11 +848,15 @@ static_assert(sizeof(HandoffParams) <= 4000, "kernel parameter block too large")
 static_assert(sizeof(dp_dual_job) == 56, "dp_dual_job layout");
 static_assert(sizeof(dp_handoff_job) == 64, "dp_handoff_job layout");
 
-__device__ __forceinline__ void release_sys(uint32_t* row, int layer, int n_layer) {
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
-  asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(row + layer) : "memory");
-  asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(row + n_layer) : "memory");
+// Release pattern: ONE system-scope fence (after the CTA barrier, it orders
+// every store of the CTA), then relaxed reductions.  The consumers acquire.
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+__device__ __forceinline__ void add_relaxed_sys(uint32_t* row, int layer, int n_layer, uint32_t n) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(row + layer), "r"(n) : "memory");
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(row + n_layer), "r"(n) : "memory");
 }
+
 
 __global__ void __launch_bounds__(kThreads) kv_gather_dual(const __grid_constant__ DualParams p) {
   const int64_t total = p.item_begin[p.n_jobs];
@@ -897,10 +903,12 @@ __global__ void __launch_bounds__(kThreads) kv_gather_dual(const __grid_constant
     if (job.ticket >= 0 || dj.de_ticket >= 0) {
       __syncthreads();
       if (tid == 0) {
+        fence_sys();
         if (job.ticket >= 0)
-          release_sys(p.pe_ctr + static_cast<int64_t>(job.ticket) * (p.n_layer + 1), layer, p.n_layer);
+          add_relaxed_sys(p.pe_ctr + static_cast<int64_t>(job.ticket) * (p.n_layer + 1), layer, p.n_layer, 1);
         if (dj.de_ticket >= 0)
-          release_sys(p.de_ctr + static_cast<int64_t>(dj.de_ticket) * (p.n_layer + 1), layer, p.n_layer);
+          add_relaxed_sys(p.de_ctr + static_cast<int64_t>(dj.de_ticket) * (p.n_layer + 1), layer,
+                          p.n_layer, 1);
       }
     }
   }
@@ -914,24 +922,24 @@ __device__ __forceinline__ uint4 content_pair(uint64_t fb, uint64_t w, uint64_t 
                     static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32));
 }
 
+// K3 work unit: (layer, group of up to kHandoffGroup pieces), a piece being
+// one chunk of one prompt block; counters advance by the group's piece count,
+// so one system-scope fence covers up to kHandoffGroup * 36 KB of pushes.
+constexpr int kHandoffGroup = 4;
+
 __global__ void __launch_bounds__(kThreads) kv_prefill_handoff(const __grid_constant__ HandoffParams p) {
   const int64_t total = p.item_begin[p.n_jobs];
   const int tid = threadIdx.x;
+  const int64_t lb = p.lb_bytes;
   for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
     const int j = decode_job(p, item);
     const dp_handoff_job& job = p.jobs[j];
     const int64_t local = item - p.item_begin[j];
-    const int64_t per_layer = static_cast<int64_t>(job.n_blk) * p.n_chunk;
-    const int layer = static_cast<int>(local / per_layer);
-    const int64_t rem = local % per_layer;
-    const int blk = static_cast<int>(rem / p.n_chunk);
-    const int chunk = static_cast<int>(rem % p.n_chunk);
-    const int64_t tok0 = static_cast<int64_t>(blk) * p.block_tokens;
-    const int64_t lb = p.lb_bytes;
-    const int64_t hit_end = max(int64_t{0}, min(lb, (job.n_cached - tok0) * p.bpt));
-    const int64_t prompt_end = max(int64_t{0}, min(lb, (job.n_prompt - tok0) * p.bpt));
-    const int64_t beg = static_cast<int64_t>(chunk) * kChunkBytes;
-    const int64_t end = min(beg + kChunkBytes, prompt_end);
+    const int64_t pieces = static_cast<int64_t>(job.n_blk) * p.n_chunk;
+    const int64_t groups = (pieces + kHandoffGroup - 1) / kHandoffGroup;
+    const int layer = static_cast<int>(local / groups);
+    const int64_t piece0 = (local % groups) * kHandoffGroup;
+    const int64_t piece1 = min(piece0 + kHandoffGroup, pieces);
     // the layer gate: layer l's hit KV must have landed before "computing" l
     if (job.pe_ticket >= 0) {
       if (tid == 0) {
@@ -950,50 +958,62 @@ __global__ void __launch_bounds__(kThreads) kv_prefill_handoff(const __grid_cons
       }
       __syncthreads();
     }
-    const int64_t pe_off = layer * p.pe_stride + static_cast<int64_t>(job.pe_slot[blk]) * lb;
-    const int64_t de_off = layer * p.de_stride + static_cast<int64_t>(job.de_slot[blk]) * lb;
-    // hit part: PeToDe pushes it, MissMerge leaves it to the DE
-    const int64_t h1 = min(end, hit_end);
-    if (job.push_hit && h1 > beg) {
-      const uint4* src = reinterpret_cast<const uint4*>(p.pe_pool + pe_off + beg);
-      uint4* dst = reinterpret_cast<uint4*>(p.de_pool + de_off + beg);
-      const int n16 = static_cast<int>((h1 - beg) >> 4);
-      for (int base = 0; base < n16; base += kThreads * kUnroll) {
-        uint4 v[kUnroll];
+    for (int64_t piece = piece0; piece < piece1; ++piece) {
+      const int blk = static_cast<int>(piece / p.n_chunk);
+      const int chunk = static_cast<int>(piece % p.n_chunk);
+      const int64_t tok0 = static_cast<int64_t>(blk) * p.block_tokens;
+      const int64_t hit_end = max(int64_t{0}, min(lb, (job.n_cached - tok0) * p.bpt));
+      const int64_t prompt_end = max(int64_t{0}, min(lb, (job.n_prompt - tok0) * p.bpt));
+      const int64_t beg = static_cast<int64_t>(chunk) * kChunkBytes;
+      const int64_t end = min(beg + kChunkBytes, prompt_end);
+      const int64_t pe_off = layer * p.pe_stride + static_cast<int64_t>(job.pe_slot[blk]) * lb;
+      const int64_t de_off = layer * p.de_stride + static_cast<int64_t>(job.de_slot[blk]) * lb;
+      // hit part: PeToDe pushes it, MissMerge leaves it to the DE
+      const int64_t h1 = min(end, hit_end);
+      if (job.push_hit && h1 > beg) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.pe_pool + pe_off + beg);
+        uint4* dst = reinterpret_cast<uint4*>(p.de_pool + de_off + beg);
+        const int n16 = static_cast<int>((h1 - beg) >> 4);
+        for (int base = 0; base < n16; base += kThreads * kUnroll) {
+          uint4 v[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int i = base + u * kThreads + tid;
-          if (i < n16) v[u] = __ldcg(src + i);  // landed by another GPU: bypass L1
-        }
+          for (int u = 0; u < kUnroll; ++u) {
+            const int i = base + u * kThreads + tid;
+            if (i < n16) v[u] = __ldcg(src + i);  // landed by another GPU: bypass L1
+          }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int i = base + u * kThreads + tid;
-          if (i < n16) st_v4(dst + i, v[u]);
+          for (int u = 0; u < kUnroll; ++u) {
+            const int i = base + u * kThreads + tid;
+            if (i < n16) st_v4(dst + i, v[u]);
+          }
         }
       }
-    }
-    // miss part: the prefill stand-in's KV for tokens [C, C+A), written into
-    // the PE pool (its KV cache) and pushed to the DE pool
-    const int64_t m0 = max(beg, hit_end);
-    if (end > m0) {
-      const uint64_t fb = static_cast<uint64_t>(job.src_fb[blk]);
-      const uint64_t w_base = static_cast<uint64_t>((layer * lb) >> 3);
-      uint4* pe_dst = reinterpret_cast<uint4*>(p.pe_pool + pe_off);
-      uint4* de_dst = reinterpret_cast<uint4*>(p.de_pool + de_off);
-      for (int64_t i = (m0 >> 4) + tid; i < (end >> 4); i += kThreads) {
-        const uint4 v = content_pair(fb, w_base + 2 * static_cast<uint64_t>(i), p.seed_mix);
-        st_v4(pe_dst + i, v);
-        st_v4(de_dst + i, v);
+      // miss part: the prefill stand-in's KV for tokens [C, C+A), written into
+      // the PE pool (its KV cache) and pushed to the DE pool
+      const int64_t m0 = max(beg, hit_end);
+      if (end > m0) {
+        const uint64_t fb = static_cast<uint64_t>(job.src_fb[blk]);
+        const uint64_t w_base = static_cast<uint64_t>((layer * lb) >> 3);
+        uint4* pe_dst = reinterpret_cast<uint4*>(p.pe_pool + pe_off);
+        uint4* de_dst = reinterpret_cast<uint4*>(p.de_pool + de_off);
+        for (int64_t i = (m0 >> 4) + tid; i < (end >> 4); i += kThreads) {
+          const uint4 v = content_pair(fb, w_base + 2 * static_cast<uint64_t>(i), p.seed_mix);
+          st_v4(pe_dst + i, v);
+          st_v4(de_dst + i, v);
+        }
       }
     }
     if (job.de_ticket >= 0 || job.pe_done_ticket >= 0) {
       __syncthreads();
       if (tid == 0) {
+        const uint32_t n = static_cast<uint32_t>(piece1 - piece0);
+        fence_sys();
         if (job.de_ticket >= 0)
-          release_sys(p.de_ctr + static_cast<int64_t>(job.de_ticket) * (p.n_layer + 1), layer, p.n_layer);
+          add_relaxed_sys(p.de_ctr + static_cast<int64_t>(job.de_ticket) * (p.n_layer + 1), layer,
+                          p.n_layer, n);
         if (job.pe_done_ticket >= 0)
-          release_sys(p.pe_ctr + static_cast<int64_t>(job.pe_done_ticket) * (p.n_layer + 1), layer,
-                      p.n_layer);
+          add_relaxed_sys(p.pe_ctr + static_cast<int64_t>(job.pe_done_ticket) * (p.n_layer + 1), layer,
+                          p.n_layer, n);
       }
     }
   }
@@ -1103,7 +1123,8 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
           job.pe_done_ticket >= pe_pool->n_tickets ||
           (job.n_blk > 0 && (!job.src_fb || !job.pe_slot || !job.de_slot)))
         return fail(DP_EINVAL, "prefill_handoff: job " + std::to_string(j0 + j) + " out of range");
-      const int64_t n = static_cast<int64_t>(job.n_blk) * p.n_chunk * g.n_layer;
+      const int64_t pieces = static_cast<int64_t>(job.n_blk) * p.n_chunk;
+      const int64_t n = (pieces + kHandoffGroup - 1) / kHandoffGroup * g.n_layer;
       if (n == 0) continue;
       p.jobs[p.n_jobs] = job;
       p.item_begin[p.n_jobs] = items;
