@@ -199,8 +199,7 @@ int dp_h2d_layer_copy(dp_pool* pe, const dp_store* src, const dp_job* jobs, int3
 int dp_set_gather_ctas(int device, int32_t ctas);
 
 /* Cap on the CTAs of a K3 (dp_prefill_handoff) launch on `device` (0 =
- * default, 4 per SM).  K3 shares the PE with K1: fewer K3 CTAs leave the
- * register file to the loads. */
+ * default, 2 per SM: 699 GB/s of NVLink pushes, profiles/r01_SUMMARY.md). */
 int dp_set_handoff_ctas(int device, int32_t ctas);
 
 /* Items (landed-counter increments) per layer for a job of n_blk blocks. */

@@ -1109,7 +1109,7 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
   p.block_tokens = g.block_tokens;
   p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
   const int ho_cap = pe_pool->device < kMaxDevices ? g_handoff_ctas[pe_pool->device] : 0;
-  const int grid_cap = ho_cap > 0 ? ho_cap : sm_count(pe_pool->device) * 4;  // NVLink-bound
+  const int grid_cap = ho_cap > 0 ? ho_cap : sm_count(pe_pool->device) * 2;  // 699 GB/s NVLink (r01)
   auto s = static_cast<cudaStream_t>(stream);
   for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_HANDOFF_JOBS_PER_LAUNCH) {
     const int32_t nj = std::min<int32_t>(DP_MAX_HANDOFF_JOBS_PER_LAUNCH, n_jobs - j0);
