@@ -183,6 +183,36 @@ int dp_h2d_push_p2p_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* de_
 int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job* jobs,
                        int32_t n_jobs, uint64_t seed, int32_t timeout_ms, dp_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Decode-side persistence: every 64 generated tokens
+ * and at completion the DE persists the new tokens' KV to storage
+ * (PersistD2H -> PersistWrite, desim.cpp:666-672, :690-693, :764-771).
+ *
+ * A span job names a session-token range [tok_begin, tok_end) that lies in
+ * the session blocks blk0 .. blk0 + n_blk - 1; slot[i] is block blk0+i's slot
+ * in the decode pool and fb[i] its storage Full Block. */
+typedef struct dp_span_job {
+  const int32_t* slot;  /* [n_blk] decode-pool slots */
+  const int64_t* fb;    /* [n_blk] storage Full Blocks (content ids / persist targets) */
+  int64_t blk0;         /* session block of slot[0] */
+  int64_t tok_begin;    /* session tokens [tok_begin, tok_end) */
+  int64_t tok_end;
+  int32_t n_blk;
+  int32_t reserved;
+} dp_span_job;
+
+#define DP_MAX_SPAN_JOBS_PER_LAUNCH 64
+
+/* Decode stand-in: writes the KV of generated tokens (the storage content
+ * formula with `seed`, i.e. what the turn will persist) into the decode pool. */
+int dp_decode_fill(dp_pool* de_pool, const dp_span_job* jobs, int32_t n_jobs, uint64_t seed,
+                   dp_stream stream);
+/* K4 (PersistD2H): gathers the span's tokens of every layer from the decode
+ * pool's layer planes into Full Blocks [L][T][b] of the pinned host `target`
+ * (the storage tier), zero-copy stores over the DE's PCIe. */
+int dp_persist_d2h(const dp_pool* de_pool, dp_store* target, const dp_span_job* jobs,
+                   int32_t n_jobs, dp_stream stream);
+
 /* K1 on the copy engine (no SMs): the same transfer as dp_h2d_layer_gather,
  * issued as one strided cudaMemcpy2DAsync per contiguous run of blocks per
  * layer (Full-Block pitch -> Layer-Block pitch) plus the partial last block,

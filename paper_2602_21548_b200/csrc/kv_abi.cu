@@ -1140,3 +1140,155 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
 }
 
 }  // extern "C"
+
+// ============================================================ persistence
+// dp_decode_fill (decode stand-in) and dp_persist_d2h (K4, PersistD2H).
+namespace {
+
+struct SpanParams {
+  char* pool;
+  char* host;            // K4: target Full Blocks (device-visible host pointer)
+  int64_t pool_stride;   // layer plane
+  int64_t lb_bytes, fb_bytes, bpt;
+  uint64_t seed_mix;
+  int32_t n_layer, block_tokens, n_chunk, n_jobs;
+  int64_t item_begin[DP_MAX_SPAN_JOBS_PER_LAUNCH + 1];
+  dp_span_job jobs[DP_MAX_SPAN_JOBS_PER_LAUNCH];
+};
+static_assert(sizeof(SpanParams) <= 4000, "kernel parameter block too large");
+static_assert(sizeof(dp_span_job) == 48, "dp_span_job layout");
+
+// item -> (job, block i, layer, chunk) and the byte range of the span inside
+// that Layer Block; false when the chunk holds none of the span.
+struct SpanItem {
+  int j, i, layer;
+  int64_t beg, end;  // bytes within the Layer Block
+};
+
+__device__ __forceinline__ bool span_item(const SpanParams& p, int64_t item, SpanItem& it) {
+  it.j = decode_job(p, item);
+  const dp_span_job& job = p.jobs[it.j];
+  const int64_t local = item - p.item_begin[it.j];
+  const int64_t per_block = static_cast<int64_t>(p.n_layer) * p.n_chunk;
+  it.i = static_cast<int>(local / per_block);
+  const int64_t rem = local % per_block;
+  it.layer = static_cast<int>(rem / p.n_chunk);
+  const int chunk = static_cast<int>(rem % p.n_chunk);
+  const int64_t blk_tok0 = (job.blk0 + it.i) * p.block_tokens;
+  const int64_t t0 = max(job.tok_begin, blk_tok0) - blk_tok0;
+  const int64_t t1 = min(job.tok_end, blk_tok0 + p.block_tokens) - blk_tok0;
+  it.beg = max(t0 * p.bpt, static_cast<int64_t>(chunk) * kChunkBytes);
+  it.end = min(t1 * p.bpt, static_cast<int64_t>(chunk + 1) * kChunkBytes);
+  return it.end > it.beg;
+}
+
+__global__ void __launch_bounds__(kThreads) kv_decode_fill(const __grid_constant__ SpanParams p) {
+  const int64_t total = p.item_begin[p.n_jobs];
+  for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+    SpanItem it;
+    if (!span_item(p, item, it)) continue;
+    const dp_span_job& job = p.jobs[it.j];
+    uint4* dst = reinterpret_cast<uint4*>(p.pool + it.layer * p.pool_stride +
+                                          static_cast<int64_t>(job.slot[it.i]) * p.lb_bytes);
+    const uint64_t fb = static_cast<uint64_t>(job.fb[it.i]);
+    const uint64_t w_base = static_cast<uint64_t>((it.layer * p.lb_bytes) >> 3);
+    for (int64_t v = (it.beg >> 4) + threadIdx.x; v < (it.end >> 4); v += kThreads)
+      st_v4(dst + v, content_pair(fb, w_base + 2 * static_cast<uint64_t>(v), p.seed_mix));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) kv_persist_d2h(const __grid_constant__ SpanParams p) {
+  const int64_t total = p.item_begin[p.n_jobs];
+  const int tid = threadIdx.x;
+  for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+    SpanItem it;
+    if (!span_item(p, item, it)) continue;
+    const dp_span_job& job = p.jobs[it.j];
+    const uint4* src = reinterpret_cast<const uint4*>(p.pool + it.layer * p.pool_stride +
+                                                      static_cast<int64_t>(job.slot[it.i]) * p.lb_bytes + it.beg);
+    uint4* dst = reinterpret_cast<uint4*>(p.host + job.fb[it.i] * p.fb_bytes + it.layer * p.lb_bytes + it.beg);
+    const int n16 = static_cast<int>((it.end - it.beg) >> 4);
+    for (int base = 0; base < n16; base += kThreads * kUnroll) {
+      uint4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int i = base + u * kThreads + tid;
+        if (i < n16) v[u] = __ldcg(src + i);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int i = base + u * kThreads + tid;
+        if (i < n16) st_v4(dst + i, v[u]);
+      }
+    }
+  }
+}
+
+template <class Kernel>
+int launch_span(const dp_pool* pool, const dp_store* target, const dp_span_job* jobs, int32_t n_jobs,
+                uint64_t seed, dp_stream stream, Kernel kernel, const char* what) {
+  if (!pool || (n_jobs > 0 && !jobs) || n_jobs < 0) return fail(DP_EINVAL, std::string(what) + ": bad argument");
+  if (!pool->owner) return fail(DP_EINVAL, std::string(what) + ": the decode pool must be local");
+  if (target && !geom_equal(pool->geom, target->geom))
+    return fail(DP_EINVAL, std::string(what) + ": geometry differs");
+  const dp_kv_geom& g = pool->geom;
+  DeviceGuard guard(pool->device);
+  SpanParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.pool = pool->base;
+  p.host = target ? target->host : nullptr;
+  p.lb_bytes = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
+  p.fb_bytes = p.lb_bytes * g.n_layer;
+  p.bpt = g.bytes_per_token_layer;
+  p.pool_stride = p.lb_bytes * pool->n_slots;
+  p.seed_mix = seed * kSeedMul;
+  p.n_layer = g.n_layer;
+  p.block_tokens = g.block_tokens;
+  p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
+  auto s = static_cast<cudaStream_t>(stream);
+  const int grid_cap = sm_count(pool->device) * 4;
+  for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_SPAN_JOBS_PER_LAUNCH) {
+    const int32_t nj = std::min<int32_t>(DP_MAX_SPAN_JOBS_PER_LAUNCH, n_jobs - j0);
+    p.n_jobs = 0;
+    int64_t items = 0;
+    for (int32_t j = 0; j < nj; ++j) {
+      const dp_span_job& job = jobs[j0 + j];
+      const int64_t T = g.block_tokens;
+      if (job.n_blk < 0 || job.blk0 < 0 || job.tok_begin < job.blk0 * T || job.tok_end < job.tok_begin ||
+          job.tok_end > (job.blk0 + job.n_blk) * T || (job.n_blk > 0 && (!job.slot || !job.fb)))
+        return fail(DP_EINVAL, std::string(what) + ": job " + std::to_string(j0 + j) + " out of range");
+      const int64_t n = static_cast<int64_t>(job.n_blk) * g.n_layer * p.n_chunk;
+      if (n == 0 || job.tok_end == job.tok_begin) continue;
+      p.jobs[p.n_jobs] = job;
+      p.item_begin[p.n_jobs] = items;
+      ++p.n_jobs;
+      items += n;
+    }
+    p.item_begin[p.n_jobs] = items;
+    if (items == 0) continue;
+    kernel<<<static_cast<int>(std::min<int64_t>(items, grid_cap)), kThreads, 0, s>>>(p);
+    DP_CUDA(cudaGetLastError());
+  }
+  return DP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dp_decode_fill(dp_pool* de_pool, const dp_span_job* jobs, int32_t n_jobs, uint64_t seed,
+                   dp_stream stream) {
+  return launch_span(de_pool, nullptr, jobs, n_jobs, seed, stream, kv_decode_fill, "decode_fill");
+}
+
+int dp_persist_d2h(const dp_pool* de_pool, dp_store* target, const dp_span_job* jobs, int32_t n_jobs,
+                   dp_stream stream) {
+  if (!target) return fail(DP_EINVAL, "persist_d2h: null target");
+  for (int32_t j = 0; j < n_jobs; ++j)
+    for (int32_t i = 0; i < jobs[j].n_blk; ++i)
+      if (jobs[j].fb[i] < 0 || jobs[j].fb[i] >= target->n_fb)
+        return fail(DP_EINVAL, "persist_d2h: target Full Block out of range");
+  return launch_span(de_pool, target, jobs, n_jobs, 0, stream, kv_persist_d2h, "persist_d2h");
+}
+
+}  // extern "C"
