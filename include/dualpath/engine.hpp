@@ -58,6 +58,10 @@ struct ExecOptions {
   // SMs) for the whole request's hit KV; 1 = K3 gates layer by layer in-kernel
   std::int32_t k3_layer_gate = 0;
   std::int32_t handoff_ctas = 0;       // K3 CTA cap on PEs (0 = default)
+  // Decode-side persistence (needs `handoff`): each DE runs
+  // the decode stand-in for the generated tokens and persists them (K4) every
+  // 64 generated tokens plus the final partial, into its persist store
+  bool persist = false;
 };
 
 // One request's hit-KV transfer (all layers), in global execution order.
@@ -90,6 +94,10 @@ struct LoadJob {
   std::vector<std::uint32_t> pe_done_targets;  // job's dual gather waits for (PE slot reuse)
   std::vector<std::int32_t> de_preds;      // decode-pool rows of the previous occupants of
   std::vector<std::uint32_t> de_pred_targets;  // this job's DE slots
+  // ---- persistence ----
+  std::int64_t gen = 0;          // generated tokens of the turn
+  std::int32_t n_tblk = 0;       // decode-pool blocks: ceil((C + A + gen) / T)
+  std::int64_t dec_off = 0;      // offset of its blocks in the DE's decode tables
 };
 
 struct ExecPlan {
@@ -127,6 +135,13 @@ struct ExecPlan {
   std::vector<std::vector<std::int32_t>> ho_de_slot;       // per PE: prompt blocks' DE slots
   std::vector<std::vector<std::int32_t>> dual_de_slot;     // per reader: hit blocks' DE slots
   std::int64_t handoff_bytes = 0;  // pushed by K3: (C+A)*L*b PE path, A*L*b DE path
+  bool persist = false;
+  std::vector<std::vector<std::int32_t>> dec_slot;         // per DE: all blocks' decode slots
+  std::vector<std::vector<std::int64_t>> dec_fb;           // per DE: their storage Full Blocks
+  std::int64_t persist_bytes = 0;                          // sum gen * L * b
+  // persist chunks of a job, [token begin, end): the reference's
+  // persist_tokens at every block_size generated tokens + the final partial
+  std::vector<std::pair<std::int64_t, std::int64_t>> persist_chunks(const LoadJob& j) const;
   std::uint32_t de_total_items(const LoadJob& j) const;    // decode-pool row target (all layers)
 };
 
@@ -223,6 +238,14 @@ class EngineRuntime {
   std::vector<std::int64_t> pe_done_off_;   // per job: offset of its pe_done_preds
   std::int64_t final_wait_off_ = 0;         // DE: all own tickets (decode-ready gate)
   std::int32_t final_wait_n_ = 0;
+  // ---- persistence (DE) ----
+  dp_store* persist_store_ = nullptr;
+  std::int32_t* d_dec_slot_ = nullptr;
+  std::int64_t* d_dec_fb_ = nullptr;
+
+ public:
+  // Bytes of Layer Block `layer` of Full Block `fb` in this DE's persist store.
+  std::vector<std::uint8_t> read_persisted(std::int64_t fb, int layer) const;
 };
 
 // Runs run_step() of several same-process engines concurrently (one host

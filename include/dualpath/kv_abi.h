@@ -248,6 +248,11 @@ int dp_wait_tickets(const dp_pool* pool, const int32_t* tickets, const uint32_t*
  * producers that are known to run (the executor's whole-request gate). */
 int dp_stream_wait_counter(const dp_pool* pool, int32_t ticket, int32_t layer, uint32_t target,
                            dp_stream stream);
+/* Stream-ordered, fenced write of landed[ticket][layer] = value on a LOCAL
+ * pool (cuStreamWriteValue32): marks the completion of copy-engine or
+ * stream-ordered work that has no kernel of its own to release a counter. */
+int dp_stream_write_counter(dp_pool* pool, int32_t ticket, int32_t layer, uint32_t value,
+                            dp_stream stream);
 /* Returns DP_ETIMEOUT if any wait on this device's pool has timed out. */
 int dp_wait_status(const dp_pool* pool);
 

@@ -49,6 +49,12 @@ class HandoffJob(ctypes.Structure):
                 ("pe_done_ticket", ctypes.c_int32)]
 
 
+class SpanJob(ctypes.Structure):
+    _fields_ = [("slot", ctypes.c_void_p), ("fb", ctypes.c_void_p), ("blk0", ctypes.c_int64),
+                ("tok_begin", ctypes.c_int64), ("tok_end", ctypes.c_int64), ("n_blk", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
 class PoolHandle(ctypes.Structure):
     _fields_ = [("ipc", ctypes.c_ubyte * 64), ("geom", Geom), ("n_slots", ctypes.c_int32),
                 ("n_tickets", ctypes.c_int32), ("device", ctypes.c_int32),
@@ -99,6 +105,9 @@ def lib():
                             ctypes.c_int),
         "dp_wait_status": ([P], ctypes.c_int),
         "dp_stream_wait_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
+        "dp_stream_write_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
+        "dp_decode_fill": ([P, ctypes.POINTER(SpanJob), ctypes.c_int32, ctypes.c_uint64, P], ctypes.c_int),
+        "dp_persist_d2h": ([P, P, ctypes.POINTER(SpanJob), ctypes.c_int32, P], ctypes.c_int),
         "dp_pool_checksum": ([P, ctypes.c_int32, P, P, ctypes.c_int32, P, P], ctypes.c_int),
         "dp_pool_copy_out": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P], ctypes.c_int),
         "dp_device_count": ([], ctypes.c_int),
@@ -248,6 +257,18 @@ def wait_layer(pool, ticket, layer, target, timeout_ms=10000, stream=0):
 
 def stream_wait_counter(pool, ticket, layer, target, stream=0):
     check(lib().dp_stream_wait_counter(pool.ptr, ticket, layer, target, ctypes.c_void_p(stream)))
+
+
+def stream_write_counter(pool, ticket, layer, value, stream=0):
+    check(lib().dp_stream_write_counter(pool.ptr, ticket, layer, value, ctypes.c_void_p(stream)))
+
+
+def decode_fill(pool, jobs, n, seed, stream=0):
+    check(lib().dp_decode_fill(pool.ptr, jobs, n, seed, ctypes.c_void_p(stream)))
+
+
+def persist_d2h(pool, target, jobs, n, stream=0):
+    check(lib().dp_persist_d2h(pool.ptr, target.ptr, jobs, n, ctypes.c_void_p(stream)))
 
 
 def wait_status(pool):

@@ -336,6 +336,7 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("gather_ctas", &dualpath::ExecOptions::gather_ctas)
       .def_readwrite("k3_layer_gate", &dualpath::ExecOptions::k3_layer_gate)
       .def_readwrite("handoff_ctas", &dualpath::ExecOptions::handoff_ctas)
+      .def_readwrite("persist", &dualpath::ExecOptions::persist)
       .def_readwrite("store_fb", &dualpath::ExecOptions::store_fb)
       .def_readwrite("store_bytes_max", &dualpath::ExecOptions::store_bytes_max)
       .def_readwrite("seed", &dualpath::ExecOptions::seed)
@@ -358,6 +359,10 @@ PYBIND11_MODULE(_core, m) {
       .def_readonly("requests", &dualpath::ExecPlan::requests)
       .def_readonly("handoff", &dualpath::ExecPlan::handoff)
       .def_readonly("handoff_bytes", &dualpath::ExecPlan::handoff_bytes)
+      .def_readonly("persist", &dualpath::ExecPlan::persist)
+      .def_readonly("persist_bytes", &dualpath::ExecPlan::persist_bytes)
+      .def("persist_chunks", [](const dualpath::ExecPlan& x, int job) { return x.persist_chunks(x.jobs.at(job)); })
+      .def("job_gen", [](const dualpath::ExecPlan& x, int job) { return x.jobs.at(job).gen; })
       .def_readonly("de_pool_slots", &dualpath::ExecPlan::de_pool_slots)
       .def_readonly("de_peak_slots", &dualpath::ExecPlan::de_peak_slots)
       .def_readonly("n_de_tickets", &dualpath::ExecPlan::n_de_tickets)
@@ -455,7 +460,11 @@ PYBIND11_MODULE(_core, m) {
       .def("checksum",
            [](dualpath::EngineRuntime& e, int layer, const std::vector<std::int32_t>& slots,
               const std::vector<std::int32_t>& ntok) { return e.checksum(layer, slots, ntok); })
-      .def("counters", &dualpath::EngineRuntime::counters);
+      .def("counters", &dualpath::EngineRuntime::counters)
+      .def("read_persisted", [](const dualpath::EngineRuntime& e, std::int64_t fb, int layer) {
+        const auto v = e.read_persisted(fb, layer);
+        return py::bytes(reinterpret_cast<const char*>(v.data()), v.size());
+      });
 
   m.def(
       "run_step_all",

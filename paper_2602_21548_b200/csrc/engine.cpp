@@ -127,6 +127,20 @@ std::uint32_t ExecPlan::de_total_items(const LoadJob& j) const {
   return static_cast<std::uint32_t>(blocks * items_per_block * cfg.n_layer);
 }
 
+std::vector<std::pair<std::int64_t, std::int64_t>> ExecPlan::persist_chunks(const LoadJob& j) const {
+  // persist_tokens(rq, k) at decode milestones k % T == 0 (k < gen) and at
+  // completion with k = gen (desim.cpp:658-661, :690-693, :760)
+  std::vector<std::pair<std::int64_t, std::int64_t>> out;
+  const std::int64_t T = cfg.block_size_tokens;
+  std::int64_t done = 0;
+  for (std::int64_t k = T; k < j.gen; k += T) {
+    out.emplace_back(j.prompt + done, j.prompt + k);
+    done = k;
+  }
+  if (j.gen > done) out.emplace_back(j.prompt + done, j.prompt + j.gen);
+  return out;
+}
+
 ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
                          std::span<const pdsim::Trajectory> trajectories,
                          const pdsim::desim::SimReport& plan, const ExecOptions& opt) {
@@ -135,6 +149,8 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
   x.cfg = cfg;
   x.opt = opt;
   x.handoff = opt.handoff;
+  x.persist = opt.persist;
+  if (x.persist && !x.handoff) throw std::invalid_argument("build_exec_plan: persist needs handoff");
   x.n_engines = cfg.total_engines();
   x.n_pe = cfg.prefill_nodes * cfg.engines_per_node;
   x.geom = {cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer};
@@ -184,6 +200,8 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     j.prompt = r.cached + r.append;
     j.n_blk = static_cast<std::int32_t>((r.cached + T - 1) / T);
     j.n_pblk = x.handoff ? static_cast<std::int32_t>((j.prompt + T - 1) / T) : j.n_blk;
+    j.gen = r.gen;
+    j.n_tblk = x.persist ? static_cast<std::int32_t>((j.prompt + j.gen + T - 1) / T) : j.n_pblk;
     j.t_admit = r.t_admit;
     j.t_read_done = r.t_read_done;
     const int idx = static_cast<int>(jobs.size());
@@ -191,7 +209,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     pe_of.push_back(r.pe);
     de_of.push_back(std::max(0, r.de));
     pblocks.push_back(jobs.back().n_pblk);
-    dblocks.push_back(jobs.back().n_pblk);
+    dblocks.push_back(jobs.back().n_tblk);
     pe_evs.push_back({r.t_read_done, 1, r.request_id, idx});
     if (r.t_pe_release >= 0) pe_evs.push_back({r.t_pe_release, 0, r.request_id, idx});
     if (x.handoff) {
@@ -273,7 +291,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
         continue;
       }
       j.de_ticket = x.n_de_tickets[j.de]++;
-      for (std::int32_t k = 0; k < j.n_pblk; ++k) {
+      for (std::int32_t k = 0; k < j.n_tblk; ++k) {
         const std::int32_t s = q.take(0);
         de_slots[e.job].push_back(s);
         const std::int32_t prev = q.owner[s];
@@ -284,7 +302,9 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
           throw std::logic_error("build_exec_plan: decode-slot predecessor is not earlier");
         if (std::find(j.de_preds.begin(), j.de_preds.end(), pj.de_ticket) == j.de_preds.end()) {
           j.de_preds.push_back(pj.de_ticket);
-          j.de_pred_targets.push_back(x.de_total_items(pj));
+          // with persistence the slot is free once the occupant is persisted
+          // (its "persist done" row, resolved at run time, reads 1)
+          j.de_pred_targets.push_back(x.persist ? 1u : x.de_total_items(pj));
         }
       }
     }
@@ -296,6 +316,8 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
   x.src_fb.assign(x.n_engines, {});
   x.slots.assign(x.n_engines, {});
   x.dual_de_slot.assign(x.n_engines, {});
+  x.dec_slot.assign(x.n_engines, {});
+  x.dec_fb.assign(x.n_engines, {});
   x.ho_src_fb.assign(x.n_pe, {});
   x.ho_pe_slot.assign(x.n_pe, {});
   x.ho_de_slot.assign(x.n_pe, {});
@@ -322,6 +344,14 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
       }
       x.handoff_bytes += (j.de_path ? j.prompt - j.cached : j.prompt) * cfg.kv_bytes_per_token();
       x.by_de[j.de].push_back(idx);
+      if (x.persist) {
+        j.dec_off = static_cast<std::int64_t>(x.dec_slot[j.de].size());
+        for (std::int32_t k = 0; k < j.n_tblk; ++k) {
+          x.dec_slot[j.de].push_back(de_slots[old][k]);
+          x.dec_fb[j.de].push_back(x.fb_of(j.traj, k));
+        }
+        x.persist_bytes += j.gen * cfg.kv_bytes_per_token();
+      }
     }
     const std::int64_t bytes = j.cached * cfg.kv_bytes_per_token();
     x.reader_bytes[j.reader] += bytes;
@@ -358,9 +388,12 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
     check(dp_pool_create(device_, &x.geom, x.pool_slots, rows, &pool_), "dp_pool_create");
     peers_[engine_] = pool_;
   } else if (x.handoff) {
-    check(dp_pool_create(device_, &x.geom, x.de_pool_slots,
-                         std::max<std::int32_t>(1, x.n_de_tickets[engine_]), &pool_),
-          "dp_pool_create (decode pool)");
+    // rows [0, n) prompt landed; with persistence rows [n, 2n) persisted
+    const std::int32_t rows = std::max<std::int32_t>(1, x.n_de_tickets[engine_]) * (x.persist ? 2 : 1);
+    check(dp_pool_create(device_, &x.geom, x.de_pool_slots, rows, &pool_), "dp_pool_create (decode pool)");
+    if (x.persist && !x.by_de[engine_].empty())  // content seed + 1: unwritten bytes differ
+      check(dp_store_create(device_, &x.geom, x.store_fb, x.opt.seed + 1, &persist_store_),
+            "dp_store_create (persist store)");
   }
   if (x.handoff) {
     upload_handoff_tables();
@@ -384,12 +417,14 @@ EngineRuntime::~EngineRuntime() {
     if (v) dp_pool_destroy(v);
   if (pool_) dp_pool_destroy(pool_);
   if (store_) dp_store_destroy(store_);
+  if (persist_store_) dp_store_destroy(persist_store_);
   for (void* p : {static_cast<void*>(d_src_), static_cast<void*>(d_slots_),
                   static_cast<void*>(d_wait_tickets_), static_cast<void*>(d_wait_targets_),
                   static_cast<void*>(d_pred_tickets_), static_cast<void*>(d_pred_targets_),
                   static_cast<void*>(d_ho_src_), static_cast<void*>(d_ho_pe_),
                   static_cast<void*>(d_ho_de_), static_cast<void*>(d_dual_de_),
-                  static_cast<void*>(d_wt_), static_cast<void*>(d_wg_)})
+                  static_cast<void*>(d_wt_), static_cast<void*>(d_wg_),
+                  static_cast<void*>(d_dec_slot_), static_cast<void*>(d_dec_fb_)})
     if (p) cudaFree(p);
   for (void* e : ev_load_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* e : ev_k3_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
@@ -457,7 +492,7 @@ void EngineRuntime::upload_handoff_tables() {
       ev_k3_.push_back(b);
       const LoadJob& j = x.jobs[mine[i]];
       de_wait_off_[mine[i]] = static_cast<std::int64_t>(wt.size());
-      wt.insert(wt.end(), j.de_preds.begin(), j.de_preds.end());
+      for (std::int32_t t : j.de_preds) wt.push_back(t + (x.persist ? x.n_de_tickets[j.de] : 0));
       wg.insert(wg.end(), j.de_pred_targets.begin(), j.de_pred_targets.end());
     }
   }
@@ -470,7 +505,7 @@ void EngineRuntime::upload_handoff_tables() {
     wg.insert(wg.end(), j.pe_done_targets.begin(), j.pe_done_targets.end());
     if (de_wait_off_[ji] < 0) {  // a DE reading for its own decode pool (always: reader == de)
       de_wait_off_[ji] = static_cast<std::int64_t>(wt.size());
-      wt.insert(wt.end(), j.de_preds.begin(), j.de_preds.end());
+      for (std::int32_t t : j.de_preds) wt.push_back(t + (x.persist ? x.n_de_tickets[j.de] : 0));
       wg.insert(wg.end(), j.de_pred_targets.begin(), j.de_pred_targets.end());
     }
   }
@@ -484,6 +519,13 @@ void EngineRuntime::upload_handoff_tables() {
   }
   d_wt_ = upload(wt);
   d_wg_ = upload(wg);
+  if (x.persist && !is_pe()) {
+    d_dec_slot_ = upload(x.dec_slot[engine_]);
+    d_dec_fb_ = upload(x.dec_fb[engine_]);
+    cudaStream_t h;
+    check_cuda(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking), "cudaStreamCreate");
+    stream_h_ = h;  // the decode stream: decode stand-in + persistence
+  }
 }
 
 dp_pool_handle EngineRuntime::export_pool() const {
@@ -740,13 +782,41 @@ StepResult EngineRuntime::run_step_handoff() {
       check(dp_h2d_push_p2p_dual(peers_[j.pe], pool_, store_, &dj, 1, s), "dp_h2d_push_p2p_dual");
       ++res.launches;
     }
-    if (final_wait_n_ > 0) {  // decode-ready: every prompt landed in this decode pool
-      check(dp_wait_tickets(pool_, d_wt_ + final_wait_off_, d_wg_ + final_wait_off_, final_wait_n_, L,
-                            x.opt.wait_timeout_ms, s),
-            "dp_wait_tickets (decode ready)");
-      ++res.launches;
+    if (x.persist) {
+      // decode stream: per request, once its whole prompt has landed (no SMs
+      // while waiting): decode stand-in for the generated tokens, then K4
+      // persists them chunk by chunk, then its "persist done" row is set
+      const std::int64_t T = x.cfg.block_size_tokens;
+      for (int ji : x.by_de[engine_]) {
+        const LoadJob& j = x.jobs[ji];
+        check(dp_stream_wait_counter(pool_, j.de_ticket, L, x.de_total_items(j), h),
+              "dp_stream_wait_counter (decode ready)");
+        const std::int64_t blk0 = j.prompt / T;
+        const std::int32_t nb = j.n_tblk - static_cast<std::int32_t>(blk0);
+        const dp_span_job fill{d_dec_slot_ + j.dec_off + blk0, d_dec_fb_ + j.dec_off + blk0, blk0,
+                               j.prompt, j.prompt + j.gen, nb, 0};
+        check(dp_decode_fill(pool_, &fill, 1, x.opt.seed, h), "dp_decode_fill");
+        std::vector<dp_span_job> chunks;
+        for (const auto& [t0, t1] : x.persist_chunks(j))
+          chunks.push_back(dp_span_job{fill.slot, fill.fb, blk0, t0, t1, nb, 0});
+        check(dp_persist_d2h(pool_, persist_store_, chunks.data(), static_cast<int32_t>(chunks.size()), h),
+              "dp_persist_d2h");
+        check(dp_stream_write_counter(pool_, j.de_ticket + x.n_de_tickets[engine_], L, 1, h),
+              "dp_stream_write_counter");
+        res.launches += 2;
+      }
+      check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), s), "cudaEventRecord");
+      check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_end_), 0), "cudaStreamWaitEvent");
+      check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), h), "cudaEventRecord");
+    } else {
+      if (final_wait_n_ > 0) {  // decode-ready: every prompt landed in this decode pool
+        check(dp_wait_tickets(pool_, d_wt_ + final_wait_off_, d_wg_ + final_wait_off_, final_wait_n_, L,
+                              x.opt.wait_timeout_ms, s),
+              "dp_wait_tickets (decode ready)");
+        ++res.launches;
+      }
+      check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), s), "cudaEventRecord");
     }
-    check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), s), "cudaEventRecord");
   }
   check_cuda(cudaEventSynchronize(static_cast<cudaEvent_t>(ev_end_)), "step sync");
   if (pool_) check(dp_wait_status(pool_), "transfer watchdog");
@@ -786,6 +856,19 @@ std::vector<std::uint64_t> EngineRuntime::checksum(int layer, std::span<const st
   return out;
 }
 
+std::vector<std::uint8_t> EngineRuntime::read_persisted(std::int64_t fb, int layer) const {
+  if (!persist_store_) throw std::logic_error("read_persisted: this engine persists nothing");
+  void* host = nullptr;
+  std::int64_t bytes = 0, n_fb = 0;
+  check(dp_store_info(persist_store_, &host, &bytes, &n_fb), "dp_store_info");
+  const ExecPlan& x = *plan_;
+  if (fb < 0 || fb >= n_fb || layer < 0 || layer >= x.cfg.n_layer)
+    throw std::out_of_range("read_persisted: Full Block / layer out of range");
+  const std::int64_t lb = x.cfg.layer_block_bytes();
+  const auto* p = static_cast<const std::uint8_t*>(host) + fb * x.cfg.full_block_bytes() + layer * lb;
+  return std::vector<std::uint8_t>(p, p + lb);
+}
+
 std::vector<std::uint32_t> EngineRuntime::counters() const {
   if (!pool_) return {};
   DeviceScope ds(device_);
@@ -795,7 +878,7 @@ std::vector<std::uint32_t> EngineRuntime::counters() const {
   check(dp_pool_info(pool_, &base, &ctr, &bytes), "dp_pool_info");
   const ExecPlan& x = *plan_;
   const std::int32_t rows = is_pe() ? std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff ? 2 : 1)
-                                    : std::max<std::int32_t>(1, x.n_de_tickets[engine_]);
+                                    : std::max<std::int32_t>(1, x.n_de_tickets[engine_]) * (x.persist ? 2 : 1);
   const std::size_t n = static_cast<std::size_t>(rows) * (x.cfg.n_layer + 1);
   std::vector<std::uint32_t> out(n);
   check_cuda(cudaMemcpy(out.data(), ctr, n * 4, cudaMemcpyDeviceToHost), "counters D2H");

@@ -711,6 +711,21 @@ int dp_stream_wait_counter(const dp_pool* pool, int32_t ticket, int32_t layer, u
   return DP_OK;
 }
 
+int dp_stream_write_counter(dp_pool* pool, int32_t ticket, int32_t layer, uint32_t value,
+                            dp_stream stream) {
+  if (!pool) return fail(DP_EINVAL, "stream_write_counter: null pool");
+  if (!pool->owner) return fail(DP_EINVAL, "stream_write_counter: the pool must be local");
+  if (ticket < 0 || ticket >= pool->n_tickets || layer < 0 || layer > pool->geom.n_layer)
+    return fail(DP_EINVAL, "stream_write_counter: ticket/layer out of range");
+  const WriteValue32Fn wv = write_value32();
+  if (!wv) return fail(DP_ECUDA, "stream_write_counter: cuStreamWriteValue32 unavailable");
+  DeviceGuard guard(pool->device);
+  uint32_t* ctr = pool->counters + static_cast<int64_t>(ticket) * (pool->geom.n_layer + 1) + layer;
+  if (wv(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(ctr), value, 0) != CUDA_SUCCESS)
+    return fail(DP_ECUDA, "stream_write_counter: cuStreamWriteValue32 failed");
+  return DP_OK;
+}
+
 int dp_set_handoff_ctas(int device, int32_t ctas) {
   if (device < 0 || device >= kMaxDevices || ctas < 0)
     return fail(DP_EINVAL, "set_handoff_ctas: bad argument");

@@ -181,3 +181,49 @@ def test_handoff_plan_invariants(P, D, tight):
         assert t == list(range(len(t))) and len(t) == xp.n_de_tickets[d]
     if tight:
         assert any(j[19] for j in jobs)  # decode-slot reuse hazards exercised
+
+
+def test_persist_chunks_match_the_reference_ledger():
+    """PersistD2H ledger (proj/tests/test_desim.cpp:168-188): the executor's
+    persist chunks equal, request by request, the planner's PersistD2H flows
+    (bit-identical to the reference's)."""
+    cfg = cluster(1, 1)
+    trajs = dp.synthesize(max_len=20000, count=8, seed=3, mean_turns=5, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, flows=True, **SB)
+    opt = dp.ExecOptions()
+    opt.handoff = True
+    opt.persist = True
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    per_tok = cfg.kv_bytes_per_token()
+    flows = {}
+    for req, stage, nbytes, t0, t1 in planned["flows"]:
+        if stage == 8:  # PersistD2H
+            flows.setdefault(req, []).append(nbytes)
+    total = 0
+    for i, j in enumerate(xp.jobs()):
+        chunks = xp.persist_chunks(i)
+        assert [(b - a) * per_tok for a, b in chunks] == flows[j[0]]
+        assert chunks[0][0] == j[14] and chunks[-1][1] == j[14] + xp.job_gen(i)
+        total += xp.job_gen(i) * per_tok
+    assert total == xp.persist_bytes
+    # the KATs of test_desim.cpp:168-188: gen 130 -> 64, 64, 2; gen 64 -> one block
+    t = dp.Trajectory()
+    t.id = "t"
+    t.rounds = [dp.Round(32, 130)]
+    u = dp.Trajectory()
+    u.id = "u"
+    u.rounds = [dp.Round(32, 64)]
+    planned = dp.plan(cfg, [t, u], **SB)
+    xp = dp.build_exec_plan(cfg, [t, u], planned, opt)
+    sizes = sorted([b - a for a, b in xp.persist_chunks(i)] for i in range(2))
+    assert sizes == [[64], [64, 64, 2]]
+
+
+def test_persist_requires_handoff():
+    cfg = cluster(1, 1)
+    trajs = dp.synthesize(max_len=8000, count=2, seed=3, mean_turns=2, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, **SB)
+    opt = dp.ExecOptions()
+    opt.persist = True
+    with pytest.raises(ValueError, match="handoff"):
+        dp.build_exec_plan(cfg, trajs, planned, opt)

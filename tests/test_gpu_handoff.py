@@ -182,3 +182,53 @@ def test_stream_wait_counter_orders_a_stream(two_gpus):
     finally:
         for x in (de_view, pe_view, de_pool, pe_pool, st_de):
             x.close()
+
+
+# ------------------------------------------------------------ persistence
+@pytest.mark.parametrize("L,T,b", [(6, 64, 576), (3, 64, 4096)])
+@pytest.mark.parametrize("P,gen", [(64 * 3 + 10, 130), (128, 64), (5, 1)])
+def test_decode_fill_then_persist_d2h(gpus, L, T, b, P, gen):
+    """Decode stand-in writes generated tokens [P, P+gen) into the decode pool;
+    K4 gathers them, every layer, into host Full Blocks [L][T][b] in chunks of
+    64 generated tokens plus the final partial (desim.cpp:666-672, :690-693)."""
+    g = abi.geom(L, T, b)
+    total = P + gen
+    blk0, blk1 = P // T, -(-total // T)
+    n = blk1 - blk0
+    pool = abi.Pool(0, g, 16, 1)
+    target = abi.Store(0, g, 24, SEED + 1)  # different content: proves the write
+    try:
+        slots = np.arange(3, 3 + n, dtype=np.int32)
+        fbs = np.arange(10, 10 + n, dtype=np.int64)
+        ds, df = dev(slots, 0, np.int32), dev(fbs, 0, np.int64)
+        fill = (abi.SpanJob * 1)()
+        fill[0] = abi.SpanJob(ds.data_ptr(), df.data_ptr(), blk0, P, total, n, 0)
+        abi.decode_fill(pool, fill, 1, SEED)
+        chunks, done = [], 0
+        for k in list(range(T, gen, T)) + [gen]:  # persist_tokens milestones
+            if k > done:
+                chunks.append((P + done, P + k))
+                done = k
+        jobs = (abi.SpanJob * len(chunks))()
+        for i, (t0, t1) in enumerate(chunks):
+            jobs[i] = abi.SpanJob(ds.data_ptr(), df.data_ptr(), blk0, t0, t1, n, 0)
+        abi.persist_d2h(pool, target, jobs, len(chunks))
+        sync_all()
+        img = np.frombuffer(target.bytes(), dtype=np.uint8)
+        gr = refpy.geom(L, T, b)
+        fb_bytes, lb = L * T * b, T * b
+        for i in range(n):
+            k = blk0 + i
+            a, z = max(P, k * T) - k * T, min(total, (k + 1) * T) - k * T
+            for layer in range(L):
+                full = refpy.layer_block(gr, SEED, int(fbs[i]), layer, T)
+                other = refpy.layer_block(gr, SEED + 1, int(fbs[i]), layer, T)
+                off = int(fbs[i]) * fb_bytes + layer * lb
+                got = img[off:off + lb]
+                assert np.array_equal(got[a * b:z * b], full[a * b:z * b])      # persisted
+                assert np.array_equal(got[:a * b], other[:a * b])               # untouched
+                assert np.array_equal(got[z * b:], other[z * b:])
+        assert sum(t1 - t0 for t0, t1 in chunks) == gen
+    finally:
+        target.close()
+        pool.close()
