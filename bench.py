@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--handoff", action="store_true",
                     help="also run the PD handoff: prefill stand-in + PeToDe/MissMerge per layer "
                          "into the DE decode pools, DE read path fused with DecodeH2D")
+    ap.add_argument("--persist", action="store_true",
+                    help="also persist generated tokens (decode stand-in + K4 D2H), implies --handoff")
     ap.add_argument("--handoff-ctas", type=int, default=0, help="K3 CTA cap on PEs (0 = default)")
     ap.add_argument("--gather-ctas", type=int, default=-1, help="K1/K2 CTA cap (-1 = auto)")
     ap.add_argument("--k1", default="sm", choices=["sm", "ce"],
@@ -263,7 +265,8 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
     if args.online > 0:
         opt.pace_scale = 1.0
     opt.k1_mode = 1 if args.k1 == "ce" else 0
-    opt.handoff = bool(args.handoff)
+    opt.handoff = bool(args.handoff or args.persist)
+    opt.persist = bool(args.persist)
     opt.handoff_ctas = args.handoff_ctas
     opt.gather_ctas = args.gather_ctas
     opt.seed = 9
@@ -303,7 +306,8 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
                     per_engine[e] = round(ms, 1)
     snic = sum(u["total_bytes"] for u in planned["usage"] if u["kind"] == "snic_read")
     info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens,
-                handoff_bytes=xp.handoff_bytes if args.handoff else 0,
+                handoff_bytes=xp.handoff_bytes if (args.handoff or args.persist) else 0,
+                persist_bytes=xp.persist_bytes if args.persist else 0,
                 model_gbps=snic / planned["makespan"] / 1e9 if planned["makespan"] > 0 else None,
                 requests=xp.requests, reader_bytes=list(xp.reader_bytes),
                 de_path=sum(1 for d in planned["decisions"] if d[4] == 1),
@@ -563,7 +567,12 @@ def main():
                 out["round_robin"] = {"value": round(rr_v, 3), "unit": "GB/s",
                                       "adaptive_vs_rr": round(value / rr_v, 3)}
                 out["balance"]["round_robin"] = storage_balance(rr["info"]["spans"], rr["info"]["caps"], P + D)
-        if args.handoff:
+        if args.persist:
+            out["persist"] = {"bytes_per_step": info["persist_bytes"],
+                              "gbps": round(info["persist_bytes"] * K / dev_s / 1e9, 3),
+                              "what": "decode stand-in + K4 D2H Full-Block gather every 64 generated "
+                                      "tokens + final partial (PersistD2H ledger of the reference)"}
+        if args.handoff or args.persist:
             out["handoff"] = {"bytes_per_step": info["handoff_bytes"],
                               "gbps": round(info["handoff_bytes"] * K / dev_s / 1e9, 3),
                               "what": "PeToDe/MissMerge per layer into DE decode pools (K3, NVLink) "

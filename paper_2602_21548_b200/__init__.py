@@ -18,6 +18,13 @@ import os as _os
 
 _HERE = _os.path.dirname(_os.path.abspath(__file__))
 
+# The executor waits on device counters with stream memory operations
+# (cuStreamWaitValue32) on some streams while other streams of the same GPU
+# produce the awaited data; streams multiplexed onto one hardware queue would
+# serialise behind such a wait.  Give every stream its own queue (must be set
+# before the CUDA context exists).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 try:
     from . import _core
 except ImportError as exc:  # pragma: no cover - exercised only on broken builds

@@ -757,54 +757,67 @@ StepResult EngineRuntime::run_step_handoff() {
     check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_end_), 0), "cudaStreamWaitEvent");
     check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), h), "cudaEventRecord");
   } else {
-    for (int ji : x.by_reader[engine_]) {  // DE read path: dual gather
-      const LoadJob& j = x.jobs[ji];
-      if (!peers_[j.pe]) throw std::runtime_error("run_step: PE " + std::to_string(j.pe) + " not attached");
-      if (!j.pe_done_preds.empty()) {
-        const std::int64_t off = pe_done_off_[ji];
-        check(dp_wait_tickets(peers_[j.pe], d_wt_ + off, d_wg_ + off,
-                              static_cast<int32_t>(j.pe_done_preds.size()), L, x.opt.wait_timeout_ms, s),
-              "dp_wait_tickets (prefill slots)");
+    // A DE enqueues its work job by job in the global order, across its two
+    // streams: every operation a wait depends on belongs to an earlier job,
+    // so it was enqueued earlier -- even if the driver multiplexes both
+    // streams onto one hardware queue, a blocked wait never sits in front of
+    // its own producer.
+    const std::int64_t T = x.cfg.block_size_tokens;
+    std::size_t ri = 0, di = 0;
+    const auto& reads = x.by_reader[engine_];
+    const auto& decodes = x.by_de[engine_];
+    while (ri < reads.size() || (x.persist && di < decodes.size())) {
+      const bool take_read = ri < reads.size() && (!x.persist || di >= decodes.size() || reads[ri] <= decodes[di]);
+      if (take_read) {  // DE read path: dual gather
+        const int ji = reads[ri++];
+        const LoadJob& j = x.jobs[ji];
+        if (!peers_[j.pe]) throw std::runtime_error("run_step: PE " + std::to_string(j.pe) + " not attached");
+        if (!j.pe_done_preds.empty()) {
+          const std::int64_t off = pe_done_off_[ji];
+          check(dp_wait_tickets(peers_[j.pe], d_wt_ + off, d_wg_ + off,
+                                static_cast<int32_t>(j.pe_done_preds.size()), L, x.opt.wait_timeout_ms, s),
+                "dp_wait_tickets (prefill slots)");
+          ++res.launches;
+        }
+        if (!j.de_preds.empty()) {
+          const std::int64_t off = de_wait_off_[ji];
+          check(dp_wait_tickets(pool_, d_wt_ + off, d_wg_ + off, static_cast<int32_t>(j.de_preds.size()),
+                                L, x.opt.wait_timeout_ms, s),
+                "dp_wait_tickets (decode slots)");
+          ++res.launches;
+        }
+        storage_gate(j);
+        dp_dual_job dj{{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket},
+                       d_dual_de_ + j.blk_off,
+                       j.de_ticket,
+                       0};
+        check(dp_h2d_push_p2p_dual(peers_[j.pe], pool_, store_, &dj, 1, s), "dp_h2d_push_p2p_dual");
         ++res.launches;
+        continue;
       }
-      if (!j.de_preds.empty()) {
-        const std::int64_t off = de_wait_off_[ji];
-        check(dp_wait_tickets(pool_, d_wt_ + off, d_wg_ + off, static_cast<int32_t>(j.de_preds.size()),
-                              L, x.opt.wait_timeout_ms, s),
-              "dp_wait_tickets (decode slots)");
-        ++res.launches;
-      }
-      storage_gate(j);
-      dp_dual_job dj{{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket},
-                     d_dual_de_ + j.blk_off,
-                     j.de_ticket,
-                     0};
-      check(dp_h2d_push_p2p_dual(peers_[j.pe], pool_, store_, &dj, 1, s), "dp_h2d_push_p2p_dual");
-      ++res.launches;
+      // decode stream: once the request's whole prompt has landed, the
+      // decode stand-in writes its generated tokens, K4 persists them chunk
+      // by chunk, then its "persist done" row is set
+      const std::int64_t pos = static_cast<std::int64_t>(di);
+      const LoadJob& j = x.jobs[decodes[di++]];
+      check(dp_wait_tickets(pool_, d_wt_ + final_wait_off_ + pos, d_wg_ + final_wait_off_ + pos, 1, L,
+                            x.opt.wait_timeout_ms, h),
+            "dp_wait_tickets (decode ready)");
+      const std::int64_t blk0 = j.prompt / T;
+      const std::int32_t nb = j.n_tblk - static_cast<std::int32_t>(blk0);
+      const dp_span_job fill{d_dec_slot_ + j.dec_off + blk0, d_dec_fb_ + j.dec_off + blk0, blk0,
+                             j.prompt, j.prompt + j.gen, nb, 0};
+      check(dp_decode_fill(pool_, &fill, 1, x.opt.seed, h), "dp_decode_fill");
+      std::vector<dp_span_job> chunks;
+      for (const auto& [t0, t1] : x.persist_chunks(j))
+        chunks.push_back(dp_span_job{fill.slot, fill.fb, blk0, t0, t1, nb, 0});
+      check(dp_persist_d2h(pool_, persist_store_, chunks.data(), static_cast<int32_t>(chunks.size()), h),
+            "dp_persist_d2h");
+      check(dp_stream_write_counter(pool_, j.de_ticket + x.n_de_tickets[engine_], L, 1, h),
+            "dp_stream_write_counter");
+      res.launches += 3;
     }
     if (x.persist) {
-      // decode stream: per request, once its whole prompt has landed (no SMs
-      // while waiting): decode stand-in for the generated tokens, then K4
-      // persists them chunk by chunk, then its "persist done" row is set
-      const std::int64_t T = x.cfg.block_size_tokens;
-      for (int ji : x.by_de[engine_]) {
-        const LoadJob& j = x.jobs[ji];
-        check(dp_stream_wait_counter(pool_, j.de_ticket, L, x.de_total_items(j), h),
-              "dp_stream_wait_counter (decode ready)");
-        const std::int64_t blk0 = j.prompt / T;
-        const std::int32_t nb = j.n_tblk - static_cast<std::int32_t>(blk0);
-        const dp_span_job fill{d_dec_slot_ + j.dec_off + blk0, d_dec_fb_ + j.dec_off + blk0, blk0,
-                               j.prompt, j.prompt + j.gen, nb, 0};
-        check(dp_decode_fill(pool_, &fill, 1, x.opt.seed, h), "dp_decode_fill");
-        std::vector<dp_span_job> chunks;
-        for (const auto& [t0, t1] : x.persist_chunks(j))
-          chunks.push_back(dp_span_job{fill.slot, fill.fb, blk0, t0, t1, nb, 0});
-        check(dp_persist_d2h(pool_, persist_store_, chunks.data(), static_cast<int32_t>(chunks.size()), h),
-              "dp_persist_d2h");
-        check(dp_stream_write_counter(pool_, j.de_ticket + x.n_de_tickets[engine_], L, 1, h),
-              "dp_stream_write_counter");
-        res.launches += 2;
-      }
       check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), s), "cudaEventRecord");
       check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_end_), 0), "cudaStreamWaitEvent");
       check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), h), "cudaEventRecord");
