@@ -202,7 +202,8 @@ def test_persist_chunks_match_the_reference_ledger():
     total = 0
     for i, j in enumerate(xp.jobs()):
         chunks = xp.persist_chunks(i)
-        assert [(b - a) * per_tok for a, b in chunks] == flows[j[0]]
+        # flows are logged at completion, so concurrent chunks may finish out of order
+        assert sorted((b - a) * per_tok for a, b in chunks) == sorted(flows[j[0]])
         assert chunks[0][0] == j[14] and chunks[-1][1] == j[14] + xp.job_gen(i)
         total += xp.job_gen(i) * per_tok
     assert total == xp.persist_bytes
