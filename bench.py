@@ -542,7 +542,7 @@ def main():
             "tokens_per_s": round(tokens_s, 1),
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": info["hit_bytes"],
-                    "d2h_bytes_per_step": 8 * n},
+                    "d2h_bytes_per_step": 8 * n + info["persist_bytes"]},
             "gpu_launches": info["launches"],
             "roofline": {"bound": "pcie", "achieved": round(achieved, 2),
                          "peak": round(peak / 1e9, 2) if peak else None, "unit": "GB/s",
