@@ -97,6 +97,46 @@ int ref_synthesize(int64_t max_len, double mean_turns, double mean_append, doubl
   }
 }
 
+// derive_variant / extend_with_synthetic_round of the reference
+// (proj/src/workload.cpp:131-176) on a trace file, written back as a trace.
+int ref_derive_variant(const char* in_path, double append_scale, double gen_scale,
+                       int64_t max_len, const char* out_path) {
+  try {
+    const auto src = load_trace(std::string(in_path));
+    save_trace(std::string(out_path), derive_variant(src, append_scale, gen_scale, max_len));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ref_extend_trace(const char* in_path, uint64_t seed, const char* out_path) {
+  try {
+    std::vector<Trajectory> out;
+    for (const auto& t : load_trace(std::string(in_path)))
+      out.push_back(extend_with_synthetic_round(t, seed));
+    save_trace(std::string(out_path), out);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// poisson_arrivals (proj/src/workload.cpp:178-192): fills up to `cap` times,
+// returns how many there are (may exceed cap), -1 on error.
+int64_t ref_poisson(double rate, double horizon, uint64_t seed, double* out, int64_t cap) {
+  try {
+    const auto v = poisson_arrivals(rate, horizon, seed);
+    for (int64_t i = 0; i < static_cast<int64_t>(v.size()) && i < cap; ++i) out[i] = v[i];
+    return static_cast<int64_t>(v.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // Runs the reference simulator on a trace file.  `kv` is "key=value;...".
 // Writes a JSON report to out_path.  Returns 0, or -2 ConfigError,
 // -3 SimulationError, -1 other.

@@ -142,6 +142,14 @@ def ref():
         lib.ref_synthesize.argtypes = [ctypes.c_int64] + [ctypes.c_double] * 6 + [
             ctypes.c_int, ctypes.c_uint64, ctypes.c_char_p]
         lib.ref_simulate.restype = ctypes.c_int
+        lib.ref_derive_variant.restype = ctypes.c_int
+        lib.ref_derive_variant.argtypes = [ctypes.c_char_p, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_int64, ctypes.c_char_p]
+        lib.ref_extend_trace.restype = ctypes.c_int
+        lib.ref_extend_trace.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p]
+        lib.ref_poisson.restype = ctypes.c_int64
+        lib.ref_poisson.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
+                                    ctypes.POINTER(ctypes.c_double), ctypes.c_int64]
         lib.ref_simulate.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p]
         I64P = ctypes.POINTER(ctypes.c_int64)
         IP = ctypes.POINTER(ctypes.c_int)
@@ -169,6 +177,28 @@ def ref_synthesize(path, max_len=65536, count=500, seed=1, mean_turns=157.0, mea
     if n < 0:
         raise ValueError(ref().ref_last_error().decode())
     return n
+
+
+def _check(rc):
+    if rc < 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return rc
+
+
+def ref_derive_variant(in_path, out_path, append_scale, gen_scale, max_len):
+    _check(ref().ref_derive_variant(in_path.encode(), append_scale, gen_scale, max_len,
+                                    out_path.encode()))
+
+
+def ref_extend_trace(in_path, out_path, seed):
+    _check(ref().ref_extend_trace(in_path.encode(), seed, out_path.encode()))
+
+
+def ref_poisson(rate, horizon, seed):
+    n = _check(ref().ref_poisson(rate, horizon, seed, None, 0))
+    buf = (ctypes.c_double * max(n, 1))()
+    _check(ref().ref_poisson(rate, horizon, seed, buf, n))
+    return list(buf[:n])
 
 
 class RefError(Exception):

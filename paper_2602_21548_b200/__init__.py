@@ -47,9 +47,12 @@ from ._core import (  # noqa: E402
     blocks_for,
     build_exec_plan,
     context_before,
+    derive_variant,
+    extend_with_synthetic_round,
     load_balance_ratio,
     load_trace,
     plan,
+    poisson_arrivals,
     run_step_all,
     save_trace,
     schedule_de_groups,
@@ -77,9 +80,12 @@ __all__ = [
     "blocks_for",
     "build_exec_plan",
     "context_before",
+    "derive_variant",
+    "extend_with_synthetic_round",
     "load_balance_ratio",
     "load_trace",
     "plan",
+    "poisson_arrivals",
     "run_step_all",
     "save_trace",
     "schedule_de_groups",

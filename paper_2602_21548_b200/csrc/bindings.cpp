@@ -172,6 +172,15 @@ PYBIND11_MODULE(_core, m) {
       py::arg("mean_turns") = 157.0, py::arg("mean_append") = 429.0, py::arg("mean_gen") = 176.0,
       py::arg("sigma_turns") = 0.5, py::arg("sigma_append") = 0.6, py::arg("sigma_gen") = 0.6);
 
+  m.def(
+      "derive_variant",
+      [](const std::vector<Trajectory>& t, double append_scale, double gen_scale,
+         std::int64_t max_len) { return derive_variant(t, append_scale, gen_scale, max_len); },
+      py::arg("trajectories"), py::arg("append_scale"), py::arg("gen_scale"), py::arg("max_len"));
+  m.def("extend_with_synthetic_round", &extend_with_synthetic_round, py::arg("base"),
+        py::arg("seed"));
+  m.def("poisson_arrivals", &poisson_arrivals, py::arg("rate"), py::arg("horizon"),
+        py::arg("seed"));
   m.def("load_trace", &load_trace);
   m.def("save_trace", [](const std::string& path, const std::vector<Trajectory>& t) {
     save_trace(path, t);

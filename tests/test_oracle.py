@@ -141,3 +141,33 @@ def test_product_synthesize_regenerates_golden_trace(tmp_path):
     mean_total = sum(t.total_tokens() for t in back) / len(back)
     # proj/tests/python/test_smoke.py:84-89
     assert abs(mean_total - 55958) / 55958 < 0.10
+
+
+@pytest.mark.skipif(not refpy.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("scales", [(1.0, 1.0, 65536), (2.0, 0.5, 200000), (0.37, 3.3, 9000),
+                                    (1.5, 1.5, 1)])
+def test_derive_variant_matches_reference(tmp_path, scales):
+    # proj/src/workload.cpp:131-162: half-up rounding, gen >= 1, cap clamp
+    a, g, cap = scales
+    src = str(tmp_path / "src.tsv")
+    dp.save_trace(src, dp.synthesize(max_len=65536, count=40, seed=3))
+    want = str(tmp_path / "ref.tsv")
+    refpy.ref_derive_variant(src, want, a, g, cap)
+    got = str(tmp_path / "got.tsv")
+    dp.save_trace(got, dp.derive_variant(dp.load_trace(src), a, g, cap))
+    assert open(got).read() == open(want).read()
+
+
+@pytest.mark.skipif(not refpy.ref_available(), reason="oracle/_ref not built")
+def test_extend_and_poisson_match_reference(tmp_path):
+    src = str(tmp_path / "src.tsv")
+    dp.save_trace(src, dp.synthesize(max_len=20000, count=8, seed=5))
+    want = str(tmp_path / "ref.tsv")
+    refpy.ref_extend_trace(src, want, 77)
+    got = str(tmp_path / "got.tsv")
+    dp.save_trace(got, [dp.extend_with_synthetic_round(t, 77) for t in dp.load_trace(src)])
+    assert open(got).read() == open(want).read()
+    for rate, horizon, seed in [(0.1, 500.0, 1), (3.0, 100.0, 42)]:
+        assert dp.poisson_arrivals(rate, horizon, seed) == refpy.ref_poisson(rate, horizon, seed)
+    with pytest.raises(ValueError):
+        dp.derive_variant(dp.load_trace(src), 0.0, 1.0, 100)
