@@ -377,6 +377,45 @@ int ref_select_read_path(int64_t pe_q, int64_t de_q) {
   return select_read_path(pe_q, de_q) == ReadPath::PEPath ? 0 : 1;
 }
 
+// build_forward_batch (src/scheduler.cpp:174-219).  items: n x 3 int64
+// {request_id, cached, bsz}; cost: {bilinear, quadratic, linear, constant}.
+// out_items: up to n x 3 {request_id, cached, bsz}; out_meta[4]: {chunked,
+// chunked_request_id, chunk_bsz, consumed_whole}; *out_time = estimated_time.
+// Returns the batch size, -2 on QuotaInfeasibleError, -1 on other errors.
+int ref_build_forward_batch(int n, const int64_t* items, double quota, const double* cost,
+                            int64_t* out_items, int64_t* out_meta, double* out_time) {
+  try {
+    std::vector<BatchItem> q(n);
+    for (int i = 0; i < n; ++i)
+      q[i] = {static_cast<int>(items[3 * i]), items[3 * i + 1], items[3 * i + 2]};
+    SchedulerParams p;
+    p.compute_quota = quota;
+    AttentionCostModel m;
+    m.coeff_bilinear = cost[0];
+    m.coeff_quadratic = cost[1];
+    m.coeff_linear = cost[2];
+    m.constant = cost[3];
+    const ForwardBatch fb = build_forward_batch(q, p, m);
+    for (size_t i = 0; i < fb.items.size(); ++i) {
+      out_items[3 * i] = fb.items[i].request_id;
+      out_items[3 * i + 1] = fb.items[i].cached;
+      out_items[3 * i + 2] = fb.items[i].bsz;
+    }
+    out_meta[0] = fb.chunked ? 1 : 0;
+    out_meta[1] = fb.chunked_request_id;
+    out_meta[2] = fb.chunk_bsz;
+    out_meta[3] = fb.consumed_whole;
+    *out_time = fb.estimated_time;
+    return static_cast<int>(fb.items.size());
+  } catch (const QuotaInfeasibleError& e) {
+    g_err = e.what();
+    return -2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 int64_t ref_context_before_file(const char* trace_path, int traj, int round) {
   try {
     const auto t = load_trace(std::string(trace_path));

@@ -142,6 +142,11 @@ def ref():
         lib.ref_synthesize.argtypes = [ctypes.c_int64] + [ctypes.c_double] * 6 + [
             ctypes.c_int, ctypes.c_uint64, ctypes.c_char_p]
         lib.ref_simulate.restype = ctypes.c_int
+        I64P = ctypes.POINTER(ctypes.c_int64)
+        lib.ref_build_forward_batch.restype = ctypes.c_int
+        lib.ref_build_forward_batch.argtypes = [ctypes.c_int, I64P, ctypes.c_double,
+                                                ctypes.POINTER(ctypes.c_double), I64P, I64P,
+                                                ctypes.POINTER(ctypes.c_double)]
         lib.ref_derive_variant.restype = ctypes.c_int
         lib.ref_derive_variant.argtypes = [ctypes.c_char_p, ctypes.c_double, ctypes.c_double,
                                            ctypes.c_int64, ctypes.c_char_p]
@@ -183,6 +188,28 @@ def _check(rc):
     if rc < 0:
         raise ValueError(ref().ref_last_error().decode())
     return rc
+
+
+class QuotaInfeasible(Exception):
+    pass
+
+
+def ref_build_forward_batch(items, quota, cost):
+    """Reference build_forward_batch.  items: [(request_id, cached, bsz)],
+    cost: (bilinear, quadratic, linear, constant).  Returns (items, chunked,
+    chunked_request_id, chunk_bsz, consumed_whole, estimated_time)."""
+    n = len(items)
+    flat = (ctypes.c_int64 * max(1, 3 * n))(*[v for it in items for v in it])
+    c = (ctypes.c_double * 4)(*cost)
+    out = (ctypes.c_int64 * max(1, 3 * n))()
+    meta = (ctypes.c_int64 * 4)()
+    t = ctypes.c_double()
+    k = ref().ref_build_forward_batch(n, flat, quota, c, out, meta, ctypes.byref(t))
+    if k == -2:
+        raise QuotaInfeasible(ref().ref_last_error().decode())
+    _check(k)
+    got = [tuple(out[3 * i:3 * i + 3]) for i in range(k)]
+    return got, bool(meta[0]), meta[1], meta[2], meta[3], t.value
 
 
 def ref_derive_variant(in_path, out_path, append_scale, gen_scale, max_len):

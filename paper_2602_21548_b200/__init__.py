@@ -45,6 +45,9 @@ from ._core import (  # noqa: E402
     StepResult,
     Trajectory,
     blocks_for,
+    build_forward_batch,
+    estimate_attention_time,
+    QuotaInfeasibleError,
     build_exec_plan,
     context_before,
     derive_variant,
@@ -77,7 +80,10 @@ __all__ = [
     "SimulationError",
     "StepResult",
     "Trajectory",
+    "QuotaInfeasibleError",
     "blocks_for",
+    "build_forward_batch",
+    "estimate_attention_time",
     "build_exec_plan",
     "context_before",
     "derive_variant",

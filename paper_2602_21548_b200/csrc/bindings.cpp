@@ -218,6 +218,41 @@ PYBIND11_MODULE(_core, m) {
     p.z_factor = z;
     return p;
   };
+  // Intra-engine compute-quota batching (scheduler.hpp build_forward_batch).
+  // items: [(request_id, cached, bsz)]; cost: (bilinear, quadratic, linear,
+  // constant).  Returns (items, chunked, chunked_request_id, chunk_bsz,
+  // consumed_whole, estimated_time).
+  auto cost_of = [](const std::tuple<double, double, double, double>& c) {
+    AttentionCostModel m;
+    std::tie(m.coeff_bilinear, m.coeff_quadratic, m.coeff_linear, m.constant) = c;
+    return m;
+  };
+  auto items_of = [](const std::vector<std::tuple<int, std::int64_t, std::int64_t>>& v) {
+    std::vector<BatchItem> q;
+    q.reserve(v.size());
+    for (const auto& [id, cached, bsz] : v) q.push_back({id, cached, bsz});
+    return q;
+  };
+  m.def(
+      "estimate_attention_time",
+      [=](const std::vector<std::tuple<int, std::int64_t, std::int64_t>>& batch,
+          const std::tuple<double, double, double, double>& cost) {
+        return estimate_attention_time(items_of(batch), cost_of(cost));
+      },
+      py::arg("batch"), py::arg("cost"));
+  m.def(
+      "build_forward_batch",
+      [=](const std::vector<std::tuple<int, std::int64_t, std::int64_t>>& queue, double quota,
+          const std::tuple<double, double, double, double>& cost) {
+        SchedulerParams p;
+        p.compute_quota = quota;
+        const ForwardBatch fb = build_forward_batch(items_of(queue), p, cost_of(cost));
+        std::vector<std::tuple<int, std::int64_t, std::int64_t>> items;
+        for (const BatchItem& b : fb.items) items.emplace_back(b.request_id, b.cached, b.bsz);
+        return py::make_tuple(items, fb.chunked, fb.chunked_request_id, fb.chunk_bsz,
+                              fb.consumed_whole, fb.estimated_time);
+      },
+      py::arg("queue"), py::arg("quota"), py::arg("cost"));
   m.def("schedule_pe_fetch",
         [=](const std::vector<std::pair<int, std::int64_t>>& q,
             const std::vector<std::vector<std::int64_t>>& snaps, std::int64_t alpha,
@@ -330,6 +365,7 @@ PYBIND11_MODULE(_core, m) {
           return out;
         });
 
+  py::register_exception<QuotaInfeasibleError>(m, "QuotaInfeasibleError", PyExc_RuntimeError);
   py::register_exception<desim::ConfigError>(m, "ConfigError");
   py::register_exception<desim::SimulationError>(m, "SimulationError");
 

@@ -140,3 +140,115 @@ def test_select_read_path_vs_reference():
     for _ in range(1000):
         a, b = rng.randrange(100), rng.randrange(100)
         assert dp.select_read_path(a, b) == refpy.ref().ref_select_read_path(a, b)
+
+
+# ---- intra-engine compute-quota batching ----------------
+# proj/src/scheduler.cpp:163-219; KATs from proj/tests/test_scheduler.cpp:196-285.
+
+def fwd(queue, quota, cost):
+    return dp.build_forward_batch(queue, quota, cost)
+
+
+def test_attention_time_closed_forms():  # test_scheduler.cpp:196-208
+    assert dp.estimate_attention_time([], (0, 0, 0, 0.5)) == pytest.approx(0.5)
+    assert dp.estimate_attention_time([(0, 0, 8)], (0, 2.0, 0, 0)) == pytest.approx(128.0)
+    assert dp.estimate_attention_time([(0, 100, 1)], (3.0, 0, 0, 0)) == pytest.approx(300.0)
+
+
+def test_forward_batch_whole_queue():  # :210-221
+    items, chunked, _, _, whole, t = fwd([(0, 0, 30), (1, 0, 40)], 100, (0, 0, 1.0, 0))
+    assert len(items) == 2 and not chunked and whole == 2 and t == pytest.approx(70.0)
+
+
+def test_forward_batch_quadratic_chunk():  # :223-234
+    _, chunked, rid, bsz, whole, _ = fwd([(0, 0, 50)], 100.0, (0, 1.0, 0, 0))
+    assert chunked and rid == 0 and bsz == 10 and whole == 0
+
+
+def test_forward_batch_second_request_chunked():  # :236-247
+    _, chunked, _, bsz, whole, t = fwd([(0, 0, 80), (1, 0, 50)], 100.0, (0, 0, 1.0, 0))
+    assert chunked and whole == 1 and bsz == 20 and t == pytest.approx(100.0)
+
+
+def test_forward_batch_quota_infeasible():  # :249-256
+    with pytest.raises(dp.QuotaInfeasibleError):
+        fwd([(0, 0, 10)], 0.5, (0, 0, 1.0, 0))
+
+
+def test_forward_batch_binary_search_equals_linear_scan():  # :258-285
+    rng = random.Random(5)
+    cost = (1e-7, 3e-6, 2e-4, 1e-3)
+    for _ in range(150):
+        bsz = 1 + rng.randrange(4096)
+        cached = rng.randrange(100000)
+        quota = 1e-3 + rng.randrange(1000) * 5e-3
+        best = 0
+        for b in range(1, bsz + 1):
+            if dp.estimate_attention_time([(0, cached, b)], cost) <= quota:
+                best = b
+            else:
+                break  # monotone in b
+        if best == 0:
+            with pytest.raises(dp.QuotaInfeasibleError):
+                fwd([(0, cached, bsz)], quota, cost)
+            continue
+        _, chunked, _, cb, _, t = fwd([(0, cached, bsz)], quota, cost)
+        assert (cb if chunked else bsz) == best and t <= quota
+
+
+@needs_ref
+def test_forward_batch_random_queues_vs_reference():
+    rng = random.Random(11)
+    for trial in range(400):
+        n = rng.randrange(0, 12)
+        q = [(i, rng.randrange(0, 200000), 1 + rng.randrange(6000)) for i in range(n)]
+        cost = (rng.choice([0, 2e-10, 1e-9]), rng.choice([0, 1e-9, 3e-8]),
+                rng.choice([0, 4e-7, 1e-6]), rng.choice([0, 1e-5, 2e-4]))
+        quota = rng.choice([2e-4, 2e-3, 2e-2, 0.3])
+        try:
+            want = refpy.ref_build_forward_batch(q, quota, cost)
+        except refpy.QuotaInfeasible:
+            with pytest.raises(dp.QuotaInfeasibleError):
+                fwd(q, quota, cost)
+            continue
+        got = fwd(q, quota, cost)
+        assert list(got[0]) == want[0], trial
+        assert tuple(got[1:5]) == tuple(want[1:5]), trial
+        assert got[5] == want[5], trial  # bit-identical double
+
+
+def test_forward_batch_balances_ranks_criterion_6():
+    # proj/tests/acceptance.cpp:333-381: 8 ranks each pack their own FIFO;
+    # per-forward attention-time max/avg <= 1.10 in >= 90% of loaded forwards
+    cost = (2e-10, 1e-9, 4e-7, 1e-5)
+    quota, layers, ranks = 2e-3, 4, 8
+    rng = random.Random(77)
+    queues = [[] for _ in range(ranks)]
+    nid = [0]
+
+    def refill(r, k):
+        for _ in range(k):
+            queues[r].append([nid[0], int(rng.lognormvariate(8.5, 1.0)),
+                              max(1, int(rng.lognormvariate(5.5, 0.9)))])
+            nid[0] += 1
+
+    for r in range(ranks):
+        refill(r, 60)
+    loaded = balanced = 0
+    for _ in range(400):
+        all_loaded = all(len(q) >= 4 for q in queues)
+        times = []
+        for r in range(ranks):
+            if not queues[r]:
+                refill(r, 10)
+            _, chunked, _, cb, whole, t = fwd([tuple(x) for x in queues[r]], quota, cost)
+            times.append(layers * t)
+            del queues[r][:whole]
+            if chunked:
+                queues[r][0][2] -= cb
+            refill(r, 2 + rng.randrange(2))
+        if all_loaded:
+            loaded += 1
+            if max(times) / (sum(times) / len(times)) <= 1.10:
+                balanced += 1
+    assert loaded >= 100 and balanced / loaded >= 0.90

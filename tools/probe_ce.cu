@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
+#include <chrono>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
   std::fprintf(stderr, "CUDA %s at %s:%d: %s\n", #x, __FILE__, __LINE__, cudaGetErrorString(e_)); std::exit(1);} } while (0)
@@ -43,6 +44,87 @@ int main() {
       float ms; CK(cudaEventElapsedTime(&ms, a, b)); if (ms < best) best = ms;
     }
     std::printf("ce2d run=%d blocks: %.1f GB/s (%d calls)\n", run, NFB * FB / (best * 1e-3) / 1e9, runs * (int)L);
+  }
+  // (1b) the same 2D copies spread round-robin over k streams: is the gap to
+  // the 1-D copy peak a per-call latency that concurrency hides?
+  {
+    cudaStream_t ss[4];
+    for (auto& x : ss) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    cudaEvent_t done[4];
+    for (auto& x : done) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    for (int k : {1, 2, 4})
+      for (int run : {16, 64, 128}) {
+        const int runs = (int)(NFB / run);
+        const size_t plane = NFB * LB;
+        float best = 1e30f;
+        for (int rep = 0; rep < 3; ++rep) {
+          CK(cudaDeviceSynchronize());
+          CK(cudaEventRecord(a, s1));
+          for (int i = 0; i < k; ++i) CK(cudaStreamWaitEvent(ss[i], a, 0));
+          int n = 0;
+          for (size_t l = 0; l < L; ++l)
+            for (int r = 0; r < runs; ++r, ++n)
+              CK(cudaMemcpy2DAsync(dev + l * plane + (size_t)r * run * LB, LB,
+                                   host + (size_t)r * run * FB + l * LB, FB, LB, run,
+                                   cudaMemcpyHostToDevice, ss[n % k]));
+          for (int i = 0; i < k; ++i) { CK(cudaEventRecord(done[i], ss[i])); CK(cudaStreamWaitEvent(s1, done[i], 0)); }
+          CK(cudaEventRecord(b, s1)); CK(cudaEventSynchronize(b));
+          float ms; CK(cudaEventElapsedTime(&ms, a, b)); if (ms < best) best = ms;
+        }
+        std::printf("ce2d %d streams run=%d: %.1f GB/s\n", k, run, NFB * FB / (best * 1e-3) / 1e9);
+      }
+  }
+  // (1c) the 2D copies captured once into a CUDA graph and replayed: if the
+  // per-call gap is host submission cost, the replay closes it.
+  for (int run : {16, 64, 128}) {
+    const int runs = (int)(NFB / run);
+    const size_t plane = NFB * LB;
+    cudaGraph_t graph; cudaGraphExec_t exec;
+    CK(cudaStreamBeginCapture(s1, cudaStreamCaptureModeThreadLocal));
+    for (size_t l = 0; l < L; ++l)
+      for (int r = 0; r < runs; ++r)
+        CK(cudaMemcpy2DAsync(dev + l * plane + (size_t)r * run * LB, LB,
+                             host + (size_t)r * run * FB + l * LB, FB, LB, run,
+                             cudaMemcpyHostToDevice, s1));
+    CK(cudaStreamEndCapture(s1, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+      CK(cudaEventRecord(a, s1)); CK(cudaGraphLaunch(exec, s1)); CK(cudaEventRecord(b, s1));
+      CK(cudaEventSynchronize(b));
+      float ms; CK(cudaEventElapsedTime(&ms, a, b)); if (ms < best) best = ms;
+    }
+    std::printf("ce2d graph run=%d: %.1f GB/s\n", run, NFB * FB / (best * 1e-3) / 1e9);
+    CK(cudaGraphExecDestroy(exec)); CK(cudaGraphDestroy(graph));
+  }
+  // host-side submission cost of one 2D call, no GPU wait
+  {
+    CK(cudaDeviceSynchronize());
+    const int n = 2000;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < n; ++i)
+      CK(cudaMemcpy2DAsync(dev + (size_t)(i % 64) * LB, LB, host + (size_t)(i % 64) * FB, FB, LB, 1,
+                           cudaMemcpyHostToDevice, s1));
+    auto t1 = std::chrono::steady_clock::now();
+    CK(cudaStreamSynchronize(s1));
+    std::printf("host submit cost per 2D call: %.2f us\n",
+                std::chrono::duration<double, std::micro>(t1 - t0).count() / n);
+  }
+  // one contiguous 1-D copy per (run, layer), same bytes: the layer-major staging shape
+  for (int run : {16, 64, 128}) {
+    const int runs = (int)(NFB / run);
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+      CK(cudaEventRecord(a, s1));
+      for (size_t l = 0; l < L; ++l)
+        for (int r = 0; r < runs; ++r) {
+          const size_t off = (l * NFB + (size_t)r * run) * LB;
+          CK(cudaMemcpyAsync(dev + off, host + off, (size_t)run * LB, cudaMemcpyHostToDevice, s1));
+        }
+      CK(cudaEventRecord(b, s1)); CK(cudaEventSynchronize(b));
+      float ms; CK(cudaEventElapsedTime(&ms, a, b)); if (ms < best) best = ms;
+    }
+    std::printf("ce1d run=%d: %.1f GB/s\n", run, NFB * FB / (best * 1e-3) / 1e9);
   }
   // (2) CE and SM together: CE copies the first half, SM the second half
   const size_t half = (NFB * FB / 2) & ~(size_t)15;
