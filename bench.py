@@ -58,6 +58,14 @@ def parse():
                     help="also persist generated tokens (decode stand-in + K4 D2H), implies --handoff")
     ap.add_argument("--handoff-ctas", type=int, default=0, help="K3 CTA cap on PEs (0 = default)")
     ap.add_argument("--gather-ctas", type=int, default=-1, help="K1/K2 CTA cap (-1 = auto)")
+    ap.add_argument("--prefill", action="store_true",
+                    help="run the prefill stand-in on every PE: compute-quota batched forwards "
+                         "(build_forward_batch) of K5 attention-score passes over the landed KV, "
+                         "layer by layer, overlapped with the loads")
+    ap.add_argument("--quota-ms", type=float, default=0.5,
+                    help="prefill: compute quota per layer of a forward (ms of the cost model)")
+    ap.add_argument("--attend-tops", type=float, default=40.0,
+                    help="prefill: cost-model rate of K5 in tera multiply-adds/s (bilinear term)")
     ap.add_argument("--k1", default="sm", choices=["sm", "ce"],
                     help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs)")
     return ap.parse_args()
@@ -241,7 +249,14 @@ def measure_k1(device, shape, target_bytes=18421383168):
         st.close()
 
 
-def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
+def prefill_cost(args, shape):
+    """Cost model of the prefill stand-in per layer (AttentionCostModel):
+    K5 does bsz * cached * b multiply-adds per request chunk (bilinear), plus
+    a fixed per-layer cost of the gate and the launch (constant)."""
+    return (shape["b"] / (args.attend_tops * 1e12), 0.0, 0.0, 20e-6)
+
+
+def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=None):
     """Plan, build engines, run W + K steps; returns per-step max-over-ranks
     device and host times, plus per-rank info.  variant = (policy, sched_mode)."""
     import paper_2602_21548_b200 as dp
@@ -270,6 +285,11 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
     opt.handoff_ctas = args.handoff_ctas
     opt.gather_ctas = args.gather_ctas
     opt.seed = 9
+    prefill = args.prefill if prefill is None else prefill
+    if prefill:
+        opt.prefill = True
+        opt.compute_quota = args.quota_ms * 1e-3
+        opt.prefill_cost = prefill_cost(args, shape)
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     from paper_2602_21548_b200 import dist as dpdist
     digests = dist.allgather(dpdist.plan_digest(planned))
@@ -304,6 +324,18 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
                 for e, (sp, ms) in part.items():
                     spans[e] = sp
                     per_engine[e] = round(ms, 1)
+    fwd = None
+    if prefill:
+        # the compute alone: the PEs' forwards again over the KV already landed
+        pes = [rt for e, rt in engines.items() if e < P]
+        dist.barrier()
+        r = [rt.run_forwards() for rt in pes]
+        alone = dist.max(max([x.device_ms for x in r], default=0.0))
+        n_fwd = sum(dist.allgather(sum(x.forwards for x in r)))
+        work = sum(it[2] * it[4] for pe in range(P) for _, items in xp.forwards(pe) for it in items)
+        fwd = dict(forwards_per_step=n_fwd, compute_alone_ms=round(alone, 3),
+                   macs_per_step=work * shape["b"] * shape["L"],
+                   est_s_per_step=sum(est for pe in range(P) for est, _ in xp.forwards(pe)) * shape["L"])
     snic = sum(u["total_bytes"] for u in planned["usage"] if u["kind"] == "snic_read")
     info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens,
                 handoff_bytes=xp.handoff_bytes if (args.handoff or args.persist) else 0,
@@ -314,7 +346,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None):
                 decisions=len(planned["decisions"]), pool_slots=xp.pool_slots, spans=spans,
                 per_engine_ms=[per_engine[e] for e in sorted(per_engine)] if per_engine else None,
                 caps=caps,
-                store_fb=xp.store_fb, launches=launches, read_bytes=read_bytes)
+                store_fb=xp.store_fb, launches=launches, read_bytes=read_bytes, prefill=fwd)
     if clocks is not None:
         clocks.__exit__()
     engines.clear()  # frees pools, stores and peer mappings before the next policy
@@ -492,6 +524,8 @@ def main():
     for name, var in zip(policies, variants):
         results[name] = run_policy(args, dist, var, trajs, shape, P, D,
                                    clocks if (name == policies[0] and dist.local == 0) else None)
+    if args.prefill:  # the same loads without the prefill: the overlap baseline
+        results["load_only"] = run_policy(args, dist, variants[0], trajs, shape, P, D, None, prefill=False)
     head = results[policies[0]]
     info = head["info"]
     dev_s = sum(head["dev_ms"]) / 1e3
@@ -577,6 +611,23 @@ def main():
                               "gbps": round(info["handoff_bytes"] * K / dev_s / 1e9, 3),
                               "what": "PeToDe/MissMerge per layer into DE decode pools (K3, NVLink) "
                                       "+ prefill stand-in; DE read path fused with DecodeH2D"}
+        if args.prefill:
+            pf = info["prefill"]
+            lo = results["load_only"]
+            lo_ms = sum(lo["dev_ms"]) / K
+            step_ms = dev_s * 1e3 / K
+            both = pf["compute_alone_ms"]
+            out["prefill"] = {
+                "what": "quota-batched forwards (build_forward_batch) of K5 attention-score passes "
+                        "over the landed KV, layer l gated on the batch's landed counters",
+                "quota_ms_per_layer": args.quota_ms, "cost_model": prefill_cost(args, shape),
+                "forwards_per_step": pf["forwards_per_step"],
+                "prompt_tokens_per_s": round(tokens_s, 1),
+                "step_ms": round(step_ms, 3), "load_only_ms": round(lo_ms, 3),
+                "compute_alone_ms": both,
+                "overlap": round((lo_ms + both - step_ms) / min(lo_ms, both), 3) if min(lo_ms, both) > 0 else None,
+                "k5_tmacs": round(pf["macs_per_step"] / (both * 1e-3) / 1e12, 2) if both > 0 else None,
+                "cost_model_s_per_step": round(pf["est_s_per_step"], 4)}
         if "pe_only" in results and n > 1:
             po = results["pe_only"]
             po_s = sum(po["dev_ms"]) / 1e3

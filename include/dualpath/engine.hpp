@@ -28,6 +28,7 @@
 
 #include "dualpath/kv_abi.h"
 #include "pdsim/desim.hpp"
+#include "pdsim/scheduler.hpp"
 #include "pdsim/types.hpp"
 
 namespace dualpath {
@@ -62,6 +63,15 @@ struct ExecOptions {
   // the decode stand-in for the generated tokens and persists them (K4) every
   // 64 generated tokens plus the final partial, into its persist store
   bool persist = false;
+  // Prefill stand-in (not with `handoff`): every PE packs
+  // its requests, in the order their KV lands, into forward batches with
+  // pdsim::build_forward_batch under `compute_quota` (seconds per layer of
+  // `prefill_cost`) and runs each batch layer by layer as K5
+  // (dp_prefill_attend), layer l gated on the batch's landed counters.
+  bool prefill = false;
+  double compute_quota = 2e-3;
+  pdsim::AttentionCostModel prefill_cost{};
+  std::int32_t attend_ctas = 0;        // K5 CTA cap (0 = default)
 };
 
 // One request's hit-KV transfer (all layers), in global execution order.
@@ -98,6 +108,27 @@ struct LoadJob {
   std::int64_t gen = 0;          // generated tokens of the turn
   std::int32_t n_tblk = 0;       // decode-pool blocks: ceil((C + A + gen) / T)
   std::int64_t dec_off = 0;      // offset of its blocks in the DE's decode tables
+  // ---- prefill ----
+  std::vector<int> consumer_waits;  // jobs whose slots this one reuses: their last forward
+                                    // must be done before this job's load writes
+  std::int64_t fwd_off = 0;         // offset of its slots in the PE's forward slot table
+};
+
+// One request chunk of a forward batch (ExecOptions::prefill).
+struct FwdItem {
+  int req = 0;               // plan request id
+  int job = -1;              // its load job (-1: no cached KV)
+  std::int64_t cached = 0;   // C
+  std::int64_t q_begin = 0;  // first query token of the chunk (offset into the append)
+  std::int64_t bsz = 0;      // query tokens of the chunk
+  std::int32_t row = 0;      // digest row of the request on its PE
+  bool first = false;        // the request's first forward (gates on its KV)
+};
+
+struct Forward {
+  std::int32_t begin = 0, end = 0;  // items [begin, end) of the PE's fwd_items
+  double estimated_time = 0;        // per layer, the cost model's (pdsim::ForwardBatch)
+  std::int32_t last_row = 0;        // FIFO row of its last item
 };
 
 struct ExecPlan {
@@ -143,6 +174,14 @@ struct ExecPlan {
   // persist_tokens at every block_size generated tokens + the final partial
   std::vector<std::pair<std::int64_t, std::int64_t>> persist_chunks(const LoadJob& j) const;
   std::uint32_t de_total_items(const LoadJob& j) const;    // decode-pool row target (all layers)
+
+  // ---- prefill ----
+  bool prefill = false;
+  std::vector<std::vector<FwdItem>> fwd_items;   // per PE: the items of its forwards, in order
+  std::vector<std::vector<Forward>> forwards;    // per PE
+  std::vector<std::vector<int>> fwd_rows;        // per PE: request id of each digest row (FIFO)
+  std::vector<std::vector<std::int32_t>> fwd_slot;  // per PE: slots of the jobs landing there
+  std::vector<int> last_fwd;                     // per job: the forward (on its PE) that reads it last
 };
 
 // Builds the executor plan from planner output.  Requests with C = 0 move no
@@ -165,6 +204,7 @@ struct StepResult {
   std::int64_t bytes_read = 0;  // hit bytes this engine read from storage
   std::int64_t launches = 0;    // kernels launched by this engine
   std::int64_t jobs = 0;
+  std::int64_t forwards = 0;    // prefill forwards run (PE, ExecOptions::prefill)
 };
 
 class EngineRuntime {
@@ -191,6 +231,11 @@ class EngineRuntime {
   // Issue this engine's transfers for one pass over the plan and wait for
   // them (and, on a PE, for every push landing in its pool).
   StepResult run_step();
+  // Prefill mode, PE only: run this PE's forwards again over the KV already
+  // in the pool (after a run_step, counters not reset): the compute alone.
+  StepResult run_forwards();
+  // Prefill mode, PE only: the K5 digests [row][layer] of the last step.
+  std::vector<std::uint64_t> prefill_digests() const;
 
   // Parity helpers: content hash of a pool Layer Block (PE only), and the
   // raw pool / counters for tests.
@@ -238,6 +283,17 @@ class EngineRuntime {
   std::vector<std::int64_t> pe_done_off_;   // per job: offset of its pe_done_preds
   std::int64_t final_wait_off_ = 0;         // DE: all own tickets (decode-ready gate)
   std::int32_t final_wait_n_ = 0;
+  // ---- prefill ----
+  StepResult run_step_prefill(bool loads);
+  void enqueue_forward(int f, StepResult& res);
+  void upload_prefill_tables();
+  std::vector<void*> ev_fwd_;               // PE: per forward, recorded after its last layer
+  std::vector<std::vector<dp_attend_item>> fwd_att_;  // PE: per forward, K5 items
+  std::vector<std::int64_t> fwd_wait_off_;  // PE: per forward, offset of its KV waits in d_wt_
+  std::vector<std::int32_t> fwd_wait_n_;
+  std::vector<std::vector<std::int32_t>> fwd_done_;   // PE: per forward, tickets read last there
+  std::uint64_t* d_digest_ = nullptr;
+  std::int32_t* d_fwd_slot_ = nullptr;
   // ---- persistence (DE) ----
   dp_store* persist_store_ = nullptr;
   std::int32_t* d_dec_slot_ = nullptr;

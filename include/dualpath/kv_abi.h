@@ -213,6 +213,38 @@ int dp_decode_fill(dp_pool* de_pool, const dp_span_job* jobs, int32_t n_jobs, ui
 int dp_persist_d2h(const dp_pool* de_pool, dp_store* target, const dp_span_job* jobs,
                    int32_t n_jobs, dp_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Prefill stand-in driven by compute-quota batching (
+ * build_forward_batch, proj/src/scheduler.cpp:174-219).
+ *
+ * K5 is the attention-score pass of one prefill layer for the items of one
+ * forward batch: item i's query tokens [q_begin, q_begin + bsz) of its append
+ * attend to its cached tokens [0, cached) of `layer`, read from the PE pool
+ * (the KV the loader landed).  Queries are procedural bytes
+ *   q(req, layer, q, w) = splitmix64(qbase ^ (q << 16 | w)),
+ *   qbase = splitmix64((req << 20 | layer) ^ seed * 0xA24BAED4963EE407),
+ * and the pass accumulates, exactly (mod 2^64), into digest[layer]
+ *   sum_q sum_t dot_u8(Q[q], K[t])      (unsigned bytes, b per token)
+ * on CUDA cores (dp4a): bsz * cached * b multiply-adds, the bilinear term of
+ * the cost model.  Chunking a request over several forwards splits its
+ * queries, so the digest of a request is independent of the batching. */
+typedef struct dp_attend_item {
+  const int32_t* slot;  /* [ceil(cached / T)] PE-pool slots of the cached blocks */
+  int64_t cached;       /* keys: tokens [0, cached) */
+  int64_t q_begin;      /* first query token (offset into the append) */
+  int64_t bsz;          /* query tokens of this chunk */
+  uint64_t* digest;     /* [n_layer] device accumulators of the request */
+  uint32_t req;         /* request key of the procedural queries */
+  int32_t reserved;
+} dp_attend_item;
+
+#define DP_MAX_ATTEND_ITEMS_PER_LAUNCH 48
+
+int dp_prefill_attend(const dp_pool* pe_pool, int32_t layer, const dp_attend_item* items,
+                      int32_t n_items, uint64_t seed, dp_stream stream);
+/* Cap on the CTAs of a K5 launch on `device` (0 = default: every SM). */
+int dp_set_attend_ctas(int device, int32_t ctas);
+
 /* K1 on the copy engine (no SMs): the same transfer as dp_h2d_layer_gather,
  * issued as one strided cudaMemcpy2DAsync per contiguous run of blocks per
  * layer (Full-Block pitch -> Layer-Block pitch) plus the partial last block,

@@ -98,6 +98,48 @@ uint64_t kvref_layer_block_hash(const kv_geom* g, uint64_t seed, int64_t fb, int
   return h;
 }
 
+/* Prefill stand-in digest (K5, dp_prefill_attend in include/dualpath/kv_abi.h):
+ *   sum_{q in [q_begin, q_begin + bsz)} sum_{t < cached} sum_i Q[q][i] * K[t][i]   (mod 2^64)
+ * over unsigned bytes i < b, K[t] = token t of Layer Block `layer` of Full
+ * Block fb[t / T], Q[q] the procedural query bytes.  Restated as the inner
+ * product of the per-lane column sums (exact: the same integer mod 2^64),
+ * so the check costs (bsz + cached) * b instead of bsz * cached * b. */
+#define QUERY_MUL 0xA24BAED4963EE407ull
+uint64_t kvref_query_word(uint64_t seed, uint32_t req, int32_t layer, int64_t q, int64_t w) {
+  const uint64_t base = splitmix64((((uint64_t)req << 20) | (uint64_t)layer) ^ (seed * QUERY_MUL));
+  return splitmix64(base ^ (((uint64_t)q << 16) | (uint64_t)w));
+}
+
+uint64_t kvref_attend_digest(const kv_geom* g, uint64_t seed, const int64_t* fb, int64_t cached,
+                             uint32_t req, int32_t layer, int64_t q_begin, int64_t bsz) {
+  const int64_t b = g->bytes_per_token_layer;
+  uint64_t* kcol = (uint64_t*)calloc((size_t)b, sizeof(uint64_t));
+  uint64_t* qcol = (uint64_t*)calloc((size_t)b, sizeof(uint64_t));
+  if (!kcol || !qcol) {
+    free(kcol);
+    free(qcol);
+    return 0;
+  }
+  const int64_t lw0 = (int64_t)layer * lb_bytes(g) / 8;
+  for (int64_t t = 0; t < cached; ++t) {
+    const int64_t blk = t / g->block_tokens, within = t % g->block_tokens;
+    for (int64_t w = 0; w < b / 8; ++w) {
+      const uint64_t word = kvref_word(seed, fb[blk], lw0 + within * (b / 8) + w);
+      for (int k = 0; k < 8; ++k) kcol[8 * w + k] += (word >> (8 * k)) & 0xff;
+    }
+  }
+  for (int64_t q = q_begin; q < q_begin + bsz; ++q)
+    for (int64_t w = 0; w < b / 8; ++w) {
+      const uint64_t word = kvref_query_word(seed, req, layer, q, w);
+      for (int k = 0; k < 8; ++k) qcol[8 * w + k] += (word >> (8 * k)) & 0xff;
+    }
+  uint64_t d = 0;
+  for (int64_t i = 0; i < b; ++i) d += qcol[i] * kcol[i];
+  free(kcol);
+  free(qcol);
+  return d;
+}
+
 /* Restated hit transfer: move each job's Layer Blocks from a store image
  * into a pool image [n_layer][n_slots][T][b] with memcpy (serial). */
 int kvref_gather(const kv_geom* g, const uint8_t* store, int64_t store_fb, const kv_job* jobs,

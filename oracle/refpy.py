@@ -49,6 +49,14 @@ def kvref():
         lib = ctypes.CDLL(KVREF_SO)
         lib.kvref_word.restype = ctypes.c_uint64
         lib.kvref_word.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64]
+        lib.kvref_attend_digest.restype = ctypes.c_uint64
+        lib.kvref_attend_digest.argtypes = [ctypes.POINTER(KvGeom), ctypes.c_uint64,
+                                            ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
+                                            ctypes.c_uint32, ctypes.c_int32, ctypes.c_int64,
+                                            ctypes.c_int64]
+        lib.kvref_query_word.restype = ctypes.c_uint64
+        lib.kvref_query_word.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32,
+                                         ctypes.c_int64, ctypes.c_int64]
         lib.kvref_splitmix64.restype = ctypes.c_uint64
         lib.kvref_splitmix64.argtypes = [ctypes.c_uint64]
         lib.kvref_fill_store.argtypes = [ctypes.POINTER(KvGeom), ctypes.c_uint64, ctypes.c_int64,
@@ -87,6 +95,23 @@ def layer_block(g, seed, fb, layer, ntok):
     out = np.empty(ntok * g.bytes_per_token_layer, dtype=np.uint8)
     kvref().kvref_layer_block(ctypes.byref(g), seed, fb, layer, ntok, out.ctypes.data)
     return out
+
+
+def attend_digest(g, seed, fbs, cached, req, layer, q_begin, bsz):
+    """Oracle of K5 (dp_prefill_attend) for one request chunk at one layer."""
+    arr = (ctypes.c_int64 * max(1, len(fbs)))(*fbs)
+    return kvref().kvref_attend_digest(ctypes.byref(g), seed, arr, cached, req, layer, q_begin, bsz)
+
+
+def attend_digest_bruteforce(g, seed, fbs, cached, req, layer, q_begin, bsz):
+    """The literal double sum in numpy (small cases): pins the column-sum form."""
+    b = g.bytes_per_token_layer
+    keys = np.concatenate([layer_block(g, seed, fb, layer, g.block_tokens) for fb in fbs])[: cached * b]
+    keys = keys.reshape(cached, b).astype(np.uint64)
+    qw = np.array([[kvref().kvref_query_word(seed, req, layer, q, w) for w in range(b // 8)]
+                   for q in range(q_begin, q_begin + bsz)], dtype=np.uint64)
+    qs = qw.view(np.uint8).reshape(bsz, b).astype(np.uint64)
+    return int((qs @ keys.T).sum(dtype=np.uint64))
 
 
 def layer_block_hash(g, seed, fb, layer, ntok):

@@ -55,6 +55,12 @@ class SpanJob(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
+class AttendItem(ctypes.Structure):
+    _fields_ = [("slot", ctypes.c_void_p), ("cached", ctypes.c_int64), ("q_begin", ctypes.c_int64),
+                ("bsz", ctypes.c_int64), ("digest", ctypes.c_void_p), ("req", ctypes.c_uint32),
+                ("reserved", ctypes.c_int32)]
+
+
 class PoolHandle(ctypes.Structure):
     _fields_ = [("ipc", ctypes.c_ubyte * 64), ("geom", Geom), ("n_slots", ctypes.c_int32),
                 ("n_tickets", ctypes.c_int32), ("device", ctypes.c_int32),
@@ -113,6 +119,9 @@ def lib():
         "dp_device_count": ([], ctypes.c_int),
         "dp_set_gather_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
         "dp_set_handoff_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
+        "dp_prefill_attend": ([P, ctypes.c_int32, ctypes.POINTER(AttendItem), ctypes.c_int32,
+                               ctypes.c_uint64, P], ctypes.c_int),
+        "dp_set_attend_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -281,6 +290,15 @@ def set_gather_ctas(device, ctas):
 
 def set_handoff_ctas(device, ctas):
     check(lib().dp_set_handoff_ctas(device, ctas))
+
+
+def prefill_attend(pool, layer, items, n, seed, stream=0):
+    """K5: attention-score pass of one prefill layer (items: AttendItem array)."""
+    check(lib().dp_prefill_attend(pool.ptr, layer, items, n, seed, ctypes.c_void_p(stream)))
+
+
+def set_attend_ctas(device, ctas):
+    check(lib().dp_set_attend_ctas(device, ctas))
 
 
 def device_count():

@@ -387,7 +387,20 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("seed", &dualpath::ExecOptions::seed)
       .def_readwrite("pool_slots", &dualpath::ExecOptions::pool_slots)
       .def_readwrite("pool_bytes_max", &dualpath::ExecOptions::pool_bytes_max)
-      .def_readwrite("wait_timeout_ms", &dualpath::ExecOptions::wait_timeout_ms);
+      .def_readwrite("wait_timeout_ms", &dualpath::ExecOptions::wait_timeout_ms)
+      .def_readwrite("prefill", &dualpath::ExecOptions::prefill)
+      .def_readwrite("compute_quota", &dualpath::ExecOptions::compute_quota)
+      .def_readwrite("attend_ctas", &dualpath::ExecOptions::attend_ctas)
+      .def_property(
+          "prefill_cost",
+          [](const dualpath::ExecOptions& o) {
+            const auto& m = o.prefill_cost;
+            return std::make_tuple(m.coeff_bilinear, m.coeff_quadratic, m.coeff_linear, m.constant);
+          },
+          [](dualpath::ExecOptions& o, const std::tuple<double, double, double, double>& c) {
+            auto& m = o.prefill_cost;
+            std::tie(m.coeff_bilinear, m.coeff_quadratic, m.coeff_linear, m.constant) = c;
+          });
 
   py::class_<dualpath::ExecPlan, std::shared_ptr<dualpath::ExecPlan>>(m, "ExecPlan")
       .def_readonly("n_engines", &dualpath::ExecPlan::n_engines)
@@ -439,7 +452,25 @@ PYBIND11_MODULE(_core, m) {
       })
       .def("by_reader", [](const dualpath::ExecPlan& x, int e) { return x.by_reader.at(e); })
       .def("by_pe", [](const dualpath::ExecPlan& x, int e) { return x.by_pe.at(e); })
-      .def("by_de", [](const dualpath::ExecPlan& x, int e) { return x.by_de.at(e); });
+      .def("by_de", [](const dualpath::ExecPlan& x, int e) { return x.by_de.at(e); })
+      .def_readonly("prefill", &dualpath::ExecPlan::prefill)
+      // forwards(pe) -> [(estimated_time, [(req, job, cached, q_begin, bsz, row)])]
+      .def("forwards",
+           [](const dualpath::ExecPlan& x, int pe) {
+             py::list out;
+             for (const dualpath::Forward& f : x.forwards.at(pe)) {
+               py::list items;
+               for (std::int32_t i = f.begin; i < f.end; ++i) {
+                 const dualpath::FwdItem& it = x.fwd_items.at(pe)[i];
+                 items.append(py::make_tuple(it.req, it.job, it.cached, it.q_begin, it.bsz, it.row));
+               }
+               out.append(py::make_tuple(f.estimated_time, items));
+             }
+             return out;
+           })
+      .def("fwd_rows", [](const dualpath::ExecPlan& x, int pe) { return x.fwd_rows.at(pe); })
+      .def("consumer_waits", [](const dualpath::ExecPlan& x, int job) { return x.jobs.at(job).consumer_waits; })
+      .def("last_fwd", [](const dualpath::ExecPlan& x, int job) { return x.last_fwd.at(job); });
 
   m.def(
       "build_exec_plan",
@@ -483,7 +514,8 @@ PYBIND11_MODULE(_core, m) {
       .def_readonly("host_ms", &dualpath::StepResult::host_ms)
       .def_readonly("bytes_read", &dualpath::StepResult::bytes_read)
       .def_readonly("launches", &dualpath::StepResult::launches)
-      .def_readonly("jobs", &dualpath::StepResult::jobs);
+      .def_readonly("jobs", &dualpath::StepResult::jobs)
+      .def_readonly("forwards", &dualpath::StepResult::forwards);
 
   py::class_<dualpath::EngineRuntime>(m, "EngineRuntime")
       .def(py::init([](std::shared_ptr<dualpath::ExecPlan> plan, int engine, int device) {
@@ -502,6 +534,8 @@ PYBIND11_MODULE(_core, m) {
       .def("attach_peer_local", &dualpath::EngineRuntime::attach_peer_local)
       .def("reset_counters", &dualpath::EngineRuntime::reset_counters)
       .def("run_step", &dualpath::EngineRuntime::run_step, py::call_guard<py::gil_scoped_release>())
+      .def("run_forwards", &dualpath::EngineRuntime::run_forwards, py::call_guard<py::gil_scoped_release>())
+      .def("prefill_digests", &dualpath::EngineRuntime::prefill_digests)
       .def("checksum",
            [](dualpath::EngineRuntime& e, int layer, const std::vector<std::int32_t>& slots,
               const std::vector<std::int32_t>& ntok) { return e.checksum(layer, slots, ntok); })

@@ -116,6 +116,87 @@ std::int32_t size_pool(std::int32_t requested, std::int64_t peak, std::int64_t s
   return static_cast<std::int32_t>(n);
 }
 
+// Prefill forwards of every PE.  A PE's FIFO is its requests in the order
+// their KV lands (t_read_done, then request id: the job order); forwards
+// are build_forward_batch over a window of that FIFO.  The window stops
+// before the first request whose slots reuse those of a request still in
+// the window: that request's load waits for the forward reading the
+// earlier one, so the two must not share a forward.
+void build_forwards(ExecPlan& x, const pdsim::desim::SimReport& plan) {
+  std::vector<int> job_of_req;
+  for (std::size_t i = 0; i < x.jobs.size(); ++i) {
+    const int r = x.jobs[i].req;
+    if (r >= static_cast<int>(job_of_req.size())) job_of_req.resize(r + 1, -1);
+    job_of_req[r] = static_cast<int>(i);
+  }
+  std::vector<std::vector<const pdsim::desim::RequestPlan*>> fifo(x.n_pe);
+  for (const auto& r : plan.requests)
+    if (r.pe >= 0 && r.pe < x.n_pe && r.t_read_done >= 0) fifo[r.pe].push_back(&r);
+  pdsim::SchedulerParams sp;
+  sp.compute_quota = x.opt.compute_quota;
+  x.fwd_items.assign(x.n_pe, {});
+  x.forwards.assign(x.n_pe, {});
+  x.fwd_rows.assign(x.n_pe, {});
+  x.last_fwd.assign(x.jobs.size(), -1);
+  std::vector<int> row_of_job(x.jobs.size(), -1);
+  for (int p = 0; p < x.n_pe; ++p) {
+    auto& q = fifo[p];
+    std::stable_sort(q.begin(), q.end(), [](const auto* a, const auto* b) {
+      return a->t_read_done != b->t_read_done ? a->t_read_done < b->t_read_done : a->request_id < b->request_id;
+    });
+    const int n = static_cast<int>(q.size());
+    std::vector<int> job(n, -1), pred_row(n, -1);
+    for (int i = 0; i < n; ++i) {
+      x.fwd_rows[p].push_back(q[i]->request_id);
+      const int rid = q[i]->request_id;
+      if (rid < static_cast<int>(job_of_req.size()) && job_of_req[rid] >= 0) {
+        job[i] = job_of_req[rid];
+        row_of_job[job[i]] = i;
+      }
+    }
+    for (int i = 0; i < n; ++i)
+      if (job[i] >= 0)
+        for (int w : x.jobs[job[i]].consumer_waits) pred_row[i] = std::max(pred_row[i], row_of_job[w]);
+    int head = 0, barrier = 0;
+    std::int64_t head_done = 0;  // query tokens of the head request already run
+    std::vector<pdsim::BatchItem> window;
+    while (head < n) {
+      barrier = std::max(barrier, head + 1);
+      while (barrier < n && pred_row[barrier] < head) ++barrier;
+      window.clear();
+      for (int i = head; i < barrier; ++i)
+        window.push_back({q[i]->request_id, q[i]->cached, q[i]->append - (i == head ? head_done : 0)});
+      const pdsim::ForwardBatch fb = pdsim::build_forward_batch(window, sp, x.opt.prefill_cost);
+      Forward f;
+      f.begin = static_cast<std::int32_t>(x.fwd_items[p].size());
+      f.estimated_time = fb.estimated_time;
+      const int fi = static_cast<int>(x.forwards[p].size());
+      for (std::size_t k = 0; k < fb.items.size(); ++k) {
+        const int row = head + static_cast<int>(k);
+        FwdItem it;
+        it.req = fb.items[k].request_id;
+        it.job = job[row];
+        it.cached = fb.items[k].cached;
+        it.q_begin = k == 0 ? head_done : 0;
+        it.bsz = fb.items[k].bsz;
+        it.row = row;
+        it.first = it.q_begin == 0;
+        x.fwd_items[p].push_back(it);
+        if (it.job >= 0) x.last_fwd[it.job] = fi;
+        f.last_row = row;
+      }
+      f.end = static_cast<std::int32_t>(x.fwd_items[p].size());
+      x.forwards[p].push_back(f);
+      if (fb.chunked) {
+        head_done = fb.consumed_whole == 0 ? head_done + fb.chunk_bsz : fb.chunk_bsz;
+      } else {
+        head_done = 0;
+      }
+      head += static_cast<int>(fb.consumed_whole);
+    }
+  }
+}
+
 }  // namespace
 
 std::int64_t ExecPlan::fb_of(int traj, std::int64_t block) const {
@@ -151,6 +232,11 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
   x.handoff = opt.handoff;
   x.persist = opt.persist;
   if (x.persist && !x.handoff) throw std::invalid_argument("build_exec_plan: persist needs handoff");
+  x.prefill = opt.prefill;
+  if (x.prefill && x.handoff)
+    throw std::invalid_argument("build_exec_plan: prefill and handoff are separate modes");
+  if (x.prefill && !(opt.compute_quota > 0))
+    throw std::invalid_argument("build_exec_plan: compute_quota must be > 0");
   x.n_engines = cfg.total_engines();
   x.n_pe = cfg.prefill_nodes * cfg.engines_per_node;
   x.geom = {cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer};
@@ -251,7 +337,12 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
       q.owner[s] = e.job;
       if (prev < 0) continue;
       const LoadJob& pj = jobs[prev];
-      if (!x.handoff) {
+      if (x.prefill) {
+        // the previous occupant's KV is read by its forwards: the reuse
+        // waits for the last of them (which implies it landed)
+        if (std::find(j.consumer_waits.begin(), j.consumer_waits.end(), prev) == j.consumer_waits.end())
+          j.consumer_waits.push_back(prev);
+      } else if (!x.handoff) {
         // same reader: stream order serialises launches, but items of one
         // launch run concurrently, so the reuse must start a new launch
         if (pj.reader == j.reader) {
@@ -322,10 +413,22 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
   x.ho_pe_slot.assign(x.n_pe, {});
   x.ho_de_slot.assign(x.n_pe, {});
   x.reader_bytes.assign(x.n_engines, 0);
+  x.fwd_slot.assign(x.n_pe, {});
   x.jobs.reserve(order.size());
   for (int old : order) {
     LoadJob j = std::move(jobs[old]);
     for (int& w : j.k3_waits) w = pos[w];
+    for (int& w : j.consumer_waits) w = pos[w];
+    if (x.prefill) {
+      if (j.reader != j.pe)  // a DE load waits on the PE's "consumed" rows [n, 2n)
+        for (int w : j.consumer_waits) {
+          j.preds.push_back(x.jobs[w].ticket + x.n_tickets[j.pe]);
+          j.pred_targets.push_back(1u);
+        }
+      j.fwd_off = static_cast<std::int64_t>(x.fwd_slot[j.pe].size());
+      x.fwd_slot[j.pe].insert(x.fwd_slot[j.pe].end(), pe_slots[old].begin(),
+                              pe_slots[old].begin() + j.n_blk);
+    }
     const int idx = static_cast<int>(x.jobs.size());
     auto& src = x.src_fb[j.reader];
     auto& dst = x.slots[j.reader];
@@ -360,6 +463,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     x.by_pe[j.pe].push_back(idx);
     x.jobs.push_back(std::move(j));
   }
+  if (x.prefill) build_forwards(x, plan);
   return x;
 }
 
@@ -384,7 +488,9 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
     check(dp_store_create(device_, &x.geom, x.store_fb, x.opt.seed, &store_), "dp_store_create");
   if (is_pe()) {
     // handoff: rows [0, n) hit-KV landed, rows [n, 2n) handoff (K3) done
-    const std::int32_t rows = std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff ? 2 : 1);
+    // handoff / prefill: rows [0, n) hit-KV landed, rows [n, 2n) handoff done / consumed
+    const std::int32_t rows =
+        std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff || x.prefill ? 2 : 1);
     check(dp_pool_create(device_, &x.geom, x.pool_slots, rows, &pool_), "dp_pool_create");
     peers_[engine_] = pool_;
   } else if (x.handoff) {
@@ -400,11 +506,71 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   } else {
     upload_tables();
   }
+  if (x.prefill && is_pe()) upload_prefill_tables();
   // K1 is PCIe-bound and keeps its rate down to ~32 CTAs; on a PE that also
   // runs K3 the remaining SMs go to the handoff
-  const std::int32_t ctas = x.opt.gather_ctas >= 0 ? x.opt.gather_ctas : (x.handoff && is_pe() ? 64 : 0);
+  const std::int32_t ctas =
+      x.opt.gather_ctas >= 0 ? x.opt.gather_ctas : ((x.handoff || x.prefill) && is_pe() ? 64 : 0);
   check(dp_set_gather_ctas(device_, ctas), "dp_set_gather_ctas");
   if (is_pe()) check(dp_set_handoff_ctas(device_, x.opt.handoff_ctas), "dp_set_handoff_ctas");
+  if (is_pe() && x.prefill) check(dp_set_attend_ctas(device_, x.opt.attend_ctas), "dp_set_attend_ctas");
+}
+
+void EngineRuntime::upload_prefill_tables() {
+  const ExecPlan& x = *plan_;
+  const auto& items = x.fwd_items[engine_];
+  const auto& fwds = x.forwards[engine_];
+  const std::int32_t L = x.cfg.n_layer;
+  cudaStream_t c;
+  check_cuda(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "cudaStreamCreate");
+  stream_h_ = c;  // the compute stream: forwards
+  // the load stream outranks the compute stream: as K5 CTAs retire, the
+  // block scheduler places pending loader CTAs first
+  int lo = 0, hi = 0;
+  check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+  cudaStream_t s;
+  check_cuda(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi), "cudaStreamCreateWithPriority");
+  check_cuda(cudaStreamDestroy(static_cast<cudaStream_t>(stream_)), "cudaStreamDestroy");
+  stream_ = s;
+  d_fwd_slot_ = upload(x.fwd_slot[engine_]);
+  const std::size_t rows = std::max<std::size_t>(1, x.fwd_rows[engine_].size());
+  check_cuda(cudaMalloc(reinterpret_cast<void**>(&d_digest_), rows * L * sizeof(std::uint64_t)),
+             "cudaMalloc digests");
+  check_cuda(cudaMemset(d_digest_, 0, rows * L * sizeof(std::uint64_t)), "cudaMemset digests");
+  std::vector<std::int32_t> wt;
+  std::vector<std::uint32_t> wg;
+  fwd_att_.assign(fwds.size(), {});
+  fwd_done_.assign(fwds.size(), {});
+  fwd_wait_off_.assign(fwds.size(), 0);
+  fwd_wait_n_.assign(fwds.size(), 0);
+  for (std::size_t f = 0; f < fwds.size(); ++f) {
+    fwd_wait_off_[f] = static_cast<std::int64_t>(wt.size());
+    for (std::int32_t i = fwds[f].begin; i < fwds[f].end; ++i) {
+      const FwdItem& it = items[i];
+      dp_attend_item a{};
+      a.cached = it.cached;
+      a.q_begin = it.q_begin;
+      a.bsz = it.bsz;
+      a.digest = d_digest_ + static_cast<std::int64_t>(it.row) * L;
+      a.req = static_cast<std::uint32_t>(it.req);
+      if (it.job >= 0) {
+        const LoadJob& j = x.jobs[it.job];
+        a.slot = d_fwd_slot_ + j.fwd_off;
+        if (it.first) {  // the request's KV is read here first: gate every layer on it
+          wt.push_back(j.ticket);
+          wg.push_back(static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block));
+        }
+        if (x.last_fwd[it.job] == static_cast<int>(f)) fwd_done_[f].push_back(j.ticket);
+      }
+      fwd_att_[f].push_back(a);
+    }
+    fwd_wait_n_[f] = static_cast<std::int32_t>(wt.size() - fwd_wait_off_[f]);
+    cudaEvent_t e;
+    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    ev_fwd_.push_back(e);
+  }
+  d_wt_ = upload(wt);
+  d_wg_ = upload(wg);
 }
 
 EngineRuntime::~EngineRuntime() {
@@ -424,10 +590,12 @@ EngineRuntime::~EngineRuntime() {
                   static_cast<void*>(d_ho_src_), static_cast<void*>(d_ho_pe_),
                   static_cast<void*>(d_ho_de_), static_cast<void*>(d_dual_de_),
                   static_cast<void*>(d_wt_), static_cast<void*>(d_wg_),
-                  static_cast<void*>(d_dec_slot_), static_cast<void*>(d_dec_fb_)})
+                  static_cast<void*>(d_dec_slot_), static_cast<void*>(d_dec_fb_),
+                  static_cast<void*>(d_digest_), static_cast<void*>(d_fwd_slot_)})
     if (p) cudaFree(p);
   for (void* e : ev_load_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* e : ev_k3_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  for (void* e : ev_fwd_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   if (ev_start_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_start_));
   if (ev_end_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_end_));
   if (stream_h_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_h_));
@@ -564,6 +732,7 @@ void EngineRuntime::reset_counters() {
 StepResult EngineRuntime::run_step() {
   const ExecPlan& x = *plan_;
   if (x.handoff) return run_step_handoff();
+  if (x.prefill && is_pe()) return run_step_prefill(true);
   DeviceScope ds(device_);
   auto s = static_cast<cudaStream_t>(stream_);
   StepResult res;
@@ -637,7 +806,7 @@ StepResult EngineRuntime::run_step() {
     ++res.jobs;
   }
   flush();
-  if (pool_ && n_wait_ > 0) {
+  if (pool_ && n_wait_ > 0 && !x.prefill) {
     check(dp_wait_tickets(pool_, d_wait_tickets_, d_wait_targets_, n_wait_, x.cfg.n_layer,
                           x.opt.wait_timeout_ms, s),
           "dp_wait_tickets");
@@ -654,6 +823,133 @@ StepResult EngineRuntime::run_step() {
   res.device_ms = ms;
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return res;
+}
+
+// Prefill step of a PE.  The load stream runs this PE's own reads (K1) in
+// FIFO order; the compute stream runs the forwards, layer by layer: a wait
+// on the landed counters of the requests the forward reads first, then K5.
+// Both are enqueued in FIFO order (a forward right after its last request's
+// load), so every wait is enqueued after its producer.  A load that reuses
+// slots waits for the event of the forward that last read them; DE loads
+// wait on the "consumed" rows the compute stream writes after that forward.
+StepResult EngineRuntime::run_step_prefill(bool loads) {
+  const ExecPlan& x = *plan_;
+  DeviceScope ds(device_);
+  auto s = static_cast<cudaStream_t>(stream_);
+  auto c = static_cast<cudaStream_t>(stream_h_);
+  StepResult res;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto start = static_cast<cudaEvent_t>(ev_start_);
+  auto end = static_cast<cudaEvent_t>(ev_end_);
+  check_cuda(cudaEventRecord(start, s), "cudaEventRecord");
+  check_cuda(cudaStreamWaitEvent(c, start, 0), "cudaStreamWaitEvent");
+  const std::int32_t L = x.cfg.n_layer;
+  const auto& rows = x.fwd_rows[engine_];
+  check_cuda(cudaMemsetAsync(d_digest_, 0, std::max<std::size_t>(1, rows.size()) * L * sizeof(std::uint64_t), c),
+             "cudaMemsetAsync digests");
+  const auto& fwds = x.forwards[engine_];
+  std::size_t fi = 0;
+  if (loads) {
+    std::vector<int> job_of_row(rows.size(), -1);
+    for (const FwdItem& it : x.fwd_items[engine_]) job_of_row[it.row] = it.job;
+    const bool k1_ce = x.opt.k1_mode == 1;
+    std::vector<dp_job> batch;
+    auto flush = [&]() {
+      if (batch.empty()) return;
+      const auto n = static_cast<int32_t>(batch.size());
+      if (k1_ce) {
+        check(dp_h2d_layer_copy(pool_, store_, batch.data(), n, s), "dp_h2d_layer_copy");
+      } else {
+        check(dp_h2d_layer_gather(pool_, store_, batch.data(), n, s), "dp_h2d_layer_gather");
+        res.launches += (n + DP_MAX_JOBS_PER_LAUNCH - 1) / DP_MAX_JOBS_PER_LAUNCH;
+      }
+      batch.clear();
+    };
+    const double cap = x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
+                                                            : x.opt.storage_cap_per_engine[engine_];
+    const double pace = x.opt.pace_scale;
+    double gate_s = 0;
+    for (std::size_t r = 0; r < rows.size(); ++r) {
+      const int ji = job_of_row[r];
+      if (ji >= 0 && x.jobs[ji].reader == engine_ && x.jobs[ji].n_blk > 0) {
+        const LoadJob& j = x.jobs[ji];
+        const std::int64_t bytes = j.cached * x.cfg.kv_bytes_per_token();
+        const bool gated = cap > 0 || pace > 0;
+        if (gated || !j.consumer_waits.empty() || batch.size() == DP_MAX_JOBS_PER_LAUNCH) flush();
+        for (int w : j.consumer_waits)
+          check_cuda(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[w]]), 0),
+                     "cudaStreamWaitEvent");
+        if (gated) {
+          const double begin = std::max(gate_s, pace > 0 ? j.t_admit * pace : 0.0);
+          gate_s = begin + (cap > 0 ? static_cast<double>(bytes) / cap : 0.0);
+          std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
+          res.spans.push_back({begin, gate_s, bytes});
+        }
+        if (k1_ce)
+          batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,
+                                 j.cached, j.n_blk, 0, L, j.ticket});
+        else
+          batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket});
+        res.bytes_read += bytes;
+        ++res.jobs;
+      }
+      while (fi < fwds.size() && fwds[fi].last_row <= static_cast<std::int32_t>(r)) {
+        flush();
+        enqueue_forward(static_cast<int>(fi++), res);
+      }
+    }
+    flush();
+  }
+  while (fi < fwds.size()) enqueue_forward(static_cast<int>(fi++), res);
+  // the step ends when both streams are drained
+  check_cuda(cudaEventRecord(end, s), "cudaEventRecord");
+  check_cuda(cudaStreamWaitEvent(c, end, 0), "cudaStreamWaitEvent");
+  check_cuda(cudaEventRecord(end, c), "cudaEventRecord");
+  check_cuda(cudaEventSynchronize(end), "step sync");
+  check(dp_wait_status(pool_), "transfer watchdog");
+  float ms = 0;
+  check_cuda(cudaEventElapsedTime(&ms, start, end), "cudaEventElapsedTime");
+  res.device_ms = ms;
+  res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return res;
+}
+
+void EngineRuntime::enqueue_forward(int f, StepResult& res) {
+  const ExecPlan& x = *plan_;
+  auto c = static_cast<cudaStream_t>(stream_h_);
+  const std::int32_t L = x.cfg.n_layer;
+  const auto& att = fwd_att_[f];
+  std::int64_t work = 0;
+  for (const dp_attend_item& a : att) work += (a.cached > 0 && a.bsz > 0) ? 1 : 0;
+  for (std::int32_t layer = 0; layer < L; ++layer) {
+    if (fwd_wait_n_[f] > 0) {
+      check(dp_wait_tickets(pool_, d_wt_ + fwd_wait_off_[f], d_wg_ + fwd_wait_off_[f], fwd_wait_n_[f], layer,
+                            x.opt.wait_timeout_ms, c),
+            "dp_wait_tickets (forward gate)");
+      ++res.launches;
+    }
+    check(dp_prefill_attend(pool_, layer, att.data(), static_cast<int32_t>(att.size()), x.opt.seed, c),
+          "dp_prefill_attend");
+    res.launches += (work + DP_MAX_ATTEND_ITEMS_PER_LAUNCH - 1) / DP_MAX_ATTEND_ITEMS_PER_LAUNCH;
+  }
+  check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_fwd_[f]), c), "cudaEventRecord");
+  for (std::int32_t t : fwd_done_[f])
+    check(dp_stream_write_counter(pool_, t + x.n_tickets[engine_], L, 1, c), "dp_stream_write_counter");
+  ++res.forwards;
+}
+
+StepResult EngineRuntime::run_forwards() {
+  if (!plan_->prefill || !is_pe()) throw std::logic_error("run_forwards: prefill mode, PE engines only");
+  return run_step_prefill(false);
+}
+
+std::vector<std::uint64_t> EngineRuntime::prefill_digests() const {
+  if (!plan_->prefill || !is_pe()) throw std::logic_error("prefill_digests: prefill mode, PE engines only");
+  DeviceScope ds(device_);
+  const std::size_t n = plan_->fwd_rows[engine_].size() * plan_->cfg.n_layer;
+  std::vector<std::uint64_t> out(n);
+  if (n) check_cuda(cudaMemcpy(out.data(), d_digest_, n * 8, cudaMemcpyDeviceToHost), "digests D2H");
+  return out;
 }
 
 // PD handoff step.  A PE runs two streams: the load stream (its own reads,
@@ -890,7 +1186,7 @@ std::vector<std::uint32_t> EngineRuntime::counters() const {
   std::int64_t bytes = 0;
   check(dp_pool_info(pool_, &base, &ctr, &bytes), "dp_pool_info");
   const ExecPlan& x = *plan_;
-  const std::int32_t rows = is_pe() ? std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff ? 2 : 1)
+  const std::int32_t rows = is_pe() ? std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff || x.prefill ? 2 : 1)
                                     : std::max<std::int32_t>(1, x.n_de_tickets[engine_]) * (x.persist ? 2 : 1);
   const std::size_t n = static_cast<std::size_t>(rows) * (x.cfg.n_layer + 1);
   std::vector<std::uint32_t> out(n);

@@ -1304,3 +1304,210 @@ int dp_persist_d2h(const dp_pool* de_pool, dp_store* target, const dp_span_job* 
 }
 
 }  // extern "C"
+
+// ============================================================ prefill stand-in
+// K5 dp_prefill_attend: the attention-score pass of one prefill layer over
+// the KV the loader landed.  Work unit = (item, 64-query
+// tile, group of kAttGroup 64-token key tiles).  A CTA stages the query tile
+// (procedural) and each key tile (from the pool, 16-byte loads) in shared
+// memory, row stride 37 x 16 B so the per-lane LDS.128 of 8 distinct rows is
+// bank-conflict free, and each thread accumulates a 4 x 4 block of
+// (query, key) dot products with dp4a.  Integer sums are order-independent,
+// so the digest is exact whatever the grid.
+namespace {
+
+constexpr int kAttRows = 64;     // query rows and key rows per tile
+constexpr int kAttWords = 144;   // 32-bit words per staged row chunk (576 B)
+constexpr int kAttStride = 148;  // padded row stride in words
+constexpr int kAttGroup = 4;     // key tiles per unit
+constexpr int kAttSmem = 2 * kAttRows * kAttStride * 4;  // 75,776 B
+constexpr uint64_t kQueryMul = 0xA24BAED4963EE407ull;
+int g_attend_ctas[kMaxDevices] = {};
+bool g_attend_init[kMaxDevices] = {};
+std::mutex g_attend_mu;
+
+struct AttendParams {
+  const char* pool;
+  int64_t bpt;
+  int64_t lb_bytes;
+  int64_t layer_off;  // layer * n_slots * lb_bytes
+  uint64_t seed_q;
+  int32_t layer;
+  int32_t block_tokens;
+  int32_t words;  // b / 4
+  int32_t n_jobs;
+  int64_t item_begin[DP_MAX_ATTEND_ITEMS_PER_LAUNCH + 1];
+  dp_attend_item jobs[DP_MAX_ATTEND_ITEMS_PER_LAUNCH];
+};
+static_assert(sizeof(AttendParams) <= 4000, "kernel parameter block too large");
+static_assert(sizeof(dp_attend_item) == 48, "dp_attend_item layout");
+
+__device__ __forceinline__ int64_t attend_key_tiles(int64_t cached) {
+  return (cached + kAttRows - 1) / kAttRows;
+}
+
+// <= 96 registers: the two K5 CTAs a default grid puts on
+// an SM leave room for a loader CTA (K1) beside them.
+__global__ void __maxnreg__(96) kv_prefill_attend(const __grid_constant__ AttendParams p) {
+  extern __shared__ uint4 att_smem[];
+  __shared__ uint64_t red[kThreads / 32];
+  uint32_t* qs = reinterpret_cast<uint32_t*>(att_smem);
+  uint32_t* ks = qs + kAttRows * kAttStride;
+  const int tid = threadIdx.x;
+  const int tq = tid >> 4, tt = tid & 15;
+  const int64_t total = p.item_begin[p.n_jobs];
+  for (int64_t unit = blockIdx.x; unit < total; unit += gridDim.x) {
+    const int j = decode_job(p, unit);
+    const dp_attend_item& it = p.jobs[j];
+    const int64_t local = unit - p.item_begin[j];
+    const int64_t n_kt = attend_key_tiles(it.cached);
+    const int64_t ng = (n_kt + kAttGroup - 1) / kAttGroup;
+    const int64_t q0 = (local / ng) * kAttRows;
+    const int64_t kt0 = (local % ng) * kAttGroup;
+    const int64_t kt1 = min(n_kt, kt0 + kAttGroup);
+    const int nq = static_cast<int>(min(static_cast<int64_t>(kAttRows), it.bsz - q0));
+    const uint64_t qbase =
+        splitmix64(((static_cast<uint64_t>(it.req) << 20) | static_cast<uint64_t>(p.layer)) ^ p.seed_q);
+    uint64_t sum = 0;
+    for (int c0 = 0; c0 < p.words; c0 += kAttWords) {
+      const int cw = min(kAttWords, p.words - c0);  // a multiple of 4 (b % 16 == 0)
+      const int half = cw / 2;
+      __syncthreads();  // the previous chunk's readers are done with qs / ks
+      for (int e = tid; e < kAttRows * half; e += kThreads) {
+        const int r = e / half, k = e - (e / half) * half;
+        uint64_t v = 0;
+        if (r < nq) {
+          const uint64_t qpos = static_cast<uint64_t>(it.q_begin + q0 + r);
+          v = splitmix64(qbase ^ ((qpos << 16) | static_cast<uint64_t>(c0 / 2 + k)));
+        }
+        *reinterpret_cast<uint64_t*>(qs + r * kAttStride + 2 * k) = v;
+      }
+      const int vec = cw / 4;
+      for (int64_t kt = kt0; kt < kt1; ++kt) {
+        if (kt > kt0) __syncthreads();  // the previous key tile's readers are done
+        for (int e = tid; e < kAttRows * vec; e += kThreads) {
+          const int r = e / vec, v4 = e - (e / vec) * vec;
+          const int64_t t = kt * kAttRows + r;
+          uint4 val = make_uint4(0, 0, 0, 0);
+          if (t < it.cached) {
+            const int64_t blk = t / p.block_tokens;
+            const char* row = p.pool + p.layer_off + static_cast<int64_t>(it.slot[blk]) * p.lb_bytes +
+                              (t - blk * p.block_tokens) * p.bpt + static_cast<int64_t>(c0) * 4;
+            val = reinterpret_cast<const uint4*>(row)[v4];
+          }
+          *reinterpret_cast<uint4*>(ks + r * kAttStride + v4 * 4) = val;
+        }
+        __syncthreads();
+        uint32_t acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = 0;
+#pragma unroll 1
+        for (int k = 0; k < cw; k += 4) {
+          uint4 qa[4], kb[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) qa[a] = *reinterpret_cast<const uint4*>(qs + (tq + 16 * a) * kAttStride + k);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) kb[b] = *reinterpret_cast<const uint4*>(ks + (tt + 16 * b) * kAttStride + k);
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              acc[a][b] = __dp4a(qa[a].x, kb[b].x, acc[a][b]);
+              acc[a][b] = __dp4a(qa[a].y, kb[b].y, acc[a][b]);
+              acc[a][b] = __dp4a(qa[a].z, kb[b].z, acc[a][b]);
+              acc[a][b] = __dp4a(qa[a].w, kb[b].w, acc[a][b]);
+            }
+        }
+        // each acc <= 144 * 4 * 255^2 < 2^26, so the 16 fit a 32-bit sum
+        uint32_t s32 = 0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) s32 += acc[a][b];
+        sum += s32;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+    if ((tid & 31) == 0) red[tid >> 5] = sum;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t all = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) all += red[w];
+      atomicAdd(reinterpret_cast<unsigned long long*>(it.digest + p.layer),
+                static_cast<unsigned long long>(all));
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int dp_set_attend_ctas(int device, int32_t ctas) {
+  if (device < 0 || device >= kMaxDevices || ctas < 0) return fail(DP_EINVAL, "set_attend_ctas: bad argument");
+  g_attend_ctas[device] = ctas;
+  return DP_OK;
+}
+
+int dp_prefill_attend(const dp_pool* pool, int32_t layer, const dp_attend_item* items, int32_t n_items,
+                      uint64_t seed, dp_stream stream) {
+  if (!pool || (n_items > 0 && !items) || n_items < 0) return fail(DP_EINVAL, "prefill_attend: null argument");
+  if (!pool->owner) return fail(DP_EINVAL, "prefill_attend: the PE pool must be local");
+  const dp_kv_geom& g = pool->geom;
+  if (layer < 0 || layer >= g.n_layer || layer >= (1 << 20))
+    return fail(DP_EINVAL, "prefill_attend: layer out of range");
+  if (g.bytes_per_token_layer >= (int64_t{1} << 19))
+    return fail(DP_EINVAL, "prefill_attend: b must be < 512 KiB (query word index is 16-bit)");
+  if (pool->device >= kMaxDevices) return fail(DP_EINVAL, "prefill_attend: device id too large");
+  DeviceGuard guard(pool->device);
+  {
+    std::lock_guard<std::mutex> lk(g_attend_mu);
+    if (!g_attend_init[pool->device]) {
+      DP_CUDA(cudaFuncSetAttribute(kv_prefill_attend, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem));
+      g_attend_init[pool->device] = true;
+    }
+  }
+  AttendParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.pool = pool->base;
+  p.bpt = g.bytes_per_token_layer;
+  p.lb_bytes = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
+  p.layer_off = static_cast<int64_t>(layer) * pool->n_slots * p.lb_bytes;
+  p.seed_q = seed * kQueryMul;
+  p.layer = layer;
+  p.block_tokens = g.block_tokens;
+  p.words = static_cast<int32_t>(g.bytes_per_token_layer / 4);
+  const int cap = g_attend_ctas[pool->device];
+  const int grid_cap = cap > 0 ? cap : sm_count(pool->device) * 2;
+  const int64_t max_tokens = static_cast<int64_t>(pool->n_slots) * g.block_tokens;
+  auto s = static_cast<cudaStream_t>(stream);
+  for (int32_t i0 = 0; i0 < n_items; i0 += DP_MAX_ATTEND_ITEMS_PER_LAUNCH) {
+    const int32_t ni = std::min<int32_t>(DP_MAX_ATTEND_ITEMS_PER_LAUNCH, n_items - i0);
+    p.n_jobs = 0;
+    int64_t units = 0;
+    for (int32_t i = 0; i < ni; ++i) {
+      const dp_attend_item& it = items[i0 + i];
+      if (it.cached < 0 || it.bsz < 0 || it.q_begin < 0 || it.q_begin + it.bsz >= (int64_t{1} << 47) ||
+          it.cached > max_tokens || (it.cached > 0 && !it.slot) || (it.cached > 0 && it.bsz > 0 && !it.digest))
+        return fail(DP_EINVAL, "prefill_attend: item " + std::to_string(i0 + i) + " out of range");
+      const int64_t n_kt = (it.cached + kAttRows - 1) / kAttRows;
+      const int64_t n = (it.bsz + kAttRows - 1) / kAttRows * ((n_kt + kAttGroup - 1) / kAttGroup);
+      if (n == 0) continue;
+      p.jobs[p.n_jobs] = it;
+      p.item_begin[p.n_jobs] = units;
+      ++p.n_jobs;
+      units += n;
+    }
+    p.item_begin[p.n_jobs] = units;
+    if (units == 0) continue;
+    kv_prefill_attend<<<static_cast<int>(std::min<int64_t>(units, grid_cap)), kThreads, kAttSmem, s>>>(p);
+    DP_CUDA(cudaGetLastError());
+  }
+  return DP_OK;
+}
+
+}  // extern "C"

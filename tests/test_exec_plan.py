@@ -228,3 +228,132 @@ def test_persist_requires_handoff():
     opt.persist = True
     with pytest.raises(ValueError, match="handoff"):
         dp.build_exec_plan(cfg, trajs, planned, opt)
+
+
+# ---- prefill forwards -----------------------------------
+COST = (2e-10, 1e-9, 4e-7, 1e-5)
+
+
+def build_prefill(P, D, quota=2e-3, tight=False, count=10, turns=6, seed=8, cost=COST):
+    cfg = cluster(P, D)
+    trajs = dp.synthesize(max_len=20000, count=count, seed=seed, mean_turns=turns, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **SB)
+    opt = dp.ExecOptions()
+    opt.prefill = True
+    opt.compute_quota = quota
+    opt.prefill_cost = cost
+    xp0 = dp.build_exec_plan(cfg, trajs, planned, opt)
+    if tight:
+        opt.pool_slots = xp0.peak_slots
+        xp0 = dp.build_exec_plan(cfg, trajs, planned, opt)
+    return cfg, trajs, planned, xp0
+
+
+@pytest.mark.parametrize("P,D,tight,quota", [(1, 1, False, 2e-3), (2, 2, True, 2e-3), (1, 3, True, 5e-4),
+                                             (2, 2, False, 0.3)])
+def test_prefill_forwards_cover_every_prompt(P, D, tight, quota):
+    cfg, trajs, planned, xp = build_prefill(P, D, quota=quota, tight=tight)
+    assert xp.prefill
+    reqs = {r[0]: r for r in planned["requests"]}
+    jobs = xp.jobs()
+    job_of = {j[0]: i for i, j in enumerate(jobs)}
+    for pe in range(xp.n_pe):
+        rows = xp.fwd_rows(pe)
+        # FIFO = the PE's requests in landing order (t_read_done, id)
+        want = sorted((r for r in planned["requests"] if r[6] == pe and r[12] >= 0),
+                      key=lambda r: (r[12], r[0]))
+        assert rows == [r[0] for r in want]
+        done = {rid: 0 for rid in rows}
+        fwds = xp.forwards(pe)
+        for fi, (est, items) in enumerate(fwds):
+            assert items, "empty forward"
+            rws = [it[5] for it in items]
+            assert rws == list(range(rws[0], rws[0] + len(rws))), "a forward is a FIFO range"
+            for req, job, cached, q0, bsz, row in items:
+                r = reqs[req]
+                assert rows[row] == req and cached == r[3]
+                assert q0 == done[req], "chunks run in order, without gaps"
+                done[req] += bsz
+                assert job == job_of.get(req, -1)
+            assert est <= quota or len(items) == 1
+            # the estimate is the cost model of exactly these chunks
+            assert est == dp.estimate_attention_time([(it[0], it[2], it[4]) for it in items], COST)
+        for rid in rows:
+            assert done[rid] == reqs[rid][4], "every append token runs exactly once"
+
+
+@pytest.mark.parametrize("P,D", [(1, 1), (2, 2), (1, 3)])
+def test_prefill_slot_reuse_waits_for_the_reader_forward(P, D):
+    cfg, trajs, planned, xp = build_prefill(P, D, tight=True, count=12, turns=8)
+    jobs = xp.jobs()
+    first_fwd = {}
+    for pe in range(xp.n_pe):
+        for fi, (_, items) in enumerate(xp.forwards(pe)):
+            for it in items:
+                if it[1] >= 0:
+                    first_fwd.setdefault(it[1], fi)
+                    assert xp.last_fwd(it[1]) >= fi
+    n_waits = 0
+    for i, j in enumerate(jobs):
+        for w in xp.consumer_waits(i):
+            n_waits += 1
+            assert w < i and jobs[w][4] == j[4]
+            # the forward that reads w last runs before this job is first read
+            assert xp.last_fwd(w) < first_fwd[i]
+        # prefill mode replaces the same-reader fence; DE loads wait on the
+        # PE's consumed rows (ticket + n_tickets, target 1)
+        assert not j[12]
+        if j[3] != j[4]:
+            assert j[11] == [jobs[w][8] + xp.n_tickets[j[4]] for w in xp.consumer_waits(i)]
+    assert n_waits > 0, "the tight pool should force slot reuse"
+
+
+@pytest.mark.skipif(not __import__("oracle.refpy", fromlist=["x"]).ref_available(),
+                    reason="oracle/_ref not built")
+def test_prefill_forwards_are_reference_build_forward_batch():
+    """Each forward is the reference's build_forward_batch over the FIFO
+    window that starts at the head chunk and stops before the first request
+    reusing a slot of a request in the window (restated here)."""
+    from oracle import refpy
+    cfg, trajs, planned, xp = build_prefill(2, 2, tight=True, count=12, turns=8, quota=1e-3)
+    reqs = {r[0]: r for r in planned["requests"]}
+    jobs = xp.jobs()
+    for pe in range(xp.n_pe):
+        rows = xp.fwd_rows(pe)
+        job_of_row = {}
+        for _, items in xp.forwards(pe):
+            for it in items:
+                job_of_row[it[5]] = it[1]
+        row_of_job = {j: r for r, j in job_of_row.items() if j >= 0}
+        pred_row = [max([row_of_job[w] for w in xp.consumer_waits(job_of_row[r])], default=-1)
+                    if job_of_row.get(r, -1) >= 0 else -1 for r in range(len(rows))]
+        head, done = 0, 0
+        for est, items in xp.forwards(pe):
+            assert items[0][5] == head and items[0][3] == done
+            barrier = head + 1
+            while barrier < len(rows) and pred_row[barrier] < head:
+                barrier += 1
+            window = [(rows[i], reqs[rows[i]][3], reqs[rows[i]][4] - (done if i == head else 0))
+                      for i in range(head, barrier)]
+            got_items, chunked, _, cb, whole, t = refpy.ref_build_forward_batch(window, 1e-3, COST)
+            assert [(it[0], it[2], it[4]) for it in items] == got_items
+            assert est == t
+            if chunked:
+                done = done + cb if whole == 0 else cb
+            else:
+                done = 0
+            head += whole
+        assert head == len(rows)
+
+
+def test_prefill_excludes_handoff():
+    cfg = cluster(1, 1)
+    trajs = dp.synthesize(max_len=20000, count=4, seed=8, mean_turns=4, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **SB)
+    opt = dp.ExecOptions()
+    opt.prefill, opt.handoff = True, True
+    with pytest.raises(ValueError):
+        dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.handoff, opt.compute_quota = False, 0.0
+    with pytest.raises(ValueError):
+        dp.build_exec_plan(cfg, trajs, planned, opt)
