@@ -240,6 +240,8 @@ typedef struct dp_attend_item {
 
 #define DP_MAX_ATTEND_ITEMS_PER_LAUNCH 48
 
+/* K5 launches on one pool must be stream-ordered (they share the pool's
+ * work-queue counter). */
 int dp_prefill_attend(const dp_pool* pe_pool, int32_t layer, const dp_attend_item* items,
                       int32_t n_items, uint64_t seed, dp_stream stream);
 /* Cap on the CTAs of a K5 launch on `device` (0 = default: every SM). */

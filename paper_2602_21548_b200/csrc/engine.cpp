@@ -509,8 +509,10 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   if (x.prefill && is_pe()) upload_prefill_tables();
   // K1 is PCIe-bound and keeps its rate down to ~32 CTAs; on a PE that also
   // runs K3 the remaining SMs go to the handoff
-  const std::int32_t ctas =
-      x.opt.gather_ctas >= 0 ? x.opt.gather_ctas : ((x.handoff || x.prefill) && is_pe() ? 64 : 0);
+  // (and on a prefill PE, 32 CTAs keep 51 GB/s while costing K5 the least:
+  // tools/prefill_interference.py)
+  std::int32_t ctas = x.opt.gather_ctas;
+  if (ctas < 0) ctas = !is_pe() ? 0 : x.prefill ? 32 : x.handoff ? 64 : 0;
   check(dp_set_gather_ctas(device_, ctas), "dp_set_gather_ctas");
   if (is_pe()) check(dp_set_handoff_ctas(device_, x.opt.handoff_ctas), "dp_set_handoff_ctas");
   if (is_pe() && x.prefill) check(dp_set_attend_ctas(device_, x.opt.attend_ctas), "dp_set_attend_ctas");
@@ -828,10 +830,10 @@ StepResult EngineRuntime::run_step() {
 // Prefill step of a PE.  The load stream runs this PE's own reads (K1) in
 // FIFO order; the compute stream runs the forwards, layer by layer: a wait
 // on the landed counters of the requests the forward reads first, then K5.
-// Both are enqueued in FIFO order (a forward right after its last request's
-// load), so every wait is enqueued after its producer.  A load that reuses
-// slots waits for the event of the forward that last read them; DE loads
-// wait on the "consumed" rows the compute stream writes after that forward.
+// A forward is enqueued after the loads of its requests, so every wait is
+// enqueued after its producer.  A load that reuses slots waits for the event
+// of the forward that last read them; DE loads wait on the "consumed" rows
+// the compute stream writes after that forward.
 StepResult EngineRuntime::run_step_prefill(bool loads) {
   const ExecPlan& x = *plan_;
   DeviceScope ds(device_);
@@ -869,34 +871,41 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
                                                             : x.opt.storage_cap_per_engine[engine_];
     const double pace = x.opt.pace_scale;
     double gate_s = 0;
-    for (std::size_t r = 0; r < rows.size(); ++r) {
-      const int ji = job_of_row[r];
-      if (ji >= 0 && x.jobs[ji].reader == engine_ && x.jobs[ji].n_blk > 0) {
-        const LoadJob& j = x.jobs[ji];
-        const std::int64_t bytes = j.cached * x.cfg.kv_bytes_per_token();
-        const bool gated = cap > 0 || pace > 0;
-        if (gated || !j.consumer_waits.empty() || batch.size() == DP_MAX_JOBS_PER_LAUNCH) flush();
-        for (int w : j.consumer_waits)
-          check_cuda(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[w]]), 0),
-                     "cudaStreamWaitEvent");
-        if (gated) {
-          const double begin = std::max(gate_s, pace > 0 ? j.t_admit * pace : 0.0);
-          gate_s = begin + (cap > 0 ? static_cast<double>(bytes) / cap : 0.0);
-          std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
-          res.spans.push_back({begin, gate_s, bytes});
-        }
-        if (k1_ce)
-          batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,
-                                 j.cached, j.n_blk, 0, L, j.ticket});
-        else
-          batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket});
-        res.bytes_read += bytes;
-        ++res.jobs;
-      }
-      while (fi < fwds.size() && fwds[fi].last_row <= static_cast<std::int32_t>(r)) {
+    // enqueue forwards whose requests' loads are all enqueued (row < r)
+    auto forwards_before = [&](std::size_t r) {
+      while (fi < fwds.size() && static_cast<std::size_t>(fwds[fi].last_row) < r) {
         flush();
         enqueue_forward(static_cast<int>(fi++), res);
       }
+    };
+    for (std::size_t r = 0; r < rows.size(); ++r) {
+      const int ji = job_of_row[r];
+      if (ji < 0 || x.jobs[ji].reader != engine_ || x.jobs[ji].n_blk == 0) continue;
+      const LoadJob& j = x.jobs[ji];
+      const std::int64_t bytes = j.cached * x.cfg.kv_bytes_per_token();
+      const bool gated = cap > 0 || pace > 0;
+      // loads run ahead of the forwards (the compute stream's queue may be
+      // long); they stop only for a slot reuse, whose reader forward must be
+      // enqueued first, and for the storage gate, which lets the forwards
+      // that are ready start before the host sleeps
+      if (gated || !j.consumer_waits.empty()) forwards_before(r);
+      if (gated || !j.consumer_waits.empty() || batch.size() == DP_MAX_JOBS_PER_LAUNCH) flush();
+      for (int w : j.consumer_waits)
+        check_cuda(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[w]]), 0),
+                   "cudaStreamWaitEvent");
+      if (gated) {
+        const double begin = std::max(gate_s, pace > 0 ? j.t_admit * pace : 0.0);
+        gate_s = begin + (cap > 0 ? static_cast<double>(bytes) / cap : 0.0);
+        std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
+        res.spans.push_back({begin, gate_s, bytes});
+      }
+      if (k1_ce)
+        batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,
+                               j.cached, j.n_blk, 0, L, j.ticket});
+      else
+        batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket});
+      res.bytes_read += bytes;
+      ++res.jobs;
     }
     flush();
   }

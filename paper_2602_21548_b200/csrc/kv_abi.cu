@@ -304,6 +304,7 @@ struct dp_pool {
   bool owner = false;
   bool ipc_opened = false;
   int* err_host = nullptr;  // mapped pinned watchdog flag
+  uint32_t* att_ctr = nullptr;  // K5 work-queue counters {next unit, CTAs done} (lazy)
 };
 
 namespace {
@@ -487,6 +488,7 @@ int dp_pool_destroy(dp_pool* pool) {
     if (pool->owner && pool->base) cudaFree(pool->base);
     if (pool->ipc_opened && pool->base) cudaIpcCloseMemHandle(pool->base);
     if (pool->err_host) cudaFreeHost(pool->err_host);
+    if (pool->att_ctr) cudaFree(pool->att_ctr);
   }
   delete pool;
   return DP_OK;
@@ -1328,6 +1330,7 @@ std::mutex g_attend_mu;
 
 struct AttendParams {
   const char* pool;
+  uint32_t* ctr;  // {next unit, CTAs done}: zero at launch, zeroed again by the last CTA
   int64_t bpt;
   int64_t lb_bytes;
   int64_t layer_off;  // layer * n_slots * lb_bytes
@@ -1355,8 +1358,16 @@ __global__ void __maxnreg__(96) kv_prefill_attend(const __grid_constant__ Attend
   uint32_t* ks = qs + kAttRows * kAttStride;
   const int tid = threadIdx.x;
   const int tq = tid >> 4, tt = tid & 15;
+  __shared__ int64_t fetched;
   const int64_t total = p.item_begin[p.n_jobs];
-  for (int64_t unit = blockIdx.x; unit < total; unit += gridDim.x) {
+  // units are handed out by an atomic counter: an SM slowed by a neighbour
+  // (a loader CTA) takes fewer, so no straggler holds the layer back
+  for (;;) {
+    __syncthreads();  // every thread has read the previous `fetched`
+    if (tid == 0) fetched = atomicAdd(p.ctr, 1u);
+    __syncthreads();
+    const int64_t unit = fetched;
+    if (unit >= total) break;
     const int j = decode_job(p, unit);
     const dp_attend_item& it = p.jobs[j];
     const int64_t local = unit - p.item_begin[j];
@@ -1441,6 +1452,10 @@ __global__ void __maxnreg__(96) kv_prefill_attend(const __grid_constant__ Attend
                 static_cast<unsigned long long>(all));
     }
   }
+  if (tid == 0 && atomicAdd(p.ctr + 1, 1u) == gridDim.x - 1) {  // the last CTA out resets
+    p.ctr[0] = 0;
+    p.ctr[1] = 0;
+  }
 }
 
 }  // namespace
@@ -1471,9 +1486,16 @@ int dp_prefill_attend(const dp_pool* pool, int32_t layer, const dp_attend_item* 
       g_attend_init[pool->device] = true;
     }
   }
+  if (!pool->att_ctr) {
+    uint32_t* c = nullptr;
+    DP_CUDA(cudaMalloc(&c, 2 * sizeof(uint32_t)));
+    DP_CUDA(cudaMemset(c, 0, 2 * sizeof(uint32_t)));
+    const_cast<dp_pool*>(pool)->att_ctr = c;
+  }
   AttendParams p;
   std::memset(&p, 0, sizeof(p));
   p.pool = pool->base;
+  p.ctr = pool->att_ctr;
   p.bpt = g.bytes_per_token_layer;
   p.lb_bytes = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
   p.layer_off = static_cast<int64_t>(layer) * pool->n_slots * p.lb_bytes;
