@@ -66,6 +66,10 @@ def parse():
                     help="prefill: compute quota per layer of a forward (ms of the cost model)")
     ap.add_argument("--attend-tops", type=float, default=40.0,
                     help="prefill: cost-model rate of K5 in tera multiply-adds/s (bilinear term)")
+    ap.add_argument("--tier", default="",
+                    help="storage tier: StorageRead reads every Full Block from this file (created "
+                         "and populated once per box; O_DIRECT) through a pinned staging ring")
+    ap.add_argument("--io-threads", type=int, default=8, help="storage tier: host IO threads per engine")
     ap.add_argument("--k1", default="sm", choices=["sm", "ce"],
                     help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs)")
     return ap.parse_args()
@@ -285,12 +289,43 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     opt.handoff_ctas = args.handoff_ctas
     opt.gather_ctas = args.gather_ctas
     opt.seed = 9
+    if args.tier:
+        opt.tier_path = args.tier
+        opt.io_threads = args.io_threads
     prefill = args.prefill if prefill is None else prefill
     if prefill:
         opt.prefill = True
         opt.compute_quota = args.quota_ms * 1e-3
         opt.prefill_cost = prefill_cost(args, shape)
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    tier = None
+    if args.tier:
+        # one file per box, written by local rank 0 (the same pages every
+        # policy reads); the others wait at the barrier
+        t0 = time.time()
+        if dist.local == 0:
+            need = xp.store_fb
+            ok = False
+            if os.path.exists(args.tier):
+                try:
+                    dp.FullBlockFile(args.tier, cfg.n_layer, cfg.block_size_tokens,
+                                     cfg.kv_bytes_per_token_per_layer, need)
+                    ok = True
+                except RuntimeError:
+                    ok = False
+            if not ok:
+                f = dp.FullBlockFile(args.tier, cfg.n_layer, cfg.block_size_tokens,
+                                     cfg.kv_bytes_per_token_per_layer, need, create=True)
+                f.populate(9, threads=os.cpu_count() or 8)
+                del f
+        dist.barrier()
+        f = dp.FullBlockFile(args.tier, cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer,
+                             xp.store_fb)
+        tier = dict(path=args.tier, direct=f.direct(), records=f.records(),
+                    file_gb=round(f.records() * f.stride() / 1e9, 2), ring_fb=xp.ring_fb,
+                    trie_nodes=xp.trie_nodes, io_threads=args.io_threads,
+                    open_or_populate_s=round(time.time() - t0, 2))
+        del f
     from paper_2602_21548_b200 import dist as dpdist
     digests = dist.allgather(dpdist.plan_digest(planned))
     assert len(set(digests)) == 1, "ranks planned differently"
@@ -305,6 +340,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     if dist.world > 1:
         dpdist.connect_pools(dist, engines, cfg.prefill_nodes)
     dev_ms, host_ms, launches, read_bytes, spans, per_engine = [], [], 0, 0, None, None
+    io_wait = 0.0
     for step in range(args.warmup + args.steps):
         for rt in engines.values():
             rt.reset_counters()
@@ -318,6 +354,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
             dev_ms.append(d)
             host_ms.append(h)
             launches += sum(dist.allgather(sum(r.launches for r in res)))
+            io_wait = max(io_wait, dist.max(max(r.io_wait_ms for r in res)))
             read_bytes += sum(dist.allgather(sum(r.bytes_read for r in res)))
             spans, per_engine = {}, {}
             for part in dist.allgather({e: (r.spans, r.device_ms) for e, r in zip(engines, res)}):
@@ -346,7 +383,8 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
                 decisions=len(planned["decisions"]), pool_slots=xp.pool_slots, spans=spans,
                 per_engine_ms=[per_engine[e] for e in sorted(per_engine)] if per_engine else None,
                 caps=caps,
-                store_fb=xp.store_fb, launches=launches, read_bytes=read_bytes, prefill=fwd)
+                store_fb=xp.store_fb, launches=launches, read_bytes=read_bytes, prefill=fwd,
+                tier=dict(tier, io_wait_ms_max_step=round(io_wait, 1)) if tier else None)
     if clocks is not None:
         clocks.__exit__()
     engines.clear()  # frees pools, stores and peer mappings before the next policy
@@ -611,6 +649,10 @@ def main():
                               "gbps": round(info["handoff_bytes"] * K / dev_s / 1e9, 3),
                               "what": "PeToDe/MissMerge per layer into DE decode pools (K3, NVLink) "
                                       "+ prefill stand-in; DE read path fused with DecodeH2D"}
+        if args.tier:
+            out["tier"] = dict(info["tier"], what="StorageRead = pread of Full Block records (trie lookup) "
+                                                  "into a pinned staging ring, then K1/K2")
+            out["config"]["storage"] = "file tier (" + ("O_DIRECT" if info["tier"]["direct"] else "buffered") + ")"
         if args.prefill:
             pf = info["prefill"]
             lo = results["load_only"]

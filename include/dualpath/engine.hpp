@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "dualpath/kv_abi.h"
+#include "dualpath/storage.hpp"
 #include "pdsim/desim.hpp"
 #include "pdsim/scheduler.hpp"
 #include "pdsim/types.hpp"
@@ -72,6 +73,15 @@ struct ExecOptions {
   double compute_quota = 2e-3;
   pdsim::AttentionCostModel prefill_cost{};
   std::int32_t attend_ctas = 0;        // K5 CTA cap (0 = default)
+  // Storage tier (the plain load path only): StorageRead
+  // becomes real file reads — every Full Block a job needs is looked up in
+  // the Full Block trie and read from `tier_path` (a FullBlockFile whose
+  // record r is page r) by `io_threads` host threads into a pinned staging
+  // ring, from which K1/K2 move its Layer Blocks.  Empty: procedural store.
+  std::string tier_path;
+  std::int32_t tier_ring_fb = 0;       // staging ring per reader, Full Blocks (0 = auto)
+  std::int32_t io_threads = 8;
+  bool tier_direct = true;             // O_DIRECT reads when the file system allows
 };
 
 // One request's hit-KV transfer (all layers), in global execution order.
@@ -112,6 +122,9 @@ struct LoadJob {
   std::vector<int> consumer_waits;  // jobs whose slots this one reuses: their last forward
                                     // must be done before this job's load writes
   std::int64_t fwd_off = 0;         // offset of its slots in the PE's forward slot table
+  // ---- storage tier ----
+  std::vector<int> ring_waits;      // jobs (same reader) whose staging positions this
+                                    // job's reads overwrite: their transfer must be done
 };
 
 // One request chunk of a forward batch (ExecOptions::prefill).
@@ -182,6 +195,12 @@ struct ExecPlan {
   std::vector<std::vector<int>> fwd_rows;        // per PE: request id of each digest row (FIFO)
   std::vector<std::vector<std::int32_t>> fwd_slot;  // per PE: slots of the jobs landing there
   std::vector<int> last_fwd;                     // per job: the forward (on its PE) that reads it last
+
+  // ---- storage tier ----
+  bool tier = false;
+  std::int32_t ring_fb = 0;                       // staging ring per reader (Full Blocks)
+  std::vector<std::vector<std::int64_t>> tier_rec;  // per reader: file record of each block
+  std::int64_t trie_nodes = 0;                    // Full Block trie size
 };
 
 // Builds the executor plan from planner output.  Requests with C = 0 move no
@@ -205,6 +224,7 @@ struct StepResult {
   std::int64_t launches = 0;    // kernels launched by this engine
   std::int64_t jobs = 0;
   std::int64_t forwards = 0;    // prefill forwards run (PE, ExecOptions::prefill)
+  double io_wait_ms = 0;        // storage tier: host time the launches waited for reads
 };
 
 class EngineRuntime {
@@ -294,6 +314,10 @@ class EngineRuntime {
   std::vector<std::vector<std::int32_t>> fwd_done_;   // PE: per forward, tickets read last there
   std::uint64_t* d_digest_ = nullptr;
   std::int32_t* d_fwd_slot_ = nullptr;
+  // ---- storage tier ----
+  std::unique_ptr<FullBlockFile> tier_file_;
+  std::vector<void*> ev_job_;               // per job in by_reader order: after its launch
+  std::vector<std::vector<int>> ring_wait_local_;  // ring_waits as by_reader positions
   // ---- persistence (DE) ----
   dp_store* persist_store_ = nullptr;
   std::int32_t* d_dec_slot_ = nullptr;

@@ -40,6 +40,8 @@ from ._core import (  # noqa: E402
     EngineRuntime,
     ExecOptions,
     ExecPlan,
+    FullBlockFile,
+    FullBlockTrie,
     Round,
     SimulationError,
     StepResult,
@@ -58,6 +60,7 @@ from ._core import (  # noqa: E402
     poisson_arrivals,
     run_step_all,
     save_trace,
+    session_chain,
     schedule_de_groups,
     schedule_de_within_group,
     schedule_pe_fetch,
@@ -75,6 +78,8 @@ __all__ = [
     "EngineRuntime",
     "ExecOptions",
     "ExecPlan",
+    "FullBlockFile",
+    "FullBlockTrie",
     "LIBDUALPATH",
     "Round",
     "SimulationError",
@@ -94,6 +99,7 @@ __all__ = [
     "poisson_arrivals",
     "run_step_all",
     "save_trace",
+    "session_chain",
     "schedule_de_groups",
     "schedule_de_within_group",
     "schedule_pe_fetch",

@@ -370,6 +370,39 @@ PYBIND11_MODULE(_core, m) {
   py::register_exception<desim::SimulationError>(m, "SimulationError");
 
   // ---------------------------------------------------------------- executor
+  // ---- storage tier (dualpath/storage.hpp) ----
+  auto geom_of = [](int L, int T, std::int64_t b) { return dp_kv_geom{L, T, b}; };
+  m.def("session_chain", &dualpath::session_chain, py::arg("id"), py::arg("n_blocks"));
+  py::class_<dualpath::FullBlockTrie>(m, "FullBlockTrie")
+      .def(py::init<>())
+      .def("insert",
+           [](dualpath::FullBlockTrie& t, const std::vector<std::uint64_t>& chain,
+              const std::vector<std::int64_t>& records) { return t.insert(chain, records); })
+      .def("match", [](const dualpath::FullBlockTrie& t,
+                       const std::vector<std::uint64_t>& chain) { return t.match(chain); })
+      .def("nodes", &dualpath::FullBlockTrie::nodes)
+      .def("save", &dualpath::FullBlockTrie::save)
+      .def_static("load", &dualpath::FullBlockTrie::load);
+  py::class_<dualpath::FullBlockFile>(m, "FullBlockFile")
+      .def(py::init([=](const std::string& path, int L, int T, std::int64_t b, std::int64_t n_records,
+                        bool create, bool direct) {
+             return std::make_unique<dualpath::FullBlockFile>(path, geom_of(L, T, b), n_records, create, direct);
+           }),
+           py::arg("path"), py::arg("n_layer"), py::arg("block_tokens"), py::arg("bytes_per_token_layer"),
+           py::arg("n_records"), py::arg("create") = false, py::arg("direct") = true)
+      .def("populate", &dualpath::FullBlockFile::populate, py::arg("seed"), py::arg("threads") = 8,
+           py::call_guard<py::gil_scoped_release>())
+      .def("read",
+           [](const dualpath::FullBlockFile& f, std::int64_t record) {
+             std::string buf(static_cast<std::size_t>(f.record_bytes()), '\0');
+             f.read(record, buf.data());
+             return py::bytes(buf);
+           })
+      .def("records", &dualpath::FullBlockFile::records)
+      .def("record_bytes", &dualpath::FullBlockFile::record_bytes)
+      .def("stride", &dualpath::FullBlockFile::stride)
+      .def("direct", &dualpath::FullBlockFile::direct);
+
   py::class_<dualpath::ExecOptions>(m, "ExecOptions")
       .def(py::init<>())
       .def_readwrite("storage_cap_Bps", &dualpath::ExecOptions::storage_cap_Bps)
@@ -388,6 +421,10 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("pool_slots", &dualpath::ExecOptions::pool_slots)
       .def_readwrite("pool_bytes_max", &dualpath::ExecOptions::pool_bytes_max)
       .def_readwrite("wait_timeout_ms", &dualpath::ExecOptions::wait_timeout_ms)
+      .def_readwrite("tier_path", &dualpath::ExecOptions::tier_path)
+      .def_readwrite("tier_ring_fb", &dualpath::ExecOptions::tier_ring_fb)
+      .def_readwrite("io_threads", &dualpath::ExecOptions::io_threads)
+      .def_readwrite("tier_direct", &dualpath::ExecOptions::tier_direct)
       .def_readwrite("prefill", &dualpath::ExecOptions::prefill)
       .def_readwrite("compute_quota", &dualpath::ExecOptions::compute_quota)
       .def_readwrite("attend_ctas", &dualpath::ExecOptions::attend_ctas)
@@ -454,6 +491,12 @@ PYBIND11_MODULE(_core, m) {
       .def("by_pe", [](const dualpath::ExecPlan& x, int e) { return x.by_pe.at(e); })
       .def("by_de", [](const dualpath::ExecPlan& x, int e) { return x.by_de.at(e); })
       .def_readonly("prefill", &dualpath::ExecPlan::prefill)
+      .def_readonly("tier", &dualpath::ExecPlan::tier)
+      .def_readonly("ring_fb", &dualpath::ExecPlan::ring_fb)
+      .def_readonly("trie_nodes", &dualpath::ExecPlan::trie_nodes)
+      .def("tier_rec", [](const dualpath::ExecPlan& x, int e) { return x.tier_rec.at(e); })
+      .def("src_fb", [](const dualpath::ExecPlan& x, int e) { return x.src_fb.at(e); })
+      .def("ring_waits", [](const dualpath::ExecPlan& x, int job) { return x.jobs.at(job).ring_waits; })
       // forwards(pe) -> [(estimated_time, [(req, job, cached, q_begin, bsz, row)])]
       .def("forwards",
            [](const dualpath::ExecPlan& x, int pe) {
@@ -515,7 +558,8 @@ PYBIND11_MODULE(_core, m) {
       .def_readonly("bytes_read", &dualpath::StepResult::bytes_read)
       .def_readonly("launches", &dualpath::StepResult::launches)
       .def_readonly("jobs", &dualpath::StepResult::jobs)
-      .def_readonly("forwards", &dualpath::StepResult::forwards);
+      .def_readonly("forwards", &dualpath::StepResult::forwards)
+      .def_readonly("io_wait_ms", &dualpath::StepResult::io_wait_ms);
 
   py::class_<dualpath::EngineRuntime>(m, "EngineRuntime")
       .def(py::init([](std::shared_ptr<dualpath::ExecPlan> plan, int engine, int device) {

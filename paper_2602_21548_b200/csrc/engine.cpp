@@ -4,8 +4,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <deque>
+#include <mutex>
 #include <stdexcept>
 #include <thread>
 
@@ -197,6 +200,52 @@ void build_forwards(ExecPlan& x, const pdsim::desim::SimReport& plan) {
   }
 }
 
+// Storage tier tables.  The Full Block trie indexes every session's chain of
+// Full Blocks (record = the page the procedural store holds for it, so the
+// bytes are the same); a job's blocks are the records its session's chain
+// matches.  Each reader stages them in a FIFO ring of pinned Full Blocks:
+// src_fb becomes ring positions, and a job whose reads overwrite positions
+// of earlier jobs waits for their transfers.
+void build_tier(ExecPlan& x, std::span<const pdsim::Trajectory> trajectories) {
+  FullBlockTrie trie;
+  std::vector<std::vector<std::uint64_t>> chains(trajectories.size());
+  for (std::size_t t = 0; t < trajectories.size(); ++t) {
+    const std::int64_t nb = pdsim::blocks_for(trajectories[t].total_tokens(), x.cfg);
+    chains[t] = session_chain(trajectories[t].id, nb);
+    std::vector<std::int64_t> rec(static_cast<std::size_t>(nb));
+    for (std::int64_t k = 0; k < nb; ++k) rec[k] = x.fb_of(static_cast<int>(t), k);
+    trie.insert(chains[t], rec);
+  }
+  x.trie_nodes = trie.nodes();
+  std::int32_t biggest = 1;
+  for (const LoadJob& j : x.jobs) biggest = std::max(biggest, j.n_blk);
+  std::int64_t ring = x.opt.tier_ring_fb > 0 ? x.opt.tier_ring_fb : std::max<std::int64_t>(4LL * biggest, 512);
+  if (ring < biggest)
+    throw std::invalid_argument("build_exec_plan: tier_ring_fb of " + std::to_string(ring) +
+                                " is below the largest job (" + std::to_string(biggest) + " Full Blocks)");
+  x.ring_fb = static_cast<std::int32_t>(ring);
+  x.tier_rec.assign(x.n_engines, {});
+  for (int e = 0; e < x.n_engines; ++e) {
+    std::vector<int> owner(static_cast<std::size_t>(ring), -1);
+    std::int64_t head = 0;
+    for (int ji : x.by_reader[e]) {
+      LoadJob& j = x.jobs[ji];
+      const auto recs = trie.match(std::span<const std::uint64_t>(chains[j.traj]).first(j.n_blk));
+      if (static_cast<std::int32_t>(recs.size()) != j.n_blk)
+        throw std::logic_error("build_exec_plan: trie lookup missed a session block");
+      for (std::int32_t k = 0; k < j.n_blk; ++k) {
+        const std::int64_t pos = (head + k) % ring;
+        if (owner[pos] >= 0 && std::find(j.ring_waits.begin(), j.ring_waits.end(), owner[pos]) == j.ring_waits.end())
+          j.ring_waits.push_back(owner[pos]);
+        owner[pos] = ji;
+        x.src_fb[e][j.blk_off + k] = pos;
+        x.tier_rec[e].push_back(recs[k]);
+      }
+      head = (head + j.n_blk) % ring;
+    }
+  }
+}
+
 }  // namespace
 
 std::int64_t ExecPlan::fb_of(int traj, std::int64_t block) const {
@@ -237,6 +286,10 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     throw std::invalid_argument("build_exec_plan: prefill and handoff are separate modes");
   if (x.prefill && !(opt.compute_quota > 0))
     throw std::invalid_argument("build_exec_plan: compute_quota must be > 0");
+  x.tier = !opt.tier_path.empty();
+  if (x.tier && (x.handoff || x.prefill))
+    throw std::invalid_argument("build_exec_plan: the storage tier runs on the plain load path");
+  if (x.tier && opt.io_threads < 1) throw std::invalid_argument("build_exec_plan: io_threads must be >= 1");
   x.n_engines = cfg.total_engines();
   x.n_pe = cfg.prefill_nodes * cfg.engines_per_node;
   x.geom = {cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer};
@@ -464,6 +517,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     x.jobs.push_back(std::move(j));
   }
   if (x.prefill) build_forwards(x, plan);
+  if (x.tier) build_tier(x, trajectories);
   return x;
 }
 
@@ -484,8 +538,25 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   ev_end_ = b;
   peers_.assign(x.n_engines, nullptr);
   de_views_.assign(x.n_engines, nullptr);
-  if (!x.by_reader[engine_].empty())
-    check(dp_store_create(device_, &x.geom, x.store_fb, x.opt.seed, &store_), "dp_store_create");
+  if (!x.by_reader[engine_].empty()) {
+    // with the storage tier the store is the pinned staging ring the reads land in
+    check(dp_store_create(device_, &x.geom, x.tier ? x.ring_fb : x.store_fb, x.opt.seed, &store_),
+          "dp_store_create");
+    if (x.tier) {
+      tier_file_ = std::make_unique<FullBlockFile>(x.opt.tier_path, x.geom, x.store_fb, false, x.opt.tier_direct);
+      const auto& mine = x.by_reader[engine_];
+      std::vector<int> local(x.jobs.size(), -1);
+      for (std::size_t i = 0; i < mine.size(); ++i) local[mine[i]] = static_cast<int>(i);
+      for (int ji : mine) {
+        cudaEvent_t e;
+        check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        ev_job_.push_back(e);
+        std::vector<int> w;
+        for (int p : x.jobs[ji].ring_waits) w.push_back(local[p]);
+        ring_wait_local_.push_back(std::move(w));
+      }
+    }
+  }
   if (is_pe()) {
     // handoff: rows [0, n) hit-KV landed, rows [n, 2n) handoff (K3) done
     // handoff / prefill: rows [0, n) hit-KV landed, rows [n, 2n) handoff done / consumed
@@ -598,6 +669,7 @@ EngineRuntime::~EngineRuntime() {
   for (void* e : ev_load_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* e : ev_k3_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* e : ev_fwd_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  for (void* e : ev_job_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   if (ev_start_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_start_));
   if (ev_end_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_end_));
   if (stream_h_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_h_));
@@ -744,8 +816,72 @@ StepResult EngineRuntime::run_step() {
   const auto& mine = x.by_reader[engine_];
   std::vector<dp_job> batch;
   batch.reserve(DP_MAX_JOBS_PER_LAUNCH);
+  std::vector<int> batch_jobs;  // by_reader positions of the jobs in `batch`
   int batch_pe = -1;
   const bool k1_ce = x.opt.k1_mode == 1;
+
+  // Storage tier: IO threads read each job's Full Blocks from the file into
+  // its staging-ring positions, in job order (first reusing a position only
+  // after the transfer that read it is done); a job is launched once read.
+  struct Io {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<char> read, launched;
+    std::atomic<int> next{0};
+    bool failed = false;
+    std::exception_ptr err;
+  } io;
+  std::vector<std::thread> workers;
+  char* staging = nullptr;
+  if (x.tier && !mine.empty()) {
+    void* host = nullptr;
+    check(dp_store_info(store_, &host, nullptr, nullptr), "dp_store_info");
+    staging = static_cast<char*>(host);
+    io.read.assign(mine.size(), 0);
+    io.launched.assign(mine.size(), 0);
+    const std::int64_t fbb = x.cfg.full_block_bytes();
+    const int dev = device_;
+    for (int t = 0; t < x.opt.io_threads; ++t)
+      workers.emplace_back([&, fbb, dev] {
+        try {
+          cudaSetDevice(dev);
+          for (int i = io.next++; i < static_cast<int>(mine.size()); i = io.next++) {
+            for (int w : ring_wait_local_[i]) {
+              {
+                std::unique_lock<std::mutex> lk(io.mu);
+                io.cv.wait(lk, [&] { return io.launched[w] || io.failed; });
+                if (io.failed) return;
+              }
+              check_cuda(cudaEventSynchronize(static_cast<cudaEvent_t>(ev_job_[w])), "ring reuse wait");
+            }
+            const LoadJob& j = x.jobs[mine[i]];
+            for (std::int32_t k = 0; k < j.n_blk; ++k)
+              tier_file_->read(x.tier_rec[engine_][j.blk_off + k], staging + x.src_fb[engine_][j.blk_off + k] * fbb);
+            std::lock_guard<std::mutex> lk(io.mu);
+            io.read[i] = 1;
+            io.cv.notify_all();
+          }
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(io.mu);
+          if (!io.err) io.err = std::current_exception();
+          io.failed = true;
+          io.cv.notify_all();
+        }
+      });
+  }
+  struct JoinWorkers {
+    Io& io;
+    std::vector<std::thread>& w;
+    ~JoinWorkers() {
+      {
+        std::lock_guard<std::mutex> lk(io.mu);
+        io.failed = true;  // releases any worker still waiting (normal exit: all done)
+        io.cv.notify_all();
+      }
+      for (auto& t : w) t.join();
+    }
+  } join_workers{io, workers};
+
   auto flush = [&]() {
     if (batch.empty()) return;
     dp_pool* dst = peers_[batch_pe];
@@ -767,6 +903,13 @@ StepResult EngineRuntime::run_step() {
       res.launches += (static_cast<std::int64_t>(batch.size()) + DP_MAX_JOBS_PER_LAUNCH - 1) /
                       DP_MAX_JOBS_PER_LAUNCH;
     batch.clear();
+    if (staging) {
+      for (int i : batch_jobs) check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_job_[i]), s), "cudaEventRecord");
+      std::lock_guard<std::mutex> lk(io.mu);
+      for (int i : batch_jobs) io.launched[i] = 1;
+      io.cv.notify_all();
+    }
+    batch_jobs.clear();
   };
   const double cap = x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
                                                           : x.opt.storage_cap_per_engine[engine_];
@@ -789,6 +932,21 @@ StepResult EngineRuntime::run_step() {
       std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
       res.spans.push_back({begin, gate_s, bytes});
     }
+    if (staging) {  // StorageRead: the job's Full Blocks must be in staging
+      bool ready;
+      {
+        std::lock_guard<std::mutex> lk(io.mu);
+        ready = io.read[i] || io.failed;
+      }
+      if (!ready) {
+        flush();  // never hold launched work while waiting on the disk
+        const auto w0 = std::chrono::steady_clock::now();
+        std::unique_lock<std::mutex> lk(io.mu);
+        io.cv.wait(lk, [&] { return io.read[i] || io.failed; });
+        res.io_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+      }
+      if (io.err) std::rethrow_exception(io.err);
+    }
     if (hazard) {
       const std::int64_t off = pred_off_[i];
       check(dp_wait_tickets(peers_[j.pe], d_pred_tickets_ + off, d_pred_targets_ + off,
@@ -804,6 +962,7 @@ StepResult EngineRuntime::run_step() {
     else
       batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0,
                              x.cfg.n_layer, j.ticket});
+    batch_jobs.push_back(static_cast<int>(i));
     res.bytes_read += bytes;
     ++res.jobs;
   }
