@@ -87,6 +87,9 @@ class FullBlockFile {
   // Reads one record into dst (O_DIRECT when dst is 4 KiB aligned and the
   // file was opened direct; buffered otherwise).  Throws on a short read.
   void read(std::int64_t record, void* dst) const;
+  // Reads records [record, record + n) into n consecutive Full Blocks at dst:
+  // one pread when records are packed (stride == record bytes), else n.
+  void read_run(std::int64_t record, std::int64_t n, void* dst) const;
 
  private:
   std::string path_;

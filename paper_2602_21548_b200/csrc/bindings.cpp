@@ -398,6 +398,12 @@ PYBIND11_MODULE(_core, m) {
              f.read(record, buf.data());
              return py::bytes(buf);
            })
+      .def("read_run",
+           [](const dualpath::FullBlockFile& f, std::int64_t record, std::int64_t n) {
+             std::string buf(static_cast<std::size_t>(f.record_bytes() * std::max<std::int64_t>(0, n)), '\0');
+             f.read_run(record, n, buf.data());
+             return py::bytes(buf);
+           })
       .def("records", &dualpath::FullBlockFile::records)
       .def("record_bytes", &dualpath::FullBlockFile::record_bytes)
       .def("stride", &dualpath::FullBlockFile::stride)

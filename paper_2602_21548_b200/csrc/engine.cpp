@@ -854,9 +854,19 @@ StepResult EngineRuntime::run_step() {
               }
               check_cuda(cudaEventSynchronize(static_cast<cudaEvent_t>(ev_job_[w])), "ring reuse wait");
             }
+            // one read per run of blocks consecutive both in the file and in
+            // the ring (a session's pages are consecutive records)
             const LoadJob& j = x.jobs[mine[i]];
-            for (std::int32_t k = 0; k < j.n_blk; ++k)
-              tier_file_->read(x.tier_rec[engine_][j.blk_off + k], staging + x.src_fb[engine_][j.blk_off + k] * fbb);
+            const std::int64_t* rec = x.tier_rec[engine_].data() + j.blk_off;
+            const std::int64_t* pos = x.src_fb[engine_].data() + j.blk_off;
+            constexpr std::int32_t kMaxRun = 8;  // 18 MB of DS-V3 Full Blocks per read
+            for (std::int32_t k = 0; k < j.n_blk;) {
+              std::int32_t run = 1;
+              while (k + run < j.n_blk && run < kMaxRun && rec[k + run] == rec[k] + run && pos[k + run] == pos[k] + run)
+                ++run;
+              tier_file_->read_run(rec[k], run, staging + pos[k] * fbb);
+              k += run;
+            }
             std::lock_guard<std::mutex> lk(io.mu);
             io.read[i] = 1;
             io.cv.notify_all();

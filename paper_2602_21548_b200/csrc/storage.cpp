@@ -179,6 +179,25 @@ void FullBlockFile::read(std::int64_t record, void* dst) const {
   }
 }
 
+void FullBlockFile::read_run(std::int64_t record, std::int64_t n, void* dst) const {
+  if (n < 1) return;
+  if (record < 0 || record + n > n_records_) throw std::out_of_range("FullBlockFile::read_run: records out of range");
+  char* p = static_cast<char*>(dst);
+  if (stride_ != record_bytes_) {
+    for (std::int64_t i = 0; i < n; ++i) read(record + i, p + i * record_bytes_);
+    return;
+  }
+  const bool aligned = (reinterpret_cast<std::uintptr_t>(dst) % kAlign) == 0;
+  const int fd = (fd_direct_ >= 0 && aligned) ? fd_direct_ : fd_;
+  const std::int64_t total = n * record_bytes_;
+  std::int64_t done = 0;
+  while (done < total) {
+    const ssize_t got = ::pread(fd, p + done, total - done, record * stride_ + done);
+    if (got <= 0) io_error("short read from", path_);
+    done += got;
+  }
+}
+
 void FullBlockFile::populate(std::uint64_t seed, int threads) {
   threads = std::max(1, threads);
   std::vector<std::thread> pool;

@@ -68,6 +68,10 @@ def test_full_block_file_records_match_the_oracle(tmp_path, L, T, b):
     assert os.path.getsize(p) == n * f.stride()
     with pytest.raises(IndexError):
         f.read(n)
+    # runs of consecutive records: one read when records are packed
+    assert f.read_run(1, 4) == b"".join(f.read(r) for r in range(1, 5))
+    with pytest.raises(IndexError):
+        f.read_run(n - 2, 3)
     # reopen read-only; asking for more records than the file holds fails
     assert dp.FullBlockFile(p, L, T, b, n).read(2) == f.read(2)
     with pytest.raises(RuntimeError):
