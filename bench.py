@@ -207,6 +207,32 @@ def measure_pcie_peak(device):
     return n / (best * 1e-3)
 
 
+def measure_concurrent_h2d(dist, device, reps=3):
+    """Every rank at once: copy-engine H2D of 1 GiB pinned, after a barrier.
+    The box's aggregate host-link ceiling for an N-GPU line (PCIe switches may
+    be shared between GPUs, so N x the single-GPU peak can overstate it)."""
+    import torch
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+    s = torch.cuda.Stream(device=device)
+    best = 0.0
+    for _ in range(reps):
+        dist.barrier()
+        with torch.cuda.stream(s):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for _ in range(4):
+                d.copy_(h, non_blocking=True)
+            b.record(s)
+            b.synchronize()
+        ms = dist.max(a.elapsed_time(b))  # the slowest rank bounds the aggregate
+        best = max(best, dist.world * 4 * n / (ms * 1e-3))
+    del h, d
+    return best
+
+
 def measure_k1(device, shape, target_bytes=18421383168):
     """The dominant kernel alone, live: one K1 launch (DS-V3 or Qwen Layer
     Blocks, 8K-token requests, random Full Blocks and slots) through the C
@@ -579,6 +605,9 @@ def main():
         except Exception as exc:  # reported, never fatal to the GPU number
             cpu = {"error": str(exc)[:200]}
     clk = clocks.summary(set(range(n)))
+    concurrent = None
+    if dist.world > 1:
+        concurrent = measure_concurrent_h2d(dist, dist.local)
     k1 = None
     if dist.rank == 0:
         k1 = measure_k1(dist.local if dist.world > 1 else 0, shape)
@@ -626,6 +655,10 @@ def main():
                          "step_rate_per_engine": round(value / max(1, n), 2)},
             "cpu_baseline": cpu,
             "clocks": clk,
+            "host_links": ({"concurrent_h2d_gbps": round(concurrent / 1e9, 2),
+                            "value_frac": round(value / (concurrent / 1e9), 4),
+                            "what": "all ranks' copy-engine H2D at once: the box's aggregate host-link "
+                                    "ceiling for this line"} if concurrent else None),
             "plan_s": round(info["plan_s"], 2),
         }
         if args.online > 0:
