@@ -367,6 +367,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
         dpdist.connect_pools(dist, engines, cfg.prefill_nodes)
     dev_ms, host_ms, launches, read_bytes, spans, per_engine = [], [], 0, 0, None, None
     io_wait = 0.0
+    d2h = 0
     for step in range(args.warmup + args.steps):
         for rt in engines.values():
             rt.reset_counters()
@@ -381,6 +382,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
             host_ms.append(h)
             launches += sum(dist.allgather(sum(r.launches for r in res)))
             io_wait = max(io_wait, dist.max(max(r.io_wait_ms for r in res)))
+            d2h = sum(dist.allgather(sum(r.d2h_bytes for r in res)))  # per step (the same each step)
             read_bytes += sum(dist.allgather(sum(r.bytes_read for r in res)))
             spans, per_engine = {}, {}
             for part in dist.allgather({e: (r.spans, r.device_ms) for e, r in zip(engines, res)}):
@@ -409,7 +411,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
                 decisions=len(planned["decisions"]), pool_slots=xp.pool_slots, spans=spans,
                 per_engine_ms=[per_engine[e] for e in sorted(per_engine)] if per_engine else None,
                 caps=caps,
-                store_fb=xp.store_fb, launches=launches, read_bytes=read_bytes, prefill=fwd,
+                store_fb=xp.store_fb, launches=launches, read_bytes=read_bytes, prefill=fwd, d2h=d2h,
                 tier=dict(tier, io_wait_ms_max_step=round(io_wait, 1)) if tier else None)
     if clocks is not None:
         clocks.__exit__()
@@ -643,7 +645,10 @@ def main():
             "tokens_per_s": round(tokens_s, 1),
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": info["hit_bytes"],
-                    "d2h_bytes_per_step": 8 * n + info["persist_bytes"]},
+                    "d2h_bytes_per_step": info["d2h"] + info["persist_bytes"],
+                    "what": "host wall time of run_step: storage read (pinned host) -> HBM inside, "
+                            "then the landed-counter column of every request read back and checked "
+                            "(+ K4's persisted tokens with --persist)"},
             "gpu_launches": info["launches"],
             "roofline": {"bound": "pcie", "achieved": round(achieved, 2),
                          "peak": round(peak / 1e9, 2) if peak else None, "unit": "GB/s",

@@ -225,6 +225,7 @@ struct StepResult {
   std::int64_t jobs = 0;
   std::int64_t forwards = 0;    // prefill forwards run (PE, ExecOptions::prefill)
   double io_wait_ms = 0;        // storage tier: host time the launches waited for reads
+  std::int64_t d2h_bytes = 0;   // result read back (PE: landed-counter column)
 };
 
 class EngineRuntime {
@@ -303,6 +304,8 @@ class EngineRuntime {
   std::vector<std::int64_t> pe_done_off_;   // per job: offset of its pe_done_preds
   std::int64_t final_wait_off_ = 0;         // DE: all own tickets (decode-ready gate)
   std::int32_t final_wait_n_ = 0;
+  void read_back_landed(StepResult& res);
+  std::vector<std::uint32_t> landed_host_;
   // ---- prefill ----
   StepResult run_step_prefill(bool loads);
   void enqueue_forward(int f, StepResult& res);

@@ -565,7 +565,8 @@ PYBIND11_MODULE(_core, m) {
       .def_readonly("launches", &dualpath::StepResult::launches)
       .def_readonly("jobs", &dualpath::StepResult::jobs)
       .def_readonly("forwards", &dualpath::StepResult::forwards)
-      .def_readonly("io_wait_ms", &dualpath::StepResult::io_wait_ms);
+      .def_readonly("io_wait_ms", &dualpath::StepResult::io_wait_ms)
+      .def_readonly("d2h_bytes", &dualpath::StepResult::d2h_bytes);
 
   py::class_<dualpath::EngineRuntime>(m, "EngineRuntime")
       .def(py::init([](std::shared_ptr<dualpath::ExecPlan> plan, int engine, int device) {

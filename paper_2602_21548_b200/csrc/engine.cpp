@@ -803,6 +803,35 @@ void EngineRuntime::reset_counters() {
   check_cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)), "reset sync");
 }
 
+// The step's result, read back to the host: on a PE, the all-layer column of
+// every hit-KV landed row (one 32-bit word per request), checked against the
+// plan -- the host-side proof that each request's KV is in the pool.
+void EngineRuntime::read_back_landed(StepResult& res) {
+  const ExecPlan& x = *plan_;
+  if (!is_pe() || !pool_) return;
+  const std::int32_t n = x.n_tickets[engine_];
+  if (n <= 0) return;
+  if (landed_host_.size() < static_cast<std::size_t>(n)) landed_host_.resize(n);
+  const std::size_t row = static_cast<std::size_t>(x.cfg.n_layer + 1) * sizeof(std::uint32_t);
+  void* base = nullptr;
+  std::uint32_t* ctr = nullptr;
+  std::int64_t bytes = 0;
+  check(dp_pool_info(pool_, &base, &ctr, &bytes), "dp_pool_info");
+  check_cuda(cudaMemcpy2D(landed_host_.data(), sizeof(std::uint32_t), ctr + x.cfg.n_layer, row,
+                          sizeof(std::uint32_t), n, cudaMemcpyDeviceToHost),
+             "landed counters D2H");
+  res.d2h_bytes += static_cast<std::int64_t>(n) * sizeof(std::uint32_t);
+  for (int ji : x.by_pe[engine_]) {
+    const LoadJob& j = x.jobs[ji];
+    const std::uint32_t want =
+        static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block * x.cfg.n_layer);
+    if (landed_host_[j.ticket] != want)
+      throw std::runtime_error("step incomplete: request " + std::to_string(j.req) + " landed " +
+                               std::to_string(landed_host_[j.ticket]) + " of " + std::to_string(want) +
+                               " items");
+  }
+}
+
 StepResult EngineRuntime::run_step() {
   const ExecPlan& x = *plan_;
   if (x.handoff) return run_step_handoff();
@@ -992,6 +1021,7 @@ StepResult EngineRuntime::run_step() {
                                   static_cast<cudaEvent_t>(ev_end_)),
              "cudaEventElapsedTime");
   res.device_ms = ms;
+  read_back_landed(res);
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return res;
 }
@@ -1088,6 +1118,7 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
   float ms = 0;
   check_cuda(cudaEventElapsedTime(&ms, start, end), "cudaEventElapsedTime");
   res.device_ms = ms;
+  read_back_landed(res);
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return res;
 }
@@ -1314,6 +1345,7 @@ StepResult EngineRuntime::run_step_handoff() {
   float ms = 0;
   check_cuda(cudaEventElapsedTime(&ms, start, static_cast<cudaEvent_t>(ev_end_)), "cudaEventElapsedTime");
   res.device_ms = ms;
+  read_back_landed(res);
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return res;
 }
