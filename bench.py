@@ -70,6 +70,8 @@ def parse():
                     help="storage tier: StorageRead reads every Full Block from this file (created "
                          "and populated once per box; O_DIRECT) through a pinned staging ring")
     ap.add_argument("--io-threads", type=int, default=8, help="storage tier: host IO threads per engine")
+    ap.add_argument("--k2", default="sm", choices=["sm", "ce"],
+                    help="DE-path loads: sm = K2 gather pushing over NVLink, ce = the DE's copy engine")
     ap.add_argument("--k1", default="sm", choices=["sm", "ce"],
                     help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs)")
     return ap.parse_args()
@@ -310,6 +312,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     if args.online > 0:
         opt.pace_scale = 1.0
     opt.k1_mode = 1 if args.k1 == "ce" else 0
+    opt.k2_mode = 1 if args.k2 == "ce" else 0
     opt.handoff = bool(args.handoff or args.persist)
     opt.persist = bool(args.persist)
     opt.handoff_ctas = args.handoff_ctas
@@ -635,7 +638,7 @@ def main():
             "config": {"workload": f"{args.workload}: {len(trajs)} sessions, "
                                    + ("1 PE loader (K1)" if n == 1 else f"{P}P{D}D dual_path"),
                        "kv": shape, "storage_cap_gbps_per_engine": args.cap_gbps or None,
-                       "k1": args.k1, "handoff_ctas": args.handoff_ctas or None,
+                       "k1": args.k1, "k2": args.k2, "handoff_ctas": args.handoff_ctas or None,
                        "requests": info["requests"], "hit_bytes_per_step": info["hit_bytes"],
                        "de_path_requests": info["de_path"],
                        "read_gb_per_engine": [round(x / 1e9, 2) for x in info["reader_bytes"]],

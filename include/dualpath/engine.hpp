@@ -48,6 +48,9 @@ struct ExecOptions {
   // PE-path loads (K1): 0 = SM gather kernel, 1 = copy engine (no SMs: the
   // isolation mode while the PE computes, and the faster PCIe read path)
   std::int32_t k1_mode = 0;
+  // DE-path loads (K2): 0 = SM gather pushing over NVLink, 1 = the DE's copy
+  // engine writing into the PE pool (no SMs on the DE: its decode is untouched)
+  std::int32_t k2_mode = 0;
   // PD handoff: every request's prompt KV also ends in its
   // DE's decode pool — prefill stand-in + PeToDe / MissMerge per layer (K3)
   // and the DE read path fused with DecodeH2D (dual store)

@@ -256,6 +256,12 @@ int dp_set_attend_ctas(int device, int32_t ctas);
  * HERE the dp_job block arrays (src_fb, dst_slot) must be HOST-readable. */
 int dp_h2d_layer_copy(dp_pool* pe, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
                       dp_stream stream);
+/* K2 on the DE's copy engine (no SMs on either GPU): the transfer of
+ * dp_h2d_push_p2p_layer as strided copies from the DE's pinned store into
+ * the PE pool through its peer view (NVLink), then fenced stream writes of
+ * the PE's landed counters.  Block arrays HOST-readable, as above. */
+int dp_h2d_push_copy(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs, int32_t n_jobs,
+                     dp_stream de_stream);
 
 /* Cap on the CTAs a K1/K2 launch on `device` may use (0 = default, 4 per SM).
  * The transfer is PCIe-bound, so a few CTAs keep the link full while leaving

@@ -848,6 +848,7 @@ StepResult EngineRuntime::run_step() {
   std::vector<int> batch_jobs;  // by_reader positions of the jobs in `batch`
   int batch_pe = -1;
   const bool k1_ce = x.opt.k1_mode == 1;
+  const bool k2_ce = x.opt.k2_mode == 1;
 
   // Storage tier: IO threads read each job's Full Blocks from the file into
   // its staging-ring positions, in job order (first reusing a position only
@@ -927,7 +928,10 @@ StepResult EngineRuntime::run_step() {
     const auto n = static_cast<int32_t>(batch.size());
     int rc;
     const char* what;
-    if (batch_pe != engine_) {
+    if (batch_pe != engine_ && k2_ce) {
+      rc = dp_h2d_push_copy(dst, store_, batch.data(), n, s);
+      what = "dp_h2d_push_copy";
+    } else if (batch_pe != engine_) {
       rc = dp_h2d_push_p2p_layer(dst, store_, batch.data(), n, s);
       what = "dp_h2d_push_p2p_layer";
     } else if (k1_ce) {
@@ -938,7 +942,8 @@ StepResult EngineRuntime::run_step() {
       what = "dp_h2d_layer_gather";
     }
     check(rc, what);
-    if (!(k1_ce && batch_pe == engine_))  // kernel launches (the copy engine path has none)
+    const bool on_ce = batch_pe == engine_ ? k1_ce : k2_ce;
+    if (!on_ce)  // kernel launches (the copy engine paths have none)
       res.launches += (static_cast<std::int64_t>(batch.size()) + DP_MAX_JOBS_PER_LAUNCH - 1) /
                       DP_MAX_JOBS_PER_LAUNCH;
     batch.clear();
@@ -995,7 +1000,7 @@ StepResult EngineRuntime::run_step() {
       ++res.launches;
     }
     batch_pe = j.pe;
-    if (k1_ce && j.pe == engine_)  // copy engine: host-readable block tables
+    if (j.pe == engine_ ? k1_ce : k2_ce)  // copy engine: host-readable block tables
       batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,
                              j.cached, j.n_blk, 0, x.cfg.n_layer, j.ticket});
     else

@@ -636,15 +636,24 @@ WriteValue32Fn write_value32() {
 
 }  // namespace
 
-int dp_h2d_layer_copy(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
-                      dp_stream stream) {
-  if (!pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0)
-    return fail(DP_EINVAL, "h2d_layer_copy: null argument");
-  if (!pool->owner) return fail(DP_EINVAL, "h2d_layer_copy: destination must be the local PE pool");
-  if (!geom_equal(pool->geom, src->geom))
-    return fail(DP_EINVAL, "h2d_layer_copy: pool and store geometry differ");
+namespace {
+
+// K1 / K2 on the copy engine: one strided copy per contiguous block run per
+// layer (Full-Block pitch -> Layer-Block pitch), then fenced stream writes of
+// the layer's landed counter and the all-layer column.  With a peer view the
+// destination (pool and counters) is the PE's memory over NVLink and the
+// stream is the DE's.
+int copy_transfer(const char* who, dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
+                  dp_stream stream, bool peer) {
+  const std::string w(who);
+  if (!pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0) return fail(DP_EINVAL, w + ": null argument");
+  if (!peer && !pool->owner) return fail(DP_EINVAL, w + ": destination must be the local PE pool");
+  if (peer && pool->owner) return fail(DP_EINVAL, w + ": destination must be a peer view of a PE pool");
+  if (peer && pool->device != src->device)
+    return fail(DP_EINVAL, w + ": the peer view must be mapped on the store's device");
+  if (!geom_equal(pool->geom, src->geom)) return fail(DP_EINVAL, w + ": pool and store geometry differ");
   const WriteValue32Fn wv = write_value32();
-  if (!wv) return fail(DP_ECUDA, "h2d_layer_copy: cuStreamWriteValue32 unavailable");
+  if (!wv) return fail(DP_ECUDA, w + ": cuStreamWriteValue32 unavailable");
   const dp_kv_geom& g = pool->geom;
   const int64_t lb = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
   const int64_t fbb = lb * g.n_layer;
@@ -657,12 +666,12 @@ int dp_h2d_layer_copy(dp_pool* pool, const dp_store* src, const dp_job* jobs, in
     const int64_t need_blk = (job.n_tokens + g.block_tokens - 1) / g.block_tokens;
     if (job.n_tokens < 0 || job.n_blk != need_blk || job.layer_begin < 0 ||
         job.layer_end > g.n_layer || job.layer_begin > job.layer_end || job.ticket >= pool->n_tickets)
-      return fail(DP_EINVAL, "h2d_layer_copy: job " + std::to_string(j) + " out of range");
+      return fail(DP_EINVAL, w + ": job " + std::to_string(j) + " out of range");
     if (job.n_blk == 0) continue;
     for (int32_t k = 0; k < job.n_blk; ++k)
       if (job.src_fb[k] < 0 || job.src_fb[k] >= src->n_fb || job.dst_slot[k] < 0 ||
           job.dst_slot[k] >= pool->n_slots)
-        return fail(DP_EINVAL, "h2d_layer_copy: block " + std::to_string(k) + " out of range");
+        return fail(DP_EINVAL, w + ": block " + std::to_string(k) + " out of range");
     const int32_t full = job.n_tokens % g.block_tokens == 0 ? job.n_blk : job.n_blk - 1;
     uint32_t* row = pool->counters + static_cast<int64_t>(job.ticket) * (g.n_layer + 1);
     for (int32_t layer = job.layer_begin; layer < job.layer_end; ++layer) {
@@ -689,11 +698,23 @@ int dp_h2d_layer_copy(dp_pool* pool, const dp_store* src, const dp_job* jobs, in
                 CUDA_SUCCESS ||
             wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + g.n_layer),
                per_layer * static_cast<uint32_t>(layer - job.layer_begin + 1), 0) != CUDA_SUCCESS)
-          return fail(DP_ECUDA, "h2d_layer_copy: cuStreamWriteValue32 failed");
+          return fail(DP_ECUDA, w + ": cuStreamWriteValue32 failed");
       }
     }
   }
   return DP_OK;
+}
+
+}  // namespace
+
+int dp_h2d_layer_copy(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
+                      dp_stream stream) {
+  return copy_transfer("h2d_layer_copy", pool, src, jobs, n_jobs, stream, /*peer=*/false);
+}
+
+int dp_h2d_push_copy(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs, int32_t n_jobs,
+                     dp_stream de_stream) {
+  return copy_transfer("h2d_push_copy", pe_view, de_src, jobs, n_jobs, de_stream, /*peer=*/true);
 }
 
 int dp_stream_wait_counter(const dp_pool* pool, int32_t ticket, int32_t layer, uint32_t target,

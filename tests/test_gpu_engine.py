@@ -310,3 +310,26 @@ def test_handoff_with_persistence(two_gpus, tight):
                 checked += 1
     assert checked > 0
     del last
+
+
+@pytest.mark.multigpu
+def test_two_engines_k2_on_copy_engine(two_gpus):
+    # tight pool: cross-reader reuse hazards with the DE's copy-engine pushes
+    cfg = cluster(1, 1, L=4)
+    trajs = small_trace(count=10, turns=6, seed=8)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.k2_mode = 1
+    probe = dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.pool_slots = probe.peak_slots
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert xp.reader_bytes[1] > 0
+    pe = dp.EngineRuntime(xp, 0, 0)
+    de = dp.EngineRuntime(xp, 1, 1)
+    de.attach_peer_local(0, pe)
+    for _ in range(2):
+        pe.reset_counters()
+        dp.run_step_all([pe, de])
+        verify_counters(pe, xp, cfg)
+        verify_pool(pe, xp, cfg)

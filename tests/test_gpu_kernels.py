@@ -258,3 +258,51 @@ def test_k1_copy_engine_parity(gpus, L, T, b):
     finally:
         pool.close()
         st.close()
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("L,T,b", [(61, 64, 576), (4, 64, 4096), (3, 16, 1024)])
+def test_k2_copy_engine_parity(two_gpus, L, T, b):
+    """K2 on the DE's copy engine (dp_h2d_push_copy): the DE's stream copies
+    its host store into the PE pool through the peer view and writes the PE's
+    counters; same bytes and counters as the kernel."""
+    rng = np.random.default_rng(23)
+    g = abi.geom(L, T, b)
+    n_fb, n_slots = 16, 64
+    st_de = abi.Store(1, g, n_fb, SEED)
+    pool = abi.Pool(0, g, n_slots, 12)
+    view = pool.peer_view(1)
+    try:
+        plain, keep, specs, used = [], [], [], 0
+        for t in range(12):
+            nblk = int(rng.integers(0, 6))
+            if used + nblk + 1 > n_slots:
+                nblk = 0
+            ntok = 0 if nblk == 0 else (nblk - 1) * T + int(rng.integers(1, T + 1))
+            fb0 = int(rng.integers(0, n_fb - nblk)) if nblk else 0
+            fbs = np.arange(fb0, fb0 + nblk, dtype=np.int64)
+            slots = np.arange(used, used + nblk, dtype=np.int32)
+            if nblk >= 3:
+                slots[nblk // 2:] += 1
+            used += nblk + 1
+            keep += [fbs, slots]
+            specs.append((fbs.ctypes.data, slots.ctypes.data, ntok, nblk, 0, L, t))
+            plain.append((fbs, slots, ntok, 0, L))
+        import torch
+        s_de = torch.cuda.Stream(device=1)
+        abi.h2d_push_copy(view, st_de, abi.make_jobs(specs), len(specs), s_de.cuda_stream)
+        # the PE observes completion through its own counters only
+        for t, (fbs, slots, ntok, l0, l1) in enumerate(plain):
+            abi.wait_layer(pool, t, L, abi.layer_items(g, len(slots)) * L, timeout_ms=10000)
+        sync()
+        torch.cuda.synchronize(1)
+        assert abi.wait_status(pool) == abi.DP_OK
+        store_img = np.frombuffer(st_de.bytes(), dtype=np.uint8).copy()
+        check_pool(pool, refpy.geom(L, T, b), plain, T, b, store_img, n_slots)
+        # a local pool is rejected (the copy targets a peer view)
+        with pytest.raises(abi.DualPathError):
+            abi.h2d_push_copy(pool, st_de, abi.make_jobs(specs), len(specs))
+    finally:
+        view.close()
+        pool.close()
+        st_de.close()
