@@ -103,11 +103,61 @@ def k3(a, g, L, T, b, n_fb, n_slots):
         st.close()
 
 
+def k4(a, g, L, T, b, n_fb, n_slots):
+    """K4 alone (PersistD2H): every token of a.jobs requests of a.blocks blocks
+    gathered from the decode pool into storage Full Blocks in pinned host
+    memory (zero-copy stores over PCIe D2H)."""
+    pool = abi.Pool(0, g, n_slots, 1)
+    target = abi.Store(0, g, n_fb, 10)
+    try:
+        rng = np.random.default_rng(0)
+        keep, spans = [], (abi.SpanJob * a.jobs)()
+        perm = rng.permutation(n_slots)
+        for j in range(a.jobs):
+            fbs = torch.tensor(rng.integers(0, n_fb, a.blocks), dtype=torch.int64, device="cuda:0")
+            sl = torch.tensor(perm[(j * a.blocks) % n_slots:][:a.blocks].astype(np.int32), device="cuda:0")
+            keep += [fbs, sl]
+            spans[j] = abi.SpanJob(sl.data_ptr(), fbs.data_ptr(), 0, 0, a.blocks * T, a.blocks, 0)
+        abi.decode_fill(pool, spans, a.jobs, 9)
+        torch.cuda.synchronize(0)
+        nbytes = a.jobs * a.blocks * T * b * L
+        times = []
+        s = torch.cuda.Stream(device=0)
+        for r in range(a.reps + 1):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            abi.persist_d2h(pool, target, spans, a.jobs, s.cuda_stream)
+            e1.record(s)
+            e1.synchronize()
+            if r:
+                times.append(e0.elapsed_time(e1))
+        ms = sorted(times)[len(times) // 2]
+        # the copy-engine D2H peak for comparison
+        h = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+        d = torch.empty(1 << 30, dtype=torch.uint8, device="cuda:0")
+        best = 1e9
+        for _ in range(3):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            with torch.cuda.stream(s):
+                h.copy_(d, non_blocking=True)
+            e1.record(s)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return {"bytes": nbytes, "ms": ms, "GBps": nbytes / ms / 1e6, "ce_d2h_GBps": (1 << 30) / best / 1e6}
+    finally:
+        pool.close()
+        target.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--k2", action="store_true")
     ap.add_argument("--k3", action="store_true")
     ap.add_argument("--k3-ctas", default="0")
+    ap.add_argument("--k4", action="store_true")
     ap.add_argument("--jobs", type=int, default=64)
     ap.add_argument("--blocks", type=int, default=128)  # 8K-token requests
     ap.add_argument("--reps", type=int, default=3)
@@ -131,6 +181,8 @@ def main():
             abi.set_handoff_ctas(0, ctas)
             out["k3" if ctas == 0 else f"k3@{ctas}"] = k3(a, g, L, T, b, n_fb, n_slots)
         abi.set_handoff_ctas(0, 0)
+    if a.k4:
+        out["k4"] = k4(a, g, L, T, b, n_fb, n_slots)
     print(json.dumps(out))
 
 
