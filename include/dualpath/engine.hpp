@@ -313,12 +313,15 @@ class EngineRuntime {
   StepResult run_step_prefill(bool loads);
   void enqueue_forward(int f, StepResult& res);
   void upload_prefill_tables();
+  void* stream_c_ = nullptr;                // PE: the compute stream (forwards)
   std::vector<void*> ev_fwd_;               // PE: per forward, recorded after its last layer
   std::vector<std::vector<dp_attend_item>> fwd_att_;  // PE: per forward, K5 items
   std::vector<std::int64_t> fwd_wait_off_;  // PE: per forward, offset of its KV waits in d_wt_
   std::vector<std::int32_t> fwd_wait_n_;
   std::vector<std::vector<std::int32_t>> fwd_done_;   // PE: per forward, tickets read last there
   std::uint64_t* d_digest_ = nullptr;
+  std::int32_t* d_fwt_ = nullptr;           // PE: forward gate tickets / targets
+  std::uint32_t* d_fwg_ = nullptr;
   std::int32_t* d_fwd_slot_ = nullptr;
   // ---- storage tier ----
   std::unique_ptr<FullBlockFile> tier_file_;

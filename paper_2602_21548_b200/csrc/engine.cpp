@@ -8,6 +8,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <deque>
+#include <limits>
 #include <mutex>
 #include <stdexcept>
 #include <thread>
@@ -155,6 +156,8 @@ void build_forwards(ExecPlan& x, const pdsim::desim::SimReport& plan) {
       if (rid < static_cast<int>(job_of_req.size()) && job_of_req[rid] >= 0) {
         job[i] = job_of_req[rid];
         row_of_job[job[i]] = i;
+      } else if (q[i]->cached > 0) {
+        throw std::logic_error("build_exec_plan: a request with cached KV reached prefill without a load job");
       }
     }
     for (int i = 0; i < n; ++i)
@@ -282,8 +285,6 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
   x.persist = opt.persist;
   if (x.persist && !x.handoff) throw std::invalid_argument("build_exec_plan: persist needs handoff");
   x.prefill = opt.prefill;
-  if (x.prefill && x.handoff)
-    throw std::invalid_argument("build_exec_plan: prefill and handoff are separate modes");
   if (x.prefill && !(opt.compute_quota > 0))
     throw std::invalid_argument("build_exec_plan: compute_quota must be > 0");
   x.tier = !opt.tier_path.empty();
@@ -409,11 +410,15 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
         // the previous occupant's K3 (same PE, handoff stream) must be done
         if (std::find(j.k3_waits.begin(), j.k3_waits.end(), prev) == j.k3_waits.end())
           j.k3_waits.push_back(prev);
+        if (x.prefill && std::find(j.consumer_waits.begin(), j.consumer_waits.end(), prev) == j.consumer_waits.end())
+          j.consumer_waits.push_back(prev);  // K3 runs after the forwards: keep them apart
       } else if (std::find(j.pe_done_preds.begin(), j.pe_done_preds.end(), pj.ticket) ==
                  j.pe_done_preds.end()) {
         j.pe_done_preds.push_back(pj.ticket);  // + n_tickets[pe] once known
         j.pe_done_targets.push_back(
             static_cast<std::uint32_t>(static_cast<std::int64_t>(pj.n_pblk) * x.items_per_block * L));
+        if (x.prefill && std::find(j.consumer_waits.begin(), j.consumer_waits.end(), prev) == j.consumer_waits.end())
+          j.consumer_waits.push_back(prev);
       }
     }
     order.push_back(e.job);
@@ -473,7 +478,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     for (int& w : j.k3_waits) w = pos[w];
     for (int& w : j.consumer_waits) w = pos[w];
     if (x.prefill) {
-      if (j.reader != j.pe)  // a DE load waits on the PE's "consumed" rows [n, 2n)
+      if (j.reader != j.pe && !x.handoff)  // a DE load waits on the PE's "consumed" rows [n, 2n)
         for (int w : j.consumer_waits) {
           j.preds.push_back(x.jobs[w].ticket + x.n_tickets[j.pe]);
           j.pred_targets.push_back(1u);
@@ -596,7 +601,7 @@ void EngineRuntime::upload_prefill_tables() {
   const std::int32_t L = x.cfg.n_layer;
   cudaStream_t c;
   check_cuda(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "cudaStreamCreate");
-  stream_h_ = c;  // the compute stream: forwards
+  stream_c_ = c;  // the compute stream: forwards
   // the load stream outranks the compute stream: as K5 CTAs retire, the
   // block scheduler places pending loader CTAs first
   int lo = 0, hi = 0;
@@ -642,14 +647,15 @@ void EngineRuntime::upload_prefill_tables() {
     check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     ev_fwd_.push_back(e);
   }
-  d_wt_ = upload(wt);
-  d_wg_ = upload(wg);
+  d_fwt_ = upload(wt);
+  d_fwg_ = upload(wg);
 }
 
 EngineRuntime::~EngineRuntime() {
   DeviceScope ds(device_);
   if (stream_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
   if (stream_h_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_h_));
+  if (stream_c_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_c_));
   for (int e = 0; e < static_cast<int>(peers_.size()); ++e)
     if (peers_[e] && peers_[e] != pool_) dp_pool_destroy(peers_[e]);
   for (dp_pool* v : de_views_)
@@ -664,7 +670,8 @@ EngineRuntime::~EngineRuntime() {
                   static_cast<void*>(d_ho_de_), static_cast<void*>(d_dual_de_),
                   static_cast<void*>(d_wt_), static_cast<void*>(d_wg_),
                   static_cast<void*>(d_dec_slot_), static_cast<void*>(d_dec_fb_),
-                  static_cast<void*>(d_digest_), static_cast<void*>(d_fwd_slot_)})
+                  static_cast<void*>(d_digest_), static_cast<void*>(d_fwd_slot_),
+                  static_cast<void*>(d_fwt_), static_cast<void*>(d_fwg_)})
     if (p) cudaFree(p);
   for (void* e : ev_load_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* e : ev_k3_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
@@ -673,6 +680,7 @@ EngineRuntime::~EngineRuntime() {
   if (ev_start_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_start_));
   if (ev_end_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_end_));
   if (stream_h_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_h_));
+  if (stream_c_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_c_));
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
 }
 
@@ -1042,7 +1050,7 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
   const ExecPlan& x = *plan_;
   DeviceScope ds(device_);
   auto s = static_cast<cudaStream_t>(stream_);
-  auto c = static_cast<cudaStream_t>(stream_h_);
+  auto c = static_cast<cudaStream_t>(stream_c_);
   StepResult res;
   const auto t0 = std::chrono::steady_clock::now();
   auto start = static_cast<cudaEvent_t>(ev_start_);
@@ -1130,14 +1138,14 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
 
 void EngineRuntime::enqueue_forward(int f, StepResult& res) {
   const ExecPlan& x = *plan_;
-  auto c = static_cast<cudaStream_t>(stream_h_);
+  auto c = static_cast<cudaStream_t>(stream_c_);
   const std::int32_t L = x.cfg.n_layer;
   const auto& att = fwd_att_[f];
   std::int64_t work = 0;
   for (const dp_attend_item& a : att) work += (a.cached > 0 && a.bsz > 0) ? 1 : 0;
   for (std::int32_t layer = 0; layer < L; ++layer) {
     if (fwd_wait_n_[f] > 0) {
-      check(dp_wait_tickets(pool_, d_wt_ + fwd_wait_off_[f], d_wg_ + fwd_wait_off_[f], fwd_wait_n_[f], layer,
+      check(dp_wait_tickets(pool_, d_fwt_ + fwd_wait_off_[f], d_fwg_ + fwd_wait_off_[f], fwd_wait_n_[f], layer,
                             x.opt.wait_timeout_ms, c),
             "dp_wait_tickets (forward gate)");
       ++res.launches;
@@ -1147,8 +1155,9 @@ void EngineRuntime::enqueue_forward(int f, StepResult& res) {
     res.launches += (work + DP_MAX_ATTEND_ITEMS_PER_LAUNCH - 1) / DP_MAX_ATTEND_ITEMS_PER_LAUNCH;
   }
   check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_fwd_[f]), c), "cudaEventRecord");
-  for (std::int32_t t : fwd_done_[f])
-    check(dp_stream_write_counter(pool_, t + x.n_tickets[engine_], L, 1, c), "dp_stream_write_counter");
+  if (!x.handoff)  // with the handoff, K3 (after the forward) marks the rows
+    for (std::int32_t t : fwd_done_[f])
+      check(dp_stream_write_counter(pool_, t + x.n_tickets[engine_], L, 1, c), "dp_stream_write_counter");
   ++res.forwards;
 }
 
@@ -1201,36 +1210,25 @@ StepResult EngineRuntime::run_step_handoff() {
   const auto nt = [&](int pe) { return x.n_tickets[pe]; };
 
   if (is_pe()) {
-    for (int ji : x.by_pe[engine_]) {
+    const bool pf = x.prefill;
+    auto c = static_cast<cudaStream_t>(stream_c_);
+    const auto& mine = x.by_pe[engine_];
+    std::vector<std::int32_t> row_of;  // prefill: FIFO row of each job of this PE
+    if (pf) {
+      check_cuda(cudaStreamWaitEvent(c, start, 0), "cudaStreamWaitEvent");
+      const std::size_t rows = std::max<std::size_t>(1, x.fwd_rows[engine_].size());
+      check_cuda(cudaMemsetAsync(d_digest_, 0, rows * L * sizeof(std::uint64_t), c), "cudaMemsetAsync digests");
+      row_of.assign(x.jobs.size(), -1);
+      for (const FwdItem& it : x.fwd_items[engine_])
+        if (it.job >= 0) row_of[it.job] = it.row;
+    }
+    // K3 of one job on the handoff stream: decode-slot hazards, then K3
+    auto enqueue_k3 = [&](int ji) {
       const LoadJob& j = x.jobs[ji];
-      const int li = pe_local_[ji];
-      auto ev_load = static_cast<cudaEvent_t>(ev_load_[li]);
-      auto ev_k3 = static_cast<cudaEvent_t>(ev_k3_[li]);
-      if (!de_views_[j.de]) throw std::runtime_error("run_step: DE " + std::to_string(j.de) + " not attached");
-      // --- load stream: this PE's own reads (PE path)
-      if (!j.de_path && j.n_blk > 0) {
-        for (int w : j.k3_waits)
-          check_cuda(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_k3_[pe_local_[w]]), 0),
-                     "cudaStreamWaitEvent");
-        storage_gate(j);
-        dp_job job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket};
-        if (x.opt.k1_mode == 1) {
-          job.src_fb = x.src_fb[engine_].data() + j.blk_off;
-          job.dst_slot = x.slots[engine_].data() + j.blk_off;
-          check(dp_h2d_layer_copy(pool_, store_, &job, 1, s), "dp_h2d_layer_copy");
-        } else {
-          check(dp_h2d_layer_gather(pool_, store_, &job, 1, s), "dp_h2d_layer_gather");
-          ++res.launches;
-        }
-        check_cuda(cudaEventRecord(ev_load, s), "cudaEventRecord");
-        check_cuda(cudaStreamWaitEvent(h, ev_load, 0), "cudaStreamWaitEvent");
-      } else if (!j.de_path) {
-        // cold request on the PE path: only its K3 reuses slots
-        for (int w : j.k3_waits)
-          check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_k3_[pe_local_[w]]), 0),
-                     "cudaStreamWaitEvent");
-      }
-      // --- handoff stream: decode-slot hazards, then K3
+      auto ev_k3 = static_cast<cudaEvent_t>(ev_k3_[pe_local_[ji]]);
+      if (pf)  // the prompt is handed off after its last forward
+        check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[ji]]), 0),
+                   "cudaStreamWaitEvent");
       if (!j.de_preds.empty()) {
         const std::int64_t off = de_wait_off_[ji];
         check(dp_wait_tickets(de_views_[j.de], d_wt_ + off, d_wg_ + off,
@@ -1261,11 +1259,63 @@ StepResult EngineRuntime::run_step_handoff() {
             "dp_prefill_handoff");
       ++res.launches;
       check_cuda(cudaEventRecord(ev_k3, h), "cudaEventRecord");
+    };
+    // prefill: forwards whose requests' loads are all enqueued (row < r), and
+    // the K3s of the requests they finish
+    static const std::vector<Forward> kNone;
+    const std::vector<Forward>& fwds = pf ? x.forwards[engine_] : kNone;
+    std::size_t fi = 0, ki = 0;
+    auto drain = [&](std::int64_t r) {
+      while (fi < fwds.size() && fwds[fi].last_row < r) {
+        enqueue_forward(static_cast<int>(fi++), res);
+        while (ki < mine.size() && x.last_fwd[mine[ki]] < static_cast<int>(fi)) enqueue_k3(mine[ki++]);
+      }
+    };
+    for (int ji : mine) {
+      const LoadJob& j = x.jobs[ji];
+      const int li = pe_local_[ji];
+      auto ev_load = static_cast<cudaEvent_t>(ev_load_[li]);
+      if (!de_views_[j.de]) throw std::runtime_error("run_step: DE " + std::to_string(j.de) + " not attached");
+      // a load reusing slots waits for K3s, which wait for forwards: enqueue them first
+      if (pf && (!j.k3_waits.empty() || gated)) drain(row_of[ji]);
+      // --- load stream: this PE's own reads (PE path)
+      if (!j.de_path && j.n_blk > 0) {
+        for (int w : j.k3_waits)
+          check_cuda(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_k3_[pe_local_[w]]), 0),
+                     "cudaStreamWaitEvent");
+        storage_gate(j);
+        dp_job job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket};
+        if (x.opt.k1_mode == 1) {
+          job.src_fb = x.src_fb[engine_].data() + j.blk_off;
+          job.dst_slot = x.slots[engine_].data() + j.blk_off;
+          check(dp_h2d_layer_copy(pool_, store_, &job, 1, s), "dp_h2d_layer_copy");
+        } else {
+          check(dp_h2d_layer_gather(pool_, store_, &job, 1, s), "dp_h2d_layer_gather");
+          ++res.launches;
+        }
+        check_cuda(cudaEventRecord(ev_load, s), "cudaEventRecord");
+        check_cuda(cudaStreamWaitEvent(h, ev_load, 0), "cudaStreamWaitEvent");
+      } else if (!j.de_path) {
+        // cold request on the PE path: only its K3 reuses slots
+        for (int w : j.k3_waits)
+          check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_k3_[pe_local_[w]]), 0),
+                     "cudaStreamWaitEvent");
+      }
+      if (!pf) enqueue_k3(ji);
     }
-    // the step ends when both streams are drained
-    check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), s), "cudaEventRecord");
-    check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_end_), 0), "cudaStreamWaitEvent");
-    check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), h), "cudaEventRecord");
+    if (pf) {
+      drain(std::numeric_limits<std::int64_t>::max());
+      while (ki < mine.size()) enqueue_k3(mine[ki++]);
+    }
+    // the step ends when every stream is drained
+    auto end_ev = static_cast<cudaEvent_t>(ev_end_);
+    check_cuda(cudaEventRecord(end_ev, s), "cudaEventRecord");
+    check_cuda(cudaStreamWaitEvent(h, end_ev, 0), "cudaStreamWaitEvent");
+    if (pf) {
+      check_cuda(cudaEventRecord(end_ev, c), "cudaEventRecord");
+      check_cuda(cudaStreamWaitEvent(h, end_ev, 0), "cudaStreamWaitEvent");
+    }
+    check_cuda(cudaEventRecord(end_ev, h), "cudaEventRecord");
   } else {
     // A DE enqueues its work job by job in the global order, across its two
     // streams: every operation a wait depends on belongs to an earlier job,

@@ -346,14 +346,49 @@ def test_prefill_forwards_are_reference_build_forward_batch():
         assert head == len(rows)
 
 
-def test_prefill_excludes_handoff():
+def test_prefill_rejects_bad_quota():
     cfg = cluster(1, 1)
     trajs = dp.synthesize(max_len=20000, count=4, seed=8, mean_turns=4, sigma_turns=0)
     planned = dp.plan(cfg, trajs, policy="dual_path", **SB)
     opt = dp.ExecOptions()
-    opt.prefill, opt.handoff = True, True
+    opt.prefill, opt.compute_quota = True, 0.0
     with pytest.raises(ValueError):
         dp.build_exec_plan(cfg, trajs, planned, opt)
-    opt.handoff, opt.compute_quota = False, 0.0
-    with pytest.raises(ValueError):
-        dp.build_exec_plan(cfg, trajs, planned, opt)
+
+
+@pytest.mark.parametrize("P,D,tight", [(1, 1, True), (2, 2, True), (1, 3, False)])
+def test_prefill_with_handoff_keeps_k3_after_forwards(P, D, tight):
+    """Handoff + prefill: K3 of a request runs after its last forward, so a
+    load that waits for an earlier request's K3 (PE slot reuse) must not share
+    a forward with it; every request of the PE is prefilled exactly once."""
+    cfg = cluster(P, D)
+    trajs = dp.synthesize(max_len=20000, count=10, seed=8, mean_turns=6, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **SB)
+    opt = dp.ExecOptions()
+    opt.handoff, opt.prefill, opt.compute_quota, opt.prefill_cost = True, True, 2e-3, COST
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    if tight:
+        opt.pool_slots = xp.peak_slots
+        xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    jobs = xp.jobs()
+    reqs = {r[0]: r for r in planned["requests"]}
+    n_waits = 0
+    for pe in range(xp.n_pe):
+        first = {}
+        done = {}
+        for fi, (_, items) in enumerate(xp.forwards(pe)):
+            for req, job, cached, q0, bsz, row in items:
+                assert job >= 0, "with the handoff every prefilled request has a job"
+                first.setdefault(job, fi)
+                assert q0 == done.get(req, 0)
+                done[req] = q0 + bsz
+        for rid, n in done.items():
+            assert n == reqs[rid][4]
+        for i in xp.by_pe(pe):
+            for w in xp.consumer_waits(i):
+                n_waits += 1
+                assert xp.last_fwd(w) < first[i]
+            # the k3_waits / pe_done_preds hazards are all covered
+            assert set(jobs[i][20]) <= set(xp.consumer_waits(i))
+    if tight:
+        assert n_waits > 0

@@ -217,3 +217,40 @@ def test_prefill_1p1d_dual_path(two_gpus, tight):
         res = dp.run_step_all([pe, de])
         assert res[0].bytes_read + res[1].bytes_read == xp.hit_bytes
         check_digests(pe, cfg, planned, xp)
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("tight,persist", [(False, False), (True, False), (True, True)])
+def test_prefill_with_handoff_1p1d(two_gpus, tight, persist):
+    """The whole pipeline: loads on both paths, quota-batched K5 forwards on
+    the PE, K3 handoff of each prompt after its last forward, (decode +
+    K4 persistence).  Digests equal the oracle's and every prompt lands in its
+    DE's decode pool."""
+    from test_gpu_engine import handoff_engines, verify_prompt_pool
+    cfg = cluster(1, 1, L=4)
+    trajs = dp.synthesize(max_len=12000, count=8, seed=6, mean_turns=5, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.handoff = True
+    opt.persist = persist
+    opt.prefill = True
+    opt.compute_quota = 5e-4
+    opt.prefill_cost = COST
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    if tight:
+        opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots
+        xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    rts = handoff_engines(xp, 2)
+    for _ in range(2):
+        for rt in rts:
+            rt.reset_counters()
+        res = dp.run_step_all(rts)
+        assert sum(r.bytes_read for r in res) == xp.hit_bytes
+        assert res[0].forwards == len(xp.forwards(0)) > 1
+        check_digests(rts[0], cfg, planned, xp)
+    assert verify_prompt_pool(rts[1], xp, cfg) > 0
+    ctr = np.asarray(rts[1].counters(), dtype=np.int64).reshape(-1, cfg.n_layer + 1)
+    for job in xp.jobs():
+        blocks = (job[7] if job[5] else 0) + job[15]
+        assert ctr[job[16], cfg.n_layer] == blocks * xp.items_per_block * cfg.n_layer
