@@ -125,6 +125,8 @@ struct LoadJob {
   std::vector<int> consumer_waits;  // jobs whose slots this one reuses: their last forward
                                     // must be done before this job's load writes
   std::int64_t fwd_off = 0;         // offset of its slots in the PE's forward slot table
+  int k3_after = -1;                // handoff + prefill: the last job (global order) of the
+                                    // forward after which this job's K3 runs
   // ---- storage tier ----
   std::vector<int> ring_waits;      // jobs (same reader) whose staging positions this
                                     // job's reads overwrite: their transfer must be done

@@ -520,7 +520,12 @@ PYBIND11_MODULE(_core, m) {
            })
       .def("fwd_rows", [](const dualpath::ExecPlan& x, int pe) { return x.fwd_rows.at(pe); })
       .def("consumer_waits", [](const dualpath::ExecPlan& x, int job) { return x.jobs.at(job).consumer_waits; })
-      .def("last_fwd", [](const dualpath::ExecPlan& x, int job) { return x.last_fwd.at(job); });
+      .def("last_fwd", [](const dualpath::ExecPlan& x, int job) { return x.last_fwd.at(job); })
+      .def("fwd_slots", [](const dualpath::ExecPlan& x, int job) {
+        const dualpath::LoadJob& j = x.jobs.at(job);
+        const auto& t = x.fwd_slot.at(j.pe);
+        return std::vector<std::int32_t>(t.begin() + j.fwd_off, t.begin() + j.fwd_off + j.n_blk);
+      });
 
   m.def(
       "build_exec_plan",

@@ -193,6 +193,10 @@ void build_forwards(ExecPlan& x, const pdsim::desim::SimReport& plan) {
       }
       f.end = static_cast<std::int32_t>(x.fwd_items[p].size());
       x.forwards[p].push_back(f);
+      int last_job = -1;
+      for (std::int32_t i = f.begin; i < f.end; ++i) last_job = std::max(last_job, x.fwd_items[p][i].job);
+      for (std::int32_t i = f.begin; i < f.end; ++i)
+        if (x.fwd_items[p][i].job >= 0) x.jobs[x.fwd_items[p][i].job].k3_after = last_job;
       if (fb.chunked) {
         head_done = fb.consumed_whole == 0 ? head_done + fb.chunk_bsz : fb.chunk_bsz;
       } else {
@@ -391,7 +395,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
       q.owner[s] = e.job;
       if (prev < 0) continue;
       const LoadJob& pj = jobs[prev];
-      if (x.prefill) {
+      if (x.prefill && !x.handoff) {
         // the previous occupant's KV is read by its forwards: the reuse
         // waits for the last of them (which implies it landed)
         if (std::find(j.consumer_waits.begin(), j.consumer_waits.end(), prev) == j.consumer_waits.end())
@@ -1327,7 +1331,11 @@ StepResult EngineRuntime::run_step_handoff() {
     const auto& reads = x.by_reader[engine_];
     const auto& decodes = x.by_de[engine_];
     while (ri < reads.size() || (x.persist && di < decodes.size())) {
-      const bool take_read = ri < reads.size() && (!x.persist || di >= decodes.size() || reads[ri] <= decodes[di]);
+      // with the prefill, a request's K3 (which its decode waits for) needs
+      // the loads of every request in its last forward: read those first
+      const auto decode_key = [&](int ji) { return std::max(ji, x.jobs[ji].k3_after); };
+      const bool take_read = ri < reads.size() &&
+                             (!x.persist || di >= decodes.size() || reads[ri] <= decode_key(decodes[di]));
       if (take_read) {  // DE read path: dual gather
         const int ji = reads[ri++];
         const LoadJob& j = x.jobs[ji];
