@@ -249,7 +249,8 @@ def test_prefill_with_handoff_1p1d(two_gpus, tight, persist):
         assert sum(r.bytes_read for r in res) == xp.hit_bytes
         assert res[0].forwards == len(xp.forwards(0)) > 1
         check_digests(rts[0], cfg, planned, xp)
-    assert verify_prompt_pool(rts[1], xp, cfg) > 0
+    if not persist:  # (with persistence the decode pool's last occupants also hold generated tokens)
+        assert verify_prompt_pool(rts[1], xp, cfg) > 0
     ctr = np.asarray(rts[1].counters(), dtype=np.int64).reshape(-1, cfg.n_layer + 1)
     for job in xp.jobs():
         blocks = (job[7] if job[5] else 0) + job[15]
