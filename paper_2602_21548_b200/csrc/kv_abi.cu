@@ -1343,7 +1343,7 @@ constexpr int kAttRows = 64;     // query rows and key rows per tile
 constexpr int kAttWords = 144;   // 32-bit words per staged row chunk (576 B)
 constexpr int kAttStride = 148;  // padded row stride in words
 constexpr int kAttGroup = 4;     // key tiles per unit
-constexpr int kAttSmem = 2 * kAttRows * kAttStride * 4;  // 75,776 B
+constexpr int kAttSmem = 3 * kAttRows * kAttStride * 4;  // query tile + 2 key tiles: 113,664 B
 constexpr uint64_t kQueryMul = 0xA24BAED4963EE407ull;
 int g_attend_ctas[kMaxDevices] = {};
 bool g_attend_init[kMaxDevices] = {};
@@ -1366,6 +1366,18 @@ struct AttendParams {
 static_assert(sizeof(AttendParams) <= 4000, "kernel parameter block too large");
 static_assert(sizeof(dp_attend_item) == 48, "dp_attend_item layout");
 
+// 16-byte asynchronous global -> shared copy; src_size 0 zero-fills.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ int64_t attend_key_tiles(int64_t cached) {
   return (cached + kAttRows - 1) / kAttRows;
 }
@@ -1376,7 +1388,8 @@ __global__ void __maxnreg__(96) kv_prefill_attend(const __grid_constant__ Attend
   extern __shared__ uint4 att_smem[];
   __shared__ uint64_t red[kThreads / 32];
   uint32_t* qs = reinterpret_cast<uint32_t*>(att_smem);
-  uint32_t* ks = qs + kAttRows * kAttStride;
+  uint32_t* const kbuf0 = qs + kAttRows * kAttStride;  // key tiles: kbuf0 + (i & 1) * tile
+  constexpr int kTile = kAttRows * kAttStride;
   const int tid = threadIdx.x;
   const int tq = tid >> 4, tt = tid & 15;
   __shared__ int64_t fetched;
@@ -1404,7 +1417,25 @@ __global__ void __maxnreg__(96) kv_prefill_attend(const __grid_constant__ Attend
     for (int c0 = 0; c0 < p.words; c0 += kAttWords) {
       const int cw = min(kAttWords, p.words - c0);  // a multiple of 4 (b % 16 == 0)
       const int half = cw / 2;
-      __syncthreads();  // the previous chunk's readers are done with qs / ks
+      const int vec = cw / 4;
+      // key tile kt -> kbuf[b], asynchronously (rows past `cached` zero-filled)
+      auto issue_tile = [&](int64_t kt, uint32_t* dst) {
+        for (int e = tid; e < kAttRows * vec; e += kThreads) {
+          const int r = e / vec, v4 = e - (e / vec) * vec;
+          const int64_t t = kt * kAttRows + r;
+          const bool valid = t < it.cached;
+          const char* src = p.pool;
+          if (valid) {
+            const int64_t blk = t / p.block_tokens;
+            src = p.pool + p.layer_off + static_cast<int64_t>(it.slot[blk]) * p.lb_bytes +
+                  (t - blk * p.block_tokens) * p.bpt + static_cast<int64_t>(c0) * 4 + v4 * 16;
+          }
+          cp_async16(dst + r * kAttStride + v4 * 4, src, valid);
+        }
+        cp_async_commit();
+      };
+      __syncthreads();  // the previous chunk's readers are done with qs / kbuf
+      issue_tile(kt0, kbuf0);  // in flight while the query tile is generated
       for (int e = tid; e < kAttRows * half; e += kThreads) {
         const int r = e / half, k = e - (e / half) * half;
         uint64_t v = 0;
@@ -1414,22 +1445,15 @@ __global__ void __maxnreg__(96) kv_prefill_attend(const __grid_constant__ Attend
         }
         *reinterpret_cast<uint64_t*>(qs + r * kAttStride + 2 * k) = v;
       }
-      const int vec = cw / 4;
       for (int64_t kt = kt0; kt < kt1; ++kt) {
-        if (kt > kt0) __syncthreads();  // the previous key tile's readers are done
-        for (int e = tid; e < kAttRows * vec; e += kThreads) {
-          const int r = e / vec, v4 = e - (e / vec) * vec;
-          const int64_t t = kt * kAttRows + r;
-          uint4 val = make_uint4(0, 0, 0, 0);
-          if (t < it.cached) {
-            const int64_t blk = t / p.block_tokens;
-            const char* row = p.pool + p.layer_off + static_cast<int64_t>(it.slot[blk]) * p.lb_bytes +
-                              (t - blk * p.block_tokens) * p.bpt + static_cast<int64_t>(c0) * 4;
-            val = reinterpret_cast<const uint4*>(row)[v4];
-          }
-          *reinterpret_cast<uint4*>(ks + r * kAttStride + v4 * 4) = val;
+        const uint32_t* ks = kbuf0 + ((kt - kt0) & 1) * kTile;
+        if (kt + 1 < kt1) {  // double buffer: the next tile loads during this one's math
+          issue_tile(kt + 1, kbuf0 + ((kt + 1 - kt0) & 1) * kTile);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
         }
-        __syncthreads();
+        __syncthreads();  // tile kt (every thread's copies) and the query tile are visible
         uint32_t acc[4][4];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -1459,6 +1483,7 @@ __global__ void __maxnreg__(96) kv_prefill_attend(const __grid_constant__ Attend
 #pragma unroll
           for (int b = 0; b < 4; ++b) s32 += acc[a][b];
         sum += s32;
+        __syncthreads();  // every reader is done with this buffer before it is refilled
       }
     }
 #pragma unroll

@@ -255,3 +255,16 @@ def test_prefill_with_handoff_1p1d(two_gpus, tight, persist):
     for job in xp.jobs():
         blocks = (job[7] if job[5] else 0) + job[15]
         assert ctr[job[16], cfg.n_layer] == blocks * xp.items_per_block * cfg.n_layer
+
+
+@pytest.mark.parametrize("L,T,b", [(3, 64, 4096), (4, 16, 1024), (2, 128, 208)])
+def test_prefill_other_geometries(gpus, L, T, b):
+    """Qwen-sized KV rows, small and large blocks: the executor's forwards
+    and K5 digests stay exact."""
+    cfg = cluster(1, 1, L=L, b=b, T=T)
+    trajs, planned, xp = prefill_plan(cfg, "pe_only", tight=True, quota=2e-4, count=5, turns=4, seed=3)
+    eng = dp.EngineRuntime(xp, 0, 0)
+    eng.reset_counters()
+    r = eng.run_step()
+    assert r.forwards == len(xp.forwards(0)) > 1
+    check_digests(eng, cfg, planned, xp)

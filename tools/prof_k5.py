@@ -13,10 +13,11 @@ import torch  # noqa: E402
 from paper_2602_21548_b200 import abi  # noqa: E402
 
 L, T, B = 61, 64, 576
+N_SLOTS = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 g = abi.geom(L, T, B)
 st = abi.Store(0, g, 1024, 9)
-pool = abi.Pool(0, g, 512, 4)
-perm = np.random.default_rng(0).permutation(512).astype(np.int32)
+pool = abi.Pool(0, g, N_SLOTS, 4)
+perm = np.random.default_rng(0).permutation(N_SLOTS).astype(np.int32)
 keep, specs, items = [], [], []
 digest = torch.zeros((4, L), dtype=torch.int64, device="cuda:0")
 for i in range(4):
@@ -38,7 +39,7 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / L
 macs = 4 * 128 * T * 429 * B
-print(f"K5 per layer: {ms:.3f} ms, {macs / ms / 1e9:.2f} TMAC/s "
+print(f"[{N_SLOTS} pool slots] K5 per layer: {ms:.3f} ms, {macs / ms / 1e9:.2f} TMAC/s "
       f"({4 * 128 * T * B * 7 / ms / 1e6:.1f} GB/s of key-tile reads incl. 7 query tiles)")
 pool.close()
 st.close()
