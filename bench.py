@@ -72,8 +72,9 @@ def parse():
     ap.add_argument("--io-threads", type=int, default=8, help="storage tier: host IO threads per engine")
     ap.add_argument("--k2", default="sm", choices=["sm", "ce"],
                     help="DE-path loads: sm = K2 gather pushing over NVLink, ce = the DE's copy engine")
-    ap.add_argument("--k1", default="sm", choices=["sm", "ce"],
-                    help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs)")
+    ap.add_argument("--k1", default="sm", choices=["sm", "ce", "hybrid"],
+                    help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs), "
+                         "hybrid = both at once, jobs split by bytes")
     return ap.parse_args()
 
 
@@ -311,7 +312,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
         opt.storage_cap_per_engine = caps
     if args.online > 0:
         opt.pace_scale = 1.0
-    opt.k1_mode = 1 if args.k1 == "ce" else 0
+    opt.k1_mode = {"sm": 0, "ce": 1, "hybrid": 2}[args.k1]
     opt.k2_mode = 1 if args.k2 == "ce" else 0
     opt.handoff = bool(args.handoff or args.persist)
     opt.persist = bool(args.persist)

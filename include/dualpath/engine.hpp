@@ -46,7 +46,8 @@ struct ExecOptions {
   std::int64_t pool_bytes_max = 120LL << 30;
   std::int32_t wait_timeout_ms = 30000;
   // PE-path loads (K1): 0 = SM gather kernel, 1 = copy engine (no SMs: the
-  // isolation mode while the PE computes, and the faster PCIe read path)
+  // isolation mode while the PE computes), 2 = both at once, jobs split by
+  // bytes (the plain load path; the two read paths together beat either)
   std::int32_t k1_mode = 0;
   // DE-path loads (K2): 0 = SM gather pushing over NVLink, 1 = the DE's copy
   // engine writing into the PE pool (no SMs on the DE: its decode is untouched)
@@ -316,6 +317,8 @@ class EngineRuntime {
   void enqueue_forward(int f, StepResult& res);
   void upload_prefill_tables();
   void* stream_c_ = nullptr;                // PE: the compute stream (forwards)
+  void* stream_ce_ = nullptr;               // PE, k1_mode 2: the copy-engine share of K1
+  std::vector<void*> ev_ce_;
   std::vector<void*> ev_fwd_;               // PE: per forward, recorded after its last layer
   std::vector<std::vector<dp_attend_item>> fwd_att_;  // PE: per forward, K5 items
   std::vector<std::int64_t> fwd_wait_off_;  // PE: per forward, offset of its KV waits in d_wt_

@@ -333,3 +333,28 @@ def test_two_engines_k2_on_copy_engine(two_gpus):
         dp.run_step_all([pe, de])
         verify_counters(pe, xp, cfg)
         verify_pool(pe, xp, cfg)
+
+
+@pytest.mark.parametrize("tight", [False, True])
+def test_k1_hybrid_sm_and_copy_engine(gpus, tight):
+    """k1_mode 2: the PE's jobs split between the SM gather and the copy
+    engine on two streams; a tight pool makes slot reuse cross the streams."""
+    cfg = cluster(1, 1, L=4)
+    trajs = small_trace(count=6, turns=6)
+    planned = dp.plan(cfg, trajs, policy="pe_only", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.k1_mode = 2
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    if tight:
+        opt.pool_slots = xp.peak_slots
+        xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+        assert any(job[12] for job in xp.jobs())
+    eng = dp.EngineRuntime(xp, 0, 0)
+    for _ in range(2):
+        eng.reset_counters()
+        r = eng.run_step()
+        assert r.bytes_read == xp.hit_bytes
+        assert 0 < r.launches < len(xp.jobs())  # some jobs went to the copy engine
+    verify_counters(eng, xp, cfg)
+    verify_pool(eng, xp, cfg)
