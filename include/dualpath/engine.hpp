@@ -234,6 +234,8 @@ struct StepResult {
   std::int64_t d2h_bytes = 0;   // result read back (PE: landed-counter column)
 };
 
+class TierReader;
+
 class EngineRuntime {
  public:
   EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, int device);
@@ -329,6 +331,7 @@ class EngineRuntime {
   std::uint32_t* d_fwg_ = nullptr;
   std::int32_t* d_fwd_slot_ = nullptr;
   // ---- storage tier ----
+  friend class TierReader;
   std::unique_ptr<FullBlockFile> tier_file_;
   std::vector<void*> ev_job_;               // per job in by_reader order: after its launch
   std::vector<std::vector<int>> ring_wait_local_;  // ring_waits as by_reader positions

@@ -4,6 +4,7 @@
 // engine_handoff.cpp.
 #include "dualpath/engine.hpp"
 #include "engine_detail.hpp"
+#include "tier_reader.hpp"
 
 #include <cuda_runtime.h>
 
@@ -319,77 +320,9 @@ StepResult EngineRuntime::run_step() {
   double sm_bytes = 0, ce_bytes = 0;
   if (hybrid) check_cuda(cudaStreamWaitEvent(sc, static_cast<cudaEvent_t>(ev_start_), 0), "cudaStreamWaitEvent");
 
-  // Storage tier: IO threads read each job's Full Blocks from the file into
-  // its staging-ring positions, in job order (first reusing a position only
-  // after the transfer that read it is done); a job is launched once read.
-  struct Io {
-    std::mutex mu;
-    std::condition_variable cv;
-    std::vector<char> read, launched;
-    std::atomic<int> next{0};
-    bool failed = false;
-    std::exception_ptr err;
-  } io;
-  std::vector<std::thread> workers;
-  char* staging = nullptr;
-  if (x.tier && !mine.empty()) {
-    void* host = nullptr;
-    check(dp_store_info(store_, &host, nullptr, nullptr), "dp_store_info");
-    staging = static_cast<char*>(host);
-    io.read.assign(mine.size(), 0);
-    io.launched.assign(mine.size(), 0);
-    const std::int64_t fbb = x.cfg.full_block_bytes();
-    const int dev = device_;
-    for (int t = 0; t < x.opt.io_threads; ++t)
-      workers.emplace_back([&, fbb, dev] {
-        try {
-          cudaSetDevice(dev);
-          for (int i = io.next++; i < static_cast<int>(mine.size()); i = io.next++) {
-            for (int w : ring_wait_local_[i]) {
-              {
-                std::unique_lock<std::mutex> lk(io.mu);
-                io.cv.wait(lk, [&] { return io.launched[w] || io.failed; });
-                if (io.failed) return;
-              }
-              check_cuda(cudaEventSynchronize(static_cast<cudaEvent_t>(ev_job_[w])), "ring reuse wait");
-            }
-            // one read per run of blocks consecutive both in the file and in
-            // the ring (a session's pages are consecutive records)
-            const LoadJob& j = x.jobs[mine[i]];
-            const std::int64_t* rec = x.tier_rec[engine_].data() + j.blk_off;
-            const std::int64_t* pos = x.src_fb[engine_].data() + j.blk_off;
-            constexpr std::int32_t kMaxRun = 8;  // 18 MB of DS-V3 Full Blocks per read
-            for (std::int32_t k = 0; k < j.n_blk;) {
-              std::int32_t run = 1;
-              while (k + run < j.n_blk && run < kMaxRun && rec[k + run] == rec[k] + run && pos[k + run] == pos[k] + run)
-                ++run;
-              tier_file_->read_run(rec[k], run, staging + pos[k] * fbb);
-              k += run;
-            }
-            std::lock_guard<std::mutex> lk(io.mu);
-            io.read[i] = 1;
-            io.cv.notify_all();
-          }
-        } catch (...) {
-          std::lock_guard<std::mutex> lk(io.mu);
-          if (!io.err) io.err = std::current_exception();
-          io.failed = true;
-          io.cv.notify_all();
-        }
-      });
-  }
-  struct JoinWorkers {
-    Io& io;
-    std::vector<std::thread>& w;
-    ~JoinWorkers() {
-      {
-        std::lock_guard<std::mutex> lk(io.mu);
-        io.failed = true;  // releases any worker still waiting (normal exit: all done)
-        io.cv.notify_all();
-      }
-      for (auto& t : w) t.join();
-    }
-  } join_workers{io, workers};
+  // Storage tier: IO threads stage each job's Full Blocks (TierReader)
+  std::unique_ptr<TierReader> tier;
+  if (x.tier && !mine.empty()) tier = std::make_unique<TierReader>(*this, mine);
 
   auto flush = [&]() {
     if (batch.empty()) return;
@@ -416,12 +349,7 @@ StepResult EngineRuntime::run_step() {
       res.launches += (static_cast<std::int64_t>(batch.size()) + DP_MAX_JOBS_PER_LAUNCH - 1) /
                       DP_MAX_JOBS_PER_LAUNCH;
     batch.clear();
-    if (staging) {
-      for (int i : batch_jobs) check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_job_[i]), s), "cudaEventRecord");
-      std::lock_guard<std::mutex> lk(io.mu);
-      for (int i : batch_jobs) io.launched[i] = 1;
-      io.cv.notify_all();
-    }
+    if (tier) tier->launched(batch_jobs, s);
     batch_jobs.clear();
   };
   auto flush_ce = [&]() {
@@ -465,20 +393,9 @@ StepResult EngineRuntime::run_step() {
       std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
       res.spans.push_back({begin, gate_s, bytes});
     }
-    if (staging) {  // StorageRead: the job's Full Blocks must be in staging
-      bool ready;
-      {
-        std::lock_guard<std::mutex> lk(io.mu);
-        ready = io.read[i] || io.failed;
-      }
-      if (!ready) {
-        flush();  // never hold launched work while waiting on the disk
-        const auto w0 = std::chrono::steady_clock::now();
-        std::unique_lock<std::mutex> lk(io.mu);
-        io.cv.wait(lk, [&] { return io.read[i] || io.failed; });
-        res.io_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
-      }
-      if (io.err) std::rethrow_exception(io.err);
+    if (tier && !tier->ready(static_cast<int>(i))) {  // StorageRead: the job's Full Blocks in staging
+      flush();  // never hold launched work while waiting on the disk
+      res.io_wait_ms += tier->wait(static_cast<int>(i));
     }
     if (hazard) {
       const std::int64_t off = pred_off_[i];

@@ -4,10 +4,12 @@
 
 #include <algorithm>
 #include <chrono>
+#include <memory>
 #include <thread>
 
 #include "dualpath/engine.hpp"
 #include "engine_detail.hpp"
+#include "tier_reader.hpp"
 
 namespace dualpath {
 
@@ -102,6 +104,10 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
     for (const FwdItem& it : x.fwd_items[engine_]) job_of_row[it.row] = it.job;
     const bool k1_ce = x.opt.k1_mode == 1;
     std::vector<dp_job> batch;
+    std::vector<int> batch_jobs;  // by_reader positions (the storage tier's job ids)
+    std::unique_ptr<TierReader> tier;
+    if (x.tier && !x.by_reader[engine_].empty()) tier = std::make_unique<TierReader>(*this, x.by_reader[engine_]);
+    int li = 0;  // by_reader position of the next own load
     auto flush = [&]() {
       if (batch.empty()) return;
       const auto n = static_cast<int32_t>(batch.size());
@@ -112,6 +118,8 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
         res.launches += (n + DP_MAX_JOBS_PER_LAUNCH - 1) / DP_MAX_JOBS_PER_LAUNCH;
       }
       batch.clear();
+      if (tier) tier->launched(batch_jobs, s);
+      batch_jobs.clear();
     };
     const double cap = x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
                                                             : x.opt.storage_cap_per_engine[engine_];
@@ -130,10 +138,16 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
       const LoadJob& j = x.jobs[ji];
       const std::int64_t bytes = j.cached * x.cfg.kv_bytes_per_token();
       const bool gated = cap > 0 || pace > 0;
+      const int pos = li++;
       // loads run ahead of the forwards (the compute stream's queue may be
       // long); they stop only for a slot reuse, whose reader forward must be
-      // enqueued first, and for the storage gate, which lets the forwards
-      // that are ready start before the host sleeps
+      // enqueued first, and for the storage gate or a read still on the disk,
+      // which let the forwards that are ready start before the host waits
+      if (tier && !tier->ready(pos)) {
+        forwards_before(r);
+        flush();
+        res.io_wait_ms += tier->wait(pos);
+      }
       if (gated || !j.consumer_waits.empty()) forwards_before(r);
       if (gated || !j.consumer_waits.empty() || batch.size() == DP_MAX_JOBS_PER_LAUNCH) flush();
       for (int w : j.consumer_waits)
@@ -150,6 +164,7 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
                                j.cached, j.n_blk, 0, L, j.ticket});
       else
         batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket});
+      batch_jobs.push_back(pos);
       res.bytes_read += bytes;
       ++res.jobs;
     }

@@ -262,8 +262,8 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
   if (x.prefill && !(opt.compute_quota > 0))
     throw std::invalid_argument("build_exec_plan: compute_quota must be > 0");
   x.tier = !opt.tier_path.empty();
-  if (x.tier && (x.handoff || x.prefill))
-    throw std::invalid_argument("build_exec_plan: the storage tier runs on the plain load path");
+  if (x.tier && x.handoff)
+    throw std::invalid_argument("build_exec_plan: the storage tier runs on the load and prefill paths, not the handoff");
   if (x.tier && opt.io_threads < 1) throw std::invalid_argument("build_exec_plan: io_threads must be >= 1");
   x.n_engines = cfg.total_engines();
   x.n_pe = cfg.prefill_nodes * cfg.engines_per_node;

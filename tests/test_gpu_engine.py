@@ -358,3 +358,40 @@ def test_k1_hybrid_sm_and_copy_engine(gpus, tight):
         assert 0 < r.launches < len(xp.jobs())  # some jobs went to the copy engine
     verify_counters(eng, xp, cfg)
     verify_pool(eng, xp, cfg)
+
+
+def test_edge_cold_only_plan(gpus):
+    """Every request cold (first turns only): no hit KV, no jobs; the step
+    runs and moves nothing."""
+    cfg = cluster(1, 1)
+    trajs = small_trace(count=5, turns=1)
+    planned = dp.plan(cfg, trajs, policy="pe_only", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert xp.hit_bytes == 0 and len(xp.jobs()) == 0
+    eng = dp.EngineRuntime(xp, 0, 0)
+    eng.reset_counters()
+    r = eng.run_step()
+    assert r.bytes_read == 0 and r.jobs == 0
+
+
+def test_edge_128k_context(gpus):
+    """One 128K-token context (2048 Full Blocks per layer per request): the
+    largest BASELINE config-2 request, loaded and checked block by block."""
+    cfg = cluster(1, 1, L=2)
+    t = dp.Trajectory()
+    t.id = "long"
+    t.rounds = [dp.Round(131071, 1), dp.Round(429, 1)]
+    planned = dp.plan(cfg, [t], policy="pe_only", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    xp = dp.build_exec_plan(cfg, [t], planned, opt)
+    jobs = xp.jobs()
+    assert len(jobs) == 1 and jobs[0][6] == 131072 and jobs[0][7] == 2048
+    eng = dp.EngineRuntime(xp, 0, 0)
+    eng.reset_counters()
+    r = eng.run_step()
+    assert r.bytes_read == xp.hit_bytes == 131072 * 2 * 576
+    verify_counters(eng, xp, cfg)
+    verify_pool(eng, xp, cfg)

@@ -95,3 +95,29 @@ def test_tier_missing_file_fails_loudly(gpus, tmp_path):
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     with pytest.raises(RuntimeError):
         dp.EngineRuntime(xp, 0, 0)
+
+
+def test_tier_with_prefill(gpus, tmp_path):
+    """StorageRead from the file feeding the quota-batched forwards: the K5
+    digests equal the oracle's (a tight ring: reads wait on earlier loads)."""
+    from test_gpu_prefill import check_digests, COST
+    cfg = cluster(1, 1)
+    trajs = dp.synthesize(max_len=12000, count=8, seed=4, mean_turns=5, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="pe_only", **SB)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.tier_path = str(tmp_path / "tier.bin")
+    opt.io_threads = 4
+    opt.prefill, opt.compute_quota, opt.prefill_cost = True, 5e-4, COST
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.tier_ring_fb = max(j[7] for j in xp.jobs())
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    f = dp.FullBlockFile(opt.tier_path, cfg.n_layer, cfg.block_size_tokens,
+                         cfg.kv_bytes_per_token_per_layer, xp.store_fb, create=True)
+    f.populate(SEED, threads=4)
+    eng = dp.EngineRuntime(xp, 0, 0)
+    for _ in range(2):
+        eng.reset_counters()
+        r = eng.run_step()
+        assert r.forwards == len(xp.forwards(0)) and r.bytes_read == xp.hit_bytes
+        check_digests(eng, cfg, planned, xp)

@@ -141,3 +141,5 @@ def test_tier_plan_rejects_bad_configs():
     opt.handoff = True
     with pytest.raises(ValueError):
         dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.handoff, opt.prefill = False, True  # the tier feeds the prefill path
+    assert dp.build_exec_plan(cfg, trajs, planned, opt).tier
