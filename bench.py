@@ -104,7 +104,7 @@ def workload(args, n_gpus):
     return trajs, shape
 
 
-def cluster(shape, P, D, cap_bps, caps=None):
+def cluster(shape, P, D, cap_bps, caps=None, link_bps=PCIE_ZC_BPS):
     import paper_2602_21548_b200 as dp
     cfg = dp.ClusterConfig()
     if caps:
@@ -114,7 +114,7 @@ def cluster(shape, P, D, cap_bps, caps=None):
     # compute network = NVLink (the DE->PE push), storage NIC = the engine's
     # PCIe read rate, or the emulated cap when one is set
     cfg.cnic_bandwidth = NVLINK_BPS
-    cfg.storage_multiple = (cap_bps if cap_bps > 0 else PCIE_ZC_BPS) / NVLINK_BPS
+    cfg.storage_multiple = (cap_bps if cap_bps > 0 else link_bps) / NVLINK_BPS
     cfg.dram_bandwidth = 2e12
     cfg.hbm_capacity_tokens = 100_000_000
     cfg.pe_buffer_bytes = 1 << 42
@@ -236,6 +236,50 @@ def measure_concurrent_h2d(dist, device, reps=3):
     return best
 
 
+def measure_host_ceiling_local(n, reps=3):
+    """One process driving GPUs 0..n-1 at once: copy-engine H2D of 1 GiB pinned
+    x 4 per GPU on its own stream.  The same aggregate host-link ceiling as
+    measure_concurrent_h2d, for the reference arm (rank 0 alone)."""
+    import torch
+    size = 1 << 30
+    bufs = []
+    for d in range(n):
+        with torch.cuda.device(d):
+            bufs.append((torch.empty(size, dtype=torch.uint8, pin_memory=True),
+                         torch.empty(size, dtype=torch.uint8, device=f"cuda:{d}"),
+                         torch.cuda.Stream(device=d)))
+    best = 0.0
+    for _ in range(reps):
+        for d in range(n):
+            torch.cuda.synchronize(d)
+        evs = []
+        for d, (h, dv, st) in enumerate(bufs):
+            with torch.cuda.device(d), torch.cuda.stream(st):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                for _ in range(4):
+                    dv.copy_(h, non_blocking=True)
+                b.record(st)
+                evs.append((a, b))
+        ms = 0.0
+        for a, b in evs:
+            b.synchronize()
+            ms = max(ms, a.elapsed_time(b))
+        best = max(best, n * 4 * size / (ms * 1e-3))
+    del bufs
+    return best
+
+
+def link_per_engine(ceiling_bps, n):
+    """The storage-read rate one engine can sustain on this box: the SM
+    zero-copy rate, or its share of the box's concurrent host-link ceiling
+    when all engines read at once (some boxes cap 4 GPUs at 116-152 GB/s)."""
+    if not ceiling_bps or n <= 1:
+        return PCIE_ZC_BPS
+    return min(PCIE_ZC_BPS, ceiling_bps / n)
+
+
 def measure_k1(device, shape, target_bytes=18421383168):
     """The dominant kernel alone, live: one K1 launch (DS-V3 or Qwen Layer
     Blocks, 8K-token requests, random Full Blocks and slots) through the C
@@ -289,7 +333,7 @@ def prefill_cost(args, shape):
     return (shape["b"] / (args.attend_tops * 1e12), 0.0, 0.0, 20e-6)
 
 
-def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=None):
+def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=None, link_bps=PCIE_ZC_BPS):
     """Plan, build engines, run W + K steps; returns per-step max-over-ranks
     device and host times, plus per-rank info.  variant = (policy, sched_mode)."""
     import paper_2602_21548_b200 as dp
@@ -298,7 +342,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     caps = [float(x) * 1e9 for x in args.caps.split(",")] if args.caps else None
     if caps and len(caps) != P + D:
         raise SystemExit(f"--caps needs {P + D} entries")
-    cfg = cluster(shape, P, D, cap, caps)
+    cfg = cluster(shape, P, D, cap, caps, link_bps)
     kw = dict(PLAN_KW)
     if args.online > 0:
         # Poisson arrivals (desim.cpp:1036-1051); SLO / steady-state stops off
@@ -493,7 +537,10 @@ def reference_arm(args):
     if args.pd:
         P, D = (int(x) for x in args.pd.split(":"))
     cap = args.cap_gbps * 1e9
-    cfg = cluster(shape, P, D, cap)
+    # the same per-engine link rate our arm plans with on this box
+    ceiling = measure_host_ceiling_local(n) if n > 1 else None
+    link_bps = link_per_engine(ceiling, n)
+    cfg = cluster(shape, P, D, cap, None, link_bps)
     sample = trajs[: max(2, min(len(trajs), 4 * n))]
     path = f"/tmp/dp_ref_sample_{os.getpid()}.tsv"
     dp.save_trace(path, sample)
@@ -525,7 +572,11 @@ def reference_arm(args):
                                        f"(the reference simulator, 1 thread); value = its storage-read "
                                        f"bytes / makespan; {statistics.median(walls):.2f} s wall per run"},
             "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "reference_wall_s_per_run": round(statistics.median(walls), 3)}
+            "reference_wall_s_per_run": round(statistics.median(walls), 3),
+            "link_model": {"per_engine_gbps": round(link_bps / 1e9, 2),
+                           "concurrent_h2d_gbps": round(ceiling / 1e9, 2) if ceiling else None,
+                           "what": "the reference simulator's storage rate per engine: the same "
+                                   "min(51.5, box ceiling / N) our arm plans with"}}
 
 
 def storage_balance(spans, caps, n_engines, width=0.05, window=4):
@@ -588,14 +639,21 @@ def main():
     peak = None
     if dist.rank == 0:
         peak = measure_pcie_peak(dist.local if dist.world > 1 else 0)
+    # the box's aggregate host-link ceiling, measured before planning: the
+    # planner (the reference's model) then uses the per-engine rate this box
+    # actually sustains when every engine reads
+    concurrent = measure_concurrent_h2d(dist, dist.local) if dist.world > 1 else None
+    link_bps = link_per_engine(concurrent, n)
     results = {}
     clocks = ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
                           if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_{os.getpid()}.csv")
     for name, var in zip(policies, variants):
         results[name] = run_policy(args, dist, var, trajs, shape, P, D,
-                                   clocks if (name == policies[0] and dist.local == 0) else None)
+                                   clocks if (name == policies[0] and dist.local == 0) else None,
+                                   link_bps=link_bps)
     if args.prefill:  # the same loads without the prefill: the overlap baseline
-        results["load_only"] = run_policy(args, dist, variants[0], trajs, shape, P, D, None, prefill=False)
+        results["load_only"] = run_policy(args, dist, variants[0], trajs, shape, P, D, None, prefill=False,
+                                          link_bps=link_bps)
     head = results[policies[0]]
     info = head["info"]
     dev_s = sum(head["dev_ms"]) / 1e3
@@ -611,9 +669,6 @@ def main():
         except Exception as exc:  # reported, never fatal to the GPU number
             cpu = {"error": str(exc)[:200]}
     clk = clocks.summary(set(range(n)))
-    concurrent = None
-    if dist.world > 1:
-        concurrent = measure_concurrent_h2d(dist, dist.local)
     k1 = None
     if dist.rank == 0:
         k1 = measure_k1(dist.local if dist.world > 1 else 0, shape)
@@ -666,8 +721,10 @@ def main():
             "clocks": clk,
             "host_links": ({"concurrent_h2d_gbps": round(concurrent / 1e9, 2),
                             "value_frac": round(value / (concurrent / 1e9), 4),
+                            "per_engine_model_gbps": round(link_bps / 1e9, 2),
                             "what": "all ranks' copy-engine H2D at once: the box's aggregate host-link "
-                                    "ceiling for this line"} if concurrent else None),
+                                    "ceiling for this line; the planner's per-engine storage rate is "
+                                    "min(51.5, ceiling / N)"} if concurrent else None),
             "plan_s": round(info["plan_s"], 2),
         }
         if args.online > 0:
