@@ -133,6 +133,9 @@ PYBIND11_MODULE(_core, m) {
       .def("kv_bytes_per_token", &ClusterConfig::kv_bytes_per_token)
       .def("layer_block_bytes", &ClusterConfig::layer_block_bytes)
       .def("full_block_bytes", &ClusterConfig::full_block_bytes)
+      .def("node_storage_bandwidth",
+           [](const ClusterConfig& c, int node) { return node < 0 ? c.node_storage_bandwidth() : c.node_storage_bandwidth(node); },
+           py::arg("node") = -1)
       .def("total_engines", &ClusterConfig::total_engines);
 
   py::class_<Round>(m, "Round")

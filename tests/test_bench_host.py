@@ -1,0 +1,64 @@
+"""Host-side logic of bench.py (CPU): the workloads, the link model, the
+storage-balance metric and the reference arm's configuration."""
+
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+import paper_2602_21548_b200 as dp  # noqa: E402
+
+
+class Args:
+    sessions_per_gpu = 2
+    workload = "c1"
+
+
+def test_link_model():
+    # one engine, or a box whose host links outrun the engines: the SM rate
+    assert bench.link_per_engine(None, 4) == bench.PCIE_ZC_BPS
+    assert bench.link_per_engine(55.6e9, 1) == bench.PCIE_ZC_BPS
+    assert bench.link_per_engine(220e9, 4) == bench.PCIE_ZC_BPS
+    # a shared host ceiling: its share per engine
+    assert bench.link_per_engine(116e9, 4) == pytest.approx(29e9)
+
+
+@pytest.mark.parametrize("wl,L,b", [("c1", 61, 576), ("c3", 64, 4096), ("c2", 61, 576)])
+def test_workloads_and_cluster(wl, L, b):
+    a = Args()
+    a.workload = wl
+    trajs, shape = bench.workload(a, 2)
+    assert len(trajs) == 4 and shape["L"] == L and shape["b"] == b
+    cfg = bench.cluster(shape, 1, 1, 0.0, None, 29e9)
+    cfg.validate()
+    assert cfg.node_storage_bandwidth() == pytest.approx(29e9)
+    capped = bench.cluster(shape, 1, 1, 6.25e9)
+    assert capped.node_storage_bandwidth() == pytest.approx(6.25e9)
+    asym = bench.cluster(shape, 1, 1, 0.0, [6.25e9, 3.125e9])
+    assert asym.node_storage_bandwidth(1) == pytest.approx(3.125e9)
+
+
+def test_c1_is_the_baseline_generator():
+    # BASELINE config 1: 20 turns, append 429, gen 500, ~95 % token-weighted hit
+    a = Args()
+    a.sessions_per_gpu = 64
+    trajs, _ = bench.workload(a, 1)
+    assert all(len(t.rounds) == 20 for t in trajs)
+    hit = sum(dp.context_before(t, r) for t in trajs for r in range(len(t.rounds)))
+    prompt = sum(dp.context_before(t, r) + t.rounds[r].append_tokens for t in trajs for r in range(len(t.rounds)))
+    assert 0.94 < hit / prompt < 0.97
+
+
+def test_storage_balance_metric():
+    # two engines, one reads twice the other's bytes in every window
+    spans = {0: [(0.0, 1.0, 2_000_000)], 1: [(0.0, 1.0, 1_000_000)]}
+    res = bench.storage_balance(spans, None, 2, width=0.1, window=2)
+    assert res["bytes_max_avg"] == pytest.approx(2 / 1.5, abs=1e-4)  # rounded to 4 places
+    # normalised by caps 2:1 the utilisation is balanced
+    res = bench.storage_balance(spans, [2.0, 1.0], 2, width=0.1, window=2)
+    assert res["utilisation_max_avg"] == pytest.approx(1.0, abs=1e-4)
+    assert bench.storage_balance({}, None, 2) is None
