@@ -180,6 +180,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ distributed
+def my_device(dist):
+    """This rank's GPU: its local rank (one process per GPU).  More ranks than
+    GPUs (a control-plane rehearsal of a larger N) wrap around."""
+    import torch
+    return (dist.local if dist.world > 1 else 0) % max(1, torch.cuda.device_count())
+
+
 def make_group(n):
     from paper_2602_21548_b200 import dist as dpdist
     g = dpdist.Group("nccl")
@@ -243,6 +250,7 @@ def measure_host_ceiling_local(n, reps=3):
     import torch
     size = 1 << 30
     bufs = []
+    n = min(n, torch.cuda.device_count())
     for d in range(n):
         with torch.cuda.device(d):
             bufs.append((torch.empty(size, dtype=torch.uint8, pin_memory=True),
@@ -409,7 +417,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
         my = [0]  # N=1: only the PE engine exists on this box
     engines = {}
     for e in my:
-        dev = dist.local if dist.world > 1 else 0
+        dev = my_device(dist)
         engines[e] = dp.EngineRuntime(xp, e, dev)
     if dist.world > 1:
         dpdist.connect_pools(dist, engines, cfg.prefill_nodes)
@@ -638,11 +646,11 @@ def main():
     policies = [v[0] if v[1] == "adaptive" else v[1] for v in variants]
     peak = None
     if dist.rank == 0:
-        peak = measure_pcie_peak(dist.local if dist.world > 1 else 0)
+        peak = measure_pcie_peak(my_device(dist))
     # the box's aggregate host-link ceiling, measured before planning: the
     # planner (the reference's model) then uses the per-engine rate this box
     # actually sustains when every engine reads
-    concurrent = measure_concurrent_h2d(dist, dist.local) if dist.world > 1 else None
+    concurrent = measure_concurrent_h2d(dist, my_device(dist)) if dist.world > 1 else None
     link_bps = link_per_engine(concurrent, n)
     results = {}
     clocks = ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
@@ -671,7 +679,7 @@ def main():
     clk = clocks.summary(set(range(n)))
     k1 = None
     if dist.rank == 0:
-        k1 = measure_k1(dist.local if dist.world > 1 else 0, shape)
+        k1 = measure_k1(my_device(dist), shape)
     if dist.rank == 0:
         # roofline of the dominant kernel, K1 (K2 is the same kernel body with
         # peer stores, 0.999x its rate, profiles/r01_k1_k2_events.json),
