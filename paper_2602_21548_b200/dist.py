@@ -35,11 +35,16 @@ class Group:
         if self.world > 1:
             import torch
             import torch.distributed as td
-            if backend == "nccl":
+            n_dev = torch.cuda.device_count() if backend == "nccl" else 0
+            if backend == "nccl" and self.local < n_dev:
                 torch.cuda.set_device(self.local)
                 td.init_process_group("nccl", device_id=torch.device(f"cuda:{self.local}"))
             else:
-                td.init_process_group(backend or "gloo")
+                # more ranks than GPUs (a rehearsal of a larger N): NCCL
+                # cannot put two ranks on one GPU; the control plane is gloo
+                if backend == "nccl" and n_dev:
+                    torch.cuda.set_device(self.local % n_dev)
+                td.init_process_group("gloo")
             self.td = td
 
     def barrier(self):
