@@ -392,3 +392,15 @@ def test_prefill_with_handoff_keeps_k3_after_forwards(P, D, tight):
             assert set(jobs[i][20]) <= set(xp.consumer_waits(i))
     if tight:
         assert n_waits > 0
+
+
+def test_prefill_quota_infeasible_propagates():
+    # a quota below a 1-token chunk of some request: the reference's
+    # QuotaInfeasibleError (scheduler.cpp:203-206) reaches the caller
+    cfg = cluster(1, 1)
+    trajs = dp.synthesize(max_len=20000, count=4, seed=8, mean_turns=4, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **SB)
+    opt = dp.ExecOptions()
+    opt.prefill, opt.compute_quota, opt.prefill_cost = True, 1e-6, (1e-9, 0.0, 0.0, 1e-5)
+    with pytest.raises(dp.QuotaInfeasibleError):
+        dp.build_exec_plan(cfg, trajs, planned, opt)
