@@ -16,6 +16,16 @@
  *                            (desim.cpp:623-628)
  *   dp_pool_*             <- the PE HBM KV pool (paged; not modelled by the reference,
  *                            SPEC.md:106) and BlockRef layer_block (types.cpp:62-71)
+ *   dp_h2d_layer_copy     <- LoopbackH2D on the copy engine; dp_h2d_push_copy <- DeToPe
+ *                            on the DE's copy engine (same Stages, no SMs)
+ *   dp_h2d_push_p2p_dual  <- DeToPe fused with the hit half of DecodeH2D
+ *                            (desim.cpp:617-619, :650-651)
+ *   dp_prefill_handoff    <- Stage::PeToDe / Stage::MissMerge per layer (desim.cpp:630-640)
+ *   dp_decode_fill,       <- Decode (stand-in) and Stage::PersistD2H, every 64 generated
+ *   dp_persist_d2h           tokens + the final partial (desim.cpp:666-672, :690-693)
+ *   dp_prefill_attend     <- Stage::LayerCompute of a forward batch
+ *                            (layer_time desim.cpp:576-579; build_forward_batch
+ *                            scheduler.cpp:174-219)
  *
  * Conventions (no exceptions cross this ABI):
  *   - every call returns int: 0 = ok, < 0 = dp_status error code;
