@@ -70,6 +70,7 @@ def parse():
                     help="storage tier: StorageRead reads every Full Block from this file (created "
                          "and populated once per box; O_DIRECT) through a pinned staging ring")
     ap.add_argument("--io-threads", type=int, default=8, help="storage tier: host IO threads per engine")
+    ap.add_argument("--wait-timeout-ms", type=int, default=30000, help="watchdog of every cross-engine wait")
     ap.add_argument("--k2", default="sm", choices=["sm", "ce"],
                     help="DE-path loads: sm = K2 gather pushing over NVLink, ce = the DE's copy engine")
     ap.add_argument("--k1", default="sm", choices=["sm", "ce", "hybrid"],
@@ -366,6 +367,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
         opt.pace_scale = 1.0
     opt.k1_mode = {"sm": 0, "ce": 1, "hybrid": 2}[args.k1]
     opt.k2_mode = 1 if args.k2 == "ce" else 0
+    opt.wait_timeout_ms = args.wait_timeout_ms
     opt.handoff = bool(args.handoff or args.persist)
     opt.persist = bool(args.persist)
     opt.handoff_ctas = args.handoff_ctas
