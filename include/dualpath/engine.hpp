@@ -126,8 +126,7 @@ struct LoadJob {
   std::vector<int> consumer_waits;  // jobs whose slots this one reuses: their last forward
                                     // must be done before this job's load writes
   std::int64_t fwd_off = 0;         // offset of its slots in the PE's forward slot table
-  int k3_after = -1;                // handoff + prefill: the last job (global order) of the
-                                    // forward after which this job's K3 runs
+  std::vector<int> de_pred_jobs;    // jobs whose decode slots this one reuses (global order)
   // ---- storage tier ----
   std::vector<int> ring_waits;      // jobs (same reader) whose staging positions this
                                     // job's reads overwrite: their transfer must be done
@@ -201,6 +200,8 @@ struct ExecPlan {
   std::vector<std::vector<int>> fwd_rows;        // per PE: request id of each digest row (FIFO)
   std::vector<std::vector<std::int32_t>> fwd_slot;  // per PE: slots of the jobs landing there
   std::vector<int> last_fwd;                     // per job: the forward (on its PE) that reads it last
+  // handoff + prefill: each DE's enqueue order; job j = a read, -1 - j = a decode
+  std::vector<std::vector<int>> de_order;
 
   // ---- storage tier ----
   bool tier = false;

@@ -524,6 +524,10 @@ PYBIND11_MODULE(_core, m) {
       .def("fwd_rows", [](const dualpath::ExecPlan& x, int pe) { return x.fwd_rows.at(pe); })
       .def("consumer_waits", [](const dualpath::ExecPlan& x, int job) { return x.jobs.at(job).consumer_waits; })
       .def("last_fwd", [](const dualpath::ExecPlan& x, int job) { return x.last_fwd.at(job); })
+      .def("de_order", [](const dualpath::ExecPlan& x, int e) {
+        return e < static_cast<int>(x.de_order.size()) ? x.de_order[e] : std::vector<int>{};
+      })
+      .def("de_pred_jobs", [](const dualpath::ExecPlan& x, int job) { return x.jobs.at(job).de_pred_jobs; })
       .def("fwd_slots", [](const dualpath::ExecPlan& x, int job) {
         const dualpath::LoadJob& j = x.jobs.at(job);
         const auto& t = x.fwd_slot.at(j.pe);

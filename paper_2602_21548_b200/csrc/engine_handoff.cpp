@@ -165,17 +165,28 @@ StepResult EngineRuntime::run_step_handoff() {
     // streams onto one hardware queue, a blocked wait never sits in front of
     // its own producer.
     const std::int64_t T = x.cfg.block_size_tokens;
-    std::size_t ri = 0, di = 0;
+    // With the prefill the order is the plan's (ExecPlan::de_order): a
+    // request's K3 follows forwards that may hold later requests, so global
+    // order alone is not enough.
+    std::size_t ri = 0, di = 0, oi = 0;
     const auto& reads = x.by_reader[engine_];
     const auto& decodes = x.by_de[engine_];
-    while (ri < reads.size() || (x.persist && di < decodes.size())) {
-      // with the prefill, a request's K3 (which its decode waits for) needs
-      // the loads of every request in its last forward: read those first
-      const auto decode_key = [&](int ji) { return std::max(ji, x.jobs[ji].k3_after); };
-      const bool take_read = ri < reads.size() &&
-                             (!x.persist || di >= decodes.size() || reads[ri] <= decode_key(decodes[di]));
+    const auto& order = x.prefill ? x.de_order[engine_] : std::vector<int>{};
+    while (x.prefill ? oi < order.size() : (ri < reads.size() || (x.persist && di < decodes.size()))) {
+      bool take_read;
+      int next_read = -1;
+      if (x.prefill) {
+        const int code = order[oi++];
+        take_read = code >= 0;
+        if (take_read) next_read = code;
+        else if (di >= decodes.size() || decodes[di] != -1 - code)
+          throw std::logic_error("run_step: DE order out of step with its decodes");
+      } else {
+        take_read = ri < reads.size() && (!x.persist || di >= decodes.size() || reads[ri] <= decodes[di]);
+        if (take_read) next_read = reads[ri++];
+      }
       if (take_read) {  // DE read path: dual gather
-        const int ji = reads[ri++];
+        const int ji = next_read;
         const LoadJob& j = x.jobs[ji];
         if (!peers_[j.pe]) throw std::runtime_error("run_step: PE " + std::to_string(j.pe) + " not attached");
         if (!j.pe_done_preds.empty()) {

@@ -163,10 +163,6 @@ void build_forwards(ExecPlan& x, const pdsim::desim::SimReport& plan) {
       }
       f.end = static_cast<std::int32_t>(x.fwd_items[p].size());
       x.forwards[p].push_back(f);
-      int last_job = -1;
-      for (std::int32_t i = f.begin; i < f.end; ++i) last_job = std::max(last_job, x.fwd_items[p][i].job);
-      for (std::int32_t i = f.begin; i < f.end; ++i)
-        if (x.fwd_items[p][i].job >= 0) x.jobs[x.fwd_items[p][i].job].k3_after = last_job;
       if (fb.chunked) {
         head_done = fb.consumed_whole == 0 ? head_done + fb.chunk_bsz : fb.chunk_bsz;
       } else {
@@ -219,6 +215,91 @@ void build_tier(ExecPlan& x, std::span<const pdsim::Trajectory> trajectories) {
         x.tier_rec[e].push_back(recs[k]);
       }
       head = (head + j.n_blk) % ring;
+    }
+  }
+}
+
+// The enqueue order of each DE in handoff + prefill mode.  A DE's reads and
+// decodes spin-wait on work of other engines, and a spin-wait at the head of
+// a hardware queue holds everything behind it, so each wait's producers that
+// run on this DE must be enqueued first:
+//   * the decode of j waits for K3(j), which follows j's PE forwards up to
+//     j's last one: this DE's reads of every request in those forwards first;
+//   * a read reusing decode slots of p waits for p's release: with
+//     persistence p's decode on this DE, without it K3(p) (p's forwards).
+// Reads of one PE's requests stay in global order, decodes in by_de order;
+// among ready operations the lowest job goes first (reads before decodes).
+// A plan with no such order is rejected rather than left to hang.
+void build_de_orders(ExecPlan& x) {
+  const int n_pe = x.n_pe;
+  // B[pe][f]: the largest job of forwards 0..f of the PE (their loads)
+  std::vector<std::vector<int>> upto(n_pe);
+  for (int p = 0; p < n_pe; ++p) {
+    int m = -1;
+    for (const Forward& f : x.forwards[p]) {
+      for (std::int32_t i = f.begin; i < f.end; ++i) m = std::max(m, x.fwd_items[p][i].job);
+      upto[p].push_back(m);
+    }
+  }
+  auto bound = [&](int j) {  // the loads K3(j) depends on: jobs of its PE up to this
+    const LoadJob& lj = x.jobs[j];
+    const int f = x.last_fwd[j];
+    return f < 0 ? -1 : upto[lj.pe][f];
+  };
+  x.de_order.assign(x.n_engines, {});
+  for (int d = x.n_pe; d < x.n_engines; ++d) {
+    std::vector<std::vector<int>> lists(n_pe);  // this DE's reads, per PE, global order
+    for (int ji : x.by_reader[d]) lists[x.jobs[ji].pe].push_back(ji);
+    std::vector<std::size_t> head(n_pe, 0);
+    // emitted reads of PE p with job <= b
+    auto reads_done_upto = [&](int p, int b) {
+      const auto& l = lists[p];
+      // lists are increasing: every element <= b must be before head
+      return head[p] >= l.size() || l[head[p]] > b;
+    };
+    const auto& decs = x.persist ? x.by_de[d] : std::vector<int>{};
+    std::vector<int> dec_pos(x.jobs.size(), -1);
+    for (std::size_t k = 0; k < decs.size(); ++k) dec_pos[decs[k]] = static_cast<int>(k);
+    std::size_t dh = 0;
+    const std::size_t total = x.by_reader[d].size() + decs.size();
+    auto& order = x.de_order[d];
+    order.reserve(total);
+    while (order.size() < total) {
+      int best = -1;
+      bool best_is_read = false;
+      for (int p = 0; p < n_pe; ++p) {
+        if (head[p] >= lists[p].size()) continue;
+        const int ji = lists[p][head[p]];
+        bool ready = true;
+        for (int q : x.jobs[ji].de_pred_jobs) {
+          if (x.persist) {
+            if (dec_pos[q] >= 0 && static_cast<std::size_t>(dec_pos[q]) >= dh) ready = false;
+          } else if (!reads_done_upto(x.jobs[q].pe, bound(q))) {
+            ready = false;
+          }
+        }
+        if (ready && (best < 0 || ji < best)) {
+          best = ji;
+          best_is_read = true;
+        }
+      }
+      if (dh < decs.size()) {
+        const int jd = decs[dh];
+        if (reads_done_upto(x.jobs[jd].pe, bound(jd)) && (best < 0 || jd < best)) {
+          best = jd;
+          best_is_read = false;
+        }
+      }
+      if (best < 0)
+        throw std::logic_error("build_exec_plan: no deadlock-free enqueue order for DE " + std::to_string(d) +
+                               " (handoff + prefill)");
+      if (best_is_read) {
+        ++head[x.jobs[best].pe];
+        order.push_back(best);
+      } else {
+        ++dh;
+        order.push_back(-1 - best);  // a decode
+      }
     }
   }
 }
@@ -425,6 +506,13 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
           throw std::logic_error("build_exec_plan: decode-slot predecessor is not earlier");
         if (std::find(j.de_preds.begin(), j.de_preds.end(), pj.de_ticket) == j.de_preds.end()) {
           j.de_preds.push_back(pj.de_ticket);
+          j.de_pred_jobs.push_back(prev);  // -> global position below
+          // with the prefill, the previous occupant is released after its
+          // last forward (K3 follows it): on the same PE the two must not
+          // share a forward
+          if (x.prefill && pj.pe == j.pe &&
+              std::find(j.consumer_waits.begin(), j.consumer_waits.end(), prev) == j.consumer_waits.end())
+            j.consumer_waits.push_back(prev);
           // with persistence the slot is free once the occupant is persisted
           // (its "persist done" row, resolved at run time, reads 1)
           j.de_pred_targets.push_back(x.persist ? 1u : x.de_total_items(pj));
@@ -451,6 +539,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     LoadJob j = std::move(jobs[old]);
     for (int& w : j.k3_waits) w = pos[w];
     for (int& w : j.consumer_waits) w = pos[w];
+    for (int& w : j.de_pred_jobs) w = pos[w];
     if (x.prefill) {
       if (j.reader != j.pe && !x.handoff)  // a DE load waits on the PE's "consumed" rows [n, 2n)
         for (int w : j.consumer_waits) {
@@ -496,6 +585,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     x.jobs.push_back(std::move(j));
   }
   if (x.prefill) build_forwards(x, plan);
+  if (x.prefill && x.handoff) build_de_orders(x);
   if (x.tier) build_tier(x, trajectories);
   return x;
 }

@@ -404,3 +404,52 @@ def test_prefill_quota_infeasible_propagates():
     opt.prefill, opt.compute_quota, opt.prefill_cost = True, 1e-6, (1e-9, 0.0, 0.0, 1e-5)
     with pytest.raises(dp.QuotaInfeasibleError):
         dp.build_exec_plan(cfg, trajs, planned, opt)
+
+
+@pytest.mark.parametrize("P,D,persist,cap", [(2, 2, True, 6.25e9), (2, 2, False, 6.25e9), (1, 3, True, 0),
+                                             (3, 1, True, 6.25e9)])
+def test_handoff_prefill_de_orders_respect_every_wait(P, D, persist, cap):
+    """Each DE's enqueue order puts every spin-wait after its producers on
+    that DE: a decode after this DE's reads of every request its K3 follows,
+    a read reusing decode slots after the previous occupant's decode (or, with
+    no persistence, after the reads its K3 follows)."""
+    cfg = cluster(P, D, cap=cap if cap else 6.25e9)
+    trajs = dp.synthesize(max_len=20000, count=6 * (P + D), seed=8, mean_turns=6, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **SB)
+    opt = dp.ExecOptions()
+    opt.handoff, opt.persist, opt.prefill = True, persist, True
+    opt.compute_quota, opt.prefill_cost = 2e-3, COST
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots  # tight: reuse everywhere
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    jobs = xp.jobs()
+    # the loads each job's K3 follows: jobs of its PE up to the largest job of
+    # its forwards 0..last
+    upto = {}
+    for pe in range(xp.n_pe):
+        m = -1
+        for fi, (_, items) in enumerate(xp.forwards(pe)):
+            m = max([m] + [it[1] for it in items])
+            upto[(pe, fi)] = m
+    bound = lambda j: upto[(jobs[j][4], xp.last_fwd(j))]
+    n_reuse = 0
+    for d in range(xp.n_pe, xp.n_engines):
+        order = xp.de_order(d)
+        assert sorted(c for c in order if c >= 0) == sorted(xp.by_reader(d))
+        assert [-1 - c for c in order if c < 0] == (xp.by_de(d) if persist else [])
+        pos = {("r", c) if c >= 0 else ("d", -1 - c): i for i, c in enumerate(order)}
+        reads = [c for c in order if c >= 0]
+        for i, c in enumerate(order):
+            if c < 0:  # decode of j
+                j = -1 - c
+                need = [y for y in reads if jobs[y][4] == jobs[j][4] and y <= bound(j)]
+                assert all(pos[("r", y)] < i for y in need)
+            else:
+                for p in xp.de_pred_jobs(c):
+                    n_reuse += 1
+                    if persist:
+                        assert pos[("d", p)] < i
+                    else:
+                        need = [y for y in reads if jobs[y][4] == jobs[p][4] and y <= bound(p)]
+                        assert all(pos[("r", y)] < i for y in need)
+    assert n_reuse > 0
