@@ -171,3 +171,16 @@ def test_extend_and_poisson_match_reference(tmp_path):
         assert dp.poisson_arrivals(rate, horizon, seed) == refpy.ref_poisson(rate, horizon, seed)
     with pytest.raises(ValueError):
         dp.derive_variant(dp.load_trace(src), 0.0, 1.0, 100)
+
+
+@pytest.mark.parametrize("L,T,b", [(2, 16, 64), (3, 64, 576), (1, 8, 208)])
+def test_attend_digest_column_sum_form_is_exact(L, T, b):
+    """The oracle of K5 computes sum_q sum_t dot(Q, K) as an inner product of
+    column sums; pin it against the literal double sum on small cases,
+    including partial blocks and a chunk starting mid-append."""
+    g = refpy.geom(L, T, b)
+    fbs = [5, 2, 9, 1]
+    for C, q0, bsz in [(1, 0, 1), (T + 3, 2, 5), (3 * T, 0, 17), (4 * T - 1, 11, 3)]:
+        for layer in range(L):
+            assert refpy.attend_digest(g, 9, fbs, C, 123, layer, q0, bsz) == \
+                refpy.attend_digest_bruteforce(g, 9, fbs, C, 123, layer, q0, bsz)
