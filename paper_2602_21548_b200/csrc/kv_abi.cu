@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <cstdint>
 #include <cstdio>
@@ -262,8 +263,9 @@ __global__ void kv_store_fill(uint64_t* dst, int64_t n_pairs, int64_t words_per_
 }
 
 constexpr int kMaxDevices = 64;
-int g_gather_ctas[kMaxDevices] = {};  // 0 = default
-int g_handoff_ctas[kMaxDevices] = {};  // 0 = default
+// per-device CTA caps (0 = default); set by one thread, read by launching ones
+std::atomic<int> g_gather_ctas[kMaxDevices] = {};
+std::atomic<int> g_handoff_ctas[kMaxDevices] = {};
 
 int sm_count(int device) {
   int n = 0;
@@ -304,7 +306,7 @@ struct dp_pool {
   bool owner = false;
   bool ipc_opened = false;
   int* err_host = nullptr;  // mapped pinned watchdog flag
-  uint32_t* att_ctr = nullptr;  // K5 work-queue counters {next unit, CTAs done} (lazy)
+  uint32_t* att_ctr = nullptr;  // K5 work-queue counters {next unit, CTAs done} (owner pools)
 };
 
 namespace {
@@ -334,7 +336,7 @@ int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_
   p.n_layer = g.n_layer;
   p.block_tokens = g.block_tokens;
   p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
-  const int dev_cap = (pool->device >= 0 && pool->device < kMaxDevices) ? g_gather_ctas[pool->device] : 0;
+  const int dev_cap = (pool->device >= 0 && pool->device < kMaxDevices) ? g_gather_ctas[pool->device].load() : 0;
   const int grid_cap = dev_cap > 0 ? dev_cap : sm_count(pool->device) * 4;
   auto s = static_cast<cudaStream_t>(stream);
   for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_JOBS_PER_LAUNCH) {
@@ -471,7 +473,11 @@ int dp_pool_create(int device, const dp_kv_geom* geom, int32_t n_slots, int32_t 
   if (e == cudaSuccess)
     e = cudaHostAlloc(reinterpret_cast<void**>(&pool->err_host), sizeof(int), cudaHostAllocMapped |
                                                                             cudaHostAllocPortable);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&pool->att_ctr), 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(pool->att_ctr, 0, 2 * sizeof(uint32_t));
   if (e != cudaSuccess) {
+    if (pool->att_ctr) cudaFree(pool->att_ctr);
+    if (pool->err_host) cudaFreeHost(pool->err_host);
     cudaFree(pool->base);
     delete pool;
     return fail(DP_ECUDA, std::string("pool_create: ") + cudaGetErrorString(e));
@@ -1088,7 +1094,7 @@ int dp_h2d_push_p2p_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* src
   p.n_layer = g.n_layer;
   p.block_tokens = g.block_tokens;
   p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
-  const int dev_cap = de_pool->device < kMaxDevices ? g_gather_ctas[de_pool->device] : 0;
+  const int dev_cap = de_pool->device < kMaxDevices ? g_gather_ctas[de_pool->device].load() : 0;
   const int grid_cap = dev_cap > 0 ? dev_cap : sm_count(de_pool->device) * 4;
   auto s = static_cast<cudaStream_t>(stream);
   for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_DUAL_JOBS_PER_LAUNCH) {
@@ -1146,7 +1152,7 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
   p.n_layer = g.n_layer;
   p.block_tokens = g.block_tokens;
   p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
-  const int ho_cap = pe_pool->device < kMaxDevices ? g_handoff_ctas[pe_pool->device] : 0;
+  const int ho_cap = pe_pool->device < kMaxDevices ? g_handoff_ctas[pe_pool->device].load() : 0;
   const int grid_cap = ho_cap > 0 ? ho_cap : sm_count(pe_pool->device) * 2;  // 699 GB/s NVLink (r01)
   auto s = static_cast<cudaStream_t>(stream);
   for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_HANDOFF_JOBS_PER_LAUNCH) {
@@ -1345,7 +1351,7 @@ constexpr int kAttStride = 148;  // padded row stride in words
 constexpr int kAttGroup = 4;     // key tiles per unit
 constexpr int kAttSmem = 3 * kAttRows * kAttStride * 4;  // query tile + 2 key tiles: 113,664 B
 constexpr uint64_t kQueryMul = 0xA24BAED4963EE407ull;
-int g_attend_ctas[kMaxDevices] = {};
+std::atomic<int> g_attend_ctas[kMaxDevices] = {};
 bool g_attend_init[kMaxDevices] = {};
 std::mutex g_attend_mu;
 
@@ -1532,12 +1538,7 @@ int dp_prefill_attend(const dp_pool* pool, int32_t layer, const dp_attend_item* 
       g_attend_init[pool->device] = true;
     }
   }
-  if (!pool->att_ctr) {
-    uint32_t* c = nullptr;
-    DP_CUDA(cudaMalloc(&c, 2 * sizeof(uint32_t)));
-    DP_CUDA(cudaMemset(c, 0, 2 * sizeof(uint32_t)));
-    const_cast<dp_pool*>(pool)->att_ctr = c;
-  }
+  if (!pool->att_ctr) return fail(DP_EINVAL, "prefill_attend: pool has no work-queue counter");
   AttendParams p;
   std::memset(&p, 0, sizeof(p));
   p.pool = pool->base;
@@ -1549,7 +1550,7 @@ int dp_prefill_attend(const dp_pool* pool, int32_t layer, const dp_attend_item* 
   p.layer = layer;
   p.block_tokens = g.block_tokens;
   p.words = static_cast<int32_t>(g.bytes_per_token_layer / 4);
-  const int cap = g_attend_ctas[pool->device];
+  const int cap = g_attend_ctas[pool->device].load();
   const int grid_cap = cap > 0 ? cap : sm_count(pool->device) * 2;
   const int64_t max_tokens = static_cast<int64_t>(pool->n_slots) * g.block_tokens;
   auto s = static_cast<cudaStream_t>(stream);
