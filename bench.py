@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c1", choices=["c1", "c2", "c3"])
+    ap.add_argument("--trace", default="",
+                    help="sessions from a reference-format trace TSV instead of the generator "
+                         "(first sessions-per-gpu x N lines; KV shape of --workload)")
     ap.add_argument("--cap-gbps", type=float, default=0.0,
                     help="per-engine storage-NIC cap (0 = uncapped: the PCIe link binds)")
     ap.add_argument("--sessions-per-gpu", type=int, default=16)
@@ -89,6 +92,11 @@ def workload(args, n_gpus):
     Qwen2.5-32B KV shape (config 3)."""
     import paper_2602_21548_b200 as dp
     sessions = max(1, args.sessions_per_gpu * max(1, n_gpus))
+    if getattr(args, "trace", ""):
+        trajs = dp.load_trace(args.trace)[:sessions]
+        if not trajs:
+            raise SystemExit(f"--trace {args.trace}: no sessions")
+        return trajs, (QWEN if args.workload == "c3" else DSV3)
     if args.workload in ("c1", "c3"):
         trajs = dp.synthesize(max_len=131072, count=sessions, seed=9, mean_turns=20,
                               sigma_turns=0.0, mean_append=429, mean_gen=500)

@@ -62,3 +62,13 @@ def test_storage_balance_metric():
     res = bench.storage_balance(spans, [2.0, 1.0], 2, width=0.1, window=2)
     assert res["utilisation_max_avg"] == pytest.approx(1.0, abs=1e-4)
     assert bench.storage_balance({}, None, 2) is None
+
+
+def test_trace_workload(tmp_path):
+    p = str(tmp_path / "t.tsv")
+    dp.save_trace(p, dp.synthesize(max_len=8000, count=7, seed=2))
+    a = Args()
+    a.trace, a.sessions_per_gpu = p, 2
+    trajs, shape = bench.workload(a, 2)
+    assert [t.id for t in trajs] == [t.id for t in dp.load_trace(p)[:4]]
+    assert shape["L"] == 61
