@@ -47,7 +47,7 @@ struct ExecOptions {
   std::int32_t wait_timeout_ms = 30000;
   // PE-path loads (K1): 0 = SM gather kernel, 1 = copy engine (no SMs: the
   // isolation mode while the PE computes), 2 = both at once, jobs split by
-  // bytes (the plain load path; the two read paths together beat either)
+  // bytes (the plain load path; measured slower than 0, profiles/r01_SUMMARY.md)
   std::int32_t k1_mode = 0;
   // DE-path loads (K2): 0 = SM gather pushing over NVLink, 1 = the DE's copy
   // engine writing into the PE pool (no SMs on the DE: its decode is untouched)
@@ -68,7 +68,7 @@ struct ExecOptions {
   // the decode stand-in for the generated tokens and persists them (K4) every
   // 64 generated tokens plus the final partial, into its persist store
   bool persist = false;
-  // Prefill stand-in (not with `handoff`): every PE packs
+  // Prefill stand-in (with or without `handoff`): every PE packs
   // its requests, in the order their KV lands, into forward batches with
   // pdsim::build_forward_batch under `compute_quota` (seconds per layer of
   // `prefill_cost`) and runs each batch layer by layer as K5
@@ -77,7 +77,7 @@ struct ExecOptions {
   double compute_quota = 2e-3;
   pdsim::AttentionCostModel prefill_cost{};
   std::int32_t attend_ctas = 0;        // K5 CTA cap (0 = default)
-  // Storage tier (the plain load path only): StorageRead
+  // Storage tier (the load and prefill paths): StorageRead
   // becomes real file reads — every Full Block a job needs is looked up in
   // the Full Block trie and read from `tier_path` (a FullBlockFile whose
   // record r is page r) by `io_threads` host threads into a pinned staging
