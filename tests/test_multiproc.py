@@ -48,13 +48,21 @@ def worker(rank, world, port, P, policy, q):
         planned = dp.plan(cfg, trajs, policy=policy, **SB)
         xp = dp.build_exec_plan(cfg, trajs, planned, dp.ExecOptions())
         digests = g.allgather(dist.plan_digest(planned))
+        # the full pipeline's plan (forwards, DE orders) is the same on every rank
+        opt = dp.ExecOptions()
+        opt.handoff = opt.persist = opt.prefill = True
+        opt.compute_quota, opt.prefill_cost = 1e-3, (2e-10, 1e-9, 4e-7, 1e-5)
+        full = dp.build_exec_plan(cfg, trajs, planned, opt)
+        shape = repr([full.forwards(p) for p in range(P)] +
+                     [full.de_order(d) for d in range(P, world)])
+        pipeline = g.allgather(shape)
         mine = sorted(xp.jobs()[i][0] for i in xp.by_reader(rank))
         shares = g.allgather(mine)
         rt = {rank: FakeRuntime(rank)}
         table = dist.connect_pools(g, rt, P)
         t = g.max(float(rank))
         q.put((rank, digests, shares, sorted(j[0] for j in xp.jobs()), xp.reader_bytes,
-               sorted(rt[rank].attached), sorted(table), t))
+               sorted(rt[rank].attached), sorted(table), t, len(set(pipeline))))
     finally:
         g.close()
 
@@ -85,6 +93,7 @@ def test_two_rank_plan_agreement_and_partition(P, policy):
         assert shares[1], "the DE rank should read its share"
     assert r1[5] == [0] and r0[5] == []                      # the DE attached the PE pool
     assert r0[6] == [0] and r0[7] == 1.0                     # handle table, max over ranks
+    assert r0[8] == r1[8] == 1                               # same forwards and DE orders
 
 
 def test_roles():
