@@ -106,6 +106,7 @@ struct LoadJob {
   std::vector<std::uint32_t> pred_targets; // reuses (written by another engine), and their
                                            // all-layer landed-item targets
   bool fence = false;  // reuses a slot this reader wrote earlier: must not share a launch
+  std::vector<int> fence_jobs;  // ... with these jobs (global order)
   // ---- PD handoff (ExecOptions::handoff) ----
   int de = -1;                   // the request's decode engine
   std::int64_t prompt = 0;       // C + A

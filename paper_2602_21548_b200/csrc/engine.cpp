@@ -309,6 +309,7 @@ StepResult EngineRuntime::run_step() {
   std::vector<dp_job> batch;
   batch.reserve(DP_MAX_JOBS_PER_LAUNCH);
   std::vector<int> batch_jobs;  // by_reader positions of the jobs in `batch`
+  std::vector<char> in_batch(x.jobs.size(), 0);  // job index -> in `batch`
   int batch_pe = -1;
   const bool k1_ce = x.opt.k1_mode == 1;
   const bool k2_ce = x.opt.k2_mode == 1;
@@ -350,6 +351,7 @@ StepResult EngineRuntime::run_step() {
                       DP_MAX_JOBS_PER_LAUNCH;
     batch.clear();
     if (tier) tier->launched(batch_jobs, s);
+    for (int i : batch_jobs) in_batch[mine[i]] = 0;
     batch_jobs.clear();
   };
   auto flush_ce = [&]() {
@@ -378,7 +380,11 @@ StepResult EngineRuntime::run_step() {
     const std::int64_t bytes = j.cached * x.cfg.kv_bytes_per_token();
     const bool gated = cap > 0 || pace > 0;
     const bool hazard = !j.preds.empty();
-    if (gated || hazard || j.fence || batch_pe != j.pe || batch.size() == DP_MAX_JOBS_PER_LAUNCH)
+    // a same-reader slot reuse only needs a launch boundary when the previous
+    // occupant is in the launch being built (launches on one stream are ordered)
+    bool fence_now = false;
+    for (int w : j.fence_jobs) fence_now = fence_now || in_batch[w];
+    if (gated || hazard || fence_now || batch_pe != j.pe || batch.size() == DP_MAX_JOBS_PER_LAUNCH)
       flush();
     if (hybrid) {
       if (hazard || j.fence) join_streams();
@@ -427,6 +433,7 @@ StepResult EngineRuntime::run_step() {
       batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0,
                              x.cfg.n_layer, j.ticket});
     batch_jobs.push_back(static_cast<int>(i));
+    in_batch[mine[i]] = 1;
     res.bytes_read += bytes;
     ++res.jobs;
   }

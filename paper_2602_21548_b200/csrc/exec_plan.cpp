@@ -456,6 +456,8 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
         // launch run concurrently, so the reuse must start a new launch
         if (pj.reader == j.reader) {
           j.fence = true;
+          if (std::find(j.fence_jobs.begin(), j.fence_jobs.end(), prev) == j.fence_jobs.end())
+            j.fence_jobs.push_back(prev);
         } else if (std::find(j.preds.begin(), j.preds.end(), pj.ticket) == j.preds.end()) {
           j.preds.push_back(pj.ticket);
           j.pred_targets.push_back(static_cast<std::uint32_t>(
@@ -540,6 +542,7 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
     for (int& w : j.k3_waits) w = pos[w];
     for (int& w : j.consumer_waits) w = pos[w];
     for (int& w : j.de_pred_jobs) w = pos[w];
+    for (int& w : j.fence_jobs) w = pos[w];
     if (x.prefill) {
       if (j.reader != j.pe && !x.handoff)  // a DE load waits on the PE's "consumed" rows [n, 2n)
         for (int w : j.consumer_waits) {
