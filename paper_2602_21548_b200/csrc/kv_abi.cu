@@ -494,7 +494,8 @@ int dp_pool_destroy(dp_pool* pool) {
     if (pool->owner && pool->base) cudaFree(pool->base);
     if (pool->ipc_opened && pool->base) cudaIpcCloseMemHandle(pool->base);
     if (pool->err_host) cudaFreeHost(pool->err_host);
-    if (pool->att_ctr) cudaFree(pool->att_ctr);
+    if (pool->owner && pool->att_ctr) cudaFree(pool->att_ctr);
+    cudaGetLastError();  // a teardown failure must not surface in the next caller's check
   }
   delete pool;
   return DP_OK;
@@ -583,6 +584,7 @@ int dp_pool_peer_view(int device, const dp_pool* pool, dp_pool** out) {
   v->owner = false;
   v->ipc_opened = false;
   v->err_host = nullptr;
+  v->att_ctr = nullptr;  // owner-only resources stay with the owner
   e = cudaHostAlloc(reinterpret_cast<void**>(&v->err_host), sizeof(int),
                     cudaHostAllocMapped | cudaHostAllocPortable);
   if (e != cudaSuccess) {
