@@ -4,6 +4,8 @@
 #include <deque>
 #include <stdexcept>
 #include <string>
+#include <limits>
+#include <unordered_map>
 
 #include "dualpath/engine.hpp"
 #include "dualpath/storage.hpp"
@@ -219,88 +221,153 @@ void build_tier(ExecPlan& x, std::span<const pdsim::Trajectory> trajectories) {
   }
 }
 
-// The enqueue order of each DE in handoff + prefill mode.  A DE's reads and
-// decodes spin-wait on work of other engines, and a spin-wait at the head of
-// a hardware queue holds everything behind it, so each wait's producers that
-// run on this DE must be enqueued first:
-//   * the decode of j waits for K3(j), which follows j's PE forwards up to
-//     j's last one: this DE's reads of every request in those forwards first;
-//   * a read reusing decode slots of p waits for p's release: with
-//     persistence p's decode on this DE, without it K3(p) (p's forwards).
-// Reads of one PE's requests stay in global order, decodes in by_de order;
-// among ready operations the lowest job goes first (reads before decodes).
-// A plan with no such order is rejected rather than left to hang.
+// The enqueue order of each DE in handoff + prefill mode.  Reads and
+// decodes spin-wait on work of other engines, and in the worst case every
+// stream of a device shares one hardware FIFO, so an operation also waits for
+// everything enqueued before it on its device.  The orders are found by
+// running the whole step in that model: each PE's sequence is the one its
+// runtime enqueues (loads in FIFO order, forwards and the K3s they finish
+// drained before a load that reuses slots or meets the storage gate), and
+// each DE appends, among its next read per PE and its next decode, the one
+// whose dependencies have completed (lowest job first).  A complete run of the
+// model proves the orders cannot deadlock under one FIFO per device; a plan
+// without one is rejected.
 void build_de_orders(ExecPlan& x) {
-  const int n_pe = x.n_pe;
-  // B[pe][f]: the largest job of forwards 0..f of the PE (their loads)
-  std::vector<std::vector<int>> upto(n_pe);
-  for (int p = 0; p < n_pe; ++p) {
-    int m = -1;
-    for (const Forward& f : x.forwards[p]) {
-      for (std::int32_t i = f.begin; i < f.end; ++i) m = std::max(m, x.fwd_items[p][i].job);
-      upto[p].push_back(m);
+  enum Kind : std::int64_t { kLoad = 0, kRead = 1, kK3 = 2, kDecode = 3, kFwd = 4 };
+  const std::int64_t J = static_cast<std::int64_t>(x.jobs.size()) + 1;
+  auto op = [&](Kind k, std::int64_t id) { return static_cast<std::int64_t>(k) * J * 64 + id; };
+  auto fwd_op = [&](int p, int f) { return op(kFwd, static_cast<std::int64_t>(f) * 64 + p); };
+  std::unordered_map<std::int64_t, char> done;
+  auto is_done = [&](std::int64_t o) { return done.count(o) != 0; };
+  const bool gated = x.opt.storage_cap_Bps > 0 || !x.opt.storage_cap_per_engine.empty() || x.opt.pace_scale > 0;
+  if (x.n_pe > 64) throw std::invalid_argument("build_exec_plan: at most 64 PEs with handoff + prefill");
+
+  auto fetch = [&](int y) { return x.jobs[y].reader == x.jobs[y].pe ? op(kLoad, y) : op(kRead, y); };
+  auto add_release = [&](int q, std::vector<std::int64_t>& deps) {
+    if (x.persist) {
+      deps.push_back(op(kDecode, q));
+    } else {
+      deps.push_back(op(kK3, q));
+      if (x.jobs[q].de_path && x.jobs[q].n_blk > 0) deps.push_back(op(kRead, q));
     }
+  };
+  struct Op {
+    std::int64_t id;
+    std::vector<std::int64_t> deps;
+  };
+  // each PE's enqueue sequence, as engine_handoff.cpp builds it
+  std::vector<std::vector<Op>> pe_seq(x.n_pe);
+  for (int p = 0; p < x.n_pe; ++p) {
+    auto& seq = pe_seq[p];
+    const auto& fwds = x.forwards[p];
+    const auto& mine = x.by_pe[p];
+    std::vector<int> row(x.jobs.size(), -1);
+    for (const FwdItem& it : x.fwd_items[p])
+      if (it.job >= 0) row[it.job] = it.row;
+    std::size_t fi = 0, ki = 0;
+    auto k3 = [&](int j) {
+      Op o{op(kK3, j), {fwd_op(p, x.last_fwd[j])}};
+      for (int q : x.jobs[j].de_pred_jobs) add_release(q, o.deps);
+      seq.push_back(std::move(o));
+    };
+    auto drain = [&](std::int64_t r) {
+      while (fi < fwds.size() && fwds[fi].last_row < r) {
+        Op o{fwd_op(p, static_cast<int>(fi)), {}};
+        for (std::int32_t i = fwds[fi].begin; i < fwds[fi].end; ++i) {
+          const FwdItem& it = x.fwd_items[p][i];
+          if (it.job >= 0 && it.cached > 0) o.deps.push_back(fetch(it.job));
+        }
+        seq.push_back(std::move(o));
+        ++fi;
+        while (ki < mine.size() && x.last_fwd[mine[ki]] < static_cast<int>(fi)) k3(mine[ki++]);
+      }
+    };
+    for (int j : mine) {
+      const LoadJob& lj = x.jobs[j];
+      if (!lj.k3_waits.empty() || gated) drain(row[j]);
+      if (!lj.de_path && lj.n_blk > 0) {
+        Op o{op(kLoad, j), {}};
+        for (int w : lj.k3_waits) o.deps.push_back(op(kK3, w));
+        seq.push_back(std::move(o));
+      }
+    }
+    drain(std::numeric_limits<std::int64_t>::max());
+    while (ki < mine.size()) k3(mine[ki++]);
   }
-  auto bound = [&](int j) {  // the loads K3(j) depends on: jobs of its PE up to this
-    const LoadJob& lj = x.jobs[j];
-    const int f = x.last_fwd[j];
-    return f < 0 ? -1 : upto[lj.pe][f];
+  // the DEs' candidate operations
+  const int n_de = x.n_engines - x.n_pe;
+  std::vector<std::vector<std::vector<int>>> lists(n_de, std::vector<std::vector<int>>(x.n_pe));
+  for (int d = 0; d < n_de; ++d)
+    for (int ji : x.by_reader[x.n_pe + d]) lists[d][x.jobs[ji].pe].push_back(ji);
+  std::vector<std::vector<std::size_t>> head(n_de, std::vector<std::size_t>(x.n_pe, 0));
+  std::vector<std::size_t> dh(n_de, 0), ph(x.n_pe, 0);
+  auto read_deps = [&](int ji) {
+    std::vector<std::int64_t> deps;
+    for (int q : x.jobs[ji].consumer_waits) deps.push_back(op(kK3, q));
+    for (int q : x.jobs[ji].de_pred_jobs) add_release(q, deps);
+    return deps;
+  };
+  auto decode_deps = [&](int j) {
+    std::vector<std::int64_t> deps{op(kK3, j)};
+    if (x.jobs[j].de_path && x.jobs[j].n_blk > 0) deps.push_back(op(kRead, j));
+    return deps;
+  };
+  auto all_done = [&](const std::vector<std::int64_t>& deps) {
+    for (std::int64_t d : deps)
+      if (!is_done(d)) return false;
+    return true;
   };
   x.de_order.assign(x.n_engines, {});
-  for (int d = x.n_pe; d < x.n_engines; ++d) {
-    std::vector<std::vector<int>> lists(n_pe);  // this DE's reads, per PE, global order
-    for (int ji : x.by_reader[d]) lists[x.jobs[ji].pe].push_back(ji);
-    std::vector<std::size_t> head(n_pe, 0);
-    // emitted reads of PE p with job <= b
-    auto reads_done_upto = [&](int p, int b) {
-      const auto& l = lists[p];
-      // lists are increasing: every element <= b must be before head
-      return head[p] >= l.size() || l[head[p]] > b;
-    };
-    const auto& decs = x.persist ? x.by_de[d] : std::vector<int>{};
-    std::vector<int> dec_pos(x.jobs.size(), -1);
-    for (std::size_t k = 0; k < decs.size(); ++k) dec_pos[decs[k]] = static_cast<int>(k);
-    std::size_t dh = 0;
-    const std::size_t total = x.by_reader[d].size() + decs.size();
-    auto& order = x.de_order[d];
-    order.reserve(total);
-    while (order.size() < total) {
-      int best = -1;
-      bool best_is_read = false;
-      for (int p = 0; p < n_pe; ++p) {
-        if (head[p] >= lists[p].size()) continue;
-        const int ji = lists[p][head[p]];
-        bool ready = true;
-        for (int q : x.jobs[ji].de_pred_jobs) {
-          if (x.persist) {
-            if (dec_pos[q] >= 0 && static_cast<std::size_t>(dec_pos[q]) >= dh) ready = false;
-          } else if (!reads_done_upto(x.jobs[q].pe, bound(q))) {
-            ready = false;
+  std::size_t remaining = 0;
+  for (int p = 0; p < x.n_pe; ++p) remaining += pe_seq[p].size();
+  for (int d = 0; d < n_de; ++d)
+    remaining += x.by_reader[x.n_pe + d].size() + (x.persist ? x.by_de[x.n_pe + d].size() : 0);
+  while (remaining > 0) {
+    bool progress = false;
+    for (int p = 0; p < x.n_pe; ++p)
+      while (ph[p] < pe_seq[p].size() && all_done(pe_seq[p][ph[p]].deps)) {
+        done[pe_seq[p][ph[p]].id] = 1;
+        ++ph[p];
+        --remaining;
+        progress = true;
+      }
+    for (int d = 0; d < n_de; ++d) {
+      const int e = x.n_pe + d;
+      const auto& decs = x.persist ? x.by_de[e] : std::vector<int>{};
+      for (;;) {
+        int best = -1;
+        bool best_read = false;
+        for (int p = 0; p < x.n_pe; ++p) {
+          if (head[d][p] >= lists[d][p].size()) continue;
+          const int ji = lists[d][p][head[d][p]];
+          if ((best < 0 || ji < best) && all_done(read_deps(ji))) {
+            best = ji;
+            best_read = true;
           }
         }
-        if (ready && (best < 0 || ji < best)) {
-          best = ji;
-          best_is_read = true;
+        if (dh[d] < decs.size()) {
+          const int jd = decs[dh[d]];
+          if ((best < 0 || jd < best) && all_done(decode_deps(jd))) {
+            best = jd;
+            best_read = false;
+          }
         }
-      }
-      if (dh < decs.size()) {
-        const int jd = decs[dh];
-        if (reads_done_upto(x.jobs[jd].pe, bound(jd)) && (best < 0 || jd < best)) {
-          best = jd;
-          best_is_read = false;
+        if (best < 0) break;
+        if (best_read) {
+          ++head[d][x.jobs[best].pe];
+          done[op(kRead, best)] = 1;
+          x.de_order[e].push_back(best);
+        } else {
+          ++dh[d];
+          done[op(kDecode, best)] = 1;
+          x.de_order[e].push_back(-1 - best);
         }
-      }
-      if (best < 0)
-        throw std::logic_error("build_exec_plan: no deadlock-free enqueue order for DE " + std::to_string(d) +
-                               " (handoff + prefill)");
-      if (best_is_read) {
-        ++head[x.jobs[best].pe];
-        order.push_back(best);
-      } else {
-        ++dh;
-        order.push_back(-1 - best);  // a decode
+        --remaining;
+        progress = true;
       }
     }
+    if (!progress)
+      throw std::logic_error("build_exec_plan: no deadlock-free enqueue order (handoff + prefill)");
   }
 }
 
