@@ -118,3 +118,73 @@ def test_handoff_prefill_enqueue_order_cannot_deadlock(P, D, sessions, cap, pers
     stuck, n_ops = enqueue_model(xp, persist, gated)
     assert n_ops > 0
     assert not stuck, f"deadlock under one FIFO per device: {stuck}"
+
+
+def handoff_model(xp, persist):
+    """engine_handoff.cpp without the prefill: a PE enqueues per job its load
+    then its K3; a DE interleaves reads and decodes in global order."""
+    jobs = xp.jobs()
+    by_ticket = {(j[4], j[8]): i for i, j in enumerate(jobs)}          # PE row -> job
+    by_de_ticket = {(j[13], j[16]): i for i, j in enumerate(jobs)}     # decode row -> job
+    fifo = {}
+
+    def release(q):
+        if persist:
+            return [("decode", q)]
+        return [("k3", q)] + ([("read", q)] if jobs[q][5] and jobs[q][7] else [])
+
+    de_pred = {i: [by_de_ticket[(j[13], t)] for t in j[19]] for i, j in enumerate(jobs)}
+    for p in range(xp.n_pe):
+        ops = fifo.setdefault(("pe", p), [])
+        for j in xp.by_pe(p):
+            jj = jobs[j]
+            if not jj[5] and jj[7] > 0:
+                ops.append((("load", j), [("k3", w) for w in jj[20]]))
+            deps = []
+            if jj[7] > 0:
+                deps.append(("read", j) if jj[5] else ("load", j))
+            if not jj[5] and jj[7] == 0:
+                deps += [("k3", w) for w in jj[20]]
+            for q in de_pred[j]:
+                deps += release(q)
+            ops.append((("k3", j), deps))
+    for d in range(xp.n_pe, xp.n_engines):
+        ops = fifo.setdefault(("de", d), [])
+        reads, decs = xp.by_reader(d), (xp.by_de(d) if persist else [])
+        ri = di = 0
+        while ri < len(reads) or di < len(decs):
+            if ri < len(reads) and (di >= len(decs) or reads[ri] <= decs[di]):
+                x = reads[ri]
+                ri += 1
+                deps = [("k3", by_ticket[(jobs[x][4], t)]) for t in jobs[x][21]]
+                for q in de_pred[x]:
+                    deps += release(q)
+                ops.append((("read", x), deps))
+            else:
+                j = decs[di]
+                di += 1
+                ops.append((("decode", j), [("k3", j)] + ([("read", j)] if jobs[j][5] and jobs[j][7] else [])))
+    done, heads = set(), {k: 0 for k in fifo}
+    progress = True
+    while progress:
+        progress = False
+        for k, ops in fifo.items():
+            while heads[k] < len(ops) and all(dep in done for dep in ops[heads[k]][1]):
+                done.add(ops[heads[k]][0])
+                heads[k] += 1
+                progress = True
+    return {k: fifo[k][heads[k]] for k in fifo if heads[k] < len(fifo[k])}
+
+
+@pytest.mark.parametrize("P,D,persist", [(1, 1, True), (2, 2, True), (2, 2, False), (1, 3, True), (3, 1, True)])
+def test_handoff_enqueue_order_cannot_deadlock(P, D, persist):
+    cfg = cluster(P, D, 6.25e9)
+    trajs = dp.synthesize(max_len=20000, count=6 * (P + D), seed=9, mean_turns=8, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **SB)
+    opt = dp.ExecOptions()
+    opt.handoff, opt.persist = True, persist
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    stuck = handoff_model(xp, persist)
+    assert not stuck, f"deadlock under one FIFO per device: {stuck}"
