@@ -188,3 +188,70 @@ def test_handoff_enqueue_order_cannot_deadlock(P, D, persist):
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     stuck = handoff_model(xp, persist)
     assert not stuck, f"deadlock under one FIFO per device: {stuck}"
+
+
+def prefill_model(xp, gated):
+    """engine_prefill.cpp (PE) + engine.cpp run_step (DE) in prefill mode."""
+    jobs = xp.jobs()
+    fifo = {}
+    for p in range(xp.n_pe):
+        ops = fifo.setdefault(("pe", p), [])
+        fwds = xp.forwards(p)
+        rows = xp.fwd_rows(p)
+        job_of_row = {}
+        for _, items in fwds:
+            for it in items:
+                job_of_row[it[5]] = it[1]
+        last_row = [max(it[5] for it in items) for _, items in fwds]
+        fi = 0
+
+        def fetch(y):
+            return ("load", y) if jobs[y][3] == jobs[y][4] else ("read", y)
+
+        def forwards_before(r):
+            nonlocal fi
+            while fi < len(fwds) and last_row[fi] < r:
+                ops.append((("fwd", p, fi), [fetch(it[1]) for it in fwds[fi][1] if it[1] >= 0 and it[2] > 0]))
+                fi += 1
+
+        for r in range(len(rows)):
+            j = job_of_row.get(r, -1)
+            if j < 0 or jobs[j][3] != p or jobs[j][7] == 0:
+                continue
+            waits = xp.consumer_waits(j)
+            if gated or waits:
+                forwards_before(r)
+            ops.append((("load", j), [("fwd", p, xp.last_fwd(w)) for w in waits]))
+        forwards_before(float("inf"))
+    for d in range(xp.n_pe, xp.n_engines):
+        ops = fifo.setdefault(("de", d), [])
+        for x in xp.by_reader(d):
+            ops.append((("read", x), [("fwd", jobs[x][4], xp.last_fwd(w)) for w in xp.consumer_waits(x)]))
+    done, heads = set(), {k: 0 for k in fifo}
+    progress = True
+    while progress:
+        progress = False
+        for k, ops in fifo.items():
+            while heads[k] < len(ops) and all(dep in done for dep in ops[heads[k]][1]):
+                done.add(ops[heads[k]][0])
+                heads[k] += 1
+                progress = True
+    return {k: fifo[k][heads[k]] for k in fifo if heads[k] < len(fifo[k])}
+
+
+@pytest.mark.parametrize("P,D", [(1, 1), (2, 2), (1, 3), (3, 1)])
+@pytest.mark.parametrize("gated", [False, True])
+def test_prefill_enqueue_order_cannot_deadlock(P, D, gated):
+    cfg = cluster(P, D, 6.25e9)
+    trajs = dp.synthesize(max_len=20000, count=6 * (P + D), seed=9, mean_turns=8, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **SB)
+    opt = dp.ExecOptions()
+    opt.prefill, opt.compute_quota, opt.prefill_cost = True, 5e-4, COST
+    if gated:
+        opt.storage_cap_Bps = 6.25e9
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.pool_slots = xp.peak_slots
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert any(xp.consumer_waits(i) for i in range(len(xp.jobs())))
+    stuck = prefill_model(xp, gated)
+    assert not stuck, f"deadlock under one FIFO per device: {stuck}"
