@@ -255,3 +255,42 @@ def test_prefill_enqueue_order_cannot_deadlock(P, D, gated):
     assert any(xp.consumer_waits(i) for i in range(len(xp.jobs())))
     stuck = prefill_model(xp, gated)
     assert not stuck, f"deadlock under one FIFO per device: {stuck}"
+
+
+def plain_model(xp):
+    """engine.cpp run_step: each reader's loads in its order, a load reusing a
+    slot another engine wrote waits for that load; a PE ends with a wait on
+    every push into its pool."""
+    jobs = xp.jobs()
+    by_ticket = {(j[4], j[8]): i for i, j in enumerate(jobs)}
+    fifo = {}
+    for e in range(xp.n_engines):
+        ops = fifo.setdefault(e, [])
+        for x in xp.by_reader(e):
+            ops.append((("load", x), [("load", by_ticket[(jobs[x][4], t)]) for t in jobs[x][11]]))
+        if e < xp.n_pe:
+            ops.append((("end", e), [("load", i) for i in xp.by_pe(e) if jobs[i][3] != e]))
+    done, heads = set(), {k: 0 for k in fifo}
+    progress = True
+    while progress:
+        progress = False
+        for k, ops in fifo.items():
+            while heads[k] < len(ops) and all(dep in done for dep in ops[heads[k]][1]):
+                done.add(ops[heads[k]][0])
+                heads[k] += 1
+                progress = True
+    return {k: fifo[k][heads[k]] for k in fifo if heads[k] < len(fifo[k])}
+
+
+@pytest.mark.parametrize("P,D", [(1, 1), (2, 2), (1, 3), (3, 1)])
+def test_plain_enqueue_order_cannot_deadlock(P, D):
+    cfg = cluster(P, D, 6.25e9)
+    trajs = dp.synthesize(max_len=20000, count=6 * (P + D), seed=9, mean_turns=8, sigma_turns=0)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **SB)
+    opt = dp.ExecOptions()
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    opt.pool_slots = xp.peak_slots
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert any(j[11] for j in xp.jobs())  # cross-reader reuse exists
+    stuck = plain_model(xp)
+    assert not stuck, f"deadlock under one FIFO per device: {stuck}"
