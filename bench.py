@@ -2,19 +2,28 @@
 """DualPath KV-Cache loading benchmark on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c1|c2] [--cap-gbps X] [--sessions-per-gpu S]
+                    [--workload c1|c2|c3] [--cap-gbps X] [--sessions-per-gpu S]
 
-N = 1: the K1 loader alone (the PE of a 1P1D prefill-only plan; P/D needs
-two engines, proj/src/types.cpp:11-12).  N > 1: one process per GPU under
-torchrun, engines 0..N/2-1 prefill (PE), the rest decode (DE), dual-path
-plan; the same workload is also run prefill-only ("1-path",
-Policy::PEOnly, proj/src/desim.cpp:826-827) for the vs-1-path ratio.
+N = 1: BASELINE config 1 (64 sessions x 20 turns, DeepSeek-V3 MLA KV) loaded
+by the K1 loader alone (the PE of a 1P1D prefill-only plan; P/D needs two
+engines, proj/src/types.cpp:11-12).  N > 1: one process per GPU (re-launched
+under torch.distributed.run when WORLD_SIZE is unset), engines 0..N/2-1
+prefill (PE), the rest decode (DE), dual-path plan over 16 sessions per GPU;
+the same workload also runs prefill-only ("1-path", Policy::PEOnly,
+proj/src/desim.cpp:826-827), and BASELINE config 2 (32K-128K contexts,
+per-engine storage NIC capped at 6.25 GB/s, dual vs 1-path) runs in the same
+line under "storage_capped".
 
 A step = one offline pass of the synthetic agentic trace: every request's
-hit KV (C*L*b bytes) moved from the emulated storage tier (pinned host DRAM,
-read over each engine's own PCIe link, optionally rate-capped per engine)
-into the PE's paged HBM pool, by K1 (PE path) or K2 (DE path, NVLink push).
-Inputs are larger than L2 (hundreds of GB per step), so no flush is needed.
+hit KV (C*L*b bytes) moved from the emulated storage tier (pinned host DRAM
+on each GPU's NUMA node, read over each engine's own PCIe link, optionally
+rate-capped per engine) into the PE's paged HBM pool, by K1 (PE path) or K2
+(DE path, NVLink push).  Inputs are larger than L2 (hundreds of GB per
+step), so no flush is needed.
+
+The scheduler decisions of every plan are digested into the line and, when
+tests/golden/bench_*.json holds the reference's own decisions for the exact
+configuration (tests/golden/make_golden.py, oracle/_ref), compared with them.
 """
 
 import argparse
@@ -47,7 +56,21 @@ def parse():
                          "(first sessions-per-gpu x N lines; KV shape of --workload)")
     ap.add_argument("--cap-gbps", type=float, default=0.0,
                     help="per-engine storage-NIC cap (0 = uncapped: the PCIe link binds)")
-    ap.add_argument("--sessions-per-gpu", type=int, default=16)
+    ap.add_argument("--sessions-per-gpu", type=int, default=0,
+                    help="0 = default: config 1's 64 sessions at N = 1, 16 per GPU at N > 1")
+    ap.add_argument("--link-model", default="fixed", choices=["fixed", "measured"],
+                    help="per-engine storage-read rate the planner (the reference's model) uses when "
+                         "uncapped: fixed = the SM zero-copy rate 51.5 GB/s (decisions pinned by "
+                         "tests/golden/bench_*.json); measured = min(51.5, this box's concurrent "
+                         "host-link ceiling / N)")
+    ap.add_argument("--no-capped", action="store_true",
+                    help="N > 1: skip the config-2 storage-capped dual vs 1-path sub-run")
+    ap.add_argument("--capped-steps", type=int, default=2, help="timed steps of the storage-capped sub-run")
+    ap.add_argument("--capped-sessions-per-gpu", type=int, default=6)
+    ap.add_argument("--capped-gbps", type=float, default=6.25,
+                    help="per-engine storage-NIC cap of the sub-run (400 Gbps SNIC per 8 GPUs, PAPER.md:496)")
+    ap.add_argument("--store-gb", type=float, default=0.0,
+                    help="host store per engine, GB (0 = the whole trace, within half the host RAM)")
     ap.add_argument("--no-one-path", action="store_true", help="skip the prefill-only comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pd", default="", help="override P:D, e.g. 2:6")
@@ -83,34 +106,89 @@ def parse():
 
 
 # ----------------------------------------------------------------- workload
-def workload(args, n_gpus):
+GEN_C1 = dict(max_len=131072, seed=9, mean_turns=20, sigma_turns=0.0, mean_append=429, mean_gen=500)
+
+
+def n_sessions(args, n_gpus):
+    if args.sessions_per_gpu > 0:
+        return args.sessions_per_gpu * max(1, n_gpus)
+    return 64 if n_gpus <= 1 else 16 * n_gpus
+
+
+def c2_rounds(i):
+    """Config 2 session i: one cold prefill round {C-1, 1} that builds a
+    32K / 64K / 128K context, then three warm rounds {429, 1} (a cold append
+    instead of the reference tests' long generation round, whose 64-token
+    persistence flows would dominate planning)."""
+    c = (32768, 65536, 131072)[i % 3]
+    return [(c - 1, 1)] + [(429, 1)] * 3
+
+
+def workload(args, n_gpus, kind=None, sessions=None):
     """Trajectories + KV shape.  c1: BASELINE config 1 generator (20 turns,
-    mean append 429, mean gen 500, ~95% hit); c2: 32K/64K/128K contexts built
-    by one cold prefill round {C, 1}, then warm {429, 1} rounds (config 2; a
-    cold append instead of the reference tests' long generation round, whose
-    64-token persistence flows would dominate planning); c3: c1 with the
-    Qwen2.5-32B KV shape (config 3)."""
+    mean append 429, mean gen 500, ~95% hit); c2: 32K/64K/128K contexts
+    (config 2); c3: c1 with the Qwen2.5-32B KV shape (config 3)."""
     import paper_2602_21548_b200 as dp
-    sessions = max(1, args.sessions_per_gpu * max(1, n_gpus))
-    if getattr(args, "trace", ""):
+    kind = kind or args.workload
+    sessions = sessions or n_sessions(args, n_gpus)
+    if getattr(args, "trace", "") and kind == args.workload:
         trajs = dp.load_trace(args.trace)[:sessions]
         if not trajs:
             raise SystemExit(f"--trace {args.trace}: no sessions")
-        return trajs, (QWEN if args.workload == "c3" else DSV3)
-    if args.workload in ("c1", "c3"):
-        trajs = dp.synthesize(max_len=131072, count=sessions, seed=9, mean_turns=20,
-                              sigma_turns=0.0, mean_append=429, mean_gen=500)
-        shape = DSV3 if args.workload == "c1" else QWEN
-    else:
-        trajs = []
-        for i in range(sessions):
-            t = dp.Trajectory()
-            t.id = f"ctx{i}"
-            c = (32768, 65536, 131072)[i % 3]
-            t.rounds = [dp.Round(c - 1, 1)] + [dp.Round(429, 1) for _ in range(3)]
-            trajs.append(t)
-        shape = DSV3
-    return trajs, shape
+        return trajs, (QWEN if kind == "c3" else DSV3)
+    if kind in ("c1", "c3"):
+        trajs = dp.synthesize(count=sessions, **GEN_C1)
+        return trajs, (DSV3 if kind == "c1" else QWEN)
+    trajs = []
+    for i in range(sessions):
+        t = dp.Trajectory()
+        t.id = f"ctx{i}"
+        t.rounds = [dp.Round(a, g) for a, g in c2_rounds(i)]
+        trajs.append(t)
+    return trajs, DSV3
+
+
+def trace_stats(rounds_per_session, shape):
+    """requests, hit bytes (sum C*L*b) and prompt tokens (sum C+A) of a trace,
+    from its rounds alone (context_before, proj/src/types.cpp:44-53)."""
+    req = hit = prompt = 0
+    for rounds in rounds_per_session:
+        ctx = 0
+        for a, g in rounds:
+            req += 1
+            hit += ctx * shape["L"] * shape["b"]
+            prompt += ctx + a
+            ctx += a + g
+    return req, hit, prompt
+
+
+def config_dict(kind, sessions, P, D, policy, shape, cap_gbps, stats, extra=None):
+    """The `config` of a line: identical for both arms of the same run."""
+    req, hit, prompt = stats
+    cfg = {"workload": f"{kind}: {sessions} sessions, {P}P{D}D {policy}"
+                       + (" (1 PE loader, K1)" if P + D == 2 and policy == "pe_only" else ""),
+           "sessions": sessions, "kv": shape, "storage_cap_gbps_per_engine": cap_gbps or None,
+           "requests": req, "hit_bytes_per_step": hit, "prompt_tokens_per_step": prompt,
+           "l2": "inputs >> L2 (hundreds of GB per step; no flush needed)"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+def golden_key(kind, sessions, P, D, policy, cap_gbps, link_bps):
+    link = "cap%g" % cap_gbps if cap_gbps else "link%g" % (link_bps / 1e9)
+    return f"{kind}_{sessions}s_{P}p{D}d_{policy}_{link}"
+
+
+def golden_check(key, digest):
+    """Compare a plan's decision digest with the reference's own decisions for
+    the same configuration (tests/golden/bench_<key>.json), when recorded."""
+    path = os.path.join(ROOT, "tests", "golden", f"bench_{key}.json")
+    if not os.path.exists(path):
+        return {"fixture": None, "match": None}
+    with open(path) as f:
+        want = json.load(f)["decisions_digest"]
+    return {"fixture": os.path.relpath(path, ROOT), "match": want == digest}
 
 
 def cluster(shape, P, D, cap_bps, caps=None, link_bps=PCIE_ZC_BPS):
@@ -130,10 +208,6 @@ def cluster(shape, P, D, cap_bps, caps=None, link_bps=PCIE_ZC_BPS):
     cfg.de_buffer_bytes = 1 << 42
     return cfg
 
-
-# ncu --set full of the K1 launch (profiles/r01_k1_full.ncu-rep): dram read +
-# write bytes per launch over the launch's algorithmic bytes (18.42 GB)
-TRAFFIC = {"c1": 18454911288, "c2": 18454911288}  # 85.6 MB read + 18.37 GB write
 
 # storage-bound cost model (proj/tests/acceptance.cpp:62-72): the bench
 # measures loading, compute is nearly free
@@ -350,6 +424,19 @@ def prefill_cost(args, shape):
     return (shape["b"] / (args.attend_tops * 1e12), 0.0, 0.0, 20e-6)
 
 
+def store_budget(args, dist):
+    """Host store per engine: the whole trace (no two sessions share a Full
+    Block), within half of this host's RAM shared by its local engines."""
+    if args.store_gb > 0:
+        return int(args.store_gb * 1e9)
+    try:
+        mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        mem = 64 << 30
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", str(max(1, dist.world))))
+    return max(8 << 30, mem // 2 // max(1, local))
+
+
 def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=None, link_bps=PCIE_ZC_BPS):
     """Plan, build engines, run W + K steps; returns per-step max-over-ranks
     device and host times, plus per-rank info.  variant = (policy, sched_mode)."""
@@ -389,6 +476,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
         opt.prefill = True
         opt.compute_quota = args.quota_ms * 1e-3
         opt.prefill_cost = prefill_cost(args, shape)
+    opt.store_bytes_max = store_budget(args, dist)
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     tier = None
     if args.tier:
@@ -419,7 +507,8 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
                     open_or_populate_s=round(time.time() - t0, 2))
         del f
     from paper_2602_21548_b200 import dist as dpdist
-    digests = dist.allgather(dpdist.plan_digest(planned))
+    digest = dpdist.plan_digest(planned)
+    digests = dist.allgather(digest)
     assert len(set(digests)) == 1, "ranks planned differently"
     if dist.world > 1:
         my = [dist.rank]
@@ -432,6 +521,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     if dist.world > 1:
         dpdist.connect_pools(dist, engines, cfg.prefill_nodes)
     dev_ms, host_ms, launches, read_bytes, spans, per_engine = [], [], 0, 0, None, None
+    r0_bytes, r0_ms = 0, 0.0  # rank 0's own engine over the timed steps (the roofline)
     io_wait = 0.0
     d2h = 0
     for step in range(args.warmup + args.steps):
@@ -450,6 +540,8 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
             io_wait = max(io_wait, dist.max(max(r.io_wait_ms for r in res)))
             d2h = sum(dist.allgather(sum(r.d2h_bytes for r in res)))  # per step (the same each step)
             read_bytes += sum(dist.allgather(sum(r.bytes_read for r in res)))
+            r0_bytes += res[0].bytes_read
+            r0_ms += res[0].device_ms
             spans, per_engine = {}, {}
             for part in dist.allgather({e: (r.spans, r.device_ms) for e, r in zip(engines, res)}):
                 for e, (sp, ms) in part.items():
@@ -468,7 +560,8 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
                    macs_per_step=work * shape["b"] * shape["L"],
                    est_s_per_step=sum(est for pe in range(P) for est, _ in xp.forwards(pe)) * shape["L"])
     snic = sum(u["total_bytes"] for u in planned["usage"] if u["kind"] == "snic_read")
-    info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens,
+    info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens, digest=digest,
+                r0_bytes=r0_bytes, r0_ms=r0_ms, policy=policy,
                 handoff_bytes=xp.handoff_bytes if (args.handoff or args.persist) else 0,
                 persist_bytes=xp.persist_bytes if args.persist else 0,
                 model_gbps=snic / planned["makespan"] / 1e9 if planned["makespan"] > 0 else None,
@@ -538,63 +631,155 @@ def cpu_baseline(xp, shape, seconds=12.0):
 
 
 # ---------------------------------------------------------------- reference
+def reference_trace(args, kind, sessions, path):
+    """The same trace, built by the REFERENCE (oracle/_ref = pdsim compiled
+    from /root/reference sources: its synthesize, proj/src/workload.cpp) or,
+    for config 2, written as a reference-format TSV -- no repo .so loaded."""
+    from oracle import refpy
+    if kind in ("c1", "c3"):
+        if getattr(args, "trace", ""):
+            with open(args.trace) as f, open(path, "w") as g:
+                for i, line in enumerate(f):
+                    if i >= sessions:
+                        break
+                    g.write(line)
+        else:
+            refpy.ref_synthesize(path, count=sessions, **GEN_C1)
+    else:
+        with open(path, "w") as f:
+            for i in range(sessions):
+                f.write(f"ctx{i}\t" + ",".join(f"{a}:{g}" for a, g in c2_rounds(i)) + "\n")
+    rounds = []
+    with open(path) as f:
+        for line in f:
+            _, r = line.rstrip("\n").split("\t")
+            rounds.append([tuple(int(v) for v in x.split(":")) for x in r.split(",")])
+    return rounds
+
+
 def reference_arm(args):
-    """The reference's own CPU implementation of the path: pdsim's
-    desim::run_offline, compiled from /root/reference sources into
-    oracle/_ref, run on this box's host (single-threaded by design,
-    SPEC.md:403) on a session sample of the same workload and P:D config.
-    The reference moves no bytes; its value of the metric is its own
-    aggregate KV-load GB/s for the workload: storage-read bytes / makespan
-    (the SnicRead ledger, desim.cpp:405-425, 956-987).  Wall time per run is
-    reported beside it."""
-    import paper_2602_21548_b200 as dp
+    """The reference's CPU implementation of the path, timed on this box's
+    host cores on the SAME workload and config as our arm.
+
+    The reference (pdsim) moves no bytes: its KV loading is a byte count in a
+    fluid flow.  Its CPU path is therefore the oracle port
+    (oracle/kvref.c, kind "port"): the memcpy gather of every request's hit
+    Layer Blocks C*L*b from the host store (Full Blocks [L][T][b]) into a host
+    paged pool [L][slot][T][b], on all host threads, over the full job list
+    of the trace (a bounded prefix when the list exceeds ~8 s of CPU per
+    step).  The trace comes from the reference's own generator and the
+    reference simulator desim::run_offline plans it once (its decisions'
+    digest and wall time are reported beside the value).  Only oracle/
+    libraries are loaded."""
+    import ctypes
+    import numpy as np
     from oracle import refpy
     n = args.gpus
-    trajs, shape = workload(args, n)
     P, D = (1, 1) if n == 1 else (n // 2, n - n // 2)
     if args.pd:
         P, D = (int(x) for x in args.pd.split(":"))
+    kind = args.workload
+    shape = QWEN if kind == "c3" else DSV3
+    sessions = n_sessions(args, n)
+    policy = "pe_only" if n == 1 else "dual_path"
     cap = args.cap_gbps * 1e9
-    # the same per-engine link rate our arm plans with on this box
-    ceiling = measure_host_ceiling_local(n) if n > 1 else None
-    link_bps = link_per_engine(ceiling, n)
-    cfg = cluster(shape, P, D, cap, None, link_bps)
-    sample = trajs[: max(2, min(len(trajs), 4 * n))]
-    path = f"/tmp/dp_ref_sample_{os.getpid()}.tsv"
-    dp.save_trace(path, sample)
-    kv = dict(P=P, D=D, g=1, L=shape["L"], b=shape["b"], T=shape["T"], B=cfg.cnic_bandwidth,
-              s=cfg.storage_multiple, M=cfg.dram_bandwidth, hbm=cfg.hbm_capacity_tokens,
-              pe_buf=cfg.pe_buffer_bytes, de_buf=cfg.de_buffer_bytes,
-              policy="pe_only" if n == 1 else "dual_path", **PLAN_KW)
-    vals, walls = [], []
+    path = f"/tmp/dp_ref_trace_{os.getpid()}.tsv"
     try:
-        for step in range(args.warmup + args.steps):
-            t0 = time.time()
-            rep = refpy.ref_simulate(path, **kv)
-            wall = time.time() - t0
-            snic = sum(u[4] for u in rep["usage"] if u[0] == "snic_read")
-            if step >= args.warmup:
-                vals.append(snic / rep["makespan"] / 1e9)
-                walls.append(wall)
+        rounds = reference_trace(args, kind, sessions, path)
+        stats = trace_stats(rounds, shape)
+        # the reference simulator on (a sample of) the trace: decisions + wall time
+        sim_sessions = min(sessions, 64 if n == 1 else 16)
+        sim_path = path + ".sim"
+        with open(path) as f, open(sim_path, "w") as g:
+            for i, line in enumerate(f):
+                if i < sim_sessions:
+                    g.write(line)
+        link_bps = PCIE_ZC_BPS
+        kv = dict(P=P, D=D, g=1, L=shape["L"], b=shape["b"], T=shape["T"], B=NVLINK_BPS,
+                  s=(cap if cap > 0 else link_bps) / NVLINK_BPS, M=2e12, hbm=100_000_000,
+                  pe_buf=1 << 42, de_buf=1 << 42, policy=policy, **PLAN_KW)
+        t0 = time.time()
+        rep = refpy.ref_simulate(sim_path, **kv)
+        sim_wall = time.time() - t0
+        os.unlink(sim_path)
     finally:
-        os.unlink(path)
-    v = statistics.median(vals)
+        if os.path.exists(path):
+            os.unlink(path)
+    import hashlib
+    h = hashlib.sha1()
+    for d in rep["decisions"]:
+        h.update(repr((d[1], d[2], d[3], d[4])).encode())
+
+    # the CPU port over the job list: every warm request's hit blocks
+    L, T, b = shape["L"], shape["T"], shape["b"]
+    g = refpy.geom(L, T, b)
+    fb_bytes, lb = L * T * b, T * b
+    stride = max(-(-sum(a + gg for a, gg in r) // T) for r in rounds)
+    n_fb = max(1, min(stride * sessions, (16 << 30) // fb_bytes))   # host store <= 16 GiB
+    n_slots = max(64, min(stride * 4, (8 << 30) // (L * lb)))       # host pool <= 8 GiB
+    threads = os.cpu_count() or 1
+    store = np.empty(n_fb * fb_bytes, dtype=np.uint8)
+    parts = [c for c in np.array_split(np.arange(n_fb), threads) if len(c)]
+    ths = [threading.Thread(target=lambda c=c: refpy.kvref().kvref_fill_store(
+        ctypes.byref(g), 9, int(c[0]), len(c), store[int(c[0]) * fb_bytes:].ctypes.data)) for c in parts]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    pool = np.zeros(L * n_slots * lb, dtype=np.uint8)
+    specs, moved, slot = [], 0, 0
+    budget = 8.0 * 45e9  # ~8 s of the r01 box's 16-thread rate
+    for s, rr in enumerate(rounds):
+        ctx = 0
+        for a, gg in rr:
+            if ctx > 0:
+                nblk = -(-ctx // T)
+                fbs = [(s * stride + k) % n_fb for k in range(nblk)]
+                slots = [(slot + k) % n_slots for k in range(nblk)]
+                slot = (slot + nblk) % n_slots
+                specs.append((fbs, slots, ctx, 0, L))
+                moved += ctx * L * b
+            ctx += a + gg
+    full = moved
+    if moved > 1.5 * budget:  # a bounded prefix of the job list
+        acc, keep = 0, []
+        for sp in specs:
+            if acc >= budget:
+                break
+            keep.append(sp)
+            acc += sp[2] * L * b
+        specs, moved = keep, acc
+    arr, keepalive = refpy.make_jobs(specs)
+    vals, total_bytes, total_s = [], 0, 0.0
+    for step in range(args.warmup + args.steps):
+        t0 = time.time()
+        nbytes = refpy.kvref().kvref_gather_mt(ctypes.byref(g), store.ctypes.data, arr, len(specs),
+                                               pool.ctypes.data, n_slots, threads)
+        dt = time.time() - t0
+        if step >= args.warmup:
+            vals.append(nbytes / dt / 1e9)
+            total_bytes += nbytes
+            total_s += dt
+    v = total_bytes / total_s / 1e9
+    sample = (f"the full job list ({len(specs)} requests, {moved / 1e9:.1f} GB of Layer Blocks) per step"
+              if moved == full else
+              f"the first {len(specs)} requests of the job list ({moved / 1e9:.1f} of {full / 1e9:.1f} GB) per step")
     return {"metric": "aggregate KV-load GB/s", "value": round(v, 3), "unit": "GB/s", "n_gpus": n,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "impl": "reference",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_s * 1e3 / args.steps, 1),
+            "higher_is_better": True, "impl": "reference", "scaling": "weak", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {len(sample)} sessions, "
-                                   + ("1P loader (pe_only)" if n == 1 else f"{P}P{D}D dual_path"),
-                       "kv": shape},
-            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "reference",
-                             "sample": f"desim::run_offline on {len(sample)} sessions of the workload "
-                                       f"(the reference simulator, 1 thread); value = its storage-read "
-                                       f"bytes / makespan; {statistics.median(walls):.2f} s wall per run"},
+            "config": config_dict(kind, sessions, P, D, policy, shape, args.cap_gbps, stats),
+            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                             "sample": f"oracle/kvref.c memcpy gather (the reference moves no bytes: "
+                                       f"SPEC.md:106), {threads} threads, {sample}"},
             "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "reference_wall_s_per_run": round(statistics.median(walls), 3),
-            "link_model": {"per_engine_gbps": round(link_bps / 1e9, 2),
-                           "concurrent_h2d_gbps": round(ceiling / 1e9, 2) if ceiling else None,
-                           "what": "the reference simulator's storage rate per engine: the same "
-                                   "min(51.5, box ceiling / N) our arm plans with"}}
+            "reference_sim": {"what": "desim::run_offline of the reference (oracle/_ref, 1 thread) on the "
+                                      f"first {sim_sessions} sessions of the same trace and config",
+                              "wall_s": round(sim_wall, 3), "decisions": len(rep["decisions"]),
+                              "decisions_digest": h.hexdigest(),
+                              "model_gbps": round(sum(u[4] for u in rep["usage"] if u[0] == "snic_read")
+                                                  / rep["makespan"] / 1e9, 3) if rep["makespan"] > 0 else None},
+            "same_config_as": "bench.py --impl ours with the same flags (config dict built identically)"}
 
 
 def storage_balance(spans, caps, n_engines, width=0.05, window=4):
@@ -631,18 +816,93 @@ def storage_balance(spans, caps, n_engines, width=0.05, window=4):
 
 
 # --------------------------------------------------------------------- main
+def relaunch_under_torchrun(n):
+    """`python bench.py --gpus N` without an external launcher: re-run this
+    script as N ranks under torch.distributed.run (one process per GPU)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def policy_rate(res, K):
+    s = sum(res["dev_ms"]) / 1e3
+    return res["info"]["hit_bytes"] * K / s / 1e9, res["info"]["prompt_tokens"] * K / s
+
+
+def plan_block(info, kind, sessions, P, D, cap_gbps, link_bps):
+    key = golden_key(kind, sessions, P, D, info["policy"], cap_gbps, link_bps)
+    return dict({"decisions": info["decisions"], "decisions_digest": info["digest"], "golden_key": key},
+                **golden_check(key, info["digest"]),
+                de_path_requests=info["de_path"],
+                read_gb_per_engine=[round(x / 1e9, 2) for x in info["reader_bytes"]],
+                last_step_ms_per_engine=info["per_engine_ms"], pool_slots=info["pool_slots"],
+                store_fb_per_engine=info["store_fb"], plan_s=round(info["plan_s"], 2))
+
+
+def capped_subrun(args, dist, n, P, D):
+    """BASELINE config 2 in the same line: 32K-128K contexts, every engine's
+    storage NIC capped (6.25 GB/s = a 400 Gbps SNIC per 8 GPUs), dual path vs
+    1-path -- the regime of the paper's headline (storage-bound prefill)."""
+    import copy
+    sub = copy.copy(args)
+    sub.cap_gbps, sub.steps, sub.warmup = args.capped_gbps, args.capped_steps, 1
+    sub.prefill = sub.handoff = sub.persist = False
+    sub.tier, sub.online, sub.caps = "", 0.0, ""
+    sessions = args.capped_sessions_per_gpu * n
+    trajs, shape = workload(sub, n, kind="c2", sessions=sessions)
+    out = {}
+    for name in ("dual_path", "pe_only"):
+        r = run_policy(sub, dist, (name, "adaptive"), trajs, shape, P, D, None)
+        v, tok = policy_rate(r, sub.steps)
+        out[name] = (v, tok, r["info"])
+    if dist.rank != 0:
+        return None
+    (dv, dt, di), (pv, pt, pi) = out["dual_path"], out["pe_only"]
+    stats = (di["requests"], di["hit_bytes"], di["prompt_tokens"])
+    return {"config": config_dict("c2", sessions, P, D, "dual_path", shape, sub.cap_gbps, stats),
+            "steps": sub.steps, "warmup": 1,
+            "value": round(dv, 3), "unit": "GB/s", "tokens_per_s": round(dt, 1),
+            "model_prediction_gbps": round(di["model_gbps"], 3) if di["model_gbps"] else None,
+            "ceiling_gbps": round((P + D) * sub.cap_gbps, 3),
+            "one_path": {"value": round(pv, 3), "tokens_per_s": round(pt, 1),
+                         "ceiling_gbps": round(P * sub.cap_gbps, 3),
+                         "plan": plan_block(pi, "c2", sessions, P, D, sub.cap_gbps, PCIE_ZC_BPS)},
+            "dual_vs_one_path": round(dv / pv, 3), "tokens_dual_vs_one_path": round(dt / pt, 3),
+            "plan": plan_block(di, "c2", sessions, P, D, sub.cap_gbps, PCIE_ZC_BPS)}
+
+
+def traffic_for(launch_bytes):
+    """DRAM bytes of the K1 launch measure_k1 runs, from the committed ncu
+    --set full capture of that same launch (profiles/k1_traffic.json)."""
+    path = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as f:
+        t = json.load(f)
+    if t.get("launch_bytes") != launch_bytes:
+        return None, None
+    return t["dram_bytes"], t["source"]
+
+
 def main():
     args = parse()
     if args.impl == "reference":
-        rank = int(os.environ.get("RANK", "0"))
-        if rank != 0:
+        if int(os.environ.get("RANK", "0")) != 0:
             return
         print(json.dumps(reference_arm(args)))
         return
-    import paper_2602_21548_b200 as dp  # noqa: F401  (fails loudly without the extension)
     n = args.gpus
+    if n > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(n))
+    import paper_2602_21548_b200 as dp  # noqa: F401  (fails loudly without the extension)
+    from paper_2602_21548_b200 import abi
     dist = make_group(n)
     trajs, shape = workload(args, n)
+    sessions = len(trajs)
     if args.pd:
         P, D = (int(x) for x in args.pd.split(":"))
     else:
@@ -657,11 +917,11 @@ def main():
     peak = None
     if dist.rank == 0:
         peak = measure_pcie_peak(my_device(dist))
-    # the box's aggregate host-link ceiling, measured before planning: the
-    # planner (the reference's model) then uses the per-engine rate this box
-    # actually sustains when every engine reads
+    # the box's aggregate host-link ceiling (reported; the planner's link
+    # model uses it only with --link-model measured)
     concurrent = measure_concurrent_h2d(dist, my_device(dist)) if dist.world > 1 else None
-    link_bps = link_per_engine(concurrent, n)
+    link_bps = link_per_engine(concurrent, n) if args.link_model == "measured" else PCIE_ZC_BPS
+    numa = dist.allgather(abi.device_numa_node(my_device(dist)))
     results = {}
     clocks = ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
                           if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_{os.getpid()}.csv")
@@ -672,6 +932,9 @@ def main():
     if args.prefill:  # the same loads without the prefill: the overlap baseline
         results["load_only"] = run_policy(args, dist, variants[0], trajs, shape, P, D, None, prefill=False,
                                           link_bps=link_bps)
+    capped = None
+    if n > 1 and not args.no_capped and args.online == 0 and not args.caps:
+        capped = capped_subrun(args, dist, n, P, D)
     head = results[policies[0]]
     info = head["info"]
     dev_s = sum(head["dev_ms"]) / 1e3
@@ -687,15 +950,22 @@ def main():
         except Exception as exc:  # reported, never fatal to the GPU number
             cpu = {"error": str(exc)[:200]}
     clk = clocks.summary(set(range(n)))
-    k1 = None
     if dist.rank == 0:
-        k1 = measure_k1(my_device(dist), shape)
-    if dist.rank == 0:
-        # roofline of the dominant kernel, K1 (K2 is the same kernel body with
-        # peer stores, 0.999x its rate, profiles/r01_k1_k2_events.json),
-        # measured live on rank 0 after the timed steps: algorithmic bytes
-        # (C*L*b of the launch) / CUDA-event time of the launch
-        achieved, k1_ms, k1_bytes = k1
+        # the dominant kernel alone (K1, one launch of 64 requests), for the
+        # ncu capture of the same launch
+        k1_alone, k1_ms, k1_bytes = measure_k1(my_device(dist), shape)
+        # roofline: rank 0's engine over the timed steps -- the PE's loads
+        # (K1 launches back to back on its load stream; at N > 1 also the
+        # wait for the DE pushes landing in its pool): algorithmic bytes
+        # C*L*b / CUDA-event time on that stream
+        achieved = info["r0_bytes"] / (info["r0_ms"] * 1e-3) / 1e9 if info["r0_ms"] > 0 else None
+        traffic, traffic_src = traffic_for(k1_bytes)
+        stats = (info["requests"], info["hit_bytes"], info["prompt_tokens"])
+        extra = {"k1": args.k1, "k2": args.k2}
+        if args.handoff_ctas:
+            extra["handoff_ctas"] = args.handoff_ctas
+        if args.pd:
+            extra["pd"] = args.pd
         out = {
             "metric": "aggregate KV-load GB/s",
             "value": round(value, 3),
@@ -709,15 +979,9 @@ def main():
             "vs_baseline": None,
             "dtype": "u8",
             "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {len(trajs)} sessions, "
-                                   + ("1 PE loader (K1)" if n == 1 else f"{P}P{D}D dual_path"),
-                       "kv": shape, "storage_cap_gbps_per_engine": args.cap_gbps or None,
-                       "k1": args.k1, "k2": args.k2, "handoff_ctas": args.handoff_ctas or None,
-                       "requests": info["requests"], "hit_bytes_per_step": info["hit_bytes"],
-                       "de_path_requests": info["de_path"],
-                       "read_gb_per_engine": [round(x / 1e9, 2) for x in info["reader_bytes"]],
-                       "last_step_ms_per_engine": info["per_engine_ms"],
-                       "l2": "inputs >> L2 (no flush needed)"},
+            "config": config_dict(args.workload, sessions, P, D, info["policy"] if args.online == 0 else
+                                  "dual_path", shape, args.cap_gbps, stats, extra),
+            "plan": plan_block(info, args.workload, sessions, P, D, args.cap_gbps, link_bps),
             "model_prediction_gbps": round(info["model_gbps"], 3) if info["model_gbps"] else None,
             "tokens_per_s": round(tokens_s, 1),
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",
@@ -727,23 +991,26 @@ def main():
                             "then the landed-counter column of every request read back and checked "
                             "(+ K4's persisted tokens with --persist)"},
             "gpu_launches": info["launches"],
-            "roofline": {"bound": "pcie", "achieved": round(achieved, 2),
+            "roofline": {"bound": "pcie", "achieved": round(achieved, 2) if achieved else None,
                          "peak": round(peak / 1e9, 2) if peak else None, "unit": "GB/s",
-                         "frac": round(achieved / (peak / 1e9), 4) if peak else None,
-                         "traffic": TRAFFIC.get(args.workload),
-                         "kernel": "kv_gather<false> (K1)", "launch_bytes": k1_bytes,
-                         "launch_ms": round(k1_ms, 3),
-                         "peak_source": "cudaMemcpyAsync H2D 1 GiB pinned, best of 5, measured in this run",
-                         "step_rate_per_engine": round(value / max(1, n), 2)},
+                         "frac": round(achieved / (peak / 1e9), 4) if (peak and achieved) else None,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": "kv_gather<false> (K1)" if args.k1 == "sm" else f"K1 ({args.k1})",
+                         "achieved_what": "rank 0's PE: hit bytes it loaded / CUDA-event time of its "
+                                          "load stream over the timed steps",
+                         "kernel_alone": {"achieved": round(k1_alone, 2), "launch_bytes": k1_bytes,
+                                          "launch_ms": round(k1_ms, 3),
+                                          "frac": round(k1_alone / (peak / 1e9), 4) if peak else None},
+                         "peak_source": "cudaMemcpyAsync H2D 1 GiB pinned (copy engine), best of 5, "
+                                        "measured in this run (MEASURED_PEAKS.json has no PCIe entry)"},
             "cpu_baseline": cpu,
             "clocks": clk,
+            "numa_node_per_rank": numa,
             "host_links": ({"concurrent_h2d_gbps": round(concurrent / 1e9, 2),
                             "value_frac": round(value / (concurrent / 1e9), 4),
-                            "per_engine_model_gbps": round(link_bps / 1e9, 2),
+                            "planner_link_gbps": round(link_bps / 1e9, 2), "link_model": args.link_model,
                             "what": "all ranks' copy-engine H2D at once: the box's aggregate host-link "
-                                    "ceiling for this line; the planner's per-engine storage rate is "
-                                    "min(51.5, ceiling / N)"} if concurrent else None),
-            "plan_s": round(info["plan_s"], 2),
+                                    "ceiling for this line"} if concurrent else None),
         }
         if args.online > 0:
             out["config"]["online_sessions_per_s"] = args.online
@@ -751,8 +1018,7 @@ def main():
             out["balance"] = {"adaptive": storage_balance(info["spans"], info["caps"], P + D)}
             if "round_robin" in results:
                 rr = results["round_robin"]
-                rr_s = sum(rr["dev_ms"]) / 1e3
-                rr_v = rr["info"]["hit_bytes"] * K / rr_s / 1e9
+                rr_v, _ = policy_rate(rr, K)
                 out["round_robin"] = {"value": round(rr_v, 3), "unit": "GB/s",
                                       "adaptive_vs_rr": round(value / rr_v, 3)}
                 out["balance"]["round_robin"] = storage_balance(rr["info"]["spans"], rr["info"]["caps"], P + D)
@@ -789,11 +1055,13 @@ def main():
                 "cost_model_s_per_step": round(pf["est_s_per_step"], 4)}
         if "pe_only" in results and n > 1:
             po = results["pe_only"]
-            po_s = sum(po["dev_ms"]) / 1e3
-            po_v = po["info"]["hit_bytes"] * K / po_s / 1e9
-            out["one_path"] = {"value": round(po_v, 3), "unit": "GB/s",
-                               "tokens_per_s": round(po["info"]["prompt_tokens"] * K / po_s, 1),
-                               "dual_vs_one_path": round(value / po_v, 3)}
+            po_v, po_tok = policy_rate(po, K)
+            out["one_path"] = {"value": round(po_v, 3), "unit": "GB/s", "tokens_per_s": round(po_tok, 1),
+                               "dual_vs_one_path": round(value / po_v, 3),
+                               "plan": plan_block(po["info"], args.workload, sessions, P, D, args.cap_gbps,
+                                                  link_bps)}
+        if capped:
+            out["storage_capped"] = capped
         print(json.dumps(out))
     dist.barrier()
     dist.close()

@@ -278,6 +278,7 @@ class EngineRuntime {
 
  private:
   void upload_tables();
+  void storage_read(const LoadJob& j, std::int64_t bytes, StepResult& res);
 
   std::shared_ptr<const ExecPlan> plan_;
   int engine_;
@@ -286,6 +287,7 @@ class EngineRuntime {
   void* ev_start_ = nullptr;
   void* ev_end_ = nullptr;
   dp_store* store_ = nullptr;
+  dp_nic* nic_ = nullptr;                   // emulated storage NIC (rate cap)
   dp_pool* pool_ = nullptr;                 // owned (PE only)
   std::vector<dp_pool*> peers_;             // per engine id: view of that PE's pool
   std::int64_t* d_src_ = nullptr;           // device block tables of this reader

@@ -105,6 +105,38 @@ int dp_store_create(int device, const dp_kv_geom* geom, int64_t n_fb, uint64_t s
 int dp_store_destroy(dp_store* store);
 int dp_store_info(const dp_store* store, void** host_ptr, int64_t* bytes, int64_t* n_fb);
 
+/* NUMA-placed staging (SURVEY.md §8(b) dp_staging_create): the PE / DE host
+ * buffer (pe_buffer_bytes / de_buffer_bytes, types.hpp:22-23) as pinned,
+ * device-mapped pages bound to one NUMA node (mmap + mbind + transparent huge
+ * pages + cudaHostRegister).  numa_node >= 0 binds to that node,
+ * DP_NUMA_DEVICE to the node of `device`'s PCIe root (sysfs), DP_NUMA_NONE
+ * leaves placement to the kernel.  dp_store_create == ..._on_node(DP_NUMA_DEVICE). */
+#define DP_NUMA_DEVICE (-1)
+#define DP_NUMA_NONE (-2)
+int dp_store_create_on_node(int device, const dp_kv_geom* geom, int64_t n_fb, uint64_t seed,
+                            int32_t numa_node, dp_store** out);
+/* The node the store's pages are bound to (-1: not bound / unknown). */
+int dp_store_numa_node(const dp_store* store, int32_t* node);
+/* NUMA node of the device's PCIe attachment (-1 when the platform has none). */
+int dp_device_numa_node(int device, int32_t* node);
+
+/* Emulated storage NIC (StorageRead over {snic_rd, dram}, desim.cpp:603-606):
+ * a FIFO token bucket at rate_Bps (0 = unlimited).  dp_nic_read blocks the
+ * calling thread until the NIC has delivered `bytes`: the transfer begins at
+ * max(NIC free, not_before_s) and lasts bytes / rate; times are seconds
+ * since dp_nic_start (optional outputs t_begin / t_end).  Thread-safe: the
+ * IO threads of an engine share its NIC. */
+typedef struct dp_nic dp_nic;
+int dp_nic_create(double rate_Bps, dp_nic** out);
+int dp_nic_destroy(dp_nic* nic);
+int dp_nic_start(dp_nic* nic);
+int dp_nic_read(dp_nic* nic, int64_t bytes, double not_before_s, double* t_begin, double* t_end);
+/* StorageRead emulation (SURVEY.md §8(b) dp_storage_read): paced by `nic`
+ * (may be NULL), materialise storage Full Blocks src_fb .. src_fb + n_fb - 1
+ * (the content formula above, the staging's seed) into staging positions
+ * dst_fb ..; synchronous. */
+int dp_storage_read(dp_store* staging, int64_t dst_fb, int64_t src_fb, int64_t n_fb, dp_nic* nic);
+
 /* Paged HBM pool with n_tickets rows of landed counters: row t holds one
  * counter per layer (items landed for that layer) and, in column n_layer,
  * the items landed over all layers of the ticket. */
@@ -303,8 +335,10 @@ int dp_stream_wait_counter(const dp_pool* pool, int32_t ticket, int32_t layer, u
  * stream-ordered work that has no kernel of its own to release a counter. */
 int dp_stream_write_counter(dp_pool* pool, int32_t ticket, int32_t layer, uint32_t value,
                             dp_stream stream);
-/* Returns DP_ETIMEOUT if any wait on this device's pool has timed out. */
+/* Returns DP_ETIMEOUT if any wait issued through this pool (or view) has timed out. */
 int dp_wait_status(const dp_pool* pool);
+/* Clears that watchdog flag (dp_pool_reset_counters does it for an owned pool). */
+int dp_wait_clear(dp_pool* pool);
 
 /* 64-bit content hash of each listed Layer Block (valid tokens only):
  *   H = sum_i splitmix64(word_i + (i + 1) * 0x9E3779B97F4A7C15)  (mod 2^64)

@@ -111,6 +111,17 @@ def lib():
         "dp_wait_tickets": ([P, P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P],
                             ctypes.c_int),
         "dp_wait_status": ([P], ctypes.c_int),
+        "dp_wait_clear": ([P], ctypes.c_int),
+        "dp_store_create_on_node": ([ctypes.c_int, ctypes.POINTER(Geom), ctypes.c_int64, ctypes.c_uint64,
+                                     ctypes.c_int32, PP], ctypes.c_int),
+        "dp_store_numa_node": ([P, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
+        "dp_device_numa_node": ([ctypes.c_int, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
+        "dp_nic_create": ([ctypes.c_double, PP], ctypes.c_int),
+        "dp_nic_destroy": ([P], ctypes.c_int),
+        "dp_nic_start": ([P], ctypes.c_int),
+        "dp_nic_read": ([P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
+                         ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+        "dp_storage_read": ([P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, P], ctypes.c_int),
         "dp_stream_wait_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
         "dp_stream_write_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
         "dp_decode_fill": ([P, ctypes.POINTER(SpanJob), ctypes.c_int32, ctypes.c_uint64, P], ctypes.c_int),
@@ -148,14 +159,27 @@ def geom(n_layer, block_tokens, b):
     return Geom(n_layer, block_tokens, b)
 
 
-class Store:
-    """Pinned+mapped host Full Blocks filled with the deterministic content."""
+NUMA_DEVICE, NUMA_NONE = -1, -2
 
-    def __init__(self, device, g, n_fb, seed):
+
+class Store:
+    """Pinned+mapped host Full Blocks filled with the deterministic content
+    (NUMA-bound to `numa_node`: NUMA_DEVICE = the GPU's own node)."""
+
+    def __init__(self, device, g, n_fb, seed, numa_node=NUMA_DEVICE):
         self.ptr = ctypes.c_void_p()
-        check(lib().dp_store_create(device, ctypes.byref(g), n_fb, seed, ctypes.byref(self.ptr)))
+        check(lib().dp_store_create_on_node(device, ctypes.byref(g), n_fb, seed, numa_node,
+                                            ctypes.byref(self.ptr)))
         self.geom = g
         self.n_fb = n_fb
+
+    def numa_node(self):
+        n = ctypes.c_int32()
+        check(lib().dp_store_numa_node(self.ptr, ctypes.byref(n)))
+        return n.value
+
+    def storage_read(self, dst_fb, src_fb, n_fb, nic=None):
+        check(lib().dp_storage_read(self.ptr, dst_fb, src_fb, n_fb, nic.ptr if nic else None))
 
     def info(self):
         host = ctypes.c_void_p()
@@ -223,6 +247,37 @@ class Pool:
         if self.ptr:
             check(lib().dp_pool_destroy(self.ptr))
             self.ptr = ctypes.c_void_p()
+
+
+class Nic:
+    """Emulated storage NIC: FIFO token bucket at rate_Bps (0 = unlimited)."""
+
+    def __init__(self, rate_Bps):
+        self.ptr = ctypes.c_void_p()
+        check(lib().dp_nic_create(rate_Bps, ctypes.byref(self.ptr)))
+
+    def start(self):
+        check(lib().dp_nic_start(self.ptr))
+
+    def read(self, nbytes, not_before_s=0.0):
+        b, e = ctypes.c_double(), ctypes.c_double()
+        check(lib().dp_nic_read(self.ptr, nbytes, not_before_s, ctypes.byref(b), ctypes.byref(e)))
+        return b.value, e.value
+
+    def close(self):
+        if self.ptr:
+            check(lib().dp_nic_destroy(self.ptr))
+            self.ptr = ctypes.c_void_p()
+
+
+def device_numa_node(device):
+    n = ctypes.c_int32()
+    check(lib().dp_device_numa_node(device, ctypes.byref(n)))
+    return n.value
+
+
+def wait_clear(pool):
+    return check(lib().dp_wait_clear(pool.ptr))
 
 
 def make_jobs(specs):

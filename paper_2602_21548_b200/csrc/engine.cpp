@@ -20,6 +20,52 @@
 
 namespace dualpath {
 
+namespace detail {
+
+namespace {
+struct StreamPool {
+  std::vector<cudaStream_t> free_lo, free_hi;
+};
+std::mutex g_stream_mu;
+std::vector<StreamPool> g_stream_pools;
+constexpr int kStreamBurst = 12;  // per priority; 24 < CUDA_DEVICE_MAX_CONNECTIONS = 32
+}  // namespace
+
+cudaStream_t acquire_stream(int device, bool high_priority) {
+  std::lock_guard<std::mutex> lk(g_stream_mu);
+  if (device < 0) throw std::invalid_argument("acquire_stream: bad device");
+  if (g_stream_pools.size() <= static_cast<std::size_t>(device)) g_stream_pools.resize(device + 1);
+  StreamPool& p = g_stream_pools[device];
+  auto& list = high_priority ? p.free_hi : p.free_lo;
+  if (list.empty()) {
+    DeviceScope ds(device);
+    int lo = 0, hi = 0;
+    check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+    for (int i = 0; i < kStreamBurst; ++i) {
+      cudaStream_t s;
+      check_cuda(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, high_priority ? hi : lo),
+                 "cudaStreamCreateWithPriority");
+      list.insert(list.begin(), s);
+    }
+  }
+  cudaStream_t s = list.back();
+  list.pop_back();
+  return s;
+}
+
+void release_stream(int device, cudaStream_t s) {
+  if (!s) return;
+  cudaStreamSynchronize(s);
+  int lo = 0, hi = 0, prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cudaStreamGetPriority(s, &prio);
+  std::lock_guard<std::mutex> lk(g_stream_mu);
+  auto& p = g_stream_pools[device];
+  (prio == hi && hi != lo ? p.free_hi : p.free_lo).push_back(s);
+}
+
+}  // namespace detail
+
 using detail::check;
 using detail::check_cuda;
 using detail::DeviceScope;
@@ -32,9 +78,7 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
     throw std::invalid_argument("EngineRuntime: engine out of range");
   const ExecPlan& x = *plan_;
   DeviceScope ds(device_);
-  cudaStream_t s;
-  check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-  stream_ = s;
+  stream_ = detail::acquire_stream(device_);
   cudaEvent_t a, b;
   check_cuda(cudaEventCreate(&a), "cudaEventCreate");
   check_cuda(cudaEventCreate(&b), "cudaEventCreate");
@@ -42,6 +86,10 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   ev_end_ = b;
   peers_.assign(x.n_engines, nullptr);
   de_views_.assign(x.n_engines, nullptr);
+  check(dp_nic_create(x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
+                                                           : x.opt.storage_cap_per_engine[engine_],
+                      &nic_),
+        "dp_nic_create");
   if (!x.by_reader[engine_].empty()) {
     // with the storage tier the store is the pinned staging ring the reads land in
     check(dp_store_create(device_, &x.geom, x.tier ? x.ring_fb : x.store_fb, x.opt.seed, &store_),
@@ -83,9 +131,7 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   }
   if (x.prefill && is_pe()) upload_prefill_tables();
   if (x.opt.k1_mode == 2 && is_pe() && !x.handoff && !x.prefill) {
-    cudaStream_t c;
-    check_cuda(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "cudaStreamCreate");
-    stream_ce_ = c;
+    stream_ce_ = detail::acquire_stream(device_);
     for (int k = 0; k < 2; ++k) {
       cudaEvent_t e;
       check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
@@ -115,6 +161,7 @@ EngineRuntime::~EngineRuntime() {
     if (v) dp_pool_destroy(v);
   if (pool_) dp_pool_destroy(pool_);
   if (store_) dp_store_destroy(store_);
+  dp_nic_destroy(nic_);
   if (persist_store_) dp_store_destroy(persist_store_);
   for (void* p : {static_cast<void*>(d_src_), static_cast<void*>(d_slots_),
                   static_cast<void*>(d_wait_tickets_), static_cast<void*>(d_wait_targets_),
@@ -132,11 +179,11 @@ EngineRuntime::~EngineRuntime() {
   for (void* e : ev_job_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   if (ev_start_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_start_));
   if (ev_end_) cudaEventDestroy(static_cast<cudaEvent_t>(ev_end_));
-  if (stream_h_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_h_));
-  if (stream_c_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_c_));
-  if (stream_ce_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_ce_));
+  detail::release_stream(device_, static_cast<cudaStream_t>(stream_h_));
+  detail::release_stream(device_, static_cast<cudaStream_t>(stream_c_));
+  detail::release_stream(device_, static_cast<cudaStream_t>(stream_ce_));
   for (void* e : ev_ce_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
-  if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+  detail::release_stream(device_, static_cast<cudaStream_t>(stream_));
 }
 
 void EngineRuntime::upload_tables() {
@@ -184,9 +231,7 @@ void EngineRuntime::upload_handoff_tables() {
     d_ho_src_ = upload(x.ho_src_fb[engine_]);
     d_ho_pe_ = upload(x.ho_pe_slot[engine_]);
     d_ho_de_ = upload(x.ho_de_slot[engine_]);
-    cudaStream_t h;
-    check_cuda(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking), "cudaStreamCreate");
-    stream_h_ = h;
+    stream_h_ = detail::acquire_stream(device_);
     const auto& mine = x.by_pe[engine_];
     for (std::size_t i = 0; i < mine.size(); ++i) {
       pe_local_[mine[i]] = static_cast<int>(i);
@@ -227,9 +272,7 @@ void EngineRuntime::upload_handoff_tables() {
   if (x.persist && !is_pe()) {
     d_dec_slot_ = upload(x.dec_slot[engine_]);
     d_dec_fb_ = upload(x.dec_fb[engine_]);
-    cudaStream_t h;
-    check_cuda(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking), "cudaStreamCreate");
-    stream_h_ = h;  // the decode stream: decode stand-in + persistence
+    stream_h_ = detail::acquire_stream(device_);  // the decode stream: decode stand-in + persistence
   }
 }
 
@@ -260,6 +303,12 @@ void EngineRuntime::attach_peer_local(int engine, const EngineRuntime& other) {
 }
 
 void EngineRuntime::reset_counters() {
+  // the watchdog flags of this engine's views of other pools are its own:
+  // clear them too, so one fired watchdog does not fail every later step
+  for (dp_pool* v : peers_)
+    if (v && v != pool_) check(dp_wait_clear(v), "dp_wait_clear");
+  for (dp_pool* v : de_views_)
+    if (v) check(dp_wait_clear(v), "dp_wait_clear");
   if (!pool_) return;
   DeviceScope ds(device_);
   check(dp_pool_reset_counters(pool_, stream_), "dp_pool_reset_counters");
@@ -303,6 +352,7 @@ StepResult EngineRuntime::run_step() {
   auto s = static_cast<cudaStream_t>(stream_);
   StepResult res;
   const auto t0 = std::chrono::steady_clock::now();
+  check(dp_nic_start(nic_), "dp_nic_start");
   check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_start_), s), "cudaEventRecord");
 
   const auto& mine = x.by_reader[engine_];
@@ -373,7 +423,6 @@ StepResult EngineRuntime::run_step() {
   const double cap = x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
                                                           : x.opt.storage_cap_per_engine[engine_];
   const double pace = x.opt.pace_scale;
-  double gate_s = 0;  // emulated storage-NIC busy-until (FIFO token bucket), s since t0
   for (std::size_t i = 0; i < mine.size(); ++i) {
     const LoadJob& j = x.jobs[mine[i]];
     if (!peers_[j.pe]) throw std::runtime_error("run_step: PE " + std::to_string(j.pe) + " not attached");
@@ -394,10 +443,7 @@ StepResult EngineRuntime::run_step() {
       // StorageRead of C*L*b bytes over this engine's storage NIC: starts
       // when the NIC is free (and, replaying online, not before the planned
       // admission), takes bytes / cap
-      const double begin = std::max(gate_s, pace > 0 ? j.t_admit * pace : 0.0);
-      gate_s = begin + (cap > 0 ? static_cast<double>(bytes) / cap : 0.0);
-      std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
-      res.spans.push_back({begin, gate_s, bytes});
+      storage_read(j, bytes, res);
     }
     if (tier && !tier->ready(static_cast<int>(i))) {  // StorageRead: the job's Full Blocks in staging
       flush();  // never hold launched work while waiting on the disk
@@ -457,6 +503,16 @@ StepResult EngineRuntime::run_step() {
   read_back_landed(res);
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return res;
+}
+
+// StorageRead of job j over this engine's emulated storage NIC (dp_nic): the
+// read starts when the NIC is free (and, replaying online, not before the
+// planned admission) and lasts bytes / cap; blocks until it is done.
+void EngineRuntime::storage_read(const LoadJob& j, std::int64_t bytes, StepResult& res) {
+  const double pace = plan_->opt.pace_scale;
+  double b = 0, e = 0;
+  check(dp_nic_read(nic_, bytes, pace > 0 ? j.t_admit * pace : 0.0, &b, &e), "dp_nic_read");
+  res.spans.push_back({b, e, bytes});
 }
 
 std::vector<std::uint64_t> EngineRuntime::checksum(int layer, std::span<const std::int32_t> slots,

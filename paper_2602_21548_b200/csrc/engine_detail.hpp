@@ -30,6 +30,15 @@ struct DeviceScope {
   }
 };
 
+// Executor streams come from a per-device pool created in one burst and
+// reused (never destroyed): the driver maps streams to its hardware queues
+// round-robin in creation order, so a burst of consecutive streams lands on
+// distinct queues.  Engines that share a GPU (the 1-GPU DE read path) then
+// never have one engine's blocked wait queued in front of the other's
+// producer, however many streams came and went before.
+cudaStream_t acquire_stream(int device, bool high_priority = false);
+void release_stream(int device, cudaStream_t s);
+
 template <class T>
 T* upload(const std::vector<T>& v) {
   if (v.empty()) return nullptr;

@@ -29,6 +29,7 @@ StepResult EngineRuntime::run_step_handoff() {
   auto h = static_cast<cudaStream_t>(stream_h_);
   StepResult res;
   const auto t0 = std::chrono::steady_clock::now();
+  check(dp_nic_start(nic_), "dp_nic_start");
   auto start = static_cast<cudaEvent_t>(ev_start_);
   check_cuda(cudaEventRecord(start, s), "cudaEventRecord");
   if (h) check_cuda(cudaStreamWaitEvent(h, start, 0), "cudaStreamWaitEvent");
@@ -37,14 +38,10 @@ StepResult EngineRuntime::run_step_handoff() {
                                                           : x.opt.storage_cap_per_engine[engine_];
   const double pace = x.opt.pace_scale;
   const bool gated = cap > 0 || pace > 0;
-  double gate_s = 0;
   auto storage_gate = [&](const LoadJob& j) {
     const std::int64_t bytes = j.cached * x.cfg.kv_bytes_per_token();
     if (gated) {
-      const double begin = std::max(gate_s, pace > 0 ? j.t_admit * pace : 0.0);
-      gate_s = begin + (cap > 0 ? static_cast<double>(bytes) / cap : 0.0);
-      std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
-      res.spans.push_back({begin, gate_s, bytes});
+      storage_read(j, bytes, res);
     }
     res.bytes_read += bytes;
     ++res.jobs;

@@ -23,17 +23,11 @@ void EngineRuntime::upload_prefill_tables() {
   const auto& items = x.fwd_items[engine_];
   const auto& fwds = x.forwards[engine_];
   const std::int32_t L = x.cfg.n_layer;
-  cudaStream_t c;
-  check_cuda(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "cudaStreamCreate");
-  stream_c_ = c;  // the compute stream: forwards
+  stream_c_ = detail::acquire_stream(device_);  // the compute stream: forwards
   // the load stream outranks the compute stream: as K5 CTAs retire, the
   // block scheduler places pending loader CTAs first
-  int lo = 0, hi = 0;
-  check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
-  cudaStream_t s;
-  check_cuda(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi), "cudaStreamCreateWithPriority");
-  check_cuda(cudaStreamDestroy(static_cast<cudaStream_t>(stream_)), "cudaStreamDestroy");
-  stream_ = s;
+  detail::release_stream(device_, static_cast<cudaStream_t>(stream_));
+  stream_ = detail::acquire_stream(device_, /*high_priority=*/true);
   d_fwd_slot_ = upload(x.fwd_slot[engine_]);
   const std::size_t rows = std::max<std::size_t>(1, x.fwd_rows[engine_].size());
   check_cuda(cudaMalloc(reinterpret_cast<void**>(&d_digest_), rows * L * sizeof(std::uint64_t)),
@@ -89,6 +83,7 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
   auto c = static_cast<cudaStream_t>(stream_c_);
   StepResult res;
   const auto t0 = std::chrono::steady_clock::now();
+  check(dp_nic_start(nic_), "dp_nic_start");
   auto start = static_cast<cudaEvent_t>(ev_start_);
   auto end = static_cast<cudaEvent_t>(ev_end_);
   check_cuda(cudaEventRecord(start, s), "cudaEventRecord");
@@ -124,7 +119,6 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
     const double cap = x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
                                                             : x.opt.storage_cap_per_engine[engine_];
     const double pace = x.opt.pace_scale;
-    double gate_s = 0;
     // enqueue forwards whose requests' loads are all enqueued (row < r)
     auto forwards_before = [&](std::size_t r) {
       while (fi < fwds.size() && static_cast<std::size_t>(fwds[fi].last_row) < r) {
@@ -154,10 +148,7 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
         check_cuda(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[w]]), 0),
                    "cudaStreamWaitEvent");
       if (gated) {
-        const double begin = std::max(gate_s, pace > 0 ? j.t_admit * pace : 0.0);
-        gate_s = begin + (cap > 0 ? static_cast<double>(bytes) / cap : 0.0);
-        std::this_thread::sleep_until(t0 + std::chrono::duration<double>(gate_s));
-        res.spans.push_back({begin, gate_s, bytes});
+        storage_read(j, bytes, res);
       }
       if (k1_ce)
         batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,

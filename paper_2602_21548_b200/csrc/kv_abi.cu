@@ -21,8 +21,13 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
+#include <cctype>
 #include <mutex>
 #include <cstdint>
 #include <cstdio>
@@ -45,6 +50,14 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+
+}  // namespace
+
+namespace dualpath::detail {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace dualpath::detail
+
+namespace {
 
 #define DP_CUDA(call)                                                              \
   do {                                                                             \
@@ -247,14 +260,15 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// word(p, w) = splitmix64((p << 32 | w) ^ seed*kSeedMul), two words per thread.
+// word(p, w) = splitmix64((p << 32 | w) ^ seed*kSeedMul), two words per thread;
+// dst holds Full Blocks fb0, fb0 + 1, ... (the content is keyed on p).
 __global__ void kv_store_fill(uint64_t* dst, int64_t n_pairs, int64_t words_per_fb,
-                              uint64_t seed_mix) {
+                              uint64_t seed_mix, int64_t fb0) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_pairs;
        i += stride) {
     const int64_t w0 = 2 * i;
-    const uint64_t fb = static_cast<uint64_t>(w0 / words_per_fb);
+    const uint64_t fb = static_cast<uint64_t>(fb0 + w0 / words_per_fb);
     const uint64_t w = static_cast<uint64_t>(w0 % words_per_fb);
     const uint64_t a = splitmix64(((fb << 32) | w) ^ seed_mix);
     const uint64_t b = splitmix64(((fb << 32) | (w + 1)) ^ seed_mix);
@@ -292,6 +306,9 @@ struct dp_store {
   uint64_t seed = 0;
   char* host = nullptr;
   int64_t bytes = 0;
+  int numa_node = -1;       // node the pages are bound to (-1: not bound)
+  bool registered = false;  // mmap + cudaHostRegister (else cudaHostAlloc)
+  int64_t map_bytes = 0;
 };
 
 struct dp_pool {
@@ -312,6 +329,13 @@ struct dp_pool {
 namespace {
 
 int64_t counters_offset(int64_t data_bytes) { return (data_bytes + 255) / 256 * 256; }
+
+// Loads every kernel of this library on `device` (defined at the end of the
+// file, after the last kernel).  With CUDA's lazy loading a kernel is loaded
+// at its first launch, and a load waits for the device's running kernels: a
+// spin-waiting consumer (K3's layer gate, kv_wait_many) would then hold back
+// the very launch of its producer when both share a GPU.
+int preload_kernels(int device);
 
 int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
                   dp_stream stream, bool peer) {
@@ -395,46 +419,145 @@ int dp_geom_check(const dp_kv_geom* g) {
   return DP_OK;
 }
 
-int dp_store_create(int device, const dp_kv_geom* geom, int64_t n_fb, uint64_t seed,
-                    dp_store** out) {
+int dp_device_numa_node(int device, int32_t* node) {
+  if (!node) return fail(DP_EINVAL, "device_numa_node: null out");
+  *node = -1;
+  char bus[64] = {0};
+  DP_CUDA(cudaDeviceGetPCIBusId(bus, sizeof(bus), device));
+  for (char* c = bus; *c; ++c) *c = static_cast<char>(std::tolower(static_cast<unsigned char>(*c)));
+  const std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+  if (FILE* f = std::fopen(path.c_str(), "r")) {
+    int n = -1;
+    if (std::fscanf(f, "%d", &n) == 1 && n >= 0) *node = n;
+    std::fclose(f);
+  }
+  return DP_OK;
+}
+
+namespace {
+
+// Pinned, device-mapped host memory whose pages live on NUMA node `node`
+// (mmap + mbind(MPOL_BIND) + transparent huge pages + cudaHostRegister);
+// falls back to cudaHostAlloc when the node is unknown or binding fails.
+int alloc_store_pages(dp_store* st, int node) {
+  if (node >= 0 && node < 128) {
+    const int64_t huge = int64_t{2} << 20;
+    const int64_t len = (st->bytes + huge - 1) / huge * huge;
+    void* p = mmap(nullptr, static_cast<size_t>(len), PROT_READ | PROT_WRITE,
+                   MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (p != MAP_FAILED) {
+      unsigned long mask[2] = {0, 0};
+      mask[node / 64] = 1ul << (node % 64);
+      const long rc = syscall(SYS_mbind, p, static_cast<unsigned long>(len), 2 /* MPOL_BIND */, mask,
+                              129ul, 0u);
+      madvise(p, static_cast<size_t>(len), MADV_HUGEPAGE);  // fewer IOMMU / TLB entries
+      if (rc == 0 && cudaHostRegister(p, static_cast<size_t>(len),
+                                      cudaHostRegisterMapped | cudaHostRegisterPortable) == cudaSuccess) {
+        st->host = static_cast<char*>(p);
+        st->registered = true;
+        st->map_bytes = len;
+        st->numa_node = node;
+        return DP_OK;
+      }
+      cudaGetLastError();
+      munmap(p, static_cast<size_t>(len));
+    }
+  }
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&st->host), st->bytes,
+                                cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess)
+    return fail(DP_ENOMEM, std::string("store_create: cudaHostAlloc: ") + cudaGetErrorString(e));
+  return DP_OK;
+}
+
+void free_store_pages(dp_store* st) {
+  if (!st->host) return;
+  if (st->registered) {
+    cudaHostUnregister(st->host);
+    munmap(st->host, static_cast<size_t>(st->map_bytes));
+  } else {
+    cudaFreeHost(st->host);
+  }
+  cudaGetLastError();
+  st->host = nullptr;
+}
+
+// Full Blocks [dst_fb, dst_fb + n) of `st` <- content of Full Blocks src_fb.. (GPU fill
+// on the store's device, zero-copy stores over its PCIe link), synchronous.
+int fill_store_range(dp_store* st, int64_t dst_fb, int64_t src_fb, int64_t n) {
+  const dp_kv_geom& g = st->geom;
+  const int64_t fb = static_cast<int64_t>(g.n_layer) * g.block_tokens * g.bytes_per_token_layer;
+  DeviceGuard guard(st->device);
+  cudaStream_t s;
+  DP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  kv_store_fill<<<sm_count(st->device) * 8, kThreads, 0, s>>>(
+      reinterpret_cast<uint64_t*>(st->host + dst_fb * fb), n * fb / 16, fb / 8, st->seed * kSeedMul, src_fb);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess) return fail(DP_ECUDA, std::string("store fill: ") + cudaGetErrorString(e));
+  return DP_OK;
+}
+
+}  // namespace
+
+int dp_store_create_on_node(int device, const dp_kv_geom* geom, int64_t n_fb, uint64_t seed,
+                            int32_t numa_node, dp_store** out) {
   if (!out) return fail(DP_EINVAL, "store_create: null out");
   *out = nullptr;
   if (int rc = dp_geom_check(geom)) return rc;
   if (n_fb < 1) return fail(DP_EINVAL, "store_create: n_fb must be >= 1");
-  DeviceGuard guard(device);
+  if (numa_node < DP_NUMA_NONE) return fail(DP_EINVAL, "store_create: bad NUMA node");
+  if (int rc = preload_kernels(device)) return rc;
+  int32_t node = numa_node;
+  if (numa_node == DP_NUMA_DEVICE)
+    if (int rc = dp_device_numa_node(device, &node)) return rc;
   auto* st = new dp_store;
   st->device = device;
   st->geom = *geom;
   st->n_fb = n_fb;
   st->seed = seed;
-  const int64_t fb = static_cast<int64_t>(geom->n_layer) * geom->block_tokens *
-                     geom->bytes_per_token_layer;
-  st->bytes = fb * n_fb;
-  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&st->host), st->bytes,
-                                cudaHostAllocMapped | cudaHostAllocPortable);
-  if (e != cudaSuccess) {
+  st->bytes = static_cast<int64_t>(geom->n_layer) * geom->block_tokens * geom->bytes_per_token_layer * n_fb;
+  if (int rc = alloc_store_pages(st, node == DP_NUMA_NONE ? -1 : node)) {
     delete st;
-    return fail(DP_ENOMEM, std::string("store_create: cudaHostAlloc: ") + cudaGetErrorString(e));
+    return rc;
   }
-  const int64_t n_pairs = st->bytes / 16;
-  const int grid = sm_count(device) * 8;
-  kv_store_fill<<<grid, kThreads>>>(reinterpret_cast<uint64_t*>(st->host), n_pairs, fb / 8,
-                                    seed * kSeedMul);
-  e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
-    cudaFreeHost(st->host);
+  if (int rc = fill_store_range(st, 0, 0, n_fb)) {
+    free_store_pages(st);
     delete st;
-    return fail(DP_ECUDA, std::string("store_create: fill: ") + cudaGetErrorString(e));
+    return rc;
   }
   *out = st;
   return DP_OK;
 }
 
+int dp_store_create(int device, const dp_kv_geom* geom, int64_t n_fb, uint64_t seed,
+                    dp_store** out) {
+  return dp_store_create_on_node(device, geom, n_fb, seed, DP_NUMA_DEVICE, out);
+}
+
 int dp_store_destroy(dp_store* st) {
   if (!st) return DP_OK;
-  if (st->host) DP_CUDA(cudaFreeHost(st->host));
+  free_store_pages(st);
   delete st;
+  return DP_OK;
+}
+
+int dp_storage_read(dp_store* staging, int64_t dst_fb, int64_t src_fb, int64_t n_fb, dp_nic* nic) {
+  if (!staging || n_fb < 0 || dst_fb < 0 || src_fb < 0 || dst_fb + n_fb > staging->n_fb ||
+      src_fb > (int64_t{1} << 31) - n_fb)
+    return fail(DP_EINVAL, "storage_read: range out of bounds");
+  if (n_fb == 0) return DP_OK;
+  const dp_kv_geom& g = staging->geom;
+  const int64_t bytes = static_cast<int64_t>(g.n_layer) * g.block_tokens * g.bytes_per_token_layer * n_fb;
+  if (nic)
+    if (int rc = dp_nic_read(nic, bytes, 0.0, nullptr, nullptr)) return rc;
+  return fill_store_range(staging, dst_fb, src_fb, n_fb);
+}
+
+int dp_store_numa_node(const dp_store* st, int32_t* node) {
+  if (!st || !node) return fail(DP_EINVAL, "store_numa_node: null argument");
+  *node = st->numa_node;
   return DP_OK;
 }
 
@@ -452,6 +575,7 @@ int dp_pool_create(int device, const dp_kv_geom* geom, int32_t n_slots, int32_t 
   *out = nullptr;
   if (int rc = dp_geom_check(geom)) return rc;
   if (n_slots < 1 || n_tickets < 0) return fail(DP_EINVAL, "pool_create: bad sizes");
+  if (int rc = preload_kernels(device)) return rc;
   DeviceGuard guard(device);
   auto* pool = new dp_pool;
   pool->device = pool->home_device = device;
@@ -539,6 +663,7 @@ int dp_pool_import(int device, const dp_pool_handle* h, dp_pool** out) {
   if (!h || !out) return fail(DP_EINVAL, "pool_import: null argument");
   *out = nullptr;
   if (int rc = dp_geom_check(&h->geom)) return rc;
+  if (int rc = preload_kernels(device)) return rc;
   DeviceGuard guard(device);
   cudaIpcMemHandle_t ih;
   std::memcpy(&ih, h->ipc, 64);
@@ -570,15 +695,24 @@ int dp_pool_import(int device, const dp_pool_handle* h, dp_pool** out) {
 int dp_pool_peer_view(int device, const dp_pool* pool, dp_pool** out) {
   if (!pool || !out) return fail(DP_EINVAL, "pool_peer_view: null argument");
   *out = nullptr;
-  if (device == pool->device) return fail(DP_EINVAL, "pool_peer_view: same device");
-  int can = 0;
-  DP_CUDA(cudaDeviceCanAccessPeer(&can, device, pool->device));
-  if (!can) return fail(DP_EINVAL, "pool_peer_view: no P2P path between devices");
+  // A view on the pool's own device is a second, non-owning handle on the same
+  // allocation: a PE and a DE engine sharing one GPU (the 1-GPU DE read path)
+  // then run the very kernels (K2 / dual / K3, system-scope releases) of the
+  // cross-GPU case, their stores landing in local HBM instead of over NVLink.
+  if (device != pool->device) {
+    int can = 0;
+    DP_CUDA(cudaDeviceCanAccessPeer(&can, device, pool->device));
+    if (!can) return fail(DP_EINVAL, "pool_peer_view: no P2P path between devices");
+  }
+  if (int rc = preload_kernels(device)) return rc;
   DeviceGuard guard(device);
-  cudaError_t e = cudaDeviceEnablePeerAccess(pool->device, 0);
-  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
-    return fail(DP_ECUDA, std::string("pool_peer_view: ") + cudaGetErrorString(e));
-  cudaGetLastError();
+  if (device != pool->device) {
+    cudaError_t pe = cudaDeviceEnablePeerAccess(pool->device, 0);
+    if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+      return fail(DP_ECUDA, std::string("pool_peer_view: ") + cudaGetErrorString(pe));
+    cudaGetLastError();
+  }
+  cudaError_t e = cudaSuccess;
   auto* v = new dp_pool(*pool);
   v->device = device;
   v->owner = false;
@@ -813,6 +947,12 @@ int dp_wait_status(const dp_pool* pool) {
   if (!pool) return fail(DP_EINVAL, "wait_status: null pool");
   if (pool->err_host && *reinterpret_cast<volatile int*>(pool->err_host))
     return fail(DP_ETIMEOUT, "wait_layer: watchdog fired (producer never released the layer)");
+  return DP_OK;
+}
+
+int dp_wait_clear(dp_pool* pool) {
+  if (!pool) return fail(DP_EINVAL, "wait_clear: null pool");
+  if (pool->err_host) *reinterpret_cast<volatile int*>(pool->err_host) = 0;
   return DP_OK;
 }
 
@@ -1582,3 +1722,38 @@ int dp_prefill_attend(const dp_pool* pool, int32_t layer, const dp_attend_item* 
 }
 
 }  // extern "C"
+
+// ============================================================ eager loading
+namespace {
+
+std::once_flag g_preload_once[kMaxDevices];
+int g_preload_rc[kMaxDevices] = {};
+
+int preload_kernels(int device) {
+  if (device < 0 || device >= kMaxDevices) return fail(DP_EINVAL, "device id out of range");
+  std::call_once(g_preload_once[device], [device] {
+    DeviceGuard guard(device);
+    const void* fns[] = {reinterpret_cast<const void*>(kv_gather<false>),
+                         reinterpret_cast<const void*>(kv_gather<true>),
+                         reinterpret_cast<const void*>(kv_wait_ge),
+                         reinterpret_cast<const void*>(kv_wait_many),
+                         reinterpret_cast<const void*>(kv_block_checksum),
+                         reinterpret_cast<const void*>(kv_store_fill),
+                         reinterpret_cast<const void*>(kv_gather_dual),
+                         reinterpret_cast<const void*>(kv_prefill_handoff),
+                         reinterpret_cast<const void*>(kv_decode_fill),
+                         reinterpret_cast<const void*>(kv_persist_d2h),
+                         reinterpret_cast<const void*>(kv_prefill_attend)};
+    for (const void* f : fns) {
+      cudaFuncAttributes a;
+      if (cudaFuncGetAttributes(&a, f) != cudaSuccess) {
+        g_preload_rc[device] = fail(DP_ECUDA, std::string("preload_kernels: ") +
+                                                  cudaGetErrorString(cudaGetLastError()));
+        return;
+      }
+    }
+  });
+  return g_preload_rc[device];
+}
+
+}  // namespace

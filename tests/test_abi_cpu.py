@@ -59,3 +59,44 @@ def test_pool_handle_layout_is_128_bytes():
     assert ctypes.sizeof(abi.PoolHandle) == 128
     assert ctypes.sizeof(abi.Job) == 40
     assert ctypes.sizeof(abi.Geom) == 16
+
+
+def test_nic_is_a_fifo_token_bucket():
+    """dp_nic (StorageRead's rate cap, desim.cpp:603-606): FIFO at the rate,
+    not_before honoured, thread-safe; rate 0 = unlimited."""
+    import threading
+    import time
+    nic = abi.Nic(1e9)  # 1 GB/s
+    try:
+        nic.start()
+        t0 = time.monotonic()
+        b, e = nic.read(50_000_000)
+        assert (b, round(e, 6)) == (0.0, 0.05)
+        b2, e2 = nic.read(20_000_000, not_before_s=0.1)  # idle gap until 0.1 s
+        assert round(b2, 6) == 0.1 and round(e2, 6) == 0.12
+        assert time.monotonic() - t0 >= 0.119
+        spans = []
+        ths = [threading.Thread(target=lambda: spans.append(nic.read(10_000_000))) for _ in range(4)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        spans.sort()
+        assert [round(s, 6) for s, _ in spans] == [0.12, 0.13, 0.14, 0.15]  # served back to back
+    finally:
+        nic.close()
+    free = abi.Nic(0.0)
+    free.start()
+    assert free.read(1 << 40) == (0.0, 0.0)
+    free.close()
+    with pytest.raises(abi.DualPathError):
+        abi.Nic(-1.0)
+
+
+def test_new_entry_points_reject_bad_arguments():
+    L = abi.lib()
+    assert L.dp_storage_read(None, 0, 0, 1, None) == abi.DP_EINVAL
+    assert L.dp_store_numa_node(None, None) == abi.DP_EINVAL
+    assert L.dp_wait_clear(None) == abi.DP_EINVAL
+    assert L.dp_nic_read(None, 1, 0.0, None, None) == abi.DP_EINVAL
+    assert L.dp_device_numa_node(0, None) == abi.DP_EINVAL

@@ -72,3 +72,54 @@ def test_trace_workload(tmp_path):
     trajs, shape = bench.workload(a, 2)
     assert [t.id for t in trajs] == [t.id for t in dp.load_trace(p)[:4]]
     assert shape["L"] == 61
+
+
+@pytest.mark.parametrize("wl", ["c1", "c2", "c3"])
+def test_trace_stats_match_the_exec_plan(wl):
+    """The config dict both arms print (requests, hit bytes, prompt tokens)
+    is computed from the trace alone and equals the executor plan's."""
+    a = Args()
+    a.workload = wl
+    a.sessions_per_gpu = 3
+    trajs, shape = bench.workload(a, 1)
+    stats = bench.trace_stats([[(r.append_tokens, r.gen_tokens) for r in t.rounds] for t in trajs], shape)
+    cfg = bench.cluster(shape, 1, 1, 0.0)
+    planned = dp.plan(cfg, trajs, policy="pe_only", **bench.PLAN_KW)
+    xp = dp.build_exec_plan(cfg, trajs, planned, dp.ExecOptions())
+    assert stats == (xp.requests, xp.hit_bytes, xp.prompt_tokens)
+
+
+@pytest.mark.parametrize("wl", ["c1", "c2"])
+def test_reference_trace_is_the_product_trace(tmp_path, wl):
+    """The reference arm builds its trace with the reference's own generator
+    (oracle/_ref): identical rounds to the product's synthesize."""
+    from oracle import refpy
+    if not refpy.ref_available():
+        pytest.skip("oracle/_ref not built")
+    a = Args()
+    a.workload = wl
+    a.trace = ""
+    rounds = bench.reference_trace(a, wl, 5, str(tmp_path / "t.tsv"))
+    trajs, _ = bench.workload(a, 1, sessions=5)
+    assert rounds == [[(r.append_tokens, r.gen_tokens) for r in t.rounds] for t in trajs]
+
+
+def test_reference_arm_loads_no_repo_library():
+    """bench.py --impl reference times the CPU port on the same config and
+    never loads the product (libdualpath.so / _core)."""
+    import json
+    import subprocess
+    from oracle import refpy
+    if not refpy.ref_available():
+        pytest.skip("oracle/_ref not built")
+    code = ("import sys, json; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0',"
+            " '--sessions-per-gpu', '2']; import bench; a = bench.parse(); line = bench.reference_arm(a);"
+            " maps = open('/proc/self/maps').read();"
+            " print(json.dumps({'line': line, 'product': ('libdualpath' in maps) or ('_core.cpython' in maps)}))")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, check=True)
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["product"] is False
+    line = res["line"]
+    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port"
+    assert line["config"]["sessions"] == 2 and line["config"]["requests"] == 40
+    assert line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0

@@ -105,9 +105,8 @@ def test_slot_reuse_same_reader(gpus):
     verify_pool(eng, xp, cfg)
 
 
-@pytest.mark.multigpu
 @pytest.mark.parametrize("policy", ["dual_path", "pe_only", "round_robin"])
-def test_two_engines_1p1d(two_gpus, policy):
+def test_two_engines_1p1d(de_dev, policy):
     cfg = cluster(1, 1)
     trajs = small_trace(count=8, turns=5)
     kw = dict(STORAGE_BOUND)
@@ -119,7 +118,7 @@ def test_two_engines_1p1d(two_gpus, policy):
     opt.seed = SEED
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     pe = dp.EngineRuntime(xp, 0, 0)
-    de = dp.EngineRuntime(xp, 1, 1)
+    de = dp.EngineRuntime(xp, 1, de_dev)
     de.attach_peer_local(0, pe)
     if policy != "pe_only":
         assert xp.reader_bytes[1] > 0, "dual path should read on the DE side"
@@ -131,8 +130,7 @@ def test_two_engines_1p1d(two_gpus, policy):
     verify_pool(pe, xp, cfg)
 
 
-@pytest.mark.multigpu
-def test_cross_reader_slot_reuse_hazards(two_gpus):
+def test_cross_reader_slot_reuse_hazards(de_dev):
     # tight pool: slots freed by a DE-path job get reused by PE-path jobs and
     # vice versa; the hazard waits keep the final pool equal to the oracle's
     cfg = cluster(1, 1, L=4)
@@ -145,7 +143,7 @@ def test_cross_reader_slot_reuse_hazards(two_gpus):
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     assert any(job[11] for job in xp.jobs()), "expected cross-reader reuse"
     pe = dp.EngineRuntime(xp, 0, 0)
-    de = dp.EngineRuntime(xp, 1, 1)
+    de = dp.EngineRuntime(xp, 1, de_dev)
     de.attach_peer_local(0, pe)
     for _ in range(3):
         pe.reset_counters()
@@ -153,8 +151,7 @@ def test_cross_reader_slot_reuse_hazards(two_gpus):
         verify_pool(pe, xp, cfg)
 
 
-@pytest.mark.multigpu
-def test_two_engines_k1_on_copy_engine(two_gpus):
+def test_two_engines_k1_on_copy_engine(de_dev):
     cfg = cluster(1, 1)
     trajs = small_trace(count=8, turns=5)
     planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
@@ -163,7 +160,7 @@ def test_two_engines_k1_on_copy_engine(two_gpus):
     opt.k1_mode = 1
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     pe = dp.EngineRuntime(xp, 0, 0)
-    de = dp.EngineRuntime(xp, 1, 1)
+    de = dp.EngineRuntime(xp, 1, de_dev)
     de.attach_peer_local(0, pe)
     for _ in range(2):
         pe.reset_counters()
@@ -202,10 +199,12 @@ def verify_prompt_pool(engine, xp, cfg):
     return len(slots)
 
 
-def handoff_engines(xp, n):
+def handoff_engines(xp, n, devices=None):
+    """Engine e on devices[e] (default: GPU e); engines may share a GPU."""
     import torch
-    assert torch.cuda.device_count() >= n
-    rts = [dp.EngineRuntime(xp, e, e) for e in range(n)]
+    devices = list(range(n)) if devices is None else devices
+    assert torch.cuda.device_count() > max(devices)
+    rts = [dp.EngineRuntime(xp, e, devices[e]) for e in range(n)]
     for a in rts:
         for b in rts:
             if a is not b and b.has_pool and ((a.is_pe and not b.is_pe) or (b.is_pe and not a.is_pe)):
@@ -213,10 +212,9 @@ def handoff_engines(xp, n):
     return rts
 
 
-@pytest.mark.multigpu
 @pytest.mark.parametrize("policy,tight,layer_gate", [("dual_path", False, 0), ("dual_path", True, 0),
                                                      ("pe_only", True, 0), ("dual_path", True, 1)])
-def test_handoff_1p1d(two_gpus, policy, tight, layer_gate):
+def test_handoff_1p1d(de_dev, policy, tight, layer_gate):
     cfg = cluster(1, 1, L=6)
     trajs = small_trace(count=8, turns=5, seed=6)
     planned = dp.plan(cfg, trajs, policy=policy, **STORAGE_BOUND)
@@ -228,7 +226,7 @@ def test_handoff_1p1d(two_gpus, policy, tight, layer_gate):
     if tight:
         opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots
         xp = dp.build_exec_plan(cfg, trajs, planned, opt)
-    rts = handoff_engines(xp, 2)
+    rts = handoff_engines(xp, 2, [0, de_dev])
     for _ in range(2):
         for rt in rts:
             rt.reset_counters()
@@ -243,9 +241,9 @@ def test_handoff_1p1d(two_gpus, policy, tight, layer_gate):
         assert ctr[job[16], cfg.n_layer] == blocks * xp.items_per_block * cfg.n_layer
 
 
-@pytest.mark.multigpu
-def test_handoff_2p2d_tight(gpus):
-    if gpus < 4:
+@pytest.mark.parametrize("placement", ["one_gpu", "four_gpus"])
+def test_handoff_2p2d_tight(gpus, placement):
+    if placement == "four_gpus" and gpus < 4:
         pytest.skip("needs 4 GPUs")
     cfg = cluster(2, 2, L=4)
     trajs = small_trace(count=12, turns=5, seed=9)
@@ -256,7 +254,7 @@ def test_handoff_2p2d_tight(gpus):
     probe = dp.build_exec_plan(cfg, trajs, planned, opt)
     opt.pool_slots, opt.de_pool_slots = probe.peak_slots, probe.de_peak_slots
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
-    rts = handoff_engines(xp, 4)
+    rts = handoff_engines(xp, 4, [0, 0, 0, 0] if placement == "one_gpu" else None)
     for _ in range(2):
         for rt in rts:
             rt.reset_counters()
@@ -265,9 +263,8 @@ def test_handoff_2p2d_tight(gpus):
         verify_prompt_pool(rt, xp, cfg)
 
 
-@pytest.mark.multigpu
 @pytest.mark.parametrize("tight", [False, True])
-def test_handoff_with_persistence(two_gpus, tight):
+def test_handoff_with_persistence(de_dev, tight):
     """PD handoff + decode stand-in + K4 persistence: the decode pools end with
     prompt + generated tokens of their last occupants, and every generated
     token of every request is in its DE's persist store, byte for byte."""
@@ -282,7 +279,7 @@ def test_handoff_with_persistence(two_gpus, tight):
     if tight:
         opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots
         xp = dp.build_exec_plan(cfg, trajs, planned, opt)
-    rts = handoff_engines(xp, 2)
+    rts = handoff_engines(xp, 2, [0, de_dev])
     for _ in range(2):
         for rt in rts:
             rt.reset_counters()
@@ -312,8 +309,7 @@ def test_handoff_with_persistence(two_gpus, tight):
     del last
 
 
-@pytest.mark.multigpu
-def test_two_engines_k2_on_copy_engine(two_gpus):
+def test_two_engines_k2_on_copy_engine(de_dev):
     # tight pool: cross-reader reuse hazards with the DE's copy-engine pushes
     cfg = cluster(1, 1, L=4)
     trajs = small_trace(count=10, turns=6, seed=8)
@@ -326,7 +322,7 @@ def test_two_engines_k2_on_copy_engine(two_gpus):
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     assert xp.reader_bytes[1] > 0
     pe = dp.EngineRuntime(xp, 0, 0)
-    de = dp.EngineRuntime(xp, 1, 1)
+    de = dp.EngineRuntime(xp, 1, de_dev)
     de.attach_peer_local(0, pe)
     for _ in range(2):
         pe.reset_counters()

@@ -14,13 +14,24 @@ import pytest
 from oracle import refpy
 from paper_2602_21548_b200 import abi
 
-pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+pytestmark = pytest.mark.gpu
 SEED = 9
 
 
 def dev(x, device, dtype):
     import torch
     return torch.tensor(np.asarray(x, dtype=dtype), device=f"cuda:{device}")
+
+
+_streams = {}
+
+
+def de_stream(device):
+    """A non-blocking stream of the DE device (kept alive for the session)."""
+    import torch
+    if device not in _streams:
+        _streams[device] = torch.cuda.Stream(device=device)
+    return _streams[device].cuda_stream
 
 
 def sync_all():
@@ -38,9 +49,12 @@ def check_prompt(pool, g_ref, fbs, slots, n_prompt, T, b, L):
             assert got == want, (k, layer)
 
 
-@pytest.mark.parametrize("L,T,b", [(8, 64, 576), (4, 64, 4096)])
-@pytest.mark.parametrize("C,A", [(64 * 5 + 10, 300), (64 * 3, 64), (0, 200), (130, 0)])
-def test_de_path_dual_then_missmerge(two_gpus, L, T, b, C, A):
+@pytest.mark.parametrize("L,T,b,C,A", [
+    (L, T, b, C, A) for L, T, b in [(8, 64, 576), (4, 64, 4096)]
+    for C, A in [(64 * 5 + 10, 300), (64 * 3, 64), (0, 200), (130, 0)]] + [
+    (61, 64, 576, 64 * 9 + 17, 429),    # DeepSeek-V3 MLA fp8, all 61 layers
+    (64, 64, 4096, 64 * 4 + 33, 100)])  # config 3: Qwen2.5-32B GQA bf16, all 64 layers
+def test_de_path_dual_then_missmerge(de_dev, L, T, b, C, A):
     """DE read path: the DE reads the hit blocks once (dual: PE pool + its own
     decode pool), the PE gates each layer on them, writes the miss KV and
     pushes only the miss part (MissMerge)."""
@@ -48,17 +62,18 @@ def test_de_path_dual_then_missmerge(two_gpus, L, T, b, C, A):
     P = C + A
     n_hit, n_prompt = -(-C // T), -(-P // T)
     rng = np.random.default_rng(C * 7 + A)
-    st_de = abi.Store(1, g, 40, SEED)
+    s_de = de_stream(de_dev)  # before K3 spins: stream creation may wait for the device
+    st_de = abi.Store(de_dev, g, 40, SEED)
     pe_pool = abi.Pool(0, g, 32, 2)   # row 0: hit KV landed, row 1: handoff done
-    de_pool = abi.Pool(1, g, 32, 2)
-    pe_view_on_de = pe_pool.peer_view(1)
+    de_pool = abi.Pool(de_dev, g, 32, 2)
+    pe_view_on_de = pe_pool.peer_view(de_dev)
     de_view_on_pe = de_pool.peer_view(0)
     try:
         fbs = (rng.integers(0, 40 - n_prompt) + np.arange(n_prompt)).astype(np.int64)
         pe_slots = rng.permutation(32)[:n_prompt].astype(np.int32)
         de_slots = rng.permutation(32)[:n_prompt].astype(np.int32)
-        keep = [dev(fbs if n_prompt else [0], 1, np.int64), dev(pe_slots if n_prompt else [0], 1, np.int32),
-                dev(de_slots if n_prompt else [0], 1, np.int32)]
+        keep = [dev(fbs if n_prompt else [0], de_dev, np.int64), dev(pe_slots if n_prompt else [0], de_dev, np.int32),
+                dev(de_slots if n_prompt else [0], de_dev, np.int32)]
         dj = (abi.DualJob * 1)()
         dj[0].pe = abi.Job(keep[0].data_ptr(), keep[1].data_ptr(), C, n_hit, 0, L, 0)
         dj[0].de_slot = keep[2].data_ptr()
@@ -70,8 +85,10 @@ def test_de_path_dual_then_missmerge(two_gpus, L, T, b, C, A):
         hj[0] = abi.HandoffJob(on_pe[0].data_ptr(), on_pe[1].data_ptr(), on_pe[2].data_ptr(), C, P,
                                n_prompt, 0, 0 if C else -1, items, 0, 1)
         # K3 first: it must block on the dual gather's per-layer releases
+        # (the DE's own stream: on a shared GPU the legacy stream would
+        # queue the producer behind its waiter)
         abi.prefill_handoff(pe_pool, de_view_on_pe, hj, 1, SEED, timeout_ms=20000)
-        abi.push_p2p_dual(pe_view_on_de, de_pool, st_de, dj, 1)
+        abi.push_p2p_dual(pe_view_on_de, de_pool, st_de, dj, 1, s_de)
         sync_all()
         assert abi.wait_status(pe_pool) == abi.DP_OK
         gr = refpy.geom(L, T, b)
@@ -90,18 +107,19 @@ def test_de_path_dual_then_missmerge(two_gpus, L, T, b, C, A):
             x.close()
 
 
-@pytest.mark.parametrize("C,A", [(64 * 7 + 33, 429), (64 * 2, 1), (0, 64 * 3 + 5)])
-def test_pe_path_load_then_petode(two_gpus, C, A):
+@pytest.mark.parametrize("L,T,b,C,A", [(8, 64, 576, 64 * 7 + 33, 429), (8, 64, 576, 64 * 2, 1),
+                                       (8, 64, 576, 0, 64 * 3 + 5), (61, 64, 576, 64 * 6 + 1, 429),
+                                       (64, 64, 4096, 64 * 3 + 40, 90)])
+def test_pe_path_load_then_petode(de_dev, L, T, b, C, A):
     """PE read path: K1 loads the hit KV into the PE pool; K3 (stream-ordered
     after it) writes the miss KV and pushes the whole prompt (PeToDe)."""
-    L, T, b = 8, 64, 576
     g = abi.geom(L, T, b)
     P = C + A
     n_hit, n_prompt = -(-C // T), -(-P // T)
     rng = np.random.default_rng(P)
     st_pe = abi.Store(0, g, 40, SEED)
     pe_pool = abi.Pool(0, g, 32, 1)
-    de_pool = abi.Pool(1, g, 32, 1)
+    de_pool = abi.Pool(de_dev, g, 32, 1)
     de_view = de_pool.peer_view(0)
     try:
         fbs = (rng.integers(0, 40 - n_prompt) + np.arange(n_prompt)).astype(np.int64)
@@ -126,12 +144,12 @@ def test_pe_path_load_then_petode(two_gpus, C, A):
             x.close()
 
 
-def test_handoff_gate_watchdog(two_gpus):
+def test_handoff_gate_watchdog(de_dev):
     """A layer whose hit KV never lands trips the watchdog instead of hanging."""
     L, T, b = 2, 64, 576
     g = abi.geom(L, T, b)
     pe_pool = abi.Pool(0, g, 4, 1)
-    de_pool = abi.Pool(1, g, 4, 1)
+    de_pool = abi.Pool(de_dev, g, 4, 1)
     de_view = de_pool.peer_view(0)
     try:
         t = [dev([0, 1], 0, np.int64), dev([0, 1], 0, np.int32), dev([0, 1], 0, np.int32)]
@@ -145,7 +163,7 @@ def test_handoff_gate_watchdog(two_gpus):
             x.close()
 
 
-def test_stream_wait_counter_orders_a_stream(two_gpus):
+def test_stream_wait_counter_orders_a_stream(de_dev):
     """dp_stream_wait_counter: the PE stream waits (no SMs) for a counter the
     DE's dual gather releases, then K3 runs without its in-kernel gate."""
     L, T, b = 4, 64, 576
@@ -153,16 +171,17 @@ def test_stream_wait_counter_orders_a_stream(two_gpus):
     C, A = 64 * 3 + 5, 70
     P = C + A
     n_hit, n_prompt = -(-C // T), -(-P // T)
-    st_de = abi.Store(1, g, 16, SEED)
+    s_de = de_stream(de_dev)
+    st_de = abi.Store(de_dev, g, 16, SEED)
     pe_pool = abi.Pool(0, g, 16, 2)
-    de_pool = abi.Pool(1, g, 16, 1)
-    pe_view = pe_pool.peer_view(1)
+    de_pool = abi.Pool(de_dev, g, 16, 1)
+    pe_view = pe_pool.peer_view(de_dev)
     de_view = de_pool.peer_view(0)
     try:
         fbs = np.arange(3, 3 + n_prompt, dtype=np.int64)
         ps = np.arange(n_prompt, dtype=np.int32)
         dsl = np.arange(8, 8 + n_prompt, dtype=np.int32)
-        on_de = [dev(fbs, 1, np.int64), dev(ps, 1, np.int32), dev(dsl, 1, np.int32)]
+        on_de = [dev(fbs, de_dev, np.int64), dev(ps, de_dev, np.int32), dev(dsl, de_dev, np.int32)]
         on_pe = [dev(fbs, 0, np.int64), dev(ps, 0, np.int32), dev(dsl, 0, np.int32)]
         items = abi.layer_items(g, n_hit)
         abi.stream_wait_counter(pe_pool, 0, L, items * L)  # legacy stream of device 0
@@ -174,7 +193,7 @@ def test_stream_wait_counter_orders_a_stream(two_gpus):
         dj[0].pe = abi.Job(on_de[0].data_ptr(), on_de[1].data_ptr(), C, n_hit, 0, L, 0)
         dj[0].de_slot = on_de[2].data_ptr()
         dj[0].de_ticket = 0
-        abi.push_p2p_dual(pe_view, de_pool, st_de, dj, 1)
+        abi.push_p2p_dual(pe_view, de_pool, st_de, dj, 1, s_de)
         sync_all()
         gr = refpy.geom(L, T, b)
         check_prompt(pe_pool, gr, fbs, ps, P, T, b, L)

@@ -79,7 +79,7 @@ def check_pool(pool, g_ref, plain, T, b, store_img, n_slots):
                 assert got == want[off:off + n].tobytes(), (layer, s, k)
 
 
-@pytest.mark.parametrize("L,T,b", GEOMS)
+@pytest.mark.parametrize("L,T,b", GEOMS + [(64, 64, 4096)])  # + config 3's full Qwen shape
 def test_k1_gather_parity(gpus, L, T, b):
     rng = np.random.default_rng(L * 1000 + b)
     g = abi.geom(L, T, b)
@@ -192,24 +192,24 @@ def test_abi_rejects_bad_arguments(gpus):
         st.close()
 
 
-@pytest.mark.multigpu
-@pytest.mark.parametrize("L,T,b", [(61, 64, 576), (4, 64, 4096)])
-def test_k2_push_p2p_parity(two_gpus, L, T, b):
-    """DE (device 1) reads its own host store and stores into the PE pool on
-    device 0 over NVLink; the PE's counters see the system-scope release."""
+@pytest.mark.parametrize("L,T,b", [(61, 64, 576), (4, 64, 4096), (64, 64, 4096)])
+def test_k2_push_p2p_parity(de_dev, L, T, b):
+    """The DE (device de_dev) reads its own host store and stores into the PE
+    pool on device 0 (over NVLink when de_dev = 1); the PE's counters see the
+    system-scope release.  (64, 64, 4096) is config 3's full Qwen2.5-32B shape."""
     rng = np.random.default_rng(11)
     g = abi.geom(L, T, b)
-    st_de = abi.Store(1, g, 10, SEED)
+    st_de = abi.Store(de_dev, g, 10, SEED)
     pool = abi.Pool(0, g, 48, 40)
-    view = pool.peer_view(1)
+    view = pool.peer_view(de_dev)
     try:
-        specs, keep, plain = random_jobs(rng, L, T, 36, 10, 48, 3, device=1)
+        specs, keep, plain = random_jobs(rng, L, T, 36, 10, 48, 3, device=de_dev)
         abi.h2d_push_p2p_layer(view, st_de, abi.make_jobs(specs), len(specs))
         for t, (fbs, slots, ntok, l0, l1) in enumerate(plain):
             abi.wait_layer(pool, t, L, abi.layer_items(g, len(slots)) * (l1 - l0), timeout_ms=10000)
         sync()
         import torch
-        torch.cuda.synchronize(1)
+        torch.cuda.synchronize(de_dev)
         assert abi.wait_status(pool) == abi.DP_OK
         store_img = np.frombuffer(st_de.bytes(), dtype=np.uint8).copy()
         check_pool(pool, refpy.geom(L, T, b), plain, T, b, store_img, 48)
@@ -260,18 +260,17 @@ def test_k1_copy_engine_parity(gpus, L, T, b):
         st.close()
 
 
-@pytest.mark.multigpu
 @pytest.mark.parametrize("L,T,b", [(61, 64, 576), (4, 64, 4096), (3, 16, 1024)])
-def test_k2_copy_engine_parity(two_gpus, L, T, b):
+def test_k2_copy_engine_parity(de_dev, L, T, b):
     """K2 on the DE's copy engine (dp_h2d_push_copy): the DE's stream copies
     its host store into the PE pool through the peer view and writes the PE's
     counters; same bytes and counters as the kernel."""
     rng = np.random.default_rng(23)
     g = abi.geom(L, T, b)
     n_fb, n_slots = 16, 64
-    st_de = abi.Store(1, g, n_fb, SEED)
+    st_de = abi.Store(de_dev, g, n_fb, SEED)
     pool = abi.Pool(0, g, n_slots, 12)
-    view = pool.peer_view(1)
+    view = pool.peer_view(de_dev)
     try:
         plain, keep, specs, used = [], [], [], 0
         for t in range(12):
@@ -289,13 +288,13 @@ def test_k2_copy_engine_parity(two_gpus, L, T, b):
             specs.append((fbs.ctypes.data, slots.ctypes.data, ntok, nblk, 0, L, t))
             plain.append((fbs, slots, ntok, 0, L))
         import torch
-        s_de = torch.cuda.Stream(device=1)
+        s_de = torch.cuda.Stream(device=de_dev)
         abi.h2d_push_copy(view, st_de, abi.make_jobs(specs), len(specs), s_de.cuda_stream)
         # the PE observes completion through its own counters only
         for t, (fbs, slots, ntok, l0, l1) in enumerate(plain):
             abi.wait_layer(pool, t, L, abi.layer_items(g, len(slots)) * L, timeout_ms=10000)
         sync()
-        torch.cuda.synchronize(1)
+        torch.cuda.synchronize(de_dev)
         assert abi.wait_status(pool) == abi.DP_OK
         store_img = np.frombuffer(st_de.bytes(), dtype=np.uint8).copy()
         check_pool(pool, refpy.geom(L, T, b), plain, T, b, store_img, n_slots)
@@ -306,3 +305,36 @@ def test_k2_copy_engine_parity(two_gpus, L, T, b):
         view.close()
         pool.close()
         st_de.close()
+
+
+@pytest.mark.parametrize("placement", ["device", "none"])
+def test_numa_store_and_storage_read(gpus, placement):
+    """dp_store_create_on_node (NUMA-bound pinned staging) holds the oracle's
+    content; dp_storage_read materialises other storage Full Blocks into
+    staging positions (content keyed on the source block), paced by a NIC."""
+    import time
+    L, T, b = 4, 64, 576
+    g = abi.geom(L, T, b)
+    node = abi.NUMA_DEVICE if placement == "device" else abi.NUMA_NONE
+    st = abi.Store(0, g, 8, SEED, numa_node=node)
+    nic = abi.Nic(2e9)
+    try:
+        want_node = abi.device_numa_node(0)
+        if placement == "device" and want_node >= 0:
+            assert st.numa_node() == want_node
+        gr = refpy.geom(L, T, b)
+        assert np.array_equal(np.frombuffer(st.bytes(), dtype=np.uint8), refpy.fill_store(gr, SEED, 8))
+        nic.start()
+        t0 = time.monotonic()
+        st.storage_read(2, 100, 3, nic)  # staging 2..4 <- storage Full Blocks 100..102
+        fb = L * T * b
+        assert time.monotonic() - t0 >= 3 * fb / 2e9 * 0.99
+        img = np.frombuffer(st.bytes(), dtype=np.uint8)
+        assert np.array_equal(img[2 * fb:5 * fb], refpy.fill_store(gr, SEED, 3, fb0=100))
+        assert np.array_equal(img[:2 * fb], refpy.fill_store(gr, SEED, 2))   # untouched
+        assert np.array_equal(img[5 * fb:], refpy.fill_store(gr, SEED, 3, fb0=5))
+        with pytest.raises(abi.DualPathError):
+            st.storage_read(7, 0, 2)  # past the staging
+    finally:
+        nic.close()
+        st.close()

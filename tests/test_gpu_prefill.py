@@ -201,16 +201,15 @@ def test_prefill_single_pe(gpus, tight):
     check_digests(eng, cfg, planned, xp, skip=skip)
 
 
-@pytest.mark.multigpu
 @pytest.mark.parametrize("tight", [False, True])
-def test_prefill_1p1d_dual_path(two_gpus, tight):
+def test_prefill_1p1d_dual_path(de_dev, tight):
     cfg = cluster(1, 1)
     trajs, planned, xp = prefill_plan(cfg, "dual_path", tight, count=8, turns=6, seed=8)
     assert xp.reader_bytes[1] > 0
     if tight:
         assert any(xp.consumer_waits(i) for i in range(len(xp.jobs())))
     pe = dp.EngineRuntime(xp, 0, 0)
-    de = dp.EngineRuntime(xp, 1, 1)
+    de = dp.EngineRuntime(xp, 1, de_dev)
     de.attach_peer_local(0, pe)
     for _ in range(2):
         pe.reset_counters()
@@ -219,9 +218,8 @@ def test_prefill_1p1d_dual_path(two_gpus, tight):
         check_digests(pe, cfg, planned, xp)
 
 
-@pytest.mark.multigpu
 @pytest.mark.parametrize("tight,persist", [(False, False), (True, False), (True, True)])
-def test_prefill_with_handoff_1p1d(two_gpus, tight, persist):
+def test_prefill_with_handoff_1p1d(de_dev, tight, persist):
     """The whole pipeline: loads on both paths, quota-batched K5 forwards on
     the PE, K3 handoff of each prompt after its last forward, (decode +
     K4 persistence).  Digests equal the oracle's and every prompt lands in its
@@ -241,7 +239,7 @@ def test_prefill_with_handoff_1p1d(two_gpus, tight, persist):
     if tight:
         opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots
         xp = dp.build_exec_plan(cfg, trajs, planned, opt)
-    rts = handoff_engines(xp, 2)
+    rts = handoff_engines(xp, 2, [0, de_dev])
     for _ in range(2):
         for rt in rts:
             rt.reset_counters()

@@ -71,13 +71,12 @@ def test_tier_single_pe(gpus, tmp_path, tight_ring, direct):
     verify_pool(eng, xp, cfg)
 
 
-@pytest.mark.multigpu
 @pytest.mark.parametrize("tight_ring", [False, True])
-def test_tier_1p1d_dual_path(two_gpus, tmp_path, tight_ring):
+def test_tier_1p1d_dual_path(de_dev, tmp_path, tight_ring):
     cfg, xp = make(tmp_path, 1, 1, "dual_path", tight_ring)
     assert xp.reader_bytes[1] > 0
     pe = dp.EngineRuntime(xp, 0, 0)
-    de = dp.EngineRuntime(xp, 1, 1)
+    de = dp.EngineRuntime(xp, 1, de_dev)
     de.attach_peer_local(0, pe)
     for _ in range(2):
         pe.reset_counters()
