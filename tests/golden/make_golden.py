@@ -9,6 +9,10 @@ Fixtures:
   decisions_<name>.json  scheduler decisions + makespan + per-stage byte
                          ledger of desim::run_offline on a synthetic trace
   kvref_kat.json         known answers of the content / hash formulas
+  bench_<key>.json       the reference's decisions (digest, makespan, ledger)
+                         for the exact workloads bench.py measures
+                         (`python tests/golden/make_golden.py --bench`; the
+                         8-GPU ones take ~10 min of reference CPU each)
 """
 
 import hashlib
@@ -43,6 +47,66 @@ STAGES = ["storage_read", "loopback_h2d", "pe_to_de", "de_to_pe", "miss_merge", 
           "layer_compute", "decode", "persist_d2h", "persist_write", "burst"]
 
 
+# bench.py's configurations: (workload, sessions, P, D, policy, cap GB/s)
+BENCH = [("c1", 64, 1, 1, "pe_only", 0), ("c1", 16, 1, 1, "pe_only", 0)]
+for _n in (2, 4, 8):
+    for _pol in ("dual_path", "pe_only"):
+        BENCH.append(("c1", 16 * _n, _n // 2, _n - _n // 2, _pol, 0))
+        BENCH.append(("c2", 6 * _n, _n // 2, _n - _n // 2, _pol, 6.25))
+for _pol in ("dual_path", "pe_only"):
+    BENCH.append(("c1", 128, 2, 6, _pol, 0))
+    BENCH.append(("c2", 24, 1, 3, _pol, 6.25))  # N = 4, P:D = 1:3
+
+
+def bench_case(case):
+    """One bench configuration through the reference simulator."""
+    import bench
+    wl, sessions, P, D, policy, cap = case
+    shape = bench.QWEN if wl == "c3" else bench.DSV3
+    key = bench.golden_key(wl, sessions, P, D, policy, cap, bench.PCIE_ZC_BPS)
+    trace = f"/tmp/golden_bench_{key}.tsv"
+
+    class A:
+        workload, trace_path = wl, ""
+    A.trace = ""
+    rounds = bench.reference_trace(A, wl, sessions, trace)
+    rate = cap * 1e9 if cap else bench.PCIE_ZC_BPS
+    kv = dict(P=P, D=D, g=1, L=shape["L"], b=shape["b"], T=shape["T"], B=bench.NVLINK_BPS,
+              s=rate / bench.NVLINK_BPS, M=2e12, hbm=100_000_000, pe_buf=1 << 42, de_buf=1 << 42,
+              policy=policy, flows=1, **bench.PLAN_KW)
+    t0 = __import__("time").time()
+    rep = refpy.ref_simulate(trace, **kv)
+    wall = __import__("time").time() - t0
+    h = hashlib.sha1()
+    for d in rep["decisions"]:
+        h.update(repr((d[1], d[2], d[3], d[4])).encode())
+    ledger = {}
+    for req, stage, nbytes, a, b in rep["flows"]:
+        ledger[STAGES[stage]] = ledger.get(STAGES[stage], 0.0) + nbytes
+    out = {"key": key, "workload": wl, "sessions": sessions, "P": P, "D": D, "policy": policy,
+           "cap_gbps": cap, "simulate": {k: v for k, v in kv.items() if k != "flows"},
+           "trace_md5": hashlib.md5(open(trace, "rb").read()).hexdigest(),
+           "requests": sum(len(r) for r in rounds), "decisions": len(rep["decisions"]),
+           "de_path": sum(1 for d in rep["decisions"] if d[4] == 1),
+           "decisions_digest": h.hexdigest(), "makespan": rep["makespan"], "ledger": ledger,
+           "reference_wall_s": round(wall, 2)}
+    os.unlink(trace)
+    with open(os.path.join(HERE, f"bench_{key}.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    return key, len(rep["decisions"]), round(wall, 1)
+
+
+def main_bench(only=None):
+    from multiprocessing import Pool
+    sys.path.insert(0, ROOT)
+    cases = [c for c in BENCH if not only or any(o in "_".join(map(str, c)) for o in only)]
+    # longest first: the 8-GPU c1 cases dominate
+    cases.sort(key=lambda c: -(c[1] * (3 if c[0] == "c1" else 1)))
+    with Pool(min(len(cases), os.cpu_count() or 1)) as pool:
+        for res in pool.imap_unordered(bench_case, cases):
+            print(*res, flush=True)
+
+
 def main():
     for name, (syn, sim) in CASES.items():
         trace = os.path.join(HERE, f"trace_{name}.tsv")
@@ -73,4 +137,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--bench":
+        main_bench(sys.argv[2:])
+    else:
+        main()

@@ -123,3 +123,31 @@ def test_reference_arm_loads_no_repo_library():
     assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port"
     assert line["config"]["sessions"] == 2 and line["config"]["requests"] == 40
     assert line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _bench_fixtures():
+    import glob
+    return sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "bench_*.json")))
+
+
+@pytest.mark.parametrize("path", _bench_fixtures(), ids=lambda p: os.path.basename(p)[6:-5])
+def test_bench_plans_match_reference_fixtures(path):
+    """Every configuration bench.py measures: the product planner's decisions
+    (request -> PE, DE, read path) and makespan are the reference simulator's
+    own, bit for bit (fixtures from oracle/_ref, tests/golden/make_golden.py)."""
+    import json
+    from paper_2602_21548_b200 import dist as dpdist
+    with open(path) as f:
+        want = json.load(f)
+    a = Args()
+    a.workload = want["workload"]
+    a.trace = ""
+    trajs, shape = bench.workload(a, 1, sessions=want["sessions"])
+    cfg = bench.cluster(shape, want["P"], want["D"], want["cap_gbps"] * 1e9)
+    planned = dp.plan(cfg, trajs, policy=want["policy"], **bench.PLAN_KW)
+    assert bench.golden_key(want["workload"], want["sessions"], want["P"], want["D"], want["policy"],
+                            want["cap_gbps"], bench.PCIE_ZC_BPS) == want["key"]
+    assert len(planned["decisions"]) == want["decisions"]
+    assert sum(1 for d in planned["decisions"] if d[4] == 1) == want["de_path"]
+    assert dpdist.plan_digest(planned) == want["decisions_digest"]
+    assert planned["makespan"] == want["makespan"]
