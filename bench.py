@@ -97,11 +97,14 @@ def parse():
                          "and populated once per box; O_DIRECT) through a pinned staging ring")
     ap.add_argument("--io-threads", type=int, default=8, help="storage tier: host IO threads per engine")
     ap.add_argument("--wait-timeout-ms", type=int, default=30000, help="watchdog of every cross-engine wait")
-    ap.add_argument("--k2", default="sm", choices=["sm", "ce"],
-                    help="DE-path loads: sm = K2 gather pushing over NVLink, ce = the DE's copy engine")
-    ap.add_argument("--k1", default="sm", choices=["sm", "ce", "hybrid"],
+    ap.add_argument("--k2", default="sm", choices=["sm", "ce", "staged"],
+                    help="DE-path loads: sm = K2 gather pushing over NVLink, ce = the DE's copy engine, "
+                         "staged = copy engine into an HBM ring + NVLink scatter kernel")
+    ap.add_argument("--k1", default="sm", choices=["sm", "ce", "hybrid", "staged"],
                     help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs), "
-                         "hybrid = both at once, jobs split by bytes")
+                         "hybrid = both at once, jobs split by bytes, staged = copy engine into an HBM "
+                         "ring + scatter kernel")
+    ap.add_argument("--stage-ctas", type=int, default=32, help="staged modes: scatter kernel CTAs")
     return ap.parse_args()
 
 
@@ -460,8 +463,9 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
         opt.storage_cap_per_engine = caps
     if args.online > 0:
         opt.pace_scale = 1.0
-    opt.k1_mode = {"sm": 0, "ce": 1, "hybrid": 2}[args.k1]
-    opt.k2_mode = 1 if args.k2 == "ce" else 0
+    opt.k1_mode = {"sm": 0, "ce": 1, "hybrid": 2, "staged": 3}[args.k1]
+    opt.k2_mode = {"sm": 0, "ce": 1, "staged": 2}[args.k2]
+    opt.stage_ctas = args.stage_ctas
     opt.wait_timeout_ms = args.wait_timeout_ms
     opt.handoff = bool(args.handoff or args.persist)
     opt.persist = bool(args.persist)

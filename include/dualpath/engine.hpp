@@ -48,10 +48,17 @@ struct ExecOptions {
   // PE-path loads (K1): 0 = SM gather kernel, 1 = copy engine (no SMs: the
   // isolation mode while the PE computes), 2 = both at once, jobs split by
   // bytes (the plain load path; measured slower than 0, profiles/r01_SUMMARY.md)
+  // 3 = staged: the copy engine moves whole Full-Block runs into an HBM ring at
+  // the link's full rate, a small scatter kernel (stage_ctas CTAs) lands them
+  // in the pool's layer planes (dp_h2d_layer_staged)
   std::int32_t k1_mode = 0;
   // DE-path loads (K2): 0 = SM gather pushing over NVLink, 1 = the DE's copy
   // engine writing into the PE pool (no SMs on the DE: its decode is untouched)
+  // 2 = staged: the DE's copy engine into its HBM ring, then the scatter kernel
+  // pushes over NVLink into the PE pool (dp_h2d_push_staged)
   std::int32_t k2_mode = 0;
+  std::int64_t stage_ring_bytes = 1LL << 30;  // staged modes: HBM ring per engine
+  std::int32_t stage_ctas = 32;               // staged modes: scatter CTAs
   // PD handoff: every request's prompt KV also ends in its
   // DE's decode pool — prefill stand-in + PeToDe / MissMerge per layer (K3)
   // and the DE read path fused with DecodeH2D (dual store)
@@ -288,6 +295,8 @@ class EngineRuntime {
   void* ev_end_ = nullptr;
   dp_store* store_ = nullptr;
   dp_nic* nic_ = nullptr;                   // emulated storage NIC (rate cap)
+  dp_stager* stager_ = nullptr;             // staged K1 / K2: HBM ring (k1_mode 3 / k2_mode 2)
+  std::int64_t stager_launches() const;
   dp_pool* pool_ = nullptr;                 // owned (PE only)
   std::vector<dp_pool*> peers_;             // per engine id: view of that PE's pool
   std::int64_t* d_src_ = nullptr;           // device block tables of this reader

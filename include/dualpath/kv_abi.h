@@ -305,6 +305,25 @@ int dp_h2d_layer_copy(dp_pool* pe, const dp_store* src, const dp_job* jobs, int3
 int dp_h2d_push_copy(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs, int32_t n_jobs,
                      dp_stream de_stream);
 
+/* Staged K1 / K2: the copy engine moves whole Full-Block runs host -> an HBM
+ * staging ring at the link's full rate (1D copies of contiguous runs, a 2D
+ * copy of the valid rows of a partial last block), then the gather kernel
+ * scatters the ring into the pool's layer planes (K2: over NVLink into the
+ * PE pool) and releases the landed counters as K1 / K2 do.  The copies run
+ * on the stager's own stream, the scatters on `stream` (ordered after its
+ * earlier work; later work on `stream` sees the landed bytes).  Jobs move
+ * all layers; src_fb HOST-readable, dst_slot device-readable.  A stager
+ * serves one stream at a time.  ring_bytes 0 = 1 GiB. */
+typedef struct dp_stager dp_stager;
+int dp_stager_create(int device, const dp_kv_geom* geom, int64_t ring_bytes, dp_stager** out);
+int dp_stager_destroy(dp_stager* stager);
+int dp_stager_set_ctas(dp_stager* stager, int32_t ctas);  /* scatter CTAs (0 = 32) */
+int dp_stager_launches(const dp_stager* stager, int64_t* n);  /* scatter kernels so far */
+int dp_h2d_layer_staged(dp_pool* pe, const dp_store* src, dp_stager* stager, const dp_job* jobs,
+                        int32_t n_jobs, dp_stream stream);
+int dp_h2d_push_staged(dp_pool* pe_view, const dp_store* de_src, dp_stager* stager, const dp_job* jobs,
+                       int32_t n_jobs, dp_stream de_stream);
+
 /* Cap on the CTAs a K1/K2 launch on `device` may use (0 = default, 4 per SM).
  * The transfer is PCIe-bound, so a few CTAs keep the link full while leaving
  * the SMs to the prefill compute (the isolation knob of config 4). */

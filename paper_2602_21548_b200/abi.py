@@ -122,6 +122,12 @@ def lib():
         "dp_nic_read": ([P, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
                          ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "dp_storage_read": ([P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, P], ctypes.c_int),
+        "dp_stager_create": ([ctypes.c_int, ctypes.POINTER(Geom), ctypes.c_int64, PP], ctypes.c_int),
+        "dp_stager_destroy": ([P], ctypes.c_int),
+        "dp_stager_set_ctas": ([P, ctypes.c_int32], ctypes.c_int),
+        "dp_stager_launches": ([P, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "dp_h2d_layer_staged": ([P, P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
+        "dp_h2d_push_staged": ([P, P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_stream_wait_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
         "dp_stream_write_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
         "dp_decode_fill": ([P, ctypes.POINTER(SpanJob), ctypes.c_int32, ctypes.c_uint64, P], ctypes.c_int),
@@ -268,6 +274,35 @@ class Nic:
         if self.ptr:
             check(lib().dp_nic_destroy(self.ptr))
             self.ptr = ctypes.c_void_p()
+
+
+class Stager:
+    """HBM staging ring of the staged K1 / K2 (copy engine + scatter kernel)."""
+
+    def __init__(self, device, g, ring_bytes=0):
+        self.ptr = ctypes.c_void_p()
+        check(lib().dp_stager_create(device, ctypes.byref(g), ring_bytes, ctypes.byref(self.ptr)))
+
+    def set_ctas(self, n):
+        check(lib().dp_stager_set_ctas(self.ptr, n))
+
+    def launches(self):
+        n = ctypes.c_int64()
+        check(lib().dp_stager_launches(self.ptr, ctypes.byref(n)))
+        return n.value
+
+    def close(self):
+        if self.ptr:
+            check(lib().dp_stager_destroy(self.ptr))
+            self.ptr = ctypes.c_void_p()
+
+
+def h2d_layer_staged(pool, store, stager, jobs, n, stream=0):
+    return check(lib().dp_h2d_layer_staged(pool.ptr, store.ptr, stager.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def h2d_push_staged(pool_view, store, stager, jobs, n, stream=0):
+    return check(lib().dp_h2d_push_staged(pool_view.ptr, store.ptr, stager.ptr, jobs, n, ctypes.c_void_p(stream)))
 
 
 def device_numa_node(device):

@@ -419,6 +419,8 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("pace_scale", &dualpath::ExecOptions::pace_scale)
       .def_readwrite("k1_mode", &dualpath::ExecOptions::k1_mode)
       .def_readwrite("k2_mode", &dualpath::ExecOptions::k2_mode)
+      .def_readwrite("stage_ring_bytes", &dualpath::ExecOptions::stage_ring_bytes)
+      .def_readwrite("stage_ctas", &dualpath::ExecOptions::stage_ctas)
       .def_readwrite("handoff", &dualpath::ExecOptions::handoff)
       .def_readwrite("de_pool_slots", &dualpath::ExecOptions::de_pool_slots)
       .def_readwrite("gather_ctas", &dualpath::ExecOptions::gather_ctas)

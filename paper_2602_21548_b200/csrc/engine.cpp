@@ -124,6 +124,10 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
       check(dp_store_create(device_, &x.geom, x.store_fb, x.opt.seed + 1, &persist_store_),
             "dp_store_create (persist store)");
   }
+  if (!x.by_reader[engine_].empty() && ((is_pe() && x.opt.k1_mode == 3) || (!is_pe() && x.opt.k2_mode == 2))) {
+    check(dp_stager_create(device_, &x.geom, x.opt.stage_ring_bytes, &stager_), "dp_stager_create");
+    check(dp_stager_set_ctas(stager_, x.opt.stage_ctas), "dp_stager_set_ctas");
+  }
   if (x.handoff) {
     upload_handoff_tables();
   } else {
@@ -160,6 +164,7 @@ EngineRuntime::~EngineRuntime() {
   for (dp_pool* v : de_views_)
     if (v) dp_pool_destroy(v);
   if (pool_) dp_pool_destroy(pool_);
+  dp_stager_destroy(stager_);
   if (store_) dp_store_destroy(store_);
   dp_nic_destroy(nic_);
   if (persist_store_) dp_store_destroy(persist_store_);
@@ -363,6 +368,9 @@ StepResult EngineRuntime::run_step() {
   int batch_pe = -1;
   const bool k1_ce = x.opt.k1_mode == 1;
   const bool k2_ce = x.opt.k2_mode == 1;
+  const bool k1_st = x.opt.k1_mode == 3 && stager_;
+  const bool k2_st = x.opt.k2_mode == 2 && stager_;
+  const std::int64_t st_launch0 = stager_launches();
   // K1 hybrid (k1_mode 2): the PE's own jobs split by bytes between the SM
   // gather (load stream) and the copy engine (a second stream), run together
   const bool hybrid = x.opt.k1_mode == 2 && stream_ce_ != nullptr && !x.tier;
@@ -384,6 +392,12 @@ StepResult EngineRuntime::run_step() {
     if (batch_pe != engine_ && k2_ce) {
       rc = dp_h2d_push_copy(dst, store_, batch.data(), n, s);
       what = "dp_h2d_push_copy";
+    } else if (batch_pe != engine_ && k2_st) {
+      rc = dp_h2d_push_staged(dst, store_, stager_, batch.data(), n, s);
+      what = "dp_h2d_push_staged";
+    } else if (batch_pe == engine_ && k1_st) {
+      rc = dp_h2d_layer_staged(dst, store_, stager_, batch.data(), n, s);
+      what = "dp_h2d_layer_staged";
     } else if (batch_pe != engine_) {
       rc = dp_h2d_push_p2p_layer(dst, store_, batch.data(), n, s);
       what = "dp_h2d_push_p2p_layer";
@@ -395,8 +409,8 @@ StepResult EngineRuntime::run_step() {
       what = "dp_h2d_layer_gather";
     }
     check(rc, what);
-    const bool on_ce = batch_pe == engine_ ? k1_ce : k2_ce;
-    if (!on_ce)  // kernel launches (the copy engine paths have none)
+    const bool on_ce = batch_pe == engine_ ? (k1_ce || k1_st) : (k2_ce || k2_st);
+    if (!on_ce)  // kernel launches (the copy engine paths have none; staged ones are counted below)
       res.launches += (static_cast<std::int64_t>(batch.size()) + DP_MAX_JOBS_PER_LAUNCH - 1) /
                       DP_MAX_JOBS_PER_LAUNCH;
     batch.clear();
@@ -472,7 +486,10 @@ StepResult EngineRuntime::run_step() {
       sm_bytes += static_cast<double>(bytes);
     }
     batch_pe = j.pe;
-    if (j.pe == engine_ ? k1_ce : k2_ce)  // copy engine: host-readable block tables
+    if (j.pe == engine_ ? k1_st : k2_st)  // staged: host-readable sources, device slots
+      batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0,
+                             x.cfg.n_layer, j.ticket});
+    else if (j.pe == engine_ ? k1_ce : k2_ce)  // copy engine: host-readable block tables
       batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,
                              j.cached, j.n_blk, 0, x.cfg.n_layer, j.ticket});
     else
@@ -491,6 +508,7 @@ StepResult EngineRuntime::run_step() {
           "dp_wait_tickets");
     ++res.launches;
   }
+  res.launches += stager_launches() - st_launch0;
   check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), s), "cudaEventRecord");
   check_cuda(cudaEventSynchronize(static_cast<cudaEvent_t>(ev_end_)), "step sync");
   for (dp_pool* p : peers_)
@@ -503,6 +521,12 @@ StepResult EngineRuntime::run_step() {
   read_back_landed(res);
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return res;
+}
+
+std::int64_t EngineRuntime::stager_launches() const {
+  std::int64_t n = 0;
+  if (stager_) check(dp_stager_launches(stager_, &n), "dp_stager_launches");
+  return n;
 }
 
 // StorageRead of job j over this engine's emulated storage NIC (dp_nic): the

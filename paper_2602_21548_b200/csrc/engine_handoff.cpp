@@ -128,6 +128,11 @@ StepResult EngineRuntime::run_step_handoff() {
           job.src_fb = x.src_fb[engine_].data() + j.blk_off;
           job.dst_slot = x.slots[engine_].data() + j.blk_off;
           check(dp_h2d_layer_copy(pool_, store_, &job, 1, s), "dp_h2d_layer_copy");
+        } else if (x.opt.k1_mode == 3 && stager_) {
+          job.src_fb = x.src_fb[engine_].data() + j.blk_off;
+          const std::int64_t l0 = stager_launches();
+          check(dp_h2d_layer_staged(pool_, store_, stager_, &job, 1, s), "dp_h2d_layer_staged");
+          res.launches += stager_launches() - l0;
         } else {
           check(dp_h2d_layer_gather(pool_, store_, &job, 1, s), "dp_h2d_layer_gather");
           ++res.launches;

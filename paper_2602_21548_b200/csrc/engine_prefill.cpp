@@ -98,6 +98,8 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
     std::vector<int> job_of_row(rows.size(), -1);
     for (const FwdItem& it : x.fwd_items[engine_]) job_of_row[it.row] = it.job;
     const bool k1_ce = x.opt.k1_mode == 1;
+    const bool k1_st = x.opt.k1_mode == 3 && stager_;
+    const std::int64_t st_launch0 = stager_launches();
     std::vector<dp_job> batch;
     std::vector<int> batch_jobs;  // by_reader positions (the storage tier's job ids)
     std::unique_ptr<TierReader> tier;
@@ -108,6 +110,8 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
       const auto n = static_cast<int32_t>(batch.size());
       if (k1_ce) {
         check(dp_h2d_layer_copy(pool_, store_, batch.data(), n, s), "dp_h2d_layer_copy");
+      } else if (k1_st) {
+        check(dp_h2d_layer_staged(pool_, store_, stager_, batch.data(), n, s), "dp_h2d_layer_staged");
       } else {
         check(dp_h2d_layer_gather(pool_, store_, batch.data(), n, s), "dp_h2d_layer_gather");
         res.launches += (n + DP_MAX_JOBS_PER_LAUNCH - 1) / DP_MAX_JOBS_PER_LAUNCH;
@@ -153,6 +157,9 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
       if (k1_ce)
         batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,
                                j.cached, j.n_blk, 0, L, j.ticket});
+      else if (k1_st)
+        batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0,
+                               L, j.ticket});
       else
         batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket});
       batch_jobs.push_back(pos);
@@ -160,6 +167,7 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
       ++res.jobs;
     }
     flush();
+    res.launches += stager_launches() - st_launch0;
   }
   while (fi < fwds.size()) enqueue_forward(static_cast<int>(fi++), res);
   // the step ends when both streams are drained

@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "dualpath/kv_abi.h"
 
@@ -338,7 +339,7 @@ int64_t counters_offset(int64_t data_bytes) { return (data_bytes + 255) / 256 * 
 int preload_kernels(int device);
 
 int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
-                  dp_stream stream, bool peer) {
+                  dp_stream stream, bool peer, int ctas_override = 0) {
   if (!pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0)
     return fail(DP_EINVAL, "gather: null argument");
   if (!geom_equal(pool->geom, src->geom))
@@ -361,7 +362,7 @@ int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_
   p.block_tokens = g.block_tokens;
   p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
   const int dev_cap = (pool->device >= 0 && pool->device < kMaxDevices) ? g_gather_ctas[pool->device].load() : 0;
-  const int grid_cap = dev_cap > 0 ? dev_cap : sm_count(pool->device) * 4;
+  const int grid_cap = ctas_override > 0 ? ctas_override : dev_cap > 0 ? dev_cap : sm_count(pool->device) * 4;
   auto s = static_cast<cudaStream_t>(stream);
   for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_JOBS_PER_LAUNCH) {
     const int32_t nj = std::min<int32_t>(DP_MAX_JOBS_PER_LAUNCH, n_jobs - j0);
@@ -1719,6 +1720,204 @@ int dp_prefill_attend(const dp_pool* pool, int32_t layer, const dp_attend_item* 
     DP_CUDA(cudaGetLastError());
   }
   return DP_OK;
+}
+
+}  // extern "C"
+
+// ============================================================ staged K1 / K2
+// The copy engine moves whole Full-Block runs host -> an HBM staging ring at
+// the link's full rate (one 1D copy per contiguous run, a 2D copy of the
+// valid rows of a partial last block); the gather kernel then scatters the
+// ring's Full Blocks [L][T][b] into the pool's layer planes (HBM -> HBM, or
+// over NVLink into a peer PE pool) and releases the landed counters exactly
+// as K1 / K2 do.  The ring is split into kStageSegs segments used round
+// robin: the copies into a segment wait for the scatter that last read it
+// (ev_free), the scatter waits for its copies (ev_copied).
+namespace {
+constexpr int kStageSegs = 4;
+}  // namespace
+
+struct dp_stager {
+  int device = -1;
+  dp_kv_geom geom{};
+  int64_t seg_fb = 0;        // Full Blocks per segment
+  dp_store ring;             // device ring of kStageSegs * seg_fb Full Blocks (base in ring.host)
+  int64_t* iota = nullptr;   // device [0, 1, ..., ring_fb): ring positions as a src_fb table
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_copied[kStageSegs] = {};
+  cudaEvent_t ev_free[kStageSegs] = {};
+  int seg = 0;
+  int32_t ctas = 32;         // scatter CTAs (HBM-bound: a few keep up with the link)
+  int64_t launches = 0;      // scatter kernels launched so far
+};
+
+namespace {
+
+void stager_free(dp_stager* st) {
+  DeviceGuard guard(st->device);
+  if (st->copy) cudaStreamSynchronize(st->copy);
+  for (int i = 0; i < kStageSegs; ++i) {
+    if (st->ev_copied[i]) cudaEventDestroy(st->ev_copied[i]);
+    if (st->ev_free[i]) cudaEventDestroy(st->ev_free[i]);
+  }
+  if (st->copy) cudaStreamDestroy(st->copy);
+  if (st->ring.host) cudaFree(st->ring.host);
+  if (st->iota) cudaFree(st->iota);
+  cudaGetLastError();
+  delete st;
+}
+
+// One staged transfer.  The jobs' src_fb arrays are HOST-readable (the copies
+// are planned on the host), dst_slot device-readable (the kernel reads it).
+int staged_transfer(const char* who, dp_pool* pool, const dp_store* src, dp_stager* st, const dp_job* jobs,
+                    int32_t n_jobs, dp_stream stream, bool peer) {
+  const std::string w(who);
+  if (!pool || !src || !st || (n_jobs > 0 && !jobs) || n_jobs < 0) return fail(DP_EINVAL, w + ": null argument");
+  if (peer == pool->owner)
+    return fail(DP_EINVAL, w + (peer ? ": destination must be a peer view" : ": destination must be the local pool"));
+  if (pool->device != st->device || src->device != st->device)
+    return fail(DP_EINVAL, w + ": pool view, store and stager must be on one device");
+  if (!geom_equal(pool->geom, src->geom) || !geom_equal(st->geom, src->geom))
+    return fail(DP_EINVAL, w + ": geometry differs");
+  const dp_kv_geom& g = src->geom;
+  const int64_t T = g.block_tokens, b = g.bytes_per_token_layer;
+  const int64_t lb = T * b, fbb = lb * g.n_layer;
+  for (int32_t j = 0; j < n_jobs; ++j) {  // validate everything before enqueueing anything
+    const dp_job& job = jobs[j];
+    const int64_t need_blk = (job.n_tokens + T - 1) / T;
+    if (job.n_tokens < 0 || job.n_blk != need_blk || job.layer_begin != 0 || job.layer_end != g.n_layer ||
+        job.ticket >= pool->n_tickets || (job.n_blk > 0 && (!job.src_fb || !job.dst_slot)))
+      return fail(DP_EINVAL, w + ": job " + std::to_string(j) + " out of range (staged jobs move all layers)");
+    for (int32_t k = 0; k < job.n_blk; ++k)
+      if (job.src_fb[k] < 0 || job.src_fb[k] >= src->n_fb)
+        return fail(DP_EINVAL, w + ": job " + std::to_string(j) + ": source block out of range");
+  }
+  DeviceGuard guard(st->device);
+  auto s = static_cast<cudaStream_t>(stream);
+  std::vector<dp_job> sub;
+  int64_t used = 0;     // Full Blocks of the open segment
+  bool open = false;
+  auto flush = [&]() -> int {
+    if (!open) return DP_OK;
+    const int seg = st->seg;
+    DP_CUDA(cudaEventRecord(st->ev_copied[seg], st->copy));
+    DP_CUDA(cudaStreamWaitEvent(s, st->ev_copied[seg], 0));
+    if (!sub.empty()) {
+      if (int rc = launch_gather(pool, &st->ring, sub.data(), static_cast<int32_t>(sub.size()), stream, peer,
+                                 st->ctas))
+        return rc;
+      ++st->launches;
+    }
+    DP_CUDA(cudaEventRecord(st->ev_free[seg], s));
+    st->seg = (seg + 1) % kStageSegs;
+    sub.clear();
+    used = 0;
+    open = false;
+    return DP_OK;
+  };
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    const dp_job& job = jobs[j];
+    for (int32_t k0 = 0; k0 < job.n_blk;) {
+      if (open && (used == st->seg_fb || sub.size() == DP_MAX_JOBS_PER_LAUNCH))
+        if (int rc = flush()) return rc;
+      if (!open) {  // the segment's copies wait for the scatter that last read it
+        DP_CUDA(cudaStreamWaitEvent(st->copy, st->ev_free[st->seg], 0));
+        open = true;
+      }
+      const int32_t k1 = static_cast<int32_t>(std::min<int64_t>(job.n_blk, k0 + (st->seg_fb - used)));
+      const int64_t base = st->seg * st->seg_fb + used;  // ring position of block k0
+      const bool last_partial = k1 == job.n_blk && job.n_tokens % T != 0;
+      const int32_t full_end = last_partial ? k1 - 1 : k1;
+      for (int32_t k = k0; k < full_end;) {  // runs of consecutive storage Full Blocks
+        int32_t run = 1;
+        while (k + run < full_end && job.src_fb[k + run] == job.src_fb[k] + run) ++run;
+        DP_CUDA(cudaMemcpyAsync(st->ring.host + (base + (k - k0)) * fbb, src->host + job.src_fb[k] * fbb,
+                                run * fbb, cudaMemcpyHostToDevice, st->copy));
+        k += run;
+      }
+      if (last_partial) {  // only the valid tokens of every layer
+        const int32_t k = k1 - 1;
+        const int64_t ntok = job.n_tokens - static_cast<int64_t>(k) * T;
+        DP_CUDA(cudaMemcpy2DAsync(st->ring.host + (base + (k - k0)) * fbb, lb, src->host + job.src_fb[k] * fbb,
+                                  lb, ntok * b, g.n_layer, cudaMemcpyHostToDevice, st->copy));
+      }
+      const int64_t tok0 = static_cast<int64_t>(k0) * T;
+      sub.push_back(dp_job{st->iota + base, job.dst_slot + k0, std::min<int64_t>(job.n_tokens, k1 * T) - tok0,
+                           k1 - k0, 0, g.n_layer, job.ticket});
+      used += k1 - k0;
+      k0 = k1;
+    }
+  }
+  return flush();
+}
+
+}  // namespace
+
+extern "C" {
+
+int dp_stager_create(int device, const dp_kv_geom* geom, int64_t ring_bytes, dp_stager** out) {
+  if (!out) return fail(DP_EINVAL, "stager_create: null out");
+  *out = nullptr;
+  if (int rc = dp_geom_check(geom)) return rc;
+  if (ring_bytes < 0) return fail(DP_EINVAL, "stager_create: negative ring size");
+  if (int rc = preload_kernels(device)) return rc;
+  const int64_t fbb = static_cast<int64_t>(geom->n_layer) * geom->block_tokens * geom->bytes_per_token_layer;
+  const int64_t seg_fb = std::max<int64_t>(1, (ring_bytes > 0 ? ring_bytes : int64_t{1} << 30) / fbb / kStageSegs);
+  DeviceGuard guard(device);
+  auto* st = new dp_stager;
+  st->device = device;
+  st->geom = *geom;
+  st->seg_fb = seg_fb;
+  st->ring.device = device;
+  st->ring.geom = *geom;
+  st->ring.n_fb = seg_fb * kStageSegs;
+  st->ring.bytes = st->ring.n_fb * fbb;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&st->ring.host), st->ring.bytes);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&st->iota), st->ring.n_fb * sizeof(int64_t));
+  if (e == cudaSuccess) {
+    std::vector<int64_t> iota(st->ring.n_fb);
+    for (int64_t i = 0; i < st->ring.n_fb; ++i) iota[i] = i;
+    e = cudaMemcpy(st->iota, iota.data(), iota.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st->copy, cudaStreamNonBlocking);
+  for (int i = 0; i < kStageSegs && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&st->ev_copied[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->ev_free[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    stager_free(st);
+    return fail(e == cudaErrorMemoryAllocation ? DP_ENOMEM : DP_ECUDA,
+                std::string("stager_create: ") + cudaGetErrorString(e));
+  }
+  *out = st;
+  return DP_OK;
+}
+
+int dp_stager_destroy(dp_stager* st) {
+  if (st) stager_free(st);
+  return DP_OK;
+}
+
+int dp_stager_launches(const dp_stager* st, int64_t* n) {
+  if (!st || !n) return fail(DP_EINVAL, "stager_launches: null argument");
+  *n = st->launches;
+  return DP_OK;
+}
+
+int dp_stager_set_ctas(dp_stager* st, int32_t ctas) {
+  if (!st || ctas < 0) return fail(DP_EINVAL, "stager_set_ctas: bad argument");
+  st->ctas = ctas > 0 ? ctas : 32;
+  return DP_OK;
+}
+
+int dp_h2d_layer_staged(dp_pool* pe, const dp_store* src, dp_stager* st, const dp_job* jobs, int32_t n_jobs,
+                        dp_stream stream) {
+  return staged_transfer("h2d_layer_staged", pe, src, st, jobs, n_jobs, stream, /*peer=*/false);
+}
+
+int dp_h2d_push_staged(dp_pool* pe_view, const dp_store* de_src, dp_stager* st, const dp_job* jobs,
+                       int32_t n_jobs, dp_stream de_stream) {
+  return staged_transfer("h2d_push_staged", pe_view, de_src, st, jobs, n_jobs, de_stream, /*peer=*/true);
 }
 
 }  // extern "C"

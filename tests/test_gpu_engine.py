@@ -391,3 +391,32 @@ def test_edge_128k_context(gpus):
     assert r.bytes_read == xp.hit_bytes == 131072 * 2 * 576
     verify_counters(eng, xp, cfg)
     verify_pool(eng, xp, cfg)
+
+
+@pytest.mark.parametrize("tight", [False, True])
+def test_staged_loaders(de_dev, tight):
+    """k1_mode 3 / k2_mode 2: copy engine into the HBM ring + scatter kernel on
+    both read paths, with a small ring (jobs span segments) and, tight, slot
+    reuse across readers; final pool and counters equal the oracle's."""
+    cfg = cluster(1, 1, L=4)
+    trajs = small_trace(count=10, turns=6, seed=8)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.k1_mode, opt.k2_mode = 3, 2
+    opt.stage_ring_bytes = 24 * 4 * 64 * 576 * 4  # 24 Full Blocks per segment
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    if tight:
+        opt.pool_slots = xp.peak_slots
+        xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    assert xp.reader_bytes[1] > 0
+    pe = dp.EngineRuntime(xp, 0, 0)
+    de = dp.EngineRuntime(xp, 1, de_dev)
+    de.attach_peer_local(0, pe)
+    for _ in range(2):
+        pe.reset_counters()
+        res = dp.run_step_all([pe, de])
+        assert res[0].bytes_read + res[1].bytes_read == xp.hit_bytes
+        assert res[0].launches > 0 and res[1].launches > 0  # the scatter kernels
+        verify_counters(pe, xp, cfg)
+        verify_pool(pe, xp, cfg)

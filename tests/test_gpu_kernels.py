@@ -338,3 +338,70 @@ def test_numa_store_and_storage_read(gpus, placement):
     finally:
         nic.close()
         st.close()
+
+
+@pytest.mark.parametrize("L,T,b,ring", [(61, 64, 576, 40 << 20), (4, 64, 4096, 16 << 20), (3, 16, 1024, 0),
+                                        (64, 64, 4096, 256 << 20)])
+@pytest.mark.parametrize("side", ["pe", "de_same_gpu", "de_peer_gpu"])
+def test_staged_k1_k2_parity(gpus, L, T, b, ring, side):
+    """Staged K1 / K2 (copy engine into an HBM ring + scatter kernel): same
+    bytes and counters as the gather kernel, with runs broken by
+    non-consecutive Full Blocks, partial last blocks, jobs larger than a ring
+    segment (small rings) and more than one call reusing the ring."""
+    import torch
+    if side == "de_peer_gpu" and gpus < 2:
+        pytest.skip("needs >= 2 GPUs")
+    dev = {"pe": 0, "de_same_gpu": 0, "de_peer_gpu": 1}[side]
+    rng = np.random.default_rng(L + b)
+    g = abi.geom(L, T, b)
+    n_fb, n_slots = 40, 96
+    st = abi.Store(dev, g, n_fb, SEED)
+    pool = abi.Pool(0, g, n_slots, 16)
+    view = pool.peer_view(dev) if side != "pe" else None
+    stager = abi.Stager(dev, g, ring)
+    s = torch.cuda.Stream(device=dev)
+    try:
+        plain, keep, specs, used = [], [], [], 0
+        perm = rng.permutation(n_slots)
+        for t in range(16):
+            nblk = int(rng.integers(0, 9))
+            if used + nblk > n_slots:
+                nblk = 0
+            ntok = 0 if nblk == 0 else (nblk - 1) * T + int(rng.integers(1, T + 1))
+            fb0 = int(rng.integers(0, n_fb - nblk)) if nblk else 0
+            fbs = np.arange(fb0, fb0 + nblk, dtype=np.int64)
+            if nblk >= 4:
+                fbs[nblk // 2:] = rng.integers(0, n_fb, nblk - nblk // 2)  # break the run
+            slots = perm[used:used + nblk].astype(np.int32)
+            used += nblk
+            ds = dev_i32(slots if nblk else [0], dev)
+            keep += [fbs, ds]
+            specs.append((fbs.ctypes.data, ds.data_ptr(), ntok, nblk, 0, L, t))
+            plain.append((fbs, slots, ntok, 0, L))
+        for half in (specs[:7], specs[7:]):  # two calls: the ring is reused across calls
+            jobs = abi.make_jobs(half)
+            if side == "pe":
+                abi.h2d_layer_staged(pool, st, stager, jobs, len(half), s.cuda_stream)
+            else:
+                abi.h2d_push_staged(view, st, stager, jobs, len(half), s.cuda_stream)
+        s.synchronize()
+        for t, (fbs, slots, ntok, l0, l1) in enumerate(plain):
+            items = abi.layer_items(g, len(slots))
+            abi.wait_layer(pool, t, L, items * L, timeout_ms=10000)
+            if len(slots):
+                abi.wait_layer(pool, t, L - 1, items, timeout_ms=10000)
+        sync()
+        assert abi.wait_status(pool) == abi.DP_OK
+        assert stager.launches() >= 2
+        store_img = np.frombuffer(st.bytes(), dtype=np.uint8).copy()
+        check_pool(pool, refpy.geom(L, T, b), plain, T, b, store_img, n_slots)
+        bad = abi.make_jobs([(specs[1][0], specs[1][1], specs[1][2], specs[1][3], 1, L, 1)])  # layer subrange
+        with pytest.raises(abi.DualPathError):
+            abi.h2d_layer_staged(pool, st, stager, bad, 1) if side == "pe" else \
+                abi.h2d_push_staged(view, st, stager, bad, 1)
+    finally:
+        stager.close()
+        if view:
+            view.close()
+        pool.close()
+        st.close()

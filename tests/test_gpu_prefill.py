@@ -140,11 +140,12 @@ def cluster(P, D, L=4, b=576, T=64):
     return cfg
 
 
-def prefill_plan(cfg, policy, tight, quota=5e-4, count=6, turns=5, seed=4):
+def prefill_plan(cfg, policy, tight, quota=5e-4, count=6, turns=5, seed=4, k1_mode=0):
     trajs = dp.synthesize(max_len=12000, count=count, seed=seed, mean_turns=turns, sigma_turns=0)
     planned = dp.plan(cfg, trajs, policy=policy, **STORAGE_BOUND)
     opt = dp.ExecOptions()
     opt.seed = SEED
+    opt.k1_mode = k1_mode
     opt.prefill = True
     opt.compute_quota = quota
     opt.prefill_cost = COST
@@ -266,3 +267,17 @@ def test_prefill_other_geometries(gpus, L, T, b):
     r = eng.run_step()
     assert r.forwards == len(xp.forwards(0)) > 1
     check_digests(eng, cfg, planned, xp)
+
+
+@pytest.mark.parametrize("tight", [False, True])
+def test_prefill_with_staged_loads(gpus, tight):
+    """k1_mode 3 (copy engine into the HBM ring + scatter kernel) under the
+    quota-batched prefill: every K5 digest equals the oracle's."""
+    cfg = cluster(1, 1)
+    trajs, planned, xp = prefill_plan(cfg, "pe_only", tight, k1_mode=3)
+    eng = dp.EngineRuntime(xp, 0, 0)
+    for _ in range(2):
+        eng.reset_counters()
+        r = eng.run_step()
+        assert r.bytes_read == xp.hit_bytes
+        check_digests(eng, cfg, planned, xp)
