@@ -83,6 +83,8 @@ def parse():
     ap.add_argument("--persist", action="store_true",
                     help="also persist generated tokens (decode stand-in + K4 D2H), implies --handoff")
     ap.add_argument("--handoff-ctas", type=int, default=0, help="K3 CTA cap on PEs (0 = default)")
+    ap.add_argument("--no-layerwise", action="store_true",
+                    help="handoff + prefill: K3 after a request's last forward instead of layer by layer")
     ap.add_argument("--gather-ctas", type=int, default=-1, help="K1/K2 CTA cap (-1 = auto)")
     ap.add_argument("--prefill", action="store_true",
                     help="run the prefill stand-in on every PE: compute-quota batched forwards "
@@ -97,10 +99,10 @@ def parse():
                          "and populated once per box; O_DIRECT) through a pinned staging ring")
     ap.add_argument("--io-threads", type=int, default=8, help="storage tier: host IO threads per engine")
     ap.add_argument("--wait-timeout-ms", type=int, default=30000, help="watchdog of every cross-engine wait")
-    ap.add_argument("--k2", default="sm", choices=["sm", "ce", "staged"],
+    ap.add_argument("--k2", default="staged", choices=["sm", "ce", "staged"],
                     help="DE-path loads: sm = K2 gather pushing over NVLink, ce = the DE's copy engine, "
                          "staged = copy engine into an HBM ring + NVLink scatter kernel")
-    ap.add_argument("--k1", default="sm", choices=["sm", "ce", "hybrid", "staged"],
+    ap.add_argument("--k1", default="staged", choices=["sm", "ce", "hybrid", "staged"],
                     help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs), "
                          "hybrid = both at once, jobs split by bytes, staged = copy engine into an HBM "
                          "ring + scatter kernel")
@@ -374,30 +376,38 @@ def link_per_engine(ceiling_bps, n):
     return min(PCIE_ZC_BPS, ceiling_bps / n)
 
 
-def measure_k1(device, shape, target_bytes=18421383168):
-    """The dominant kernel alone, live: one K1 launch (DS-V3 or Qwen Layer
-    Blocks, 8K-token requests, random Full Blocks and slots) through the C
-    ABI, CUDA events on its stream, median of 3 after a warm-up."""
+def measure_k1(device, shape, mode="staged", stage_ctas=32, target_bytes=18421383168):
+    """The dominant transfer alone, live: one K1 call of 64 requests x 128
+    random Full Blocks (DS-V3: 18.4 GB, the launch ncu profiled) through the
+    C ABI -- the staged path (copy engine into the HBM ring + scatter kernel)
+    or the SM gather kernel -- CUDA events on its stream, median of 3 after a
+    warm-up."""
     import numpy as np
     import torch
     from paper_2602_21548_b200 import abi
     L, T, b = shape["L"], shape["T"], shape["b"]
     blocks = 128
     per_job = blocks * T * b * L
-    jobs_n = max(1, min(64, target_bytes // per_job))  # DS-V3: the 64-job launch ncu profiled
+    jobs_n = max(1, min(64, target_bytes // per_job))
     g = abi.geom(L, T, b)
     n_fb = max(blocks, (2 << 30) // (L * T * b))
     st = abi.Store(device, g, n_fb, 9)
     pool = abi.Pool(device, g, jobs_n * blocks, jobs_n)
+    stager = abi.Stager(device, g) if mode == "staged" else None
+    if stager:
+        stager.set_ctas(stage_ctas)
     try:
         rng = np.random.default_rng(0)
         keep, specs = [], []
         perm = rng.permutation(jobs_n * blocks).astype(np.int32)
         for j in range(jobs_n):
-            f = torch.tensor(rng.integers(0, n_fb, blocks), dtype=torch.int64, device=f"cuda:{device}")
+            fbs = rng.integers(0, n_fb - blocks) + np.arange(blocks)  # one session's consecutive Full Blocks
+            f_host = np.ascontiguousarray(fbs, dtype=np.int64)
+            f = torch.tensor(f_host, device=f"cuda:{device}")
             sl = torch.tensor(perm[j * blocks:(j + 1) * blocks], device=f"cuda:{device}")
-            keep += [f, sl]
-            specs.append((f.data_ptr(), sl.data_ptr(), blocks * T, blocks, 0, L, j))
+            keep += [f_host, f, sl]
+            src = f_host.ctypes.data if stager else f.data_ptr()
+            specs.append((src, sl.data_ptr(), blocks * T, blocks, 0, L, j))
         jobs = abi.make_jobs(specs)
         s = torch.cuda.Stream(device=device)
         times = []
@@ -407,7 +417,10 @@ def measure_k1(device, shape, target_bytes=18421383168):
             e1 = torch.cuda.Event(enable_timing=True)
             with torch.cuda.device(device):
                 e0.record(s)
-                abi.h2d_layer_gather(pool, st, jobs, len(specs), s.cuda_stream)
+                if stager:
+                    abi.h2d_layer_staged(pool, st, stager, jobs, len(specs), s.cuda_stream)
+                else:
+                    abi.h2d_layer_gather(pool, st, jobs, len(specs), s.cuda_stream)
                 e1.record(s)
             e1.synchronize()
             if r:
@@ -416,6 +429,8 @@ def measure_k1(device, shape, target_bytes=18421383168):
         nbytes = jobs_n * per_job
         return nbytes / (ms * 1e-3) / 1e9, ms, nbytes
     finally:
+        if stager:
+            stager.close()
         pool.close()
         st.close()
 
@@ -470,6 +485,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     opt.handoff = bool(args.handoff or args.persist)
     opt.persist = bool(args.persist)
     opt.handoff_ctas = args.handoff_ctas
+    opt.handoff_layerwise = not args.no_layerwise
     opt.gather_ctas = args.gather_ctas
     opt.seed = 9
     if args.tier:
@@ -526,6 +542,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
         dpdist.connect_pools(dist, engines, cfg.prefill_nodes)
     dev_ms, host_ms, launches, read_bytes, spans, per_engine = [], [], 0, 0, None, None
     r0_bytes, r0_ms = 0, 0.0  # rank 0's own engine over the timed steps (the roofline)
+    ttft, lag = [], []
     io_wait = 0.0
     d2h = 0
     for step in range(args.warmup + args.steps):
@@ -546,6 +563,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
             read_bytes += sum(dist.allgather(sum(r.bytes_read for r in res)))
             r0_bytes += res[0].bytes_read
             r0_ms += res[0].device_ms
+            ttft, lag = list(res[0].ttft_ms), list(res[0].handoff_lag_ms)
             spans, per_engine = {}, {}
             for part in dist.allgather({e: (r.spans, r.device_ms) for e, r in zip(engines, res)}):
                 for e, (sp, ms) in part.items():
@@ -565,7 +583,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
                    est_s_per_step=sum(est for pe in range(P) for est, _ in xp.forwards(pe)) * shape["L"])
     snic = sum(u["total_bytes"] for u in planned["usage"] if u["kind"] == "snic_read")
     info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens, digest=digest,
-                r0_bytes=r0_bytes, r0_ms=r0_ms, policy=policy,
+                r0_bytes=r0_bytes, r0_ms=r0_ms, policy=policy, ttft_ms=ttft, lag_ms=lag,
                 handoff_bytes=xp.handoff_bytes if (args.handoff or args.persist) else 0,
                 persist_bytes=xp.persist_bytes if args.persist else 0,
                 model_gbps=snic / planned["makespan"] / 1e9 if planned["makespan"] > 0 else None,
@@ -879,10 +897,10 @@ def capped_subrun(args, dist, n, P, D):
             "plan": plan_block(di, "c2", sessions, P, D, sub.cap_gbps, PCIE_ZC_BPS)}
 
 
-def traffic_for(launch_bytes):
-    """DRAM bytes of the K1 launch measure_k1 runs, from the committed ncu
-    --set full capture of that same launch (profiles/k1_traffic.json)."""
-    path = os.path.join(ROOT, "profiles", "k1_traffic.json")
+def traffic_for(launch_bytes, mode):
+    """DRAM bytes of the K1 call measure_k1 runs, from the committed ncu
+    --set full capture of that same call (profiles/k1_traffic*.json)."""
+    path = os.path.join(ROOT, "profiles", "k1_traffic.json" if mode == "sm" else f"k1_traffic_{mode}.json")
     if not os.path.exists(path):
         return None, None
     with open(path) as f:
@@ -957,13 +975,14 @@ def main():
     if dist.rank == 0:
         # the dominant kernel alone (K1, one launch of 64 requests), for the
         # ncu capture of the same launch
-        k1_alone, k1_ms, k1_bytes = measure_k1(my_device(dist), shape)
+        k1_mode = "staged" if args.k1 == "staged" else "sm"
+        k1_alone, k1_ms, k1_bytes = measure_k1(my_device(dist), shape, k1_mode, args.stage_ctas)
         # roofline: rank 0's engine over the timed steps -- the PE's loads
         # (K1 launches back to back on its load stream; at N > 1 also the
         # wait for the DE pushes landing in its pool): algorithmic bytes
         # C*L*b / CUDA-event time on that stream
         achieved = info["r0_bytes"] / (info["r0_ms"] * 1e-3) / 1e9 if info["r0_ms"] > 0 else None
-        traffic, traffic_src = traffic_for(k1_bytes)
+        traffic, traffic_src = traffic_for(k1_bytes, k1_mode)
         stats = (info["requests"], info["hit_bytes"], info["prompt_tokens"])
         extra = {"k1": args.k1, "k2": args.k2}
         if args.handoff_ctas:
@@ -999,10 +1018,13 @@ def main():
                          "peak": round(peak / 1e9, 2) if peak else None, "unit": "GB/s",
                          "frac": round(achieved / (peak / 1e9), 4) if (peak and achieved) else None,
                          "traffic": traffic, "traffic_source": traffic_src,
-                         "kernel": "kv_gather<false> (K1)" if args.k1 == "sm" else f"K1 ({args.k1})",
+                         "kernel": {"sm": "kv_gather<false> (K1)",
+                                    "staged": "K1 staged: copy-engine Full-Block runs into the HBM ring "
+                                              "+ kv_gather<false> scatter (dp_h2d_layer_staged)"}.get(
+                                        args.k1, f"K1 ({args.k1})"),
                          "achieved_what": "rank 0's PE: hit bytes it loaded / CUDA-event time of its "
                                           "load stream over the timed steps",
-                         "kernel_alone": {"achieved": round(k1_alone, 2), "launch_bytes": k1_bytes,
+                         "kernel_alone": {"mode": k1_mode, "achieved": round(k1_alone, 2), "launch_bytes": k1_bytes,
                                           "launch_ms": round(k1_ms, 3),
                                           "frac": round(k1_alone / (peak / 1e9), 4) if peak else None},
                          "peak_source": "cudaMemcpyAsync H2D 1 GiB pinned (copy engine), best of 5, "
@@ -1032,6 +1054,16 @@ def main():
                               "what": "decode stand-in + K4 D2H Full-Block gather every 64 generated "
                                       "tokens + final partial (PersistD2H ledger of the reference)"}
         if args.handoff or args.persist:
+            tt = sorted(info["ttft_ms"] or [0.0])
+            lag = sorted(info["lag_ms"] or [0.0])
+            out["handoff_latency_ms"] = {
+                "what": "per request (rank 0's PE, last timed step): step start -> whole prompt KV in "
+                        "its DE's decode pool (offline TTFT of the prefill path); lag = that minus the end "
+                        "of the forward that finishes it",
+                "layerwise": not args.no_layerwise,
+                "ttft_mean": round(sum(tt) / len(tt), 3), "ttft_p50": round(tt[len(tt) // 2], 3),
+                "ttft_p99": round(tt[min(len(tt) - 1, int(len(tt) * 0.99))], 3),
+                "lag_mean": round(sum(lag) / len(lag), 3), "lag_p99": round(lag[min(len(lag) - 1, int(len(lag) * 0.99))], 3)}
             out["handoff"] = {"bytes_per_step": info["handoff_bytes"],
                               "gbps": round(info["handoff_bytes"] * K / dev_s / 1e9, 3),
                               "what": "PeToDe/MissMerge per layer into DE decode pools (K3, NVLink) "

@@ -67,10 +67,17 @@ struct ExecOptions {
   // CTA cap of the SM gathers (dp_set_gather_ctas) on this run's devices;
   // 0 = default (4 per SM), -1 = auto: 64 on a PE when the handoff shares it
   std::int32_t gather_ctas = -1;
-  // DE-path gate of K3: 0 = the handoff stream waits (cuStreamWaitValue32, no
-  // SMs) for the whole request's hit KV; 1 = K3 gates layer by layer in-kernel
+  // DE-path gate of K3: 0 = the handoff stream waits (a one-thread spin kernel
+  // with the watchdog) for the whole request's hit KV; 1 = K3 gates layer by
+  // layer in-kernel
   std::int32_t k3_layer_gate = 0;
   std::int32_t handoff_ctas = 0;       // K3 CTA cap on PEs (0 = default)
+  // handoff + prefill: K3 pushes layer l of a request as soon as the forward
+  // that finishes it has computed layer l (the reference starts PeToDe /
+  // MissMerge of layer l at LayerCompute l's completion, desim.cpp:630-640,
+  // :721-738), gated in-kernel on per-(forward, layer) done counters the
+  // compute stream writes; false: K3 waits for the forward's last layer
+  bool handoff_layerwise = true;
   // Decode-side persistence (needs `handoff`): each DE runs
   // the decode stand-in for the generated tokens and persists them (K4) every
   // 64 generated tokens plus the final partial, into its persist store
@@ -240,6 +247,11 @@ struct StepResult {
   std::int64_t jobs = 0;
   std::int64_t forwards = 0;    // prefill forwards run (PE, ExecOptions::prefill)
   double io_wait_ms = 0;        // storage tier: host time the launches waited for reads
+  // handoff (PE): per request, ms from the step start until its whole prompt
+  // KV is in its DE's decode pool (the offline TTFT of the prefill path), and
+  // the handoff lag: that time minus the end of the forward finishing it
+  std::vector<float> ttft_ms;
+  std::vector<float> handoff_lag_ms;
   std::int64_t d2h_bytes = 0;   // result read back (PE: landed-counter column)
 };
 
@@ -285,6 +297,10 @@ class EngineRuntime {
 
  private:
   void upload_tables();
+  bool layerwise_handoff() const {
+    return plan_->handoff && plan_->prefill && plan_->opt.handoff_layerwise && is_pe();
+  }
+  std::int32_t fwd_row0_ = 0;               // PE: first per-forward layer-done row
   void storage_read(const LoadJob& j, std::int64_t bytes, StepResult& res);
 
   std::shared_ptr<const ExecPlan> plan_;

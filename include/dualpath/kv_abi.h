@@ -294,7 +294,9 @@ int dp_set_attend_ctas(int device, int32_t ctas);
  * layer (Full-Block pitch -> Layer-Block pitch) plus the partial last block,
  * and after each layer a stream-ordered, fenced 32-bit write of the landed
  * counters (cuStreamWriteValue32): ctr[ticket][l] = items, ctr[ticket][L] =
- * items * layers done.  The isolation mode for a PE that is computing.
+ * items * layers done (absolute values: jobs start at layer 0 and a ticket
+ * belongs to one job per call, else DP_EINVAL).  The isolation mode for a PE
+ * that is computing.
  * HERE the dp_job block arrays (src_fb, dst_slot) must be HOST-readable. */
 int dp_h2d_layer_copy(dp_pool* pe, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
                       dp_stream stream);

@@ -425,6 +425,7 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("de_pool_slots", &dualpath::ExecOptions::de_pool_slots)
       .def_readwrite("gather_ctas", &dualpath::ExecOptions::gather_ctas)
       .def_readwrite("k3_layer_gate", &dualpath::ExecOptions::k3_layer_gate)
+      .def_readwrite("handoff_layerwise", &dualpath::ExecOptions::handoff_layerwise)
       .def_readwrite("handoff_ctas", &dualpath::ExecOptions::handoff_ctas)
       .def_readwrite("persist", &dualpath::ExecOptions::persist)
       .def_readwrite("store_fb", &dualpath::ExecOptions::store_fb)
@@ -581,7 +582,9 @@ PYBIND11_MODULE(_core, m) {
       .def_readonly("jobs", &dualpath::StepResult::jobs)
       .def_readonly("forwards", &dualpath::StepResult::forwards)
       .def_readonly("io_wait_ms", &dualpath::StepResult::io_wait_ms)
-      .def_readonly("d2h_bytes", &dualpath::StepResult::d2h_bytes);
+      .def_readonly("d2h_bytes", &dualpath::StepResult::d2h_bytes)
+      .def_readonly("ttft_ms", &dualpath::StepResult::ttft_ms)
+      .def_readonly("handoff_lag_ms", &dualpath::StepResult::handoff_lag_ms);
 
   py::class_<dualpath::EngineRuntime>(m, "EngineRuntime")
       .def(py::init([](std::shared_ptr<dualpath::ExecPlan> plan, int engine, int device) {

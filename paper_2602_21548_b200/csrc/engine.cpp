@@ -112,8 +112,10 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   if (is_pe()) {
     // handoff: rows [0, n) hit-KV landed, rows [n, 2n) handoff (K3) done
     // handoff / prefill: rows [0, n) hit-KV landed, rows [n, 2n) handoff done / consumed
+    // + with the layerwise handoff, one row per forward: its per-layer done flags
+    fwd_row0_ = std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff || x.prefill ? 2 : 1);
     const std::int32_t rows =
-        std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff || x.prefill ? 2 : 1);
+        fwd_row0_ + (layerwise_handoff() ? static_cast<std::int32_t>(x.forwards[engine_].size()) : 0);
     check(dp_pool_create(device_, &x.geom, x.pool_slots, rows, &pool_), "dp_pool_create");
     peers_[engine_] = pool_;
   } else if (x.handoff) {
@@ -149,7 +151,11 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   std::int32_t ctas = x.opt.gather_ctas;
   if (ctas < 0) ctas = !is_pe() ? 0 : x.prefill ? 32 : x.handoff ? 64 : 0;
   check(dp_set_gather_ctas(device_, ctas), "dp_set_gather_ctas");
-  if (is_pe()) check(dp_set_handoff_ctas(device_, x.opt.handoff_ctas), "dp_set_handoff_ctas");
+  // layerwise K3 CTAs wait in-kernel for the forward's layers: a few suffice
+  // and leave the SMs to the prefill compute
+  if (is_pe())
+    check(dp_set_handoff_ctas(device_, x.opt.handoff_ctas ? x.opt.handoff_ctas : layerwise_handoff() ? 32 : 0),
+          "dp_set_handoff_ctas");
   if (is_pe() && x.prefill) check(dp_set_attend_ctas(device_, x.opt.attend_ctas), "dp_set_attend_ctas");
 }
 
@@ -242,7 +248,7 @@ void EngineRuntime::upload_handoff_tables() {
       pe_local_[mine[i]] = static_cast<int>(i);
       cudaEvent_t a, b;
       check_cuda(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "cudaEventCreate");
-      check_cuda(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaEventCreate(&b), "cudaEventCreate");  // timed: per-request TTFT
       ev_load_.push_back(a);
       ev_k3_.push_back(b);
       const LoadJob& j = x.jobs[mine[i]];
@@ -585,7 +591,9 @@ std::vector<std::uint32_t> EngineRuntime::counters() const {
   std::int64_t bytes = 0;
   check(dp_pool_info(pool_, &base, &ctr, &bytes), "dp_pool_info");
   const ExecPlan& x = *plan_;
-  const std::int32_t rows = is_pe() ? std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff || x.prefill ? 2 : 1)
+  const std::int32_t rows = is_pe() ? fwd_row0_ + (layerwise_handoff() ? static_cast<std::int32_t>(
+                                                                            x.forwards[engine_].size())
+                                                                      : 0)
                                     : std::max<std::int32_t>(1, x.n_de_tickets[engine_]) * (x.persist ? 2 : 1);
   const std::size_t n = static_cast<std::size_t>(rows) * (x.cfg.n_layer + 1);
   std::vector<std::uint32_t> out(n);

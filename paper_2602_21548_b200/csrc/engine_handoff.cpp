@@ -65,7 +65,8 @@ StepResult EngineRuntime::run_step_handoff() {
     auto enqueue_k3 = [&](int ji) {
       const LoadJob& j = x.jobs[ji];
       auto ev_k3 = static_cast<cudaEvent_t>(ev_k3_[pe_local_[ji]]);
-      if (pf)  // the prompt is handed off after its last forward
+      const bool lw = pf && layerwise_handoff();
+      if (pf && !lw)  // the prompt is handed off after its last forward
         check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[ji]]), 0),
                    "cudaStreamWaitEvent");
       if (!j.de_preds.empty()) {
@@ -76,12 +77,15 @@ StepResult EngineRuntime::run_step_handoff() {
         ++res.launches;
       }
       const bool layer_gate = x.opt.k3_layer_gate == 1;
-      if (j.de_path && j.n_blk > 0 && !layer_gate) {
-        check(dp_stream_wait_counter(pool_, j.ticket, L,
-                                     static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) *
-                                                                x.items_per_block * L),
-                                     h),
-              "dp_stream_wait_counter");
+      if (j.de_path && j.n_blk > 0 && !layer_gate && !lw) {
+        // the whole request's hit KV, pushed by its DE: a one-thread spin
+        // kernel with the watchdog (a DE that never pushes -- e.g. its rank
+        // died -- fails the step with DP_ETIMEOUT instead of hanging it)
+        check(dp_wait_layer(pool_, j.ticket, L,
+                            static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block * L),
+                            x.opt.wait_timeout_ms, h),
+              "dp_wait_layer (handoff gate)");
+        ++res.launches;
       }
       dp_handoff_job hj{d_ho_src_ + j.ho_off,
                         d_ho_pe_ + j.ho_off,
@@ -90,8 +94,10 @@ StepResult EngineRuntime::run_step_handoff() {
                         j.prompt,
                         j.n_pblk,
                         j.de_path ? 0 : 1,
-                        (j.de_path && j.n_blk > 0 && layer_gate) ? j.ticket : -1,
-                        static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block),
+                        // layerwise: layer l waits for the finishing forward's layer l (which
+                        // itself waited for the request's hit KV of layer l)
+                        lw ? fwd_row0_ + x.last_fwd[ji] : (j.de_path && j.n_blk > 0 && layer_gate) ? j.ticket : -1,
+                        lw ? 1u : static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block),
                         j.de_ticket,
                         j.ticket + nt(engine_)};
       check(dp_prefill_handoff(pool_, de_views_[j.de], &hj, 1, x.opt.seed, x.opt.wait_timeout_ms, h),
@@ -259,6 +265,19 @@ StepResult EngineRuntime::run_step_handoff() {
   float ms = 0;
   check_cuda(cudaEventElapsedTime(&ms, start, static_cast<cudaEvent_t>(ev_end_)), "cudaEventElapsedTime");
   res.device_ms = ms;
+  if (is_pe()) {  // per request: its prompt KV complete in the decode pool
+    for (int ji : x.by_pe[engine_]) {
+      float t = 0, tf = 0;
+      check_cuda(cudaEventElapsedTime(&t, start, static_cast<cudaEvent_t>(ev_k3_[pe_local_[ji]])),
+                 "cudaEventElapsedTime");
+      res.ttft_ms.push_back(t);
+      if (x.prefill) {
+        check_cuda(cudaEventElapsedTime(&tf, start, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[ji]])),
+                   "cudaEventElapsedTime");
+        res.handoff_lag_ms.push_back(t - tf);
+      }
+    }
+  }
   read_back_landed(res);
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return res;

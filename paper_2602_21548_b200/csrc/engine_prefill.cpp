@@ -62,7 +62,7 @@ void EngineRuntime::upload_prefill_tables() {
     }
     fwd_wait_n_[f] = static_cast<std::int32_t>(wt.size() - fwd_wait_off_[f]);
     cudaEvent_t e;
-    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    check_cuda(cudaEventCreate(&e), "cudaEventCreate");  // timed: the handoff lag
     ev_fwd_.push_back(e);
   }
   d_fwt_ = upload(wt);
@@ -201,6 +201,8 @@ void EngineRuntime::enqueue_forward(int f, StepResult& res) {
     check(dp_prefill_attend(pool_, layer, att.data(), static_cast<int32_t>(att.size()), x.opt.seed, c),
           "dp_prefill_attend");
     res.launches += (work + DP_MAX_ATTEND_ITEMS_PER_LAUNCH - 1) / DP_MAX_ATTEND_ITEMS_PER_LAUNCH;
+    if (layerwise_handoff())  // forward f computed layer l: K3 may push it
+      check(dp_stream_write_counter(pool_, fwd_row0_ + f, layer, 1, c), "dp_stream_write_counter");
   }
   check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_fwd_[f]), c), "cudaEventRecord");
   if (!x.handoff)  // with the handoff, K3 (after the forward) marks the rows

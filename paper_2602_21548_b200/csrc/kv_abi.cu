@@ -804,12 +804,23 @@ int copy_transfer(const char* who, dp_pool* pool, const dp_store* src, const dp_
   const int32_t items = static_cast<int32_t>(chunks_per_block(g));
   DeviceGuard guard(pool->device);
   auto s = static_cast<cudaStream_t>(stream);
+  // The counter writes are absolute (ctr[l] = items, ctr[L] = items * layers
+  // done), not the kernels' increments: a job must start at layer 0 and own
+  // its ticket within the call, or a column could go backwards.
+  std::vector<int32_t> seen;
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    const dp_job& job = jobs[j];
+    if (job.ticket < 0) continue;
+    if (std::find(seen.begin(), seen.end(), job.ticket) != seen.end())
+      return fail(DP_EINVAL, w + ": ticket " + std::to_string(job.ticket) + " used by two jobs of one call");
+    seen.push_back(job.ticket);
+  }
   for (int32_t j = 0; j < n_jobs; ++j) {
     const dp_job& job = jobs[j];
     const int64_t need_blk = (job.n_tokens + g.block_tokens - 1) / g.block_tokens;
-    if (job.n_tokens < 0 || job.n_blk != need_blk || job.layer_begin < 0 ||
+    if (job.n_tokens < 0 || job.n_blk != need_blk || job.layer_begin != 0 ||
         job.layer_end > g.n_layer || job.layer_begin > job.layer_end || job.ticket >= pool->n_tickets)
-      return fail(DP_EINVAL, w + ": job " + std::to_string(j) + " out of range");
+      return fail(DP_EINVAL, w + ": job " + std::to_string(j) + " out of range (copy mode starts at layer 0)");
     if (job.n_blk == 0) continue;
     for (int32_t k = 0; k < job.n_blk; ++k)
       if (job.src_fb[k] < 0 || job.src_fb[k] >= src->n_fb || job.dst_slot[k] < 0 ||

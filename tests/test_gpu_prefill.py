@@ -219,12 +219,15 @@ def test_prefill_1p1d_dual_path(de_dev, tight):
         check_digests(pe, cfg, planned, xp)
 
 
-@pytest.mark.parametrize("tight,persist", [(False, False), (True, False), (True, True)])
-def test_prefill_with_handoff_1p1d(de_dev, tight, persist):
+@pytest.mark.parametrize("tight,persist,layerwise,k1", [(False, False, True, 0), (True, False, True, 0),
+                                                     (True, True, True, 0), (True, False, False, 0),
+                                                     (True, True, True, 3)])
+def test_prefill_with_handoff_1p1d(de_dev, tight, persist, layerwise, k1):
     """The whole pipeline: loads on both paths, quota-batched K5 forwards on
-    the PE, K3 handoff of each prompt after its last forward, (decode +
-    K4 persistence).  Digests equal the oracle's and every prompt lands in its
-    DE's decode pool."""
+    the PE, K3 handoff of each prompt -- layer by layer as its finishing
+    forward computes each layer (layerwise), or after that forward -- (decode
+    + K4 persistence).  Digests equal the oracle's and every prompt lands in
+    its DE's decode pool."""
     from test_gpu_engine import handoff_engines, verify_prompt_pool
     cfg = cluster(1, 1, L=4)
     trajs = dp.synthesize(max_len=12000, count=8, seed=6, mean_turns=5, sigma_turns=0)
@@ -236,6 +239,8 @@ def test_prefill_with_handoff_1p1d(de_dev, tight, persist):
     opt.prefill = True
     opt.compute_quota = 5e-4
     opt.prefill_cost = COST
+    opt.handoff_layerwise = layerwise
+    opt.k1_mode = k1
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     if tight:
         opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots
@@ -248,6 +253,9 @@ def test_prefill_with_handoff_1p1d(de_dev, tight, persist):
         assert sum(r.bytes_read for r in res) == xp.hit_bytes
         assert res[0].forwards == len(xp.forwards(0)) > 1
         check_digests(rts[0], cfg, planned, xp)
+        # every request's prompt is handed off, after (layerwise: as) its last forward computes
+        assert len(res[0].ttft_ms) == len(res[0].handoff_lag_ms) == len(xp.jobs())
+        assert min(res[0].handoff_lag_ms) > -1e-3 and max(res[0].ttft_ms) <= res[0].device_ms + 1e-3
     if not persist:  # (with persistence the decode pool's last occupants also hold generated tokens)
         assert verify_prompt_pool(rts[1], xp, cfg) > 0
     ctr = np.asarray(rts[1].counters(), dtype=np.int64).reshape(-1, cfg.n_layer + 1)
