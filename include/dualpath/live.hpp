@@ -1,0 +1,98 @@
+// dualpath/live.hpp — live-mode scheduling: the reference's
+// global scheduler run on MEASURED engine state while the bytes move.
+//
+// Plan mode (pdsim::desim) fixes every decision in virtual time, bit-exact
+// with the reference for a trace and config, and the executor replays them.
+// Live mode instead runs the reference's scheduler glue
+// (/root/reference/proj/src/desim.cpp:851-906: DE phase 1 -> phase 2 per DE
+// node -> PE fetch over the DE-assigned FIFO, then a FIFO admission pass) on
+// counters that real completions update, as the reference's do:
+//
+//   read_q[node] += C at the decision (desim.cpp:833-835),
+//                -= C when the request's StorageRead completes (:702-704),
+//   tok_e / seq_e of the PE fall at its release (:646-647), of the DE at
+//   the request's completion (:781-783, with hbm_free),
+//   a session's next turn arrives when its previous turn completes.
+//
+// StorageRead is the engine's emulated storage NIC (dp_nic, the rate cap);
+// the hit transfer is K1 / K2 (or their staged variants) on the GPUs; the PE
+// is released when the request's KV has landed in its pool (the load path:
+// no prefill compute), the DE holds the request for gen x decode_s_per_token.
+// Admission reserves the request's blocks in the PE's paged pool (bounded:
+// pe_pool_slots) and stalls, FIFO, while the pool is full -- the staging
+// bound of try_admit (desim.cpp:587-599).
+//
+// Every scheduler invocation's inputs and outputs are logged, so each one can
+// be replayed through the reference's own functions (oracle/_ref) for
+// per-invocation parity (tests/test_live.py).  Decisions themselves depend
+// on real timing; whole-run parity is plan mode's job.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "dualpath/engine.hpp"
+#include "pdsim/desim.hpp"
+#include "pdsim/scheduler.hpp"
+#include "pdsim/types.hpp"
+
+namespace dualpath {
+
+struct LiveOptions {
+  pdsim::desim::SimOptions sim;      // policy, sched_mode, scheduler parameters
+  ExecOptions exec;                  // storage cap, content seed, k1 / k2 modes, store size
+  std::int32_t pe_pool_slots = 0;    // paged pool per PE; 0 = 4x the largest request's blocks
+  double decode_s_per_token = 0;     // emulated decode on the DE after the KV has landed
+  bool gpu = true;                   // false: timed backend (transfers sleep bytes / link_Bps)
+  double link_Bps = 50e9;            // timed backend: per-reader transfer rate
+  std::vector<int> devices;          // engine -> CUDA device (gpu backend; default engine % count)
+  double timeout_s = 600;            // whole-run watchdog
+};
+
+// One scheduler function call, its inputs and result.
+struct LiveInvocation {
+  std::string fn;  // schedule_de_groups | schedule_de_within_group | schedule_pe_fetch | select_read_path
+  double t = 0;
+  std::vector<pdsim::PendingRequest> queue;
+  std::vector<pdsim::EngineSnapshot> snapshots;
+  std::vector<pdsim::GroupLoad> groups;
+  std::vector<pdsim::Assignment> out;  // de_groups: {request, group, 0}
+  std::int64_t pe_read_q = 0, de_read_q = 0;
+  int path = 0;                        // select_read_path: 0 PE, 1 DE
+};
+
+struct LiveRequest {
+  int id = 0, traj = 0, round = 0;
+  std::int64_t cached = 0, append = 0, gen = 0;
+  int pe = -1, de = -1, path = 0, reader = -1;
+  double t_arrival = -1, t_sched = -1, t_admit = -1, t_read_done = -1, t_landed = -1, t_done = -1;
+};
+
+struct LiveReport {
+  std::vector<pdsim::desim::SchedDecision> decisions;
+  std::vector<LiveInvocation> invocations;
+  std::vector<LiveRequest> requests;
+  double wall_s = 0;
+  std::int64_t hit_bytes = 0;
+  std::vector<std::int64_t> reader_bytes;  // per engine
+  std::int64_t admission_stalls = 0;       // admission passes that left a request waiting for pool slots
+  std::int32_t pool_slots = 0;
+  // gpu backend, per PE: the final occupant of every slot (slot, Full Block,
+  // valid tokens) and its content hash for layers 0 and L-1 (parity vs kvref)
+  struct Occupant {
+    int pe = 0;
+    std::int32_t slot = 0;
+    std::int64_t fb = 0;
+    std::int32_t ntok = 0;
+    std::uint64_t hash_first = 0, hash_last = 0;
+  };
+  std::vector<Occupant> final_slots;
+  std::int64_t store_fb = 0, fb_stride = 0;  // content mapping fb = (traj * stride + k) % store_fb
+};
+
+LiveReport run_live(const pdsim::ClusterConfig& cfg, std::span<const pdsim::Trajectory> trajectories,
+                    const LiveOptions& options);
+
+}  // namespace dualpath

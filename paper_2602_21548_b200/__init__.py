@@ -59,6 +59,7 @@ from ._core import (  # noqa: E402
     plan,
     poisson_arrivals,
     run_step_all,
+    run_live,
     save_trace,
     session_chain,
     schedule_de_groups,
@@ -98,6 +99,7 @@ __all__ = [
     "plan",
     "poisson_arrivals",
     "run_step_all",
+    "run_live",
     "save_trace",
     "session_chain",
     "schedule_de_groups",

@@ -14,6 +14,7 @@
 
 #include "dualpath/engine.hpp"
 #include "dualpath/kv_abi.h"
+#include "dualpath/live.hpp"
 #include "pdsim/desim.hpp"
 #include "pdsim/metrics.hpp"
 #include "pdsim/scheduler.hpp"
@@ -613,6 +614,80 @@ PYBIND11_MODULE(_core, m) {
         const auto v = e.read_persisted(fb, layer);
         return py::bytes(reinterpret_cast<const char*>(v.data()), v.size());
       });
+
+  // Live-mode scheduling (dualpath/live.hpp): the reference's scheduler on
+  // measured state while K1 / K2 move the bytes; every invocation logged.
+  m.def(
+      "run_live",
+      [](const ClusterConfig& cfg, const std::vector<Trajectory>& trajs, const std::string& policy,
+         const std::string& sched_mode, std::int64_t alpha, std::int64_t beta, double z,
+         const dualpath::ExecOptions& exec, std::int32_t pe_pool_slots, double decode_s_per_token, bool gpu,
+         double link_Bps, const std::vector<int>& devices, double timeout_s) {
+        dualpath::LiveOptions o;
+        o.sim = make_options(policy, sched_mode, static_cast<double>(alpha), static_cast<double>(beta), 1);
+        o.sim.sched.z_factor = z;
+        o.exec = exec;
+        o.pe_pool_slots = pe_pool_slots;
+        o.decode_s_per_token = decode_s_per_token;
+        o.gpu = gpu;
+        o.link_Bps = link_Bps;
+        o.devices = devices;
+        o.timeout_s = timeout_s;
+        dualpath::LiveReport rep;
+        {
+          py::gil_scoped_release nogil;
+          rep = dualpath::run_live(cfg, trajs, o);
+        }
+        py::dict d;
+        py::list dec;
+        for (const auto& x : rep.decisions)
+          dec.append(py::make_tuple(x.t, x.request_id, x.pe, x.de, x.path == ReadPath::PEPath ? 0 : 1,
+                                    x.pe_category, x.de_category));
+        d["decisions"] = dec;
+        py::list inv;
+        for (const auto& v : rep.invocations) {
+          py::dict e;
+          e["fn"] = v.fn;
+          e["t"] = v.t;
+          py::list q, sn, gr, out;
+          for (const auto& p : v.queue) q.append(py::make_tuple(p.id, p.tokens));
+          for (const auto& x : v.snapshots)
+            sn.append(py::make_tuple(x.engine_id, x.node_id, x.kind == EngineKind::PE ? 0 : 1, x.seq_e, x.tok_e,
+                                     x.read_q, x.hbm_free_tokens));
+          for (const auto& g : v.groups) gr.append(py::make_tuple(g.group_id, g.tok_sum));
+          for (const auto& a : v.out) out.append(py::make_tuple(a.request_id, a.engine_id, a.category));
+          e["queue"] = q;
+          e["snapshots"] = sn;
+          e["groups"] = gr;
+          e["out"] = out;
+          e["pe_read_q"] = v.pe_read_q;
+          e["de_read_q"] = v.de_read_q;
+          e["path"] = v.path;
+          inv.append(e);
+        }
+        d["invocations"] = inv;
+        py::list reqs;
+        for (const auto& r : rep.requests)
+          reqs.append(py::make_tuple(r.id, r.traj, r.round, r.cached, r.append, r.gen, r.pe, r.de, r.path, r.reader,
+                                     r.t_arrival, r.t_sched, r.t_admit, r.t_read_done, r.t_landed, r.t_done));
+        d["requests"] = reqs;
+        py::list occ;
+        for (const auto& x : rep.final_slots)
+          occ.append(py::make_tuple(x.pe, x.slot, x.fb, x.ntok, x.hash_first, x.hash_last));
+        d["final_slots"] = occ;
+        d["wall_s"] = rep.wall_s;
+        d["reader_bytes"] = rep.reader_bytes;
+        d["admission_stalls"] = rep.admission_stalls;
+        d["pool_slots"] = rep.pool_slots;
+        d["store_fb"] = rep.store_fb;
+        d["fb_stride"] = rep.fb_stride;
+        return d;
+      },
+      py::arg("cfg"), py::arg("trajectories"), py::arg("policy") = "dual_path",
+      py::arg("sched_mode") = "adaptive", py::arg("alpha") = 100000, py::arg("beta") = 500000,
+      py::arg("z") = 1.05, py::arg("exec") = dualpath::ExecOptions{}, py::arg("pe_pool_slots") = 0,
+      py::arg("decode_s_per_token") = 0.0, py::arg("gpu") = true, py::arg("link_Bps") = 50e9,
+      py::arg("devices") = std::vector<int>{}, py::arg("timeout_s") = 600.0);
 
   m.def(
       "run_step_all",

@@ -1,0 +1,653 @@
+// Live-mode scheduling (include/dualpath/live.hpp): the reference's global
+// scheduler (/root/reference/proj/src/desim.cpp:797-906) driven by real
+// completions, the bytes moved by the C ABI's K1 / K2 on the GPUs (or by a
+// timed backend for host-only tests).
+#include "dualpath/live.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <queue>
+#include <stdexcept>
+#include <thread>
+#include <unordered_map>
+
+#include "engine_detail.hpp"
+
+namespace dualpath {
+namespace {
+
+using detail::check;
+using detail::check_cuda;
+using detail::DeviceScope;
+using Clock = std::chrono::steady_clock;
+
+struct Req {
+  LiveRequest r;
+  std::int64_t total() const { return r.cached + r.append + r.gen; }
+  std::int32_t n_blk = 0;
+  std::int64_t tab_off = 0;  // its blocks in the slot / Full Block tables
+};
+
+struct Msg {
+  enum Kind { ReadDone, Landed } kind;
+  int req;
+};
+
+// One reader engine's transfer pipeline: a FIFO worker (storage NIC, then
+// the launch) and a completion thread (waits for each transfer in order).
+struct Reader {
+  int engine = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<int> jobs;          // requests to read, FIFO
+  std::deque<std::pair<int, cudaEvent_t>> inflight;
+  std::deque<double> inflight_done;  // timed backend: completion times
+  bool stop = false;
+  std::thread worker, completer;
+};
+
+class Live {
+ public:
+  Live(const pdsim::ClusterConfig& cfg, std::span<const pdsim::Trajectory> trajs, const LiveOptions& o)
+      : cfg_(cfg), trajs_(trajs), o_(o) {
+    cfg_.validate();
+    g_ = cfg_.engines_per_node;
+    n_pe_ = cfg_.prefill_nodes * g_;
+    n_eng_ = cfg_.total_engines();
+    tok_.assign(n_eng_, 0);
+    seq_.assign(n_eng_, 0);
+    hbm_free_.assign(n_eng_, cfg_.hbm_capacity_tokens);
+    read_q_.assign(cfg_.prefill_nodes + cfg_.decode_nodes, 0);
+    private_q_.assign(cfg_.prefill_nodes + cfg_.decode_nodes, {});
+    next_round_.assign(trajs_.size(), 0);
+    T_ = cfg_.block_size_tokens;
+    L_ = cfg_.n_layer;
+    // every turn of every session, ids in arrival order are assigned at arrival
+    std::int64_t max_blk = 1, total_blk = 0;
+    for (const auto& t : trajs_) {
+      fb_stride_ = std::max(fb_stride_, pdsim::blocks_for(t.total_tokens(), cfg_));
+      for (std::size_t k = 0; k < t.rounds.size(); ++k) {
+        const std::int64_t c = pdsim::context_before(t, k);
+        const std::int64_t nb = (c + T_ - 1) / T_;
+        max_blk = std::max(max_blk, nb);
+        total_blk += nb;
+        ++total_reqs_;
+      }
+    }
+    reqs_.reserve(static_cast<std::size_t>(total_reqs_));  // workers hold references: never reallocate
+    pool_slots_ = o_.pe_pool_slots > 0 ? o_.pe_pool_slots : static_cast<std::int32_t>(4 * max_blk);
+    if (pool_slots_ < max_blk)
+      throw pdsim::desim::ConfigError("run_live: pe_pool_slots smaller than the largest request");
+    const std::int64_t fbb = cfg_.full_block_bytes();
+    store_fb_ = std::max<std::int64_t>(
+        1, std::min<std::int64_t>(fb_stride_ * static_cast<std::int64_t>(std::max<std::size_t>(1, trajs_.size())),
+                                  o_.exec.store_bytes_max / fbb));
+    free_slots_.assign(n_pe_, {});
+    for (int p = 0; p < n_pe_; ++p)
+      for (std::int32_t s = pool_slots_ - 1; s >= 0; --s) free_slots_[p].push_back(s);
+    occupant_.assign(static_cast<std::size_t>(n_pe_) * pool_slots_, {-1, 0});
+    reader_bytes_.assign(n_eng_, 0);
+    if (o_.gpu) setup_gpu(total_blk);
+    else {
+      tab_slot_h_ = new std::int32_t[std::max<std::int64_t>(1, total_blk)];
+      tab_fb_h_ = new std::int64_t[std::max<std::int64_t>(1, total_blk)];
+    }
+    for (int e = 0; e < n_eng_; ++e) {
+      dp_nic* nic = nullptr;
+      const double cap = o_.exec.storage_cap_per_engine.empty() ? o_.exec.storage_cap_Bps
+                                                                : o_.exec.storage_cap_per_engine.at(e);
+      check(dp_nic_create(cap, &nic), "dp_nic_create");
+      nics_.push_back(nic);
+    }
+  }
+
+  ~Live() {
+    for (auto& r : readers_) {
+      {
+        std::lock_guard<std::mutex> lk(r->mu);
+        r->stop = true;
+      }
+      r->cv.notify_all();
+      if (r->worker.joinable()) r->worker.join();
+      if (r->completer.joinable()) r->completer.join();
+    }
+    for (dp_nic* n : nics_) dp_nic_destroy(n);
+    for (dp_stager* s : stagers_) dp_stager_destroy(s);
+    for (auto& row : views_)
+      for (dp_pool* v : row)
+        if (v) dp_pool_destroy(v);
+    for (dp_pool* p : pools_) dp_pool_destroy(p);
+    for (dp_store* s : stores_) dp_store_destroy(s);
+    for (std::size_t e = 0; e < streams_.size(); ++e)
+      if (streams_[e]) detail::release_stream(devs_[e], streams_[e]);
+    if (o_.gpu) {
+      if (tab_slot_h_) cudaFreeHost(tab_slot_h_);
+      if (tab_fb_h_) cudaFreeHost(tab_fb_h_);
+    } else {
+      delete[] tab_slot_h_;
+      delete[] tab_fb_h_;
+    }
+  }
+
+  LiveReport run() {
+    t0_ = Clock::now();
+    for (dp_nic* n : nics_) check(dp_nic_start(n), "dp_nic_start");
+    for (int e = 0; e < n_eng_; ++e) {
+      readers_.push_back(std::make_unique<Reader>());
+      Reader* rd = readers_.back().get();
+      rd->engine = e;
+      rd->worker = std::thread([this, rd] { worker(rd); });
+      rd->completer = std::thread([this, rd] { completer(rd); });
+    }
+    for (std::size_t t = 0; t < trajs_.size(); ++t) arrive(static_cast<int>(t));
+    wake();
+    auto last_progress = Clock::now();
+    while (completed_ < total_reqs_) {
+      std::vector<Msg> msgs;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        const auto until = timers_.empty() ? Clock::now() + std::chrono::milliseconds(200)
+                                           : t0_ + std::chrono::duration_cast<Clock::duration>(
+                                                       std::chrono::duration<double>(timers_.top().first));
+        cv_.wait_until(lk, until, [this] { return !msgs_.empty() || !worker_error_.empty(); });
+        if (!worker_error_.empty()) throw std::runtime_error("run_live: " + worker_error_);
+        msgs.swap(msgs_);
+      }
+      const bool progress = !msgs.empty();
+      for (const Msg& m : msgs) handle(m);
+      while (!timers_.empty() && timers_.top().first <= now()) {
+        const int id = timers_.top().second;
+        timers_.pop();
+        complete(id);
+      }
+      wake();
+      if (progress) last_progress = Clock::now();
+      if (std::chrono::duration<double>(Clock::now() - last_progress).count() > o_.timeout_s)
+        throw std::runtime_error("run_live: no progress for " + std::to_string(o_.timeout_s) + " s");
+    }
+    rep_.wall_s = now();
+    for (auto& r : readers_) {
+      {
+        std::lock_guard<std::mutex> lk(r->mu);
+        r->stop = true;
+      }
+      r->cv.notify_all();
+      r->worker.join();
+      r->completer.join();
+    }
+    readers_.clear();
+    if (o_.gpu) final_occupants();
+    for (auto& q : reqs_) rep_.requests.push_back(q.r);
+    rep_.reader_bytes = reader_bytes_;
+    rep_.pool_slots = pool_slots_;
+    rep_.store_fb = store_fb_;
+    rep_.fb_stride = fb_stride_;
+    return std::move(rep_);
+  }
+
+ private:
+  double now() const { return std::chrono::duration<double>(Clock::now() - t0_).count(); }
+  int node_of(int e) const { return e / g_; }
+  bool is_pe(int e) const { return e < n_pe_; }
+  std::int64_t fb_of(int traj, std::int64_t k) const { return (traj * fb_stride_ + k) % store_fb_; }
+
+  void post(Msg m) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      msgs_.push_back(m);
+    }
+    cv_.notify_one();
+  }
+  void fail_async(const std::string& what) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      if (worker_error_.empty()) worker_error_ = what;
+    }
+    cv_.notify_one();
+  }
+
+  // ---- the reference's request life cycle, on measured events ----------
+  void arrive(int t) {  // on_arrival (desim.cpp:551-566)
+    const pdsim::Trajectory& tr = trajs_[t];
+    const int round = next_round_[t]++;
+    Req q;
+    q.r.id = static_cast<int>(reqs_.size());
+    q.r.traj = t;
+    q.r.round = round;
+    q.r.cached = pdsim::context_before(tr, static_cast<std::size_t>(round));
+    q.r.append = tr.rounds[round].append_tokens;
+    q.r.gen = tr.rounds[round].gen_tokens;
+    q.r.t_arrival = now();
+    q.n_blk = static_cast<std::int32_t>((q.r.cached + T_ - 1) / T_);
+    q.tab_off = tab_used_;
+    tab_used_ += q.n_blk;
+    reqs_.push_back(q);
+    de_global_.push_back(q.r.id);
+  }
+
+  pdsim::EngineSnapshot snapshot_of(int e) const {  // desim.cpp:797-807
+    pdsim::EngineSnapshot s;
+    s.engine_id = e;
+    s.node_id = node_of(e);
+    s.kind = is_pe(e) ? pdsim::EngineKind::PE : pdsim::EngineKind::DE;
+    s.seq_e = seq_[e];
+    s.tok_e = tok_[e];
+    s.read_q = read_q_[node_of(e)];
+    s.hbm_free_tokens = hbm_free_[e];
+    return s;
+  }
+
+  void assign_de(Req& q, int de, int cat) {  // desim.cpp:809-817
+    q.r.de = de;
+    de_cat_[q.r.id] = cat;
+    tok_[de] += q.total();
+    seq_[de] += 1;
+    hbm_free_[de] -= q.total();
+    pe_waiting_.push_back(q.r.id);
+  }
+
+  void assign_pe(Req& q, int pe, int cat) {  // desim.cpp:819-849
+    q.r.pe = pe;
+    tok_[pe] += q.total();
+    seq_[pe] += 1;
+    q.r.t_sched = now();
+    pdsim::ReadPath path;
+    const auto& pol = o_.sim;
+    if (pol.policy == pdsim::desim::Policy::PEOnly) {
+      path = pdsim::ReadPath::PEPath;
+    } else if (pol.sched_mode == pdsim::desim::SchedMode::RoundRobin) {
+      path = (rr_path_++ % 2 == 0) ? pdsim::ReadPath::PEPath : pdsim::ReadPath::DEPath;
+    } else {
+      const std::int64_t a = read_q_[node_of(q.r.pe)], b = read_q_[node_of(q.r.de)];
+      path = pdsim::select_read_path(a, b);
+      LiveInvocation inv;
+      inv.fn = "select_read_path";
+      inv.t = now();
+      inv.pe_read_q = a;
+      inv.de_read_q = b;
+      inv.path = path == pdsim::ReadPath::PEPath ? 0 : 1;
+      rep_.invocations.push_back(std::move(inv));
+    }
+    q.r.path = path == pdsim::ReadPath::PEPath ? 0 : 1;
+    q.r.reader = q.r.path == 0 ? q.r.pe : q.r.de;
+    if (q.r.cached > 0 && pol.policy != pdsim::desim::Policy::Oracle) read_q_[node_of(q.r.reader)] += q.r.cached;
+    admission_.push_back(q.r.id);
+    rep_.decisions.push_back({q.r.t_sched, q.r.id, q.r.pe, q.r.de, path, cat, de_cat_[q.r.id]});
+  }
+
+  void schedule_adaptive() {  // desim.cpp:865-906
+    if (!de_global_.empty()) {
+      std::vector<pdsim::GroupLoad> groups;
+      for (int n = cfg_.prefill_nodes; n < cfg_.prefill_nodes + cfg_.decode_nodes; ++n) {
+        pdsim::GroupLoad gl{n, 0};
+        for (int k = 0; k < g_; ++k) gl.tok_sum += tok_[n * g_ + k];
+        for (int id : private_q_[n]) gl.tok_sum += reqs_[id].total();
+        groups.push_back(gl);
+      }
+      std::vector<pdsim::PendingRequest> pending;
+      for (int id : de_global_) pending.push_back({id, reqs_[id].total()});
+      const auto out = pdsim::schedule_de_groups(pending, groups);
+      LiveInvocation inv;
+      inv.fn = "schedule_de_groups";
+      inv.t = now();
+      inv.queue = pending;
+      inv.groups = groups;
+      for (const auto& [req, group] : out) {
+        private_q_[group].push_back(req);
+        inv.out.push_back({req, group, 0});
+      }
+      rep_.invocations.push_back(std::move(inv));
+      de_global_.clear();
+    }
+    for (int n = cfg_.prefill_nodes; n < cfg_.prefill_nodes + cfg_.decode_nodes; ++n) {
+      auto& q = private_q_[n];
+      if (q.empty()) continue;
+      std::vector<pdsim::PendingRequest> pending;
+      for (int id : q) pending.push_back({id, reqs_[id].total()});
+      std::vector<pdsim::EngineSnapshot> snaps;
+      for (int k = 0; k < g_; ++k) snaps.push_back(snapshot_of(n * g_ + k));
+      const auto asg = pdsim::schedule_de_within_group(pending, snaps, o_.sim.sched);
+      LiveInvocation inv;
+      inv.fn = "schedule_de_within_group";
+      inv.t = now();
+      inv.queue = pending;
+      inv.snapshots = snaps;
+      inv.out = asg;
+      rep_.invocations.push_back(std::move(inv));
+      for (const auto& a : asg) assign_de(reqs_[a.request_id], a.engine_id, a.category);
+      q.erase(q.begin(), q.begin() + static_cast<std::ptrdiff_t>(asg.size()));
+    }
+    if (!pe_waiting_.empty()) {
+      std::vector<pdsim::PendingRequest> pending;
+      for (int id : pe_waiting_) pending.push_back({id, reqs_[id].total()});
+      std::vector<pdsim::EngineSnapshot> snaps;
+      for (int e = 0; e < n_pe_; ++e) snaps.push_back(snapshot_of(e));
+      const auto asg = pdsim::schedule_pe_fetch(pending, snaps, o_.sim.sched);
+      LiveInvocation inv;
+      inv.fn = "schedule_pe_fetch";
+      inv.t = now();
+      inv.queue = pending;
+      inv.snapshots = snaps;
+      inv.out = asg;
+      rep_.invocations.push_back(std::move(inv));
+      for (const auto& a : asg) assign_pe(reqs_[a.request_id], a.engine_id, a.category);
+      pe_waiting_.erase(pe_waiting_.begin(), pe_waiting_.begin() + static_cast<std::ptrdiff_t>(asg.size()));
+    }
+  }
+
+  void schedule_round_robin() {  // desim.cpp:908-933
+    while (!de_global_.empty()) {
+      Req& q = reqs_[de_global_.front()];
+      const int n_de = n_eng_ - n_pe_;
+      int chosen = -1;
+      for (int i = 0; i < n_de; ++i) {
+        const int e = n_pe_ + (rr_de_ + i) % n_de;
+        if (hbm_free_[e] >= q.total()) {
+          chosen = e;
+          rr_de_ = (rr_de_ + i + 1) % n_de;
+          break;
+        }
+      }
+      if (chosen < 0) break;
+      de_global_.pop_front();
+      assign_de(q, chosen, 0);
+    }
+    while (!pe_waiting_.empty()) {
+      Req& q = reqs_[pe_waiting_.front()];
+      pe_waiting_.pop_front();
+      const int pe = rr_pe_ % n_pe_;
+      rr_pe_ = (rr_pe_ + 1) % n_pe_;
+      assign_pe(q, pe, 0);
+    }
+  }
+
+  void wake() {  // scheduler_wake (desim.cpp:851-863)
+    if (o_.sim.sched_mode == pdsim::desim::SchedMode::Adaptive) schedule_adaptive();
+    else schedule_round_robin();
+    // admission pass, FIFO; PEs progress independently.  The bounded
+    // resource is the PE's paged pool: a request waits for its blocks.
+    bool stalled = false;
+    for (auto it = admission_.begin(); it != admission_.end();) {
+      Req& q = reqs_[*it];
+      auto& fl = free_slots_[q.r.pe];
+      if (static_cast<std::int64_t>(fl.size()) < q.n_blk) {
+        stalled = true;
+        ++it;
+        continue;
+      }
+      for (std::int32_t k = 0; k < q.n_blk; ++k) {
+        const std::int32_t s = fl.back();
+        fl.pop_back();
+        tab_slot_h_[q.tab_off + k] = s;
+        tab_fb_h_[q.tab_off + k] = fb_of(q.r.traj, k);
+        occupant_[static_cast<std::size_t>(q.r.pe) * pool_slots_ + s] = {
+            tab_fb_h_[q.tab_off + k], static_cast<std::int32_t>(std::min<std::int64_t>(T_, q.r.cached - k * T_))};
+      }
+      q.r.t_admit = now();
+      const int id = q.r.id;
+      it = admission_.erase(it);
+      if (q.r.cached == 0) {  // no hit KV: nothing to read (desim.cpp:709)
+        q.r.t_read_done = q.r.t_landed = q.r.t_admit;
+        handle({Msg::Landed, id});
+        continue;
+      }
+      Reader* rd = readers_[q.r.reader].get();
+      {
+        std::lock_guard<std::mutex> lk(rd->mu);
+        rd->jobs.push_back(id);
+      }
+      rd->cv.notify_all();
+    }
+    if (stalled) ++rep_.admission_stalls;
+  }
+
+  void handle(const Msg& m) {
+    Req& q = reqs_[m.req];
+    if (m.kind == Msg::ReadDone) {  // complete_stage(StorageRead): read_q -= C (desim.cpp:702-704)
+      q.r.t_read_done = now();
+      if (o_.sim.policy != pdsim::desim::Policy::Oracle) read_q_[node_of(q.r.reader)] -= q.r.cached;
+      return;
+    }
+    // the hit KV is in the PE pool: the load path's PE release (desim.cpp:646-647)
+    if (q.r.t_landed < 0) q.r.t_landed = now();
+    tok_[q.r.pe] -= q.total();
+    seq_[q.r.pe] -= 1;
+    auto& fl = free_slots_[q.r.pe];
+    for (std::int32_t k = 0; k < q.n_blk; ++k) fl.push_back(tab_slot_h_[q.tab_off + k]);
+    if (o_.decode_s_per_token > 0)
+      timers_.push({now() + static_cast<double>(q.r.gen) * o_.decode_s_per_token, q.r.id});
+    else
+      complete(q.r.id);
+  }
+
+  void complete(int id) {  // request done on its DE (desim.cpp:776-787), then the next turn
+    Req& q = reqs_[id];
+    q.r.t_done = now();
+    tok_[q.r.de] -= q.total();
+    seq_[q.r.de] -= 1;
+    hbm_free_[q.r.de] += q.total();
+    ++completed_;
+    if (next_round_[q.r.traj] < static_cast<int>(trajs_[q.r.traj].rounds.size())) arrive(q.r.traj);
+  }
+
+  // ---- reader threads ---------------------------------------------------
+  void worker(Reader* rd) {
+    const int e = rd->engine;
+    try {
+      if (o_.gpu) check_cuda(cudaSetDevice(devs_[e]), "cudaSetDevice");
+      for (;;) {
+        int id;
+        {
+          std::unique_lock<std::mutex> lk(rd->mu);
+          rd->cv.wait(lk, [rd] { return rd->stop || !rd->jobs.empty(); });
+          if (rd->jobs.empty()) return;
+          id = rd->jobs.front();
+          rd->jobs.pop_front();
+        }
+        const Req& q = reqs_[id];  // fields read here are fixed once admitted
+        const std::int64_t bytes = q.r.cached * cfg_.kv_bytes_per_token();
+        check(dp_nic_read(nics_[e], bytes, 0.0, nullptr, nullptr), "dp_nic_read");  // StorageRead
+        post({Msg::ReadDone, id});
+        reader_bytes_[e] += bytes;
+        cudaEvent_t ev = nullptr;
+        if (o_.gpu) ev = launch(e, q);
+        {
+          std::lock_guard<std::mutex> lk(rd->mu);
+          rd->inflight.emplace_back(id, ev);
+          if (!o_.gpu) {
+            const double start = std::max(now(), rd->inflight_done.empty() ? 0.0 : rd->inflight_done.back());
+            rd->inflight_done.push_back(start + static_cast<double>(bytes) / o_.link_Bps);
+          }
+        }
+        rd->cv.notify_all();
+      }
+    } catch (const std::exception& ex) {
+      fail_async(ex.what());
+    }
+  }
+
+  void completer(Reader* rd) {
+    try {
+      if (o_.gpu) check_cuda(cudaSetDevice(devs_[rd->engine]), "cudaSetDevice");
+      for (;;) {
+        int id;
+        cudaEvent_t ev;
+        double done_at = 0;
+        {
+          std::unique_lock<std::mutex> lk(rd->mu);
+          rd->cv.wait(lk, [rd] { return !rd->inflight.empty() || (rd->stop && rd->jobs.empty()); });
+          if (rd->inflight.empty()) return;
+          std::tie(id, ev) = rd->inflight.front();
+          rd->inflight.pop_front();
+          if (!o_.gpu) {
+            done_at = rd->inflight_done.front();
+            rd->inflight_done.pop_front();
+          }
+        }
+        if (o_.gpu) {
+          check_cuda(cudaEventSynchronize(ev), "transfer sync");
+          cudaEventDestroy(ev);
+          const Req& q = reqs_[id];
+          for (dp_pool* p : {pools_[q.r.pe], views_[rd->engine][q.r.pe]})
+            if (p) check(dp_wait_status(p), "transfer watchdog");
+        } else {
+          std::this_thread::sleep_until(t0_ + std::chrono::duration_cast<Clock::duration>(
+                                                  std::chrono::duration<double>(done_at)));
+        }
+        post({Msg::Landed, id});
+      }
+    } catch (const std::exception& ex) {
+      fail_async(ex.what());
+    }
+  }
+
+  // ---- gpu backend ------------------------------------------------------
+  void setup_gpu(std::int64_t total_blk) {
+    int ndev = 0;
+    check_cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (ndev < 1) throw std::runtime_error("run_live: no CUDA device");
+    devs_ = o_.devices;
+    if (devs_.empty())
+      for (int e = 0; e < n_eng_; ++e) devs_.push_back(e % ndev);
+    if (static_cast<int>(devs_.size()) != n_eng_) throw std::invalid_argument("run_live: one device per engine");
+    const dp_kv_geom geom{L_, T_, cfg_.kv_bytes_per_token_per_layer};
+    check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&tab_slot_h_), std::max<std::int64_t>(1, total_blk) * 4,
+                             cudaHostAllocMapped | cudaHostAllocPortable),
+               "cudaHostAlloc tables");
+    check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&tab_fb_h_), std::max<std::int64_t>(1, total_blk) * 8,
+                             cudaHostAllocMapped | cudaHostAllocPortable),
+               "cudaHostAlloc tables");
+    for (int e = 0; e < n_eng_; ++e) {
+      dp_store* st = nullptr;
+      check(dp_store_create(devs_[e], &geom, store_fb_, o_.exec.seed, &st), "dp_store_create");
+      stores_.push_back(st);
+      streams_.push_back(detail::acquire_stream(devs_[e]));
+      dp_stager* sg = nullptr;
+      if ((is_pe(e) && o_.exec.k1_mode == 3) || (!is_pe(e) && o_.exec.k2_mode == 2)) {
+        check(dp_stager_create(devs_[e], &geom, o_.exec.stage_ring_bytes, &sg), "dp_stager_create");
+        check(dp_stager_set_ctas(sg, o_.exec.stage_ctas), "dp_stager_set_ctas");
+      }
+      stagers_.push_back(sg);
+    }
+    for (int p = 0; p < n_pe_; ++p) {
+      dp_pool* pool = nullptr;
+      check(dp_pool_create(devs_[p], &geom, pool_slots_, static_cast<std::int32_t>(std::max<std::int64_t>(1, total_reqs_)),
+                           &pool),
+            "dp_pool_create");
+      pools_.push_back(pool);
+    }
+    views_.assign(n_eng_, std::vector<dp_pool*>(n_pe_, nullptr));
+    for (int e = 0; e < n_eng_; ++e)
+      for (int p = 0; p < n_pe_; ++p)
+        if (e != p) check(dp_pool_peer_view(devs_[e], pools_[p], &views_[e][p]), "dp_pool_peer_view");
+  }
+
+  cudaEvent_t launch(int e, const Req& q) {
+    DeviceScope ds(devs_[e]);
+    const bool local = e == q.r.pe;
+    dp_pool* dst = local ? pools_[q.r.pe] : views_[e][q.r.pe];
+    dp_job job{tab_fb_h_ + q.tab_off, tab_slot_h_ + q.tab_off, q.r.cached, q.n_blk, 0, L_, q.r.id};
+    cudaStream_t s = streams_[e];
+    if (stagers_[e]) {
+      check(local ? dp_h2d_layer_staged(dst, stores_[e], stagers_[e], &job, 1, s)
+                  : dp_h2d_push_staged(dst, stores_[e], stagers_[e], &job, 1, s),
+            "staged transfer");
+    } else {
+      check(local ? dp_h2d_layer_gather(dst, stores_[e], &job, 1, s)
+                  : dp_h2d_push_p2p_layer(dst, stores_[e], &job, 1, s),
+            "gather transfer");
+    }
+    cudaEvent_t ev;
+    check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+    check_cuda(cudaEventRecord(ev, s), "cudaEventRecord");
+    return ev;
+  }
+
+  void final_occupants() {
+    for (int p = 0; p < n_pe_; ++p) {
+      std::vector<std::int32_t> slots, ntok;
+      std::vector<std::int64_t> fbs;
+      for (std::int32_t s = 0; s < pool_slots_; ++s) {
+        const auto& oc = occupant_[static_cast<std::size_t>(p) * pool_slots_ + s];
+        if (oc.first < 0) continue;
+        slots.push_back(s);
+        fbs.push_back(oc.first);
+        ntok.push_back(oc.second);
+      }
+      if (slots.empty()) continue;
+      DeviceScope ds(devs_[p]);
+      const std::size_t n = slots.size();
+      std::int32_t *d_s = nullptr, *d_n = nullptr;
+      std::uint64_t* d_o = nullptr;
+      check_cuda(cudaMalloc(reinterpret_cast<void**>(&d_s), n * 4), "cudaMalloc");
+      check_cuda(cudaMalloc(reinterpret_cast<void**>(&d_n), n * 4), "cudaMalloc");
+      check_cuda(cudaMalloc(reinterpret_cast<void**>(&d_o), n * 8), "cudaMalloc");
+      check_cuda(cudaMemcpy(d_s, slots.data(), n * 4, cudaMemcpyHostToDevice), "H2D");
+      check_cuda(cudaMemcpy(d_n, ntok.data(), n * 4, cudaMemcpyHostToDevice), "H2D");
+      std::vector<std::uint64_t> h0(n), h1(n);
+      check(dp_pool_checksum(pools_[p], 0, d_s, d_n, static_cast<std::int32_t>(n), d_o, nullptr), "checksum");
+      check_cuda(cudaMemcpy(h0.data(), d_o, n * 8, cudaMemcpyDeviceToHost), "D2H");
+      check(dp_pool_checksum(pools_[p], L_ - 1, d_s, d_n, static_cast<std::int32_t>(n), d_o, nullptr), "checksum");
+      check_cuda(cudaMemcpy(h1.data(), d_o, n * 8, cudaMemcpyDeviceToHost), "D2H");
+      cudaFree(d_s);
+      cudaFree(d_n);
+      cudaFree(d_o);
+      for (std::size_t i = 0; i < n; ++i)
+        rep_.final_slots.push_back({p, slots[i], fbs[i], ntok[i], h0[i], h1[i]});
+    }
+  }
+
+  pdsim::ClusterConfig cfg_;
+  std::span<const pdsim::Trajectory> trajs_;
+  LiveOptions o_;
+  int g_ = 1, n_pe_ = 1, n_eng_ = 2;
+  std::int32_t T_ = 64, L_ = 1;
+  std::int64_t total_reqs_ = 0, completed_ = 0, fb_stride_ = 1, store_fb_ = 1, tab_used_ = 0;
+  std::int32_t pool_slots_ = 0;
+  Clock::time_point t0_;
+  std::vector<Req> reqs_;
+  std::vector<int> next_round_;
+  std::vector<std::int64_t> tok_, seq_, hbm_free_, read_q_;
+  std::deque<int> de_global_, pe_waiting_;
+  std::vector<std::vector<int>> private_q_;
+  std::vector<int> admission_;
+  std::unordered_map<int, int> de_cat_;
+  int rr_de_ = 0, rr_pe_ = 0;
+  std::uint64_t rr_path_ = 0;
+  std::vector<std::vector<std::int32_t>> free_slots_;
+  std::vector<std::pair<std::int64_t, std::int32_t>> occupant_;
+  using Timer = std::pair<double, int>;
+  std::priority_queue<Timer, std::vector<Timer>, std::greater<Timer>> timers_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::vector<Msg> msgs_;
+  std::string worker_error_;
+  std::vector<std::unique_ptr<Reader>> readers_;
+  std::vector<dp_nic*> nics_;
+  std::vector<std::int64_t> reader_bytes_;
+  // gpu backend
+  std::vector<int> devs_;
+  std::vector<dp_store*> stores_;
+  std::vector<dp_stager*> stagers_;
+  std::vector<dp_pool*> pools_;
+  std::vector<std::vector<dp_pool*>> views_;
+  std::vector<cudaStream_t> streams_;
+  std::int32_t* tab_slot_h_ = nullptr;
+  std::int64_t* tab_fb_h_ = nullptr;
+  LiveReport rep_;
+};
+
+}  // namespace
+
+LiveReport run_live(const pdsim::ClusterConfig& cfg, std::span<const pdsim::Trajectory> trajectories,
+                    const LiveOptions& options) {
+  Live live(cfg, trajectories, options);
+  return live.run();
+}
+
+}  // namespace dualpath

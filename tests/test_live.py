@@ -1,0 +1,125 @@
+"""Live-mode scheduling (include/dualpath/live.hpp): the
+reference's scheduler glue driven by measured completions.  Every scheduler
+invocation's inputs and outputs are logged; each is replayed through the
+REFERENCE's own functions (oracle/_ref: schedule_de_groups,
+schedule_de_within_group, schedule_pe_fetch, select_read_path) and must agree
+bit for bit.  Host tests use the timed backend (transfers sleep bytes /
+rate); the GPU tests move the bytes with K1 / K2 and check the final pools
+against the content oracle."""
+
+import numpy as np
+import pytest
+
+import paper_2602_21548_b200 as dp
+from oracle import refpy
+
+needs_ref = pytest.mark.skipif(not refpy.ref_available(), reason="oracle/_ref not built")
+
+
+def cluster(P, D, L=4, b=576, T=64, hbm=100_000_000):
+    cfg = dp.ClusterConfig()
+    cfg.prefill_nodes, cfg.decode_nodes, cfg.engines_per_node = P, D, 1
+    cfg.n_layer, cfg.kv_bytes_per_token_per_layer, cfg.block_size_tokens = L, b, T
+    cfg.hbm_capacity_tokens = hbm
+    return cfg
+
+
+def replay(rep, alpha, beta, z=1.05):
+    """Every logged invocation through the reference's function."""
+    n = 0
+    for inv in rep["invocations"]:
+        fn = inv["fn"]
+        q = [tuple(x) for x in inv["queue"]]
+        snaps = [(s[0], s[1], s[3], s[4], s[5], s[6]) for s in inv["snapshots"]]
+        got = [tuple(x) for x in inv["out"]]
+        if fn == "schedule_de_groups":
+            want = refpy.ref_schedule_de_groups(q, [tuple(g) for g in inv["groups"]])
+            assert [(r, g) for r, g, _ in got] == want, inv
+        elif fn == "schedule_de_within_group":
+            assert got == refpy.ref_schedule("ref_schedule_de_within_group", q, snaps, alpha, beta, z), inv
+        elif fn == "schedule_pe_fetch":
+            assert got == refpy.ref_schedule("ref_schedule_pe_fetch", q, snaps, alpha, beta, z), inv
+        elif fn == "select_read_path":
+            assert inv["path"] == refpy.ref().ref_select_read_path(inv["pe_read_q"], inv["de_read_q"]), inv
+        else:
+            raise AssertionError(fn)
+        n += 1
+    return n
+
+
+def check_lifecycle(rep, trajs):
+    reqs = rep["requests"]
+    assert len(reqs) == sum(len(t.rounds) for t in trajs)
+    assert len(rep["decisions"]) == len(reqs)
+    by_traj = {}
+    for r in reqs:
+        rid, traj, rnd, C, A, G, pe, de, path, reader, t_arr, t_sched, t_admit, t_read, t_land, t_done = r
+        assert 0 <= t_arr <= t_sched <= t_admit <= t_read <= t_land <= t_done
+        assert reader == (pe if path == 0 else de)
+        by_traj.setdefault(traj, []).append((rnd, t_arr, t_done))
+    for turns in by_traj.values():  # a session's next turn arrives after the previous completes
+        turns.sort()
+        for (r0, _, done), (r1, arr, _) in zip(turns, turns[1:]):
+            assert r1 == r0 + 1 and arr >= done
+
+
+@needs_ref
+@pytest.mark.parametrize("P,D,policy,mode,cap,slots", [
+    (1, 1, "dual_path", "adaptive", 2e9, 0),
+    (2, 2, "dual_path", "adaptive", 1e9, 0),
+    (1, 3, "dual_path", "adaptive", 4e9, 0),
+    (2, 2, "pe_only", "adaptive", 1e9, 0),
+    (2, 2, "dual_path", "round_robin", 1e9, 0),
+    (2, 2, "dual_path", "adaptive", 1e9, "tight"),
+])
+def test_live_invocations_replay_through_the_reference(P, D, policy, mode, cap, slots):
+    trajs = dp.synthesize(max_len=16000, count=4 * (P + D), seed=11, mean_turns=5, sigma_turns=0)
+    cfg = cluster(P, D, hbm=60_000)  # DE HBM bound: phase 2 leaves requests queued
+    ex = dp.ExecOptions()
+    ex.storage_cap_Bps = cap
+    big = max(-(-dp.context_before(t, len(t.rounds) - 1) // 64) for t in trajs)
+    rep = dp.run_live(cfg, trajs, policy=policy, sched_mode=mode, alpha=20000, beta=60000, exec=ex,
+                      gpu=False, link_Bps=8e9, decode_s_per_token=2e-6,
+                      pe_pool_slots=big if slots == "tight" else 0)
+    check_lifecycle(rep, trajs)
+    n = replay(rep, 20000, 60000)
+    assert n >= len(rep["decisions"]) if mode == "adaptive" else n == 0
+    if policy == "pe_only":
+        assert all(d[4] == 0 for d in rep["decisions"])
+    if policy == "dual_path" and mode == "adaptive" and P == 2:
+        assert any(d[4] == 1 for d in rep["decisions"])   # both read paths used
+    if slots == "tight":
+        assert rep["admission_stalls"] > 0                 # the bounded pool made requests wait
+    assert sum(rep["reader_bytes"]) == sum(r[3] for r in rep["requests"]) * cfg.kv_bytes_per_token()
+
+
+def test_live_rejects_a_pool_smaller_than_a_request():
+    trajs = dp.synthesize(max_len=16000, count=2, seed=1, mean_turns=4, sigma_turns=0)
+    with pytest.raises(dp.ConfigError):
+        dp.run_live(cluster(1, 1), trajs, gpu=False, pe_pool_slots=1)
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("k1,k2,tight", [(0, 0, False), (3, 2, True)])
+def test_live_gpu_moves_the_bytes(de_dev, k1, k2, tight):
+    """1P1D live on the GPU: K1 / K2 (or staged) move every request's hit KV
+    into the PE pool; the final occupant of every slot matches the oracle's
+    content and the invocations replay through the reference."""
+    trajs = dp.synthesize(max_len=12000, count=6, seed=4, mean_turns=5, sigma_turns=0)
+    cfg = cluster(1, 1)
+    ex = dp.ExecOptions()
+    ex.seed = 9
+    ex.storage_cap_Bps = 4e9
+    ex.k1_mode, ex.k2_mode = k1, k2
+    big = max(-(-dp.context_before(t, len(t.rounds) - 1) // 64) for t in trajs)
+    rep = dp.run_live(cfg, trajs, exec=ex, devices=[0, de_dev], pe_pool_slots=big + 4 if tight else 0,
+                      alpha=20000, beta=60000)
+    check_lifecycle(rep, trajs)
+    replay(rep, 20000, 60000)
+    assert rep["reader_bytes"][1] > 0
+    g = refpy.geom(cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer)
+    assert rep["final_slots"]
+    for pe, slot, fb, ntok, h0, h1 in rep["final_slots"]:
+        assert h0 == refpy.layer_block_hash(g, 9, fb, 0, ntok)
+        assert h1 == refpy.layer_block_hash(g, 9, fb, cfg.n_layer - 1, ntok)

@@ -13,6 +13,10 @@ Single process, two GPUs (PE = cuda:0, DE = cuda:1):
    compute stream, the maybe_start_compute gate, proj/src/desim.cpp:623-628);
    compare with load-then-compute.
 
+r02: the staged loaders (copy engine into an HBM ring + a scatter kernel of
+8 / 32 CTAs) on both sides, and the DE's own compute (a GEMM on the DE)
+while it pushes with K2 on SMs or staged.
+
 Prints one JSON object.  GEMMs use torch.matmul (cuBLAS) — a stand-in for
 the model's prefill compute, not part of the product path.
 """
@@ -46,14 +50,14 @@ def make_jobs(device, n_jobs, blocks, n_fb, n_slots, rng, layers=(0, L), ticket0
     return abi.make_jobs(specs), keep
 
 
-def gemm_times(a, b, n, stream):
+def gemm_times(a, b, n, stream, dev=0):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
     with torch.cuda.stream(stream):
         for e0, e1 in ev:
             e0.record(stream)
             torch.matmul(a, b)
             e1.record(stream)
-    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(dev)
     return [e0.elapsed_time(e1) for e0, e1 in ev]
 
 
@@ -62,6 +66,8 @@ def main():
     ap.add_argument("--m", type=int, default=8192)
     ap.add_argument("--k", type=int, default=4096)
     ap.add_argument("--gemms", type=int, default=6000)
+    ap.add_argument("--only-staged", action="store_true", help="only the staged-loader cases")
+    ap.add_argument("--skip-layerwise", action="store_true")
     a = ap.parse_args()
     assert torch.cuda.device_count() >= 2, "needs 2 GPUs"
     g = abi.geom(L, T, B)
@@ -82,19 +88,37 @@ def main():
         ce_keep += [fbs, sl]
         ce_specs.append((fbs.ctypes.data, sl.ctypes.data, blocks * T, blocks, 0, L, j))
     jobs_ce = abi.make_jobs(ce_specs)
+    # staged (copy engine into an HBM ring + scatter kernel): host src_fb, device slots
+    st_keep, st1, st2 = [], [], []
+    for j in range(n_jobs):
+        fbs = np.arange(j * blocks, (j + 1) * blocks, dtype=np.int64) % n_fb
+        s0 = torch.tensor(np.arange(j * blocks, (j + 1) * blocks, dtype=np.int32) % n_slots, device="cuda:0")
+        s1 = torch.tensor(np.arange(j * blocks, (j + 1) * blocks, dtype=np.int32) % n_slots, device="cuda:1")
+        st_keep += [fbs, s0, s1]
+        st1.append((fbs.ctypes.data, s0.data_ptr(), blocks * T, blocks, 0, L, j))
+        st2.append((fbs.ctypes.data, s1.data_ptr(), blocks * T, blocks, 0, L, n_jobs + j))
+    jobs_st1, jobs_st2 = abi.make_jobs(st1), abi.make_jobs(st2)
+    stager0, stager1 = abi.Stager(0, g), abi.Stager(1, g)
     s_gemm = torch.cuda.Stream(device=0, priority=-1)  # high priority compute
     s_k1 = torch.cuda.Stream(device=0, priority=0)
     s_k2 = torch.cuda.Stream(device=1)
     x = torch.randn(a.m, a.k, device="cuda:0", dtype=torch.bfloat16)
     w = torch.randn(a.k, a.m, device="cuda:0", dtype=torch.bfloat16)
+    s_gemm_de = torch.cuda.Stream(device=1, priority=-1)
+    x1 = torch.randn(a.m, a.k, device="cuda:1", dtype=torch.bfloat16)
+    w1 = torch.randn(a.k, a.m, device="cuda:1", dtype=torch.bfloat16)
     for _ in range(20):
         torch.matmul(x, w)
+        torch.matmul(x1, w1)
     torch.cuda.synchronize(0)
+    torch.cuda.synchronize(1)
     flops = 2.0 * a.m * a.m * a.k
 
-    def run_with(k1=False, k2=False, ctas=0, ce=False):
+    def run_with(k1=False, k2=False, ctas=0, ce=False, staged=False, stage_ctas=32, on_de=False):
         for dev in (0, 1):
             abi.set_gather_ctas(dev, ctas)
+        stager0.set_ctas(stage_ctas)
+        stager1.set_ctas(stage_ctas)
         stop = threading.Event()
         done = {"k1": [], "k2": []}  # completion wall times of each loader launch
         per_launch = n_jobs * blocks * T * B * L
@@ -103,7 +127,11 @@ def main():
             dev, stream = (0, s_k1) if kind == "k1" else (1, s_k2)
             with torch.cuda.device(dev):
                 while not stop.is_set():
-                    if kind == "k1" and ce:
+                    if staged and kind == "k1":
+                        abi.h2d_layer_staged(pool, st_pe, stager0, jobs_st1, n_jobs, stream.cuda_stream)
+                    elif staged:
+                        abi.h2d_push_staged(view, st_de, stager1, jobs_st2, n_jobs, stream.cuda_stream)
+                    elif kind == "k1" and ce:
                         abi.h2d_layer_copy(pool, st_pe, jobs_ce, n_jobs, stream.cuda_stream)
                     elif kind == "k1":
                         abi.h2d_layer_gather(pool, st_pe, jobs_k1, n_jobs, stream.cuda_stream)
@@ -116,7 +144,11 @@ def main():
             t.start()
         time.sleep(0.5)
         t0 = time.time()
-        ts = gemm_times(x, w, a.gemms, s_gemm)
+        if on_de:  # the DE's own compute (its decode stand-in) while it pushes
+            with torch.cuda.device(1):
+                ts = gemm_times(x1, w1, a.gemms, s_gemm_de, dev=1)
+        else:
+            ts = gemm_times(x, w, a.gemms, s_gemm)
         t1 = time.time()
         stop.set()
         for t in ths:
@@ -134,12 +166,34 @@ def main():
     out = {"gemm": {"m": a.m, "n": a.m, "k": a.k, "dtype": "bf16"}}
     out["alone"] = run_with()
     base = out["alone"]["gemm_ms"]
-    cases = [("k2_push", dict(k2=True)), ("k1_default", dict(k1=True)),
+    out["de_alone"] = run_with(on_de=True)
+    base_de = out["de_alone"]["gemm_ms"]
+    for name, kw in [("de_k2_sm", dict(k2=True)), ("de_k2_staged", dict(k2=True, staged=True)),
+                     ("de_k2_staged_8ctas", dict(k2=True, staged=True, stage_ctas=8)),
+                     ("de_k2_copy_engine", dict(k2=True, ce=True))]:
+        if kw.get("ce"):
+            continue  # the DE copy-engine push needs host tables (dp_h2d_push_copy): see r01
+        r = run_with(on_de=True, **kw)
+        r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base_de - 1.0), 2)
+        out[name] = r
+    if a.only_staged:
+        cases = [("k1_staged", dict(k1=True, staged=True)), ("k1_staged_8ctas", dict(k1=True, staged=True, stage_ctas=8)),
+                 ("k2_staged", dict(k2=True, staged=True)),
+                 ("k1_staged+k2_staged", dict(k1=True, k2=True, staged=True)),
+                 ("k1_staged_8ctas+k2_staged_8ctas", dict(k1=True, k2=True, staged=True, stage_ctas=8))]
+    else:
+        cases = [("k1_staged", dict(k1=True, staged=True)), ("k1_staged_8ctas", dict(k1=True, staged=True, stage_ctas=8)),
+                 ("k2_staged", dict(k2=True, staged=True)),
+                 ("k1_staged+k2_staged", dict(k1=True, k2=True, staged=True)),
+                 ("k1_staged_8ctas+k2_staged_8ctas", dict(k1=True, k2=True, staged=True, stage_ctas=8))] + [("k2_push", dict(k2=True)), ("k1_default", dict(k1=True)),
              ("k1_148ctas", dict(k1=True, ctas=148)), ("k1_32ctas", dict(k1=True, ctas=32)),
              ("k1_8ctas", dict(k1=True, ctas=8)), ("k1_32ctas+k2", dict(k1=True, k2=True, ctas=32)),
              ("k1_default+k2", dict(k1=True, k2=True)),
              ("k1_copy_engine", dict(k1=True, ce=True)),
              ("k1_copy_engine+k2", dict(k1=True, k2=True, ce=True))]
+    if a.skip_layerwise:
+        print(json.dumps(out))
+        return
     for name, kw in cases:
         r = run_with(**kw)
         r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base - 1.0), 2)
