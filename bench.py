@@ -83,6 +83,7 @@ def parse():
     ap.add_argument("--persist", action="store_true",
                     help="also persist generated tokens (decode stand-in + K4 D2H), implies --handoff")
     ap.add_argument("--handoff-ctas", type=int, default=0, help="K3 CTA cap on PEs (0 = default)")
+    ap.add_argument("--k3-tma", action="store_true", help="K3's hit push through the TMA (bulk copies)")
     ap.add_argument("--no-layerwise", action="store_true",
                     help="handoff + prefill: K3 after a request's last forward instead of layer by layer")
     ap.add_argument("--gather-ctas", type=int, default=-1, help="K1/K2 CTA cap (-1 = auto)")
@@ -486,6 +487,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     opt.persist = bool(args.persist)
     opt.handoff_ctas = args.handoff_ctas
     opt.handoff_layerwise = not args.no_layerwise
+    opt.handoff_tma = args.k3_tma
     opt.gather_ctas = args.gather_ctas
     opt.seed = 9
     if args.tier:

@@ -72,6 +72,7 @@ struct ExecOptions {
   // layer in-kernel
   std::int32_t k3_layer_gate = 0;
   std::int32_t handoff_ctas = 0;       // K3 CTA cap on PEs (0 = default)
+  bool handoff_tma = false;            // K3's hit push through the TMA (dp_set_handoff_tma)
   // handoff + prefill: K3 pushes layer l of a request as soon as the forward
   // that finishes it has computed layer l (the reference starts PeToDe /
   // MissMerge of layer l at LayerCompute l's completion, desim.cpp:630-640,

@@ -334,6 +334,9 @@ int dp_set_gather_ctas(int device, int32_t ctas);
 /* Cap on the CTAs of a K3 (dp_prefill_handoff) launch on `device` (0 =
  * default, 2 per SM: 699 GB/s of NVLink pushes, profiles/r01_SUMMARY.md). */
 int dp_set_handoff_ctas(int device, int32_t ctas);
+/* K3's PE-path hit push through the TMA (cp.async.bulk HBM -> shared -> peer
+ * HBM, 4 x 16 KB stages per CTA) instead of 16-byte register copies; process-wide. */
+int dp_set_handoff_tma(int32_t on);
 
 /* Items (landed-counter increments) per layer for a job of n_blk blocks. */
 int dp_layer_items(const dp_kv_geom* geom, int32_t n_blk, int32_t* out);

@@ -137,6 +137,7 @@ def lib():
         "dp_device_count": ([], ctypes.c_int),
         "dp_set_gather_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
         "dp_set_handoff_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
+        "dp_set_handoff_tma": ([ctypes.c_int32], ctypes.c_int),
         "dp_prefill_attend": ([P, ctypes.c_int32, ctypes.POINTER(AttendItem), ctypes.c_int32,
                                ctypes.c_uint64, P], ctypes.c_int),
         "dp_set_attend_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
@@ -382,6 +383,10 @@ def wait_status(pool):
 
 def set_gather_ctas(device, ctas):
     check(lib().dp_set_gather_ctas(device, ctas))
+
+
+def set_handoff_tma(on):
+    check(lib().dp_set_handoff_tma(1 if on else 0))
 
 
 def set_handoff_ctas(device, ctas):

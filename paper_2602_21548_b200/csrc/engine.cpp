@@ -151,6 +151,7 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   std::int32_t ctas = x.opt.gather_ctas;
   if (ctas < 0) ctas = !is_pe() ? 0 : x.prefill ? 32 : x.handoff ? 64 : 0;
   check(dp_set_gather_ctas(device_, ctas), "dp_set_gather_ctas");
+  if (is_pe() && x.handoff) check(dp_set_handoff_tma(x.opt.handoff_tma ? 1 : 0), "dp_set_handoff_tma");
   // layerwise K3 CTAs wait in-kernel for the forward's layers: a few suffice
   // and leave the SMs to the prefill compute
   if (is_pe())

@@ -281,6 +281,7 @@ constexpr int kMaxDevices = 64;
 // per-device CTA caps (0 = default); set by one thread, read by launching ones
 std::atomic<int> g_gather_ctas[kMaxDevices] = {};
 std::atomic<int> g_handoff_ctas[kMaxDevices] = {};
+std::atomic<bool> g_handoff_tma{false};  // K3 hit push through the TMA (dp_set_handoff_tma)
 
 int sm_count(int device) {
   int n = 0;
@@ -910,6 +911,11 @@ int dp_set_handoff_ctas(int device, int32_t ctas) {
   return DP_OK;
 }
 
+int dp_set_handoff_tma(int32_t on) {
+  g_handoff_tma = on != 0;
+  return DP_OK;
+}
+
 int dp_set_gather_ctas(int device, int32_t ctas) {
   if (device < 0 || device >= kMaxDevices || ctas < 0)
     return fail(DP_EINVAL, "set_gather_ctas: bad argument");
@@ -1125,10 +1131,92 @@ __device__ __forceinline__ uint4 content_pair(uint64_t fb, uint64_t w, uint64_t 
 // so one system-scope fence covers up to kHandoffGroup * 36 KB of pushes.
 constexpr int kHandoffGroup = 4;
 
+// TMA bulk-copy helpers (sm_90+ async proxy): global -> shared completing on
+// an mbarrier, shared -> global in bulk groups.
+constexpr int kBulkStages = 4;
+constexpr int kBulkBytes = 16 * 1024;
+constexpr int kHandoffTmaSmem = kBulkStages * kBulkBytes;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// K3's hit push by one thread through the TMA: HBM -> shared -> peer HBM in
+// kBulkBytes pieces over kBulkStages buffers; returns once every store has
+// completed (the caller's system-scope release then publishes them).
+__device__ void tma_push(char* dst, const char* src, int64_t bytes, char* smem, uint64_t* bars, uint32_t& phases) {
+  const int64_t n = (bytes + kBulkBytes - 1) / kBulkBytes;
+  auto piece = [&](int64_t i) {
+    const int64_t left = bytes - i * kBulkBytes;
+    return static_cast<uint32_t>(left < kBulkBytes ? left : kBulkBytes);
+  };
+  for (int64_t i = 0; i <= n; ++i) {
+    if (i < n) {
+      const int st = static_cast<int>(i % kBulkStages);
+      // stores 0 .. i-2 are committed; the buffer's last reader, store
+      // i - stages, must be done: at most stages - 2 may still be reading
+      if (i >= kBulkStages) bulk_wait_read<kBulkStages - 2>();
+      bulk_load(smem + st * kBulkBytes, src + i * kBulkBytes, piece(i), &bars[st]);
+    }
+    if (i >= 1) {
+      const int64_t k = i - 1;
+      const int st = static_cast<int>(k % kBulkStages);
+      mbar_wait(&bars[st], (phases >> st) & 1u);
+      phases ^= 1u << st;
+      bulk_store(dst + k * kBulkBytes, smem + st * kBulkBytes, piece(k));
+    }
+  }
+  bulk_wait_all();
+}
+
+template <bool kTma>
 __global__ void __launch_bounds__(kThreads) kv_prefill_handoff(const __grid_constant__ HandoffParams p) {
   const int64_t total = p.item_begin[p.n_jobs];
   const int tid = threadIdx.x;
   const int64_t lb = p.lb_bytes;
+  extern __shared__ __align__(128) char tma_smem[];
+  __shared__ __align__(8) uint64_t tma_bars[kBulkStages];
+  uint32_t tma_phases = 0;  // thread 0's parity per stage
+  if (kTma) {
+    if (tid == 0) {
+      for (int st = 0; st < kBulkStages; ++st) mbar_init(&tma_bars[st]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
     const int j = decode_job(p, item);
     const dp_handoff_job& job = p.jobs[j];
@@ -1168,7 +1256,10 @@ __global__ void __launch_bounds__(kThreads) kv_prefill_handoff(const __grid_cons
       const int64_t de_off = layer * p.de_stride + static_cast<int64_t>(job.de_slot[blk]) * lb;
       // hit part: PeToDe pushes it, MissMerge leaves it to the DE
       const int64_t h1 = min(end, hit_end);
-      if (job.push_hit && h1 > beg) {
+      if (kTma && job.push_hit && h1 > beg) {
+        if (tid == 0) tma_push(p.de_pool + de_off + beg, p.pe_pool + pe_off + beg, h1 - beg, tma_smem, tma_bars,
+                               tma_phases);
+      } else if (job.push_hit && h1 > beg) {
         const uint4* src = reinterpret_cast<const uint4*>(p.pe_pool + pe_off + beg);
         uint4* dst = reinterpret_cast<uint4*>(p.de_pool + de_off + beg);
         const int n16 = static_cast<int>((h1 - beg) >> 4);
@@ -1331,7 +1422,11 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
     }
     p.item_begin[p.n_jobs] = items;
     if (items == 0) continue;
-    kv_prefill_handoff<<<static_cast<int>(std::min<int64_t>(items, grid_cap)), kThreads, 0, s>>>(p);
+    const int grid = static_cast<int>(std::min<int64_t>(items, grid_cap));
+    if (g_handoff_tma.load())
+      kv_prefill_handoff<true><<<grid, kThreads, kHandoffTmaSmem, s>>>(p);
+    else
+      kv_prefill_handoff<false><<<grid, kThreads, 0, s>>>(p);
     DP_CUDA(cudaGetLastError());
   }
   return DP_OK;
@@ -1950,10 +2045,16 @@ int preload_kernels(int device) {
                          reinterpret_cast<const void*>(kv_block_checksum),
                          reinterpret_cast<const void*>(kv_store_fill),
                          reinterpret_cast<const void*>(kv_gather_dual),
-                         reinterpret_cast<const void*>(kv_prefill_handoff),
+                         reinterpret_cast<const void*>(kv_prefill_handoff<false>),
+                         reinterpret_cast<const void*>(kv_prefill_handoff<true>),
                          reinterpret_cast<const void*>(kv_decode_fill),
                          reinterpret_cast<const void*>(kv_persist_d2h),
                          reinterpret_cast<const void*>(kv_prefill_attend)};
+    if (cudaFuncSetAttribute(kv_prefill_handoff<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kHandoffTmaSmem) != cudaSuccess) {
+      g_preload_rc[device] = fail(DP_ECUDA, "preload_kernels: K3 TMA shared memory");
+      return;
+    }
     for (const void* f : fns) {
       cudaFuncAttributes a;
       if (cudaFuncGetAttributes(&a, f) != cudaSuccess) {

@@ -110,9 +110,12 @@ def test_de_path_dual_then_missmerge(de_dev, L, T, b, C, A):
 @pytest.mark.parametrize("L,T,b,C,A", [(8, 64, 576, 64 * 7 + 33, 429), (8, 64, 576, 64 * 2, 1),
                                        (8, 64, 576, 0, 64 * 3 + 5), (61, 64, 576, 64 * 6 + 1, 429),
                                        (64, 64, 4096, 64 * 3 + 40, 90)])
-def test_pe_path_load_then_petode(de_dev, L, T, b, C, A):
+@pytest.mark.parametrize("tma", [False, True])
+def test_pe_path_load_then_petode(de_dev, L, T, b, C, A, tma):
     """PE read path: K1 loads the hit KV into the PE pool; K3 (stream-ordered
-    after it) writes the miss KV and pushes the whole prompt (PeToDe)."""
+    after it) writes the miss KV and pushes the whole prompt (PeToDe) --
+    the hit part by 16-byte register copies or through the TMA."""
+    abi.set_handoff_tma(tma)
     g = abi.geom(L, T, b)
     P = C + A
     n_hit, n_prompt = -(-C // T), -(-P // T)
@@ -136,10 +139,11 @@ def test_pe_path_load_then_petode(de_dev, L, T, b, C, A):
         gr = refpy.geom(L, T, b)
         check_prompt(pe_pool, gr, fbs, pe_slots, P, T, b, L)
         check_prompt(de_pool, gr, fbs, de_slots, P, T, b, L)
-        abi.wait_layer(de_pool, 0, L, n_prompt * L, timeout_ms=2000)
+        abi.wait_layer(de_pool, 0, L, n_prompt * abi.layer_items(g, 1) * L, timeout_ms=2000)
         sync_all()
         assert abi.wait_status(de_pool) == abi.DP_OK
     finally:
+        abi.set_handoff_tma(False)
         for x in (de_view, de_pool, pe_pool, st_pe):
             x.close()
 

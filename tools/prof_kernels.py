@@ -152,11 +152,33 @@ def k4(a, g, L, T, b, n_fb, n_slots):
         target.close()
 
 
+def ce_peer():
+    """cudaMemcpyPeerAsync of 1 GiB device 0 -> device 1, best of 5: the copy
+    engine's NVLink rate, the practical ceiling K3 is compared with."""
+    n = 1 << 30
+    a = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    b = torch.empty(n, dtype=torch.uint8, device="cuda:1")
+    s = torch.cuda.Stream(device=0)
+    best = 1e9
+    for _ in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            b.copy_(a, non_blocking=True)
+            e1.record(s)
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return {"bytes": n, "ms": best, "GBps": n / best / 1e6}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--k2", action="store_true")
     ap.add_argument("--k3", action="store_true")
     ap.add_argument("--k3-ctas", default="0")
+    ap.add_argument("--k3-tma", default="off", choices=["off", "on", "both"])
+    ap.add_argument("--peer", action="store_true", help="also the copy-engine peer copy of 1 GiB (0 -> 1)")
     ap.add_argument("--k4", action="store_true")
     ap.add_argument("--jobs", type=int, default=64)
     ap.add_argument("--blocks", type=int, default=128)  # 8K-token requests
@@ -177,10 +199,16 @@ def main():
     for dev in range(torch.cuda.device_count()):
         abi.set_gather_ctas(dev, 0)
     if a.k3:
-        for ctas in [int(x) for x in a.k3_ctas.split(",")]:
-            abi.set_handoff_ctas(0, ctas)
-            out["k3" if ctas == 0 else f"k3@{ctas}"] = k3(a, g, L, T, b, n_fb, n_slots)
+        for tma in ([False, True] if a.k3_tma == "both" else [a.k3_tma == "on"]):
+            abi.set_handoff_tma(tma)
+            for ctas in [int(x) for x in a.k3_ctas.split(",")]:
+                abi.set_handoff_ctas(0, ctas)
+                key = ("k3_tma" if tma else "k3") + ("" if ctas == 0 else f"@{ctas}")
+                out[key] = k3(a, g, L, T, b, n_fb, n_slots)
         abi.set_handoff_ctas(0, 0)
+        abi.set_handoff_tma(False)
+    if a.peer:
+        out["ce_peer_copy"] = ce_peer()
     if a.k4:
         out["k4"] = k4(a, g, L, T, b, n_fb, n_slots)
     print(json.dumps(out))
