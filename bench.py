@@ -909,6 +909,8 @@ def traffic_for(launch_bytes, mode):
         t = json.load(f)
     if t.get("launch_bytes") != launch_bytes:
         return None, None
+    if t.get("scatter_kernel"):  # staged: the copy engine carries the bytes; the kernel only scatters
+        return t["dram_bytes"], dict(t["scatter_kernel"], note=t["source"])
     return t["dram_bytes"], t["source"]
 
 
