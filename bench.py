@@ -108,6 +108,8 @@ def parse():
                          "hybrid = both at once, jobs split by bytes, staged = copy engine into an HBM "
                          "ring + scatter kernel")
     ap.add_argument("--stage-ctas", type=int, default=32, help="staged modes: scatter kernel CTAs")
+    ap.add_argument("--stage-scatter", default="kernel", choices=["kernel", "ce"],
+                    help="staged modes: ring -> pool scatter by a kernel or by the copy engine (no SMs)")
     return ap.parse_args()
 
 
@@ -174,6 +176,7 @@ def config_dict(kind, sessions, P, D, policy, shape, cap_gbps, stats, extra=None
     cfg = {"workload": f"{kind}: {sessions} sessions, {P}P{D}D {policy}"
                        + (" (1 PE loader, K1)" if P + D == 2 and policy == "pe_only" else ""),
            "sessions": sessions, "kv": shape, "storage_cap_gbps_per_engine": cap_gbps or None,
+           "host_buffer_bytes_per_engine": buffer_bytes(shape),
            "requests": req, "hit_bytes_per_step": hit, "prompt_tokens_per_step": prompt,
            "l2": "inputs >> L2 (hundreds of GB per step; no flush needed)"}
     if extra:
@@ -181,9 +184,17 @@ def config_dict(kind, sessions, P, D, policy, shape, cap_gbps, stats, extra=None
     return cfg
 
 
+def buffer_bytes(shape):
+    """Host staging per engine (pe_buffer_bytes = de_buffer_bytes): the paper's
+    DRAM allocation per 8-GPU node (80 GB for DeepSeek, 320 GB for Qwen 32B,
+    PAPER.md:862-863) shared by its 8 engines.  The planner's admissions and
+    the executor's reads (BufferGate) both honour it."""
+    return int((320e9 if shape["b"] >= 4096 else 80e9) / 8)
+
+
 def golden_key(kind, sessions, P, D, policy, cap_gbps, link_bps):
     link = "cap%g" % cap_gbps if cap_gbps else "link%g" % (link_bps / 1e9)
-    return f"{kind}_{sessions}s_{P}p{D}d_{policy}_{link}"
+    return f"{kind}_{sessions}s_{P}p{D}d_{policy}_{link}_buf"
 
 
 def golden_check(key, digest):
@@ -210,8 +221,7 @@ def cluster(shape, P, D, cap_bps, caps=None, link_bps=PCIE_ZC_BPS):
     cfg.storage_multiple = (cap_bps if cap_bps > 0 else link_bps) / NVLINK_BPS
     cfg.dram_bandwidth = 2e12
     cfg.hbm_capacity_tokens = 100_000_000
-    cfg.pe_buffer_bytes = 1 << 42
-    cfg.de_buffer_bytes = 1 << 42
+    cfg.pe_buffer_bytes = cfg.de_buffer_bytes = buffer_bytes(shape)
     return cfg
 
 
@@ -482,6 +492,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     opt.k1_mode = {"sm": 0, "ce": 1, "hybrid": 2, "staged": 3}[args.k1]
     opt.k2_mode = {"sm": 0, "ce": 1, "staged": 2}[args.k2]
     opt.stage_ctas = args.stage_ctas
+    opt.stage_scatter = 1 if args.stage_scatter == "ce" else 0
     opt.wait_timeout_ms = args.wait_timeout_ms
     opt.handoff = bool(args.handoff or args.persist)
     opt.persist = bool(args.persist)
@@ -545,6 +556,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     dev_ms, host_ms, launches, read_bytes, spans, per_engine = [], [], 0, 0, None, None
     r0_bytes, r0_ms = 0, 0.0  # rank 0's own engine over the timed steps (the roofline)
     ttft, lag = [], []
+    stalls, bwait = 0, 0.0
     io_wait = 0.0
     d2h = 0
     for step in range(args.warmup + args.steps):
@@ -565,6 +577,8 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
             read_bytes += sum(dist.allgather(sum(r.bytes_read for r in res)))
             r0_bytes += res[0].bytes_read
             r0_ms += res[0].device_ms
+            stalls += sum(dist.allgather(sum(r.buffer_stalls for r in res)))
+            bwait = max(bwait, dist.max(max(r.buffer_wait_ms for r in res)))
             ttft, lag = list(res[0].ttft_ms), list(res[0].handoff_lag_ms)
             spans, per_engine = {}, {}
             for part in dist.allgather({e: (r.spans, r.device_ms) for e, r in zip(engines, res)}):
@@ -586,6 +600,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     snic = sum(u["total_bytes"] for u in planned["usage"] if u["kind"] == "snic_read")
     info = dict(plan_s=plan_s, hit_bytes=xp.hit_bytes, prompt_tokens=xp.prompt_tokens, digest=digest,
                 r0_bytes=r0_bytes, r0_ms=r0_ms, policy=policy, ttft_ms=ttft, lag_ms=lag,
+                buffer_stalls=stalls, buffer_wait_ms=bwait,
                 handoff_bytes=xp.handoff_bytes if (args.handoff or args.persist) else 0,
                 persist_bytes=xp.persist_bytes if args.persist else 0,
                 model_gbps=snic / planned["makespan"] / 1e9 if planned["makespan"] > 0 else None,
@@ -721,7 +736,7 @@ def reference_arm(args):
         link_bps = PCIE_ZC_BPS
         kv = dict(P=P, D=D, g=1, L=shape["L"], b=shape["b"], T=shape["T"], B=NVLINK_BPS,
                   s=(cap if cap > 0 else link_bps) / NVLINK_BPS, M=2e12, hbm=100_000_000,
-                  pe_buf=1 << 42, de_buf=1 << 42, policy=policy, **PLAN_KW)
+                  pe_buf=buffer_bytes(shape), de_buf=buffer_bytes(shape), policy=policy, **PLAN_KW)
         t0 = time.time()
         rep = refpy.ref_simulate(sim_path, **kv)
         sim_wall = time.time() - t0
@@ -988,11 +1003,7 @@ def main():
         achieved = info["r0_bytes"] / (info["r0_ms"] * 1e-3) / 1e9 if info["r0_ms"] > 0 else None
         traffic, traffic_src = traffic_for(k1_bytes, k1_mode)
         stats = (info["requests"], info["hit_bytes"], info["prompt_tokens"])
-        extra = {"k1": args.k1, "k2": args.k2}
-        if args.handoff_ctas:
-            extra["handoff_ctas"] = args.handoff_ctas
-        if args.pd:
-            extra["pd"] = args.pd
+        extra = {"pd": args.pd} if args.pd else None
         out = {
             "metric": "aggregate KV-load GB/s",
             "value": round(value, 3),
@@ -1009,6 +1020,11 @@ def main():
             "config": config_dict(args.workload, sessions, P, D, info["policy"] if args.online == 0 else
                                   "dual_path", shape, args.cap_gbps, stats, extra),
             "plan": plan_block(info, args.workload, sessions, P, D, args.cap_gbps, link_bps),
+            "loaders": {"k1": args.k1, "k2": args.k2, "stage_ctas": args.stage_ctas,
+                        "stage_scatter": args.stage_scatter,
+                        "handoff_ctas": args.handoff_ctas or None,
+                        "buffer_stalls": info["buffer_stalls"],
+                        "buffer_wait_ms": round(info["buffer_wait_ms"], 1)},
             "model_prediction_gbps": round(info["model_gbps"], 3) if info["model_gbps"] else None,
             "tokens_per_s": round(tokens_s, 1),
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",

@@ -36,6 +36,9 @@ namespace dualpath {
 
 struct ExecOptions {
   double storage_cap_Bps = 0;          // per-engine storage NIC; 0 = uncapped (PCIe binds)
+  // host staging bound of a reading engine (the plan's pe_buffer_bytes /
+  // de_buffer_bytes): true = enforce it (BufferGate) on the load paths
+  bool buffer_bound = true;
   std::vector<double> storage_cap_per_engine;  // overrides storage_cap_Bps per engine
   double pace_scale = 0;               // > 0: online replay, a job's storage read starts no
                                        // earlier than its planned t_admit * pace_scale
@@ -59,6 +62,8 @@ struct ExecOptions {
   std::int32_t k2_mode = 0;
   std::int64_t stage_ring_bytes = 1LL << 30;  // staged modes: HBM ring per engine
   std::int32_t stage_ctas = 32;               // staged modes: scatter CTAs
+  std::int32_t stage_scatter = 0;             // staged modes: 0 = scatter kernel, 1 = copy engine
+                                              // (DP_SCATTER_CE: no SM work at all)
   // PD handoff: every request's prompt KV also ends in its
   // DE's decode pool — prefill stand-in + PeToDe / MissMerge per layer (K3)
   // and the DE read path fused with DecodeH2D (dual store)
@@ -251,6 +256,8 @@ struct StepResult {
   // handoff (PE): per request, ms from the step start until its whole prompt
   // KV is in its DE's decode pool (the offline TTFT of the prefill path), and
   // the handoff lag: that time minus the end of the forward finishing it
+  std::int64_t buffer_stalls = 0;   // waits for the reader's host staging bound
+  double buffer_wait_ms = 0;
   std::vector<float> ttft_ms;
   std::vector<float> handoff_lag_ms;
   std::int64_t d2h_bytes = 0;   // result read back (PE: landed-counter column)
@@ -314,6 +321,8 @@ class EngineRuntime {
   dp_nic* nic_ = nullptr;                   // emulated storage NIC (rate cap)
   dp_stager* stager_ = nullptr;             // staged K1 / K2: HBM ring (k1_mode 3 / k2_mode 2)
   std::int64_t stager_launches() const;
+  const std::int32_t* stage_slots() const;
+  std::int64_t buffer_budget() const;
   dp_pool* pool_ = nullptr;                 // owned (PE only)
   std::vector<dp_pool*> peers_;             // per engine id: view of that PE's pool
   std::int64_t* d_src_ = nullptr;           // device block tables of this reader

@@ -321,6 +321,14 @@ int dp_stager_create(int device, const dp_kv_geom* geom, int64_t ring_bytes, dp_
 int dp_stager_destroy(dp_stager* stager);
 int dp_stager_set_ctas(dp_stager* stager, int32_t ctas);  /* scatter CTAs (0 = 32) */
 int dp_stager_launches(const dp_stager* stager, int64_t* n);  /* scatter kernels so far */
+/* The scatter ring -> pool: DP_SCATTER_KERNEL (default; kv_gather from the
+ * ring, dst_slot device-readable) or DP_SCATTER_CE (copy engines only: one 2D
+ * copy per run of consecutive slots per layer + fenced stream writes of the
+ * landed counters, absolute values as dp_h2d_layer_copy's; dst_slot
+ * HOST-readable; no SM work on either GPU). */
+#define DP_SCATTER_KERNEL 0
+#define DP_SCATTER_CE 1
+int dp_stager_set_mode(dp_stager* stager, int32_t mode);
 int dp_h2d_layer_staged(dp_pool* pe, const dp_store* src, dp_stager* stager, const dp_job* jobs,
                         int32_t n_jobs, dp_stream stream);
 int dp_h2d_push_staged(dp_pool* pe_view, const dp_store* de_src, dp_stager* stager, const dp_job* jobs,

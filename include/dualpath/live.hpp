@@ -49,6 +49,16 @@ struct LiveOptions {
   double link_Bps = 50e9;            // timed backend: per-reader transfer rate
   std::vector<int> devices;          // engine -> CUDA device (gpu backend; default engine % count)
   double timeout_s = 600;            // whole-run watchdog
+  // online (run_online, desim.cpp:1036-1051): session i's first turn arrives
+  // at arrival_times[i] seconds (empty: all at 0, offline)
+  std::vector<double> arrival_times;
+  // the reference's online stops, on MEASURED latencies: a turn's TTFT here is
+  // the load path's (arrival -> its hit KV landed in the PE pool); the run
+  // stops when one exceeds slo_ttft_s (> 0; desim.cpp:679-685) or when the
+  // TTFT series is steady (steady_window > 0: detect_steady_state every
+  // window / 2, desim.cpp:942-953)
+  double slo_ttft_s = 0;
+  double steady_window = 0, steady_lookback = 180, steady_threshold = 0.05;
 };
 
 // One scheduler function call, its inputs and result.
@@ -90,6 +100,9 @@ struct LiveReport {
   };
   std::vector<Occupant> final_slots;
   std::int64_t store_fb = 0, fb_stride = 0;  // content mapping fb = (traj * stride + k) % store_fb
+  bool slo_violated = false, steady_state = false;
+  std::size_t completed_requests = 0, total_requests = 0;
+  std::vector<std::pair<double, double>> ttft_series;  // (t, ttft) per landed turn
 };
 
 LiveReport run_live(const pdsim::ClusterConfig& cfg, std::span<const pdsim::Trajectory> trajectories,

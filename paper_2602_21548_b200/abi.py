@@ -126,6 +126,7 @@ def lib():
         "dp_stager_destroy": ([P], ctypes.c_int),
         "dp_stager_set_ctas": ([P, ctypes.c_int32], ctypes.c_int),
         "dp_stager_launches": ([P, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "dp_stager_set_mode": ([P, ctypes.c_int32], ctypes.c_int),
         "dp_h2d_layer_staged": ([P, P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_h2d_push_staged": ([P, P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_stream_wait_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
@@ -167,6 +168,7 @@ def geom(n_layer, block_tokens, b):
 
 
 NUMA_DEVICE, NUMA_NONE = -1, -2
+SCATTER_KERNEL, SCATTER_CE = 0, 1
 
 
 class Store:
@@ -286,6 +288,10 @@ class Stager:
 
     def set_ctas(self, n):
         check(lib().dp_stager_set_ctas(self.ptr, n))
+
+    def set_mode(self, mode):
+        """SCATTER_KERNEL (0) or SCATTER_CE (1: copy engines only; host slot tables)."""
+        check(lib().dp_stager_set_mode(self.ptr, mode))
 
     def launches(self):
         n = ctypes.c_int64()

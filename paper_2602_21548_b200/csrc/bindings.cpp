@@ -416,12 +416,14 @@ PYBIND11_MODULE(_core, m) {
   py::class_<dualpath::ExecOptions>(m, "ExecOptions")
       .def(py::init<>())
       .def_readwrite("storage_cap_Bps", &dualpath::ExecOptions::storage_cap_Bps)
+      .def_readwrite("buffer_bound", &dualpath::ExecOptions::buffer_bound)
       .def_readwrite("storage_cap_per_engine", &dualpath::ExecOptions::storage_cap_per_engine)
       .def_readwrite("pace_scale", &dualpath::ExecOptions::pace_scale)
       .def_readwrite("k1_mode", &dualpath::ExecOptions::k1_mode)
       .def_readwrite("k2_mode", &dualpath::ExecOptions::k2_mode)
       .def_readwrite("stage_ring_bytes", &dualpath::ExecOptions::stage_ring_bytes)
       .def_readwrite("stage_ctas", &dualpath::ExecOptions::stage_ctas)
+      .def_readwrite("stage_scatter", &dualpath::ExecOptions::stage_scatter)
       .def_readwrite("handoff", &dualpath::ExecOptions::handoff)
       .def_readwrite("de_pool_slots", &dualpath::ExecOptions::de_pool_slots)
       .def_readwrite("gather_ctas", &dualpath::ExecOptions::gather_ctas)
@@ -586,6 +588,8 @@ PYBIND11_MODULE(_core, m) {
       .def_readonly("io_wait_ms", &dualpath::StepResult::io_wait_ms)
       .def_readonly("d2h_bytes", &dualpath::StepResult::d2h_bytes)
       .def_readonly("ttft_ms", &dualpath::StepResult::ttft_ms)
+      .def_readonly("buffer_stalls", &dualpath::StepResult::buffer_stalls)
+      .def_readonly("buffer_wait_ms", &dualpath::StepResult::buffer_wait_ms)
       .def_readonly("handoff_lag_ms", &dualpath::StepResult::handoff_lag_ms);
 
   py::class_<dualpath::EngineRuntime>(m, "EngineRuntime")
@@ -623,8 +627,15 @@ PYBIND11_MODULE(_core, m) {
       [](const ClusterConfig& cfg, const std::vector<Trajectory>& trajs, const std::string& policy,
          const std::string& sched_mode, std::int64_t alpha, std::int64_t beta, double z,
          const dualpath::ExecOptions& exec, std::int32_t pe_pool_slots, double decode_s_per_token, bool gpu,
-         double link_Bps, const std::vector<int>& devices, double timeout_s) {
+         double link_Bps, const std::vector<int>& devices, double timeout_s,
+         const std::vector<double>& arrival_times, double slo_ttft, double steady_window,
+         double steady_lookback, double steady_threshold) {
         dualpath::LiveOptions o;
+        o.arrival_times = arrival_times;
+        o.slo_ttft_s = slo_ttft;
+        o.steady_window = steady_window;
+        o.steady_lookback = steady_lookback;
+        o.steady_threshold = steady_threshold;
         o.sim = make_options(policy, sched_mode, static_cast<double>(alpha), static_cast<double>(beta), 1);
         o.sim.sched.z_factor = z;
         o.exec = exec;
@@ -682,13 +693,20 @@ PYBIND11_MODULE(_core, m) {
         d["pool_slots"] = rep.pool_slots;
         d["store_fb"] = rep.store_fb;
         d["fb_stride"] = rep.fb_stride;
+        d["slo_violated"] = rep.slo_violated;
+        d["steady_state"] = rep.steady_state;
+        d["completed_requests"] = rep.completed_requests;
+        d["total_requests"] = rep.total_requests;
+        d["ttft_series"] = rep.ttft_series;
         return d;
       },
       py::arg("cfg"), py::arg("trajectories"), py::arg("policy") = "dual_path",
       py::arg("sched_mode") = "adaptive", py::arg("alpha") = 100000, py::arg("beta") = 500000,
       py::arg("z") = 1.05, py::arg("exec") = dualpath::ExecOptions{}, py::arg("pe_pool_slots") = 0,
       py::arg("decode_s_per_token") = 0.0, py::arg("gpu") = true, py::arg("link_Bps") = 50e9,
-      py::arg("devices") = std::vector<int>{}, py::arg("timeout_s") = 600.0);
+      py::arg("devices") = std::vector<int>{}, py::arg("timeout_s") = 600.0,
+      py::arg("arrival_times") = std::vector<double>{}, py::arg("slo_ttft") = 0.0,
+      py::arg("steady_window") = 0.0, py::arg("steady_lookback") = 180.0, py::arg("steady_threshold") = 0.05);
 
   m.def(
       "run_step_all",

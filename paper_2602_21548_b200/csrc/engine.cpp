@@ -129,6 +129,7 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   if (!x.by_reader[engine_].empty() && ((is_pe() && x.opt.k1_mode == 3) || (!is_pe() && x.opt.k2_mode == 2))) {
     check(dp_stager_create(device_, &x.geom, x.opt.stage_ring_bytes, &stager_), "dp_stager_create");
     check(dp_stager_set_ctas(stager_, x.opt.stage_ctas), "dp_stager_set_ctas");
+    check(dp_stager_set_mode(stager_, x.opt.stage_scatter), "dp_stager_set_mode");
   }
   if (x.handoff) {
     upload_handoff_tables();
@@ -390,6 +391,7 @@ StepResult EngineRuntime::run_step() {
   std::unique_ptr<TierReader> tier;
   if (x.tier && !mine.empty()) tier = std::make_unique<TierReader>(*this, mine);
 
+  detail::BufferGate buf(x.opt.buffer_bound && !hybrid ? buffer_budget() : 0);
   auto flush = [&]() {
     if (batch.empty()) return;
     dp_pool* dst = peers_[batch_pe];
@@ -416,6 +418,7 @@ StepResult EngineRuntime::run_step() {
       what = "dp_h2d_layer_gather";
     }
     check(rc, what);
+    buf.launched(s);
     const bool on_ce = batch_pe == engine_ ? (k1_ce || k1_st) : (k2_ce || k2_st);
     if (!on_ce)  // kernel launches (the copy engine paths have none; staged ones are counted below)
       res.launches += (static_cast<std::int64_t>(batch.size()) + DP_MAX_JOBS_PER_LAUNCH - 1) /
@@ -460,6 +463,7 @@ StepResult EngineRuntime::run_step() {
       if (hazard || j.fence) join_streams();
       else if (gated || batch_ce.size() == DP_MAX_JOBS_PER_LAUNCH) flush_ce();
     }
+    buf.reserve(bytes, flush);  // the reader's staging bound (may launch, then wait)
     if (gated) {
       // StorageRead of C*L*b bytes over this engine's storage NIC: starts
       // when the NIC is free (and, replaying online, not before the planned
@@ -493,9 +497,9 @@ StepResult EngineRuntime::run_step() {
       sm_bytes += static_cast<double>(bytes);
     }
     batch_pe = j.pe;
-    if (j.pe == engine_ ? k1_st : k2_st)  // staged: host-readable sources, device slots
-      batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0,
-                             x.cfg.n_layer, j.ticket});
+    if (j.pe == engine_ ? k1_st : k2_st)  // staged: host-readable sources; slots for the scatter
+      batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, stage_slots() + j.blk_off, j.cached, j.n_blk,
+                             0, x.cfg.n_layer, j.ticket});
     else if (j.pe == engine_ ? k1_ce : k2_ce)  // copy engine: host-readable block tables
       batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,
                              j.cached, j.n_blk, 0, x.cfg.n_layer, j.ticket});
@@ -516,6 +520,8 @@ StepResult EngineRuntime::run_step() {
     ++res.launches;
   }
   res.launches += stager_launches() - st_launch0;
+  res.buffer_stalls = buf.stalls();
+  res.buffer_wait_ms = buf.wait_ms();
   check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_end_), s), "cudaEventRecord");
   check_cuda(cudaEventSynchronize(static_cast<cudaEvent_t>(ev_end_)), "step sync");
   for (dp_pool* p : peers_)
@@ -528,6 +534,19 @@ StepResult EngineRuntime::run_step() {
   read_back_landed(res);
   res.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return res;
+}
+
+// This engine's host staging bound as a reader: its node's PE buffer when it
+// is a PE, the DE buffer otherwise (types.hpp:22-23).
+std::int64_t EngineRuntime::buffer_budget() const {
+  const ExecPlan& x = *plan_;
+  return is_pe() ? x.cfg.pe_buffer_bytes : x.cfg.de_buffer_bytes;
+}
+
+// The slot table the staged scatter reads: device memory for the kernel,
+// host memory for the copy-engine scatter.
+const std::int32_t* EngineRuntime::stage_slots() const {
+  return plan_->opt.stage_scatter == DP_SCATTER_CE ? plan_->slots[engine_].data() : d_slots_;
 }
 
 std::int64_t EngineRuntime::stager_launches() const {

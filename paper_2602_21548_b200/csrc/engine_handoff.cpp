@@ -136,6 +136,7 @@ StepResult EngineRuntime::run_step_handoff() {
           check(dp_h2d_layer_copy(pool_, store_, &job, 1, s), "dp_h2d_layer_copy");
         } else if (x.opt.k1_mode == 3 && stager_) {
           job.src_fb = x.src_fb[engine_].data() + j.blk_off;
+          job.dst_slot = stage_slots() + j.blk_off;
           const std::int64_t l0 = stager_launches();
           check(dp_h2d_layer_staged(pool_, store_, stager_, &job, 1, s), "dp_h2d_layer_staged");
           res.launches += stager_launches() - l0;

@@ -102,6 +102,7 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
     const std::int64_t st_launch0 = stager_launches();
     std::vector<dp_job> batch;
     std::vector<int> batch_jobs;  // by_reader positions (the storage tier's job ids)
+    detail::BufferGate buf(x.opt.buffer_bound ? buffer_budget() : 0);
     std::unique_ptr<TierReader> tier;
     if (x.tier && !x.by_reader[engine_].empty()) tier = std::make_unique<TierReader>(*this, x.by_reader[engine_]);
     int li = 0;  // by_reader position of the next own load
@@ -119,6 +120,7 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
       batch.clear();
       if (tier) tier->launched(batch_jobs, s);
       batch_jobs.clear();
+      buf.launched(s);
     };
     const double cap = x.opt.storage_cap_per_engine.empty() ? x.opt.storage_cap_Bps
                                                             : x.opt.storage_cap_per_engine[engine_];
@@ -148,6 +150,7 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
       }
       if (gated || !j.consumer_waits.empty()) forwards_before(r);
       if (gated || !j.consumer_waits.empty() || batch.size() == DP_MAX_JOBS_PER_LAUNCH) flush();
+      buf.reserve(bytes, flush);
       for (int w : j.consumer_waits)
         check_cuda(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[w]]), 0),
                    "cudaStreamWaitEvent");
@@ -158,8 +161,8 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
         batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, x.slots[engine_].data() + j.blk_off,
                                j.cached, j.n_blk, 0, L, j.ticket});
       else if (k1_st)
-        batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0,
-                               L, j.ticket});
+        batch.push_back(dp_job{x.src_fb[engine_].data() + j.blk_off, stage_slots() + j.blk_off, j.cached,
+                               j.n_blk, 0, L, j.ticket});
       else
         batch.push_back(dp_job{d_src_ + j.blk_off, d_slots_ + j.blk_off, j.cached, j.n_blk, 0, L, j.ticket});
       batch_jobs.push_back(pos);
@@ -168,6 +171,8 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
     }
     flush();
     res.launches += stager_launches() - st_launch0;
+    res.buffer_stalls = buf.stalls();
+    res.buffer_wait_ms = buf.wait_ms();
   }
   while (fi < fwds.size()) enqueue_forward(static_cast<int>(fi++), res);
   // the step ends when both streams are drained

@@ -1855,6 +1855,7 @@ struct dp_stager {
   int seg = 0;
   int32_t ctas = 32;         // scatter CTAs (HBM-bound: a few keep up with the link)
   int64_t launches = 0;      // scatter kernels launched so far
+  int32_t mode = 0;          // DP_SCATTER_KERNEL or DP_SCATTER_CE
 };
 
 namespace {
@@ -1897,23 +1898,63 @@ int staged_transfer(const char* who, dp_pool* pool, const dp_store* src, dp_stag
     for (int32_t k = 0; k < job.n_blk; ++k)
       if (job.src_fb[k] < 0 || job.src_fb[k] >= src->n_fb)
         return fail(DP_EINVAL, w + ": job " + std::to_string(j) + ": source block out of range");
+    if (st->mode == DP_SCATTER_CE)  // absolute counter writes: one job per ticket and call
+      for (int32_t i = 0; i < j; ++i)
+        if (job.ticket >= 0 && jobs[i].ticket == job.ticket)
+          return fail(DP_EINVAL, w + ": ticket used by two jobs of one call (copy-engine scatter)");
   }
   DeviceGuard guard(st->device);
   auto s = static_cast<cudaStream_t>(stream);
   std::vector<dp_job> sub;
   int64_t used = 0;     // Full Blocks of the open segment
   bool open = false;
+  std::vector<int64_t> sub_cum;  // CE mode: the job's items per layer landed after each sub-job
   auto flush = [&]() -> int {
     if (!open) return DP_OK;
     const int seg = st->seg;
     DP_CUDA(cudaEventRecord(st->ev_copied[seg], st->copy));
     DP_CUDA(cudaStreamWaitEvent(s, st->ev_copied[seg], 0));
-    if (!sub.empty()) {
+    if (!sub.empty() && st->mode == DP_SCATTER_CE) {
+      // the scatter on a copy engine too: per run of consecutive pool slots and
+      // layer one 2D copy ring (Full-Block pitch) -> layer plane (Layer-Block
+      // pitch), then fenced stream writes of the landed counters (absolute:
+      // the job's items landed so far, per layer and over all layers)
+      const int64_t plane = lb * pool->n_slots;
+      for (size_t q = 0; q < sub.size(); ++q) {
+        const dp_job& jb = sub[q];
+        const int64_t pos0 = jb.src_fb - st->iota;  // ring position of the sub-job's first block
+        const bool part = jb.n_tokens % T != 0;
+        const int32_t full = part ? jb.n_blk - 1 : jb.n_blk;
+        for (int32_t k = 0; k < jb.n_blk;) {
+          int32_t run = 1;
+          const bool pk = part && k == jb.n_blk - 1;
+          if (!pk)
+            while (k + run < full && jb.dst_slot[k + run] == jb.dst_slot[k] + run) ++run;
+          const int64_t width = pk ? (jb.n_tokens - static_cast<int64_t>(k) * T) * b : lb;
+          for (int32_t layer = 0; layer < g.n_layer; ++layer)
+            DP_CUDA(cudaMemcpy2DAsync(pool->base + layer * plane + static_cast<int64_t>(jb.dst_slot[k]) * lb, lb,
+                                      st->ring.host + (pos0 + k) * fbb + layer * lb, fbb, width, run,
+                                      cudaMemcpyDeviceToDevice, s));
+          k += run;
+        }
+        if (jb.ticket >= 0) {
+          const WriteValue32Fn wv = write_value32();
+          if (!wv) return fail(DP_ECUDA, w + ": cuStreamWriteValue32 unavailable");
+          uint32_t* row = pool->counters + static_cast<int64_t>(jb.ticket) * (g.n_layer + 1);
+          const uint32_t v = static_cast<uint32_t>(sub_cum[q]);
+          for (int32_t layer = 0; layer <= g.n_layer; ++layer)
+            if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + layer),
+                   layer == g.n_layer ? v * static_cast<uint32_t>(g.n_layer) : v, 0) != CUDA_SUCCESS)
+              return fail(DP_ECUDA, w + ": cuStreamWriteValue32 failed");
+        }
+      }
+    } else if (!sub.empty()) {
       if (int rc = launch_gather(pool, &st->ring, sub.data(), static_cast<int32_t>(sub.size()), stream, peer,
                                  st->ctas))
         return rc;
       ++st->launches;
     }
+    sub_cum.clear();
     DP_CUDA(cudaEventRecord(st->ev_free[seg], s));
     st->seg = (seg + 1) % kStageSegs;
     sub.clear();
@@ -1950,6 +1991,7 @@ int staged_transfer(const char* who, dp_pool* pool, const dp_store* src, dp_stag
       const int64_t tok0 = static_cast<int64_t>(k0) * T;
       sub.push_back(dp_job{st->iota + base, job.dst_slot + k0, std::min<int64_t>(job.n_tokens, k1 * T) - tok0,
                            k1 - k0, 0, g.n_layer, job.ticket});
+      sub_cum.push_back(static_cast<int64_t>(k1) * chunks_per_block(g));
       used += k1 - k0;
       k0 = k1;
     }
@@ -2007,6 +2049,12 @@ int dp_stager_destroy(dp_stager* st) {
 int dp_stager_launches(const dp_stager* st, int64_t* n) {
   if (!st || !n) return fail(DP_EINVAL, "stager_launches: null argument");
   *n = st->launches;
+  return DP_OK;
+}
+
+int dp_stager_set_mode(dp_stager* st, int32_t mode) {
+  if (!st || (mode != DP_SCATTER_KERNEL && mode != DP_SCATTER_CE)) return fail(DP_EINVAL, "stager_set_mode: bad argument");
+  st->mode = mode;
   return DP_OK;
 }
 

@@ -17,6 +17,7 @@
 #include <unordered_map>
 
 #include "engine_detail.hpp"
+#include "pdsim/metrics.hpp"
 
 namespace dualpath {
 namespace {
@@ -48,6 +49,7 @@ struct Reader {
   std::deque<std::pair<int, cudaEvent_t>> inflight;
   std::deque<double> inflight_done;  // timed backend: completion times
   bool stop = false;
+  bool worker_done = false;  // the completer drains in-flight transfers until then
   std::thread worker, completer;
 };
 
@@ -106,16 +108,29 @@ class Live {
     }
   }
 
-  ~Live() {
+  // Stop every reader: reads not yet started are dropped (a stopped online
+  // run), transfers already launched are waited for before the pools go.
+  void shutdown_readers() {
     for (auto& r : readers_) {
       {
         std::lock_guard<std::mutex> lk(r->mu);
+        r->jobs.clear();
         r->stop = true;
       }
       r->cv.notify_all();
       if (r->worker.joinable()) r->worker.join();
+      {
+        std::lock_guard<std::mutex> lk(r->mu);
+        r->worker_done = true;
+      }
+      r->cv.notify_all();
       if (r->completer.joinable()) r->completer.join();
     }
+    readers_.clear();
+  }
+
+  ~Live() {
+    shutdown_readers();
     for (dp_nic* n : nics_) dp_nic_destroy(n);
     for (dp_stager* s : stagers_) dp_stager_destroy(s);
     for (auto& row : views_)
@@ -144,10 +159,17 @@ class Live {
       rd->worker = std::thread([this, rd] { worker(rd); });
       rd->completer = std::thread([this, rd] { completer(rd); });
     }
-    for (std::size_t t = 0; t < trajs_.size(); ++t) arrive(static_cast<int>(t));
+    if (!o_.arrival_times.empty() && o_.arrival_times.size() != trajs_.size())
+      throw std::invalid_argument("run_live: one arrival time per trajectory");
+    for (std::size_t t = 0; t < trajs_.size(); ++t) {
+      const double at = o_.arrival_times.empty() ? 0.0 : o_.arrival_times[t];
+      if (at <= 0) arrive(static_cast<int>(t));
+      else timers_.push({at, -1 - static_cast<int>(t)});  // a session's first turn
+    }
+    if (o_.steady_window > 0) next_steady_ = o_.steady_window / 2;
     wake();
     auto last_progress = Clock::now();
-    while (completed_ < total_reqs_) {
+    while (completed_ < total_reqs_ && !stop_) {
       std::vector<Msg> msgs;
       {
         std::unique_lock<std::mutex> lk(mu_);
@@ -163,30 +185,33 @@ class Live {
       while (!timers_.empty() && timers_.top().first <= now()) {
         const int id = timers_.top().second;
         timers_.pop();
-        complete(id);
+        if (id < 0) arrive(-1 - id);  // online arrival of a session
+        else complete(id);
       }
+      if (next_steady_ > 0 && now() >= next_steady_ && !stop_) {  // on_steady_check (desim.cpp:942-953)
+        if (pdsim::detect_steady_state(rep_.ttft_series, o_.steady_window, o_.steady_lookback,
+                                       o_.steady_threshold)) {
+          rep_.steady_state = true;
+          stop_ = true;
+        }
+        next_steady_ = now() + o_.steady_window / 2;
+      }
+      if (stop_) break;
       wake();
       if (progress) last_progress = Clock::now();
       if (std::chrono::duration<double>(Clock::now() - last_progress).count() > o_.timeout_s)
         throw std::runtime_error("run_live: no progress for " + std::to_string(o_.timeout_s) + " s");
     }
     rep_.wall_s = now();
-    for (auto& r : readers_) {
-      {
-        std::lock_guard<std::mutex> lk(r->mu);
-        r->stop = true;
-      }
-      r->cv.notify_all();
-      r->worker.join();
-      r->completer.join();
-    }
-    readers_.clear();
-    if (o_.gpu) final_occupants();
+    shutdown_readers();
+    if (o_.gpu && !stop_) final_occupants();
     for (auto& q : reqs_) rep_.requests.push_back(q.r);
     rep_.reader_bytes = reader_bytes_;
     rep_.pool_slots = pool_slots_;
     rep_.store_fb = store_fb_;
     rep_.fb_stride = fb_stride_;
+    rep_.completed_requests = static_cast<std::size_t>(completed_);
+    rep_.total_requests = static_cast<std::size_t>(total_reqs_);
     return std::move(rep_);
   }
 
@@ -415,6 +440,12 @@ class Live {
     }
     // the hit KV is in the PE pool: the load path's PE release (desim.cpp:646-647)
     if (q.r.t_landed < 0) q.r.t_landed = now();
+    const double ttft = q.r.t_landed - q.r.t_arrival;
+    rep_.ttft_series.emplace_back(q.r.t_landed, ttft);
+    if (o_.slo_ttft_s > 0 && ttft > o_.slo_ttft_s) {  // the SLO stop (desim.cpp:679-685)
+      rep_.slo_violated = true;
+      stop_ = true;
+    }
     tok_[q.r.pe] -= q.total();
     seq_[q.r.pe] -= 1;
     auto& fl = free_slots_[q.r.pe];
@@ -480,7 +511,7 @@ class Live {
         double done_at = 0;
         {
           std::unique_lock<std::mutex> lk(rd->mu);
-          rd->cv.wait(lk, [rd] { return !rd->inflight.empty() || (rd->stop && rd->jobs.empty()); });
+          rd->cv.wait(lk, [rd] { return !rd->inflight.empty() || rd->worker_done; });
           if (rd->inflight.empty()) return;
           std::tie(id, ev) = rd->inflight.front();
           rd->inflight.pop_front();
@@ -531,6 +562,7 @@ class Live {
       if ((is_pe(e) && o_.exec.k1_mode == 3) || (!is_pe(e) && o_.exec.k2_mode == 2)) {
         check(dp_stager_create(devs_[e], &geom, o_.exec.stage_ring_bytes, &sg), "dp_stager_create");
         check(dp_stager_set_ctas(sg, o_.exec.stage_ctas), "dp_stager_set_ctas");
+        check(dp_stager_set_mode(sg, o_.exec.stage_scatter), "dp_stager_set_mode");
       }
       stagers_.push_back(sg);
     }
@@ -608,6 +640,8 @@ class Live {
   int g_ = 1, n_pe_ = 1, n_eng_ = 2;
   std::int32_t T_ = 64, L_ = 1;
   std::int64_t total_reqs_ = 0, completed_ = 0, fb_stride_ = 1, store_fb_ = 1, tab_used_ = 0;
+  bool stop_ = false;
+  double next_steady_ = 0;
   std::int32_t pool_slots_ = 0;
   Clock::time_point t0_;
   std::vector<Req> reqs_;

@@ -72,7 +72,8 @@ def bench_case(case):
     rounds = bench.reference_trace(A, wl, sessions, trace)
     rate = cap * 1e9 if cap else bench.PCIE_ZC_BPS
     kv = dict(P=P, D=D, g=1, L=shape["L"], b=shape["b"], T=shape["T"], B=bench.NVLINK_BPS,
-              s=rate / bench.NVLINK_BPS, M=2e12, hbm=100_000_000, pe_buf=1 << 42, de_buf=1 << 42,
+              s=rate / bench.NVLINK_BPS, M=2e12, hbm=100_000_000, pe_buf=bench.buffer_bytes(shape),
+              de_buf=bench.buffer_bytes(shape),
               policy=policy, flows=1, **bench.PLAN_KW)
     t0 = __import__("time").time()
     rep = refpy.ref_simulate(trace, **kv)

@@ -394,7 +394,8 @@ def test_edge_128k_context(gpus):
 
 
 @pytest.mark.parametrize("tight", [False, True])
-def test_staged_loaders(de_dev, tight):
+@pytest.mark.parametrize("scatter", [0, 1])
+def test_staged_loaders(de_dev, tight, scatter):
     """k1_mode 3 / k2_mode 2: copy engine into the HBM ring + scatter kernel on
     both read paths, with a small ring (jobs span segments) and, tight, slot
     reuse across readers; final pool and counters equal the oracle's."""
@@ -404,6 +405,7 @@ def test_staged_loaders(de_dev, tight):
     opt = dp.ExecOptions()
     opt.seed = SEED
     opt.k1_mode, opt.k2_mode = 3, 2
+    opt.stage_scatter = scatter
     opt.stage_ring_bytes = 24 * 4 * 64 * 576 * 4  # 24 Full Blocks per segment
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     if tight:
@@ -417,6 +419,33 @@ def test_staged_loaders(de_dev, tight):
         pe.reset_counters()
         res = dp.run_step_all([pe, de])
         assert res[0].bytes_read + res[1].bytes_read == xp.hit_bytes
-        assert res[0].launches > 0 and res[1].launches > 0  # the scatter kernels
+        if scatter == 0:
+            assert res[0].launches > 0 and res[1].launches > 0  # the scatter kernels
         verify_counters(pe, xp, cfg)
         verify_pool(pe, xp, cfg)
+
+
+@pytest.mark.parametrize("k1", [0, 3])
+def test_buffer_bound_stalls(de_dev, k1):
+    """A host staging bound (pe_buffer_bytes / de_buffer_bytes, the reference's
+    try_admit reservation) just above the largest request: the planner's
+    admissions stall in virtual time, the executor's reads wait for earlier
+    transfers to land (buffer_stalls > 0), and the pool is still exact."""
+    cfg = cluster(1, 1, L=4)
+    trajs = small_trace(count=8, turns=5, seed=5)
+    kvt = cfg.kv_bytes_per_token()
+    big = max(dp.context_before(t, len(t.rounds) - 1) + t.rounds[-1].append_tokens for t in trajs) * kvt
+    cfg.pe_buffer_bytes = cfg.de_buffer_bytes = int(big * 1.5)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.k1_mode = k1
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    pe = dp.EngineRuntime(xp, 0, 0)
+    de = dp.EngineRuntime(xp, 1, de_dev)
+    de.attach_peer_local(0, pe)
+    pe.reset_counters()
+    res = dp.run_step_all([pe, de])
+    assert res[0].buffer_stalls + res[1].buffer_stalls > 0
+    verify_counters(pe, xp, cfg)
+    verify_pool(pe, xp, cfg)

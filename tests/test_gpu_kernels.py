@@ -343,7 +343,8 @@ def test_numa_store_and_storage_read(gpus, placement):
 @pytest.mark.parametrize("L,T,b,ring", [(61, 64, 576, 40 << 20), (4, 64, 4096, 16 << 20), (3, 16, 1024, 0),
                                         (64, 64, 4096, 256 << 20)])
 @pytest.mark.parametrize("side", ["pe", "de_same_gpu", "de_peer_gpu"])
-def test_staged_k1_k2_parity(gpus, L, T, b, ring, side):
+@pytest.mark.parametrize("scatter", ["kernel", "ce"])
+def test_staged_k1_k2_parity(gpus, L, T, b, ring, side, scatter):
     """Staged K1 / K2 (copy engine into an HBM ring + scatter kernel): same
     bytes and counters as the gather kernel, with runs broken by
     non-consecutive Full Blocks, partial last blocks, jobs larger than a ring
@@ -354,15 +355,17 @@ def test_staged_k1_k2_parity(gpus, L, T, b, ring, side):
     dev = {"pe": 0, "de_same_gpu": 0, "de_peer_gpu": 1}[side]
     rng = np.random.default_rng(L + b)
     g = abi.geom(L, T, b)
-    n_fb, n_slots = 40, 96
+    n_fb, n_slots = 40, 192
     st = abi.Store(dev, g, n_fb, SEED)
     pool = abi.Pool(0, g, n_slots, 16)
     view = pool.peer_view(dev) if side != "pe" else None
     stager = abi.Stager(dev, g, ring)
+    ce = scatter == "ce"
+    if ce:
+        stager.set_mode(abi.SCATTER_CE)
     s = torch.cuda.Stream(device=dev)
     try:
         plain, keep, specs, used = [], [], [], 0
-        perm = rng.permutation(n_slots)
         for t in range(16):
             nblk = int(rng.integers(0, 9))
             if used + nblk > n_slots:
@@ -372,11 +375,14 @@ def test_staged_k1_k2_parity(gpus, L, T, b, ring, side):
             fbs = np.arange(fb0, fb0 + nblk, dtype=np.int64)
             if nblk >= 4:
                 fbs[nblk // 2:] = rng.integers(0, n_fb, nblk - nblk // 2)  # break the run
-            slots = perm[used:used + nblk].astype(np.int32)
-            used += nblk
+            # runs of consecutive slots (the copy-engine scatter's 2D copies), broken once
+            slots = (used + np.arange(nblk)).astype(np.int32)
+            if nblk >= 4:
+                slots[nblk // 2:] += 1
+            used += nblk + 2
             ds = dev_i32(slots if nblk else [0], dev)
-            keep += [fbs, ds]
-            specs.append((fbs.ctypes.data, ds.data_ptr(), ntok, nblk, 0, L, t))
+            keep += [fbs, ds, slots]
+            specs.append((fbs.ctypes.data, slots.ctypes.data if ce else ds.data_ptr(), ntok, nblk, 0, L, t))
             plain.append((fbs, slots, ntok, 0, L))
         for half in (specs[:7], specs[7:]):  # two calls: the ring is reused across calls
             jobs = abi.make_jobs(half)
@@ -392,7 +398,7 @@ def test_staged_k1_k2_parity(gpus, L, T, b, ring, side):
                 abi.wait_layer(pool, t, L - 1, items, timeout_ms=10000)
         sync()
         assert abi.wait_status(pool) == abi.DP_OK
-        assert stager.launches() >= 2
+        assert stager.launches() >= (0 if ce else 2)
         store_img = np.frombuffer(st.bytes(), dtype=np.uint8).copy()
         check_pool(pool, refpy.geom(L, T, b), plain, T, b, store_img, n_slots)
         bad = abi.make_jobs([(specs[1][0], specs[1][1], specs[1][2], specs[1][3], 1, L, 1)])  # layer subrange

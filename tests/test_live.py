@@ -123,3 +123,29 @@ def test_live_gpu_moves_the_bytes(de_dev, k1, k2, tight):
     for pe, slot, fb, ntok, h0, h1 in rep["final_slots"]:
         assert h0 == refpy.layer_block_hash(g, 9, fb, 0, ntok)
         assert h1 == refpy.layer_block_hash(g, 9, fb, cfg.n_layer - 1, ntok)
+
+
+def test_live_online_slo_stop_and_arrivals():
+    """Online: sessions arrive at given times (run_online's Poisson arrivals,
+    desim.cpp:1036-1051); a turn's measured load TTFT over the SLO stops the
+    run (desim.cpp:679-685), a generous SLO lets it finish."""
+    trajs = dp.synthesize(max_len=16000, count=12, seed=3, mean_turns=4, sigma_turns=0)
+    rng = np.random.default_rng(5)
+    arrivals = list(np.cumsum(rng.exponential(1 / 400.0, len(trajs))))  # 400 sessions/s
+    ex = dp.ExecOptions()
+    ex.storage_cap_Bps = 1e9
+    ok = dp.run_live(cluster(1, 1), trajs, exec=ex, gpu=False, link_Bps=8e9, arrival_times=arrivals,
+                     slo_ttft=10.0)
+    assert not ok["slo_violated"] and ok["completed_requests"] == ok["total_requests"]
+    first = {}
+    for r in ok["requests"]:
+        if r[2] == 0:
+            first[r[1]] = r[10]
+    for t, a in enumerate(arrivals):
+        assert first[t] >= a - 1e-4  # no session arrives before its time
+    tight = dp.run_live(cluster(1, 1), trajs, exec=ex, gpu=False, link_Bps=8e9, arrival_times=arrivals,
+                        slo_ttft=1e-4)
+    assert tight["slo_violated"] and tight["completed_requests"] < tight["total_requests"]
+    steady = dp.run_live(cluster(1, 1), trajs, exec=ex, gpu=False, link_Bps=8e9, arrival_times=arrivals,
+                         steady_window=0.002, steady_lookback=0.01, steady_threshold=0.9)
+    assert steady["steady_state"] or steady["completed_requests"] == steady["total_requests"]

@@ -98,6 +98,14 @@ def main():
         st1.append((fbs.ctypes.data, s0.data_ptr(), blocks * T, blocks, 0, L, j))
         st2.append((fbs.ctypes.data, s1.data_ptr(), blocks * T, blocks, 0, L, n_jobs + j))
     jobs_st1, jobs_st2 = abi.make_jobs(st1), abi.make_jobs(st2)
+    ce1, ce2 = [], []  # the copy-engine scatter reads HOST slot tables
+    for j in range(n_jobs):
+        fbs = st_keep[3 * j]
+        sl = np.arange(j * blocks, (j + 1) * blocks, dtype=np.int32) % n_slots
+        st_keep.append(sl)
+        ce1.append((fbs.ctypes.data, sl.ctypes.data, blocks * T, blocks, 0, L, j))
+        ce2.append((fbs.ctypes.data, sl.ctypes.data, blocks * T, blocks, 0, L, n_jobs + j))
+    jobs_ce1, jobs_ce2 = abi.make_jobs(ce1), abi.make_jobs(ce2)
     stager0, stager1 = abi.Stager(0, g), abi.Stager(1, g)
     s_gemm = torch.cuda.Stream(device=0, priority=-1)  # high priority compute
     s_k1 = torch.cuda.Stream(device=0, priority=0)
@@ -114,11 +122,13 @@ def main():
     torch.cuda.synchronize(1)
     flops = 2.0 * a.m * a.m * a.k
 
-    def run_with(k1=False, k2=False, ctas=0, ce=False, staged=False, stage_ctas=32, on_de=False):
+    def run_with(k1=False, k2=False, ctas=0, ce=False, staged=False, stage_ctas=32, on_de=False, ce_scatter=False):
         for dev in (0, 1):
             abi.set_gather_ctas(dev, ctas)
         stager0.set_ctas(stage_ctas)
         stager1.set_ctas(stage_ctas)
+        for sg in (stager0, stager1):
+            sg.set_mode(abi.SCATTER_CE if ce_scatter else abi.SCATTER_KERNEL)
         stop = threading.Event()
         done = {"k1": [], "k2": []}  # completion wall times of each loader launch
         per_launch = n_jobs * blocks * T * B * L
@@ -128,9 +138,11 @@ def main():
             with torch.cuda.device(dev):
                 while not stop.is_set():
                     if staged and kind == "k1":
-                        abi.h2d_layer_staged(pool, st_pe, stager0, jobs_st1, n_jobs, stream.cuda_stream)
+                        abi.h2d_layer_staged(pool, st_pe, stager0, jobs_ce1 if ce_scatter else jobs_st1, n_jobs,
+                                             stream.cuda_stream)
                     elif staged:
-                        abi.h2d_push_staged(view, st_de, stager1, jobs_st2, n_jobs, stream.cuda_stream)
+                        abi.h2d_push_staged(view, st_de, stager1, jobs_ce2 if ce_scatter else jobs_st2, n_jobs,
+                                            stream.cuda_stream)
                     elif kind == "k1" and ce:
                         abi.h2d_layer_copy(pool, st_pe, jobs_ce, n_jobs, stream.cuda_stream)
                     elif kind == "k1":
@@ -169,6 +181,7 @@ def main():
     out["de_alone"] = run_with(on_de=True)
     base_de = out["de_alone"]["gemm_ms"]
     for name, kw in [("de_k2_sm", dict(k2=True)), ("de_k2_staged", dict(k2=True, staged=True)),
+                     ("de_k2_staged_ce", dict(k2=True, staged=True, ce_scatter=True)),
                      ("de_k2_staged_8ctas", dict(k2=True, staged=True, stage_ctas=8)),
                      ("de_k2_copy_engine", dict(k2=True, ce=True))]:
         if kw.get("ce"):
@@ -176,8 +189,11 @@ def main():
         r = run_with(on_de=True, **kw)
         r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base_de - 1.0), 2)
         out[name] = r
+    ce_cases = [("k1_staged_ce", dict(k1=True, staged=True, ce_scatter=True)),
+                ("k2_staged_ce", dict(k2=True, staged=True, ce_scatter=True)),
+                ("k1_staged_ce+k2_staged_ce", dict(k1=True, k2=True, staged=True, ce_scatter=True))]
     if a.only_staged:
-        cases = [("k1_staged", dict(k1=True, staged=True)), ("k1_staged_8ctas", dict(k1=True, staged=True, stage_ctas=8)),
+        cases = ce_cases + [("k1_staged", dict(k1=True, staged=True)), ("k1_staged_8ctas", dict(k1=True, staged=True, stage_ctas=8)),
                  ("k2_staged", dict(k2=True, staged=True)),
                  ("k1_staged+k2_staged", dict(k1=True, k2=True, staged=True)),
                  ("k1_staged_8ctas+k2_staged_8ctas", dict(k1=True, k2=True, staged=True, stage_ctas=8))]
@@ -191,15 +207,18 @@ def main():
              ("k1_default+k2", dict(k1=True, k2=True)),
              ("k1_copy_engine", dict(k1=True, ce=True)),
              ("k1_copy_engine+k2", dict(k1=True, k2=True, ce=True))]
-    if a.skip_layerwise:
-        print(json.dumps(out))
-        return
+
     for name, kw in cases:
         r = run_with(**kw)
         r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base - 1.0), 2)
         out[name] = r
     for dev in (0, 1):
         abi.set_gather_ctas(dev, 0)
+    stager0.set_mode(abi.SCATTER_KERNEL)
+    stager1.set_mode(abi.SCATTER_KERNEL)
+    if a.skip_layerwise:
+        print(json.dumps(out))
+        return
 
     # layerwise overlap: push one 32K-token request (512 blocks) and compute
     # layer l once layer l has landed
