@@ -156,7 +156,7 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   // layerwise K3 CTAs wait in-kernel for the forward's layers: a few suffice
   // and leave the SMs to the prefill compute
   if (is_pe())
-    check(dp_set_handoff_ctas(device_, x.opt.handoff_ctas ? x.opt.handoff_ctas : layerwise_handoff() ? 32 : 0),
+    check(dp_set_handoff_ctas(device_, x.opt.handoff_ctas ? x.opt.handoff_ctas : layerwise_handoff() ? 64 : 0),
           "dp_set_handoff_ctas");
   if (is_pe() && x.prefill) check(dp_set_attend_ctas(device_, x.opt.attend_ctas), "dp_set_attend_ctas");
 }

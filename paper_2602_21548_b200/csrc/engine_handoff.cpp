@@ -61,50 +61,68 @@ StepResult EngineRuntime::run_step_handoff() {
       for (const FwdItem& it : x.fwd_items[engine_])
         if (it.job >= 0) row_of[it.job] = it.row;
     }
-    // K3 of one job on the handoff stream: decode-slot hazards, then K3
-    auto enqueue_k3 = [&](int ji) {
-      const LoadJob& j = x.jobs[ji];
-      auto ev_k3 = static_cast<cudaEvent_t>(ev_k3_[pe_local_[ji]]);
-      const bool lw = pf && layerwise_handoff();
-      if (pf && !lw)  // the prompt is handed off after its last forward
-        check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[ji]]), 0),
-                   "cudaStreamWaitEvent");
-      if (!j.de_preds.empty()) {
-        const std::int64_t off = de_wait_off_[ji];
-        check(dp_wait_tickets(de_views_[j.de], d_wt_ + off, d_wg_ + off,
-                              static_cast<int32_t>(j.de_preds.size()), L, x.opt.wait_timeout_ms, h),
-              "dp_wait_tickets (decode slots)");
-        ++res.launches;
+    // K3 of a set of jobs on the handoff stream: each job's decode-slot
+    // hazards, then one K3 call per decode engine (a layerwise forward's
+    // requests in one launch: every request's layer l moves once the forward
+    // has computed l), then each job's "K3 done" event
+    const bool lw = pf && layerwise_handoff();
+    auto enqueue_k3_set = [&](const std::vector<int>& set) {
+      std::vector<std::pair<int, dp_handoff_job>> hjs;  // (decode engine, job)
+      for (int ji : set) {
+        const LoadJob& j = x.jobs[ji];
+        if (pf && !lw)  // the prompt is handed off after its last forward
+          check_cuda(cudaStreamWaitEvent(h, static_cast<cudaEvent_t>(ev_fwd_[x.last_fwd[ji]]), 0),
+                     "cudaStreamWaitEvent");
+        if (!j.de_preds.empty()) {
+          const std::int64_t off = de_wait_off_[ji];
+          check(dp_wait_tickets(de_views_[j.de], d_wt_ + off, d_wg_ + off,
+                                static_cast<int32_t>(j.de_preds.size()), L, x.opt.wait_timeout_ms, h),
+                "dp_wait_tickets (decode slots)");
+          ++res.launches;
+        }
+        const bool layer_gate = x.opt.k3_layer_gate == 1;
+        if (j.de_path && j.n_blk > 0 && !layer_gate && !lw) {
+          // the whole request's hit KV, pushed by its DE: a one-thread spin
+          // kernel with the watchdog (a DE that never pushes -- e.g. its rank
+          // died -- fails the step with DP_ETIMEOUT instead of hanging it)
+          check(dp_wait_layer(pool_, j.ticket, L,
+                              static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block * L),
+                              x.opt.wait_timeout_ms, h),
+                "dp_wait_layer (handoff gate)");
+          ++res.launches;
+        }
+        dp_handoff_job hj{d_ho_src_ + j.ho_off,
+                          d_ho_pe_ + j.ho_off,
+                          d_ho_de_ + j.ho_off,
+                          j.cached,
+                          j.prompt,
+                          j.n_pblk,
+                          j.de_path ? 0 : 1,
+                          // layerwise: layer l waits for the finishing forward's layer l (which
+                          // itself waited for the request's hit KV of layer l)
+                          lw ? fwd_row0_ + x.last_fwd[ji] : (j.de_path && j.n_blk > 0 && layer_gate) ? j.ticket : -1,
+                          lw ? 1u : static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block),
+                          j.de_ticket,
+                          j.ticket + nt(engine_)};
+        hjs.emplace_back(j.de, hj);
       }
-      const bool layer_gate = x.opt.k3_layer_gate == 1;
-      if (j.de_path && j.n_blk > 0 && !layer_gate && !lw) {
-        // the whole request's hit KV, pushed by its DE: a one-thread spin
-        // kernel with the watchdog (a DE that never pushes -- e.g. its rank
-        // died -- fails the step with DP_ETIMEOUT instead of hanging it)
-        check(dp_wait_layer(pool_, j.ticket, L,
-                            static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block * L),
-                            x.opt.wait_timeout_ms, h),
-              "dp_wait_layer (handoff gate)");
-        ++res.launches;
+      std::vector<int> des;
+      for (const auto& [de, hj] : hjs)
+        if (std::find(des.begin(), des.end(), de) == des.end()) des.push_back(de);
+      for (int de : des) {
+        std::vector<dp_handoff_job> batch;
+        for (const auto& [d, hj] : hjs)
+          if (d == de) batch.push_back(hj);
+        check(dp_prefill_handoff(pool_, de_views_[de], batch.data(), static_cast<int32_t>(batch.size()), x.opt.seed,
+                                 x.opt.wait_timeout_ms, h),
+              "dp_prefill_handoff");
+        res.launches += (static_cast<std::int64_t>(batch.size()) + DP_MAX_HANDOFF_JOBS_PER_LAUNCH - 1) /
+                        DP_MAX_HANDOFF_JOBS_PER_LAUNCH;
       }
-      dp_handoff_job hj{d_ho_src_ + j.ho_off,
-                        d_ho_pe_ + j.ho_off,
-                        d_ho_de_ + j.ho_off,
-                        j.cached,
-                        j.prompt,
-                        j.n_pblk,
-                        j.de_path ? 0 : 1,
-                        // layerwise: layer l waits for the finishing forward's layer l (which
-                        // itself waited for the request's hit KV of layer l)
-                        lw ? fwd_row0_ + x.last_fwd[ji] : (j.de_path && j.n_blk > 0 && layer_gate) ? j.ticket : -1,
-                        lw ? 1u : static_cast<std::uint32_t>(static_cast<std::int64_t>(j.n_blk) * x.items_per_block),
-                        j.de_ticket,
-                        j.ticket + nt(engine_)};
-      check(dp_prefill_handoff(pool_, de_views_[j.de], &hj, 1, x.opt.seed, x.opt.wait_timeout_ms, h),
-            "dp_prefill_handoff");
-      ++res.launches;
-      check_cuda(cudaEventRecord(ev_k3, h), "cudaEventRecord");
+      for (int ji : set)
+        check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_k3_[pe_local_[ji]]), h), "cudaEventRecord");
     };
+    auto enqueue_k3 = [&](int ji) { enqueue_k3_set({ji}); };
     // prefill: forwards whose requests' loads are all enqueued (row < r), and
     // the K3s of the requests they finish
     static const std::vector<Forward> kNone;
@@ -113,7 +131,13 @@ StepResult EngineRuntime::run_step_handoff() {
     auto drain = [&](std::int64_t r) {
       while (fi < fwds.size() && fwds[fi].last_row < r) {
         enqueue_forward(static_cast<int>(fi++), res);
-        while (ki < mine.size() && x.last_fwd[mine[ki]] < static_cast<int>(fi)) enqueue_k3(mine[ki++]);
+        std::vector<int> set;
+        while (ki < mine.size() && x.last_fwd[mine[ki]] < static_cast<int>(fi)) set.push_back(mine[ki++]);
+        if (lw) {
+          if (!set.empty()) enqueue_k3_set(set);
+        } else {
+          for (int ji : set) enqueue_k3(ji);
+        }
       }
     };
     for (int ji : mine) {

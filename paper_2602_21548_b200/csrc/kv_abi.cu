@@ -1202,9 +1202,17 @@ __device__ void tma_push(char* dst, const char* src, int64_t bytes, char* smem, 
   bulk_wait_all();
 }
 
+constexpr int kHoUnroll = 4;  // K3's register-staged copy depth (fits the 40-register cap)
+
+// Items are LAYER-major: item = layer * G + g, g a group of one job's pieces
+// (item_begin = prefix sums of the jobs' groups, G their total), so every
+// job's layer l is pushed before any job's layer l+1 -- what a gated,
+// layerwise handoff of a whole forward's requests needs.  <= 40 registers:
+// a K3 CTA beside two K5 CTAs still fits an SM's register file.
 template <bool kTma>
-__global__ void __launch_bounds__(kThreads) kv_prefill_handoff(const __grid_constant__ HandoffParams p) {
-  const int64_t total = p.item_begin[p.n_jobs];
+__global__ void __launch_bounds__(kThreads, 6) kv_prefill_handoff(const __grid_constant__ HandoffParams p) {
+  const int64_t G = p.item_begin[p.n_jobs];
+  const int64_t total = G * p.n_layer;
   const int tid = threadIdx.x;
   const int64_t lb = p.lb_bytes;
   extern __shared__ __align__(128) char tma_smem[];
@@ -1218,13 +1226,12 @@ __global__ void __launch_bounds__(kThreads) kv_prefill_handoff(const __grid_cons
     __syncthreads();
   }
   for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
-    const int j = decode_job(p, item);
+    const int layer = static_cast<int>(item / G);
+    const int64_t gi = item - layer * G;
+    const int j = decode_job(p, gi);
     const dp_handoff_job& job = p.jobs[j];
-    const int64_t local = item - p.item_begin[j];
     const int64_t pieces = static_cast<int64_t>(job.n_blk) * p.n_chunk;
-    const int64_t groups = (pieces + kHandoffGroup - 1) / kHandoffGroup;
-    const int layer = static_cast<int>(local / groups);
-    const int64_t piece0 = (local % groups) * kHandoffGroup;
+    const int64_t piece0 = (gi - p.item_begin[j]) * kHandoffGroup;
     const int64_t piece1 = min(piece0 + kHandoffGroup, pieces);
     // the layer gate: layer l's hit KV must have landed before "computing" l
     if (job.pe_ticket >= 0) {
@@ -1263,15 +1270,15 @@ __global__ void __launch_bounds__(kThreads) kv_prefill_handoff(const __grid_cons
         const uint4* src = reinterpret_cast<const uint4*>(p.pe_pool + pe_off + beg);
         uint4* dst = reinterpret_cast<uint4*>(p.de_pool + de_off + beg);
         const int n16 = static_cast<int>((h1 - beg) >> 4);
-        for (int base = 0; base < n16; base += kThreads * kUnroll) {
-          uint4 v[kUnroll];
+        for (int base = 0; base < n16; base += kThreads * kHoUnroll) {
+          uint4 v[kHoUnroll];
 #pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
+          for (int u = 0; u < kHoUnroll; ++u) {
             const int i = base + u * kThreads + tid;
             if (i < n16) v[u] = __ldcg(src + i);  // landed by another GPU: bypass L1
           }
 #pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
+          for (int u = 0; u < kHoUnroll; ++u) {
             const int i = base + u * kThreads + tid;
             if (i < n16) st_v4(dst + i, v[u]);
           }
@@ -1413,7 +1420,7 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
           (job.n_blk > 0 && (!job.src_fb || !job.pe_slot || !job.de_slot)))
         return fail(DP_EINVAL, "prefill_handoff: job " + std::to_string(j0 + j) + " out of range");
       const int64_t pieces = static_cast<int64_t>(job.n_blk) * p.n_chunk;
-      const int64_t n = (pieces + kHandoffGroup - 1) / kHandoffGroup * g.n_layer;
+      const int64_t n = (pieces + kHandoffGroup - 1) / kHandoffGroup;  // groups per layer
       if (n == 0) continue;
       p.jobs[p.n_jobs] = job;
       p.item_begin[p.n_jobs] = items;
@@ -1422,7 +1429,7 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
     }
     p.item_begin[p.n_jobs] = items;
     if (items == 0) continue;
-    const int grid = static_cast<int>(std::min<int64_t>(items, grid_cap));
+    const int grid = static_cast<int>(std::min<int64_t>(items * g.n_layer, grid_cap));
     if (g_handoff_tma.load())
       kv_prefill_handoff<true><<<grid, kThreads, kHandoffTmaSmem, s>>>(p);
     else
