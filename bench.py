@@ -107,7 +107,9 @@ def parse():
                     help="PE-path loads: sm = K1 gather kernel, ce = copy engine (no SMs), "
                          "hybrid = both at once, jobs split by bytes, staged = copy engine into an HBM "
                          "ring + scatter kernel")
-    ap.add_argument("--stage-ctas", type=int, default=32, help="staged modes: scatter kernel CTAs")
+    ap.add_argument("--stage-ctas", type=int, default=32, help="staged K1: scatter kernel CTAs")
+    ap.add_argument("--stage-push-ctas", type=int, default=148,
+                    help="staged K2: CTAs of the scatter pushing over NVLink")
     ap.add_argument("--stage-scatter", default="kernel", choices=["kernel", "ce"],
                     help="staged modes: ring -> pool scatter by a kernel or by the copy engine (no SMs)")
     return ap.parse_args()
@@ -492,6 +494,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     opt.k1_mode = {"sm": 0, "ce": 1, "hybrid": 2, "staged": 3}[args.k1]
     opt.k2_mode = {"sm": 0, "ce": 1, "staged": 2}[args.k2]
     opt.stage_ctas = args.stage_ctas
+    opt.stage_push_ctas = args.stage_push_ctas
     opt.stage_scatter = 1 if args.stage_scatter == "ce" else 0
     opt.wait_timeout_ms = args.wait_timeout_ms
     opt.handoff = bool(args.handoff or args.persist)
@@ -1021,6 +1024,7 @@ def main():
                                   "dual_path", shape, args.cap_gbps, stats, extra),
             "plan": plan_block(info, args.workload, sessions, P, D, args.cap_gbps, link_bps),
             "loaders": {"k1": args.k1, "k2": args.k2, "stage_ctas": args.stage_ctas,
+                        "stage_push_ctas": args.stage_push_ctas,
                         "stage_scatter": args.stage_scatter,
                         "handoff_ctas": args.handoff_ctas or None,
                         "buffer_stalls": info["buffer_stalls"],

@@ -61,7 +61,9 @@ struct ExecOptions {
   // pushes over NVLink into the PE pool (dp_h2d_push_staged)
   std::int32_t k2_mode = 0;
   std::int64_t stage_ring_bytes = 1LL << 30;  // staged modes: HBM ring per engine
-  std::int32_t stage_ctas = 32;               // staged modes: scatter CTAs
+  std::int32_t stage_ctas = 32;               // staged K1: scatter CTAs (HBM -> HBM)
+  std::int32_t stage_push_ctas = 148;         // staged K2: scatter CTAs pushing over NVLink
+                                              // (peer stores need more in flight)
   std::int32_t stage_scatter = 0;             // staged modes: 0 = scatter kernel, 1 = copy engine
                                               // (DP_SCATTER_CE: no SM work at all)
   // PD handoff: every request's prompt KV also ends in its

@@ -123,7 +123,7 @@ int dp_device_numa_node(int device, int32_t* node);
 /* Emulated storage NIC (StorageRead over {snic_rd, dram}, desim.cpp:603-606):
  * a FIFO token bucket at rate_Bps (0 = unlimited).  dp_nic_read blocks the
  * calling thread until the NIC has delivered `bytes`: the transfer begins at
- * max(NIC free, not_before_s) and lasts bytes / rate; times are seconds
+ * max(NIC free, not_before_s, now) and lasts bytes / rate; times are seconds
  * since dp_nic_start (optional outputs t_begin / t_end).  Thread-safe: the
  * IO threads of an engine share its NIC. */
 typedef struct dp_nic dp_nic;

@@ -128,7 +128,7 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   }
   if (!x.by_reader[engine_].empty() && ((is_pe() && x.opt.k1_mode == 3) || (!is_pe() && x.opt.k2_mode == 2))) {
     check(dp_stager_create(device_, &x.geom, x.opt.stage_ring_bytes, &stager_), "dp_stager_create");
-    check(dp_stager_set_ctas(stager_, x.opt.stage_ctas), "dp_stager_set_ctas");
+    check(dp_stager_set_ctas(stager_, is_pe() ? x.opt.stage_ctas : x.opt.stage_push_ctas), "dp_stager_set_ctas");
     check(dp_stager_set_mode(stager_, x.opt.stage_scatter), "dp_stager_set_mode");
   }
   if (x.handoff) {

@@ -131,10 +131,33 @@ __device__ __forceinline__ int decode_job(const Params& p, int64_t item) {
   return __popc(lo) + __popc(hi);
 }
 
-template <bool kPeer>
+// L2 evict-first variants for the staged scatter (ring -> pool): the bytes
+// pass through L2 once, so they should not displace a co-running kernel's
+// working set (config 4's GEMM stand-in).
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_stream_ef(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_v4_ef(uint4* p, const uint4& v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+
+// kStream: the staged scatter's ring -> pool copy (L2 evict-first both ways).
+template <bool kPeer, bool kStream = false>
 __global__ void __launch_bounds__(kThreads) kv_gather(const __grid_constant__ GatherParams p) {
   const int64_t total = p.item_begin[p.n_jobs];
   const int tid = threadIdx.x;
+  const uint64_t pol = kStream ? evict_first_policy() : 0;
   for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
     const int j = decode_job(p, item);
     const dp_job& job = p.jobs[j];
@@ -164,12 +187,15 @@ __global__ void __launch_bounds__(kThreads) kv_gather(const __grid_constant__ Ga
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
           const int i = base + u * kThreads + tid;
-          if (i < n16) v[u] = ld_stream(src + i);
+          if (i < n16) v[u] = kStream ? ld_stream_ef(src + i, pol) : ld_stream(src + i);
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
           const int i = base + u * kThreads + tid;
-          if (i < n16) st_v4(dst + i, v[u]);
+          if (i < n16) {
+            if (kStream && !kPeer) st_v4_ef(dst + i, v[u], pol);
+            else st_v4(dst + i, v[u]);
+          }
         }
       }
     }
@@ -340,7 +366,7 @@ int64_t counters_offset(int64_t data_bytes) { return (data_bytes + 255) / 256 * 
 int preload_kernels(int device);
 
 int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
-                  dp_stream stream, bool peer, int ctas_override = 0) {
+                  dp_stream stream, bool peer, int ctas_override = 0, bool stream_hint = false) {
   if (!pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0)
     return fail(DP_EINVAL, "gather: null argument");
   if (!geom_equal(pool->geom, src->geom))
@@ -393,8 +419,12 @@ int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_
     p.item_begin[p.n_jobs] = items;
     if (items == 0) continue;
     const int grid = static_cast<int>(std::min<int64_t>(items, grid_cap));
-    if (peer)
+    if (peer && stream_hint)
+      kv_gather<true, true><<<grid, kThreads, 0, s>>>(p);
+    else if (peer)
       kv_gather<true><<<grid, kThreads, 0, s>>>(p);
+    else if (stream_hint)
+      kv_gather<false, true><<<grid, kThreads, 0, s>>>(p);
     else
       kv_gather<false><<<grid, kThreads, 0, s>>>(p);
     DP_CUDA(cudaGetLastError());
@@ -1957,7 +1987,7 @@ int staged_transfer(const char* who, dp_pool* pool, const dp_store* src, dp_stag
       }
     } else if (!sub.empty()) {
       if (int rc = launch_gather(pool, &st->ring, sub.data(), static_cast<int32_t>(sub.size()), stream, peer,
-                                 st->ctas))
+                                 st->ctas, /*stream_hint=*/true))
         return rc;
       ++st->launches;
     }
@@ -2095,6 +2125,8 @@ int preload_kernels(int device) {
     DeviceGuard guard(device);
     const void* fns[] = {reinterpret_cast<const void*>(kv_gather<false>),
                          reinterpret_cast<const void*>(kv_gather<true>),
+                         reinterpret_cast<const void*>(kv_gather<false, true>),
+                         reinterpret_cast<const void*>(kv_gather<true, true>),
                          reinterpret_cast<const void*>(kv_wait_ge),
                          reinterpret_cast<const void*>(kv_wait_many),
                          reinterpret_cast<const void*>(kv_block_checksum),

@@ -253,6 +253,7 @@ class Live {
     tab_used_ += q.n_blk;
     reqs_.push_back(q);
     de_global_.push_back(q.r.id);
+    arrived_in_wake_ = true;
   }
 
   pdsim::EngineSnapshot snapshot_of(int e) const {  // desim.cpp:797-807
@@ -392,6 +393,15 @@ class Live {
   }
 
   void wake() {  // scheduler_wake (desim.cpp:851-863)
+    // a cold turn lands at its admission and its session's next turn arrives
+    // at once: schedule again until no arrival is left waiting
+    do {
+      wake_once();
+    } while (!de_global_.empty() && !stop_ && arrived_in_wake_);
+  }
+
+  void wake_once() {
+    arrived_in_wake_ = false;
     if (o_.sim.sched_mode == pdsim::desim::SchedMode::Adaptive) schedule_adaptive();
     else schedule_round_robin();
     // admission pass, FIFO; PEs progress independently.  The bounded
@@ -561,7 +571,7 @@ class Live {
       dp_stager* sg = nullptr;
       if ((is_pe(e) && o_.exec.k1_mode == 3) || (!is_pe(e) && o_.exec.k2_mode == 2)) {
         check(dp_stager_create(devs_[e], &geom, o_.exec.stage_ring_bytes, &sg), "dp_stager_create");
-        check(dp_stager_set_ctas(sg, o_.exec.stage_ctas), "dp_stager_set_ctas");
+        check(dp_stager_set_ctas(sg, is_pe(e) ? o_.exec.stage_ctas : o_.exec.stage_push_ctas), "dp_stager_set_ctas");
         check(dp_stager_set_mode(sg, o_.exec.stage_scatter), "dp_stager_set_mode");
       }
       stagers_.push_back(sg);
@@ -641,6 +651,7 @@ class Live {
   std::int32_t T_ = 64, L_ = 1;
   std::int64_t total_reqs_ = 0, completed_ = 0, fb_stride_ = 1, store_fb_ = 1, tab_used_ = 0;
   bool stop_ = false;
+  bool arrived_in_wake_ = false;
   double next_steady_ = 0;
   std::int32_t pool_slots_ = 0;
   Clock::time_point t0_;

@@ -50,7 +50,9 @@ int dp_nic_read(dp_nic* nic, int64_t bytes, double not_before_s, double* t_begin
   std::chrono::steady_clock::time_point t0;
   {
     std::lock_guard<std::mutex> lk(nic->mu);
-    begin = std::max(nic->busy_until, not_before_s);
+    // an idle NIC starts the read now: no credit for the time it sat idle
+    const double now = std::chrono::duration<double>(std::chrono::steady_clock::now() - nic->t0).count();
+    begin = std::max({nic->busy_until, not_before_s, now});
     end = begin + (nic->rate > 0 ? static_cast<double>(bytes) / nic->rate : 0.0);
     nic->busy_until = end;
     t0 = nic->t0;

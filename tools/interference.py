@@ -122,11 +122,12 @@ def main():
     torch.cuda.synchronize(1)
     flops = 2.0 * a.m * a.m * a.k
 
-    def run_with(k1=False, k2=False, ctas=0, ce=False, staged=False, stage_ctas=32, on_de=False, ce_scatter=False):
+    def run_with(k1=False, k2=False, ctas=0, ce=False, staged=False, stage_ctas=32, on_de=False, ce_scatter=False,
+                 push_ctas=None):
         for dev in (0, 1):
             abi.set_gather_ctas(dev, ctas)
         stager0.set_ctas(stage_ctas)
-        stager1.set_ctas(stage_ctas)
+        stager1.set_ctas(push_ctas or stage_ctas)
         for sg in (stager0, stager1):
             sg.set_mode(abi.SCATTER_CE if ce_scatter else abi.SCATTER_KERNEL)
         stop = threading.Event()
@@ -182,6 +183,7 @@ def main():
     base_de = out["de_alone"]["gemm_ms"]
     for name, kw in [("de_k2_sm", dict(k2=True)), ("de_k2_staged", dict(k2=True, staged=True)),
                      ("de_k2_staged_ce", dict(k2=True, staged=True, ce_scatter=True)),
+                     ("de_k2_staged_148ctas", dict(k2=True, staged=True, push_ctas=148)),
                      ("de_k2_staged_8ctas", dict(k2=True, staged=True, stage_ctas=8)),
                      ("de_k2_copy_engine", dict(k2=True, ce=True))]:
         if kw.get("ce"):
@@ -189,7 +191,9 @@ def main():
         r = run_with(on_de=True, **kw)
         r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base_de - 1.0), 2)
         out[name] = r
-    ce_cases = [("k1_staged_ce", dict(k1=True, staged=True, ce_scatter=True)),
+    ce_cases = [("k2_staged_148ctas", dict(k2=True, staged=True, push_ctas=148)),
+                ("k1_staged+k2_staged_148ctas", dict(k1=True, k2=True, staged=True, push_ctas=148)),
+                ("k1_staged_ce", dict(k1=True, staged=True, ce_scatter=True)),
                 ("k2_staged_ce", dict(k2=True, staged=True, ce_scatter=True)),
                 ("k1_staged_ce+k2_staged_ce", dict(k1=True, k2=True, staged=True, ce_scatter=True))]
     if a.only_staged:
