@@ -90,6 +90,11 @@ struct ExecOptions {
   // the decode stand-in for the generated tokens and persists them (K4) every
   // 64 generated tokens plus the final partial, into its persist store
   bool persist = false;
+  // PersistWrite (desim.cpp:764-771): a FullBlockFile (record r = storage Full
+  // Block r) each DE writes the Full Blocks its K4 persisted into at the end of
+  // its step, so a later turn's StorageRead from the tier reads them back;
+  // empty: the persisted blocks stay in the pinned persist store
+  std::string persist_path;
   // Prefill stand-in (with or without `handoff`): every PE packs
   // its requests, in the order their KV lands, into forward batches with
   // pdsim::build_forward_batch under `compute_quota` (seconds per layer of
@@ -208,6 +213,11 @@ struct ExecPlan {
   std::vector<std::vector<std::int32_t>> dual_de_slot;     // per reader: hit blocks' DE slots
   std::int64_t handoff_bytes = 0;  // pushed by K3: (C+A)*L*b PE path, A*L*b DE path
   bool persist = false;
+  // PersistWrite (desim.cpp:764-771): a FullBlockFile (record r = storage Full
+  // Block r) each DE writes the Full Blocks its K4 persisted into at the end of
+  // its step, so a later turn's StorageRead from the tier reads them back;
+  // empty: the persisted blocks stay in the pinned persist store
+  std::string persist_path;
   std::vector<std::vector<std::int32_t>> dec_slot;         // per DE: all blocks' decode slots
   std::vector<std::vector<std::int64_t>> dec_fb;           // per DE: their storage Full Blocks
   std::int64_t persist_bytes = 0;                          // sum gen * L * b
@@ -255,6 +265,8 @@ struct StepResult {
   std::int64_t jobs = 0;
   std::int64_t forwards = 0;    // prefill forwards run (PE, ExecOptions::prefill)
   double io_wait_ms = 0;        // storage tier: host time the launches waited for reads
+  double persist_write_ms = 0;  // DE: PersistWrite of the step's persisted Full Blocks to the tier
+  std::int64_t persist_write_bytes = 0;
   // handoff (PE): per request, ms from the step start until its whole prompt
   // KV is in its DE's decode pool (the offline TTFT of the prefill path), and
   // the handoff lag: that time minus the end of the forward finishing it
@@ -378,6 +390,8 @@ class EngineRuntime {
   std::vector<std::vector<int>> ring_wait_local_;  // ring_waits as by_reader positions
   // ---- persistence (DE) ----
   dp_store* persist_store_ = nullptr;
+  std::unique_ptr<FullBlockFile> persist_file_;   // PersistWrite target (ExecOptions::persist_path)
+  void persist_write(StepResult& res);
   std::int32_t* d_dec_slot_ = nullptr;
   std::int64_t* d_dec_fb_ = nullptr;
 

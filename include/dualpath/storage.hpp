@@ -84,6 +84,8 @@ class FullBlockFile {
   // Writes records [0, n) with the content formula (threads in parallel).
   void populate(std::uint64_t seed, int threads);
   void write(std::int64_t record, const void* src);
+  // Writes bytes [offset, offset + n) of a record (buffered).
+  void write_bytes(std::int64_t record, std::int64_t offset, std::int64_t n, const void* src);
   // Reads one record into dst (O_DIRECT when dst is 4 KiB aligned and the
   // file was opened direct; buffered otherwise).  Throws on a short read.
   void read(std::int64_t record, void* dst) const;

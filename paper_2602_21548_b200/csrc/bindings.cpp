@@ -417,6 +417,7 @@ PYBIND11_MODULE(_core, m) {
       .def(py::init<>())
       .def_readwrite("storage_cap_Bps", &dualpath::ExecOptions::storage_cap_Bps)
       .def_readwrite("buffer_bound", &dualpath::ExecOptions::buffer_bound)
+      .def_readwrite("persist_path", &dualpath::ExecOptions::persist_path)
       .def_readwrite("storage_cap_per_engine", &dualpath::ExecOptions::storage_cap_per_engine)
       .def_readwrite("pace_scale", &dualpath::ExecOptions::pace_scale)
       .def_readwrite("k1_mode", &dualpath::ExecOptions::k1_mode)
@@ -590,6 +591,8 @@ PYBIND11_MODULE(_core, m) {
       .def_readonly("d2h_bytes", &dualpath::StepResult::d2h_bytes)
       .def_readonly("ttft_ms", &dualpath::StepResult::ttft_ms)
       .def_readonly("buffer_stalls", &dualpath::StepResult::buffer_stalls)
+      .def_readonly("persist_write_ms", &dualpath::StepResult::persist_write_ms)
+      .def_readonly("persist_write_bytes", &dualpath::StepResult::persist_write_bytes)
       .def_readonly("buffer_wait_ms", &dualpath::StepResult::buffer_wait_ms)
       .def_readonly("handoff_lag_ms", &dualpath::StepResult::handoff_lag_ms);
 

@@ -17,6 +17,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <thread>
+#include <tuple>
 
 namespace dualpath {
 
@@ -125,6 +126,8 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
     if (x.persist && !x.by_de[engine_].empty())  // content seed + 1: unwritten bytes differ
       check(dp_store_create(device_, &x.geom, x.store_fb, x.opt.seed + 1, &persist_store_),
             "dp_store_create (persist store)");
+    if (x.persist && !x.opt.persist_path.empty() && !x.by_de[engine_].empty())
+      persist_file_ = std::make_unique<FullBlockFile>(x.opt.persist_path, x.geom, x.store_fb, false, false);
   }
   if (!x.by_reader[engine_].empty() && ((is_pe() && x.opt.k1_mode == 3) || (!is_pe() && x.opt.k2_mode == 2))) {
     check(dp_stager_create(device_, &x.geom, x.opt.stage_ring_bytes, &stager_), "dp_stager_create");
@@ -588,6 +591,43 @@ std::vector<std::uint64_t> EngineRuntime::checksum(int layer, std::span<const st
   cudaFree(dn);
   cudaFree(dout);
   return out;
+}
+
+// PersistWrite (desim.cpp:764-771): every Full Block this DE's K4 wrote in
+// the step goes from the pinned persist store to its record in the storage
+// tier file (pwrite), after the step's device work is done.
+void EngineRuntime::persist_write(StepResult& res) {
+  if (!persist_file_) return;
+  const ExecPlan& x = *plan_;
+  const auto t0 = std::chrono::steady_clock::now();
+  void* host = nullptr;
+  std::int64_t bytes = 0, n_fb = 0;
+  check(dp_store_info(persist_store_, &host, &bytes, &n_fb), "dp_store_info");
+  const std::int64_t T = x.cfg.block_size_tokens, fbb = x.cfg.full_block_bytes();
+  const std::int64_t lb = x.cfg.layer_block_bytes(), b = x.cfg.kv_bytes_per_token_per_layer;
+  // only the persisted tokens: per (Full Block, layer), each chunk's token range
+  std::vector<std::tuple<std::int64_t, std::int64_t, std::int64_t>> ranges;  // (fb, tok a, tok z)
+  for (int ji : x.by_de[engine_]) {
+    const LoadJob& j = x.jobs[ji];
+    for (const auto& [t0, t1] : x.persist_chunks(j))
+      for (std::int64_t k = t0 / T; k < (t1 + T - 1) / T; ++k)
+        ranges.emplace_back(x.fb_of(j.traj, k), std::max(t0, k * T) - k * T, std::min(t1, (k + 1) * T) - k * T);
+  }
+  std::sort(ranges.begin(), ranges.end());
+  const char* base = static_cast<const char*>(host);
+  for (std::size_t i = 0; i < ranges.size();) {  // merge touching ranges of one block
+    auto [fb, a, z] = ranges[i];
+    std::size_t k = i + 1;
+    while (k < ranges.size() && std::get<0>(ranges[k]) == fb && std::get<1>(ranges[k]) <= z)
+      z = std::max(z, std::get<2>(ranges[k++]));
+    for (std::int32_t layer = 0; layer < x.cfg.n_layer; ++layer) {
+      const std::int64_t off = layer * lb + a * b;
+      persist_file_->write_bytes(fb, off, (z - a) * b, base + fb * fbb + off);
+    }
+    res.persist_write_bytes += (z - a) * b * x.cfg.n_layer;
+    i = k;
+  }
+  res.persist_write_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
 std::vector<std::uint8_t> EngineRuntime::read_persisted(std::int64_t fb, int layer) const {

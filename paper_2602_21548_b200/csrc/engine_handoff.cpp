@@ -290,6 +290,7 @@ StepResult EngineRuntime::run_step_handoff() {
   float ms = 0;
   check_cuda(cudaEventElapsedTime(&ms, start, static_cast<cudaEvent_t>(ev_end_)), "cudaEventElapsedTime");
   res.device_ms = ms;
+  persist_write(res);
   if (is_pe()) {  // per request: its prompt KV complete in the decode pool
     for (int ji : x.by_pe[engine_]) {
       float t = 0, tf = 0;

@@ -136,7 +136,8 @@ FullBlockFile::FullBlockFile(const std::string& path, const dp_kv_geom& g, std::
   if (n_records < 1) throw std::invalid_argument("FullBlockFile: n_records must be >= 1");
   record_bytes_ = static_cast<std::int64_t>(g.n_layer) * g.block_tokens * g.bytes_per_token_layer;
   stride_ = (record_bytes_ + kAlign - 1) / kAlign * kAlign;
-  fd_ = ::open(path.c_str(), create ? (O_RDWR | O_CREAT | O_TRUNC) : O_RDONLY, 0644);
+  fd_ = ::open(path.c_str(), create ? (O_RDWR | O_CREAT | O_TRUNC) : O_RDWR, 0644);
+  if (fd_ < 0 && !create) fd_ = ::open(path.c_str(), O_RDONLY);  // read-only tier: writes fail loudly
   if (fd_ < 0) io_error("cannot open", path);
   if (create) {
     if (::ftruncate(fd_, n_records_ * stride_) != 0) io_error("cannot size", path);
@@ -163,6 +164,18 @@ void FullBlockFile::write(std::int64_t record, const void* src) {
     const ssize_t n = ::pwrite(fd_, p + done, record_bytes_ - done, record * stride_ + done);
     if (n <= 0) io_error("short write to", path_);
     done += n;
+  }
+}
+
+void FullBlockFile::write_bytes(std::int64_t record, std::int64_t offset, std::int64_t n, const void* src) {
+  if (record < 0 || record >= n_records_ || offset < 0 || n < 0 || offset + n > record_bytes_)
+    throw std::out_of_range("FullBlockFile::write_bytes: range out of the record");
+  const char* p = static_cast<const char*>(src);
+  std::int64_t done = 0;
+  while (done < n) {
+    const ssize_t k = ::pwrite(fd_, p + done, n - done, record * stride_ + offset + done);
+    if (k <= 0) io_error("short write to", path_);
+    done += k;
   }
 }
 

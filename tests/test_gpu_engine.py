@@ -449,3 +449,54 @@ def test_buffer_bound_stalls(de_dev, k1):
     assert res[0].buffer_stalls + res[1].buffer_stalls > 0
     verify_counters(pe, xp, cfg)
     verify_pool(pe, xp, cfg)
+
+
+def test_persist_write_into_the_storage_tier(de_dev, tmp_path):
+    """PersistWrite (desim.cpp:764-771): after the step every Full Block the
+    DE's K4 persisted is written to its record of the storage-tier file, so a
+    later turn's StorageRead from the tier reads the generated tokens back.
+    The file starts with another seed's content: a persisted token range
+    equals the oracle's content, everything else is untouched."""
+    cfg = cluster(1, 1, L=3)
+    trajs = small_trace(count=5, turns=3, seed=13)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.handoff = True
+    opt.persist = True
+    probe = dp.build_exec_plan(cfg, trajs, planned, opt)
+    T, b, L = cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer, cfg.n_layer
+    path = str(tmp_path / "tier.bin")
+    f = dp.FullBlockFile(path, L, T, b, probe.store_fb, create=True, direct=False)
+    f.populate(SEED + 7, threads=4)
+    del f
+    opt.persist_path = path
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    rts = handoff_engines(xp, 2, [0, de_dev])
+    for rt in rts:
+        rt.reset_counters()
+    res = dp.run_step_all(rts)
+    assert res[1].persist_write_bytes > 0
+    f = dp.FullBlockFile(path, L, T, b, xp.store_fb, create=False, direct=False)
+    g = refpy.geom(L, T, b)
+    fbb, lb = L * T * b, T * b
+    persisted = {}
+    for i, job in enumerate(xp.jobs()):
+        traj, prompt, gen = job[1], job[14], xp.job_gen(i)
+        for k in range(prompt // T, -(-(prompt + gen) // T)):
+            a, z = max(prompt, k * T) - k * T, min(prompt + gen, (k + 1) * T) - k * T
+            persisted.setdefault(xp.fb_of(traj, k), []).append((a, z))
+    assert persisted
+    for fb, ranges in persisted.items():
+        rec = np.frombuffer(f.read(fb), dtype=np.uint8)[:fbb]
+        other = refpy.fill_store(g, SEED + 7, 1, fb0=fb)
+        want = refpy.fill_store(g, SEED, 1, fb0=fb)
+        for layer in range(L):
+            covered = np.zeros(T, dtype=bool)
+            for a, z in ranges:
+                covered[a:z] = True
+                off = layer * lb
+                assert np.array_equal(rec[off + a * b:off + z * b], want[off + a * b:off + z * b]), (fb, layer)
+            for t in np.nonzero(~covered)[0]:  # never persisted: the file's own bytes
+                off = layer * lb + t * b
+                assert np.array_equal(rec[off:off + b], other[off:off + b]), (fb, layer, t)
