@@ -333,6 +333,12 @@ int dp_h2d_layer_staged(dp_pool* pe, const dp_store* src, dp_stager* stager, con
                         int32_t n_jobs, dp_stream stream);
 int dp_h2d_push_staged(dp_pool* pe_view, const dp_store* de_src, dp_stager* stager, const dp_job* jobs,
                        int32_t n_jobs, dp_stream de_stream);
+/* The DE read path fused with DecodeH2D (dp_h2d_push_p2p_dual), staged: the
+ * copy engine into the ring, then the dual scatter stores each Layer Block to
+ * the PE pool over NVLink and to the DE's decode pool.  src_fb HOST-readable,
+ * dst_slot / de_slot device-readable; jobs move all layers. */
+int dp_h2d_push_dual_staged(dp_pool* pe_view, dp_pool* de_pool, const dp_store* de_src, dp_stager* stager,
+                            const dp_dual_job* jobs, int32_t n_jobs, dp_stream de_stream);
 
 /* Cap on the CTAs a K1/K2 launch on `device` may use (0 = default, 4 per SM).
  * The transfer is PCIe-bound, so a few CTAs keep the link full while leaving

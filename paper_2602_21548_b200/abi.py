@@ -129,6 +129,7 @@ def lib():
         "dp_stager_set_mode": ([P, ctypes.c_int32], ctypes.c_int),
         "dp_h2d_layer_staged": ([P, P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_h2d_push_staged": ([P, P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
+        "dp_h2d_push_dual_staged": ([P, P, P, P, ctypes.POINTER(DualJob), ctypes.c_int32, P], ctypes.c_int),
         "dp_stream_wait_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
         "dp_stream_write_counter": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, P], ctypes.c_int),
         "dp_decode_fill": ([P, ctypes.POINTER(SpanJob), ctypes.c_int32, ctypes.c_uint64, P], ctypes.c_int),
@@ -310,6 +311,11 @@ def h2d_layer_staged(pool, store, stager, jobs, n, stream=0):
 
 def h2d_push_staged(pool_view, store, stager, jobs, n, stream=0):
     return check(lib().dp_h2d_push_staged(pool_view.ptr, store.ptr, stager.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def push_dual_staged(pe_view, de_pool, store, stager, jobs, n, stream=0):
+    return check(lib().dp_h2d_push_dual_staged(pe_view.ptr, de_pool.ptr, store.ptr, stager.ptr, jobs, n,
+                                               ctypes.c_void_p(stream)))
 
 
 def device_numa_node(device):

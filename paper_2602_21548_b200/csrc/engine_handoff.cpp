@@ -241,8 +241,15 @@ StepResult EngineRuntime::run_step_handoff() {
                        d_dual_de_ + j.blk_off,
                        j.de_ticket,
                        0};
-        check(dp_h2d_push_p2p_dual(peers_[j.pe], pool_, store_, &dj, 1, s), "dp_h2d_push_p2p_dual");
-        ++res.launches;
+        if (x.opt.k2_mode == 2 && stager_) {  // staged: copy engine into the ring, then the dual scatter
+          dj.pe.src_fb = x.src_fb[engine_].data() + j.blk_off;
+          const std::int64_t l0 = stager_launches();
+          check(dp_h2d_push_dual_staged(peers_[j.pe], pool_, store_, stager_, &dj, 1, s), "dp_h2d_push_dual_staged");
+          res.launches += stager_launches() - l0;
+        } else {
+          check(dp_h2d_push_p2p_dual(peers_[j.pe], pool_, store_, &dj, 1, s), "dp_h2d_push_p2p_dual");
+          ++res.launches;
+        }
         continue;
       }
       // decode stream: once the request's whole prompt has landed, the

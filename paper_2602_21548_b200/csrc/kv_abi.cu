@@ -365,6 +365,11 @@ int64_t counters_offset(int64_t data_bytes) { return (data_bytes + 255) / 256 * 
 // the very launch of its producer when both share a GPU.
 int preload_kernels(int device);
 
+// The dual gather (DeToPe + the hit half of DecodeH2D) from any device-visible
+// Full-Block source: the DE's host store, or a stager ring.
+int launch_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* src, const dp_dual_job* jobs, int32_t n_jobs,
+                dp_stream stream, int ctas_override);
+
 int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
                   dp_stream stream, bool peer, int ctas_override = 0, bool stream_hint = false) {
   if (!pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0)
@@ -1351,6 +1356,15 @@ extern "C" {
 
 int dp_h2d_push_p2p_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* src,
                          const dp_dual_job* jobs, int32_t n_jobs, dp_stream stream) {
+  return launch_dual(pe_view, de_pool, src, jobs, n_jobs, stream, 0);
+}
+
+}  // extern "C"
+
+namespace {
+
+int launch_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* src, const dp_dual_job* jobs, int32_t n_jobs,
+                dp_stream stream, int ctas_override) {
   if (!pe_view || !de_pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0)
     return fail(DP_EINVAL, "push_p2p_dual: null argument");
   if (pe_view->owner) return fail(DP_EINVAL, "push_p2p_dual: PE destination must be a peer view");
@@ -1377,7 +1391,7 @@ int dp_h2d_push_p2p_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* src
   p.block_tokens = g.block_tokens;
   p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
   const int dev_cap = de_pool->device < kMaxDevices ? g_gather_ctas[de_pool->device].load() : 0;
-  const int grid_cap = dev_cap > 0 ? dev_cap : sm_count(de_pool->device) * 4;
+  const int grid_cap = ctas_override > 0 ? ctas_override : dev_cap > 0 ? dev_cap : sm_count(de_pool->device) * 4;
   auto s = static_cast<cudaStream_t>(stream);
   for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_DUAL_JOBS_PER_LAUNCH) {
     const int32_t nj = std::min<int32_t>(DP_MAX_DUAL_JOBS_PER_LAUNCH, n_jobs - j0);
@@ -1405,6 +1419,10 @@ int dp_h2d_push_p2p_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* src
   }
   return DP_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job* jobs,
                        int32_t n_jobs, uint64_t seed, int32_t timeout_ms, dp_stream stream) {
@@ -1911,6 +1929,31 @@ void stager_free(dp_stager* st) {
   delete st;
 }
 
+// Copy-engine leg of blocks [k0, k1) of `job` into ring positions base..:
+// runs of consecutive storage Full Blocks as 1D copies, a partial last block
+// as a 2D copy of its valid rows (exactly the hit bytes cross PCIe).
+int stage_copy(dp_stager* st, const dp_store* src, const dp_job& job, int32_t k0, int32_t k1, int64_t base) {
+  const dp_kv_geom& g = src->geom;
+  const int64_t T = g.block_tokens, b = g.bytes_per_token_layer;
+  const int64_t lb = T * b, fbb = lb * g.n_layer;
+  const bool last_partial = k1 == job.n_blk && job.n_tokens % T != 0;
+  const int32_t full_end = last_partial ? k1 - 1 : k1;
+  for (int32_t k = k0; k < full_end;) {
+    int32_t run = 1;
+    while (k + run < full_end && job.src_fb[k + run] == job.src_fb[k] + run) ++run;
+    DP_CUDA(cudaMemcpyAsync(st->ring.host + (base + (k - k0)) * fbb, src->host + job.src_fb[k] * fbb, run * fbb,
+                            cudaMemcpyHostToDevice, st->copy));
+    k += run;
+  }
+  if (last_partial) {
+    const int32_t k = k1 - 1;
+    const int64_t ntok = job.n_tokens - static_cast<int64_t>(k) * T;
+    DP_CUDA(cudaMemcpy2DAsync(st->ring.host + (base + (k - k0)) * fbb, lb, src->host + job.src_fb[k] * fbb, lb,
+                              ntok * b, g.n_layer, cudaMemcpyHostToDevice, st->copy));
+  }
+  return DP_OK;
+}
+
 // One staged transfer.  The jobs' src_fb arrays are HOST-readable (the copies
 // are planned on the host), dst_slot device-readable (the kernel reads it).
 int staged_transfer(const char* who, dp_pool* pool, const dp_store* src, dp_stager* st, const dp_job* jobs,
@@ -2010,21 +2053,7 @@ int staged_transfer(const char* who, dp_pool* pool, const dp_store* src, dp_stag
       }
       const int32_t k1 = static_cast<int32_t>(std::min<int64_t>(job.n_blk, k0 + (st->seg_fb - used)));
       const int64_t base = st->seg * st->seg_fb + used;  // ring position of block k0
-      const bool last_partial = k1 == job.n_blk && job.n_tokens % T != 0;
-      const int32_t full_end = last_partial ? k1 - 1 : k1;
-      for (int32_t k = k0; k < full_end;) {  // runs of consecutive storage Full Blocks
-        int32_t run = 1;
-        while (k + run < full_end && job.src_fb[k + run] == job.src_fb[k] + run) ++run;
-        DP_CUDA(cudaMemcpyAsync(st->ring.host + (base + (k - k0)) * fbb, src->host + job.src_fb[k] * fbb,
-                                run * fbb, cudaMemcpyHostToDevice, st->copy));
-        k += run;
-      }
-      if (last_partial) {  // only the valid tokens of every layer
-        const int32_t k = k1 - 1;
-        const int64_t ntok = job.n_tokens - static_cast<int64_t>(k) * T;
-        DP_CUDA(cudaMemcpy2DAsync(st->ring.host + (base + (k - k0)) * fbb, lb, src->host + job.src_fb[k] * fbb,
-                                  lb, ntok * b, g.n_layer, cudaMemcpyHostToDevice, st->copy));
-      }
+      if (int rc = stage_copy(st, src, job, k0, k1, base)) return rc;
       const int64_t tok0 = static_cast<int64_t>(k0) * T;
       sub.push_back(dp_job{st->iota + base, job.dst_slot + k0, std::min<int64_t>(job.n_tokens, k1 * T) - tok0,
                            k1 - k0, 0, g.n_layer, job.ticket});
@@ -2109,6 +2138,72 @@ int dp_h2d_layer_staged(dp_pool* pe, const dp_store* src, dp_stager* st, const d
 int dp_h2d_push_staged(dp_pool* pe_view, const dp_store* de_src, dp_stager* st, const dp_job* jobs,
                        int32_t n_jobs, dp_stream de_stream) {
   return staged_transfer("h2d_push_staged", pe_view, de_src, st, jobs, n_jobs, de_stream, /*peer=*/true);
+}
+
+int dp_h2d_push_dual_staged(dp_pool* pe_view, dp_pool* de_pool, const dp_store* de_src, dp_stager* st,
+                            const dp_dual_job* jobs, int32_t n_jobs, dp_stream de_stream) {
+  if (!pe_view || !de_pool || !de_src || !st || (n_jobs > 0 && !jobs) || n_jobs < 0)
+    return fail(DP_EINVAL, "push_dual_staged: null argument");
+  if (de_pool->device != st->device || de_src->device != st->device)
+    return fail(DP_EINVAL, "push_dual_staged: decode pool, store and stager must be on one device");
+  if (!geom_equal(st->geom, de_src->geom)) return fail(DP_EINVAL, "push_dual_staged: geometry differs");
+  const dp_kv_geom& g = de_src->geom;
+  const int64_t T = g.block_tokens;
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    const dp_job& job = jobs[j].pe;
+    if (job.n_tokens < 0 || job.n_blk != (job.n_tokens + T - 1) / T || job.layer_begin != 0 ||
+        job.layer_end != g.n_layer || (job.n_blk > 0 && (!job.src_fb || !job.dst_slot || !jobs[j].de_slot)))
+      return fail(DP_EINVAL, "push_dual_staged: job " + std::to_string(j) + " out of range (all layers)");
+    for (int32_t k = 0; k < job.n_blk; ++k)
+      if (job.src_fb[k] < 0 || job.src_fb[k] >= de_src->n_fb)
+        return fail(DP_EINVAL, "push_dual_staged: source block out of range");
+  }
+  DeviceGuard guard(st->device);
+  auto s = static_cast<cudaStream_t>(de_stream);
+  std::vector<dp_dual_job> sub;
+  int64_t used = 0;
+  bool open = false;
+  auto flush = [&]() -> int {
+    if (!open) return DP_OK;
+    const int seg = st->seg;
+    DP_CUDA(cudaEventRecord(st->ev_copied[seg], st->copy));
+    DP_CUDA(cudaStreamWaitEvent(s, st->ev_copied[seg], 0));
+    if (!sub.empty()) {
+      if (int rc = launch_dual(pe_view, de_pool, &st->ring, sub.data(), static_cast<int32_t>(sub.size()), de_stream,
+                               st->ctas))
+        return rc;
+      ++st->launches;
+    }
+    DP_CUDA(cudaEventRecord(st->ev_free[seg], s));
+    st->seg = (seg + 1) % kStageSegs;
+    sub.clear();
+    used = 0;
+    open = false;
+    return DP_OK;
+  };
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    const dp_dual_job& dj = jobs[j];
+    for (int32_t k0 = 0; k0 < dj.pe.n_blk;) {
+      if (open && (used == st->seg_fb || sub.size() == DP_MAX_DUAL_JOBS_PER_LAUNCH))
+        if (int rc = flush()) return rc;
+      if (!open) {
+        DP_CUDA(cudaStreamWaitEvent(st->copy, st->ev_free[st->seg], 0));
+        open = true;
+      }
+      const int32_t k1 = static_cast<int32_t>(std::min<int64_t>(dj.pe.n_blk, k0 + (st->seg_fb - used)));
+      const int64_t base = st->seg * st->seg_fb + used;
+      if (int rc = stage_copy(st, de_src, dj.pe, k0, k1, base)) return rc;
+      dp_dual_job part = dj;
+      part.pe = dp_job{st->iota + base, dj.pe.dst_slot + k0,
+                       std::min<int64_t>(dj.pe.n_tokens, static_cast<int64_t>(k1) * T) - static_cast<int64_t>(k0) * T,
+                       k1 - k0, 0, g.n_layer, dj.pe.ticket};
+      part.de_slot = dj.de_slot + k0;
+      sub.push_back(part);
+      used += k1 - k0;
+      k0 = k1;
+    }
+  }
+  return flush();
 }
 
 }  // extern "C"

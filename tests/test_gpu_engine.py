@@ -212,9 +212,10 @@ def handoff_engines(xp, n, devices=None):
     return rts
 
 
-@pytest.mark.parametrize("policy,tight,layer_gate", [("dual_path", False, 0), ("dual_path", True, 0),
-                                                     ("pe_only", True, 0), ("dual_path", True, 1)])
-def test_handoff_1p1d(de_dev, policy, tight, layer_gate):
+@pytest.mark.parametrize("policy,tight,layer_gate,staged", [("dual_path", False, 0, False), ("dual_path", True, 0, False),
+                                                            ("pe_only", True, 0, False), ("dual_path", True, 1, False),
+                                                            ("dual_path", True, 0, True)])
+def test_handoff_1p1d(de_dev, policy, tight, layer_gate, staged):
     cfg = cluster(1, 1, L=6)
     trajs = small_trace(count=8, turns=5, seed=6)
     planned = dp.plan(cfg, trajs, policy=policy, **STORAGE_BOUND)
@@ -222,6 +223,9 @@ def test_handoff_1p1d(de_dev, policy, tight, layer_gate):
     opt.seed = SEED
     opt.handoff = True
     opt.k3_layer_gate = layer_gate
+    if staged:  # staged K1 and the staged dual gather (ring smaller than a request)
+        opt.k1_mode, opt.k2_mode = 3, 2
+        opt.stage_ring_bytes = 16 * 6 * 64 * 576 * 4
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     if tight:
         opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots

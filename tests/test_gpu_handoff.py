@@ -255,3 +255,42 @@ def test_decode_fill_then_persist_d2h(gpus, L, T, b, P, gen):
     finally:
         target.close()
         pool.close()
+
+
+@pytest.mark.parametrize("L,T,b,C", [(8, 64, 576, 64 * 9 + 5), (4, 64, 4096, 64 * 5), (61, 64, 576, 64 * 3 + 1)])
+def test_dual_staged(de_dev, L, T, b, C):
+    """The DE read path fused with DecodeH2D, staged (copy engine into the
+    ring, then the dual scatter): PE pool and decode pool both hold the hit
+    KV, both rows released, with a ring smaller than the request."""
+    import torch
+    g = abi.geom(L, T, b)
+    nh = -(-C // T)
+    s_de = de_stream(de_dev)
+    st_de = abi.Store(de_dev, g, 40, SEED)
+    pe_pool = abi.Pool(0, g, 32, 1)
+    de_pool = abi.Pool(de_dev, g, 32, 1)
+    pe_view = pe_pool.peer_view(de_dev)
+    stager = abi.Stager(de_dev, g, 3 * L * T * b * 4)  # 3 Full Blocks per segment
+    try:
+        fbs = (np.arange(nh) * 2 + 1).astype(np.int64)  # non-consecutive: one copy per block
+        ps = np.arange(3, 3 + nh, dtype=np.int32)
+        ds = np.arange(20, 20 + nh, dtype=np.int32)[::-1].copy()
+        keep = [fbs, dev(ps, de_dev, np.int32), dev(ds, de_dev, np.int32)]
+        dj = (abi.DualJob * 1)()
+        dj[0].pe = abi.Job(fbs.ctypes.data, keep[1].data_ptr(), C, nh, 0, L, 0)
+        dj[0].de_slot = keep[2].data_ptr()
+        dj[0].de_ticket = 0
+        abi.push_dual_staged(pe_view, de_pool, st_de, stager, dj, 1, s_de)
+        sync_all()
+        gr = refpy.geom(L, T, b)
+        check_prompt(pe_pool, gr, fbs, ps, C, T, b, L)
+        check_prompt(de_pool, gr, fbs, ds, C, T, b, L)
+        items = abi.layer_items(g, nh)
+        abi.wait_layer(pe_pool, 0, L, items * L, timeout_ms=2000)
+        abi.wait_layer(de_pool, 0, L, items * L, timeout_ms=2000)
+        sync_all()
+        assert abi.wait_status(pe_pool) == abi.DP_OK and abi.wait_status(de_pool) == abi.DP_OK
+        assert stager.launches() >= 2
+    finally:
+        for x in (stager, pe_view, de_pool, pe_pool, st_de):
+            x.close()
