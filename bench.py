@@ -187,11 +187,11 @@ def config_dict(kind, sessions, P, D, policy, shape, cap_gbps, stats, extra=None
 
 
 def buffer_bytes(shape):
-    """Host staging per engine (pe_buffer_bytes = de_buffer_bytes): the paper's
-    DRAM allocation per 8-GPU node (80 GB for DeepSeek, 320 GB for Qwen 32B,
-    PAPER.md:862-863) shared by its 8 engines.  The planner's admissions and
-    the executor's reads (BufferGate) both honour it."""
-    return int((320e9 if shape["b"] >= 4096 else 80e9) / 8)
+    """Host staging per engine (pe_buffer_bytes = de_buffer_bytes): the
+    reference's own preset, 128 GiB per node (proj/src/config.cpp:57-58), one
+    node per engine here (g = 1).  The planner's admissions and the executor's
+    reads (BufferGate) both honour it."""
+    return 1 << 37
 
 
 def golden_key(kind, sessions, P, D, policy, cap_gbps, link_bps):

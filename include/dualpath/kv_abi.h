@@ -286,6 +286,11 @@ typedef struct dp_attend_item {
  * work-queue counter). */
 int dp_prefill_attend(const dp_pool* pe_pool, int32_t layer, const dp_attend_item* items,
                       int32_t n_items, uint64_t seed, dp_stream stream);
+/* The same, then *done = 1 (gpu-scope release by the last CTA out; a stream
+ * write when there is nothing to compute): the layer's "computed" flag a
+ * layerwise K3 gates on (desim.cpp:630-640). */
+int dp_prefill_attend_signal(const dp_pool* pe_pool, int32_t layer, const dp_attend_item* items,
+                             int32_t n_items, uint64_t seed, uint32_t* done, dp_stream stream);
 /* Cap on the CTAs of a K5 launch on `device` (0 = default: every SM). */
 int dp_set_attend_ctas(int device, int32_t ctas);
 

@@ -143,6 +143,8 @@ def lib():
         "dp_prefill_attend": ([P, ctypes.c_int32, ctypes.POINTER(AttendItem), ctypes.c_int32,
                                ctypes.c_uint64, P], ctypes.c_int),
         "dp_set_attend_ctas": ([ctypes.c_int, ctypes.c_int32], ctypes.c_int),
+        "dp_prefill_attend_signal": ([P, ctypes.c_int32, ctypes.POINTER(AttendItem), ctypes.c_int32,
+                                      ctypes.c_uint64, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

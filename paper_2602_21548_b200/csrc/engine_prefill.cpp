@@ -203,11 +203,19 @@ void EngineRuntime::enqueue_forward(int f, StepResult& res) {
             "dp_wait_tickets (forward gate)");
       ++res.launches;
     }
-    check(dp_prefill_attend(pool_, layer, att.data(), static_cast<int32_t>(att.size()), x.opt.seed, c),
+    // layerwise handoff: K5's last CTA out flags "forward f computed layer l"
+    // (row fwd_row0_ + f of the pool's counters), which K3 gates on
+    std::uint32_t* done = nullptr;
+    if (layerwise_handoff()) {
+      void* base = nullptr;
+      std::uint32_t* ctr = nullptr;
+      std::int64_t bytes = 0;
+      check(dp_pool_info(pool_, &base, &ctr, &bytes), "dp_pool_info");
+      done = ctr + static_cast<std::int64_t>(fwd_row0_ + f) * (L + 1) + layer;
+    }
+    check(dp_prefill_attend_signal(pool_, layer, att.data(), static_cast<int32_t>(att.size()), x.opt.seed, done, c),
           "dp_prefill_attend");
     res.launches += (work + DP_MAX_ATTEND_ITEMS_PER_LAUNCH - 1) / DP_MAX_ATTEND_ITEMS_PER_LAUNCH;
-    if (layerwise_handoff())  // forward f computed layer l: K3 may push it
-      check(dp_stream_write_counter(pool_, fwd_row0_ + f, layer, 1, c), "dp_stream_write_counter");
   }
   check_cuda(cudaEventRecord(static_cast<cudaEvent_t>(ev_fwd_[f]), c), "cudaEventRecord");
   if (!x.handoff)  // with the handoff, K3 (after the forward) marks the rows

@@ -1281,7 +1281,7 @@ __global__ void __launch_bounds__(kThreads, 6) kv_prefill_handoff(const __grid_c
             atomicExch_system(p.err_flag, 1);
             break;
           }
-          __nanosleep(256);
+          __nanosleep(1024);  // a layer of compute takes tens of microseconds
         }
       }
       __syncthreads();
@@ -1662,6 +1662,7 @@ std::mutex g_attend_mu;
 struct AttendParams {
   const char* pool;
   uint32_t* ctr;  // {next unit, CTAs done}: zero at launch, zeroed again by the last CTA
+  uint32_t* done; // or null: set to 1 by the last CTA out (the layer's "computed" flag)
   int64_t bpt;
   int64_t lb_bytes;
   int64_t layer_off;  // layer * n_slots * lb_bytes
@@ -1811,6 +1812,10 @@ __global__ void __maxnreg__(96) kv_prefill_attend(const __grid_constant__ Attend
   if (tid == 0 && atomicAdd(p.ctr + 1, 1u) == gridDim.x - 1) {  // the last CTA out resets
     p.ctr[0] = 0;
     p.ctr[1] = 0;
+    if (p.done) {  // every unit of the layer is done: release its flag
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.done), "r"(1u) : "memory");
+    }
   }
 }
 
@@ -1826,6 +1831,11 @@ int dp_set_attend_ctas(int device, int32_t ctas) {
 
 int dp_prefill_attend(const dp_pool* pool, int32_t layer, const dp_attend_item* items, int32_t n_items,
                       uint64_t seed, dp_stream stream) {
+  return dp_prefill_attend_signal(pool, layer, items, n_items, seed, nullptr, stream);
+}
+
+int dp_prefill_attend_signal(const dp_pool* pool, int32_t layer, const dp_attend_item* items, int32_t n_items,
+                             uint64_t seed, uint32_t* done, dp_stream stream) {
   if (!pool || (n_items > 0 && !items) || n_items < 0) return fail(DP_EINVAL, "prefill_attend: null argument");
   if (!pool->owner) return fail(DP_EINVAL, "prefill_attend: the PE pool must be local");
   const dp_kv_geom& g = pool->geom;
@@ -1858,8 +1868,10 @@ int dp_prefill_attend(const dp_pool* pool, int32_t layer, const dp_attend_item* 
   const int grid_cap = cap > 0 ? cap : sm_count(pool->device) * 2;
   const int64_t max_tokens = static_cast<int64_t>(pool->n_slots) * g.block_tokens;
   auto s = static_cast<cudaStream_t>(stream);
+  bool signalled = false;
   for (int32_t i0 = 0; i0 < n_items; i0 += DP_MAX_ATTEND_ITEMS_PER_LAUNCH) {
     const int32_t ni = std::min<int32_t>(DP_MAX_ATTEND_ITEMS_PER_LAUNCH, n_items - i0);
+    p.done = i0 + ni >= n_items ? done : nullptr;  // the call's last launch signals
     p.n_jobs = 0;
     int64_t units = 0;
     for (int32_t i = 0; i < ni; ++i) {
@@ -1879,6 +1891,13 @@ int dp_prefill_attend(const dp_pool* pool, int32_t layer, const dp_attend_item* 
     if (units == 0) continue;
     kv_prefill_attend<<<static_cast<int>(std::min<int64_t>(units, grid_cap)), kThreads, kAttSmem, s>>>(p);
     DP_CUDA(cudaGetLastError());
+    signalled = signalled || p.done != nullptr;
+  }
+  if (done && !signalled) {  // nothing to compute in the last launch: a stream-ordered write instead
+    const WriteValue32Fn wv = write_value32();
+    if (!wv) return fail(DP_ECUDA, "prefill_attend: cuStreamWriteValue32 unavailable");
+    if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(done), 1, 0) != CUDA_SUCCESS)
+      return fail(DP_ECUDA, "prefill_attend: cuStreamWriteValue32 failed");
   }
   return DP_OK;
 }

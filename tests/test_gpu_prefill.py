@@ -289,3 +289,35 @@ def test_prefill_with_staged_loads(gpus, tight):
         r = eng.run_step()
         assert r.bytes_read == xp.hit_bytes
         check_digests(eng, cfg, planned, xp)
+
+
+def test_attend_signal_sets_the_layer_flag(gpus):
+    """dp_prefill_attend_signal: the layer's 'computed' flag is 1 after the
+    call, released by K5's last CTA, or by a stream write when the call has
+    nothing to compute (the layerwise handoff's gate)."""
+    import ctypes
+    import torch
+    L, T, b = 2, 64, 576
+    g = abi.geom(L, T, b)
+    st = abi.Store(0, g, 4, SEED)
+    pool = abi.Pool(0, g, 8, 1)
+    try:
+        slots = dev([0, 1], np.int32)
+        fbs = dev([0, 1], np.int64)
+        abi.h2d_layer_gather(pool, st, abi.make_jobs([(fbs.data_ptr(), slots.data_ptr(), 100, 2, 0, L, -1)]), 1)
+        flags = torch.zeros(2, dtype=torch.int32, device="cuda:0")
+        digest = torch.zeros(L, dtype=torch.int64, device="cuda:0")
+        items = (abi.AttendItem * 1)()
+        items[0] = abi.AttendItem(slots.data_ptr(), 100, 0, 40, digest.data_ptr(), 3, 0)
+        abi.check(abi.lib().dp_prefill_attend_signal(pool.ptr, 0, items, 1, SEED, flags.data_ptr(), None))
+        empty = (abi.AttendItem * 1)()
+        empty[0] = abi.AttendItem(slots.data_ptr(), 0, 0, 40, digest.data_ptr(), 3, 0)  # no cached keys
+        abi.check(abi.lib().dp_prefill_attend_signal(pool.ptr, 1, empty, 1, SEED,
+                                                     flags.data_ptr() + 4, None))
+        torch.cuda.synchronize()
+        assert flags.tolist() == [1, 1]
+        want = refpy.attend_digest(refpy.geom(L, T, b), SEED, [0, 1], 100, 3, 0, 0, 40)
+        assert int(digest[0].item()) & (2 ** 64 - 1) == want
+    finally:
+        pool.close()
+        st.close()

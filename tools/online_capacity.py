@@ -85,15 +85,15 @@ def capacity(a, cfg, trajs, policy, devices):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--pd", default="1:1")
-    ap.add_argument("--sessions", type=int, default=24)
+    ap.add_argument("--sessions", type=int, default=96)
     ap.add_argument("--turns", type=int, default=6)
     ap.add_argument("--cap-gbps", type=float, default=6.25)
-    ap.add_argument("--slo", type=float, default=2.0, help="load-TTFT SLO, seconds")
+    ap.add_argument("--slo", type=float, default=0.3, help="load-TTFT SLO, seconds")
     ap.add_argument("--decode-ms", type=float, default=1.0, help="emulated decode per generated token")
     ap.add_argument("--steady-window", type=float, default=4.0)
     ap.add_argument("--steady-lookback", type=float, default=12.0)
-    ap.add_argument("--aps-start", type=float, default=0.5)
-    ap.add_argument("--aps-max", type=float, default=64.0)
+    ap.add_argument("--aps-start", type=float, default=4.0)
+    ap.add_argument("--aps-max", type=float, default=256.0)
     ap.add_argument("--bisect", type=int, default=3)
     ap.add_argument("--alpha", type=int, default=100000)
     ap.add_argument("--beta", type=int, default=500000)
