@@ -55,6 +55,10 @@ struct ExecOptions {
   // the link's full rate, a small scatter kernel (stage_ctas CTAs) lands them
   // in the pool's layer planes (dp_h2d_layer_staged)
   std::int32_t k1_mode = 0;
+  // copy-engine modes (k1_mode / k2_mode 1): release a job's counters once
+  // after its last layer (true) or after every layer (false; idles the copy
+  // engine once per layer)
+  bool copy_release_per_job = true;
   // DE-path loads (K2): 0 = SM gather pushing over NVLink, 1 = the DE's copy
   // engine writing into the PE pool (no SMs on the DE: its decode is untouched)
   // 2 = staged: the DE's copy engine into its HBM ring, then the scatter kernel

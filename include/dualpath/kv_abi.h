@@ -311,6 +311,13 @@ int dp_h2d_layer_copy(dp_pool* pe, const dp_store* src, const dp_job* jobs, int3
  * the PE's landed counters.  Block arrays HOST-readable, as above. */
 int dp_h2d_push_copy(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs, int32_t n_jobs,
                      dp_stream de_stream);
+/* The same two, releasing each job's counters once after its last layer
+ * (a stream write waits for the copies before it: per-layer releases idle
+ * the copy engine once per layer).  Consumers see all layers land at once. */
+int dp_h2d_layer_copy_job(dp_pool* pe, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
+                          dp_stream stream);
+int dp_h2d_push_copy_job(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs, int32_t n_jobs,
+                         dp_stream de_stream);
 
 /* Staged K1 / K2: the copy engine moves whole Full-Block runs host -> an HBM
  * staging ring at the link's full rate (1D copies of contiguous runs, a 2D

@@ -101,6 +101,8 @@ def lib():
         "dp_h2d_push_p2p_layer": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_h2d_layer_copy": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_h2d_push_copy": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
+        "dp_h2d_layer_copy_job": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
+        "dp_h2d_push_copy_job": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_h2d_push_p2p_dual": ([P, P, P, ctypes.POINTER(DualJob), ctypes.c_int32, P], ctypes.c_int),
         "dp_prefill_handoff": ([P, P, ctypes.POINTER(HandoffJob), ctypes.c_int32, ctypes.c_uint64,
                                 ctypes.c_int32, P], ctypes.c_int),
@@ -349,6 +351,15 @@ def h2d_push_p2p_layer(pool_view, store, jobs, n, stream=0):
 def h2d_layer_copy(pool, store, jobs, n, stream=0):
     """K1 on the copy engine; jobs' block arrays must be host memory."""
     check(lib().dp_h2d_layer_copy(pool.ptr, store.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def h2d_layer_copy_job(pool, store, jobs, n, stream=0):
+    """K1 on the copy engine, counters released once per job."""
+    check(lib().dp_h2d_layer_copy_job(pool.ptr, store.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def h2d_push_copy_job(pool_view, store, jobs, n, stream=0):
+    check(lib().dp_h2d_push_copy_job(pool_view.ptr, store.ptr, jobs, n, ctypes.c_void_p(stream)))
 
 
 def h2d_push_copy(pool_view, store, jobs, n, stream=0):

@@ -425,6 +425,7 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("stage_ring_bytes", &dualpath::ExecOptions::stage_ring_bytes)
       .def_readwrite("stage_ctas", &dualpath::ExecOptions::stage_ctas)
       .def_readwrite("stage_scatter", &dualpath::ExecOptions::stage_scatter)
+      .def_readwrite("copy_release_per_job", &dualpath::ExecOptions::copy_release_per_job)
       .def_readwrite("stage_push_ctas", &dualpath::ExecOptions::stage_push_ctas)
       .def_readwrite("handoff", &dualpath::ExecOptions::handoff)
       .def_readwrite("de_pool_slots", &dualpath::ExecOptions::de_pool_slots)

@@ -401,8 +401,9 @@ StepResult EngineRuntime::run_step() {
     const auto n = static_cast<int32_t>(batch.size());
     int rc;
     const char* what;
+    const bool per_job = x.opt.copy_release_per_job;
     if (batch_pe != engine_ && k2_ce) {
-      rc = dp_h2d_push_copy(dst, store_, batch.data(), n, s);
+      rc = per_job ? dp_h2d_push_copy_job(dst, store_, batch.data(), n, s) : dp_h2d_push_copy(dst, store_, batch.data(), n, s);
       what = "dp_h2d_push_copy";
     } else if (batch_pe != engine_ && k2_st) {
       rc = dp_h2d_push_staged(dst, store_, stager_, batch.data(), n, s);
@@ -414,7 +415,7 @@ StepResult EngineRuntime::run_step() {
       rc = dp_h2d_push_p2p_layer(dst, store_, batch.data(), n, s);
       what = "dp_h2d_push_p2p_layer";
     } else if (k1_ce) {
-      rc = dp_h2d_layer_copy(dst, store_, batch.data(), n, s);
+      rc = per_job ? dp_h2d_layer_copy_job(dst, store_, batch.data(), n, s) : dp_h2d_layer_copy(dst, store_, batch.data(), n, s);
       what = "dp_h2d_layer_copy";
     } else {
       rc = dp_h2d_layer_gather(dst, store_, batch.data(), n, s);

@@ -157,7 +157,9 @@ StepResult EngineRuntime::run_step_handoff() {
         if (x.opt.k1_mode == 1) {
           job.src_fb = x.src_fb[engine_].data() + j.blk_off;
           job.dst_slot = x.slots[engine_].data() + j.blk_off;
-          check(dp_h2d_layer_copy(pool_, store_, &job, 1, s), "dp_h2d_layer_copy");
+          check(x.opt.copy_release_per_job ? dp_h2d_layer_copy_job(pool_, store_, &job, 1, s)
+                                           : dp_h2d_layer_copy(pool_, store_, &job, 1, s),
+                "dp_h2d_layer_copy");
         } else if (x.opt.k1_mode == 3 && stager_) {
           job.src_fb = x.src_fb[engine_].data() + j.blk_off;
           job.dst_slot = stage_slots() + j.blk_off;

@@ -110,7 +110,9 @@ StepResult EngineRuntime::run_step_prefill(bool loads) {
       if (batch.empty()) return;
       const auto n = static_cast<int32_t>(batch.size());
       if (k1_ce) {
-        check(dp_h2d_layer_copy(pool_, store_, batch.data(), n, s), "dp_h2d_layer_copy");
+        check(x.opt.copy_release_per_job ? dp_h2d_layer_copy_job(pool_, store_, batch.data(), n, s)
+                                         : dp_h2d_layer_copy(pool_, store_, batch.data(), n, s),
+              "dp_h2d_layer_copy");
       } else if (k1_st) {
         check(dp_h2d_layer_staged(pool_, store_, stager_, batch.data(), n, s), "dp_h2d_layer_staged");
       } else {

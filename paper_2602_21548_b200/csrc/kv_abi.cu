@@ -823,7 +823,7 @@ namespace {
 // destination (pool and counters) is the PE's memory over NVLink and the
 // stream is the DE's.
 int copy_transfer(const char* who, dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
-                  dp_stream stream, bool peer) {
+                  dp_stream stream, bool peer, bool per_layer = true) {
   const std::string w(who);
   if (!pool || !src || (n_jobs > 0 && !jobs) || n_jobs < 0) return fail(DP_EINVAL, w + ": null argument");
   if (!peer && !pool->owner) return fail(DP_EINVAL, w + ": destination must be the local PE pool");
@@ -882,12 +882,24 @@ int copy_transfer(const char* who, dp_pool* pool, const dp_store* src, const dp_
                                 src->host + job.src_fb[k] * fbb + layer * lb, bytes,
                                 cudaMemcpyHostToDevice, s));
       }
-      if (job.ticket >= 0) {
-        const uint32_t per_layer = static_cast<uint32_t>(job.n_blk) * items;
-        if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + layer), per_layer, 0) !=
+      if (job.ticket >= 0 && per_layer) {
+        const uint32_t n_items = static_cast<uint32_t>(job.n_blk) * items;
+        if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + layer), n_items, 0) !=
                 CUDA_SUCCESS ||
             wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + g.n_layer),
-               per_layer * static_cast<uint32_t>(layer - job.layer_begin + 1), 0) != CUDA_SUCCESS)
+               n_items * static_cast<uint32_t>(layer - job.layer_begin + 1), 0) != CUDA_SUCCESS)
+          return fail(DP_ECUDA, w + ": cuStreamWriteValue32 failed");
+      }
+    }
+    if (job.ticket >= 0 && !per_layer) {
+      // one release per job: every layer's counter, then the all-layer column
+      // (each stream write waits for the copies before it, so per-layer writes
+      // would idle the copy engine once per layer)
+      const uint32_t n_items = static_cast<uint32_t>(job.n_blk) * items;
+      for (int32_t layer = job.layer_begin; layer <= job.layer_end; ++layer) {
+        const bool all = layer == job.layer_end;
+        if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + (all ? g.n_layer : layer)),
+               all ? n_items * static_cast<uint32_t>(job.layer_end - job.layer_begin) : n_items, 0) != CUDA_SUCCESS)
           return fail(DP_ECUDA, w + ": cuStreamWriteValue32 failed");
       }
     }
@@ -905,6 +917,17 @@ int dp_h2d_layer_copy(dp_pool* pool, const dp_store* src, const dp_job* jobs, in
 int dp_h2d_push_copy(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs, int32_t n_jobs,
                      dp_stream de_stream) {
   return copy_transfer("h2d_push_copy", pe_view, de_src, jobs, n_jobs, de_stream, /*peer=*/true);
+}
+
+int dp_h2d_layer_copy_job(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_t n_jobs,
+                          dp_stream stream) {
+  return copy_transfer("h2d_layer_copy_job", pool, src, jobs, n_jobs, stream, /*peer=*/false, /*per_layer=*/false);
+}
+
+int dp_h2d_push_copy_job(dp_pool* pe_view, const dp_store* de_src, const dp_job* jobs, int32_t n_jobs,
+                         dp_stream de_stream) {
+  return copy_transfer("h2d_push_copy_job", pe_view, de_src, jobs, n_jobs, de_stream, /*peer=*/true,
+                       /*per_layer=*/false);
 }
 
 int dp_stream_wait_counter(const dp_pool* pool, int32_t ticket, int32_t layer, uint32_t target,

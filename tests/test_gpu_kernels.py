@@ -220,7 +220,8 @@ def test_k2_push_p2p_parity(de_dev, L, T, b):
 
 
 @pytest.mark.parametrize("L,T,b", [(61, 64, 576), (4, 64, 4096), (3, 16, 1024)])
-def test_k1_copy_engine_parity(gpus, L, T, b):
+@pytest.mark.parametrize("per_job", [False, True])
+def test_k1_copy_engine_parity(gpus, L, T, b, per_job):
     """K1 on the copy engine (dp_h2d_layer_copy): strided 2D copies of block
     runs + fenced counter writes; same bytes and counters as the kernel."""
     rng = np.random.default_rng(21)
@@ -245,7 +246,7 @@ def test_k1_copy_engine_parity(gpus, L, T, b):
             keep += [fbs, slots]
             specs.append((fbs.ctypes.data, slots.ctypes.data, ntok, nblk, 0, L, t))
             plain.append((fbs, slots, ntok, 0, L))
-        abi.h2d_layer_copy(pool, st, abi.make_jobs(specs), len(specs))
+        (abi.h2d_layer_copy_job if per_job else abi.h2d_layer_copy)(pool, st, abi.make_jobs(specs), len(specs))
         for t, (fbs, slots, ntok, l0, l1) in enumerate(plain):
             items = abi.layer_items(g, len(slots))
             abi.wait_layer(pool, t, L, items * L, timeout_ms=5000)
@@ -261,7 +262,8 @@ def test_k1_copy_engine_parity(gpus, L, T, b):
 
 
 @pytest.mark.parametrize("L,T,b", [(61, 64, 576), (4, 64, 4096), (3, 16, 1024)])
-def test_k2_copy_engine_parity(de_dev, L, T, b):
+@pytest.mark.parametrize("per_job", [False, True])
+def test_k2_copy_engine_parity(de_dev, L, T, b, per_job):
     """K2 on the DE's copy engine (dp_h2d_push_copy): the DE's stream copies
     its host store into the PE pool through the peer view and writes the PE's
     counters; same bytes and counters as the kernel."""
@@ -289,7 +291,8 @@ def test_k2_copy_engine_parity(de_dev, L, T, b):
             plain.append((fbs, slots, ntok, 0, L))
         import torch
         s_de = torch.cuda.Stream(device=de_dev)
-        abi.h2d_push_copy(view, st_de, abi.make_jobs(specs), len(specs), s_de.cuda_stream)
+        (abi.h2d_push_copy_job if per_job else abi.h2d_push_copy)(view, st_de, abi.make_jobs(specs), len(specs),
+                                                                  s_de.cuda_stream)
         # the PE observes completion through its own counters only
         for t, (fbs, slots, ntok, l0, l1) in enumerate(plain):
             abi.wait_layer(pool, t, L, abi.layer_items(g, len(slots)) * L, timeout_ms=10000)

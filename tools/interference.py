@@ -145,7 +145,9 @@ def main():
                         abi.h2d_push_staged(view, st_de, stager1, jobs_ce2 if ce_scatter else jobs_st2, n_jobs,
                                             stream.cuda_stream)
                     elif kind == "k1" and ce:
-                        abi.h2d_layer_copy(pool, st_pe, jobs_ce, n_jobs, stream.cuda_stream)
+                        abi.h2d_layer_copy_job(pool, st_pe, jobs_ce1, n_jobs, stream.cuda_stream)
+                    elif ce:
+                        abi.h2d_push_copy_job(view, st_de, jobs_ce2, n_jobs, stream.cuda_stream)
                     elif kind == "k1":
                         abi.h2d_layer_gather(pool, st_pe, jobs_k1, n_jobs, stream.cuda_stream)
                     else:
@@ -186,12 +188,12 @@ def main():
                      ("de_k2_staged_148ctas", dict(k2=True, staged=True, push_ctas=148)),
                      ("de_k2_staged_8ctas", dict(k2=True, staged=True, stage_ctas=8)),
                      ("de_k2_copy_engine", dict(k2=True, ce=True))]:
-        if kw.get("ce"):
-            continue  # the DE copy-engine push needs host tables (dp_h2d_push_copy): see r01
         r = run_with(on_de=True, **kw)
         r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base_de - 1.0), 2)
         out[name] = r
-    ce_cases = [("k2_staged_148ctas", dict(k2=True, staged=True, push_ctas=148)),
+    ce_cases = [("k1_copy_engine_job", dict(k1=True, ce=True)), ("k2_copy_engine_job", dict(k2=True, ce=True)),
+                ("k1_copy_engine_job+k2_copy_engine_job", dict(k1=True, k2=True, ce=True)),
+                ("k2_staged_148ctas", dict(k2=True, staged=True, push_ctas=148)),
                 ("k1_staged+k2_staged_148ctas", dict(k1=True, k2=True, staged=True, push_ctas=148)),
                 ("k1_staged_ce", dict(k1=True, staged=True, ce_scatter=True)),
                 ("k2_staged_ce", dict(k2=True, staged=True, ce_scatter=True)),
