@@ -403,7 +403,7 @@ def measure_k1(device, shape, mode="staged", stage_ctas=32, target_bytes=1842138
     per_job = blocks * T * b * L
     jobs_n = max(1, min(64, target_bytes // per_job))
     g = abi.geom(L, T, b)
-    n_fb = max(blocks, (2 << 30) // (L * T * b))
+    n_fb = max(2 * blocks, (2 << 30) // (L * T * b))
     st = abi.Store(device, g, n_fb, 9)
     pool = abi.Pool(device, g, jobs_n * blocks, jobs_n)
     stager = abi.Stager(device, g) if mode == "staged" else None
@@ -414,7 +414,7 @@ def measure_k1(device, shape, mode="staged", stage_ctas=32, target_bytes=1842138
         keep, specs = [], []
         perm = rng.permutation(jobs_n * blocks).astype(np.int32)
         for j in range(jobs_n):
-            fbs = rng.integers(0, n_fb - blocks) + np.arange(blocks)  # one session's consecutive Full Blocks
+            fbs = rng.integers(0, n_fb - blocks + 1) + np.arange(blocks)  # one session's consecutive Full Blocks
             f_host = np.ascontiguousarray(fbs, dtype=np.int64)
             f = torch.tensor(f_host, device=f"cuda:{device}")
             sl = torch.tensor(perm[j * blocks:(j + 1) * blocks], device=f"cuda:{device}")
