@@ -1052,7 +1052,12 @@ def main():
                                           "launch_ms": round(k1_ms, 3),
                                           "frac": round(k1_alone / (peak / 1e9), 4) if peak else None},
                          "peak_source": "cudaMemcpyAsync H2D 1 GiB pinned (copy engine), best of 5, "
-                                        "measured in this run (MEASURED_PEAKS.json has no PCIe entry)"},
+                                        "measured in this run (MEASURED_PEAKS.json has no PCIe entry)",
+                         "frac_of_box_share": (round(achieved / (concurrent / 1e9 / n), 4)
+                                               if (concurrent and achieved) else None),
+                         "box_share_what": "achieved / (all GPUs' concurrent copy-engine H2D / N): on boxes "
+                                           "whose GPUs share host links the per-GPU link peak is not "
+                                           "reachable by all at once"},
             "cpu_baseline": cpu,
             "clocks": clk,
             "numa_node_per_rank": numa,
