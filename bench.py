@@ -84,6 +84,8 @@ def parse():
                     help="also persist generated tokens (decode stand-in + K4 D2H), implies --handoff")
     ap.add_argument("--handoff-ctas", type=int, default=0, help="K3 CTA cap on PEs (0 = default)")
     ap.add_argument("--k3-tma", action="store_true", help="K3's hit push through the TMA (bulk copies)")
+    ap.add_argument("--k3", default="kernel", choices=["kernel", "ce"],
+                    help="K3 (PD handoff push): SM kernel, or copy engines + a small side kernel per layer")
     ap.add_argument("--no-layerwise", action="store_true",
                     help="handoff + prefill: K3 after a request's last forward instead of layer by layer")
     ap.add_argument("--gather-ctas", type=int, default=-1, help="K1/K2 CTA cap (-1 = auto)")
@@ -502,6 +504,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     opt.handoff_ctas = args.handoff_ctas
     opt.handoff_layerwise = not args.no_layerwise
     opt.handoff_tma = args.k3_tma
+    opt.k3_mode = 1 if args.k3 == "ce" else 0
     opt.gather_ctas = args.gather_ctas
     opt.seed = 9
     if args.tier:
@@ -1027,6 +1030,7 @@ def main():
                         "stage_push_ctas": args.stage_push_ctas,
                         "stage_scatter": args.stage_scatter,
                         "handoff_ctas": args.handoff_ctas or None,
+                        "k3": args.k3 if (args.handoff or args.persist) else None,
                         "buffer_stalls": info["buffer_stalls"],
                         "buffer_wait_ms": round(info["buffer_wait_ms"], 1)},
             "model_prediction_gbps": round(info["model_gbps"], 3) if info["model_gbps"] else None,

@@ -106,6 +106,9 @@ def lib():
         "dp_h2d_push_p2p_dual": ([P, P, P, ctypes.POINTER(DualJob), ctypes.c_int32, P], ctypes.c_int),
         "dp_prefill_handoff": ([P, P, ctypes.POINTER(HandoffJob), ctypes.c_int32, ctypes.c_uint64,
                                 ctypes.c_int32, P], ctypes.c_int),
+        "dp_prefill_handoff_copy": ([P, P, ctypes.POINTER(HandoffJob), ctypes.c_int32, ctypes.c_uint64,
+                                     ctypes.c_int32, P], ctypes.c_int),
+        "dp_handoff_copy_launches": ([ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "dp_layer_items": ([ctypes.POINTER(Geom), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
                            ctypes.c_int),
         "dp_wait_layer": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int32, P],
@@ -374,6 +377,18 @@ def push_p2p_dual(pe_view, de_pool, store, jobs, n, stream=0):
 def prefill_handoff(pe_pool, de_view, jobs, n, seed, timeout_ms=20000, stream=0):
     check(lib().dp_prefill_handoff(pe_pool.ptr, de_view.ptr, jobs, n, seed, timeout_ms,
                                    ctypes.c_void_p(stream)))
+
+
+def prefill_handoff_copy(pe_pool, de_view, jobs, n, seed, timeout_ms=20000, stream=0):
+    """K3 on the copy engines; the jobs' block arrays must be host memory."""
+    check(lib().dp_prefill_handoff_copy(pe_pool.ptr, de_view.ptr, jobs, n, seed, timeout_ms,
+                                        ctypes.c_void_p(stream)))
+
+
+def handoff_copy_launches():
+    out = ctypes.c_int64()
+    check(lib().dp_handoff_copy_launches(ctypes.byref(out)))
+    return out.value
 
 
 def layer_items(g, n_blk):

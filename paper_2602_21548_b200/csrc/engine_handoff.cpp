@@ -113,6 +113,26 @@ StepResult EngineRuntime::run_step_handoff() {
         std::vector<dp_handoff_job> batch;
         for (const auto& [d, hj] : hjs)
           if (d == de) batch.push_back(hj);
+        if (x.opt.k3_mode == 1) {
+          // copy engines: the same jobs with host-readable block tables
+          for (dp_handoff_job& hj : batch) {
+            const std::int64_t off = hj.src_fb - d_ho_src_;
+            hj.src_fb = x.ho_src_fb[engine_].data() + off;
+            hj.pe_slot = x.ho_pe_slot[engine_].data() + off;
+            hj.de_slot = x.ho_de_slot[engine_].data() + off;
+          }
+          std::int64_t n0 = 0, n1 = 0;
+          check(dp_handoff_copy_launches(&n0), "dp_handoff_copy_launches");
+          for (std::size_t b0 = 0; b0 < batch.size(); b0 += DP_MAX_HANDOFF_JOBS_PER_LAUNCH) {
+            const auto nb = std::min<std::size_t>(DP_MAX_HANDOFF_JOBS_PER_LAUNCH, batch.size() - b0);
+            check(dp_prefill_handoff_copy(pool_, de_views_[de], batch.data() + b0, static_cast<int32_t>(nb),
+                                          x.opt.seed, x.opt.wait_timeout_ms, h),
+                  "dp_prefill_handoff_copy");
+          }
+          check(dp_handoff_copy_launches(&n1), "dp_handoff_copy_launches");
+          res.launches += n1 - n0;
+          continue;
+        }
         check(dp_prefill_handoff(pool_, de_views_[de], batch.data(), static_cast<int32_t>(batch.size()), x.opt.seed,
                                  x.opt.wait_timeout_ms, h),
               "dp_prefill_handoff");

@@ -1512,6 +1512,293 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
 
 }  // extern "C"
 
+// ============================================== K3 on the copy engines
+// dp_prefill_handoff_copy: the hit part of PeToDe moves by copy-engine copies
+// (whole runs of Layer Blocks consecutive in both pools), and one small
+// kernel per layer does the rest of K3: it releases the previous layer (its
+// copies precede it on the stream), waits for this layer's gates, and writes
+// the miss tokens' KV into both pools.
+namespace {
+
+constexpr int kHoMissDescs = 112;  // miss pieces per side-kernel launch (parameter block)
+constexpr int kHoSideCtas = 32;
+
+struct HoMissDesc {  // one block's miss tokens: bytes [b0, b1) of its Layer Block
+  int64_t fb;
+  int32_t pe_slot, de_slot;
+  int32_t b0, b1;
+};
+struct HoGate {
+  int32_t ticket;
+  uint32_t target;
+};
+struct HoRelease {
+  int32_t de_ticket, pe_done_ticket;
+  uint32_t n;  // items per layer
+};
+
+struct HoSideParams {
+  char* pe_pool;
+  char* de_pool;
+  uint32_t* pe_ctr;
+  uint32_t* de_ctr;
+  int64_t pe_stride, de_stride, lb_bytes;
+  int* err_flag;
+  uint64_t timeout_ns, seed_mix;
+  int32_t n_layer;
+  int32_t miss_l0, miss_l1;  // layers whose miss KV this launch writes (after the gates)
+  int32_t rel_l0, rel_l1;    // layers released first by CTA 0 (work stream-ordered before this launch)
+  int32_t n_gate, n_miss, n_rel;
+  HoGate gate[DP_MAX_HANDOFF_JOBS_PER_LAUNCH];
+  HoRelease rel[DP_MAX_HANDOFF_JOBS_PER_LAUNCH];
+  HoMissDesc miss[kHoMissDescs];
+};
+static_assert(sizeof(HoSideParams) <= 4000, "kernel parameter block too large");
+
+__global__ void __launch_bounds__(kThreads) kv_handoff_side(const __grid_constant__ HoSideParams p) {
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0 && p.n_rel > 0 && p.rel_l1 > p.rel_l0) {
+    // everything of layers [rel_l0, rel_l1) -- copies and earlier launches --
+    // precedes this kernel on the stream
+    fence_sys();
+    const uint32_t layers = static_cast<uint32_t>(p.rel_l1 - p.rel_l0);
+    for (int r = 0; r < p.n_rel; ++r) {
+      const HoRelease& h = p.rel[r];
+      for (int l = p.rel_l0; l < p.rel_l1; ++l) {
+        if (h.de_ticket >= 0)
+          asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(
+                           p.de_ctr + static_cast<int64_t>(h.de_ticket) * (p.n_layer + 1) + l),
+                       "r"(h.n)
+                       : "memory");
+        if (h.pe_done_ticket >= 0)
+          asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(
+                           p.pe_ctr + static_cast<int64_t>(h.pe_done_ticket) * (p.n_layer + 1) + l),
+                       "r"(h.n)
+                       : "memory");
+      }
+      if (h.de_ticket >= 0)
+        asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(
+                         p.de_ctr + static_cast<int64_t>(h.de_ticket) * (p.n_layer + 1) + p.n_layer),
+                     "r"(h.n * layers)
+                     : "memory");
+      if (h.pe_done_ticket >= 0)
+        asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(
+                         p.pe_ctr + static_cast<int64_t>(h.pe_done_ticket) * (p.n_layer + 1) + p.n_layer),
+                     "r"(h.n * layers)
+                     : "memory");
+    }
+  }
+  if (p.miss_l1 <= p.miss_l0) return;
+  // the gates of the miss layers (the maybe_start_compute gate of each job)
+  if (p.n_gate > 0) {
+    if (tid == 0) {
+      const uint64_t t0 = global_timer_ns();
+      for (int gi = 0; gi < p.n_gate; ++gi)
+        for (int l = p.miss_l0; l < p.miss_l1; ++l) {
+          const uint32_t* ctr = p.pe_ctr + static_cast<int64_t>(p.gate[gi].ticket) * (p.n_layer + 1) + l;
+          while (true) {
+            uint32_t v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= p.gate[gi].target) break;
+            if (global_timer_ns() - t0 > p.timeout_ns) {
+              atomicExch_system(p.err_flag, 1);
+              break;
+            }
+            __nanosleep(1024);
+          }
+        }
+    }
+    __syncthreads();
+  }
+  // miss KV: the prefill stand-in's content for the miss tokens, into the PE
+  // pool (its KV cache) and the DE pool (the MissMerge / PeToDe of the miss)
+  const int64_t lb = p.lb_bytes;
+  const int64_t per_layer = p.n_miss;
+  const int64_t total = per_layer * (p.miss_l1 - p.miss_l0);
+  for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+    const int layer = p.miss_l0 + static_cast<int>(item / per_layer);
+    const HoMissDesc& d = p.miss[item % per_layer];
+    const uint64_t w_base = static_cast<uint64_t>((layer * lb) >> 3);
+    uint4* pe_dst = reinterpret_cast<uint4*>(p.pe_pool + layer * p.pe_stride + static_cast<int64_t>(d.pe_slot) * lb);
+    uint4* de_dst = reinterpret_cast<uint4*>(p.de_pool + layer * p.de_stride + static_cast<int64_t>(d.de_slot) * lb);
+    for (int64_t i = (d.b0 >> 4) + tid; i < (d.b1 >> 4); i += kThreads) {
+      const uint4 v = content_pair(static_cast<uint64_t>(d.fb), w_base + 2 * static_cast<uint64_t>(i), p.seed_mix);
+      st_v4(pe_dst + i, v);
+      st_v4(de_dst + i, v);
+    }
+  }
+}
+
+// Launches kv_handoff_side: releases of layers [r0, r1) (CTA 0, first),
+// then -- with `gate` -- the jobs' gates at layers [l0, l1), then the miss KV
+// of layers [l0, l1), the descriptors split over as many launches as the
+// parameter block needs (the releases and gates ride on the first).
+int launch_side(HoSideParams& p, const std::vector<HoMissDesc>& miss, int l0, int l1, int r0, int r1, bool gate,
+                cudaStream_t s, int64_t* launches) {
+  const int32_t n_rel = p.n_rel, n_gate = p.n_gate;
+  if (!gate) p.n_gate = 0;
+  p.miss_l0 = l0;
+  p.miss_l1 = l1;
+  p.rel_l0 = r0;
+  p.rel_l1 = r1;
+  std::size_t i = 0;
+  bool first = true;
+  while (first || i < miss.size()) {
+    const std::size_t n = std::min<std::size_t>(kHoMissDescs, miss.size() - i);
+    p.n_miss = static_cast<int32_t>(n);
+    for (std::size_t k = 0; k < n; ++k) p.miss[k] = miss[i + k];
+    const bool work = (p.n_rel > 0 && r1 > r0) || (l1 > l0 && (p.n_gate > 0 || n > 0));
+    if (work) {
+      const int64_t units = static_cast<int64_t>(n) * std::max(0, l1 - l0);
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, kHoSideCtas)));
+      kv_handoff_side<<<grid, kThreads, 0, s>>>(p);
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        p.n_rel = n_rel;
+        p.n_gate = n_gate;
+        return fail(DP_ECUDA, std::string("kv_handoff_side: ") + cudaGetErrorString(e));
+      }
+      ++*launches;
+    }
+    p.n_rel = 0;  // released / gated once: later launches are stream-ordered after it
+    p.n_gate = 0;
+    first = false;
+    i += n;
+  }
+  p.n_rel = n_rel;
+  p.n_gate = n_gate;
+  return DP_OK;
+}
+
+std::atomic<int64_t> g_handoff_copy_launches{0};  // side kernels, process-wide
+
+}  // namespace
+
+extern "C" {
+
+int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job* jobs, int32_t n_jobs,
+                            uint64_t seed, int32_t timeout_ms, dp_stream stream) {
+  if (!pe_pool || !de_view || (n_jobs > 0 && !jobs) || n_jobs < 0)
+    return fail(DP_EINVAL, "prefill_handoff_copy: null argument");
+  if (!pe_pool->owner) return fail(DP_EINVAL, "prefill_handoff_copy: the PE pool must be local");
+  if (de_view->owner) return fail(DP_EINVAL, "prefill_handoff_copy: the DE pool must be a peer view");
+  if (de_view->device != pe_pool->device)
+    return fail(DP_EINVAL, "prefill_handoff_copy: the DE view must be mapped on the PE's device");
+  if (!geom_equal(pe_pool->geom, de_view->geom))
+    return fail(DP_EINVAL, "prefill_handoff_copy: geometry differs");
+  if (timeout_ms <= 0) return fail(DP_EINVAL, "prefill_handoff_copy: timeout must be > 0");
+  if (n_jobs > DP_MAX_HANDOFF_JOBS_PER_LAUNCH) {  // in groups of the parameter block's job capacity
+    for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_HANDOFF_JOBS_PER_LAUNCH)
+      if (int rc = dp_prefill_handoff_copy(pe_pool, de_view, jobs + j0,
+                                           std::min<int32_t>(DP_MAX_HANDOFF_JOBS_PER_LAUNCH, n_jobs - j0), seed,
+                                           timeout_ms, stream))
+        return rc;
+    return DP_OK;
+  }
+  const dp_kv_geom& g = pe_pool->geom;
+  const int L = g.n_layer;
+  const int64_t T = g.block_tokens, bpt = g.bytes_per_token_layer, lb = T * bpt;
+  const int64_t pe_plane = lb * pe_pool->n_slots, de_plane = lb * de_view->n_slots;
+  const uint32_t items = static_cast<uint32_t>(chunks_per_block(g));
+  DeviceGuard guard(pe_pool->device);
+  auto s = static_cast<cudaStream_t>(stream);
+  HoSideParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.pe_pool = pe_pool->base;
+  p.de_pool = de_view->base;
+  p.pe_ctr = pe_pool->counters;
+  p.de_ctr = de_view->counters;
+  p.pe_stride = pe_plane;
+  p.de_stride = de_plane;
+  p.lb_bytes = lb;
+  p.err_flag = pe_pool->err_host;
+  p.timeout_ns = static_cast<uint64_t>(timeout_ms) * 1000000ull;
+  p.seed_mix = seed * kSeedMul;
+  p.n_layer = L;
+  // per job: the hit runs to copy, the miss pieces, the gate and the release
+  struct Run {
+    int64_t pe_off, de_off, bytes;  // within a layer plane
+  };
+  std::vector<Run> runs;
+  std::vector<HoMissDesc> miss;
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    const dp_handoff_job& job = jobs[j];
+    const int64_t need = (job.n_prompt + T - 1) / T;
+    if (job.n_cached < 0 || job.n_prompt < job.n_cached || job.n_blk != need ||
+        job.pe_ticket >= pe_pool->n_tickets || job.de_ticket >= de_view->n_tickets ||
+        job.pe_done_ticket >= pe_pool->n_tickets || (job.n_blk > 0 && (!job.src_fb || !job.pe_slot || !job.de_slot)))
+      return fail(DP_EINVAL, "prefill_handoff_copy: job " + std::to_string(j) + " out of range");
+    for (int32_t k = 0; k < job.n_blk; ++k)
+      if (job.pe_slot[k] < 0 || job.pe_slot[k] >= pe_pool->n_slots || job.de_slot[k] < 0 ||
+          job.de_slot[k] >= de_view->n_slots)
+        return fail(DP_EINVAL, "prefill_handoff_copy: job " + std::to_string(j) + " block " +
+                                   std::to_string(k) + " slot out of range");
+    if (job.n_blk == 0) continue;
+    // hit part (PeToDe only): blocks [0, n_hit), the last one's valid prefix
+    const int32_t n_hit = job.push_hit ? static_cast<int32_t>((job.n_cached + T - 1) / T) : 0;
+    for (int32_t k = 0; k < n_hit;) {
+      int32_t run = 1;
+      while (k + run < n_hit && job.pe_slot[k + run] == job.pe_slot[k] + run &&
+             job.de_slot[k + run] == job.de_slot[k] + run)
+        ++run;
+      const int64_t last = k + run - 1;
+      const int64_t tail = std::min<int64_t>(T, job.n_cached - last * T) * bpt;
+      runs.push_back({job.pe_slot[k] * lb, job.de_slot[k] * lb, (run - 1) * lb + tail});
+      k += run;
+    }
+    // miss part: tokens [C, C + A) block by block
+    for (int64_t k = job.n_cached / T; k < job.n_blk; ++k) {
+      const int64_t b0 = std::max<int64_t>(0, job.n_cached - k * T) * bpt;
+      const int64_t b1 = std::min<int64_t>(T, job.n_prompt - k * T) * bpt;
+      if (b1 > b0)
+        miss.push_back({job.src_fb[k], job.pe_slot[k], job.de_slot[k], static_cast<int32_t>(b0),
+                        static_cast<int32_t>(b1)});
+    }
+    if (job.pe_ticket >= 0) {
+      bool dup = false;
+      for (int gi = 0; gi < p.n_gate; ++gi)
+        if (p.gate[gi].ticket == job.pe_ticket) {
+          p.gate[gi].target = std::max(p.gate[gi].target, job.pe_wait_items);
+          dup = true;
+        }
+      if (!dup) p.gate[p.n_gate++] = {job.pe_ticket, job.pe_wait_items};
+    }
+    if (job.de_ticket >= 0 || job.pe_done_ticket >= 0)
+      p.rel[p.n_rel++] = {job.de_ticket, job.pe_done_ticket, static_cast<uint32_t>(job.n_blk) * items};
+  }
+  int64_t launches = 0;
+  if (p.n_gate == 0) {
+    // no gates: one 2D copy per run (rows = layers), then the miss KV of
+    // every layer, then the releases of every layer
+    for (const Run& r : runs)
+      DP_CUDA(cudaMemcpy2DAsync(de_view->base + r.de_off, de_plane, pe_pool->base + r.pe_off, pe_plane, r.bytes,
+                                L, cudaMemcpyDeviceToDevice, s));
+    if (!miss.empty())
+      if (int rc = launch_side(p, miss, 0, L, 0, 0, false, s, &launches)) return rc;
+    if (int rc = launch_side(p, {}, 0, 0, 0, L, false, s, &launches)) return rc;
+  } else {
+    // layer by layer: side(l) = release of l - 1, the gates of l, the miss
+    // KV of l; then l's copies
+    for (int l = 0; l < L; ++l) {
+      if (int rc = launch_side(p, miss, l, l + 1, l > 0 ? l - 1 : 0, l, true, s, &launches)) return rc;
+      for (const Run& r : runs)
+        DP_CUDA(cudaMemcpyAsync(de_view->base + l * de_plane + r.de_off, pe_pool->base + l * pe_plane + r.pe_off,
+                                r.bytes, cudaMemcpyDeviceToDevice, s));
+    }
+    if (int rc = launch_side(p, {}, 0, 0, L - 1, L, false, s, &launches)) return rc;
+  }
+  g_handoff_copy_launches += launches;
+  return DP_OK;
+}
+
+int dp_handoff_copy_launches(int64_t* n) {
+  if (!n) return fail(DP_EINVAL, "handoff_copy_launches: null argument");
+  *n = g_handoff_copy_launches.load();
+  return DP_OK;
+}
+
+}  // extern "C"
+
 // ============================================================ persistence
 // dp_decode_fill (decode stand-in) and dp_persist_d2h (K4, PersistD2H).
 namespace {
@@ -2271,6 +2558,7 @@ int preload_kernels(int device) {
                          reinterpret_cast<const void*>(kv_gather_dual),
                          reinterpret_cast<const void*>(kv_prefill_handoff<false>),
                          reinterpret_cast<const void*>(kv_prefill_handoff<true>),
+                         reinterpret_cast<const void*>(kv_handoff_side),
                          reinterpret_cast<const void*>(kv_decode_fill),
                          reinterpret_cast<const void*>(kv_persist_d2h),
                          reinterpret_cast<const void*>(kv_prefill_attend)};

@@ -294,3 +294,127 @@ def test_dual_staged(de_dev, L, T, b, C):
     finally:
         for x in (stager, pe_view, de_pool, pe_pool, st_de):
             x.close()
+
+
+# ------------------------------------------------- K3 on the copy engines
+def _slots(rng, n, pool_slots, layout):
+    """Block tables: 'runs' = two consecutive runs (the executor's usual
+    FIFO allocation), 'scattered' = a permutation (one copy per block)."""
+    if layout == "scattered":
+        return rng.permutation(pool_slots)[:n].astype(np.int32)
+    cut = n // 2
+    return np.concatenate([np.arange(1, 1 + cut), np.arange(pool_slots - (n - cut), pool_slots)]).astype(np.int32)
+
+
+@pytest.mark.parametrize("L,T,b,C,A", [(8, 64, 576, 64 * 7 + 33, 429), (8, 64, 576, 64 * 2, 1),
+                                       (8, 64, 576, 0, 64 * 3 + 5), (8, 64, 576, 64 * 4, 0),
+                                       (61, 64, 576, 64 * 6 + 1, 429), (64, 64, 4096, 64 * 3 + 40, 90)])
+@pytest.mark.parametrize("layout", ["runs", "scattered"])
+def test_pe_path_petode_copy_engine(de_dev, L, T, b, C, A, layout):
+    """dp_prefill_handoff_copy, PE read path, no gate: one 2D copy per run of
+    hit blocks (all layers), the side kernel writes the miss KV into both
+    pools, then releases every layer -- pools and counters as K3's."""
+    g = abi.geom(L, T, b)
+    P = C + A
+    n_hit, n_prompt = -(-C // T), -(-P // T)
+    rng = np.random.default_rng(P + 1)
+    st_pe = abi.Store(0, g, 40, SEED)
+    pe_pool = abi.Pool(0, g, 32, 2)
+    de_pool = abi.Pool(de_dev, g, 32, 1)
+    de_view = de_pool.peer_view(0)
+    try:
+        fbs = (rng.integers(0, 40 - n_prompt) + np.arange(n_prompt)).astype(np.int64)
+        pe_slots = _slots(rng, n_prompt, 32, layout)
+        de_slots = _slots(rng, n_prompt, 32, layout)[::-1].copy() if layout == "scattered" else \
+            _slots(rng, n_prompt, 32, layout)
+        t = [dev(fbs, 0, np.int64), dev(pe_slots, 0, np.int32)]
+        if n_hit:
+            abi.h2d_layer_gather(pe_pool, st_pe, abi.make_jobs(
+                [(t[0].data_ptr(), t[1].data_ptr(), C, n_hit, 0, L, -1)]), 1)
+        hj = (abi.HandoffJob * 1)()
+        hj[0] = abi.HandoffJob(fbs.ctypes.data, pe_slots.ctypes.data, de_slots.ctypes.data, C, P, n_prompt, 1,
+                               -1, 0, 0, 1)
+        n0 = abi.handoff_copy_launches()
+        abi.prefill_handoff_copy(pe_pool, de_view, hj, 1, SEED)  # legacy stream: ordered after K1
+        sync_all()
+        assert abi.handoff_copy_launches() - n0 <= 2
+        gr = refpy.geom(L, T, b)
+        check_prompt(pe_pool, gr, fbs, pe_slots, P, T, b, L)
+        check_prompt(de_pool, gr, fbs, de_slots, P, T, b, L)
+        per = n_prompt * abi.layer_items(g, 1)
+        abi.wait_layer(de_pool, 0, L, per * L, timeout_ms=2000)
+        abi.wait_layer(de_pool, 0, L - 1, per, timeout_ms=2000)
+        abi.wait_layer(pe_pool, 1, L, per * L, timeout_ms=2000)  # K3 done row
+        sync_all()
+        assert abi.wait_status(de_pool) == abi.DP_OK and abi.wait_status(pe_pool) == abi.DP_OK
+    finally:
+        for x in (de_view, de_pool, pe_pool, st_pe):
+            x.close()
+
+
+@pytest.mark.parametrize("L,T,b,C,A", [(8, 64, 576, 64 * 5 + 10, 300), (8, 64, 576, 0, 200),
+                                       (61, 64, 576, 64 * 9 + 17, 429), (64, 64, 4096, 64 * 4 + 33, 100)])
+def test_de_path_missmerge_copy_engine(de_dev, L, T, b, C, A):
+    """dp_prefill_handoff_copy gated per layer on the DE's dual gather (the
+    DE read path): the side kernel of layer l waits for l's hit KV, writes
+    the miss KV into both pools and releases layer l - 1."""
+    g = abi.geom(L, T, b)
+    P = C + A
+    n_hit, n_prompt = -(-C // T), -(-P // T)
+    rng = np.random.default_rng(C * 3 + A)
+    s_de = de_stream(de_dev)
+    st_de = abi.Store(de_dev, g, 40, SEED)
+    pe_pool = abi.Pool(0, g, 32, 2)
+    de_pool = abi.Pool(de_dev, g, 32, 2)
+    pe_view_on_de = pe_pool.peer_view(de_dev)
+    de_view_on_pe = de_pool.peer_view(0)
+    try:
+        fbs = (rng.integers(0, 40 - n_prompt) + np.arange(n_prompt)).astype(np.int64)
+        pe_slots = rng.permutation(32)[:n_prompt].astype(np.int32)
+        de_slots = rng.permutation(32)[:n_prompt].astype(np.int32)
+        keep = [dev(fbs if n_prompt else [0], de_dev, np.int64), dev(pe_slots if n_prompt else [0], de_dev, np.int32),
+                dev(de_slots if n_prompt else [0], de_dev, np.int32)]
+        dj = (abi.DualJob * 1)()
+        dj[0].pe = abi.Job(keep[0].data_ptr(), keep[1].data_ptr(), C, n_hit, 0, L, 0)
+        dj[0].de_slot = keep[2].data_ptr()
+        dj[0].de_ticket = 0
+        items = abi.layer_items(g, n_hit)
+        hj = (abi.HandoffJob * 1)()
+        hj[0] = abi.HandoffJob(fbs.ctypes.data, pe_slots.ctypes.data, de_slots.ctypes.data, C, P,
+                               n_prompt, 0, 0 if C else -1, items, 0, 1)
+        abi.prefill_handoff_copy(pe_pool, de_view_on_pe, hj, 1, SEED, timeout_ms=20000)
+        abi.push_p2p_dual(pe_view_on_de, de_pool, st_de, dj, 1, s_de)
+        sync_all()
+        assert abi.wait_status(pe_pool) == abi.DP_OK
+        gr = refpy.geom(L, T, b)
+        check_prompt(pe_pool, gr, fbs, pe_slots, P, T, b, L)
+        check_prompt(de_pool, gr, fbs, de_slots, P, T, b, L)
+        per_block = abi.layer_items(g, 1)
+        want_layer = (n_hit + n_prompt) * per_block
+        abi.wait_layer(de_pool, 0, L, want_layer * L, timeout_ms=2000)
+        abi.wait_layer(de_pool, 0, L - 1, want_layer, timeout_ms=2000)
+        abi.wait_layer(pe_pool, 1, L, n_prompt * per_block * L, timeout_ms=2000)
+        sync_all()
+        assert abi.wait_status(de_pool) == abi.DP_OK and abi.wait_status(pe_pool) == abi.DP_OK
+    finally:
+        for x in (de_view_on_pe, pe_view_on_de, de_pool, pe_pool, st_de):
+            x.close()
+
+
+def test_handoff_copy_gate_watchdog(de_dev):
+    """The copy-engine K3's layer gate trips the watchdog instead of hanging."""
+    L, T, b = 2, 64, 576
+    g = abi.geom(L, T, b)
+    pe_pool = abi.Pool(0, g, 4, 1)
+    de_pool = abi.Pool(de_dev, g, 4, 1)
+    de_view = de_pool.peer_view(0)
+    try:
+        fbs, sl = np.array([0, 1], dtype=np.int64), np.array([0, 1], dtype=np.int32)
+        hj = (abi.HandoffJob * 1)()
+        hj[0] = abi.HandoffJob(fbs.ctypes.data, sl.ctypes.data, sl.ctypes.data, 64, 100, 2, 0, 0, 1, 0, -1)
+        abi.prefill_handoff_copy(pe_pool, de_view, hj, 1, SEED, timeout_ms=50)
+        sync_all()
+        assert abi.wait_status(pe_pool) == abi.DP_ETIMEOUT
+    finally:
+        for x in (de_view, de_pool, pe_pool):
+            x.close()

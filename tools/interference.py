@@ -178,7 +178,22 @@ def main():
         return {"gemm_ms": round(mean, 4), "tflops": round(flops / mean / 1e9, 1),
                 "window_s": round(t1 - t0, 2), "loader_gbps_during": rates}
 
-    out = {"gemm": {"m": a.m, "n": a.m, "k": a.k, "dtype": "bf16"}}
+    def bracketed(kw, on_de=False):
+        """The case between two runs of the GEMM alone on the same GPU (A/B/A):
+        the slowdown is against the mean of the two, and `noise_pct` (their
+        difference) is the resolution of that number."""
+        before = run_with(on_de=on_de)["gemm_ms"]
+        r = run_with(on_de=on_de, **kw)
+        after = run_with(on_de=on_de)["gemm_ms"]
+        alone = 0.5 * (before + after)
+        r["alone_ms"] = [before, after]
+        r["noise_pct"] = round(100.0 * abs(after - before) / alone, 2)
+        r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / alone - 1.0), 2)
+        return r
+
+    out = {"gemm": {"m": a.m, "n": a.m, "k": a.k, "dtype": "bf16"},
+           "method": "each case bracketed by the GEMM alone before and after (A/B/A); trimmed mean of "
+                     "per-GEMM CUDA-event times"}
     out["alone"] = run_with()
     base = out["alone"]["gemm_ms"]
     out["de_alone"] = run_with(on_de=True)
@@ -188,9 +203,7 @@ def main():
                      ("de_k2_staged_148ctas", dict(k2=True, staged=True, push_ctas=148)),
                      ("de_k2_staged_8ctas", dict(k2=True, staged=True, stage_ctas=8)),
                      ("de_k2_copy_engine", dict(k2=True, ce=True))]:
-        r = run_with(on_de=True, **kw)
-        r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base_de - 1.0), 2)
-        out[name] = r
+        out[name] = bracketed(kw, on_de=True)
     ce_cases = [("k1_copy_engine_job", dict(k1=True, ce=True)), ("k2_copy_engine_job", dict(k2=True, ce=True)),
                 ("k1_copy_engine_job+k2_copy_engine_job", dict(k1=True, k2=True, ce=True)),
                 ("k2_staged_148ctas", dict(k2=True, staged=True, push_ctas=148)),
@@ -215,9 +228,7 @@ def main():
              ("k1_copy_engine+k2", dict(k1=True, k2=True, ce=True))]
 
     for name, kw in cases:
-        r = run_with(**kw)
-        r["slowdown_pct"] = round(100.0 * (r["gemm_ms"] / base - 1.0), 2)
-        out[name] = r
+        out[name] = bracketed(kw)
     for dev in (0, 1):
         abi.set_gather_ctas(dev, 0)
     stager0.set_mode(abi.SCATTER_KERNEL)

@@ -61,8 +61,11 @@ def one(kind, a, g, L, T, b, n_fb, n_slots):
         st.close()
 
 
-def k3(a, g, L, T, b, n_fb, n_slots):
-    """K3 alone (PE path: push the whole prompt of each job, C = 7/8 of it)."""
+def k3(a, g, L, T, b, n_fb, n_slots, ce=False, contiguous=False):
+    """K3 alone (PE path: push the whole prompt of each job, C = 7/8 of it).
+    ce: dp_prefill_handoff_copy (copy engines + side kernel); contiguous: the
+    jobs' slots are consecutive runs in both pools (the executor's FIFO
+    allocation) instead of a random permutation."""
     st = abi.Store(0, g, n_fb, 9)
     pool = abi.Pool(0, g, n_slots, 2 * a.jobs)
     de_pool = abi.Pool(1, g, n_slots, a.jobs)
@@ -73,13 +76,21 @@ def k3(a, g, L, T, b, n_fb, n_slots):
         perm = rng.permutation(n_slots)
         for j in range(a.jobs):
             fbs = torch.tensor(rng.integers(0, n_fb, a.blocks), dtype=torch.int64, device="cuda:0")
-            sl = torch.tensor(perm[(j * a.blocks) % n_slots:][:a.blocks].astype(np.int32), device="cuda:0")
-            keep += [fbs, sl]
+            idx = (np.arange(j * a.blocks, (j + 1) * a.blocks) % n_slots) if contiguous else \
+                perm[(j * a.blocks) % n_slots:][:a.blocks]
+            sl_h = idx.astype(np.int32)
+            fb_h = fbs.cpu().numpy()
+            sl = torch.tensor(sl_h, device="cuda:0")
+            keep += [fbs, sl, sl_h, fb_h]
             prompt = a.blocks * T
             cached = prompt * 7 // 8
             specs.append((fbs.data_ptr(), sl.data_ptr(), cached, -(-cached // T), 0, L, j))
-            ho[j] = abi.HandoffJob(fbs.data_ptr(), sl.data_ptr(), sl.data_ptr(), cached, prompt, a.blocks,
-                                   1, -1, 0, j, a.jobs + j)
+            if ce:
+                ho[j] = abi.HandoffJob(fb_h.ctypes.data, sl_h.ctypes.data, sl_h.ctypes.data, cached, prompt,
+                                       a.blocks, 1, -1, 0, j, a.jobs + j)
+            else:
+                ho[j] = abi.HandoffJob(fbs.data_ptr(), sl.data_ptr(), sl.data_ptr(), cached, prompt, a.blocks,
+                                       1, -1, 0, j, a.jobs + j)
         abi.h2d_layer_gather(pool, st, abi.make_jobs(specs), len(specs))
         torch.cuda.synchronize(0)
         nbytes = a.jobs * a.blocks * T * b * L
@@ -89,7 +100,10 @@ def k3(a, g, L, T, b, n_fb, n_slots):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            abi.prefill_handoff(pool, de_view, ho, a.jobs, 9, 20000, s.cuda_stream)
+            if ce:
+                abi.prefill_handoff_copy(pool, de_view, ho, a.jobs, 9, 20000, s.cuda_stream)
+            else:
+                abi.prefill_handoff(pool, de_view, ho, a.jobs, 9, 20000, s.cuda_stream)
             e1.record(s)
             e1.synchronize()
             if r:
@@ -207,6 +221,9 @@ def main():
                 out[key] = k3(a, g, L, T, b, n_fb, n_slots)
         abi.set_handoff_ctas(0, 0)
         abi.set_handoff_tma(False)
+        out["k3_contiguous"] = k3(a, g, L, T, b, n_fb, n_slots, contiguous=True)
+        out["k3_ce_contiguous"] = k3(a, g, L, T, b, n_fb, n_slots, ce=True, contiguous=True)
+        out["k3_ce_scattered"] = k3(a, g, L, T, b, n_fb, n_slots, ce=True)
     if a.peer:
         out["ce_peer_copy"] = ce_peer()
     if a.k4:
