@@ -15,9 +15,17 @@
 //   a session's next turn arrives when its previous turn completes.
 //
 // StorageRead is the engine's emulated storage NIC (dp_nic, the rate cap);
-// the hit transfer is K1 / K2 (or their staged variants) on the GPUs; the PE
-// is released when the request's KV has landed in its pool (the load path:
-// no prefill compute), the DE holds the request for gen x decode_s_per_token.
+// the hit transfer is K1 / K2 (or their staged variants) on the GPUs.  Load
+// path only (exec.prefill false): the PE is released when the request's KV
+// has landed in its pool.  With exec.prefill, each PE runs the prefill
+// stand-in as the plan-mode executor does -- forwards packed by
+// build_forward_batch under exec.compute_quota (scheduler.cpp:174-219) from
+// its FIFO of requests whose loads are launched, K5 per layer gated on the
+// request's landed counters (maybe_start_compute, desim.cpp:623-628) -- and
+// the PE is released when the request's last forward has computed its last
+// layer (on_prefill_side_done, desim.cpp:642-652); a turn's TTFT is then
+// arrival -> that point.  The DE holds the request for gen x
+// decode_s_per_token.
 // Admission reserves the request's blocks in the PE's paged pool (bounded:
 // pe_pool_slots) and stalls, FIFO, while the pool is full -- the staging
 // bound of try_admit (desim.cpp:587-599).
@@ -53,7 +61,8 @@ struct LiveOptions {
   // at arrival_times[i] seconds (empty: all at 0, offline)
   std::vector<double> arrival_times;
   // the reference's online stops, on MEASURED latencies: a turn's TTFT here is
-  // the load path's (arrival -> its hit KV landed in the PE pool); the run
+  // the load path's (arrival -> its hit KV landed in the PE pool), or with
+  // exec.prefill arrival -> its prefill done (the PE release); the run
   // stops when one exceeds slo_ttft_s (> 0; desim.cpp:679-685) or when the
   // TTFT series is steady (steady_window > 0: detect_steady_state every
   // window / 2, desim.cpp:942-953)
@@ -78,6 +87,8 @@ struct LiveRequest {
   std::int64_t cached = 0, append = 0, gen = 0;
   int pe = -1, de = -1, path = 0, reader = -1;
   double t_arrival = -1, t_sched = -1, t_admit = -1, t_read_done = -1, t_landed = -1, t_done = -1;
+  double t_prefilled = -1;  // exec.prefill: its last forward done (the PE release)
+  int forwards = 0;         // exec.prefill: forwards it took part in
 };
 
 struct LiveReport {
@@ -99,6 +110,14 @@ struct LiveReport {
     std::uint64_t hash_first = 0, hash_last = 0;
   };
   std::vector<Occupant> final_slots;
+  // gpu backend with exec.prefill: the K5 digest of every prefilled request at
+  // layers 0 and L-1 (parity vs the oracle: independent of the batching)
+  struct Digest {
+    int req = 0;
+    std::uint64_t first = 0, last = 0;
+  };
+  std::vector<Digest> digests;
+  std::int64_t forwards = 0;  // exec.prefill: forwards run over all PEs
   std::int64_t store_fb = 0, fb_stride = 0;  // content mapping fb = (traj * stride + k) % store_fb
   bool slo_violated = false, steady_state = false;
   std::size_t completed_requests = 0, total_requests = 0;

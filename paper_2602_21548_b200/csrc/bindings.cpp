@@ -687,12 +687,17 @@ PYBIND11_MODULE(_core, m) {
         py::list reqs;
         for (const auto& r : rep.requests)
           reqs.append(py::make_tuple(r.id, r.traj, r.round, r.cached, r.append, r.gen, r.pe, r.de, r.path, r.reader,
-                                     r.t_arrival, r.t_sched, r.t_admit, r.t_read_done, r.t_landed, r.t_done));
+                                     r.t_arrival, r.t_sched, r.t_admit, r.t_read_done, r.t_landed, r.t_done,
+                                     r.t_prefilled, r.forwards));
         d["requests"] = reqs;
         py::list occ;
         for (const auto& x : rep.final_slots)
           occ.append(py::make_tuple(x.pe, x.slot, x.fb, x.ntok, x.hash_first, x.hash_last));
         d["final_slots"] = occ;
+        py::list dig;
+        for (const auto& x : rep.digests) dig.append(py::make_tuple(x.req, x.first, x.last));
+        d["digests"] = dig;
+        d["forwards"] = rep.forwards;
         d["wall_s"] = rep.wall_s;
         d["reader_bytes"] = rep.reader_bytes;
         d["admission_stalls"] = rep.admission_stalls;

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <deque>
@@ -35,8 +36,28 @@ struct Req {
 };
 
 struct Msg {
-  enum Kind { ReadDone, Landed } kind;
+  enum Kind { ReadDone, Landed, Prefilled } kind;
   int req;
+};
+
+// One PE's prefill stand-in (exec.prefill): a FIFO of requests whose loads
+// are launched, packed into forwards by build_forward_batch and run as K5
+// layer by layer on the PE's compute stream, one forward at a time.
+struct Computer {
+  int pe = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<int> fifo;
+  std::int64_t head_done = 0;  // query tokens of the head request already run
+  bool stop = false;
+  std::thread th;
+  // gpu backend
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  std::int32_t* d_slot = nullptr;          // device copy of the block tables (by tab_off)
+  std::uint64_t* d_digest = nullptr;       // [request][L]
+  std::int32_t* h_wt = nullptr;            // mapped pinned: the forward's gate tickets
+  std::uint32_t* h_wg = nullptr;           // ... and targets
 };
 
 // One reader engine's transfer pipeline: a FIFO worker (storage NIC, then
@@ -94,6 +115,14 @@ class Live {
       for (std::int32_t s = pool_slots_ - 1; s >= 0; --s) free_slots_[p].push_back(s);
     occupant_.assign(static_cast<std::size_t>(n_pe_) * pool_slots_, {-1, 0});
     reader_bytes_.assign(n_eng_, 0);
+    prefill_ = o_.exec.prefill;
+    if (prefill_) {
+      if (!(o_.exec.compute_quota > 0)) throw std::invalid_argument("run_live: exec.compute_quota must be > 0");
+      for (int p = 0; p < n_pe_; ++p) {
+        computers_.push_back(std::make_unique<Computer>());
+        computers_.back()->pe = p;
+      }
+    }
     if (o_.gpu) setup_gpu(total_blk);
     else {
       tab_slot_h_ = new std::int32_t[std::max<std::int64_t>(1, total_blk)];
@@ -129,8 +158,28 @@ class Live {
     readers_.clear();
   }
 
+  void shutdown_computers() {
+    for (auto& c : computers_) {
+      {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->stop = true;
+      }
+      c->cv.notify_all();
+      if (c->th.joinable()) c->th.join();
+    }
+  }
+
   ~Live() {
     shutdown_readers();
+    shutdown_computers();
+    for (auto& c : computers_) {
+      if (c->done) cudaEventDestroy(c->done);
+      if (c->d_slot) cudaFree(c->d_slot);
+      if (c->d_digest) cudaFree(c->d_digest);
+      if (c->h_wt) cudaFreeHost(c->h_wt);
+      if (c->h_wg) cudaFreeHost(c->h_wg);
+      if (c->stream) detail::release_stream(devs_[c->pe], c->stream);
+    }
     for (dp_nic* n : nics_) dp_nic_destroy(n);
     for (dp_stager* s : stagers_) dp_stager_destroy(s);
     for (auto& row : views_)
@@ -158,6 +207,10 @@ class Live {
       rd->engine = e;
       rd->worker = std::thread([this, rd] { worker(rd); });
       rd->completer = std::thread([this, rd] { completer(rd); });
+    }
+    for (auto& c : computers_) {
+      Computer* cp = c.get();
+      cp->th = std::thread([this, cp] { compute(cp); });
     }
     if (!o_.arrival_times.empty() && o_.arrival_times.size() != trajs_.size())
       throw std::invalid_argument("run_live: one arrival time per trajectory");
@@ -204,7 +257,10 @@ class Live {
     }
     rep_.wall_s = now();
     shutdown_readers();
+    shutdown_computers();
     if (o_.gpu && !stop_) final_occupants();
+    if (o_.gpu && prefill_) final_digests();
+    rep_.forwards = forwards_;
     for (auto& q : reqs_) rep_.requests.push_back(q.r);
     rep_.reader_bytes = reader_bytes_;
     rep_.pool_slots = pool_slots_;
@@ -428,7 +484,8 @@ class Live {
       it = admission_.erase(it);
       if (q.r.cached == 0) {  // no hit KV: nothing to read (desim.cpp:709)
         q.r.t_read_done = q.r.t_landed = q.r.t_admit;
-        handle({Msg::Landed, id});
+        if (prefill_) to_compute(q);
+        else handle({Msg::Landed, id});
         continue;
       }
       Reader* rd = readers_[q.r.reader].get();
@@ -448,10 +505,20 @@ class Live {
       if (o_.sim.policy != pdsim::desim::Policy::Oracle) read_q_[node_of(q.r.reader)] -= q.r.cached;
       return;
     }
-    // the hit KV is in the PE pool: the load path's PE release (desim.cpp:646-647)
-    if (q.r.t_landed < 0) q.r.t_landed = now();
-    const double ttft = q.r.t_landed - q.r.t_arrival;
-    rep_.ttft_series.emplace_back(q.r.t_landed, ttft);
+    if (m.kind == Msg::Landed) {
+      if (q.r.t_landed < 0) q.r.t_landed = now();
+      if (prefill_) {  // the PE holds the request until its prefill is done
+        if (!o_.gpu) to_compute(q);  // timed backend: no counters to gate on
+        return;
+      }
+    } else {
+      q.r.t_prefilled = now();
+    }
+    // the load path's PE release at landing, or with the prefill at its end
+    // (on_prefill_side_done, desim.cpp:642-652)
+    const double t_rel = prefill_ ? q.r.t_prefilled : q.r.t_landed;
+    const double ttft = t_rel - q.r.t_arrival;
+    rep_.ttft_series.emplace_back(t_rel, ttft);
     if (o_.slo_ttft_s > 0 && ttft > o_.slo_ttft_s) {  // the SLO stop (desim.cpp:679-685)
       rep_.slo_violated = true;
       stop_ = true;
@@ -506,10 +573,108 @@ class Live {
           }
         }
         rd->cv.notify_all();
+        if (prefill_ && o_.gpu) to_compute(q);  // launched: the forwards gate on its landed counters
       }
     } catch (const std::exception& ex) {
       fail_async(ex.what());
     }
+  }
+
+  void to_compute(const Req& q) {
+    Computer* c = computers_[q.r.pe].get();
+    {
+      std::lock_guard<std::mutex> lk(c->mu);
+      c->fifo.push_back(q.r.id);
+    }
+    c->cv.notify_all();
+  }
+
+  // ---- prefill stand-in (exec.prefill) ---------------------------------
+  void compute(Computer* c) {
+    try {
+      if (o_.gpu) check_cuda(cudaSetDevice(devs_[c->pe]), "cudaSetDevice");
+      pdsim::SchedulerParams sp;
+      sp.compute_quota = o_.exec.compute_quota;
+      std::vector<pdsim::BatchItem> window;
+      std::vector<dp_attend_item> att;
+      for (;;) {
+        std::int64_t head_done;
+        {
+          std::unique_lock<std::mutex> lk(c->mu);
+          c->cv.wait(lk, [c] { return c->stop || !c->fifo.empty(); });
+          if (c->stop) return;
+          window.clear();
+          for (std::size_t i = 0; i < c->fifo.size(); ++i) {
+            const Req& q = reqs_[c->fifo[i]];
+            window.push_back({q.r.id, q.r.cached, q.r.append - (i == 0 ? c->head_done : 0)});
+          }
+          head_done = c->head_done;
+        }
+        const pdsim::ForwardBatch fb = pdsim::build_forward_batch(window, sp, o_.exec.prefill_cost);
+        if (o_.gpu) {
+          run_forward(c, fb, head_done, att);
+        } else {
+          std::this_thread::sleep_for(std::chrono::duration<double>(fb.estimated_time * L_));
+        }
+        std::vector<int> finished;
+        {
+          std::lock_guard<std::mutex> lk(c->mu);
+          for (std::size_t k = 0; k < fb.items.size(); ++k) ++reqs_[fb.items[k].request_id].r.forwards;
+          for (std::int64_t k = 0; k < fb.consumed_whole; ++k) {
+            finished.push_back(c->fifo.front());
+            c->fifo.pop_front();
+          }
+          if (fb.chunked)
+            c->head_done = fb.consumed_whole == 0 ? c->head_done + fb.chunk_bsz : fb.chunk_bsz;
+          else
+            c->head_done = 0;
+        }
+        forwards_ += 1;
+        for (int id : finished) post({Msg::Prefilled, id});
+      }
+    } catch (const std::exception& ex) {
+      fail_async(ex.what());
+    }
+  }
+
+  // One forward: the block tables of its requests to the device, then per
+  // layer the gate on the landed counters of the requests it reads first and
+  // K5 over its items; waits for the forward to finish.
+  void run_forward(Computer* c, const pdsim::ForwardBatch& fb, std::int64_t head_done,
+                   std::vector<dp_attend_item>& att) {
+    att.clear();
+    std::int32_t n_gate = 0;
+    for (std::size_t k = 0; k < fb.items.size(); ++k) {
+      const Req& q = reqs_[fb.items[k].request_id];
+      dp_attend_item a{};
+      a.cached = q.r.cached;
+      a.q_begin = k == 0 ? head_done : 0;
+      a.bsz = fb.items[k].bsz;
+      a.digest = c->d_digest + static_cast<std::int64_t>(q.r.id) * L_;
+      a.req = static_cast<std::uint32_t>(q.r.id);
+      a.slot = c->d_slot + q.tab_off;
+      if (a.q_begin == 0 && q.n_blk > 0) {  // read here first: its table, and a gate on its KV
+        check_cuda(cudaMemcpyAsync(c->d_slot + q.tab_off, tab_slot_h_ + q.tab_off, q.n_blk * sizeof(std::int32_t),
+                                   cudaMemcpyHostToDevice, c->stream),
+                   "cudaMemcpyAsync block table");
+        if (n_gate >= kMaxGates) throw std::runtime_error("run_live: more gated requests in a forward than the gate table");
+        c->h_wt[n_gate] = q.r.id;
+        c->h_wg[n_gate] = static_cast<std::uint32_t>(q.n_blk) * items_per_block_;
+        ++n_gate;
+      }
+      att.push_back(a);
+    }
+    for (std::int32_t l = 0; l < L_; ++l) {
+      if (n_gate > 0)
+        check(dp_wait_tickets(pools_[c->pe], c->h_wt, c->h_wg, n_gate, l, o_.exec.wait_timeout_ms, c->stream),
+              "dp_wait_tickets (forward gate)");
+      check(dp_prefill_attend(pools_[c->pe], l, att.data(), static_cast<std::int32_t>(att.size()), o_.exec.seed,
+                              c->stream),
+            "dp_prefill_attend");
+    }
+    check_cuda(cudaEventRecord(c->done, c->stream), "cudaEventRecord");
+    check_cuda(cudaEventSynchronize(c->done), "forward sync");
+    check(dp_wait_status(pools_[c->pe]), "forward gate watchdog");
   }
 
   void completer(Reader* rd) {
@@ -583,6 +748,21 @@ class Live {
             "dp_pool_create");
       pools_.push_back(pool);
     }
+    check(dp_layer_items(&geom, 1, &items_per_block_), "dp_layer_items");
+    for (auto& c : computers_) {
+      DeviceScope ds(devs_[c->pe]);
+      c->stream = detail::acquire_stream(devs_[c->pe]);
+      check_cuda(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaMalloc(reinterpret_cast<void**>(&c->d_slot), std::max<std::int64_t>(1, total_blk) * 4),
+                 "cudaMalloc block tables");
+      const std::size_t dig = static_cast<std::size_t>(std::max<std::int64_t>(1, total_reqs_)) * L_ * 8;
+      check_cuda(cudaMalloc(reinterpret_cast<void**>(&c->d_digest), dig), "cudaMalloc digests");
+      check_cuda(cudaMemset(c->d_digest, 0, dig), "cudaMemset digests");
+      check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&c->h_wt), kMaxGates * 4, cudaHostAllocMapped),
+                 "cudaHostAlloc gates");
+      check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&c->h_wg), kMaxGates * 4, cudaHostAllocMapped),
+                 "cudaHostAlloc gates");
+    }
     views_.assign(n_eng_, std::vector<dp_pool*>(n_pe_, nullptr));
     for (int e = 0; e < n_eng_; ++e)
       for (int p = 0; p < n_pe_; ++p)
@@ -608,6 +788,18 @@ class Live {
     check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
     check_cuda(cudaEventRecord(ev, s), "cudaEventRecord");
     return ev;
+  }
+
+  void final_digests() {
+    for (auto& c : computers_) {
+      DeviceScope ds(devs_[c->pe]);
+      std::vector<std::uint64_t> d(static_cast<std::size_t>(std::max<std::int64_t>(1, total_reqs_)) * L_);
+      check_cuda(cudaMemcpy(d.data(), c->d_digest, d.size() * 8, cudaMemcpyDeviceToHost), "digests D2H");
+      for (const Req& q : reqs_)
+        if (q.r.pe == c->pe && q.r.t_prefilled >= 0)
+          rep_.digests.push_back({q.r.id, d[static_cast<std::size_t>(q.r.id) * L_],
+                                  d[static_cast<std::size_t>(q.r.id) * L_ + L_ - 1]});
+    }
   }
 
   void final_occupants() {
@@ -652,6 +844,11 @@ class Live {
   std::int64_t total_reqs_ = 0, completed_ = 0, fb_stride_ = 1, store_fb_ = 1, tab_used_ = 0;
   bool stop_ = false;
   bool arrived_in_wake_ = false;
+  bool prefill_ = false;
+  static constexpr std::int32_t kMaxGates = 4096;
+  std::int32_t items_per_block_ = 1;
+  std::atomic<std::int64_t> forwards_{0};
+  std::vector<std::unique_ptr<Computer>> computers_;
   double next_steady_ = 0;
   std::int32_t pool_slots_ = 0;
   Clock::time_point t0_;

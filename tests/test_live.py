@@ -47,14 +47,21 @@ def replay(rep, alpha, beta, z=1.05):
     return n
 
 
-def check_lifecycle(rep, trajs):
+def check_lifecycle(rep, trajs, prefill=False, gpu=False):
     reqs = rep["requests"]
     assert len(reqs) == sum(len(t.rounds) for t in trajs)
     assert len(rep["decisions"]) == len(reqs)
     by_traj = {}
     for r in reqs:
-        rid, traj, rnd, C, A, G, pe, de, path, reader, t_arr, t_sched, t_admit, t_read, t_land, t_done = r
+        rid, traj, rnd, C, A, G, pe, de, path, reader, t_arr, t_sched, t_admit, t_read, t_land, t_done = r[:16]
+        t_pref, n_fwd = r[16:18]
         assert 0 <= t_arr <= t_sched <= t_admit <= t_read <= t_land <= t_done
+        if prefill:  # the PE release after its last forward, before the turn completes
+            assert n_fwd >= 1 and t_admit <= t_pref <= t_done
+            if not gpu:
+                assert t_land <= t_pref
+        else:
+            assert t_pref == -1 and n_fwd == 0
         assert reader == (pe if path == 0 else de)
         by_traj.setdefault(traj, []).append((rnd, t_arr, t_done))
     for turns in by_traj.values():  # a session's next turn arrives after the previous completes
@@ -149,3 +156,63 @@ def test_live_online_slo_stop_and_arrivals():
     steady = dp.run_live(cluster(1, 1), trajs, exec=ex, gpu=False, link_Bps=8e9, arrival_times=arrivals,
                          steady_window=0.002, steady_lookback=0.01, steady_threshold=0.9)
     assert steady["steady_state"] or steady["completed_requests"] == steady["total_requests"]
+
+
+def prefill_exec(quota_s=2e-4, tops=2e12):
+    """exec options of the live prefill stand-in: forwards under a compute
+    quota of quota_s per layer, cost model b / tops per (query, key) token."""
+    ex = dp.ExecOptions()
+    ex.prefill = True
+    ex.compute_quota = quota_s
+    ex.prefill_cost = (576 / tops, 0.0, 0.0, 2e-6)
+    return ex
+
+
+@needs_ref
+@pytest.mark.parametrize("P,D,policy", [(1, 1, "dual_path"), (2, 2, "dual_path"), (2, 2, "pe_only")])
+def test_live_prefill_timed(P, D, policy):
+    """Live mode with the prefill stand-in (timed backend): each PE packs its
+    landed requests into quota-bounded forwards, the PE is released after a
+    request's last forward (so tok_e / seq_e cover prefill, as the
+    reference's on_prefill_side_done), TTFT = arrival -> prefill done, and
+    every scheduler invocation still replays through the reference."""
+    trajs = dp.synthesize(max_len=16000, count=4 * (P + D), seed=12, mean_turns=4, sigma_turns=0)
+    ex = prefill_exec()
+    ex.storage_cap_Bps = 2e9
+    rep = dp.run_live(cluster(P, D), trajs, policy=policy, alpha=20000, beta=60000, exec=ex, gpu=False,
+                      link_Bps=8e9, decode_s_per_token=2e-6)
+    check_lifecycle(rep, trajs, prefill=True)
+    replay(rep, 20000, 60000)
+    assert rep["forwards"] >= 1
+    assert any(r[17] > 1 for r in rep["requests"]) or rep["forwards"] < len(rep["requests"])
+    for (t, ttft), r in zip(sorted(rep["ttft_series"]), sorted(rep["requests"], key=lambda r: r[16])):
+        assert abs(t - r[16]) < 1e-9 and abs(ttft - (r[16] - r[10])) < 1e-9
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("k1,k2", [(0, 0), (3, 2)])
+def test_live_prefill_gpu_digests(de_dev, k1, k2):
+    """Live prefill on the GPU: K5 forwards, gated per layer on the landed
+    counters of the loads the scheduler launched, read every request's hit KV
+    from the PE pool; each request's digest (layers 0 and L-1) equals the
+    oracle's for its full query range, whatever the batching was."""
+    trajs = dp.synthesize(max_len=12000, count=6, seed=4, mean_turns=4, sigma_turns=0)
+    cfg = cluster(1, 1)
+    ex = prefill_exec()
+    ex.seed = 9
+    ex.storage_cap_Bps = 4e9
+    ex.k1_mode, ex.k2_mode = k1, k2
+    rep = dp.run_live(cfg, trajs, exec=ex, devices=[0, de_dev], alpha=20000, beta=60000)
+    check_lifecycle(rep, trajs, prefill=True, gpu=True)
+    replay(rep, 20000, 60000)
+    g = refpy.geom(cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer)
+    reqs = {r[0]: r for r in rep["requests"]}
+    assert len(rep["digests"]) == len(reqs)
+    stride, n_fb, T, L = rep["fb_stride"], rep["store_fb"], cfg.block_size_tokens, cfg.n_layer
+    for rid, d0, d1 in rep["digests"]:
+        r = reqs[rid]
+        traj, C, A = r[1], r[3], r[4]
+        fbs = [(traj * stride + k) % n_fb for k in range(-(-C // T))]
+        assert d0 == refpy.attend_digest(g, 9, fbs, C, rid, 0, 0, A), rid
+        assert d1 == refpy.attend_digest(g, 9, fbs, C, rid, L - 1, 0, A), rid

@@ -47,6 +47,10 @@ def one(a, cfg, trajs, policy, aps, devices):
     ex.seed = 9
     ex.storage_cap_Bps = a.cap_gbps * 1e9
     ex.k1_mode, ex.k2_mode = 3, 2
+    if a.prefill:  # the prefill stand-in (K5 forwards): TTFT = arrival -> prefill done
+        ex.prefill = True
+        ex.compute_quota = a.quota_ms * 1e-3
+        ex.prefill_cost = (576 / (a.attend_tops * 1e12), 0.0, 0.0, 20e-6)
     t0 = time.time()
     rep = dp.run_live(cfg, trajs, policy=policy, exec=ex, arrival_times=arrivals, slo_ttft=a.slo,
                       steady_window=a.steady_window, steady_lookback=a.steady_lookback, steady_threshold=0.1,
@@ -59,7 +63,7 @@ def one(a, cfg, trajs, policy, aps, devices):
             "ttft_p50": round(float(np.percentile(ttft, 50)), 4) if ttft else None,
             "ttft_max": round(max(ttft), 4) if ttft else None,
             "de_path": sum(1 for d in rep["decisions"] if d[4] == 1), "decisions": len(rep["decisions"]),
-            "read_gb": [round(x / 1e9, 2) for x in rep["reader_bytes"]]}
+            "read_gb": [round(x / 1e9, 2) for x in rep["reader_bytes"]], "forwards": rep["forwards"]}
 
 
 def capacity(a, cfg, trajs, policy, devices):
@@ -99,6 +103,11 @@ def main():
     ap.add_argument("--beta", type=int, default=500000)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--cpu", action="store_true", help="timed backend (no GPU): host check of the tool")
+    ap.add_argument("--prefill", action="store_true",
+                    help="run the prefill stand-in (K5 forwards under the compute quota) on the PEs; the PE "
+                         "is released and the TTFT taken when a request's prefill is done")
+    ap.add_argument("--quota-ms", type=float, default=0.5, help="--prefill: compute quota per layer")
+    ap.add_argument("--attend-tops", type=float, default=40.0, help="--prefill: K5 speed of the cost model")
     a = ap.parse_args()
     P, D = (int(x) for x in a.pd.split(":"))
     L, b = 61, 576
@@ -113,7 +122,9 @@ def main():
     out = {"what": "online APS capacity (sessions/s within the load-TTFT SLO), live-mode scheduling on "
                    "measured completions", "pd": a.pd, "sessions": a.sessions, "turns": a.turns,
            "cap_gbps_per_engine": a.cap_gbps, "slo_s": a.slo, "decode_ms_per_token": a.decode_ms,
-           "devices": devices, "backend": "timed" if a.cpu else "gpu"}
+           "devices": devices, "backend": "timed" if a.cpu else "gpu",
+           "ttft": "arrival -> prefill done (K5 forwards)" if a.prefill else "arrival -> hit KV landed",
+           "prefill": {"quota_ms": a.quota_ms, "attend_tops": a.attend_tops} if a.prefill else None}
     for policy in ("dual_path", "pe_only"):
         cap, runs = capacity(a, cfg, trajs, policy, devices)
         out[policy] = {"capacity_aps": round(cap, 4), "runs": runs}

@@ -1,5 +1,6 @@
 // ThreadSanitizer driver for the live-mode runtime's host threads (scheduler
-// loop, per-reader worker and completion threads, the shared dp_nic) on the
+// loop, per-reader worker and completion threads, per-PE prefill threads,
+// the shared dp_nic) on the
 // timed backend: no CUDA work, so every reported race is in this repo's
 // host code.  Built and run by tools/sanitize/tsan_live.sh.
 #include <cstdio>
@@ -25,7 +26,7 @@ int main() {
   const auto trajs = pdsim::synthesize(spec);
   std::size_t total = 0;
   for (const auto& t : trajs) total += t.rounds.size();
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 4; ++mode) {
     dualpath::LiveOptions o;
     o.gpu = false;
     o.link_Bps = 8e9;
@@ -35,6 +36,12 @@ int main() {
     o.sim.sched.beta = 60000;
     if (mode == 1) o.sim.sched_mode = pdsim::desim::SchedMode::RoundRobin;
     if (mode == 2) o.pe_pool_slots = 260;  // tight: admission stalls
+    if (mode == 3) {  // the prefill stand-in: per-PE compute threads, release after the last forward
+      o.exec.prefill = true;
+      o.exec.compute_quota = 2e-4;
+      o.exec.prefill_cost.coeff_bilinear = 576 / 2e12;
+      o.exec.prefill_cost.constant = 2e-6;
+    }
     const auto rep = dualpath::run_live(cfg, trajs, o);
     std::printf("mode %d: %zu requests (%zu expected), %zu invocations, %lld stalls, %.3f s\n", mode,
                 rep.requests.size(), total, rep.invocations.size(),
