@@ -84,6 +84,8 @@ def parse():
                     help="also persist generated tokens (decode stand-in + K4 D2H), implies --handoff")
     ap.add_argument("--handoff-ctas", type=int, default=0, help="K3 CTA cap on PEs (0 = default)")
     ap.add_argument("--k3-tma", action="store_true", help="K3's hit push through the TMA (bulk copies)")
+    ap.add_argument("--persist-mode", default="kernel", choices=["kernel", "staged"],
+                    help="K4 (PersistD2H): SM zero-copy stores, or a gather into an HBM ring + copy engine")
     ap.add_argument("--k3", default="kernel", choices=["kernel", "ce"],
                     help="K3 (PD handoff push): SM kernel, or copy engines + a small side kernel per layer")
     ap.add_argument("--no-layerwise", action="store_true",
@@ -505,6 +507,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     opt.handoff_layerwise = not args.no_layerwise
     opt.handoff_tma = args.k3_tma
     opt.k3_mode = 1 if args.k3 == "ce" else 0
+    opt.persist_mode = 1 if args.persist_mode == "staged" else 0
     opt.gather_ctas = args.gather_ctas
     opt.seed = 9
     if args.tier:
@@ -1031,6 +1034,7 @@ def main():
                         "stage_scatter": args.stage_scatter,
                         "handoff_ctas": args.handoff_ctas or None,
                         "k3": args.k3 if (args.handoff or args.persist) else None,
+                        "k4": args.persist_mode if args.persist else None,
                         "buffer_stalls": info["buffer_stalls"],
                         "buffer_wait_ms": round(info["buffer_wait_ms"], 1)},
             "model_prediction_gbps": round(info["model_gbps"], 3) if info["model_gbps"] else None,

@@ -98,6 +98,10 @@ struct ExecOptions {
   // the decode stand-in for the generated tokens and persists them (K4) every
   // 64 generated tokens plus the final partial, into its persist store
   bool persist = false;
+  // K4: 0 = the SM kernel's zero-copy stores over PCIe (dp_persist_d2h),
+  // 1 = staged: a gather kernel into an HBM ring of its own, then the copy
+  // engine to the host (dp_persist_staged)
+  std::int32_t persist_mode = 0;
   // PersistWrite (desim.cpp:764-771): a FullBlockFile (record r = storage Full
   // Block r) each DE writes the Full Blocks its K4 persisted into at the end of
   // its step, so a later turn's StorageRead from the tier reads them back;
@@ -341,7 +345,9 @@ class EngineRuntime {
   void* ev_end_ = nullptr;
   dp_store* store_ = nullptr;
   dp_nic* nic_ = nullptr;                   // emulated storage NIC (rate cap)
+  dp_stager* persist_stager_ = nullptr;      // staged K4 (persist_mode 1): its own ring
   dp_stager* stager_ = nullptr;             // staged K1 / K2: HBM ring (k1_mode 3 / k2_mode 2)
+  std::int64_t persist_launches() const;
   std::int64_t stager_launches() const;
   const std::int32_t* stage_slots() const;
   std::int64_t buffer_budget() const;

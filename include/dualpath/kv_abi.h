@@ -367,6 +367,16 @@ int dp_h2d_push_staged(dp_pool* pe_view, const dp_store* de_src, dp_stager* stag
 int dp_h2d_push_dual_staged(dp_pool* pe_view, dp_pool* de_pool, const dp_store* de_src, dp_stager* stager,
                             const dp_dual_job* jobs, int32_t n_jobs, dp_stream de_stream);
 
+/* K4 staged (PersistD2H at the copy engine's rate): a gather kernel packs the
+ * spans' tokens from the decode pool into Full Blocks of the stager's HBM
+ * ring, the copy engine moves them to `target` (whole blocks as 1D runs, a
+ * partial block as one 2D copy of its L token ranges); consecutive spans of
+ * one request are merged.  The same bytes as dp_persist_d2h; later work on
+ * `stream` sees them in host memory.  fb HOST-readable, slot device-readable.
+ * Use a stager of its own (not one a loader uses on another stream). */
+int dp_persist_staged(const dp_pool* de_pool, dp_store* target, dp_stager* stager, const dp_span_job* jobs,
+                      int32_t n_jobs, dp_stream stream);
+
 /* Cap on the CTAs a K1/K2 launch on `device` may use (0 = default, 4 per SM).
  * The transfer is PCIe-bound, so a few CTAs keep the link full while leaving
  * the SMs to the prefill compute (the isolation knob of config 4). */

@@ -109,6 +109,7 @@ def lib():
         "dp_prefill_handoff_copy": ([P, P, ctypes.POINTER(HandoffJob), ctypes.c_int32, ctypes.c_uint64,
                                      ctypes.c_int32, P], ctypes.c_int),
         "dp_handoff_copy_launches": ([ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "dp_persist_staged": ([P, P, P, ctypes.POINTER(SpanJob), ctypes.c_int32, P], ctypes.c_int),
         "dp_layer_items": ([ctypes.POINTER(Geom), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
                            ctypes.c_int),
         "dp_wait_layer": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int32, P],
@@ -415,6 +416,11 @@ def decode_fill(pool, jobs, n, seed, stream=0):
 
 def persist_d2h(pool, target, jobs, n, stream=0):
     check(lib().dp_persist_d2h(pool.ptr, target.ptr, jobs, n, ctypes.c_void_p(stream)))
+
+
+def persist_staged(pool, target, stager, jobs, n, stream=0):
+    """K4 staged; the jobs' fb arrays must be host memory, slot arrays device memory."""
+    check(lib().dp_persist_staged(pool.ptr, target.ptr, stager.ptr, jobs, n, ctypes.c_void_p(stream)))
 
 
 def wait_status(pool):

@@ -434,6 +434,7 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("handoff_layerwise", &dualpath::ExecOptions::handoff_layerwise)
       .def_readwrite("handoff_tma", &dualpath::ExecOptions::handoff_tma)
       .def_readwrite("k3_mode", &dualpath::ExecOptions::k3_mode)
+      .def_readwrite("persist_mode", &dualpath::ExecOptions::persist_mode)
       .def_readwrite("handoff_ctas", &dualpath::ExecOptions::handoff_ctas)
       .def_readwrite("persist", &dualpath::ExecOptions::persist)
       .def_readwrite("store_fb", &dualpath::ExecOptions::store_fb)

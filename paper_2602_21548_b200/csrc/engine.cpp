@@ -126,6 +126,9 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
     if (x.persist && !x.by_de[engine_].empty())  // content seed + 1: unwritten bytes differ
       check(dp_store_create(device_, &x.geom, x.store_fb, x.opt.seed + 1, &persist_store_),
             "dp_store_create (persist store)");
+    if (x.persist && x.opt.persist_mode == 1 && !x.by_de[engine_].empty())
+      check(dp_stager_create(device_, &x.geom, x.opt.stage_ring_bytes, &persist_stager_),
+            "dp_stager_create (persist)");
     if (x.persist && !x.opt.persist_path.empty() && !x.by_de[engine_].empty())
       persist_file_ = std::make_unique<FullBlockFile>(x.opt.persist_path, x.geom, x.store_fb, false, false);
   }
@@ -179,6 +182,7 @@ EngineRuntime::~EngineRuntime() {
     if (v) dp_pool_destroy(v);
   if (pool_) dp_pool_destroy(pool_);
   dp_stager_destroy(stager_);
+  dp_stager_destroy(persist_stager_);
   if (store_) dp_store_destroy(store_);
   dp_nic_destroy(nic_);
   if (persist_store_) dp_store_destroy(persist_store_);
@@ -554,6 +558,12 @@ std::int64_t EngineRuntime::buffer_budget() const {
 // host memory for the copy-engine scatter.
 const std::int32_t* EngineRuntime::stage_slots() const {
   return plan_->opt.stage_scatter == DP_SCATTER_CE ? plan_->slots[engine_].data() : d_slots_;
+}
+
+std::int64_t EngineRuntime::persist_launches() const {
+  std::int64_t n = 0;
+  if (persist_stager_) check(dp_stager_launches(persist_stager_, &n), "dp_stager_launches");
+  return n;
 }
 
 std::int64_t EngineRuntime::stager_launches() const {

@@ -290,8 +290,17 @@ StepResult EngineRuntime::run_step_handoff() {
       std::vector<dp_span_job> chunks;
       for (const auto& [t0, t1] : x.persist_chunks(j))
         chunks.push_back(dp_span_job{fill.slot, fill.fb, blk0, t0, t1, nb, 0});
-      check(dp_persist_d2h(pool_, persist_store_, chunks.data(), static_cast<int32_t>(chunks.size()), h),
-            "dp_persist_d2h");
+      if (persist_stager_) {  // staged: the block tables' host copy plans the copies
+        for (dp_span_job& c : chunks) c.fb = x.dec_fb[engine_].data() + j.dec_off + blk0;
+        const std::int64_t l0 = persist_launches();
+        check(dp_persist_staged(pool_, persist_store_, persist_stager_, chunks.data(),
+                                static_cast<int32_t>(chunks.size()), h),
+              "dp_persist_staged");
+        res.launches += persist_launches() - l0 - 1;  // its kernels (K4 is counted below)
+      } else {
+        check(dp_persist_d2h(pool_, persist_store_, chunks.data(), static_cast<int32_t>(chunks.size()), h),
+              "dp_persist_d2h");
+      }
       check(dp_stream_write_counter(pool_, j.de_ticket + x.n_de_tickets[engine_], L, 1, h),
             "dp_stream_write_counter");
       res.launches += 3;

@@ -1634,7 +1634,7 @@ __global__ void __launch_bounds__(kThreads) kv_handoff_side(const __grid_constan
 // of layers [l0, l1), the descriptors split over as many launches as the
 // parameter block needs (the releases and gates ride on the first).
 int launch_side(HoSideParams& p, const std::vector<HoMissDesc>& miss, int l0, int l1, int r0, int r1, bool gate,
-                cudaStream_t s, int64_t* launches) {
+                cudaStream_t s, int64_t* launches, int max_ctas = kHoSideCtas) {
   const int32_t n_rel = p.n_rel, n_gate = p.n_gate;
   if (!gate) p.n_gate = 0;
   p.miss_l0 = l0;
@@ -1650,7 +1650,7 @@ int launch_side(HoSideParams& p, const std::vector<HoMissDesc>& miss, int l0, in
     const bool work = (p.n_rel > 0 && r1 > r0) || (l1 > l0 && (p.n_gate > 0 || n > 0));
     if (work) {
       const int64_t units = static_cast<int64_t>(n) * std::max(0, l1 - l0);
-      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, kHoSideCtas)));
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, max_ctas)));
       kv_handoff_side<<<grid, kThreads, 0, s>>>(p);
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
@@ -1671,6 +1671,17 @@ int launch_side(HoSideParams& p, const std::vector<HoMissDesc>& miss, int l0, in
 }
 
 std::atomic<int64_t> g_handoff_copy_launches{0};  // side kernels, process-wide
+
+// Per device: a helper stream on which the no-gate K3 copy path writes the
+// miss KV while the copy engine pushes the hit runs (created once, kept).
+std::mutex g_aux_mu;
+cudaStream_t g_aux_stream[kMaxDevices] = {};
+
+cudaStream_t aux_stream(int device) {
+  std::lock_guard<std::mutex> lk(g_aux_mu);
+  if (!g_aux_stream[device]) cudaStreamCreateWithFlags(&g_aux_stream[device], cudaStreamNonBlocking);
+  return g_aux_stream[device];
+}
 
 }  // namespace
 
@@ -1768,13 +1779,30 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
   }
   int64_t launches = 0;
   if (p.n_gate == 0) {
-    // no gates: one 2D copy per run (rows = layers), then the miss KV of
-    // every layer, then the releases of every layer
+    // no gates: one 2D copy per run (rows = layers) on `stream` while the
+    // miss KV of every layer is written from a forked helper stream (both
+    // cross NVLink at once), then the releases of every layer
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (!miss.empty()) {
+      aux = aux_stream(pe_pool->device);
+      if (!aux) return fail(DP_ECUDA, "prefill_handoff_copy: helper stream");
+      DP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      DP_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+      DP_CUDA(cudaEventRecord(fork, s));
+      DP_CUDA(cudaStreamWaitEvent(aux, fork, 0));
+      if (int rc = launch_side(p, miss, 0, L, 0, 0, false, aux, &launches, 2 * sm_count(pe_pool->device)))
+        return rc;
+      DP_CUDA(cudaEventRecord(join, aux));
+    }
     for (const Run& r : runs)
       DP_CUDA(cudaMemcpy2DAsync(de_view->base + r.de_off, de_plane, pe_pool->base + r.pe_off, pe_plane, r.bytes,
                                 L, cudaMemcpyDeviceToDevice, s));
-    if (!miss.empty())
-      if (int rc = launch_side(p, miss, 0, L, 0, 0, false, s, &launches)) return rc;
+    if (join) {
+      DP_CUDA(cudaStreamWaitEvent(s, join, 0));
+      cudaEventDestroy(fork);  // released once their work completes
+      cudaEventDestroy(join);
+    }
     if (int rc = launch_side(p, {}, 0, 0, 0, L, false, s, &launches)) return rc;
   } else {
     // layer by layer: side(l) = release of l - 1, the gates of l, the miss
@@ -2533,6 +2561,145 @@ int dp_h2d_push_dual_staged(dp_pool* pe_view, dp_pool* de_pool, const dp_store* 
     }
   }
   return flush();
+}
+
+}  // extern "C"
+
+// ================================================ K4 staged (PersistD2H)
+// dp_persist_staged: the gather kernel (kv_persist_d2h with the ring as its
+// target) packs each span's tokens from the decode pool's layer planes into
+// Full Blocks [L][T][b] of the HBM ring; the copy engine moves them to the
+// host Full Blocks: a run of whole blocks as one 1D copy, a partial block as
+// one 2D copy of its L token ranges.  Consecutive spans of one request (the
+// 64-token persist chunks) are merged first, so only a request's first and
+// last blocks are partial.
+namespace {
+
+int persist_copy(dp_stager* st, dp_store* target, const dp_span_job& job, int64_t pos0) {
+  const dp_kv_geom& g = st->geom;
+  const int64_t T = g.block_tokens, b = g.bytes_per_token_layer;
+  const int64_t lb = T * b, fbb = lb * g.n_layer;
+  for (int32_t i = 0; i < job.n_blk;) {
+    const int64_t bt0 = (job.blk0 + i) * T;
+    const int64_t t0 = std::max(job.tok_begin, bt0) - bt0, t1 = std::min(job.tok_end, bt0 + T) - bt0;
+    if (t1 <= t0) {
+      ++i;
+      continue;
+    }
+    if (t0 == 0 && t1 == T) {  // whole blocks: runs of consecutive target Full Blocks
+      int32_t run = 1;
+      while (i + run < job.n_blk && job.fb[i + run] == job.fb[i] + run &&
+             (job.blk0 + i + run + 1) * T <= job.tok_end)
+        ++run;
+      DP_CUDA(cudaMemcpyAsync(target->host + job.fb[i] * fbb, st->ring.host + (pos0 + i) * fbb, run * fbb,
+                              cudaMemcpyDeviceToHost, st->copy));
+      i += run;
+      continue;
+    }
+    DP_CUDA(cudaMemcpy2DAsync(target->host + job.fb[i] * fbb + t0 * b, lb, st->ring.host + (pos0 + i) * fbb + t0 * b,
+                              lb, (t1 - t0) * b, g.n_layer, cudaMemcpyDeviceToHost, st->copy));
+    ++i;
+  }
+  return DP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dp_persist_staged(const dp_pool* de_pool, dp_store* target, dp_stager* st, const dp_span_job* jobs,
+                      int32_t n_jobs, dp_stream stream) {
+  if (!de_pool || !target || !st || (n_jobs > 0 && !jobs) || n_jobs < 0)
+    return fail(DP_EINVAL, "persist_staged: null argument");
+  if (!de_pool->owner) return fail(DP_EINVAL, "persist_staged: the decode pool must be local");
+  if (de_pool->device != st->device) return fail(DP_EINVAL, "persist_staged: pool and stager on different devices");
+  if (!geom_equal(de_pool->geom, target->geom) || !geom_equal(st->geom, target->geom))
+    return fail(DP_EINVAL, "persist_staged: geometry differs");
+  const dp_kv_geom& g = target->geom;
+  const int64_t T = g.block_tokens;
+  // merge consecutive spans of one request (same tables, contiguous tokens)
+  std::vector<dp_span_job> merged;
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    const dp_span_job& job = jobs[j];
+    if (job.n_blk < 0 || job.blk0 < 0 || job.tok_begin < job.blk0 * T || job.tok_end < job.tok_begin ||
+        job.tok_end > (job.blk0 + job.n_blk) * T || (job.n_blk > 0 && (!job.slot || !job.fb)))
+      return fail(DP_EINVAL, "persist_staged: job " + std::to_string(j) + " out of range");
+    for (int32_t i = 0; i < job.n_blk; ++i)
+      if (job.fb[i] < 0 || job.fb[i] >= target->n_fb)
+        return fail(DP_EINVAL, "persist_staged: job " + std::to_string(j) + ": target block out of range");
+    if (job.tok_end == job.tok_begin || job.n_blk == 0) continue;
+    if (!merged.empty()) {
+      dp_span_job& m = merged.back();
+      if (m.slot == job.slot && m.fb == job.fb && m.blk0 == job.blk0 && m.n_blk == job.n_blk &&
+          m.tok_end == job.tok_begin) {
+        m.tok_end = job.tok_end;
+        continue;
+      }
+    }
+    merged.push_back(job);
+  }
+  DeviceGuard guard(st->device);
+  auto s = static_cast<cudaStream_t>(stream);
+  struct Part {
+    dp_span_job job;  // host fb table, ring positions from pos0
+    int64_t pos0;
+  };
+  std::vector<dp_span_job> sub;  // kernel view: fb = ring positions
+  std::vector<Part> parts;
+  int64_t used = 0;
+  bool open = false;
+  int last_seg = -1;
+  auto flush = [&]() -> int {
+    if (!open) return DP_OK;
+    const int seg = st->seg;
+    if (int rc = launch_span(de_pool, &st->ring, sub.data(), static_cast<int32_t>(sub.size()), 0, stream,
+                             kv_persist_d2h, "persist_staged"))
+      return rc;
+    ++st->launches;
+    DP_CUDA(cudaEventRecord(st->ev_copied[seg], s));  // gathered into the segment
+    DP_CUDA(cudaStreamWaitEvent(st->copy, st->ev_copied[seg], 0));
+    for (const Part& pt : parts)
+      if (int rc = persist_copy(st, target, pt.job, pt.pos0)) return rc;
+    DP_CUDA(cudaEventRecord(st->ev_free[seg], st->copy));  // drained to the host
+    last_seg = seg;
+    st->seg = (seg + 1) % kStageSegs;
+    sub.clear();
+    parts.clear();
+    used = 0;
+    open = false;
+    return DP_OK;
+  };
+  for (const dp_span_job& job : merged) {
+    // blocks holding none of the span are skipped
+    int32_t first = 0, end = job.n_blk;
+    while (first < end && (job.blk0 + first + 1) * T <= job.tok_begin) ++first;
+    while (end > first && (job.blk0 + end - 1) * T >= job.tok_end) --end;
+    for (int32_t i0 = first; i0 < end;) {
+      if (open && (used == st->seg_fb || sub.size() == DP_MAX_SPAN_JOBS_PER_LAUNCH))
+        if (int rc = flush()) return rc;
+      if (!open) {  // the gather into the segment waits for the copies that last drained it
+        DP_CUDA(cudaStreamWaitEvent(s, st->ev_free[st->seg], 0));
+        open = true;
+      }
+      const int32_t i1 = static_cast<int32_t>(std::min<int64_t>(end, i0 + (st->seg_fb - used)));
+      const int64_t base = st->seg * st->seg_fb + used;
+      dp_span_job part = job;
+      part.blk0 = job.blk0 + i0;
+      part.n_blk = i1 - i0;
+      part.tok_begin = std::max(job.tok_begin, part.blk0 * T);
+      part.tok_end = std::min(job.tok_end, (part.blk0 + part.n_blk) * T);
+      part.slot = job.slot + i0;
+      part.fb = job.fb + i0;
+      parts.push_back({part, base});
+      part.fb = st->iota + base;
+      sub.push_back(part);
+      used += i1 - i0;
+      i0 = i1;
+    }
+  }
+  if (int rc = flush()) return rc;
+  if (last_seg >= 0) DP_CUDA(cudaStreamWaitEvent(s, st->ev_free[last_seg], 0));  // later work sees the host bytes
+  return DP_OK;
 }
 
 }  // extern "C"

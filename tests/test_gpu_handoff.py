@@ -257,6 +257,65 @@ def test_decode_fill_then_persist_d2h(gpus, L, T, b, P, gen):
         pool.close()
 
 
+@pytest.mark.parametrize("L,T,b", [(6, 64, 576), (3, 64, 4096), (61, 64, 576)])
+@pytest.mark.parametrize("P,gen", [(64 * 3 + 10, 330), (128, 64 * 5), (5, 1), (64 * 2 + 63, 2)])
+def test_persist_staged(gpus, L, T, b, P, gen):
+    """K4 staged: the persist chunks of a request (64 generated tokens each +
+    the final partial) gathered into the HBM ring and copied to the host
+    Full Blocks by the copy engine (whole blocks 1D, partial ones 2D), with
+    a ring of 2 Full Blocks per segment so the spans cross segments: the
+    same bytes as dp_persist_d2h, nothing outside the spans touched."""
+    g = abi.geom(L, T, b)
+    total = P + gen
+    blk0, blk1 = P // T, -(-total // T)
+    n = blk1 - blk0
+    pool = abi.Pool(0, g, 16, 1)
+    target = abi.Store(0, g, 24, SEED + 1)
+    stager = abi.Stager(0, g, 2 * L * T * b * 4)  # 4 segments of 2 Full Blocks
+    try:
+        slots = np.arange(3, 3 + n, dtype=np.int32)
+        fbs = (np.arange(n) * 2 + 1).astype(np.int64)  # non-consecutive targets, plus a run below
+        if n > 3:
+            fbs[1:4] = [14, 15, 16]
+        ds, df = dev(slots, 0, np.int32), dev(fbs, 0, np.int64)
+        fill = (abi.SpanJob * 1)()
+        fill[0] = abi.SpanJob(ds.data_ptr(), df.data_ptr(), blk0, P, total, n, 0)
+        abi.decode_fill(pool, fill, 1, SEED)
+        chunks, done = [], 0
+        for k in list(range(T, gen, T)) + [gen]:
+            if k > done:
+                chunks.append((P + done, P + k))
+                done = k
+        jobs = (abi.SpanJob * len(chunks))()
+        for i, (t0, t1) in enumerate(chunks):
+            jobs[i] = abi.SpanJob(ds.data_ptr(), fbs.ctypes.data, blk0, t0, t1, n, 0)
+        l0 = stager.launches()
+        abi.persist_staged(pool, target, stager, jobs, len(chunks))
+        sync_all()
+        assert stager.launches() > l0
+        img = np.frombuffer(target.bytes(), dtype=np.uint8)
+        gr = refpy.geom(L, T, b)
+        fb_bytes, lb = L * T * b, T * b
+        for i in range(n):
+            k = blk0 + i
+            a, z = max(P, k * T) - k * T, min(total, (k + 1) * T) - k * T
+            for layer in range(L):
+                full = refpy.layer_block(gr, SEED, int(fbs[i]), layer, T)
+                other = refpy.layer_block(gr, SEED + 1, int(fbs[i]), layer, T)
+                off = int(fbs[i]) * fb_bytes + layer * lb
+                got = img[off:off + lb]
+                assert np.array_equal(got[a * b:z * b], full[a * b:z * b]), (i, layer)
+                assert np.array_equal(got[:a * b], other[:a * b])
+                assert np.array_equal(got[z * b:], other[z * b:])
+        untouched = set(range(24)) - set(int(f) for f in fbs)
+        for f in untouched:
+            off = f * fb_bytes
+            assert np.array_equal(img[off:off + lb], refpy.layer_block(gr, SEED + 1, f, 0, T))
+    finally:
+        for x in (stager, target, pool):
+            x.close()
+
+
 @pytest.mark.parametrize("L,T,b,C", [(8, 64, 576, 64 * 9 + 5), (4, 64, 4096, 64 * 5), (61, 64, 576, 64 * 3 + 1)])
 def test_dual_staged(de_dev, L, T, b, C):
     """The DE read path fused with DecodeH2D, staged (copy engine into the

@@ -117,21 +117,26 @@ def k3(a, g, L, T, b, n_fb, n_slots, ce=False, contiguous=False):
         st.close()
 
 
-def k4(a, g, L, T, b, n_fb, n_slots):
+def k4(a, g, L, T, b, n_fb, n_slots, staged=False):
     """K4 alone (PersistD2H): every token of a.jobs requests of a.blocks blocks
     gathered from the decode pool into storage Full Blocks in pinned host
-    memory (zero-copy stores over PCIe D2H)."""
+    memory (zero-copy stores over PCIe D2H; staged: gather into an HBM ring,
+    copy engine to the host)."""
     pool = abi.Pool(0, g, n_slots, 1)
     target = abi.Store(0, g, n_fb, 10)
+    stager = abi.Stager(0, g) if staged else None
     try:
         rng = np.random.default_rng(0)
-        keep, spans = [], (abi.SpanJob * a.jobs)()
+        keep, spans, hspans = [], (abi.SpanJob * a.jobs)(), (abi.SpanJob * a.jobs)()
         perm = rng.permutation(n_slots)
         for j in range(a.jobs):
             fbs = torch.tensor(rng.integers(0, n_fb, a.blocks), dtype=torch.int64, device="cuda:0")
             sl = torch.tensor(perm[(j * a.blocks) % n_slots:][:a.blocks].astype(np.int32), device="cuda:0")
-            keep += [fbs, sl]
+            fbs_h = fbs.cpu().numpy()
+            keep += [fbs, sl, fbs_h]
             spans[j] = abi.SpanJob(sl.data_ptr(), fbs.data_ptr(), 0, 0, a.blocks * T, a.blocks, 0)
+            if staged:
+                hspans[j] = abi.SpanJob(sl.data_ptr(), fbs_h.ctypes.data, 0, 0, a.blocks * T, a.blocks, 0)
         abi.decode_fill(pool, spans, a.jobs, 9)
         torch.cuda.synchronize(0)
         nbytes = a.jobs * a.blocks * T * b * L
@@ -141,7 +146,10 @@ def k4(a, g, L, T, b, n_fb, n_slots):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            abi.persist_d2h(pool, target, spans, a.jobs, s.cuda_stream)
+            if staged:
+                abi.persist_staged(pool, target, stager, hspans, a.jobs, s.cuda_stream)
+            else:
+                abi.persist_d2h(pool, target, spans, a.jobs, s.cuda_stream)
             e1.record(s)
             e1.synchronize()
             if r:
@@ -162,6 +170,8 @@ def k4(a, g, L, T, b, n_fb, n_slots):
             best = min(best, e0.elapsed_time(e1))
         return {"bytes": nbytes, "ms": ms, "GBps": nbytes / ms / 1e6, "ce_d2h_GBps": (1 << 30) / best / 1e6}
     finally:
+        if stager:
+            stager.close()
         pool.close()
         target.close()
 
@@ -228,6 +238,7 @@ def main():
         out["ce_peer_copy"] = ce_peer()
     if a.k4:
         out["k4"] = k4(a, g, L, T, b, n_fb, n_slots)
+        out["k4_staged"] = k4(a, g, L, T, b, n_fb, n_slots, staged=True)
     print(json.dumps(out))
 
 
