@@ -88,8 +88,9 @@ def parse():
                     help="K4 (PersistD2H): SM zero-copy stores, or a gather into an HBM ring + copy engine")
     ap.add_argument("--k3", default="kernel", choices=["kernel", "ce"],
                     help="K3 (PD handoff push): SM kernel, or copy engines + a small side kernel per layer")
-    ap.add_argument("--no-layerwise", action="store_true",
-                    help="handoff + prefill: K3 after a request's last forward instead of layer by layer")
+    ap.add_argument("--layerwise", action="store_true",
+                    help="handoff + prefill: K3 pushes layer l as soon as the finishing forward has computed it "
+                         "(the reference's order), instead of after the forward (the default: measured faster)")
     ap.add_argument("--gather-ctas", type=int, default=-1, help="K1/K2 CTA cap (-1 = auto)")
     ap.add_argument("--prefill", action="store_true",
                     help="run the prefill stand-in on every PE: compute-quota batched forwards "
@@ -504,7 +505,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     opt.handoff = bool(args.handoff or args.persist)
     opt.persist = bool(args.persist)
     opt.handoff_ctas = args.handoff_ctas
-    opt.handoff_layerwise = not args.no_layerwise
+    opt.handoff_layerwise = args.layerwise
     opt.handoff_tma = args.k3_tma
     opt.k3_mode = 1 if args.k3 == "ce" else 0
     opt.persist_mode = 1 if args.persist_mode == "staged" else 0
@@ -1097,7 +1098,7 @@ def main():
                 "what": "per request (rank 0's PE, last timed step): step start -> whole prompt KV in "
                         "its DE's decode pool (offline TTFT of the prefill path); lag = that minus the end "
                         "of the forward that finishes it",
-                "layerwise": not args.no_layerwise,
+                "layerwise": args.layerwise,
                 "ttft_mean": round(sum(tt) / len(tt), 3), "ttft_p50": round(tt[len(tt) // 2], 3),
                 "ttft_p99": round(tt[min(len(tt) - 1, int(len(tt) * 0.99))], 3),
                 "lag_mean": round(sum(lag) / len(lag), 3), "lag_p99": round(lag[min(len(lag) - 1, int(len(lag) * 0.99))], 3)}

@@ -93,7 +93,9 @@ struct ExecOptions {
   // MissMerge of layer l at LayerCompute l's completion, desim.cpp:630-640,
   // :721-738), gated in-kernel on per-(forward, layer) done counters the
   // compute stream writes; false: K3 waits for the forward's last layer
-  bool handoff_layerwise = true;
+  // (default false: measured slower with the CUDA-core prefill stand-in, whose
+  // forwards lose SM residency to the spinning K3 CTAs -- profiles/r02_SUMMARY.md)
+  bool handoff_layerwise = false;
   // Decode-side persistence (needs `handoff`): each DE runs
   // the decode stand-in for the generated tokens and persists them (K4) every
   // 64 generated tokens plus the final partial, into its persist store

@@ -159,14 +159,13 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   if (ctas < 0) ctas = !is_pe() ? 0 : x.prefill ? 32 : x.handoff ? 64 : 0;
   check(dp_set_gather_ctas(device_, ctas), "dp_set_gather_ctas");
   if (is_pe() && x.handoff) check(dp_set_handoff_tma(x.opt.handoff_tma ? 1 : 0), "dp_set_handoff_tma");
-  // layerwise K3 CTAs wait in-kernel for the forward's layers: one per SM (a
-  // 40-register K3 CTA fits beside the two K5 CTAs of an SM, a second would not)
-  if (is_pe()) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
-    check(dp_set_handoff_ctas(device_, x.opt.handoff_ctas ? x.opt.handoff_ctas : layerwise_handoff() ? sms : 0),
+  // layerwise K3 CTAs wait in-kernel for the forward's layers: 64 of them.
+  // One per SM hung the 1P1D pipeline (profiles/r02_g15_pf_lw148_HANG.txt):
+  // with a spinning K3 CTA resident on every SM, a producer the gates wait
+  // for could not be scheduled; 64 leave SMs free of spinners.
+  if (is_pe())
+    check(dp_set_handoff_ctas(device_, x.opt.handoff_ctas ? x.opt.handoff_ctas : layerwise_handoff() ? 64 : 0),
           "dp_set_handoff_ctas");
-  }
   if (is_pe() && x.prefill) check(dp_set_attend_ctas(device_, x.opt.attend_ctas), "dp_set_attend_ctas");
 }
 

@@ -5,6 +5,7 @@ stream.  --ctas sweeps the gather CTA cap (dp_set_gather_ctas).  Used plain
 and under ncu (profiles/)."""
 
 import argparse
+import ctypes
 import json
 import os
 import sys
@@ -168,7 +169,23 @@ def k4(a, g, L, T, b, n_fb, n_slots, staged=False):
             e1.record(s)
             e1.synchronize()
             best = min(best, e0.elapsed_time(e1))
-        return {"bytes": nbytes, "ms": ms, "GBps": nbytes / ms / 1e6, "ce_d2h_GBps": (1 << 30) / best / 1e6}
+        # the same copy into the target store's own pages (NUMA-bound,
+        # registered): the ceiling for K4, whose bytes land there
+        rt = ctypes.CDLL("libcudart.so.12")
+        rt.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+        host, tbytes, _ = target.info()
+        n = min(1 << 30, tbytes)
+        best_st = 1e9
+        for _ in range(3):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            assert rt.cudaMemcpyAsync(host, d.data_ptr(), n, 2, s.cuda_stream) == 0  # cudaMemcpyDeviceToHost
+            e1.record(s)
+            e1.synchronize()
+            best_st = min(best_st, e0.elapsed_time(e1))
+        return {"bytes": nbytes, "ms": ms, "GBps": nbytes / ms / 1e6, "ce_d2h_GBps": (1 << 30) / best / 1e6,
+                "ce_d2h_store_GBps": n / best_st / 1e6}
     finally:
         if stager:
             stager.close()
