@@ -86,7 +86,7 @@ def parse():
     ap.add_argument("--k3-tma", action="store_true", help="K3's hit push through the TMA (bulk copies)")
     ap.add_argument("--persist-mode", default="kernel", choices=["kernel", "staged"],
                     help="K4 (PersistD2H): SM zero-copy stores, or a gather into an HBM ring + copy engine")
-    ap.add_argument("--k3", default="kernel", choices=["kernel", "ce"],
+    ap.add_argument("--k3", default="ce", choices=["kernel", "ce"],
                     help="K3 (PD handoff push): SM kernel, or copy engines + a small side kernel per layer")
     ap.add_argument("--layerwise", action="store_true",
                     help="handoff + prefill: K3 pushes layer l as soon as the finishing forward has computed it "

@@ -86,8 +86,9 @@ struct ExecOptions {
   bool handoff_tma = false;            // K3's hit push through the TMA (dp_set_handoff_tma)
   // K3: 0 = the SM kernel (dp_prefill_handoff), 1 = the copy engines push the
   // hit runs over NVLink and a small side kernel per layer does the gates,
-  // the miss KV and the releases (dp_prefill_handoff_copy)
-  std::int32_t k3_mode = 0;
+  // the miss KV and the releases (dp_prefill_handoff_copy; the default: 749 vs
+  // 702 GB/s alone, and no SM pushes beside the prefill)
+  std::int32_t k3_mode = 1;
   // handoff + prefill: K3 pushes layer l of a request as soon as the forward
   // that finishes it has computed layer l (the reference starts PeToDe /
   // MissMerge of layer l at LayerCompute l's completion, desim.cpp:630-640,

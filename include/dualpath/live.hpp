@@ -25,7 +25,14 @@
 // the PE is released when the request's last forward has computed its last
 // layer (on_prefill_side_done, desim.cpp:642-652); a turn's TTFT is then
 // arrival -> that point.  The DE holds the request for gen x
-// decode_s_per_token.
+// decode_s_per_token.  With exec.handoff too, the PE pool holds each
+// request's whole prompt, the DE read path is the dual gather (PE pool +
+// the DE's decode pool), and after the forward that finishes a request K3
+// (PeToDe / MissMerge, exec.k3_mode) moves its prompt into the DE's decode
+// pool; the PE releases it when K3 is done (every layer computed and
+// shipped) and its first token follows one decode step: TTFT as the
+// reference's (desim.cpp:679-685).  Admission also reserves the prompt's
+// decode-pool slots (bounded: de_pool_slots).
 // Admission reserves the request's blocks in the PE's paged pool (bounded:
 // pe_pool_slots) and stalls, FIFO, while the pool is full -- the staging
 // bound of try_admit (desim.cpp:587-599).
@@ -52,6 +59,7 @@ struct LiveOptions {
   pdsim::desim::SimOptions sim;      // policy, sched_mode, scheduler parameters
   ExecOptions exec;                  // storage cap, content seed, k1 / k2 modes, store size
   std::int32_t pe_pool_slots = 0;    // paged pool per PE; 0 = 4x the largest request's blocks
+  std::int32_t de_pool_slots = 0;    // exec.handoff: decode pool per DE; 0 = 4x the largest prompt's blocks
   double decode_s_per_token = 0;     // emulated decode on the DE after the KV has landed
   bool gpu = true;                   // false: timed backend (transfers sleep bytes / link_Bps)
   double link_Bps = 50e9;            // timed backend: per-reader transfer rate
@@ -110,6 +118,9 @@ struct LiveReport {
     std::uint64_t hash_first = 0, hash_last = 0;
   };
   std::vector<Occupant> final_slots;
+  // exec.handoff: the same for every DE's decode pool (pe = the DE's engine id):
+  // the whole prompt of its final occupant
+  std::vector<Occupant> final_decode_slots;
   // gpu backend with exec.prefill: the K5 digest of every prefilled request at
   // layers 0 and L-1 (parity vs the oracle: independent of the batching)
   struct Digest {

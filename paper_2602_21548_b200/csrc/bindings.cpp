@@ -636,7 +636,7 @@ PYBIND11_MODULE(_core, m) {
          const dualpath::ExecOptions& exec, std::int32_t pe_pool_slots, double decode_s_per_token, bool gpu,
          double link_Bps, const std::vector<int>& devices, double timeout_s,
          const std::vector<double>& arrival_times, double slo_ttft, double steady_window,
-         double steady_lookback, double steady_threshold) {
+         double steady_lookback, double steady_threshold, std::int32_t de_pool_slots) {
         dualpath::LiveOptions o;
         o.arrival_times = arrival_times;
         o.slo_ttft_s = slo_ttft;
@@ -647,6 +647,7 @@ PYBIND11_MODULE(_core, m) {
         o.sim.sched.z_factor = z;
         o.exec = exec;
         o.pe_pool_slots = pe_pool_slots;
+        o.de_pool_slots = de_pool_slots;
         o.decode_s_per_token = decode_s_per_token;
         o.gpu = gpu;
         o.link_Bps = link_Bps;
@@ -695,6 +696,10 @@ PYBIND11_MODULE(_core, m) {
         for (const auto& x : rep.final_slots)
           occ.append(py::make_tuple(x.pe, x.slot, x.fb, x.ntok, x.hash_first, x.hash_last));
         d["final_slots"] = occ;
+        py::list docc;
+        for (const auto& x : rep.final_decode_slots)
+          docc.append(py::make_tuple(x.pe, x.slot, x.fb, x.ntok, x.hash_first, x.hash_last));
+        d["final_decode_slots"] = docc;
         py::list dig;
         for (const auto& x : rep.digests) dig.append(py::make_tuple(x.req, x.first, x.last));
         d["digests"] = dig;
@@ -718,7 +723,8 @@ PYBIND11_MODULE(_core, m) {
       py::arg("decode_s_per_token") = 0.0, py::arg("gpu") = true, py::arg("link_Bps") = 50e9,
       py::arg("devices") = std::vector<int>{}, py::arg("timeout_s") = 600.0,
       py::arg("arrival_times") = std::vector<double>{}, py::arg("slo_ttft") = 0.0,
-      py::arg("steady_window") = 0.0, py::arg("steady_lookback") = 180.0, py::arg("steady_threshold") = 0.05);
+      py::arg("steady_window") = 0.0, py::arg("steady_lookback") = 180.0, py::arg("steady_threshold") = 0.05,
+      py::arg("de_pool_slots") = 0);
 
   m.def(
       "run_step_all",

@@ -31,8 +31,10 @@ using Clock = std::chrono::steady_clock;
 struct Req {
   LiveRequest r;
   std::int64_t total() const { return r.cached + r.append + r.gen; }
-  std::int32_t n_blk = 0;
-  std::int64_t tab_off = 0;  // its blocks in the slot / Full Block tables
+  std::int32_t n_blk = 0;     // hit blocks ceil(C / T)
+  std::int32_t n_pblk = 0;    // prompt blocks ceil((C + A) / T)
+  std::int32_t n_tab = 0;     // its table entries: n_pblk with the handoff, else n_blk
+  std::int64_t tab_off = 0;   // its blocks in the slot / Full Block tables
 };
 
 struct Msg {
@@ -91,11 +93,14 @@ class Live {
     T_ = cfg_.block_size_tokens;
     L_ = cfg_.n_layer;
     // every turn of every session, ids in arrival order are assigned at arrival
+    prefill_ = o_.exec.prefill;
+    handoff_ = o_.exec.handoff;
+    if (handoff_ && !prefill_) throw std::invalid_argument("run_live: exec.handoff needs exec.prefill");
     std::int64_t max_blk = 1, total_blk = 0;
     for (const auto& t : trajs_) {
       fb_stride_ = std::max(fb_stride_, pdsim::blocks_for(t.total_tokens(), cfg_));
       for (std::size_t k = 0; k < t.rounds.size(); ++k) {
-        const std::int64_t c = pdsim::context_before(t, k);
+        const std::int64_t c = pdsim::context_before(t, k) + (handoff_ ? t.rounds[k].append_tokens : 0);
         const std::int64_t nb = (c + T_ - 1) / T_;
         max_blk = std::max(max_blk, nb);
         total_blk += nb;
@@ -114,8 +119,16 @@ class Live {
     for (int p = 0; p < n_pe_; ++p)
       for (std::int32_t s = pool_slots_ - 1; s >= 0; --s) free_slots_[p].push_back(s);
     occupant_.assign(static_cast<std::size_t>(n_pe_) * pool_slots_, {-1, 0});
+    if (handoff_) {  // decode pools: each DE holds the whole prompt of the requests it decodes
+      de_slots_ = o_.de_pool_slots > 0 ? o_.de_pool_slots : static_cast<std::int32_t>(4 * max_blk);
+      if (de_slots_ < max_blk)
+        throw pdsim::desim::ConfigError("run_live: de_pool_slots smaller than the largest prompt");
+      free_de_.assign(n_eng_ - n_pe_, {});
+      for (auto& fl : free_de_)
+        for (std::int32_t s = de_slots_ - 1; s >= 0; --s) fl.push_back(s);
+      de_occupant_.assign(static_cast<std::size_t>(n_eng_ - n_pe_) * de_slots_, {-1, 0});
+    }
     reader_bytes_.assign(n_eng_, 0);
-    prefill_ = o_.exec.prefill;
     if (prefill_) {
       if (!(o_.exec.compute_quota > 0)) throw std::invalid_argument("run_live: exec.compute_quota must be > 0");
       for (int p = 0; p < n_pe_; ++p) {
@@ -127,6 +140,7 @@ class Live {
     else {
       tab_slot_h_ = new std::int32_t[std::max<std::int64_t>(1, total_blk)];
       tab_fb_h_ = new std::int64_t[std::max<std::int64_t>(1, total_blk)];
+      tab_de_h_ = new std::int32_t[std::max<std::int64_t>(1, total_blk)];
     }
     for (int e = 0; e < n_eng_; ++e) {
       dp_nic* nic = nullptr;
@@ -189,12 +203,18 @@ class Live {
     for (dp_store* s : stores_) dp_store_destroy(s);
     for (std::size_t e = 0; e < streams_.size(); ++e)
       if (streams_[e]) detail::release_stream(devs_[e], streams_[e]);
+    for (auto& row : de_views_)
+      for (dp_pool* v : row)
+        if (v) dp_pool_destroy(v);
+    for (dp_pool* p : de_pools_) dp_pool_destroy(p);
     if (o_.gpu) {
       if (tab_slot_h_) cudaFreeHost(tab_slot_h_);
       if (tab_fb_h_) cudaFreeHost(tab_fb_h_);
+      if (tab_de_h_) cudaFreeHost(tab_de_h_);
     } else {
       delete[] tab_slot_h_;
       delete[] tab_fb_h_;
+      delete[] tab_de_h_;
     }
   }
 
@@ -305,8 +325,10 @@ class Live {
     q.r.gen = tr.rounds[round].gen_tokens;
     q.r.t_arrival = now();
     q.n_blk = static_cast<std::int32_t>((q.r.cached + T_ - 1) / T_);
+    q.n_pblk = static_cast<std::int32_t>((q.r.cached + q.r.append + T_ - 1) / T_);
+    q.n_tab = handoff_ ? q.n_pblk : q.n_blk;
     q.tab_off = tab_used_;
-    tab_used_ += q.n_blk;
+    tab_used_ += q.n_tab;
     reqs_.push_back(q);
     de_global_.push_back(q.r.id);
     arrived_in_wake_ = true;
@@ -466,18 +488,29 @@ class Live {
     for (auto it = admission_.begin(); it != admission_.end();) {
       Req& q = reqs_[*it];
       auto& fl = free_slots_[q.r.pe];
-      if (static_cast<std::int64_t>(fl.size()) < q.n_blk) {
+      auto* dl = handoff_ ? &free_de_[q.r.de - n_pe_] : nullptr;
+      if (static_cast<std::int64_t>(fl.size()) < q.n_tab ||
+          (dl && static_cast<std::int64_t>(dl->size()) < q.n_pblk)) {
         stalled = true;
         ++it;
         continue;
       }
-      for (std::int32_t k = 0; k < q.n_blk; ++k) {
+      // the PE pool holds the hit KV, with the handoff the whole prompt (the
+      // prefill writes the miss KV there); the DE's decode pool the prompt
+      const std::int64_t held = handoff_ ? q.r.cached + q.r.append : q.r.cached;
+      for (std::int32_t k = 0; k < q.n_tab; ++k) {
         const std::int32_t s = fl.back();
         fl.pop_back();
         tab_slot_h_[q.tab_off + k] = s;
         tab_fb_h_[q.tab_off + k] = fb_of(q.r.traj, k);
-        occupant_[static_cast<std::size_t>(q.r.pe) * pool_slots_ + s] = {
-            tab_fb_h_[q.tab_off + k], static_cast<std::int32_t>(std::min<std::int64_t>(T_, q.r.cached - k * T_))};
+        const auto ntok = static_cast<std::int32_t>(std::min<std::int64_t>(T_, held - k * T_));
+        occupant_[static_cast<std::size_t>(q.r.pe) * pool_slots_ + s] = {tab_fb_h_[q.tab_off + k], ntok};
+        if (dl) {
+          const std::int32_t d = dl->back();
+          dl->pop_back();
+          tab_de_h_[q.tab_off + k] = d;
+          de_occupant_[static_cast<std::size_t>(q.r.de - n_pe_) * de_slots_ + d] = {tab_fb_h_[q.tab_off + k], ntok};
+        }
       }
       q.r.t_admit = now();
       const int id = q.r.id;
@@ -517,8 +550,12 @@ class Live {
     // the load path's PE release at landing, or with the prefill at its end
     // (on_prefill_side_done, desim.cpp:642-652)
     const double t_rel = prefill_ ? q.r.t_prefilled : q.r.t_landed;
-    const double ttft = t_rel - q.r.t_arrival;
-    rep_.ttft_series.emplace_back(t_rel, ttft);
+    // with the handoff the prompt is in the DE's decode pool at t_rel (the
+    // DecodeH2D is done): the first token follows one decode step
+    // (on_decode_token k = 1, desim.cpp:679-685)
+    const double t_tok = handoff_ ? t_rel + o_.decode_s_per_token : t_rel;
+    const double ttft = t_tok - q.r.t_arrival;
+    rep_.ttft_series.emplace_back(t_tok, ttft);
     if (o_.slo_ttft_s > 0 && ttft > o_.slo_ttft_s) {  // the SLO stop (desim.cpp:679-685)
       rep_.slo_violated = true;
       stop_ = true;
@@ -526,7 +563,7 @@ class Live {
     tok_[q.r.pe] -= q.total();
     seq_[q.r.pe] -= 1;
     auto& fl = free_slots_[q.r.pe];
-    for (std::int32_t k = 0; k < q.n_blk; ++k) fl.push_back(tab_slot_h_[q.tab_off + k]);
+    for (std::int32_t k = 0; k < q.n_tab; ++k) fl.push_back(tab_slot_h_[q.tab_off + k]);
     if (o_.decode_s_per_token > 0)
       timers_.push({now() + static_cast<double>(q.r.gen) * o_.decode_s_per_token, q.r.id});
     else
@@ -536,6 +573,10 @@ class Live {
   void complete(int id) {  // request done on its DE (desim.cpp:776-787), then the next turn
     Req& q = reqs_[id];
     q.r.t_done = now();
+    if (handoff_) {  // the decode pool's slots are free once the request is done
+      auto& dl = free_de_[q.r.de - n_pe_];
+      for (std::int32_t k = 0; k < q.n_pblk; ++k) dl.push_back(tab_de_h_[q.tab_off + k]);
+    }
     tok_[q.r.de] -= q.total();
     seq_[q.r.de] -= 1;
     hbm_free_[q.r.de] += q.total();
@@ -614,7 +655,12 @@ class Live {
         if (o_.gpu) {
           run_forward(c, fb, head_done, att);
         } else {
-          std::this_thread::sleep_for(std::chrono::duration<double>(fb.estimated_time * L_));
+          double ho = 0;  // the handoff of the requests this forward finishes
+          for (std::int64_t k = 0; handoff_ && k < fb.consumed_whole; ++k) {
+            const Req& q = reqs_[fb.items[k].request_id];
+            ho += static_cast<double>((q.r.path == 0 ? q.r.cached : 0) + q.r.append) * cfg_.kv_bytes_per_token();
+          }
+          std::this_thread::sleep_for(std::chrono::duration<double>(fb.estimated_time * L_ + ho / o_.link_Bps));
         }
         std::vector<int> finished;
         {
@@ -672,6 +718,30 @@ class Live {
                               c->stream),
             "dp_prefill_attend");
     }
+    if (handoff_) {
+      // PeToDe / MissMerge of the requests this forward finishes (K3, after
+      // the forward on its stream): the whole prompt into the DE's decode
+      // pool, the PE path pushing the hit KV too (desim.cpp:630-652)
+      std::vector<std::vector<dp_handoff_job>> by_de(n_eng_ - n_pe_);
+      for (std::int64_t k = 0; k < fb.consumed_whole; ++k) {
+        const Req& q = reqs_[fb.items[k].request_id];
+        if (q.n_pblk == 0) continue;
+        by_de[q.r.de - n_pe_].push_back(dp_handoff_job{tab_fb_h_ + q.tab_off, tab_slot_h_ + q.tab_off,
+                                                       tab_de_h_ + q.tab_off, q.r.cached, q.r.cached + q.r.append,
+                                                       q.n_pblk, q.r.path == 0 ? 1 : 0, -1, 0, q.r.id, -1});
+      }
+      for (std::size_t d = 0; d < by_de.size(); ++d) {
+        if (by_de[d].empty()) continue;
+        dp_pool* view = de_views_[c->pe][d];
+        const auto n = static_cast<std::int32_t>(by_de[d].size());
+        check(o_.exec.k3_mode == 1
+                  ? dp_prefill_handoff_copy(pools_[c->pe], view, by_de[d].data(), n, o_.exec.seed,
+                                            o_.exec.wait_timeout_ms, c->stream)
+                  : dp_prefill_handoff(pools_[c->pe], view, by_de[d].data(), n, o_.exec.seed,
+                                       o_.exec.wait_timeout_ms, c->stream),
+              "prefill handoff (K3)");
+      }
+    }
     check_cuda(cudaEventRecord(c->done, c->stream), "cudaEventRecord");
     check_cuda(cudaEventSynchronize(c->done), "forward sync");
     check(dp_wait_status(pools_[c->pe]), "forward gate watchdog");
@@ -728,6 +798,9 @@ class Live {
     check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&tab_fb_h_), std::max<std::int64_t>(1, total_blk) * 8,
                              cudaHostAllocMapped | cudaHostAllocPortable),
                "cudaHostAlloc tables");
+    check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&tab_de_h_), std::max<std::int64_t>(1, total_blk) * 4,
+                             cudaHostAllocMapped | cudaHostAllocPortable),
+               "cudaHostAlloc tables");
     for (int e = 0; e < n_eng_; ++e) {
       dp_store* st = nullptr;
       check(dp_store_create(devs_[e], &geom, store_fb_, o_.exec.seed, &st), "dp_store_create");
@@ -763,6 +836,19 @@ class Live {
       check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&c->h_wg), kMaxGates * 4, cudaHostAllocMapped),
                  "cudaHostAlloc gates");
     }
+    if (handoff_) {
+      for (int d = n_pe_; d < n_eng_; ++d) {
+        dp_pool* pool = nullptr;
+        check(dp_pool_create(devs_[d], &geom, de_slots_,
+                             static_cast<std::int32_t>(std::max<std::int64_t>(1, total_reqs_)), &pool),
+              "dp_pool_create (decode pool)");
+        de_pools_.push_back(pool);
+      }
+      de_views_.assign(n_pe_, std::vector<dp_pool*>(n_eng_ - n_pe_, nullptr));
+      for (int p = 0; p < n_pe_; ++p)
+        for (int d = 0; d < n_eng_ - n_pe_; ++d)
+          check(dp_pool_peer_view(devs_[p], de_pools_[d], &de_views_[p][d]), "dp_pool_peer_view (decode pool)");
+    }
     views_.assign(n_eng_, std::vector<dp_pool*>(n_pe_, nullptr));
     for (int e = 0; e < n_eng_; ++e)
       for (int p = 0; p < n_pe_; ++p)
@@ -775,7 +861,13 @@ class Live {
     dp_pool* dst = local ? pools_[q.r.pe] : views_[e][q.r.pe];
     dp_job job{tab_fb_h_ + q.tab_off, tab_slot_h_ + q.tab_off, q.r.cached, q.n_blk, 0, L_, q.r.id};
     cudaStream_t s = streams_[e];
-    if (stagers_[e]) {
+    if (handoff_ && !local) {  // the DE read path fused with DecodeH2D: PE pool and the DE's decode pool
+      dp_dual_job dj{job, tab_de_h_ + q.tab_off, q.r.id, 0};
+      dp_pool* de_pool = de_pools_[e - n_pe_];
+      check(stagers_[e] ? dp_h2d_push_dual_staged(dst, de_pool, stores_[e], stagers_[e], &dj, 1, s)
+                        : dp_h2d_push_p2p_dual(dst, de_pool, stores_[e], &dj, 1, s),
+            "dual transfer");
+    } else if (stagers_[e]) {
       check(local ? dp_h2d_layer_staged(dst, stores_[e], stagers_[e], &job, 1, s)
                   : dp_h2d_push_staged(dst, stores_[e], stagers_[e], &job, 1, s),
             "staged transfer");
@@ -803,18 +895,24 @@ class Live {
   }
 
   void final_occupants() {
-    for (int p = 0; p < n_pe_; ++p) {
+    hash_occupants(pools_, occupant_, pool_slots_, 0, rep_.final_slots);
+    if (handoff_) hash_occupants(de_pools_, de_occupant_, de_slots_, n_pe_, rep_.final_decode_slots);
+  }
+
+  void hash_occupants(const std::vector<dp_pool*>& pools, const std::vector<std::pair<std::int64_t, std::int32_t>>& occ,
+                      std::int32_t n_slots, int engine0, std::vector<LiveReport::Occupant>& out) {
+    for (int p = 0; p < static_cast<int>(pools.size()); ++p) {
       std::vector<std::int32_t> slots, ntok;
       std::vector<std::int64_t> fbs;
-      for (std::int32_t s = 0; s < pool_slots_; ++s) {
-        const auto& oc = occupant_[static_cast<std::size_t>(p) * pool_slots_ + s];
+      for (std::int32_t s = 0; s < n_slots; ++s) {
+        const auto& oc = occ[static_cast<std::size_t>(p) * n_slots + s];
         if (oc.first < 0) continue;
         slots.push_back(s);
         fbs.push_back(oc.first);
         ntok.push_back(oc.second);
       }
       if (slots.empty()) continue;
-      DeviceScope ds(devs_[p]);
+      DeviceScope ds(devs_[engine0 + p]);
       const std::size_t n = slots.size();
       std::int32_t *d_s = nullptr, *d_n = nullptr;
       std::uint64_t* d_o = nullptr;
@@ -824,15 +922,15 @@ class Live {
       check_cuda(cudaMemcpy(d_s, slots.data(), n * 4, cudaMemcpyHostToDevice), "H2D");
       check_cuda(cudaMemcpy(d_n, ntok.data(), n * 4, cudaMemcpyHostToDevice), "H2D");
       std::vector<std::uint64_t> h0(n), h1(n);
-      check(dp_pool_checksum(pools_[p], 0, d_s, d_n, static_cast<std::int32_t>(n), d_o, nullptr), "checksum");
+      check(dp_pool_checksum(pools[p], 0, d_s, d_n, static_cast<std::int32_t>(n), d_o, nullptr), "checksum");
       check_cuda(cudaMemcpy(h0.data(), d_o, n * 8, cudaMemcpyDeviceToHost), "D2H");
-      check(dp_pool_checksum(pools_[p], L_ - 1, d_s, d_n, static_cast<std::int32_t>(n), d_o, nullptr), "checksum");
+      check(dp_pool_checksum(pools[p], L_ - 1, d_s, d_n, static_cast<std::int32_t>(n), d_o, nullptr), "checksum");
       check_cuda(cudaMemcpy(h1.data(), d_o, n * 8, cudaMemcpyDeviceToHost), "D2H");
       cudaFree(d_s);
       cudaFree(d_n);
       cudaFree(d_o);
       for (std::size_t i = 0; i < n; ++i)
-        rep_.final_slots.push_back({p, slots[i], fbs[i], ntok[i], h0[i], h1[i]});
+        out.push_back({engine0 + p, slots[i], fbs[i], ntok[i], h0[i], h1[i]});
     }
   }
 
@@ -845,6 +943,13 @@ class Live {
   bool stop_ = false;
   bool arrived_in_wake_ = false;
   bool prefill_ = false;
+  bool handoff_ = false;
+  std::int32_t de_slots_ = 0;
+  std::vector<std::vector<std::int32_t>> free_de_;
+  std::vector<std::pair<std::int64_t, std::int32_t>> de_occupant_;
+  std::vector<dp_pool*> de_pools_;                 // per DE: its decode pool
+  std::vector<std::vector<dp_pool*>> de_views_;    // [pe][de]: decode pools mapped on the PE
+  std::int32_t* tab_de_h_ = nullptr;               // decode-pool slots (by tab_off)
   static constexpr std::int32_t kMaxGates = 4096;
   std::int32_t items_per_block_ = 1;
   std::atomic<std::int64_t> forwards_{0};

@@ -212,10 +212,12 @@ def handoff_engines(xp, n, devices=None):
     return rts
 
 
-@pytest.mark.parametrize("policy,tight,layer_gate,staged", [("dual_path", False, 0, False), ("dual_path", True, 0, False),
-                                                            ("pe_only", True, 0, False), ("dual_path", True, 1, False),
-                                                            ("dual_path", True, 0, True)])
-def test_handoff_1p1d(de_dev, policy, tight, layer_gate, staged):
+@pytest.mark.parametrize("policy,tight,layer_gate,staged,k3", [
+    ("dual_path", False, 0, False, 0), ("dual_path", True, 0, False, 0), ("pe_only", True, 0, False, 0),
+    ("dual_path", True, 1, False, 0), ("dual_path", True, 0, True, 0),
+    # K3 on the copy engines: no gate (2D copies per run), gated per layer (layer_gate 1)
+    ("dual_path", True, 0, True, 1), ("dual_path", True, 1, False, 1), ("pe_only", False, 0, False, 1)])
+def test_handoff_1p1d(de_dev, policy, tight, layer_gate, staged, k3):
     cfg = cluster(1, 1, L=6)
     trajs = small_trace(count=8, turns=5, seed=6)
     planned = dp.plan(cfg, trajs, policy=policy, **STORAGE_BOUND)
@@ -223,6 +225,7 @@ def test_handoff_1p1d(de_dev, policy, tight, layer_gate, staged):
     opt.seed = SEED
     opt.handoff = True
     opt.k3_layer_gate = layer_gate
+    opt.k3_mode = k3
     if staged:  # staged K1 and the staged dual gather (ring smaller than a request)
         opt.k1_mode, opt.k2_mode = 3, 2
         opt.stage_ring_bytes = 16 * 6 * 64 * 576 * 4
@@ -267,8 +270,8 @@ def test_handoff_2p2d_tight(gpus, placement):
         verify_prompt_pool(rt, xp, cfg)
 
 
-@pytest.mark.parametrize("tight", [False, True])
-def test_handoff_with_persistence(de_dev, tight):
+@pytest.mark.parametrize("tight,staged", [(False, False), (True, False), (True, True), (False, True)])
+def test_handoff_with_persistence(de_dev, tight, staged):
     """PD handoff + decode stand-in + K4 persistence: the decode pools end with
     prompt + generated tokens of their last occupants, and every generated
     token of every request is in its DE's persist store, byte for byte."""
@@ -279,6 +282,8 @@ def test_handoff_with_persistence(de_dev, tight):
     opt.seed = SEED
     opt.handoff = True
     opt.persist = True
+    opt.k3_mode = opt.persist_mode = 1 if staged else 0  # copy-engine K3 + staged K4, or the SM kernels
+    opt.stage_ring_bytes = 8 * 4 * 64 * 576  # small persist ring: 4 segments of 2 Full Blocks
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     if tight:
         opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots

@@ -219,10 +219,12 @@ def test_prefill_1p1d_dual_path(de_dev, tight):
         check_digests(pe, cfg, planned, xp)
 
 
-@pytest.mark.parametrize("tight,persist,layerwise,k1", [(False, False, True, 0), (True, False, True, 0),
-                                                     (True, True, True, 0), (True, False, False, 0),
-                                                     (True, True, True, 3)])
-def test_prefill_with_handoff_1p1d(de_dev, tight, persist, layerwise, k1):
+@pytest.mark.parametrize("tight,persist,layerwise,k1,k3,k4", [
+    (False, False, True, 0, 0, 0), (True, False, True, 0, 0, 0), (True, True, True, 0, 0, 0),
+    (True, False, False, 0, 0, 0), (True, True, True, 3, 0, 0),
+    # K3 on the copy engines (gated per layer / after the forward), staged K4
+    (True, False, True, 3, 1, 0), (True, True, False, 3, 1, 1), (False, True, False, 0, 1, 1)])
+def test_prefill_with_handoff_1p1d(de_dev, tight, persist, layerwise, k1, k3, k4):
     """The whole pipeline: loads on both paths, quota-batched K5 forwards on
     the PE, K3 handoff of each prompt -- layer by layer as its finishing
     forward computes each layer (layerwise), or after that forward -- (decode
@@ -241,6 +243,8 @@ def test_prefill_with_handoff_1p1d(de_dev, tight, persist, layerwise, k1):
     opt.prefill_cost = COST
     opt.handoff_layerwise = layerwise
     opt.k1_mode = k1
+    opt.k3_mode = k3
+    opt.persist_mode = k4
     xp = dp.build_exec_plan(cfg, trajs, planned, opt)
     if tight:
         opt.pool_slots, opt.de_pool_slots = xp.peak_slots, xp.de_peak_slots

@@ -216,3 +216,68 @@ def test_live_prefill_gpu_digests(de_dev, k1, k2):
         fbs = [(traj * stride + k) % n_fb for k in range(-(-C // T))]
         for layer, d in ((0, d0), (L - 1, d1)):
             assert d == (refpy.attend_digest(g, 9, fbs, C, rid, layer, 0, A) if C and A else 0), (rid, layer)
+
+
+@needs_ref
+@pytest.mark.parametrize("P,D", [(1, 1), (2, 2)])
+def test_live_handoff_timed(P, D):
+    """Live mode with prefill + PD handoff (timed backend): admission also
+    reserves the prompt's decode-pool slots (a tight decode pool stalls it),
+    the PE releases a request after its K3, and its TTFT includes one decode
+    step after the prompt reached the decode pool."""
+    trajs = dp.synthesize(max_len=16000, count=4 * (P + D), seed=13, mean_turns=4, sigma_turns=0)
+    ex = prefill_exec()
+    ex.handoff = True
+    ex.storage_cap_Bps = 2e9
+    big = max(-(-(dp.context_before(t, k) + t.rounds[k].append_tokens) // 64)
+              for t in trajs for k in range(len(t.rounds)))
+    rep = dp.run_live(cluster(P, D), trajs, alpha=20000, beta=60000, exec=ex, gpu=False, link_Bps=8e9,
+                      decode_s_per_token=2e-6, de_pool_slots=big + 2)
+    check_lifecycle(rep, trajs, prefill=True)
+    replay(rep, 20000, 60000)
+    assert rep["admission_stalls"] > 0  # the decode pool held requests back
+    ttfts = sorted(x[1] for x in rep["ttft_series"])
+    firsts = sorted(r[16] + 2e-6 - r[10] for r in rep["requests"])
+    assert all(abs(a - b) < 1e-9 for a, b in zip(ttfts, firsts))
+
+
+def test_live_handoff_needs_prefill():
+    trajs = dp.synthesize(max_len=8000, count=2, seed=1, mean_turns=2, sigma_turns=0)
+    ex = dp.ExecOptions()
+    ex.handoff = True
+    with pytest.raises(ValueError):
+        dp.run_live(cluster(1, 1), trajs, exec=ex, gpu=False)
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("k1,k2,k3", [(0, 0, 0), (3, 2, 1)])
+def test_live_handoff_gpu(de_dev, k1, k2, k3):
+    """Live prefill + handoff on the GPU: the DE read path is the dual gather,
+    K3 (SM kernel or copy engines) moves each finished prompt into its DE's
+    decode pool; the final occupant of every PE and decode-pool slot holds
+    the whole prompt block the oracle says, and every digest matches."""
+    trajs = dp.synthesize(max_len=12000, count=6, seed=4, mean_turns=4, sigma_turns=0)
+    cfg = cluster(1, 1)
+    ex = prefill_exec()
+    ex.handoff = True
+    ex.seed = 9
+    ex.storage_cap_Bps = 4e9
+    ex.k1_mode, ex.k2_mode, ex.k3_mode = k1, k2, k3
+    rep = dp.run_live(cfg, trajs, exec=ex, devices=[0, de_dev], alpha=20000, beta=60000)
+    check_lifecycle(rep, trajs, prefill=True, gpu=True)
+    replay(rep, 20000, 60000)
+    assert any(r[8] == 1 for r in rep["requests"]) or rep["reader_bytes"][1] == 0
+    g = refpy.geom(cfg.n_layer, cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer)
+    assert rep["final_slots"] and rep["final_decode_slots"]
+    for slots in (rep["final_slots"], rep["final_decode_slots"]):
+        for eng, slot, fb, ntok, h0, h1 in slots:
+            assert h0 == refpy.layer_block_hash(g, 9, fb, 0, ntok), (eng, slot)
+            assert h1 == refpy.layer_block_hash(g, 9, fb, cfg.n_layer - 1, ntok), (eng, slot)
+    reqs = {r[0]: r for r in rep["requests"]}
+    stride, n_fb, T, L = rep["fb_stride"], rep["store_fb"], cfg.block_size_tokens, cfg.n_layer
+    for rid, d0, d1 in rep["digests"]:
+        r = reqs[rid]
+        fbs = [(r[1] * stride + k) % n_fb for k in range(-(-r[3] // T))]
+        for layer, d in ((0, d0), (L - 1, d1)):
+            assert d == (refpy.attend_digest(g, 9, fbs, r[3], rid, layer, 0, r[4]) if r[3] and r[4] else 0)

@@ -51,6 +51,7 @@ def one(a, cfg, trajs, policy, aps, devices):
         ex.prefill = True
         ex.compute_quota = a.quota_ms * 1e-3
         ex.prefill_cost = (576 / (a.attend_tops * 1e12), 0.0, 0.0, 20e-6)
+        ex.handoff = a.handoff  # + K3 into the DE decode pools: TTFT = first token, as the reference's
     t0 = time.time()
     rep = dp.run_live(cfg, trajs, policy=policy, exec=ex, arrival_times=arrivals, slo_ttft=a.slo,
                       steady_window=a.steady_window, steady_lookback=a.steady_lookback, steady_threshold=0.1,
@@ -107,8 +108,13 @@ def main():
                     help="run the prefill stand-in (K5 forwards under the compute quota) on the PEs; the PE "
                          "is released and the TTFT taken when a request's prefill is done")
     ap.add_argument("--quota-ms", type=float, default=0.5, help="--prefill: compute quota per layer")
+    ap.add_argument("--handoff", action="store_true",
+                    help="with --prefill: the PD handoff (dual gather on the DE path, K3 into decode pools); the "
+                         "PE releases after K3 and the TTFT is the first token's")
     ap.add_argument("--attend-tops", type=float, default=40.0, help="--prefill: K5 speed of the cost model")
     a = ap.parse_args()
+    if a.handoff and not a.prefill:
+        ap.error("--handoff needs --prefill")
     P, D = (int(x) for x in a.pd.split(":"))
     L, b = 61, 576
     cfg = cluster(P, D, L, b)
@@ -123,7 +129,8 @@ def main():
                    "measured completions", "pd": a.pd, "sessions": a.sessions, "turns": a.turns,
            "cap_gbps_per_engine": a.cap_gbps, "slo_s": a.slo, "decode_ms_per_token": a.decode_ms,
            "devices": devices, "backend": "timed" if a.cpu else "gpu",
-           "ttft": "arrival -> prefill done (K5 forwards)" if a.prefill else "arrival -> hit KV landed",
+           "ttft": ("arrival -> first token (prefill, K3 handoff, one decode step)" if a.handoff else
+                    "arrival -> prefill done (K5 forwards)") if a.prefill else "arrival -> hit KV landed",
            "prefill": {"quota_ms": a.quota_ms, "attend_tops": a.attend_tops} if a.prefill else None}
     for policy in ("dual_path", "pe_only"):
         cap, runs = capacity(a, cfg, trajs, policy, devices)

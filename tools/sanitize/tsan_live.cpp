@@ -26,7 +26,7 @@ int main() {
   const auto trajs = pdsim::synthesize(spec);
   std::size_t total = 0;
   for (const auto& t : trajs) total += t.rounds.size();
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode = 0; mode < 5; ++mode) {
     dualpath::LiveOptions o;
     o.gpu = false;
     o.link_Bps = 8e9;
@@ -36,11 +36,12 @@ int main() {
     o.sim.sched.beta = 60000;
     if (mode == 1) o.sim.sched_mode = pdsim::desim::SchedMode::RoundRobin;
     if (mode == 2) o.pe_pool_slots = 260;  // tight: admission stalls
-    if (mode == 3) {  // the prefill stand-in: per-PE compute threads, release after the last forward
+    if (mode >= 3) {  // the prefill stand-in: per-PE compute threads, release after the last forward
       o.exec.prefill = true;
       o.exec.compute_quota = 2e-4;
       o.exec.prefill_cost.coeff_bilinear = 576 / 2e12;
       o.exec.prefill_cost.constant = 2e-6;
+      o.exec.handoff = mode == 4;  // + the PD handoff: decode-pool slots, release after K3
     }
     const auto rep = dualpath::run_live(cfg, trajs, o);
     std::printf("mode %d: %zu requests (%zu expected), %zu invocations, %lld stalls, %.3f s\n", mode,
