@@ -1672,17 +1672,6 @@ int launch_side(HoSideParams& p, const std::vector<HoMissDesc>& miss, int l0, in
 
 std::atomic<int64_t> g_handoff_copy_launches{0};  // side kernels, process-wide
 
-// Per device: a helper stream on which the no-gate K3 copy path writes the
-// miss KV while the copy engine pushes the hit runs (created once, kept).
-std::mutex g_aux_mu;
-cudaStream_t g_aux_stream[kMaxDevices] = {};
-
-cudaStream_t aux_stream(int device) {
-  std::lock_guard<std::mutex> lk(g_aux_mu);
-  if (!g_aux_stream[device]) cudaStreamCreateWithFlags(&g_aux_stream[device], cudaStreamNonBlocking);
-  return g_aux_stream[device];
-}
-
 }  // namespace
 
 extern "C" {
@@ -1779,30 +1768,16 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
   }
   int64_t launches = 0;
   if (p.n_gate == 0) {
-    // no gates: one 2D copy per run (rows = layers) on `stream` while the
-    // miss KV of every layer is written from a forked helper stream (both
-    // cross NVLink at once), then the releases of every layer
-    cudaStream_t aux = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    if (!miss.empty()) {
-      aux = aux_stream(pe_pool->device);
-      if (!aux) return fail(DP_ECUDA, "prefill_handoff_copy: helper stream");
-      DP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-      DP_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-      DP_CUDA(cudaEventRecord(fork, s));
-      DP_CUDA(cudaStreamWaitEvent(aux, fork, 0));
-      if (int rc = launch_side(p, miss, 0, L, 0, 0, false, aux, &launches, 2 * sm_count(pe_pool->device)))
-        return rc;
-      DP_CUDA(cudaEventRecord(join, aux));
-    }
+    // no gates: the miss KV of every layer (a full-width side kernel), then
+    // one 2D copy per run (rows = layers), then the releases of every layer.
+    // All on `stream`: a helper stream overlapping the miss writes with the
+    // copies was 2 % faster alone but deadlocked engines sharing a GPU (its
+    // kernel queued behind another engine's spin-wait in one hardware queue)
+    if (!miss.empty())
+      if (int rc = launch_side(p, miss, 0, L, 0, 0, false, s, &launches, 2 * sm_count(pe_pool->device))) return rc;
     for (const Run& r : runs)
       DP_CUDA(cudaMemcpy2DAsync(de_view->base + r.de_off, de_plane, pe_pool->base + r.pe_off, pe_plane, r.bytes,
                                 L, cudaMemcpyDeviceToDevice, s));
-    if (join) {
-      DP_CUDA(cudaStreamWaitEvent(s, join, 0));
-      cudaEventDestroy(fork);  // released once their work completes
-      cudaEventDestroy(join);
-    }
     if (int rc = launch_side(p, {}, 0, 0, 0, L, false, s, &launches)) return rc;
   } else {
     // layer by layer: side(l) = release of l - 1, the gates of l, the miss

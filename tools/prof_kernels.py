@@ -131,7 +131,11 @@ def k4(a, g, L, T, b, n_fb, n_slots, staged=False):
         keep, spans, hspans = [], (abi.SpanJob * a.jobs)(), (abi.SpanJob * a.jobs)()
         perm = rng.permutation(n_slots)
         for j in range(a.jobs):
-            fbs = torch.tensor(rng.integers(0, n_fb, a.blocks), dtype=torch.int64, device="cuda:0")
+            if staged:  # a request persists into its session's consecutive Full Blocks (the executor's fb_of)
+                fbs = torch.tensor(np.arange(j * a.blocks, (j + 1) * a.blocks) % n_fb, dtype=torch.int64,
+                                   device="cuda:0")
+            else:
+                fbs = torch.tensor(rng.integers(0, n_fb, a.blocks), dtype=torch.int64, device="cuda:0")
             sl = torch.tensor(perm[(j * a.blocks) % n_slots:][:a.blocks].astype(np.int32), device="cuda:0")
             fbs_h = fbs.cpu().numpy()
             keep += [fbs, sl, fbs_h]
