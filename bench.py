@@ -84,7 +84,7 @@ def parse():
                     help="also persist generated tokens (decode stand-in + K4 D2H), implies --handoff")
     ap.add_argument("--handoff-ctas", type=int, default=0, help="K3 CTA cap on PEs (0 = default)")
     ap.add_argument("--k3-tma", action="store_true", help="K3's hit push through the TMA (bulk copies)")
-    ap.add_argument("--persist-mode", default="kernel", choices=["kernel", "staged"],
+    ap.add_argument("--persist-mode", default="staged", choices=["kernel", "staged"],
                     help="K4 (PersistD2H): SM zero-copy stores, or a gather into an HBM ring + copy engine")
     ap.add_argument("--k3", default="ce", choices=["kernel", "ce"],
                     help="K3 (PD handoff push): SM kernel, or copy engines + a small side kernel per layer")

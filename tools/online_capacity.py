@@ -31,11 +31,17 @@ import numpy as np  # noqa: E402
 import paper_2602_21548_b200 as dp  # noqa: E402
 
 
-def cluster(P, D, L, b):
+def pool_slots(a, L, b):
+    """Paged-pool slots of --pool-gb HBM (a B200 holds 180 GB; the rest is the
+    model): the PE pool and each DE's decode pool."""
+    return int(a.pool_gb * 1e9 // (L * 64 * b))
+
+
+def cluster(P, D, L, b, hbm_tokens=100_000_000):
     cfg = dp.ClusterConfig()
     cfg.prefill_nodes, cfg.decode_nodes, cfg.engines_per_node = P, D, 1
     cfg.n_layer, cfg.kv_bytes_per_token_per_layer, cfg.block_size_tokens = L, b, 64
-    cfg.hbm_capacity_tokens = 100_000_000
+    cfg.hbm_capacity_tokens = hbm_tokens
     cfg.pe_buffer_bytes = cfg.de_buffer_bytes = int(80e9 / 8)
     return cfg
 
@@ -53,7 +59,9 @@ def one(a, cfg, trajs, policy, aps, devices):
         ex.prefill_cost = (576 / (a.attend_tops * 1e12), 0.0, 0.0, 20e-6)
         ex.handoff = a.handoff  # + K3 into the DE decode pools: TTFT = first token, as the reference's
     t0 = time.time()
+    slots = pool_slots(a, cfg.n_layer, cfg.kv_bytes_per_token_per_layer)
     rep = dp.run_live(cfg, trajs, policy=policy, exec=ex, arrival_times=arrivals, slo_ttft=a.slo,
+                      pe_pool_slots=slots, de_pool_slots=slots if a.handoff else 0,
                       steady_window=a.steady_window, steady_lookback=a.steady_lookback, steady_threshold=0.1,
                       decode_s_per_token=a.decode_ms * 1e-3, gpu=not a.cpu, link_Bps=50e9, devices=devices,
                       alpha=a.alpha, beta=a.beta)
@@ -108,6 +116,9 @@ def main():
                     help="run the prefill stand-in (K5 forwards under the compute quota) on the PEs; the PE "
                          "is released and the TTFT taken when a request's prefill is done")
     ap.add_argument("--quota-ms", type=float, default=0.5, help="--prefill: compute quota per layer")
+    ap.add_argument("--pool-gb", type=float, default=100.0,
+                    help="HBM of the PE pool and of each decode pool; with --handoff the DEs' HBM capacity "
+                         "the scheduler balances (hbm_capacity_tokens) is the decode pool's")
     ap.add_argument("--handoff", action="store_true",
                     help="with --prefill: the PD handoff (dual gather on the DE path, K3 into decode pools); the "
                          "PE releases after K3 and the TTFT is the first token's")
@@ -117,7 +128,7 @@ def main():
         ap.error("--handoff needs --prefill")
     P, D = (int(x) for x in a.pd.split(":"))
     L, b = 61, 576
-    cfg = cluster(P, D, L, b)
+    cfg = cluster(P, D, L, b, pool_slots(a, L, b) * 64 if a.handoff else 100_000_000)
     trajs = dp.synthesize(max_len=131072, count=a.sessions, seed=9, mean_turns=a.turns, sigma_turns=0.0,
                           mean_append=429, mean_gen=500)
     ndev = 0
@@ -125,6 +136,8 @@ def main():
         import torch
         ndev = torch.cuda.device_count()
     devices = [e % max(1, ndev) for e in range(P + D)] if ndev else []
+    if ndev:  # engines sharing a GPU share its HBM
+        a.pool_gb /= -(-(P + D) // ndev)
     out = {"what": "online APS capacity (sessions/s within the load-TTFT SLO), live-mode scheduling on "
                    "measured completions", "pd": a.pd, "sessions": a.sessions, "turns": a.turns,
            "cap_gbps_per_engine": a.cap_gbps, "slo_s": a.slo, "decode_ms_per_token": a.decode_ms,
