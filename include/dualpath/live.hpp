@@ -32,7 +32,12 @@
 // pool; the PE releases it when K3 is done (every layer computed and
 // shipped) and its first token follows one decode step: TTFT as the
 // reference's (desim.cpp:679-685).  Admission also reserves the prompt's
-// decode-pool slots (bounded: de_pool_slots).
+// decode-pool slots (bounded: de_pool_slots).  With exec.persist too, at a
+// request's completion its DE writes the generated tokens into the decode
+// pool (the decode stand-in) and persists them with staged K4 in the
+// reference's chunks (PersistD2H, desim.cpp:658-661, :690-693, :760) into
+// its persist store; the decode slots (prompt + generated blocks) are freed
+// once that is done.
 // Admission reserves the request's blocks in the PE's paged pool (bounded:
 // pe_pool_slots) and stalls, FIFO, while the pool is full -- the staging
 // bound of try_admit (desim.cpp:587-599).
@@ -121,6 +126,17 @@ struct LiveReport {
   // exec.handoff: the same for every DE's decode pool (pe = the DE's engine id):
   // the whole prompt of its final occupant
   std::vector<Occupant> final_decode_slots;
+  // exec.persist: per persisted request, block and layer (0 and L-1): the
+  // generated tokens' range [t0, t1) of the block in its storage Full Block
+  // and the hash of those bytes in the DE's persist store (dp_pool_checksum's
+  // hash over the range)
+  struct Persisted {
+    int req = 0;
+    std::int64_t fb = 0;
+    std::int32_t layer = 0, t0 = 0, t1 = 0;
+    std::uint64_t hash = 0;
+  };
+  std::vector<Persisted> persisted;
   // gpu backend with exec.prefill: the K5 digest of every prefilled request at
   // layers 0 and L-1 (parity vs the oracle: independent of the batching)
   struct Digest {

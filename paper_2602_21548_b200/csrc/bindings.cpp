@@ -700,6 +700,9 @@ PYBIND11_MODULE(_core, m) {
         for (const auto& x : rep.final_decode_slots)
           docc.append(py::make_tuple(x.pe, x.slot, x.fb, x.ntok, x.hash_first, x.hash_last));
         d["final_decode_slots"] = docc;
+        py::list pers;
+        for (const auto& x : rep.persisted) pers.append(py::make_tuple(x.req, x.fb, x.layer, x.t0, x.t1, x.hash));
+        d["persisted"] = pers;
         py::list dig;
         for (const auto& x : rep.digests) dig.append(py::make_tuple(x.req, x.first, x.last));
         d["digests"] = dig;

@@ -33,13 +33,35 @@ struct Req {
   std::int64_t total() const { return r.cached + r.append + r.gen; }
   std::int32_t n_blk = 0;     // hit blocks ceil(C / T)
   std::int32_t n_pblk = 0;    // prompt blocks ceil((C + A) / T)
-  std::int32_t n_tab = 0;     // its table entries: n_pblk with the handoff, else n_blk
+  std::int32_t n_tblk = 0;    // prompt + generated blocks ceil((C + A + G) / T)
+  std::int32_t n_pe = 0;      // its PE-pool slots: n_pblk with the handoff, else n_blk
+  std::int32_t n_de = 0;      // its decode-pool slots: n_tblk with persistence, else n_pblk
+  std::int32_t n_tab = 0;     // its table entries: max(n_pe, n_de)
   std::int64_t tab_off = 0;   // its blocks in the slot / Full Block tables
 };
 
 struct Msg {
-  enum Kind { ReadDone, Landed, Prefilled } kind;
+  enum Kind { ReadDone, Landed, Prefilled, Persisted } kind;
   int req;
+};
+
+// One DE's persistence (exec.persist): at a request's completion the decode
+// stand-in writes its generated tokens into the decode pool and K4 persists
+// them (64-token chunks + the final partial) into the DE's persist store; the
+// decode-pool slots are freed when that is done.
+struct Persister {
+  int de = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<int> fifo;
+  bool stop = false;
+  std::thread th;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  dp_stager* stager = nullptr;
+  dp_store* store = nullptr;     // seed + 1: bytes never persisted differ from the content formula
+  std::int32_t* d_slot = nullptr;
+  std::int64_t* d_fb = nullptr;
 };
 
 // One PE's prefill stand-in (exec.prefill): a FIFO of requests whose loads
@@ -95,12 +117,15 @@ class Live {
     // every turn of every session, ids in arrival order are assigned at arrival
     prefill_ = o_.exec.prefill;
     handoff_ = o_.exec.handoff;
+    persist_ = o_.exec.persist;
     if (handoff_ && !prefill_) throw std::invalid_argument("run_live: exec.handoff needs exec.prefill");
+    if (persist_ && !handoff_) throw std::invalid_argument("run_live: exec.persist needs exec.handoff");
     std::int64_t max_blk = 1, total_blk = 0;
     for (const auto& t : trajs_) {
       fb_stride_ = std::max(fb_stride_, pdsim::blocks_for(t.total_tokens(), cfg_));
       for (std::size_t k = 0; k < t.rounds.size(); ++k) {
-        const std::int64_t c = pdsim::context_before(t, k) + (handoff_ ? t.rounds[k].append_tokens : 0);
+        const std::int64_t c = pdsim::context_before(t, k) + (handoff_ ? t.rounds[k].append_tokens : 0) +
+                               (persist_ ? t.rounds[k].gen_tokens : 0);
         const std::int64_t nb = (c + T_ - 1) / T_;
         max_blk = std::max(max_blk, nb);
         total_blk += nb;
@@ -136,6 +161,11 @@ class Live {
         computers_.back()->pe = p;
       }
     }
+    if (persist_)
+      for (int d = 0; d < n_eng_ - n_pe_; ++d) {
+        persisters_.push_back(std::make_unique<Persister>());
+        persisters_.back()->de = d;
+      }
     if (o_.gpu) setup_gpu(total_blk);
     else {
       tab_slot_h_ = new std::int32_t[std::max<std::int64_t>(1, total_blk)];
@@ -183,9 +213,27 @@ class Live {
     }
   }
 
+  void shutdown_persisters() {
+    for (auto& p : persisters_) {
+      {
+        std::lock_guard<std::mutex> lk(p->mu);
+        p->stop = true;
+      }
+      p->cv.notify_all();
+      if (p->th.joinable()) p->th.join();
+    }
+  }
+
   ~Live() {
     shutdown_readers();
     shutdown_computers();
+    shutdown_persisters();
+    for (auto& p : persisters_) {
+      if (p->done) cudaEventDestroy(p->done);
+      if (p->stager) dp_stager_destroy(p->stager);
+      if (p->store) dp_store_destroy(p->store);
+      if (p->stream) detail::release_stream(devs_[n_pe_ + p->de], p->stream);
+    }
     for (auto& c : computers_) {
       if (c->done) cudaEventDestroy(c->done);
       if (c->d_slot) cudaFree(c->d_slot);
@@ -232,6 +280,10 @@ class Live {
       Computer* cp = c.get();
       cp->th = std::thread([this, cp] { compute(cp); });
     }
+    for (auto& ps : persisters_) {
+      Persister* pp = ps.get();
+      pp->th = std::thread([this, pp] { persist_loop(pp); });
+    }
     if (!o_.arrival_times.empty() && o_.arrival_times.size() != trajs_.size())
       throw std::invalid_argument("run_live: one arrival time per trajectory");
     for (std::size_t t = 0; t < trajs_.size(); ++t) {
@@ -242,7 +294,7 @@ class Live {
     if (o_.steady_window > 0) next_steady_ = o_.steady_window / 2;
     wake();
     auto last_progress = Clock::now();
-    while (completed_ < total_reqs_ && !stop_) {
+    while ((completed_ < total_reqs_ || (persist_ && persisted_ < completed_)) && !stop_) {
       std::vector<Msg> msgs;
       {
         std::unique_lock<std::mutex> lk(mu_);
@@ -278,6 +330,7 @@ class Live {
     rep_.wall_s = now();
     shutdown_readers();
     shutdown_computers();
+    shutdown_persisters();
     if (o_.gpu && !stop_) final_occupants();
     if (o_.gpu && prefill_) final_digests();
     rep_.forwards = forwards_;
@@ -326,7 +379,10 @@ class Live {
     q.r.t_arrival = now();
     q.n_blk = static_cast<std::int32_t>((q.r.cached + T_ - 1) / T_);
     q.n_pblk = static_cast<std::int32_t>((q.r.cached + q.r.append + T_ - 1) / T_);
-    q.n_tab = handoff_ ? q.n_pblk : q.n_blk;
+    q.n_tblk = static_cast<std::int32_t>((q.r.cached + q.r.append + q.r.gen + T_ - 1) / T_);
+    q.n_pe = handoff_ ? q.n_pblk : q.n_blk;
+    q.n_de = persist_ ? q.n_tblk : handoff_ ? q.n_pblk : 0;
+    q.n_tab = std::max(q.n_pe, q.n_de);
     q.tab_off = tab_used_;
     tab_used_ += q.n_tab;
     reqs_.push_back(q);
@@ -489,8 +545,8 @@ class Live {
       Req& q = reqs_[*it];
       auto& fl = free_slots_[q.r.pe];
       auto* dl = handoff_ ? &free_de_[q.r.de - n_pe_] : nullptr;
-      if (static_cast<std::int64_t>(fl.size()) < q.n_tab ||
-          (dl && static_cast<std::int64_t>(dl->size()) < q.n_pblk)) {
+      if (static_cast<std::int64_t>(fl.size()) < q.n_pe ||
+          (dl && static_cast<std::int64_t>(dl->size()) < q.n_de)) {
         stalled = true;
         ++it;
         continue;
@@ -498,17 +554,21 @@ class Live {
       // the PE pool holds the hit KV, with the handoff the whole prompt (the
       // prefill writes the miss KV there); the DE's decode pool the prompt
       const std::int64_t held = handoff_ ? q.r.cached + q.r.append : q.r.cached;
+      const std::int64_t de_held = persist_ ? q.total() : held;  // the decode pool ends with the generated tokens
       for (std::int32_t k = 0; k < q.n_tab; ++k) {
-        const std::int32_t s = fl.back();
-        fl.pop_back();
-        tab_slot_h_[q.tab_off + k] = s;
         tab_fb_h_[q.tab_off + k] = fb_of(q.r.traj, k);
-        const auto ntok = static_cast<std::int32_t>(std::min<std::int64_t>(T_, held - k * T_));
-        occupant_[static_cast<std::size_t>(q.r.pe) * pool_slots_ + s] = {tab_fb_h_[q.tab_off + k], ntok};
-        if (dl) {
+        if (k < q.n_pe) {
+          const std::int32_t s = fl.back();
+          fl.pop_back();
+          tab_slot_h_[q.tab_off + k] = s;
+          const auto ntok = static_cast<std::int32_t>(std::min<std::int64_t>(T_, held - k * T_));
+          occupant_[static_cast<std::size_t>(q.r.pe) * pool_slots_ + s] = {tab_fb_h_[q.tab_off + k], ntok};
+        }
+        if (dl && k < q.n_de) {
           const std::int32_t d = dl->back();
           dl->pop_back();
           tab_de_h_[q.tab_off + k] = d;
+          const auto ntok = static_cast<std::int32_t>(std::min<std::int64_t>(T_, de_held - k * T_));
           de_occupant_[static_cast<std::size_t>(q.r.de - n_pe_) * de_slots_ + d] = {tab_fb_h_[q.tab_off + k], ntok};
         }
       }
@@ -531,8 +591,18 @@ class Live {
     if (stalled) ++rep_.admission_stalls;
   }
 
+  void free_de_slots(const Req& q) {
+    auto& dl = free_de_[q.r.de - n_pe_];
+    for (std::int32_t k = 0; k < q.n_de; ++k) dl.push_back(tab_de_h_[q.tab_off + k]);
+  }
+
   void handle(const Msg& m) {
     Req& q = reqs_[m.req];
+    if (m.kind == Msg::Persisted) {
+      free_de_slots(q);
+      ++persisted_;
+      return;
+    }
     if (m.kind == Msg::ReadDone) {  // complete_stage(StorageRead): read_q -= C (desim.cpp:702-704)
       q.r.t_read_done = now();
       if (o_.sim.policy != pdsim::desim::Policy::Oracle) read_q_[node_of(q.r.reader)] -= q.r.cached;
@@ -563,7 +633,7 @@ class Live {
     tok_[q.r.pe] -= q.total();
     seq_[q.r.pe] -= 1;
     auto& fl = free_slots_[q.r.pe];
-    for (std::int32_t k = 0; k < q.n_tab; ++k) fl.push_back(tab_slot_h_[q.tab_off + k]);
+    for (std::int32_t k = 0; k < q.n_pe; ++k) fl.push_back(tab_slot_h_[q.tab_off + k]);
     if (o_.decode_s_per_token > 0)
       timers_.push({now() + static_cast<double>(q.r.gen) * o_.decode_s_per_token, q.r.id});
     else
@@ -573,9 +643,15 @@ class Live {
   void complete(int id) {  // request done on its DE (desim.cpp:776-787), then the next turn
     Req& q = reqs_[id];
     q.r.t_done = now();
-    if (handoff_) {  // the decode pool's slots are free once the request is done
-      auto& dl = free_de_[q.r.de - n_pe_];
-      for (std::int32_t k = 0; k < q.n_pblk; ++k) dl.push_back(tab_de_h_[q.tab_off + k]);
+    if (persist_) {  // its generated tokens to storage; the slots are freed once persisted
+      Persister* ps = persisters_[q.r.de - n_pe_].get();
+      {
+        std::lock_guard<std::mutex> lk(ps->mu);
+        ps->fifo.push_back(q.r.id);
+      }
+      ps->cv.notify_all();
+    } else if (handoff_) {  // the decode pool's slots are free once the request is done
+      free_de_slots(q);
     }
     tok_[q.r.de] -= q.total();
     seq_[q.r.de] -= 1;
@@ -681,6 +757,92 @@ class Live {
     } catch (const std::exception& ex) {
       fail_async(ex.what());
     }
+  }
+
+  // ---- persistence (exec.persist) --------------------------------------
+  void persist_loop(Persister* ps) {
+    try {
+      if (o_.gpu) check_cuda(cudaSetDevice(devs_[n_pe_ + ps->de]), "cudaSetDevice");
+      for (;;) {
+        int id;
+        {
+          std::unique_lock<std::mutex> lk(ps->mu);
+          ps->cv.wait(lk, [ps] { return ps->stop || !ps->fifo.empty(); });
+          if (ps->stop) return;
+          id = ps->fifo.front();
+          ps->fifo.pop_front();
+        }
+        const Req& q = reqs_[id];
+        if (o_.gpu) {
+          persist_gpu(ps, q);
+        } else {
+          const double bytes = static_cast<double>(q.r.gen) * cfg_.kv_bytes_per_token();
+          std::this_thread::sleep_for(std::chrono::duration<double>(bytes / o_.link_Bps));
+        }
+        post({Msg::Persisted, id});
+      }
+    } catch (const std::exception& ex) {
+      fail_async(ex.what());
+    }
+  }
+
+  // The decode stand-in writes the generated tokens [P, P + G) into the
+  // decode pool, staged K4 persists them in the reference's chunks (every 64
+  // generated tokens + the final partial, desim.cpp:658-661, :690-693, :760)
+  // into the DE's persist store; then the persisted ranges of layers 0 and
+  // L-1 are hashed for the report (parity vs the oracle).
+  void persist_gpu(Persister* ps, const Req& q) {
+    const std::int64_t P = q.r.cached + q.r.append, G = q.r.gen;
+    if (G <= 0) return;
+    const std::int64_t blk0 = P / T_;
+    const std::int32_t nb = q.n_tblk - static_cast<std::int32_t>(blk0);
+    dp_pool* pool = de_pools_[ps->de];
+    const dp_span_job fill{tab_de_h_ + q.tab_off + blk0, tab_fb_h_ + q.tab_off + blk0, blk0, P, P + G, nb, 0};
+    check(dp_decode_fill(pool, &fill, 1, o_.exec.seed, ps->stream), "dp_decode_fill");
+    std::vector<dp_span_job> chunks;
+    std::int64_t done = 0;
+    for (std::int64_t k = T_; k < G; k += T_) {
+      chunks.push_back({fill.slot, fill.fb, blk0, P + done, P + k, nb, 0});
+      done = k;
+    }
+    chunks.push_back({fill.slot, fill.fb, blk0, P + done, P + G, nb, 0});
+    check(dp_persist_staged(pool, ps->store, ps->stager, chunks.data(), static_cast<std::int32_t>(chunks.size()),
+                            ps->stream),
+          "dp_persist_staged");
+    check_cuda(cudaEventRecord(ps->done, ps->stream), "cudaEventRecord");
+    check_cuda(cudaEventSynchronize(ps->done), "persist sync");
+    void* host = nullptr;
+    std::int64_t bytes = 0, n_fb = 0;
+    check(dp_store_info(ps->store, &host, &bytes, &n_fb), "dp_store_info");
+    const std::int64_t b = cfg_.kv_bytes_per_token_per_layer, lb = T_ * b, fbb = lb * L_;
+    std::vector<LiveReport::Persisted> out;
+    for (std::int32_t i = 0; i < nb; ++i) {
+      const std::int64_t k = blk0 + i;
+      const std::int64_t t0 = std::max(P, k * T_) - k * T_, t1 = std::min(P + G, (k + 1) * T_) - k * T_;
+      if (t1 <= t0) continue;
+      const std::int64_t fb = tab_fb_h_[q.tab_off + k];
+      for (std::int32_t layer : {0, L_ - 1}) {
+        const auto* w = reinterpret_cast<const std::uint64_t*>(static_cast<const char*>(host) + fb * fbb +
+                                                               layer * lb + t0 * b);
+        out.push_back({q.r.id, fb, layer, static_cast<std::int32_t>(t0), static_cast<std::int32_t>(t1),
+                       range_hash(w, (t1 - t0) * b / 8)});
+      }
+    }
+    std::lock_guard<std::mutex> lk(persist_mu_);
+    rep_.persisted.insert(rep_.persisted.end(), out.begin(), out.end());
+  }
+
+  // H = sum_i splitmix64(word_i + (i + 1) * golden) (mod 2^64): the hash of
+  // dp_pool_checksum over a byte range (the test restates it)
+  static std::uint64_t range_hash(const std::uint64_t* w, std::int64_t n) {
+    std::uint64_t h = 0;
+    for (std::int64_t i = 0; i < n; ++i) {
+      std::uint64_t z = w[i] + static_cast<std::uint64_t>(i + 1) * 0x9E3779B97F4A7C15ull + 0x9E3779B97F4A7C15ull;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      h += z ^ (z >> 31);
+    }
+    return h;
   }
 
   // One forward: the block tables of its requests to the device, then per
@@ -844,6 +1006,14 @@ class Live {
               "dp_pool_create (decode pool)");
         de_pools_.push_back(pool);
       }
+      for (auto& ps : persisters_) {
+        const int dev = devs_[n_pe_ + ps->de];
+        DeviceScope ds(dev);
+        ps->stream = detail::acquire_stream(dev);
+        check_cuda(cudaEventCreateWithFlags(&ps->done, cudaEventDisableTiming), "cudaEventCreate");
+        check(dp_stager_create(dev, &geom, o_.exec.stage_ring_bytes, &ps->stager), "dp_stager_create (persist)");
+        check(dp_store_create(dev, &geom, store_fb_, o_.exec.seed + 1, &ps->store), "dp_store_create (persist)");
+      }
       de_views_.assign(n_pe_, std::vector<dp_pool*>(n_eng_ - n_pe_, nullptr));
       for (int p = 0; p < n_pe_; ++p)
         for (int d = 0; d < n_eng_ - n_pe_; ++d)
@@ -944,6 +1114,10 @@ class Live {
   bool arrived_in_wake_ = false;
   bool prefill_ = false;
   bool handoff_ = false;
+  bool persist_ = false;
+  std::int64_t persisted_ = 0;
+  std::mutex persist_mu_;
+  std::vector<std::unique_ptr<Persister>> persisters_;
   std::int32_t de_slots_ = 0;
   std::vector<std::vector<std::int32_t>> free_de_;
   std::vector<std::pair<std::int64_t, std::int32_t>> de_occupant_;

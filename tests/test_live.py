@@ -281,3 +281,69 @@ def test_live_handoff_gpu(de_dev, k1, k2, k3):
         fbs = [(r[1] * stride + k) % n_fb for k in range(-(-r[3] // T))]
         for layer, d in ((0, d0), (L - 1, d1)):
             assert d == (refpy.attend_digest(g, 9, fbs, r[3], rid, layer, 0, r[4]) if r[3] and r[4] else 0)
+
+
+def range_hash(words):
+    """dp_pool_checksum's hash over a range of 64-bit words (restated)."""
+    golden = np.uint64(0x9E3779B97F4A7C15)
+    with np.errstate(over="ignore"):
+        z = words + np.arange(1, len(words) + 1, dtype=np.uint64) * golden + golden
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+        return int(z.sum(dtype=np.uint64))
+
+
+@needs_ref
+def test_live_persist_timed():
+    """Live prefill + handoff + persistence (timed backend): every request
+    completes, the decode pool holds prompt + generated blocks until the
+    request is persisted, and the invocations replay through the reference."""
+    trajs = dp.synthesize(max_len=16000, count=8, seed=14, mean_turns=4, sigma_turns=0)
+    ex = prefill_exec()
+    ex.handoff = ex.persist = True
+    ex.storage_cap_Bps = 2e9
+    rep = dp.run_live(cluster(1, 1), trajs, alpha=20000, beta=60000, exec=ex, gpu=False, link_Bps=8e9,
+                      decode_s_per_token=2e-6)
+    check_lifecycle(rep, trajs, prefill=True)
+    replay(rep, 20000, 60000)
+    assert rep["completed_requests"] == rep["total_requests"]
+
+
+def test_live_persist_needs_handoff():
+    trajs = dp.synthesize(max_len=8000, count=2, seed=1, mean_turns=2, sigma_turns=0)
+    ex = prefill_exec()
+    ex.persist = True
+    with pytest.raises(ValueError):
+        dp.run_live(cluster(1, 1), trajs, exec=ex, gpu=False)
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_live_persist_gpu(de_dev):
+    """Live mode with persistence on the GPU: each request's generated tokens
+    (decode stand-in) are persisted by staged K4 into its DE's persist store;
+    every persisted range of layers 0 and L-1 equals the content oracle, and
+    the decode pools' last occupants hold prompt + generated tokens."""
+    trajs = dp.synthesize(max_len=12000, count=5, seed=5, mean_turns=4, sigma_turns=0)
+    cfg = cluster(1, 1)
+    ex = prefill_exec()
+    ex.handoff = ex.persist = True
+    ex.seed = 9
+    ex.storage_cap_Bps = 4e9
+    ex.k1_mode, ex.k2_mode = 3, 2
+    rep = dp.run_live(cfg, trajs, exec=ex, devices=[0, de_dev], alpha=20000, beta=60000, decode_s_per_token=1e-5)
+    check_lifecycle(rep, trajs, prefill=True, gpu=True)
+    replay(rep, 20000, 60000)
+    T, b = cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer
+    g = refpy.geom(cfg.n_layer, T, b)
+    reqs = {r[0]: r for r in rep["requests"]}
+    want_tokens = sum(2 * r[5] for r in rep["requests"])  # layers 0 and L-1
+    assert sum(t1 - t0 for _, _, _, t0, t1, _ in rep["persisted"]) == want_tokens
+    for rid, fb, layer, t0, t1, h in rep["persisted"]:
+        full = refpy.layer_block(g, 9, fb, layer, T)
+        assert h == range_hash(full[t0 * b:t1 * b].view(np.uint64)), (rid, fb, layer, t0, t1)
+    for eng, slot, fb, ntok, h0, h1 in rep["final_decode_slots"]:
+        assert h0 == refpy.layer_block_hash(g, 9, fb, 0, ntok), (eng, slot)
+        assert h1 == refpy.layer_block_hash(g, 9, fb, cfg.n_layer - 1, ntok), (eng, slot)
+    assert len(reqs) == rep["total_requests"]

@@ -26,7 +26,7 @@ int main() {
   const auto trajs = pdsim::synthesize(spec);
   std::size_t total = 0;
   for (const auto& t : trajs) total += t.rounds.size();
-  for (int mode = 0; mode < 5; ++mode) {
+  for (int mode = 0; mode < 6; ++mode) {
     dualpath::LiveOptions o;
     o.gpu = false;
     o.link_Bps = 8e9;
@@ -41,7 +41,8 @@ int main() {
       o.exec.compute_quota = 2e-4;
       o.exec.prefill_cost.coeff_bilinear = 576 / 2e12;
       o.exec.prefill_cost.constant = 2e-6;
-      o.exec.handoff = mode == 4;  // + the PD handoff: decode-pool slots, release after K3
+      o.exec.handoff = mode >= 4;  // + the PD handoff: decode-pool slots, release after K3
+      o.exec.persist = mode == 5;  // + persistence: per-DE persist threads, slots freed when persisted
     }
     const auto rep = dualpath::run_live(cfg, trajs, o);
     std::printf("mode %d: %zu requests (%zu expected), %zu invocations, %lld stalls, %.3f s\n", mode,
