@@ -1771,7 +1771,7 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
     // no gates: the miss KV of every layer (a full-width side kernel), then
     // one 2D copy per run (rows = layers), then the releases of every layer.
     // All on `stream`: a helper stream overlapping the miss writes with the
-    // copies was 2 % faster alone but deadlocked engines sharing a GPU (its
+    // copies gained ~0.5 % alone but deadlocked engines sharing a GPU (its
     // kernel queued behind another engine's spin-wait in one hardware queue)
     if (!miss.empty())
       if (int rc = launch_side(p, miss, 0, L, 0, 0, false, s, &launches, 2 * sm_count(pe_pool->device))) return rc;
