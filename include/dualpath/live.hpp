@@ -37,7 +37,8 @@
 // pool (the decode stand-in) and persists them with staged K4 in the
 // reference's chunks (PersistD2H, desim.cpp:658-661, :690-693, :760) into
 // its persist store; the decode slots (prompt + generated blocks) are freed
-// once that is done.
+// once that is done; with exec.persist_path each persisted range is also
+// written into that block's record of the storage-tier file (PersistWrite).
 // Admission reserves the request's blocks in the PE's paged pool (bounded:
 // pe_pool_slots) and stalls, FIFO, while the pool is full -- the staging
 // bound of try_admit (desim.cpp:587-599).
@@ -137,6 +138,7 @@ struct LiveReport {
     std::uint64_t hash = 0;
   };
   std::vector<Persisted> persisted;
+  std::int64_t persist_write_bytes = 0;  // exec.persist_path: bytes written into the storage-tier file
   // gpu backend with exec.prefill: the K5 digest of every prefilled request at
   // layers 0 and L-1 (parity vs the oracle: independent of the batching)
   struct Digest {

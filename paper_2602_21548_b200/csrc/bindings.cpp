@@ -703,6 +703,7 @@ PYBIND11_MODULE(_core, m) {
         py::list pers;
         for (const auto& x : rep.persisted) pers.append(py::make_tuple(x.req, x.fb, x.layer, x.t0, x.t1, x.hash));
         d["persisted"] = pers;
+        d["persist_write_bytes"] = rep.persist_write_bytes;
         py::list dig;
         for (const auto& x : rep.digests) dig.append(py::make_tuple(x.req, x.first, x.last));
         d["digests"] = dig;

@@ -17,6 +17,7 @@
 #include <thread>
 #include <unordered_map>
 
+#include "dualpath/storage.hpp"
 #include "engine_detail.hpp"
 #include "pdsim/metrics.hpp"
 
@@ -60,6 +61,7 @@ struct Persister {
   cudaEvent_t done = nullptr;
   dp_stager* stager = nullptr;
   dp_store* store = nullptr;     // seed + 1: bytes never persisted differ from the content formula
+  std::unique_ptr<FullBlockFile> file;  // exec.persist_path: PersistWrite into the storage tier
   std::int32_t* d_slot = nullptr;
   std::int64_t* d_fb = nullptr;
 };
@@ -816,11 +818,18 @@ class Live {
     check(dp_store_info(ps->store, &host, &bytes, &n_fb), "dp_store_info");
     const std::int64_t b = cfg_.kv_bytes_per_token_per_layer, lb = T_ * b, fbb = lb * L_;
     std::vector<LiveReport::Persisted> out;
+    std::int64_t written = 0;
     for (std::int32_t i = 0; i < nb; ++i) {
       const std::int64_t k = blk0 + i;
       const std::int64_t t0 = std::max(P, k * T_) - k * T_, t1 = std::min(P + G, (k + 1) * T_) - k * T_;
       if (t1 <= t0) continue;
       const std::int64_t fb = tab_fb_h_[q.tab_off + k];
+      if (ps->file)  // PersistWrite (desim.cpp:764-771): the generated tokens into the block's record
+        for (std::int32_t layer = 0; layer < L_; ++layer) {
+          const std::int64_t off = layer * lb + t0 * b;
+          ps->file->write_bytes(fb, off, (t1 - t0) * b, static_cast<const char*>(host) + fb * fbb + off);
+          written += (t1 - t0) * b;
+        }
       for (std::int32_t layer : {0, L_ - 1}) {
         const auto* w = reinterpret_cast<const std::uint64_t*>(static_cast<const char*>(host) + fb * fbb +
                                                                layer * lb + t0 * b);
@@ -830,6 +839,7 @@ class Live {
     }
     std::lock_guard<std::mutex> lk(persist_mu_);
     rep_.persisted.insert(rep_.persisted.end(), out.begin(), out.end());
+    rep_.persist_write_bytes += written;
   }
 
   // H = sum_i splitmix64(word_i + (i + 1) * golden) (mod 2^64): the hash of
@@ -1013,6 +1023,8 @@ class Live {
         check_cuda(cudaEventCreateWithFlags(&ps->done, cudaEventDisableTiming), "cudaEventCreate");
         check(dp_stager_create(dev, &geom, o_.exec.stage_ring_bytes, &ps->stager), "dp_stager_create (persist)");
         check(dp_store_create(dev, &geom, store_fb_, o_.exec.seed + 1, &ps->store), "dp_store_create (persist)");
+        if (!o_.exec.persist_path.empty())
+          ps->file = std::make_unique<FullBlockFile>(o_.exec.persist_path, geom, store_fb_, false, false);
       }
       de_views_.assign(n_pe_, std::vector<dp_pool*>(n_eng_ - n_pe_, nullptr));
       for (int p = 0; p < n_pe_; ++p)

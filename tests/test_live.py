@@ -320,19 +320,33 @@ def test_live_persist_needs_handoff():
 
 @pytest.mark.gpu
 @needs_ref
-def test_live_persist_gpu(de_dev):
+def test_live_persist_gpu(de_dev, tmp_path):
     """Live mode with persistence on the GPU: each request's generated tokens
-    (decode stand-in) are persisted by staged K4 into its DE's persist store;
-    every persisted range of layers 0 and L-1 equals the content oracle, and
-    the decode pools' last occupants hold prompt + generated tokens."""
+    (decode stand-in) are persisted by staged K4 into its DE's persist store
+    and written into the storage-tier file (PersistWrite); every persisted
+    range of layers 0 and L-1 equals the content oracle (in the store and in
+    the file), and the decode pools' last occupants hold prompt + generated
+    tokens."""
     trajs = dp.synthesize(max_len=12000, count=5, seed=5, mean_turns=4, sigma_turns=0)
     cfg = cluster(1, 1)
+    T, b, L = cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer, cfg.n_layer
     ex = prefill_exec()
     ex.handoff = ex.persist = True
     ex.seed = 9
     ex.storage_cap_Bps = 4e9
     ex.k1_mode, ex.k2_mode = 3, 2
+    n_rec = max(-(-t.total_tokens() // T) for t in trajs) * len(trajs)  # = the live store's Full Blocks
+    path = str(tmp_path / "tier.bin")
+    f = dp.FullBlockFile(path, L, T, b, n_rec, create=True, direct=False)
+    f.populate(9 + 7, threads=4)
+    del f
+    ex.persist_path = path
     rep = dp.run_live(cfg, trajs, exec=ex, devices=[0, de_dev], alpha=20000, beta=60000, decode_s_per_token=1e-5)
+    assert rep["persist_write_bytes"] == sum(r[5] for r in rep["requests"]) * L * b
+    f = dp.FullBlockFile(path, L, T, b, n_rec, create=False, direct=False)
+    for rid, fb, layer, t0, t1, h in rep["persisted"]:
+        rec = np.frombuffer(f.read(fb), dtype=np.uint8)
+        assert h == range_hash(rec[layer * T * b + t0 * b:layer * T * b + t1 * b].copy().view(np.uint64)), (rid, fb)
     check_lifecycle(rep, trajs, prefill=True, gpu=True)
     replay(rep, 20000, 60000)
     T, b = cfg.block_size_tokens, cfg.kv_bytes_per_token_per_layer
