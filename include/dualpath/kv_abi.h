@@ -237,6 +237,11 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
  * (src_fb, pe_slot, de_slot) must be HOST-readable. */
 int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job* jobs, int32_t n_jobs,
                             uint64_t seed, int32_t timeout_ms, dp_stream stream);
+/* Gates of dp_prefill_handoff_copy as stream waits (cuStreamWaitValue32 GEQ
+ * on the PE pool's counter, no SM spinning, no watchdog) instead of the side
+ * kernel's spin; process-wide.  For gates whose producer runs on the PE's own
+ * GPU (the layerwise handoff's per-forward rows, released by K5). */
+int dp_set_handoff_gate_memop(int32_t on);
 /* Kernels dp_prefill_handoff_copy has launched in this process. */
 int dp_handoff_copy_launches(int64_t* n);
 

@@ -109,6 +109,7 @@ def lib():
         "dp_prefill_handoff_copy": ([P, P, ctypes.POINTER(HandoffJob), ctypes.c_int32, ctypes.c_uint64,
                                      ctypes.c_int32, P], ctypes.c_int),
         "dp_handoff_copy_launches": ([ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "dp_set_handoff_gate_memop": ([ctypes.c_int32], ctypes.c_int),
         "dp_persist_staged": ([P, P, P, ctypes.POINTER(SpanJob), ctypes.c_int32, P], ctypes.c_int),
         "dp_layer_items": ([ctypes.POINTER(Geom), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
                            ctypes.c_int),
@@ -384,6 +385,10 @@ def prefill_handoff_copy(pe_pool, de_view, jobs, n, seed, timeout_ms=20000, stre
     """K3 on the copy engines; the jobs' block arrays must be host memory."""
     check(lib().dp_prefill_handoff_copy(pe_pool.ptr, de_view.ptr, jobs, n, seed, timeout_ms,
                                         ctypes.c_void_p(stream)))
+
+
+def set_handoff_gate_memop(on):
+    check(lib().dp_set_handoff_gate_memop(1 if on else 0))
 
 
 def handoff_copy_launches():

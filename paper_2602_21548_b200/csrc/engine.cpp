@@ -159,6 +159,10 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
   if (ctas < 0) ctas = !is_pe() ? 0 : x.prefill ? 32 : x.handoff ? 64 : 0;
   check(dp_set_gather_ctas(device_, ctas), "dp_set_gather_ctas");
   if (is_pe() && x.handoff) check(dp_set_handoff_tma(x.opt.handoff_tma ? 1 : 0), "dp_set_handoff_tma");
+  // layerwise with the copy-engine K3: its gates are this PE's own forward
+  // rows (released by K5 on this GPU), so stream waits, not spinning CTAs
+  if (is_pe() && x.handoff)
+    check(dp_set_handoff_gate_memop(layerwise_handoff() && x.opt.k3_mode == 1 ? 1 : 0), "dp_set_handoff_gate_memop");
   // layerwise K3 CTAs wait in-kernel for the forward's layers: 64 of them.
   // One per SM hung the 1P1D pipeline (profiles/r02_g15_pf_lw148_HANG.txt):
   // with a spinning K3 CTA resident on every SM, a producer the gates wait

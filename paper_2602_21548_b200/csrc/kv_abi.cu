@@ -1671,6 +1671,7 @@ int launch_side(HoSideParams& p, const std::vector<HoMissDesc>& miss, int l0, in
 }
 
 std::atomic<int64_t> g_handoff_copy_launches{0};  // side kernels, process-wide
+std::atomic<bool> g_handoff_gate_memop{false};     // dp_set_handoff_gate_memop
 
 }  // namespace
 
@@ -1781,9 +1782,19 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
     if (int rc = launch_side(p, {}, 0, 0, 0, L, false, s, &launches)) return rc;
   } else {
     // layer by layer: side(l) = release of l - 1, the gates of l, the miss
-    // KV of l; then l's copies
+    // KV of l; then l's copies.  With dp_set_handoff_gate_memop the gates are
+    // stream waits (cuStreamWaitValue32, no SM) and side(l) does not spin
+    const bool memop = g_handoff_gate_memop.load();
+    const WaitValue32Fn wait = memop ? wait_value32() : nullptr;
+    if (memop && !wait) return fail(DP_ECUDA, "prefill_handoff_copy: cuStreamWaitValue32 unavailable");
     for (int l = 0; l < L; ++l) {
-      if (int rc = launch_side(p, miss, l, l + 1, l > 0 ? l - 1 : 0, l, true, s, &launches)) return rc;
+      for (int gi = 0; memop && gi < p.n_gate; ++gi) {
+        const uint32_t* ctr = pe_pool->counters + static_cast<int64_t>(p.gate[gi].ticket) * (L + 1) + l;
+        if (wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(ctr), p.gate[gi].target,
+                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+          return fail(DP_ECUDA, "prefill_handoff_copy: cuStreamWaitValue32 failed");
+      }
+      if (int rc = launch_side(p, miss, l, l + 1, l > 0 ? l - 1 : 0, l, !memop, s, &launches)) return rc;
       for (const Run& r : runs)
         DP_CUDA(cudaMemcpyAsync(de_view->base + l * de_plane + r.de_off, pe_pool->base + l * pe_plane + r.pe_off,
                                 r.bytes, cudaMemcpyDeviceToDevice, s));
@@ -1791,6 +1802,11 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
     if (int rc = launch_side(p, {}, 0, 0, L - 1, L, false, s, &launches)) return rc;
   }
   g_handoff_copy_launches += launches;
+  return DP_OK;
+}
+
+int dp_set_handoff_gate_memop(int32_t on) {
+  g_handoff_gate_memop = on != 0;
   return DP_OK;
 }
 

@@ -413,10 +413,16 @@ def test_pe_path_petode_copy_engine(de_dev, L, T, b, C, A, layout):
 
 @pytest.mark.parametrize("L,T,b,C,A", [(8, 64, 576, 64 * 5 + 10, 300), (8, 64, 576, 0, 200),
                                        (61, 64, 576, 64 * 9 + 17, 429), (64, 64, 4096, 64 * 4 + 33, 100)])
-def test_de_path_missmerge_copy_engine(de_dev, L, T, b, C, A):
+@pytest.mark.parametrize("memop", [False, True])
+def test_de_path_missmerge_copy_engine(de_dev, L, T, b, C, A, memop):
     """dp_prefill_handoff_copy gated per layer on the DE's dual gather (the
-    DE read path): the side kernel of layer l waits for l's hit KV, writes
-    the miss KV into both pools and releases layer l - 1."""
+    DE read path): the side kernel of layer l waits for l's hit KV (or, with
+    dp_set_handoff_gate_memop, the stream waits for it), writes the miss KV
+    into both pools and releases layer l - 1."""
+    if memop and de_dev == 0:
+        pytest.skip("a stream wait blocks its hardware queue: its producer on the same GPU must be "
+                    "enqueued first (the executor's order), which this two-stream test does not do")
+    abi.set_handoff_gate_memop(memop)
     g = abi.geom(L, T, b)
     P = C + A
     n_hit, n_prompt = -(-C // T), -(-P // T)
@@ -456,6 +462,7 @@ def test_de_path_missmerge_copy_engine(de_dev, L, T, b, C, A):
         sync_all()
         assert abi.wait_status(de_pool) == abi.DP_OK and abi.wait_status(pe_pool) == abi.DP_OK
     finally:
+        abi.set_handoff_gate_memop(False)
         for x in (de_view_on_pe, pe_view_on_de, de_pool, pe_pool, st_de):
             x.close()
 

@@ -53,7 +53,8 @@ print("ok")
 
 @pytest.mark.parametrize("prefill,persist,layerwise,k1,k2,k3", [
     (False, False, False, 0, 0, 0), (False, True, False, 3, 2, 1),
-    (True, False, False, 0, 0, 1), (True, True, False, 3, 2, 1), (True, False, True, 0, 0, 0)])
+    (True, False, False, 0, 0, 1), (True, True, False, 3, 2, 1), (True, False, True, 0, 0, 0),
+    (True, False, True, 3, 2, 1)])  # layerwise copy-engine K3: stream waits on the forward rows
 def test_pipeline_on_one_hardware_queue_per_device(two_gpus, prefill, persist, layerwise, k1, k2, k3):
     env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="1", CUDA_VISIBLE_DEVICES=os.environ.get(
         "CUDA_VISIBLE_DEVICES", "0,1"))
