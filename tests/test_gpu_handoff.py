@@ -484,3 +484,87 @@ def test_handoff_copy_gate_watchdog(de_dev):
     finally:
         for x in (de_view, de_pool, pe_pool):
             x.close()
+
+
+def test_handoff_copy_many_jobs(de_dev):
+    """dp_prefill_handoff_copy with more jobs than one parameter block holds
+    (50 > DP_MAX_HANDOFF_JOBS_PER_LAUNCH): handled in groups, every prompt in
+    both pools, every DE row released once per layer and block."""
+    L, T, b = 3, 64, 576
+    g = abi.geom(L, T, b)
+    n_jobs, per = 50, 2  # 2 prompt blocks per job: 1 hit block + a partial miss block
+    st_pe = abi.Store(0, g, 2 * n_jobs + 4, SEED)
+    pe_pool = abi.Pool(0, g, 2 * n_jobs, 1)
+    de_pool = abi.Pool(de_dev, g, 2 * n_jobs, n_jobs)
+    de_view = de_pool.peer_view(0)
+    try:
+        keep, jobs_k1 = [], []
+        hj = (abi.HandoffJob * n_jobs)()
+        C, P = T, T + 17
+        for j in range(n_jobs):
+            fbs = np.array([2 * j + 1, 2 * j + 2], dtype=np.int64)
+            ps = np.array([2 * j, 2 * j + 1], dtype=np.int32)
+            ds = np.array([2 * n_jobs - 1 - 2 * j, 2 * n_jobs - 2 - 2 * j], dtype=np.int32)  # reversed: runs of 1
+            t = [dev(fbs, 0, np.int64), dev(ps, 0, np.int32)]
+            keep += [fbs, ps, ds] + t
+            jobs_k1.append((t[0].data_ptr(), t[1].data_ptr(), C, 1, 0, L, -1))
+            hj[j] = abi.HandoffJob(fbs.ctypes.data, ps.ctypes.data, ds.ctypes.data, C, P, per, 1, -1, 0, j, -1)
+        abi.h2d_layer_gather(pe_pool, st_pe, abi.make_jobs(jobs_k1), n_jobs)
+        abi.prefill_handoff_copy(pe_pool, de_view, hj, n_jobs, SEED)
+        sync_all()
+        gr = refpy.geom(L, T, b)
+        items = abi.layer_items(g, per)
+        for j in range(n_jobs):
+            fbs, ds = keep[5 * j], keep[5 * j + 2]
+            check_prompt(de_pool, gr, fbs, ds, P, T, b, L)
+            abi.wait_layer(de_pool, j, L, items * L, timeout_ms=2000)
+        sync_all()
+        assert abi.wait_status(de_pool) == abi.DP_OK
+    finally:
+        for x in (de_view, de_pool, pe_pool, st_pe):
+            x.close()
+
+
+def test_persist_staged_two_requests(gpus):
+    """dp_persist_staged with the chunks of two requests interleaved in one
+    call, an empty span among them, and a ring of one Full Block per segment:
+    spans are merged only within a request; the bytes equal dp_persist_d2h's."""
+    L, T, b = 4, 64, 576
+    g = abi.geom(L, T, b)
+    pool = abi.Pool(0, g, 32, 1)
+    a_store = abi.Store(0, g, 24, SEED + 1)
+    b_store = abi.Store(0, g, 24, SEED + 1)
+    stager = abi.Stager(0, g, 1 * L * T * b * 4)
+    try:
+        reqs = [(64 * 2 + 5, 200, np.arange(0, 6, dtype=np.int32), np.arange(10, 16, dtype=np.int64)),
+                (64 + 63, 70, np.arange(8, 12, dtype=np.int32), np.array([3, 5, 7, 9], dtype=np.int64))]
+        keep, dev_jobs, host_jobs = [], [], []
+        for P, gen, slots, fbs in reqs:
+            blk0, n = P // T, -(-(P + gen) // T) - P // T
+            ds, df = dev(slots[:n], 0, np.int32), dev(fbs[:n], 0, np.int64)
+            fh = fbs[:n].copy()
+            keep += [ds, df, fh]
+            fill = (abi.SpanJob * 1)()
+            fill[0] = abi.SpanJob(ds.data_ptr(), df.data_ptr(), blk0, P, P + gen, n, 0)
+            abi.decode_fill(pool, fill, 1, SEED)
+            done = 0
+            for k in list(range(T, gen, T)) + [gen]:
+                if k > done:
+                    dev_jobs.append((ds.data_ptr(), df.data_ptr(), blk0, P + done, P + k, n))
+                    host_jobs.append((ds.data_ptr(), fh.ctypes.data, blk0, P + done, P + k, n))
+                    done = k
+        order = [0, len(dev_jobs) - 1, 1] + list(range(2, len(dev_jobs) - 1))  # interleave the requests
+        for jobs, fn, target in ((dev_jobs, abi.persist_d2h, a_store), (host_jobs, None, b_store)):
+            arr = (abi.SpanJob * (len(order) + 1))()
+            for i, o in enumerate(order):
+                arr[i] = abi.SpanJob(*jobs[o], 0)
+            arr[len(order)] = abi.SpanJob(jobs[0][0], jobs[0][1], jobs[0][2], jobs[0][3], jobs[0][3], jobs[0][5], 0)
+            if fn:
+                fn(pool, target, arr, len(order) + 1)
+            else:
+                abi.persist_staged(pool, target, stager, arr, len(order) + 1)
+        sync_all()
+        assert a_store.bytes() == b_store.bytes()
+    finally:
+        for x in (stager, b_store, a_store, pool):
+            x.close()
