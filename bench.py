@@ -113,6 +113,7 @@ def parse():
                          "hybrid = both at once, jobs split by bytes, staged = copy engine into an HBM "
                          "ring + scatter kernel")
     ap.add_argument("--stage-ctas", type=int, default=32, help="staged K1: scatter kernel CTAs")
+    ap.add_argument("--stage-ring-mb", type=int, default=1024, help="staged loaders: HBM ring per engine, MiB")
     ap.add_argument("--stage-push-ctas", type=int, default=148,
                     help="staged K2: CTAs of the scatter pushing over NVLink")
     ap.add_argument("--stage-scatter", default="kernel", choices=["kernel", "ce"],
@@ -497,6 +498,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
     if args.online > 0:
         opt.pace_scale = 1.0
     opt.k1_mode = {"sm": 0, "ce": 1, "hybrid": 2, "staged": 3}[args.k1]
+    opt.stage_ring_bytes = args.stage_ring_mb << 20
     opt.k2_mode = {"sm": 0, "ce": 1, "staged": 2}[args.k2]
     opt.stage_ctas = args.stage_ctas
     opt.stage_push_ctas = args.stage_push_ctas

@@ -68,6 +68,7 @@ def main():
     ap.add_argument("--gemms", type=int, default=6000)
     ap.add_argument("--only-staged", action="store_true", help="only the staged-loader cases")
     ap.add_argument("--skip-layerwise", action="store_true")
+    ap.add_argument("--ring-mb", default="", help="only K1 staged (scatter kernel) at these HBM ring sizes, MiB")
     a = ap.parse_args()
     assert torch.cuda.device_count() >= 2, "needs 2 GPUs"
     g = abi.geom(L, T, B)
@@ -107,6 +108,7 @@ def main():
         ce2.append((fbs.ctypes.data, sl.ctypes.data, blocks * T, blocks, 0, L, n_jobs + j))
     jobs_ce1, jobs_ce2 = abi.make_jobs(ce1), abi.make_jobs(ce2)
     stager0, stager1 = abi.Stager(0, g), abi.Stager(1, g)
+    ring_stagers = {int(r): abi.Stager(0, g, int(r) << 20) for r in a.ring_mb.split(",") if r}
     s_gemm = torch.cuda.Stream(device=0, priority=-1)  # high priority compute
     s_k1 = torch.cuda.Stream(device=0, priority=0)
     s_k2 = torch.cuda.Stream(device=1)
@@ -123,7 +125,7 @@ def main():
     flops = 2.0 * a.m * a.m * a.k
 
     def run_with(k1=False, k2=False, ctas=0, ce=False, staged=False, stage_ctas=32, on_de=False, ce_scatter=False,
-                 push_ctas=None):
+                 push_ctas=None, ring=None):
         for dev in (0, 1):
             abi.set_gather_ctas(dev, ctas)
         stager0.set_ctas(stage_ctas)
@@ -139,8 +141,8 @@ def main():
             with torch.cuda.device(dev):
                 while not stop.is_set():
                     if staged and kind == "k1":
-                        abi.h2d_layer_staged(pool, st_pe, stager0, jobs_ce1 if ce_scatter else jobs_st1, n_jobs,
-                                             stream.cuda_stream)
+                        abi.h2d_layer_staged(pool, st_pe, ring_stagers[ring] if ring else stager0,
+                                             jobs_ce1 if ce_scatter else jobs_st1, n_jobs, stream.cuda_stream)
                     elif staged:
                         abi.h2d_push_staged(view, st_de, stager1, jobs_ce2 if ce_scatter else jobs_st2, n_jobs,
                                             stream.cuda_stream)
@@ -211,6 +213,12 @@ def main():
                 ("k1_staged_ce", dict(k1=True, staged=True, ce_scatter=True)),
                 ("k2_staged_ce", dict(k2=True, staged=True, ce_scatter=True)),
                 ("k1_staged_ce+k2_staged_ce", dict(k1=True, k2=True, staged=True, ce_scatter=True))]
+    if a.ring_mb:
+        cases = [(f"k1_staged_ring{r}MiB", dict(k1=True, staged=True, ring=r)) for r in ring_stagers]
+        for name, kw in cases:
+            out[name] = bracketed(kw)
+        print(json.dumps(out))
+        return
     if a.only_staged:
         cases = ce_cases + [("k1_staged", dict(k1=True, staged=True)), ("k1_staged_8ctas", dict(k1=True, staged=True, stage_ctas=8)),
                  ("k2_staged", dict(k2=True, staged=True)),
