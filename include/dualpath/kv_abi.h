@@ -225,15 +225,17 @@ int dp_h2d_push_p2p_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* de_
 int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job* jobs,
                        int32_t n_jobs, uint64_t seed, int32_t timeout_ms, dp_stream stream);
 
-/* K3 on the copy engines: the transfer of dp_prefill_handoff with the hit
- * part of PeToDe moved by copy-engine copies over NVLink -- one per run of
- * prompt blocks consecutive in both pools; with no gate (every pe_ticket -1)
- * ONE 2D copy per run covers all layers (rows = layers, pitches = the pools'
- * layer planes) -- and one small kernel (kv_handoff_side, <= 32 CTAs) per
- * layer for the rest: it releases the previous layer's DE / pe_done rows
- * (system scope, the same increments as K3's), waits for the layer's gates
- * (watchdog as K3's) and writes the miss tokens' KV into both pools.  The
- * final pools and counters equal dp_prefill_handoff's.  Here the job arrays
+/* K3 on the copy engines: the transfer of dp_prefill_handoff with its bytes
+ * moved by copy-engine copies over NVLink from the PE pool -- the whole
+ * prompt on the PE path (PeToDe), the miss tokens on the DE path
+ * (MissMerge); one copy per run of prompt blocks consecutive in both pools,
+ * and with no gate (every pe_ticket -1) ONE 2D copy per run covers all
+ * layers (rows = layers, pitches = the pools' layer planes).  Before a
+ * layer's copies a small kernel (kv_handoff_side) releases the previous
+ * layer's DE / pe_done rows (system scope, the same increments as K3's),
+ * waits for the layer's gates (watchdog as K3's) and writes the miss
+ * tokens' KV into the PE pool.  The final pools and counters equal
+ * dp_prefill_handoff's.  Here the job arrays
  * (src_fb, pe_slot, de_slot) must be HOST-readable. */
 int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job* jobs, int32_t n_jobs,
                             uint64_t seed, int32_t timeout_ms, dp_stream stream);

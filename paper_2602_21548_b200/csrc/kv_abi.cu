@@ -1513,19 +1513,19 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
 }  // extern "C"
 
 // ============================================== K3 on the copy engines
-// dp_prefill_handoff_copy: the hit part of PeToDe moves by copy-engine copies
-// (whole runs of Layer Blocks consecutive in both pools), and one small
-// kernel per layer does the rest of K3: it releases the previous layer (its
-// copies precede it on the stream), waits for this layer's gates, and writes
-// the miss tokens' KV into both pools.
+// dp_prefill_handoff_copy: one small kernel per layer (kv_handoff_side)
+// releases the previous layer (its copies precede it on the stream), waits
+// for this layer's gates and writes the miss tokens' KV into the PE pool;
+// then copy-engine copies push the layer's PeToDe / MissMerge bytes from the
+// PE pool to the DE pool (whole runs of Layer Blocks consecutive in both).
 namespace {
 
 constexpr int kHoMissDescs = 112;  // miss pieces per side-kernel launch (parameter block)
 constexpr int kHoSideCtas = 32;
 
-struct HoMissDesc {  // one block's miss tokens: bytes [b0, b1) of its Layer Block
+struct HoMissDesc {  // one block's miss tokens: bytes [b0, b1) of its Layer Block in the PE pool
   int64_t fb;
-  int32_t pe_slot, de_slot;
+  int32_t pe_slot;
   int32_t b0, b1;
 };
 struct HoGate {
@@ -1611,7 +1611,7 @@ __global__ void __launch_bounds__(kThreads) kv_handoff_side(const __grid_constan
     __syncthreads();
   }
   // miss KV: the prefill stand-in's content for the miss tokens, into the PE
-  // pool (its KV cache) and the DE pool (the MissMerge / PeToDe of the miss)
+  // pool (its KV cache, local HBM); the copies that follow push it to the DE
   const int64_t lb = p.lb_bytes;
   const int64_t per_layer = p.n_miss;
   const int64_t total = per_layer * (p.miss_l1 - p.miss_l0);
@@ -1620,12 +1620,8 @@ __global__ void __launch_bounds__(kThreads) kv_handoff_side(const __grid_constan
     const HoMissDesc& d = p.miss[item % per_layer];
     const uint64_t w_base = static_cast<uint64_t>((layer * lb) >> 3);
     uint4* pe_dst = reinterpret_cast<uint4*>(p.pe_pool + layer * p.pe_stride + static_cast<int64_t>(d.pe_slot) * lb);
-    uint4* de_dst = reinterpret_cast<uint4*>(p.de_pool + layer * p.de_stride + static_cast<int64_t>(d.de_slot) * lb);
-    for (int64_t i = (d.b0 >> 4) + tid; i < (d.b1 >> 4); i += kThreads) {
-      const uint4 v = content_pair(static_cast<uint64_t>(d.fb), w_base + 2 * static_cast<uint64_t>(i), p.seed_mix);
-      st_v4(pe_dst + i, v);
-      st_v4(de_dst + i, v);
-    }
+    for (int64_t i = (d.b0 >> 4) + tid; i < (d.b1 >> 4); i += kThreads)
+      st_v4(pe_dst + i, content_pair(static_cast<uint64_t>(d.fb), w_base + 2 * static_cast<uint64_t>(i), p.seed_mix));
   }
 }
 
@@ -1735,16 +1731,22 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
         return fail(DP_EINVAL, "prefill_handoff_copy: job " + std::to_string(j) + " block " +
                                    std::to_string(k) + " slot out of range");
     if (job.n_blk == 0) continue;
-    // hit part (PeToDe only): blocks [0, n_hit), the last one's valid prefix
-    const int32_t n_hit = job.push_hit ? static_cast<int32_t>((job.n_cached + T - 1) / T) : 0;
-    for (int32_t k = 0; k < n_hit;) {
+    // the pushed tokens: the whole prompt [0, C + A) on the PE path
+    // (PeToDe), the miss tokens [C, C + A) on the DE path (MissMerge), from
+    // the PE pool once the side kernel has written the miss KV there; runs of
+    // blocks consecutive in both pools, only the range's first and last
+    // blocks partial
+    const int64_t push0 = job.push_hit ? 0 : job.n_cached;
+    for (int64_t k = push0 / T; k < job.n_blk;) {
       int32_t run = 1;
-      while (k + run < n_hit && job.pe_slot[k + run] == job.pe_slot[k] + run &&
+      while (k + run < job.n_blk && job.pe_slot[k + run] == job.pe_slot[k] + run &&
              job.de_slot[k + run] == job.de_slot[k] + run)
         ++run;
       const int64_t last = k + run - 1;
-      const int64_t tail = std::min<int64_t>(T, job.n_cached - last * T) * bpt;
-      runs.push_back({job.pe_slot[k] * lb, job.de_slot[k] * lb, (run - 1) * lb + tail});
+      const int64_t head = std::max<int64_t>(0, push0 - k * T) * bpt;
+      const int64_t tail = std::min<int64_t>(T, job.n_prompt - last * T) * bpt;
+      const int64_t bytes = (run - 1) * lb + tail - head;
+      if (bytes > 0) runs.push_back({job.pe_slot[k] * lb + head, job.de_slot[k] * lb + head, bytes});
       k += run;
     }
     // miss part: tokens [C, C + A) block by block
@@ -1752,8 +1754,7 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
       const int64_t b0 = std::max<int64_t>(0, job.n_cached - k * T) * bpt;
       const int64_t b1 = std::min<int64_t>(T, job.n_prompt - k * T) * bpt;
       if (b1 > b0)
-        miss.push_back({job.src_fb[k], job.pe_slot[k], job.de_slot[k], static_cast<int32_t>(b0),
-                        static_cast<int32_t>(b1)});
+        miss.push_back({job.src_fb[k], job.pe_slot[k], static_cast<int32_t>(b0), static_cast<int32_t>(b1)});
     }
     if (job.pe_ticket >= 0) {
       bool dup = false;
