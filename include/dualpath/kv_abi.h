@@ -234,8 +234,11 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
  * layer's copies a small kernel (kv_handoff_side) releases the previous
  * layer's DE / pe_done rows (system scope, the same increments as K3's),
  * waits for the layer's gates (watchdog as K3's) and writes the miss
- * tokens' KV into the PE pool.  The final pools and counters equal
- * dp_prefill_handoff's.  Here the job arrays
+ * tokens' KV into the PE pool (gated calls: into both pools, the copies then
+ * carry only PeToDe's hit part -- a few operations per layer, so a caller
+ * that enqueues a gate's producer after this call on the same thread does
+ * not fill the stream's queue behind the gate).  The final pools and
+ * counters equal dp_prefill_handoff's.  Here the job arrays
  * (src_fb, pe_slot, de_slot) must be HOST-readable. */
 int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job* jobs, int32_t n_jobs,
                             uint64_t seed, int32_t timeout_ms, dp_stream stream);

@@ -1523,9 +1523,9 @@ namespace {
 constexpr int kHoMissDescs = 112;  // miss pieces per side-kernel launch (parameter block)
 constexpr int kHoSideCtas = 32;
 
-struct HoMissDesc {  // one block's miss tokens: bytes [b0, b1) of its Layer Block in the PE pool
+struct HoMissDesc {  // one block's miss tokens: bytes [b0, b1) of its Layer Block
   int64_t fb;
-  int32_t pe_slot;
+  int32_t pe_slot, de_slot;
   int32_t b0, b1;
 };
 struct HoGate {
@@ -1549,6 +1549,7 @@ struct HoSideParams {
   int32_t miss_l0, miss_l1;  // layers whose miss KV this launch writes (after the gates)
   int32_t rel_l0, rel_l1;    // layers released first by CTA 0 (work stream-ordered before this launch)
   int32_t n_gate, n_miss, n_rel;
+  int32_t miss_to_de;        // gated calls: the miss KV is also stored into the DE pool (no copies of it)
   HoGate gate[DP_MAX_HANDOFF_JOBS_PER_LAUNCH];
   HoRelease rel[DP_MAX_HANDOFF_JOBS_PER_LAUNCH];
   HoMissDesc miss[kHoMissDescs];
@@ -1612,6 +1613,7 @@ __global__ void __launch_bounds__(kThreads) kv_handoff_side(const __grid_constan
   }
   // miss KV: the prefill stand-in's content for the miss tokens, into the PE
   // pool (its KV cache, local HBM); the copies that follow push it to the DE
+  // (gated calls store it into the DE pool here as well)
   const int64_t lb = p.lb_bytes;
   const int64_t per_layer = p.n_miss;
   const int64_t total = per_layer * (p.miss_l1 - p.miss_l0);
@@ -1620,8 +1622,12 @@ __global__ void __launch_bounds__(kThreads) kv_handoff_side(const __grid_constan
     const HoMissDesc& d = p.miss[item % per_layer];
     const uint64_t w_base = static_cast<uint64_t>((layer * lb) >> 3);
     uint4* pe_dst = reinterpret_cast<uint4*>(p.pe_pool + layer * p.pe_stride + static_cast<int64_t>(d.pe_slot) * lb);
-    for (int64_t i = (d.b0 >> 4) + tid; i < (d.b1 >> 4); i += kThreads)
-      st_v4(pe_dst + i, content_pair(static_cast<uint64_t>(d.fb), w_base + 2 * static_cast<uint64_t>(i), p.seed_mix));
+    uint4* de_dst = reinterpret_cast<uint4*>(p.de_pool + layer * p.de_stride + static_cast<int64_t>(d.de_slot) * lb);
+    for (int64_t i = (d.b0 >> 4) + tid; i < (d.b1 >> 4); i += kThreads) {
+      const uint4 v = content_pair(static_cast<uint64_t>(d.fb), w_base + 2 * static_cast<uint64_t>(i), p.seed_mix);
+      st_v4(pe_dst + i, v);
+      if (p.miss_to_de) st_v4(de_dst + i, v);
+    }
   }
 }
 
@@ -1718,6 +1724,9 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
   };
   std::vector<Run> runs;
   std::vector<HoMissDesc> miss;
+  bool gated_call = false;  // any gate: the per-layer path
+  for (int32_t j = 0; j < n_jobs; ++j) gated_call = gated_call || jobs[j].pe_ticket >= 0;
+  p.miss_to_de = gated_call ? 1 : 0;
   for (int32_t j = 0; j < n_jobs; ++j) {
     const dp_handoff_job& job = jobs[j];
     const int64_t need = (job.n_prompt + T - 1) / T;
@@ -1731,20 +1740,26 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
         return fail(DP_EINVAL, "prefill_handoff_copy: job " + std::to_string(j) + " block " +
                                    std::to_string(k) + " slot out of range");
     if (job.n_blk == 0) continue;
-    // the pushed tokens: the whole prompt [0, C + A) on the PE path
+    // the copied tokens: the whole prompt [0, C + A) on the PE path
     // (PeToDe), the miss tokens [C, C + A) on the DE path (MissMerge), from
     // the PE pool once the side kernel has written the miss KV there; runs of
     // blocks consecutive in both pools, only the range's first and last
-    // blocks partial
+    // blocks partial.  Gated calls copy only the hit part [0, C) of the PE
+    // path, per layer, and the side kernel stores the miss KV into both
+    // pools: a few operations per layer (a long chain of copies queued behind
+    // a gate can block the enqueueing thread until the queue drains, and so
+    // deadlock a caller that enqueues the gate's producer after this call)
     const int64_t push0 = job.push_hit ? 0 : job.n_cached;
-    for (int64_t k = push0 / T; k < job.n_blk;) {
+    const int64_t push1 = gated_call ? (job.push_hit ? job.n_cached : 0) : job.n_prompt;
+    const int32_t blk1 = static_cast<int32_t>((push1 + T - 1) / T);
+    for (int64_t k = push0 / T; k < blk1 && push1 > push0;) {
       int32_t run = 1;
-      while (k + run < job.n_blk && job.pe_slot[k + run] == job.pe_slot[k] + run &&
+      while (k + run < blk1 && job.pe_slot[k + run] == job.pe_slot[k] + run &&
              job.de_slot[k + run] == job.de_slot[k] + run)
         ++run;
       const int64_t last = k + run - 1;
       const int64_t head = std::max<int64_t>(0, push0 - k * T) * bpt;
-      const int64_t tail = std::min<int64_t>(T, job.n_prompt - last * T) * bpt;
+      const int64_t tail = std::min<int64_t>(T, push1 - last * T) * bpt;
       const int64_t bytes = (run - 1) * lb + tail - head;
       if (bytes > 0) runs.push_back({job.pe_slot[k] * lb + head, job.de_slot[k] * lb + head, bytes});
       k += run;
@@ -1754,7 +1769,8 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
       const int64_t b0 = std::max<int64_t>(0, job.n_cached - k * T) * bpt;
       const int64_t b1 = std::min<int64_t>(T, job.n_prompt - k * T) * bpt;
       if (b1 > b0)
-        miss.push_back({job.src_fb[k], job.pe_slot[k], static_cast<int32_t>(b0), static_cast<int32_t>(b1)});
+        miss.push_back({job.src_fb[k], job.pe_slot[k], job.de_slot[k], static_cast<int32_t>(b0),
+                        static_cast<int32_t>(b1)});
     }
     if (job.pe_ticket >= 0) {
       bool dup = false;
