@@ -2,8 +2,9 @@
 """Small, stream-ordered invocations of every kernel of libdualpath.so for
 compute-sanitizer (memcheck / racecheck / synccheck / initcheck): K1 gather,
 K2 push (a same-GPU pool view), staged K1 (copy engine + scatter), the dual
-gather, K3 handoff (PE and DE path), the decode stand-in + K4 persistence,
-K5 attend, the checksum and the store fill.  No cross-kernel spin waits (the
+gather, K3 handoff (SM kernel and copy engines + kv_handoff_side), the
+decode stand-in + K4 persistence (SM kernel and staged), K5 attend, the
+checksum and the store fill.  No cross-kernel spin waits (the
 sanitizers serialise kernels), every result checked against the oracle."""
 
 import os
@@ -45,6 +46,13 @@ def main():
         hj = (abi.HandoffJob * 1)()
         hj[0] = abi.HandoffJob(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), C, P, npb, 1, -1, 0, 0, 2)
         abi.prefill_handoff(pe, de_view, hj, 1, SEED)
+        # the same handoff on the copy engines into a second decode pool
+        # (host block tables; kv_handoff_side + 2D copies)
+        de2 = abi.Pool(0, g, 16, 4)
+        de2_view = de2.peer_view(0)
+        hc = (abi.HandoffJob * 1)()
+        hc[0] = abi.HandoffJob(fbs.ctypes.data, ps.ctypes.data, ds.ctypes.data, C, P, npb, 1, -1, 0, 0, -1)
+        abi.prefill_handoff_copy(pe, de2_view, hc, 1, SEED)
         torch.cuda.synchronize()
         for k in range(npb):
             n = min(T, P - k * T)
@@ -52,6 +60,9 @@ def main():
                 want = refpy.layer_block(gr, SEED, int(fbs[k]), layer, n).tobytes()
                 assert pe.copy_out(layer, int(ps[k]), n * b) == want
                 assert de.copy_out(layer, int(ds[k]), n * b) == want
+                assert de2.copy_out(layer, int(ds[k]), n * b) == want
+        de2_view.close()
+        de2.close()
         # K2 into the PE pool (view on the same GPU), ticket 1; the dual gather, ticket 3
         ps2 = np.arange(8, 8 + nh, dtype=np.int32)
         t2 = dev(ps2, np.int32)
@@ -78,7 +89,16 @@ def main():
         sp[0] = abi.SpanJob(t[2].data_ptr(), t[0].data_ptr(), 0, P, npb * T, npb, 0)
         abi.decode_fill(de, sp, 1, SEED)
         abi.persist_d2h(de, target, sp, 1)
+        # staged K4 (gather into an HBM ring + copy engine): the same bytes
+        target2 = abi.Store(0, g, 12, SEED + 1)
+        pstager = abi.Stager(0, g, 4 * L * T * b * 4)
+        sph = (abi.SpanJob * 1)()
+        sph[0] = abi.SpanJob(t[2].data_ptr(), fbs.ctypes.data, 0, P, npb * T, npb, 0)
+        abi.persist_staged(de, target2, pstager, sph, 1)
         torch.cuda.synchronize()
+        assert target2.bytes() == target.bytes()
+        pstager.close()
+        target2.close()
         img = np.frombuffer(target.bytes(), dtype=np.uint8)
         fbb = L * T * b
         k = npb - 1
