@@ -1,14 +1,17 @@
-// The reference's acceptance criteria 5 and 10 (/root/reference/proj/tests/
-// acceptance.cpp:274-331, :551-601) restated against THIS build's planner
+// The reference's acceptance criteria 5, 7 and 10 (/root/reference/proj/tests/
+// acceptance.cpp:274-331, :383-420, :551-601) restated against THIS build's planner
 // (include/pdsim + libdualpath.so).  The reference's acceptance.cpp cannot be
 // compiled here as a whole (its criteria 1-2 need the Boost-based analyzer,
-// out of scope), so the two criteria on the path -- the adaptive scheduler
-// balancing the storage NICs, and the online dual-path gain -- are restated
+// out of scope), so the criteria on the path not restated elsewhere -- the
+// adaptive scheduler balancing the storage NICs, the isolation of
+// model-execution bursts from KV traffic, and the online dual-path gain --
+// are restated
 // with the same scenarios, seeds and thresholds.  Built and run by
 // tests/test_acceptance_cpp.py; prints one line per criterion, exit 1 on a
 // failure.
 #include <algorithm>
 #include <cmath>
+#include <numeric>
 #include <cstdio>
 #include <random>
 #include <string>
@@ -111,6 +114,54 @@ void criterion_5() {
          std::to_string(wins) + "/" + std::to_string(seeds) + " seeds, sign-test p=" + std::to_string(p_value));
 }
 
+std::vector<Trajectory> saturating_workload(const ClusterConfig& cfg, std::int64_t tokens, int warm,
+                                            int per_engine) {  // acceptance.cpp:76-90
+  std::vector<Trajectory> out;
+  const int count = per_engine * cfg.total_engines();
+  for (int i = 0; i < count; ++i) {
+    Trajectory t;
+    t.id = "s" + std::to_string(i);
+    t.rounds.push_back({tokens, 1});
+    for (int r = 0; r < warm; ++r) t.rounds.push_back({0, 1});
+    out.push_back(std::move(t));
+  }
+  return out;
+}
+
+// Criterion 7: model-execution bursts (high priority, WRR) slowed <= 2 % by
+// a saturating KV workload, and the low-priority floor of the WRR arbitration
+// >= 0.9 % of the link.
+void criterion_7() {
+  ClusterConfig cfg = cluster(1, 1, 2);
+  BurstSpec bursts;
+  bursts.period = 2e-3;
+  bursts.bytes_per_burst = 5e7;
+  bursts.start = 0.0;
+  bursts.stop = 0.4;
+  SimOptions idle = storage_bound_options();
+  idle.bursts = bursts;
+  const auto base = run(cfg, {}, {}, idle);
+  SimOptions loaded = storage_bound_options();
+  loaded.bursts = bursts;
+  const auto trajs = saturating_workload(cfg, 40'000, 8, 4);
+  const auto busy = run_offline(cfg, trajs, loaded);
+  auto mean = [](const std::vector<double>& v) {
+    return v.empty() ? 0.0 : std::accumulate(v.begin(), v.end(), 0.0) / v.size();
+  };
+  const double slowdown = mean(busy.burst_latencies) / mean(base.burst_latencies);
+  std::vector<Resource> rs(1);
+  rs[0].id = 0;
+  rs[0].kind = ResKind::CnicRead;
+  rs[0].capacity = cfg.cnic_bandwidth;
+  rs[0].wrr = true;
+  std::vector<FlowDemand> flows = {{0, true, {0}}, {1, false, {0}}};
+  const double low_share = arbitrate(rs, flows)[1] / cfg.cnic_bandwidth;
+  const bool pass = slowdown <= 1.02 && low_share >= 0.009 && !base.burst_latencies.empty() &&
+                    busy.burst_latencies.size() == base.burst_latencies.size();
+  report(7, pass, "traffic isolation: bursts slowed <=2%, low floor >=0.9%",
+         "slowdown=" + std::to_string(slowdown) + ", low_share=" + std::to_string(low_share));
+}
+
 // Criterion 10: online, 1P1D with slow storage: at 3 sessions/s the
 // dual-path mean TTFT is no worse than PE-only's, and the first SLO-violating
 // arrival rate (geometric grid x1.12 from 3) is >= 1.3x PE-only's.
@@ -159,6 +210,7 @@ void criterion_10() {
 
 int main() {
   criterion_5();
+  criterion_7();
   criterion_10();
   return failures ? 1 : 0;
 }
