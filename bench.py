@@ -114,6 +114,9 @@ def parse():
                          "ring + scatter kernel")
     ap.add_argument("--stage-ctas", type=int, default=32, help="staged K1: scatter kernel CTAs")
     ap.add_argument("--stage-ring-mb", type=int, default=1024, help="staged loaders: HBM ring per engine, MiB")
+    ap.add_argument("--pool-layout", default="layer", choices=["layer", "block"],
+                    help="PE pool: per-layer planes, or whole Full Blocks per slot (with --k1 ce / --k2 ce the copy "
+                         "engine lands Full-Block runs in one copy: no ring, no SM work)")
     ap.add_argument("--stage-push-ctas", type=int, default=148,
                     help="staged K2: CTAs of the scatter pushing over NVLink")
     ap.add_argument("--stage-scatter", default="kernel", choices=["kernel", "ce"],
@@ -499,6 +502,7 @@ def run_policy(args, dist, variant, trajs, shape, P, D, clocks=None, prefill=Non
         opt.pace_scale = 1.0
     opt.k1_mode = {"sm": 0, "ce": 1, "hybrid": 2, "staged": 3}[args.k1]
     opt.stage_ring_bytes = args.stage_ring_mb << 20
+    opt.pool_layout = 1 if args.pool_layout == "block" else 0
     opt.k2_mode = {"sm": 0, "ce": 1, "staged": 2}[args.k2]
     opt.stage_ctas = args.stage_ctas
     opt.stage_push_ctas = args.stage_push_ctas
@@ -1038,6 +1042,7 @@ def main():
                         "handoff_ctas": args.handoff_ctas or None,
                         "k3": args.k3 if (args.handoff or args.persist) else None,
                         "k4": args.persist_mode if args.persist else None,
+                        "pool_layout": args.pool_layout,
                         "buffer_stalls": info["buffer_stalls"],
                         "buffer_wait_ms": round(info["buffer_wait_ms"], 1)},
             "model_prediction_gbps": round(info["model_gbps"], 3) if info["model_gbps"] else None,

@@ -55,6 +55,11 @@ struct ExecOptions {
   // the link's full rate, a small scatter kernel (stage_ctas CTAs) lands them
   // in the pool's layer planes (dp_h2d_layer_staged)
   std::int32_t k1_mode = 0;
+  // PE pool layout: DP_POOL_LAYER_MAJOR (0, per-layer planes) or
+  // DP_POOL_BLOCK_MAJOR (1, whole Full Blocks per slot: with k1_mode /
+  // k2_mode 1 the copy engines land each run of Full Blocks in one copy, no
+  // ring and no SM work); block-major takes the load and prefill paths only
+  std::int32_t pool_layout = 0;
   // copy-engine modes (k1_mode / k2_mode 1): release a job's counters once
   // after its last layer (true) or after every layer (false; idles the copy
   // engine once per layer)

@@ -142,6 +142,20 @@ int dp_storage_read(dp_store* staging, int64_t dst_fb, int64_t src_fb, int64_t n
  * the items landed over all layers of the ticket. */
 int dp_pool_create(int device, const dp_kv_geom* geom, int32_t n_slots, int32_t n_tickets,
                    dp_pool** out);
+/* Pool layouts.  Layer-major (dp_pool_create): one plane per layer,
+ * [n_layer][n_slots][T][b], the per-layer paged layout attention kernels
+ * read.  Block-major: [n_slots][n_layer][T][b], every slot a whole Full
+ * Block, so the copy engine lands a run of storage Full Blocks in ONE
+ * contiguous copy (dp_h2d_layer_copy / dp_h2d_push_copy and their _job
+ * forms: no ring, no SM work) -- the loading path's kernels (K1 / K2 / staged
+ * / K5 / checksum / copy-out) take either; the handoff and persistence
+ * kernels take layer-major pools only (DP_EINVAL otherwise).  The layout
+ * travels in dp_pool_handle (reserved[0]) to imported views. */
+#define DP_POOL_LAYER_MAJOR 0
+#define DP_POOL_BLOCK_MAJOR 1
+int dp_pool_create_layout(int device, const dp_kv_geom* geom, int32_t n_slots, int32_t n_tickets, int32_t layout,
+                          dp_pool** out);
+int dp_pool_layout(const dp_pool* pool, int32_t* layout);
 int dp_pool_destroy(dp_pool* pool);
 int dp_pool_info(const dp_pool* pool, void** base, uint32_t** counters, int64_t* data_bytes);
 int dp_pool_reset_counters(dp_pool* pool, dp_stream stream);

@@ -96,6 +96,9 @@ def lib():
         "dp_pool_reset_counters": ([P, P], ctypes.c_int),
         "dp_pool_export": ([P, ctypes.POINTER(PoolHandle)], ctypes.c_int),
         "dp_pool_import": ([ctypes.c_int, ctypes.POINTER(PoolHandle), PP], ctypes.c_int),
+        "dp_pool_create_layout": ([ctypes.c_int, ctypes.POINTER(Geom), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                   PP], ctypes.c_int),
+        "dp_pool_layout": ([P, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
         "dp_pool_peer_view": ([ctypes.c_int, P, PP], ctypes.c_int),
         "dp_h2d_layer_gather": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
         "dp_h2d_push_p2p_layer": ([P, P, ctypes.POINTER(Job), ctypes.c_int32, P], ctypes.c_int),
@@ -178,6 +181,7 @@ def geom(n_layer, block_tokens, b):
 
 
 NUMA_DEVICE, NUMA_NONE = -1, -2
+POOL_LAYER_MAJOR, POOL_BLOCK_MAJOR = 0, 1
 SCATTER_KERNEL, SCATTER_CE = 0, 1
 
 
@@ -220,7 +224,7 @@ class Store:
 class Pool:
     """Paged HBM pool [L][n_slots][T][b] + landed counters [n_tickets][L+1]."""
 
-    def __init__(self, device=None, g=None, n_slots=0, n_tickets=0, _ptr=None):
+    def __init__(self, device=None, g=None, n_slots=0, n_tickets=0, _ptr=None, layout=0):
         self.geom = g
         self.n_slots = n_slots
         self.n_tickets = n_tickets
@@ -228,7 +232,13 @@ class Pool:
             self.ptr = _ptr
             return
         self.ptr = ctypes.c_void_p()
-        check(lib().dp_pool_create(device, ctypes.byref(g), n_slots, n_tickets, ctypes.byref(self.ptr)))
+        check(lib().dp_pool_create_layout(device, ctypes.byref(g), n_slots, n_tickets, layout,
+                                          ctypes.byref(self.ptr)))
+
+    def layout(self):
+        out = ctypes.c_int32()
+        check(lib().dp_pool_layout(self.ptr, ctypes.byref(out)))
+        return out.value
 
     def info(self):
         base = ctypes.c_void_p()

@@ -435,6 +435,7 @@ PYBIND11_MODULE(_core, m) {
       .def_readwrite("handoff_tma", &dualpath::ExecOptions::handoff_tma)
       .def_readwrite("k3_mode", &dualpath::ExecOptions::k3_mode)
       .def_readwrite("persist_mode", &dualpath::ExecOptions::persist_mode)
+      .def_readwrite("pool_layout", &dualpath::ExecOptions::pool_layout)
       .def_readwrite("handoff_ctas", &dualpath::ExecOptions::handoff_ctas)
       .def_readwrite("persist", &dualpath::ExecOptions::persist)
       .def_readwrite("store_fb", &dualpath::ExecOptions::store_fb)

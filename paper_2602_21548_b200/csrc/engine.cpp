@@ -117,7 +117,7 @@ EngineRuntime::EngineRuntime(std::shared_ptr<const ExecPlan> plan, int engine, i
     fwd_row0_ = std::max<std::int32_t>(1, x.n_tickets[engine_]) * (x.handoff || x.prefill ? 2 : 1);
     const std::int32_t rows =
         fwd_row0_ + (layerwise_handoff() ? static_cast<std::int32_t>(x.forwards[engine_].size()) : 0);
-    check(dp_pool_create(device_, &x.geom, x.pool_slots, rows, &pool_), "dp_pool_create");
+    check(dp_pool_create_layout(device_, &x.geom, x.pool_slots, rows, x.opt.pool_layout, &pool_), "dp_pool_create");
     peers_[engine_] = pool_;
   } else if (x.handoff) {
     // rows [0, n) prompt landed; with persistence rows [n, 2n) persisted

@@ -406,6 +406,9 @@ ExecPlan build_exec_plan(const pdsim::ClusterConfig& cfg,
   x.handoff = opt.handoff;
   x.persist = opt.persist;
   if (x.persist && !x.handoff) throw std::invalid_argument("build_exec_plan: persist needs handoff");
+  if (opt.pool_layout != 0 && opt.pool_layout != 1) throw std::invalid_argument("build_exec_plan: bad pool_layout");
+  if (opt.pool_layout == 1 && x.handoff)
+    throw std::invalid_argument("build_exec_plan: a block-major PE pool takes the load and prefill paths only");
   x.prefill = opt.prefill;
   if (x.prefill && !(opt.compute_quota > 0))
     throw std::invalid_argument("build_exec_plan: compute_quota must be > 0");

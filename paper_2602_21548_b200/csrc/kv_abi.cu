@@ -93,7 +93,8 @@ struct GatherParams {
   int64_t lb_bytes;      // Layer Block bytes T*b
   int64_t fb_bytes;      // Full Block bytes L*T*b
   int64_t bpt;           // b, bytes per token per layer
-  int64_t layer_stride;  // n_slots * lb_bytes
+  int64_t layer_stride;  // pool: layer plane (layer-major) or Layer Block (block-major)
+  int64_t slot_stride;   // pool: Layer Block (layer-major) or Full Block (block-major)
   int32_t n_layer;
   int32_t block_tokens;
   int32_t n_chunk;       // items per Layer Block
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kThreads) kv_gather(const __grid_constant__ Ga
       const uint4* src = reinterpret_cast<const uint4*>(p.store + fb * p.fb_bytes +
                                                         layer * p.lb_bytes + beg);
       uint4* dst = reinterpret_cast<uint4*>(p.pool + layer * p.layer_stride +
-                                            slot * p.lb_bytes + beg);
+                                            slot * p.slot_stride + beg);
       const int n16 = static_cast<int>((end - beg) >> 4);
       for (int base = 0; base < n16; base += kThreads * kUnroll) {
         uint4 v[kUnroll];
@@ -264,12 +265,12 @@ __global__ void kv_wait_many(const uint32_t* counters, int32_t row_len, const in
 }
 
 __global__ void __launch_bounds__(kThreads)
-    kv_block_checksum(const char* pool, int64_t layer_off, int64_t lb_bytes, int64_t bpt,
+    kv_block_checksum(const char* pool, int64_t layer_off, int64_t slot_stride, int64_t bpt,
                       const int32_t* slots, const int32_t* ntok, int32_t n, uint64_t* out) {
   __shared__ uint64_t partial[kThreads / 32];
   for (int b = blockIdx.x; b < n; b += gridDim.x) {
     const uint64_t* words =
-        reinterpret_cast<const uint64_t*>(pool + layer_off + static_cast<int64_t>(slots[b]) * lb_bytes);
+        reinterpret_cast<const uint64_t*>(pool + layer_off + static_cast<int64_t>(slots[b]) * slot_stride);
     const int64_t nw = static_cast<int64_t>(ntok[b]) * bpt / 8;
     uint64_t acc = 0;
     for (int64_t i = threadIdx.x; i < nw; i += kThreads)
@@ -352,11 +353,23 @@ struct dp_pool {
   bool ipc_opened = false;
   int* err_host = nullptr;  // mapped pinned watchdog flag
   uint32_t* att_ctr = nullptr;  // K5 work-queue counters {next unit, CTAs done} (owner pools)
+  int32_t layout = 0;           // DP_POOL_LAYER_MAJOR or DP_POOL_BLOCK_MAJOR
 };
 
 namespace {
 
 int64_t counters_offset(int64_t data_bytes) { return (data_bytes + 255) / 256 * 256; }
+
+// Layer Block (layer, slot) of a pool lives at layer * layer_stride + slot *
+// slot_stride: layer planes [L][slots][T][b] (layer-major, the default) or
+// whole Full Blocks per slot [slots][L][T][b] (block-major).
+int64_t pool_lb(const dp_pool* p) { return static_cast<int64_t>(p->geom.block_tokens) * p->geom.bytes_per_token_layer; }
+int64_t layer_stride(const dp_pool* p) {
+  return p->layout == DP_POOL_BLOCK_MAJOR ? pool_lb(p) : pool_lb(p) * p->n_slots;
+}
+int64_t slot_stride(const dp_pool* p) {
+  return p->layout == DP_POOL_BLOCK_MAJOR ? pool_lb(p) * p->geom.n_layer : pool_lb(p);
+}
 
 // Loads every kernel of this library on `device` (defined at the end of the
 // file, after the last kernel).  With CUDA's lazy loading a kernel is loaded
@@ -389,7 +402,8 @@ int launch_gather(dp_pool* pool, const dp_store* src, const dp_job* jobs, int32_
   p.lb_bytes = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
   p.fb_bytes = p.lb_bytes * g.n_layer;
   p.bpt = g.bytes_per_token_layer;
-  p.layer_stride = p.lb_bytes * pool->n_slots;
+  p.layer_stride = layer_stride(pool);
+  p.slot_stride = slot_stride(pool);
   p.n_layer = g.n_layer;
   p.block_tokens = g.block_tokens;
   p.n_chunk = static_cast<int32_t>(chunks_per_block(g));
@@ -608,7 +622,13 @@ int dp_store_info(const dp_store* st, void** host_ptr, int64_t* bytes, int64_t* 
 
 int dp_pool_create(int device, const dp_kv_geom* geom, int32_t n_slots, int32_t n_tickets,
                    dp_pool** out) {
+  return dp_pool_create_layout(device, geom, n_slots, n_tickets, DP_POOL_LAYER_MAJOR, out);
+}
+
+int dp_pool_create_layout(int device, const dp_kv_geom* geom, int32_t n_slots, int32_t n_tickets, int32_t layout,
+                          dp_pool** out) {
   if (!out) return fail(DP_EINVAL, "pool_create: null out");
+  if (layout != DP_POOL_LAYER_MAJOR && layout != DP_POOL_BLOCK_MAJOR) return fail(DP_EINVAL, "pool_create: bad layout");
   *out = nullptr;
   if (int rc = dp_geom_check(geom)) return rc;
   if (n_slots < 1 || n_tickets < 0) return fail(DP_EINVAL, "pool_create: bad sizes");
@@ -619,6 +639,7 @@ int dp_pool_create(int device, const dp_kv_geom* geom, int32_t n_slots, int32_t 
   pool->geom = *geom;
   pool->n_slots = n_slots;
   pool->n_tickets = n_tickets;
+  pool->layout = layout;
   pool->data_bytes = static_cast<int64_t>(geom->n_layer) * n_slots * geom->block_tokens *
                      geom->bytes_per_token_layer;
   const int64_t ctr_bytes = static_cast<int64_t>(n_tickets) * (geom->n_layer + 1) * 4;
@@ -662,6 +683,12 @@ int dp_pool_destroy(dp_pool* pool) {
   return DP_OK;
 }
 
+int dp_pool_layout(const dp_pool* pool, int32_t* layout) {
+  if (!pool || !layout) return fail(DP_EINVAL, "pool_layout: null argument");
+  *layout = pool->layout;
+  return DP_OK;
+}
+
 int dp_pool_info(const dp_pool* pool, void** base, uint32_t** counters, int64_t* data_bytes) {
   if (!pool) return fail(DP_EINVAL, "pool_info: null pool");
   if (base) *base = pool->base;
@@ -693,6 +720,7 @@ int dp_pool_export(const dp_pool* pool, dp_pool_handle* out) {
   out->n_slots = pool->n_slots;
   out->n_tickets = pool->n_tickets;
   out->device = pool->device;
+  out->reserved[0] = pool->layout;
   return DP_OK;
 }
 
@@ -712,6 +740,7 @@ int dp_pool_import(int device, const dp_pool_handle* h, dp_pool** out) {
   v->geom = h->geom;
   v->n_slots = h->n_slots;
   v->n_tickets = h->n_tickets;
+  v->layout = h->reserved[0];
   v->base = static_cast<char*>(ptr);
   v->data_bytes = static_cast<int64_t>(h->geom.n_layer) * h->n_slots * h->geom.block_tokens *
                   h->geom.bytes_per_token_layer;
@@ -836,7 +865,7 @@ int copy_transfer(const char* who, dp_pool* pool, const dp_store* src, const dp_
   const dp_kv_geom& g = pool->geom;
   const int64_t lb = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
   const int64_t fbb = lb * g.n_layer;
-  const int64_t plane = lb * pool->n_slots;
+  const int64_t plane = layer_stride(pool), sstride = slot_stride(pool);
   const int32_t items = static_cast<int32_t>(chunks_per_block(g));
   DeviceGuard guard(pool->device);
   auto s = static_cast<cudaStream_t>(stream);
@@ -864,31 +893,52 @@ int copy_transfer(const char* who, dp_pool* pool, const dp_store* src, const dp_
         return fail(DP_EINVAL, w + ": block " + std::to_string(k) + " out of range");
     const int32_t full = job.n_tokens % g.block_tokens == 0 ? job.n_blk : job.n_blk - 1;
     uint32_t* row = pool->counters + static_cast<int64_t>(job.ticket) * (g.n_layer + 1);
-    for (int32_t layer = job.layer_begin; layer < job.layer_end; ++layer) {
+    if (pool->layout == DP_POOL_BLOCK_MAJOR && !per_layer && job.layer_end == g.n_layer) {
+      // a block-major pool holds whole Full Blocks: a run of consecutive
+      // storage Full Blocks into consecutive slots is ONE contiguous copy
+      // (every layer), the partial last block a 2D copy of its L token ranges
       for (int32_t k = 0; k < full;) {
         int32_t run = 1;
         while (k + run < full && job.src_fb[k + run] == job.src_fb[k] + run &&
                job.dst_slot[k + run] == job.dst_slot[k] + run)
           ++run;
-        DP_CUDA(cudaMemcpy2DAsync(pool->base + layer * plane + job.dst_slot[k] * lb, lb,
-                                  src->host + job.src_fb[k] * fbb + layer * lb, fbb, lb, run,
-                                  cudaMemcpyHostToDevice, s));
+        DP_CUDA(cudaMemcpyAsync(pool->base + job.dst_slot[k] * sstride, src->host + job.src_fb[k] * fbb, run * fbb,
+                                cudaMemcpyHostToDevice, s));
         k += run;
       }
       if (full < job.n_blk) {
         const int32_t k = full;
         const int64_t bytes = (job.n_tokens - static_cast<int64_t>(k) * g.block_tokens) * g.bytes_per_token_layer;
-        DP_CUDA(cudaMemcpyAsync(pool->base + layer * plane + job.dst_slot[k] * lb,
-                                src->host + job.src_fb[k] * fbb + layer * lb, bytes,
-                                cudaMemcpyHostToDevice, s));
+        DP_CUDA(cudaMemcpy2DAsync(pool->base + job.dst_slot[k] * sstride, lb, src->host + job.src_fb[k] * fbb, lb,
+                                  bytes, g.n_layer, cudaMemcpyHostToDevice, s));
       }
-      if (job.ticket >= 0 && per_layer) {
-        const uint32_t n_items = static_cast<uint32_t>(job.n_blk) * items;
-        if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + layer), n_items, 0) !=
-                CUDA_SUCCESS ||
-            wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + g.n_layer),
-               n_items * static_cast<uint32_t>(layer - job.layer_begin + 1), 0) != CUDA_SUCCESS)
-          return fail(DP_ECUDA, w + ": cuStreamWriteValue32 failed");
+    } else {
+      for (int32_t layer = job.layer_begin; layer < job.layer_end; ++layer) {
+        for (int32_t k = 0; k < full;) {
+          int32_t run = 1;
+          while (k + run < full && job.src_fb[k + run] == job.src_fb[k] + run &&
+                 job.dst_slot[k + run] == job.dst_slot[k] + run)
+            ++run;
+          DP_CUDA(cudaMemcpy2DAsync(pool->base + layer * plane + job.dst_slot[k] * sstride, sstride,
+                                    src->host + job.src_fb[k] * fbb + layer * lb, fbb, lb, run,
+                                    cudaMemcpyHostToDevice, s));
+          k += run;
+        }
+        if (full < job.n_blk) {
+          const int32_t k = full;
+          const int64_t bytes = (job.n_tokens - static_cast<int64_t>(k) * g.block_tokens) * g.bytes_per_token_layer;
+          DP_CUDA(cudaMemcpyAsync(pool->base + layer * plane + job.dst_slot[k] * sstride,
+                                  src->host + job.src_fb[k] * fbb + layer * lb, bytes,
+                                  cudaMemcpyHostToDevice, s));
+        }
+        if (job.ticket >= 0 && per_layer) {
+          const uint32_t n_items = static_cast<uint32_t>(job.n_blk) * items;
+          if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + layer), n_items, 0) !=
+                  CUDA_SUCCESS ||
+              wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + g.n_layer),
+                 n_items * static_cast<uint32_t>(layer - job.layer_begin + 1), 0) != CUDA_SUCCESS)
+            return fail(DP_ECUDA, w + ": cuStreamWriteValue32 failed");
+        }
       }
     }
     if (job.ticket >= 0 && !per_layer) {
@@ -1042,8 +1092,9 @@ int dp_pool_checksum(const dp_pool* pool, int32_t layer, const int32_t* slots,
   DeviceGuard guard(pool->device);
   const int64_t lb = static_cast<int64_t>(pool->geom.block_tokens) * pool->geom.bytes_per_token_layer;
   const int grid = std::min(n, sm_count(pool->device) * 8);
+  (void)lb;
   kv_block_checksum<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      pool->base, layer * lb * pool->n_slots, lb, pool->geom.bytes_per_token_layer, slots, ntok,
+      pool->base, layer * layer_stride(pool), slot_stride(pool), pool->geom.bytes_per_token_layer, slots, ntok,
       n, out);
   DP_CUDA(cudaGetLastError());
   return DP_OK;
@@ -1056,7 +1107,7 @@ int dp_pool_copy_out(const dp_pool* pool, int32_t layer, int32_t slot, int64_t b
   if (layer < 0 || layer >= pool->geom.n_layer || slot < 0 || slot >= pool->n_slots || bytes > lb)
     return fail(DP_EINVAL, "pool_copy_out: out of range");
   DeviceGuard guard(pool->device);
-  const char* src = pool->base + (static_cast<int64_t>(layer) * pool->n_slots + slot) * lb;
+  const char* src = pool->base + layer * layer_stride(pool) + slot * slot_stride(pool);
   DP_CUDA(cudaMemcpy(host_out, src, bytes, cudaMemcpyDeviceToHost));
   return DP_OK;
 }
@@ -1394,6 +1445,8 @@ int launch_dual(dp_pool* pe_view, dp_pool* de_pool, const dp_store* src, const d
   if (!de_pool->owner) return fail(DP_EINVAL, "push_p2p_dual: decode pool must be the local pool");
   if (pe_view->device != de_pool->device)
     return fail(DP_EINVAL, "push_p2p_dual: the PE view must be mapped on the decode pool's device");
+  if (pe_view->layout != DP_POOL_LAYER_MAJOR || de_pool->layout != DP_POOL_LAYER_MAJOR)
+    return fail(DP_EINVAL, "push_p2p_dual: layer-major pools only");
   if (!geom_equal(pe_view->geom, src->geom) || !geom_equal(de_pool->geom, src->geom))
     return fail(DP_EINVAL, "push_p2p_dual: geometry differs");
   const dp_kv_geom& g = src->geom;
@@ -1456,6 +1509,8 @@ int dp_prefill_handoff(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff_job*
   if (de_view->device != pe_pool->device)
     return fail(DP_EINVAL, "prefill_handoff: the DE view must be mapped on the PE's device");
   if (!geom_equal(pe_pool->geom, de_view->geom)) return fail(DP_EINVAL, "prefill_handoff: geometry differs");
+  if (pe_pool->layout != DP_POOL_LAYER_MAJOR || de_view->layout != DP_POOL_LAYER_MAJOR)
+    return fail(DP_EINVAL, "prefill_handoff: layer-major pools only");
   if (timeout_ms <= 0) return fail(DP_EINVAL, "prefill_handoff: timeout must be > 0");
   const dp_kv_geom& g = pe_pool->geom;
   DeviceGuard guard(pe_pool->device);
@@ -1689,6 +1744,8 @@ int dp_prefill_handoff_copy(dp_pool* pe_pool, dp_pool* de_view, const dp_handoff
     return fail(DP_EINVAL, "prefill_handoff_copy: the DE view must be mapped on the PE's device");
   if (!geom_equal(pe_pool->geom, de_view->geom))
     return fail(DP_EINVAL, "prefill_handoff_copy: geometry differs");
+  if (pe_pool->layout != DP_POOL_LAYER_MAJOR || de_view->layout != DP_POOL_LAYER_MAJOR)
+    return fail(DP_EINVAL, "prefill_handoff_copy: layer-major pools only");
   if (timeout_ms <= 0) return fail(DP_EINVAL, "prefill_handoff_copy: timeout must be > 0");
   if (n_jobs > DP_MAX_HANDOFF_JOBS_PER_LAUNCH) {  // in groups of the parameter block's job capacity
     for (int32_t j0 = 0; j0 < n_jobs; j0 += DP_MAX_HANDOFF_JOBS_PER_LAUNCH)
@@ -1923,6 +1980,7 @@ int launch_span(const dp_pool* pool, const dp_store* target, const dp_span_job* 
                 uint64_t seed, dp_stream stream, Kernel kernel, const char* what) {
   if (!pool || (n_jobs > 0 && !jobs) || n_jobs < 0) return fail(DP_EINVAL, std::string(what) + ": bad argument");
   if (!pool->owner) return fail(DP_EINVAL, std::string(what) + ": the decode pool must be local");
+  if (pool->layout != DP_POOL_LAYER_MAJOR) return fail(DP_EINVAL, std::string(what) + ": layer-major pools only");
   if (target && !geom_equal(pool->geom, target->geom))
     return fail(DP_EINVAL, std::string(what) + ": geometry differs");
   const dp_kv_geom& g = pool->geom;
@@ -2011,7 +2069,8 @@ struct AttendParams {
   uint32_t* done; // or null: set to 1 by the last CTA out (the layer's "computed" flag)
   int64_t bpt;
   int64_t lb_bytes;
-  int64_t layer_off;  // layer * n_slots * lb_bytes
+  int64_t layer_off;    // layer * the pool's layer stride
+  int64_t slot_stride;  // the pool's slot stride (Layer Block or Full Block)
   uint64_t seed_q;
   int32_t layer;
   int32_t block_tokens;
@@ -2084,7 +2143,7 @@ __global__ void __maxnreg__(96) kv_prefill_attend(const __grid_constant__ Attend
           const char* src = p.pool;
           if (valid) {
             const int64_t blk = t / p.block_tokens;
-            src = p.pool + p.layer_off + static_cast<int64_t>(it.slot[blk]) * p.lb_bytes +
+            src = p.pool + p.layer_off + static_cast<int64_t>(it.slot[blk]) * p.slot_stride +
                   (t - blk * p.block_tokens) * p.bpt + static_cast<int64_t>(c0) * 4 + v4 * 16;
           }
           cp_async16(dst + r * kAttStride + v4 * 4, src, valid);
@@ -2205,7 +2264,8 @@ int dp_prefill_attend_signal(const dp_pool* pool, int32_t layer, const dp_attend
   p.ctr = pool->att_ctr;
   p.bpt = g.bytes_per_token_layer;
   p.lb_bytes = static_cast<int64_t>(g.block_tokens) * g.bytes_per_token_layer;
-  p.layer_off = static_cast<int64_t>(layer) * pool->n_slots * p.lb_bytes;
+  p.layer_off = static_cast<int64_t>(layer) * layer_stride(pool);
+  p.slot_stride = slot_stride(pool);
   p.seed_q = seed * kQueryMul;
   p.layer = layer;
   p.block_tokens = g.block_tokens;
@@ -2364,7 +2424,7 @@ int staged_transfer(const char* who, dp_pool* pool, const dp_store* src, dp_stag
       // layer one 2D copy ring (Full-Block pitch) -> layer plane (Layer-Block
       // pitch), then fenced stream writes of the landed counters (absolute:
       // the job's items landed so far, per layer and over all layers)
-      const int64_t plane = lb * pool->n_slots;
+      const int64_t plane = layer_stride(pool), sstride = slot_stride(pool);
       for (size_t q = 0; q < sub.size(); ++q) {
         const dp_job& jb = sub[q];
         const int64_t pos0 = jb.src_fb - st->iota;  // ring position of the sub-job's first block
@@ -2377,8 +2437,8 @@ int staged_transfer(const char* who, dp_pool* pool, const dp_store* src, dp_stag
             while (k + run < full && jb.dst_slot[k + run] == jb.dst_slot[k] + run) ++run;
           const int64_t width = pk ? (jb.n_tokens - static_cast<int64_t>(k) * T) * b : lb;
           for (int32_t layer = 0; layer < g.n_layer; ++layer)
-            DP_CUDA(cudaMemcpy2DAsync(pool->base + layer * plane + static_cast<int64_t>(jb.dst_slot[k]) * lb, lb,
-                                      st->ring.host + (pos0 + k) * fbb + layer * lb, fbb, width, run,
+            DP_CUDA(cudaMemcpy2DAsync(pool->base + layer * plane + static_cast<int64_t>(jb.dst_slot[k]) * sstride,
+                                      sstride, st->ring.host + (pos0 + k) * fbb + layer * lb, fbb, width, run,
                                       cudaMemcpyDeviceToDevice, s));
           k += run;
         }
@@ -2511,6 +2571,8 @@ int dp_h2d_push_dual_staged(dp_pool* pe_view, dp_pool* de_pool, const dp_store* 
     return fail(DP_EINVAL, "push_dual_staged: null argument");
   if (de_pool->device != st->device || de_src->device != st->device)
     return fail(DP_EINVAL, "push_dual_staged: decode pool, store and stager must be on one device");
+  if (pe_view->layout != DP_POOL_LAYER_MAJOR || de_pool->layout != DP_POOL_LAYER_MAJOR)
+    return fail(DP_EINVAL, "push_dual_staged: layer-major pools only");
   if (!geom_equal(st->geom, de_src->geom)) return fail(DP_EINVAL, "push_dual_staged: geometry differs");
   const dp_kv_geom& g = de_src->geom;
   const int64_t T = g.block_tokens;
@@ -2620,6 +2682,7 @@ int dp_persist_staged(const dp_pool* de_pool, dp_store* target, dp_stager* st, c
   if (!de_pool || !target || !st || (n_jobs > 0 && !jobs) || n_jobs < 0)
     return fail(DP_EINVAL, "persist_staged: null argument");
   if (!de_pool->owner) return fail(DP_EINVAL, "persist_staged: the decode pool must be local");
+  if (de_pool->layout != DP_POOL_LAYER_MAJOR) return fail(DP_EINVAL, "persist_staged: layer-major pools only");
   if (de_pool->device != st->device) return fail(DP_EINVAL, "persist_staged: pool and stager on different devices");
   if (!geom_equal(de_pool->geom, target->geom) || !geom_equal(st->geom, target->geom))
     return fail(DP_EINVAL, "persist_staged: geometry differs");

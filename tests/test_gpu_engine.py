@@ -170,6 +170,41 @@ def test_two_engines_k1_on_copy_engine(de_dev):
     verify_pool(pe, xp, cfg)
 
 
+@pytest.mark.parametrize("k1,k2,prefill", [(1, 1, False), (0, 0, False), (1, 1, True)])
+def test_two_engines_block_major_pool(de_dev, k1, k2, prefill):
+    """A block-major PE pool (ExecOptions::pool_layout = 1): with the copy
+    engines on both paths every load is whole Full-Block runs straight into
+    the pool (no kernels on the PE or the DE); the SM gathers and the
+    prefill stand-in read and write it through the slot stride.  Final pool
+    and counters as the oracle says."""
+    cfg = cluster(1, 1)
+    trajs = small_trace(count=8, turns=5)
+    planned = dp.plan(cfg, trajs, policy="dual_path", **STORAGE_BOUND)
+    opt = dp.ExecOptions()
+    opt.seed = SEED
+    opt.pool_layout = 1
+    opt.k1_mode, opt.k2_mode = k1, k2
+    if prefill:
+        opt.prefill = True
+        opt.compute_quota = 5e-4
+        opt.prefill_cost = (2e-10, 1e-9, 4e-7, 1e-5)
+    xp = dp.build_exec_plan(cfg, trajs, planned, opt)
+    pe = dp.EngineRuntime(xp, 0, 0)
+    de = dp.EngineRuntime(xp, 1, de_dev)
+    de.attach_peer_local(0, pe)
+    for _ in range(2):
+        pe.reset_counters()
+        res = dp.run_step_all([pe, de])
+        assert sum(r.bytes_read for r in res) == xp.hit_bytes
+        if k1 == 1 and not prefill:
+            assert res[0].launches <= 1  # the PE issues copies only (at most its final wait)
+    verify_counters(pe, xp, cfg)
+    verify_pool(pe, xp, cfg)
+    opt.handoff = True
+    with pytest.raises(ValueError):
+        dp.build_exec_plan(cfg, trajs, planned, opt)
+
+
 # ------------------------------------------------------------ PD handoff
 def prompt_occupants(xp, engine, T=64):
     """slot -> (Full Block, valid prompt tokens) of the last job that used it,

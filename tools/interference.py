@@ -69,6 +69,8 @@ def main():
     ap.add_argument("--only-staged", action="store_true", help="only the staged-loader cases")
     ap.add_argument("--skip-layerwise", action="store_true")
     ap.add_argument("--ring-mb", default="", help="only K1 staged (scatter kernel) at these HBM ring sizes, MiB")
+    ap.add_argument("--block-major", action="store_true",
+                    help="only the copy-engine loaders into a block-major PE pool (whole Full-Block runs, no ring)")
     a = ap.parse_args()
     assert torch.cuda.device_count() >= 2, "needs 2 GPUs"
     g = abi.geom(L, T, B)
@@ -78,6 +80,8 @@ def main():
     st_de = abi.Store(1, g, n_fb, 9)
     pool = abi.Pool(0, g, n_slots, 2 * n_jobs + 1)
     view = pool.peer_view(1)
+    bpool = abi.Pool(0, g, n_slots, 2 * n_jobs + 1, layout=abi.POOL_BLOCK_MAJOR) if a.block_major else None
+    bview = bpool.peer_view(1) if bpool else None
     rng = np.random.default_rng(0)
     jobs_k2, keep2 = make_jobs(1, n_jobs, blocks, n_fb, n_slots, rng)
     jobs_k1, keep1 = make_jobs(0, n_jobs, blocks, n_fb, n_slots, rng)
@@ -125,7 +129,7 @@ def main():
     flops = 2.0 * a.m * a.m * a.k
 
     def run_with(k1=False, k2=False, ctas=0, ce=False, staged=False, stage_ctas=32, on_de=False, ce_scatter=False,
-                 push_ctas=None, ring=None):
+                 push_ctas=None, ring=None, block=False):
         for dev in (0, 1):
             abi.set_gather_ctas(dev, ctas)
         stager0.set_ctas(stage_ctas)
@@ -147,9 +151,9 @@ def main():
                         abi.h2d_push_staged(view, st_de, stager1, jobs_ce2 if ce_scatter else jobs_st2, n_jobs,
                                             stream.cuda_stream)
                     elif kind == "k1" and ce:
-                        abi.h2d_layer_copy_job(pool, st_pe, jobs_ce1, n_jobs, stream.cuda_stream)
+                        abi.h2d_layer_copy_job(bpool if block else pool, st_pe, jobs_ce1, n_jobs, stream.cuda_stream)
                     elif ce:
-                        abi.h2d_push_copy_job(view, st_de, jobs_ce2, n_jobs, stream.cuda_stream)
+                        abi.h2d_push_copy_job(bview if block else view, st_de, jobs_ce2, n_jobs, stream.cuda_stream)
                     elif kind == "k1":
                         abi.h2d_layer_gather(pool, st_pe, jobs_k1, n_jobs, stream.cuda_stream)
                     else:
@@ -205,6 +209,8 @@ def main():
                      ("de_k2_staged_148ctas", dict(k2=True, staged=True, push_ctas=148)),
                      ("de_k2_staged_8ctas", dict(k2=True, staged=True, stage_ctas=8)),
                      ("de_k2_copy_engine", dict(k2=True, ce=True))]:
+        if a.block_major or a.ring_mb:
+            break  # the focused sweeps below
         out[name] = bracketed(kw, on_de=True)
     ce_cases = [("k1_copy_engine_job", dict(k1=True, ce=True)), ("k2_copy_engine_job", dict(k2=True, ce=True)),
                 ("k1_copy_engine_job+k2_copy_engine_job", dict(k1=True, k2=True, ce=True)),
@@ -213,6 +219,14 @@ def main():
                 ("k1_staged_ce", dict(k1=True, staged=True, ce_scatter=True)),
                 ("k2_staged_ce", dict(k2=True, staged=True, ce_scatter=True)),
                 ("k1_staged_ce+k2_staged_ce", dict(k1=True, k2=True, staged=True, ce_scatter=True))]
+    if a.block_major:
+        for name, kw, de in [("k1_ce_block_major", dict(k1=True, ce=True, block=True), False),
+                             ("k2_ce_block_major", dict(k2=True, ce=True, block=True), False),
+                             ("k1_ce_block_major+k2_ce_block_major", dict(k1=True, k2=True, ce=True, block=True), False),
+                             ("de_k2_ce_block_major", dict(k2=True, ce=True, block=True), True)]:
+            out[name] = bracketed(kw, on_de=de)
+        print(json.dumps(out))
+        return
     if a.ring_mb:
         cases = [(f"k1_staged_ring{r}MiB", dict(k1=True, staged=True, ring=r)) for r in ring_stagers]
         for name, kw in cases:
