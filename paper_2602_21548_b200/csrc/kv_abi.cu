@@ -842,6 +842,54 @@ WriteValue32Fn write_value32() {
   return fn;
 }
 
+using BatchMemOpFn = CUresult (*)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
+
+BatchMemOpFn batch_memop() {
+  static BatchMemOpFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<BatchMemOpFn>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// Stream-ordered 32-bit writes of (counter, value) pairs: ONE batched
+// stream memory operation (cuStreamBatchMemOp) when the driver has it --
+// each separate write waits for the copies before it, so L + 1 of them per
+// job left the copy engine idle between jobs -- else one write each.
+int write_counters(cudaStream_t s, const std::vector<std::pair<uint32_t*, uint32_t>>& writes, const std::string& who) {
+  if (writes.empty()) return DP_OK;
+  const BatchMemOpFn batch = batch_memop();
+  if (batch) {
+    constexpr std::size_t kMaxOps = 256;
+    for (std::size_t i0 = 0; i0 < writes.size(); i0 += kMaxOps) {
+      const std::size_t n = std::min(kMaxOps, writes.size() - i0);
+      std::vector<CUstreamBatchMemOpParams> ops(n);
+      std::memset(ops.data(), 0, n * sizeof(CUstreamBatchMemOpParams));
+      for (std::size_t k = 0; k < n; ++k) {
+        ops[k].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+        ops[k].writeValue.address = reinterpret_cast<CUdeviceptr>(writes[i0 + k].first);
+        ops[k].writeValue.value = writes[i0 + k].second;
+        ops[k].writeValue.flags = 0;
+      }
+      if (batch(reinterpret_cast<CUstream>(s), static_cast<unsigned int>(n), ops.data(), 0) != CUDA_SUCCESS)
+        return fail(DP_ECUDA, who + ": cuStreamBatchMemOp failed");
+    }
+    return DP_OK;
+  }
+  const WriteValue32Fn wv = write_value32();
+  if (!wv) return fail(DP_ECUDA, who + ": cuStreamWriteValue32 unavailable");
+  for (const auto& [ptr, v] : writes)
+    if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(ptr), v, 0) != CUDA_SUCCESS)
+      return fail(DP_ECUDA, who + ": cuStreamWriteValue32 failed");
+  return DP_OK;
+}
+
 }  // namespace
 
 namespace {
@@ -942,16 +990,17 @@ int copy_transfer(const char* who, dp_pool* pool, const dp_store* src, const dp_
       }
     }
     if (job.ticket >= 0 && !per_layer) {
-      // one release per job: every layer's counter, then the all-layer column
-      // (each stream write waits for the copies before it, so per-layer writes
-      // would idle the copy engine once per layer)
+      // one release per job: every layer's counter, then the all-layer column,
+      // as one batched memory operation (per-layer writes would idle the copy
+      // engine once per layer)
       const uint32_t n_items = static_cast<uint32_t>(job.n_blk) * items;
+      std::vector<std::pair<uint32_t*, uint32_t>> writes;
       for (int32_t layer = job.layer_begin; layer <= job.layer_end; ++layer) {
         const bool all = layer == job.layer_end;
-        if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + (all ? g.n_layer : layer)),
-               all ? n_items * static_cast<uint32_t>(job.layer_end - job.layer_begin) : n_items, 0) != CUDA_SUCCESS)
-          return fail(DP_ECUDA, w + ": cuStreamWriteValue32 failed");
+        writes.emplace_back(row + (all ? g.n_layer : layer),
+                            all ? n_items * static_cast<uint32_t>(job.layer_end - job.layer_begin) : n_items);
       }
+      if (int rc = write_counters(s, writes, w)) return rc;
     }
   }
   return DP_OK;
@@ -2443,14 +2492,12 @@ int staged_transfer(const char* who, dp_pool* pool, const dp_store* src, dp_stag
           k += run;
         }
         if (jb.ticket >= 0) {
-          const WriteValue32Fn wv = write_value32();
-          if (!wv) return fail(DP_ECUDA, w + ": cuStreamWriteValue32 unavailable");
           uint32_t* row = pool->counters + static_cast<int64_t>(jb.ticket) * (g.n_layer + 1);
           const uint32_t v = static_cast<uint32_t>(sub_cum[q]);
+          std::vector<std::pair<uint32_t*, uint32_t>> writes;
           for (int32_t layer = 0; layer <= g.n_layer; ++layer)
-            if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(row + layer),
-                   layer == g.n_layer ? v * static_cast<uint32_t>(g.n_layer) : v, 0) != CUDA_SUCCESS)
-              return fail(DP_ECUDA, w + ": cuStreamWriteValue32 failed");
+            writes.emplace_back(row + layer, layer == g.n_layer ? v * static_cast<uint32_t>(g.n_layer) : v);
+          if (int rc = write_counters(s, writes, w)) return rc;
         }
       }
     } else if (!sub.empty()) {
