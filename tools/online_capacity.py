@@ -52,6 +52,8 @@ def one(a, cfg, trajs, policy, aps, devices):
     ex = dp.ExecOptions()
     ex.seed = 9
     ex.storage_cap_Bps = a.cap_gbps * 1e9
+    if a.caps:  # config 5: asymmetric per-engine storage NICs
+        ex.storage_cap_per_engine = [float(x) * 1e9 for x in a.caps.split(",")]
     ex.k1_mode, ex.k2_mode = 3, 2
     if a.prefill:  # the prefill stand-in (K5 forwards): TTFT = arrival -> prefill done
         ex.prefill = True
@@ -101,6 +103,7 @@ def main():
     ap.add_argument("--sessions", type=int, default=96)
     ap.add_argument("--turns", type=int, default=6)
     ap.add_argument("--cap-gbps", type=float, default=6.25)
+    ap.add_argument("--caps", default="", help="config 5: per-engine storage caps, GB/s, comma list (one per engine)")
     ap.add_argument("--slo", type=float, default=0.3, help="load-TTFT SLO, seconds")
     ap.add_argument("--decode-ms", type=float, default=1.0, help="emulated decode per generated token")
     ap.add_argument("--steady-window", type=float, default=4.0)
@@ -126,6 +129,8 @@ def main():
     a = ap.parse_args()
     if a.handoff and not a.prefill:
         ap.error("--handoff needs --prefill")
+    if a.caps and len(a.caps.split(",")) != sum(int(x) for x in a.pd.split(":")):
+        ap.error("--caps needs one cap per engine")
     P, D = (int(x) for x in a.pd.split(":"))
     L, b = 61, 576
     cfg = cluster(P, D, L, b, pool_slots(a, L, b) * 64 if a.handoff else 100_000_000)
@@ -140,7 +145,8 @@ def main():
         a.pool_gb /= -(-(P + D) // ndev)
     out = {"what": "online APS capacity (sessions/s within the load-TTFT SLO), live-mode scheduling on "
                    "measured completions", "pd": a.pd, "sessions": a.sessions, "turns": a.turns,
-           "cap_gbps_per_engine": a.cap_gbps, "slo_s": a.slo, "decode_ms_per_token": a.decode_ms,
+           "cap_gbps_per_engine": [float(x) for x in a.caps.split(",")] if a.caps else a.cap_gbps,
+           "slo_s": a.slo, "decode_ms_per_token": a.decode_ms,
            "devices": devices, "backend": "timed" if a.cpu else "gpu",
            "ttft": ("arrival -> first token (prefill, K3 handoff, one decode step)" if a.handoff else
                     "arrival -> prefill done (K5 forwards)") if a.prefill else "arrival -> hit KV landed",
